@@ -1,0 +1,189 @@
+/*
+ * actc.h -- C ABI of the B200-native COMET activation codec (libactc.so).
+ *
+ * The reference (/root/reference/pkg, Python) exposes this path as Python
+ * functions; this header is the native boundary its FFI would bind
+ * (see INTEGRATION.md for the ctypes binding).  Each entry point cites the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *  - Every pointer named *_dev is CUDA device memory; every call is
+ *    stream-ordered on the given cudaStream_t and does not block the host
+ *    unless stated.  Buffers are caller-owned (the host wrapper allocates
+ *    them from the PyTorch caching allocator); the context owns only
+ *    scratch.
+ *  - Return value: ACTC_OK or an error class mirroring the reference's
+ *    exception taxonomy (errors.py:4-33).  actc_last_error() gives text.
+ *  - Device-detected errors (decode faults, marker mismatch, code length
+ *    > 63) are reported in the `status` field of the host-visible structs
+ *    below after the caller synchronizes the stream.
+ */
+#ifndef ACTC_H
+#define ACTC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACTC_OK 0
+#define ACTC_EPARAM 1  /* -> ParameterError (errors.py:12) */
+#define ACTC_EDATA 2   /* -> DataError      (errors.py:16) */
+#define ACTC_EFORMAT 3 /* -> FormatError    (errors.py:20) */
+#define ACTC_ENOMEM 4
+#define ACTC_ECUDA 5
+
+#define ACTC_FLAG_PRESERVE_ZEROS 1u /* CMTZ flags bit0 (codec.py:96) */
+
+#define ACTC_DTYPE_F32 0
+#define ACTC_DTYPE_F64 1
+
+/* Symbols per decode chunk: the encoder records the bit offset of every
+ * ACTC_CHUNK-th symbol in a device-side index (not part of CMTZ). */
+#define ACTC_CHUNK 256
+#define ACTC_MAX_CODE_LENGTH 63 /* huffman.py:34 */
+
+typedef void *actc_stream; /* a cudaStream_t */
+typedef struct actc_ctx actc_ctx;
+
+/* Result of compress phase 1 (quantize + Lorenzo + histogram + codebook);
+ * valid on the host after the stream is synchronized. */
+typedef struct {
+  uint64_t n;             /* element count (= symbol_count, codec.py:323) */
+  uint64_t n_outliers;    /* len(outlier_indices) (codec.py:321) */
+  uint64_t payload_bits;  /* sum_s hist[s]*len[s] (huffman.py:189) */
+  uint32_t live_symbols;  /* number of symbols with a code */
+  uint32_t max_len;       /* longest code length */
+  uint64_t rle_runs;      /* CMTZ RLE records incl. 65535-splits (codec.py:201-226) */
+  double entropy_bits;    /* stream_entropy_bits(hist) (huffman.py:239-246) */
+  uint32_t status;        /* ACTC_OK or ACTC_EPARAM (code length > 63) */
+  uint32_t sym_bytes;     /* 2 (u16 symbols, radius <= 2^15) or 4 */
+} actc_plan_t;
+
+/* A compressed stream as the decoder sees it (all arrays on the device).
+ * Field meaning follows CompressedActivation (codec.py:74-86); the code
+ * table is kept in canonical form (symbols ordered by (length, symbol),
+ * huffman.py:78-94) instead of the per-symbol length table. */
+typedef struct {
+  uint64_t n;
+  double eb;
+  uint32_t radius;
+  uint32_t flags;
+  uint64_t n_outliers;
+  const uint64_t *outlier_idx_dev; /* ascending, codec.py:321 */
+  const float *outlier_val_dev;    /* exact originals, codec.py:322 */
+  uint32_t live_symbols;
+  const uint32_t *canon_syms_dev;  /* [live_symbols] */
+  const uint32_t *len_counts_dev;  /* [64]: number of codes of each length */
+  const uint8_t *payload_dev;      /* MSB-first bitstream; 4-byte aligned, >=8 B tail pad */
+  uint64_t payload_bits;
+  const uint64_t *chunk_offsets_dev; /* [ceil(n/ACTC_CHUNK)] or NULL (rebuilt) */
+} actc_stream_t;
+
+/* Result of a decompression; valid after the stream is synchronized. */
+typedef struct {
+  uint64_t nonzero;  /* count_nonzero(reconstruction) -> R (training.py:351-352) */
+  uint64_t markers;  /* number of outlier markers decoded */
+  uint32_t status;   /* ACTC_OK or ACTC_EFORMAT */
+  uint32_t reserved;
+} actc_decode_result_t;
+
+const char *actc_last_error(void);
+int actc_version(void);
+
+/* One context per stream: owns grow-on-demand device scratch. */
+int actc_ctx_create(int device, actc_ctx **out);
+void actc_ctx_destroy(actc_ctx *ctx);
+
+/* compress(), phase 1 -- replaces codec.py:296-316 up to the codebook:
+ * prequantize (:238-251), bound check (:311-312), lorenzo_encode
+ * (:254-272), bincount (huffman.py:183), build_code_lengths
+ * (huffman.py:37-75), canonical_codes (huffman.py:78-94).
+ * plan_host must be pinned host memory; it is written asynchronously. */
+int actc_compress_plan(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb,
+                       uint32_t radius, uint32_t flags, actc_plan_t *plan_host,
+                       actc_stream s);
+
+/* compress(), phase 2 -- huffman_encode bit packing (huffman.py:188-207)
+ * plus outlier extraction (codec.py:321-322) and the decode chunk index.
+ * `plan` is the synchronized phase-1 result; buffers are sized from it:
+ *   payload_dev      >= 4*ceil(payload_bits/32) + 8 bytes, 4-byte aligned
+ *   outlier_idx_dev  [n_outliers], outlier_val_dev [n_outliers]
+ *   canon_syms_dev   [live_symbols], len_counts_dev [64]
+ *   chunk_offsets_dev [ceil(n/ACTC_CHUNK)]
+ * Must follow actc_compress_plan on the same ctx and stream. */
+int actc_compress_encode(actc_ctx *ctx, const float *x_dev, const actc_plan_t *plan,
+                         uint8_t *payload_dev, uint64_t *outlier_idx_dev,
+                         float *outlier_val_dev, uint32_t *canon_syms_dev,
+                         uint32_t *len_counts_dev, uint64_t *chunk_offsets_dev,
+                         actc_stream s);
+
+/* decompress() -- replaces codec.py:343-369: huffman_decode
+ * (huffman.py:210-236), marker check (codec.py:356-359), lorenzo_decode
+ * (codec.py:275-293), recon/splice/re-zero (codec.py:364-368).
+ * out_dtype ACTC_DTYPE_F64 is bit-identical to the reference's fp64
+ * output; ACTC_DTYPE_F32 stores fp32(that value).  result_host is pinned
+ * host memory written asynchronously. */
+int actc_decompress(actc_ctx *ctx, const actc_stream_t *stream, void *out_dev,
+                    int out_dtype, actc_decode_result_t *result_host, actc_stream s);
+
+/* Build the canonical code table from a per-symbol length table (the
+ * form CMTZ stores, codec.py:164) -- used after from_bytes
+ * (codec.py:121-179).  canon_syms_dev needs [count of nonzero lengths]. */
+int actc_codebook_from_lengths(actc_ctx *ctx, const uint16_t *lengths_dev, uint64_t alphabet,
+                               uint32_t *canon_syms_dev, uint32_t *len_counts_dev,
+                               uint32_t *live_host, actc_stream s);
+
+/* Rebuild the chunk index of a stream that lacks one (blobs parsed by
+ * from_bytes): self-synchronising parallel decode.  Synchronizes. */
+int actc_build_chunk_index(actc_ctx *ctx, const actc_stream_t *stream,
+                           uint64_t *chunk_offsets_dev, uint32_t *status_host, actc_stream s);
+
+/* ---- debug / conformance entry points (reference internals) ---- */
+
+/* prequantize (codec.py:238-251); x_dtype ACTC_DTYPE_F32 or _F64 */
+int actc_prequantize(const void *x_dev, int x_dtype, uint64_t n, double eb, int64_t *q_dev,
+                     actc_stream s);
+/* lorenzo_encode (codec.py:254-272); symbols_dev u32, force_dev may be NULL;
+ * n_outliers_host pinned, written async */
+int actc_lorenzo_encode(const int64_t *lattice_dev, uint64_t n, uint32_t radius,
+                        const uint8_t *force_dev, uint32_t *symbols_dev,
+                        uint64_t *n_outliers_host, actc_stream s);
+/* lorenzo_decode (codec.py:275-293); status_host gets ACTC_EFORMAT on a
+ * marker/value count mismatch */
+int actc_lorenzo_decode(const uint32_t *symbols_dev, uint64_t n, const int64_t *outlier_lattice_dev,
+                        uint64_t k, uint32_t radius, int64_t *out_dev, uint32_t *status_host,
+                        actc_stream s);
+/* huffman_encode (huffman.py:171-207) over an arbitrary u32 symbol stream:
+ * phase 1 builds histogram + codebook; lengths_dev receives the u16
+ * per-symbol length table (build_code_lengths). */
+int actc_huffman_plan(actc_ctx *ctx, const uint32_t *symbols_dev, uint64_t n, uint64_t alphabet,
+                      uint16_t *lengths_dev, actc_plan_t *plan_host, actc_stream s);
+int actc_huffman_encode(actc_ctx *ctx, const uint32_t *symbols_dev, const actc_plan_t *plan,
+                        uint8_t *payload_dev, uint32_t *canon_syms_dev, uint32_t *len_counts_dev,
+                        uint64_t *chunk_offsets_dev, actc_stream s);
+/* huffman_decode (huffman.py:210-236): symbols out as u32 */
+int actc_huffman_decode(actc_ctx *ctx, const actc_stream_t *stream, uint32_t *symbols_dev,
+                        actc_decode_result_t *result_host, actc_stream s);
+/* build_code_lengths (huffman.py:37-75) from a u64 frequency table */
+int actc_code_lengths(actc_ctx *ctx, const uint64_t *freqs_dev, uint64_t alphabet,
+                      uint16_t *lengths_dev, actc_plan_t *plan_host, actc_stream s);
+
+/* ---- per-layer statistics (controller inputs) ---- */
+
+/* count_nonzero (tensor.py:181, training.py:352); out_host pinned */
+int actc_count_nonzero(const void *x_dev, int dtype, uint64_t n, uint64_t *out_host, actc_stream s);
+/* mean(|x|) with numpy's pairwise summation order (tensor.py:182,
+ * nn.py:249-253): fp32 input -> f32(f64(sum_f32)/n) */
+int actc_mean_abs(actc_ctx *ctx, const void *x_dev, int dtype, uint64_t n, double *out_host,
+                  actc_stream s);
+/* np.abs(g).reshape(N,-1).max(axis=1).mean() (training.py:358-361);
+ * per_sample_max_dev optional [N] output in the input dtype */
+int actc_lbar(actc_ctx *ctx, const void *g_dev, int dtype, uint64_t N, uint64_t per_sample,
+              void *per_sample_max_dev, double *out_host, actc_stream s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACTC_H */

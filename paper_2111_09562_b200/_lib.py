@@ -1,0 +1,193 @@
+"""ctypes binding of the C ABI in include/actc.h (libactc.so, sm_100a).
+
+The product path has no fallback: if the library is missing or no CUDA
+device is present, every codec call raises.  PyTorch is used only for device
+memory (caching allocator), streams and pinned host buffers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import DataError, FormatError, ParameterError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libactc.so")
+
+ACTC_OK, ACTC_EPARAM, ACTC_EDATA, ACTC_EFORMAT, ACTC_ENOMEM, ACTC_ECUDA = range(6)
+ACTC_FLAG_PRESERVE_ZEROS = 1
+ACTC_DTYPE_F32, ACTC_DTYPE_F64 = 0, 1
+ACTC_CHUNK = 256
+
+
+class Plan(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint64),
+        ("n_outliers", C.c_uint64),
+        ("payload_bits", C.c_uint64),
+        ("live_symbols", C.c_uint32),
+        ("max_len", C.c_uint32),
+        ("rle_runs", C.c_uint64),
+        ("entropy_bits", C.c_double),
+        ("status", C.c_uint32),
+        ("sym_bytes", C.c_uint32),
+    ]
+
+
+class StreamDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint64),
+        ("eb", C.c_double),
+        ("radius", C.c_uint32),
+        ("flags", C.c_uint32),
+        ("n_outliers", C.c_uint64),
+        ("outlier_idx_dev", C.c_void_p),
+        ("outlier_val_dev", C.c_void_p),
+        ("live_symbols", C.c_uint32),
+        ("canon_syms_dev", C.c_void_p),
+        ("len_counts_dev", C.c_void_p),
+        ("payload_dev", C.c_void_p),
+        ("payload_bits", C.c_uint64),
+        ("chunk_offsets_dev", C.c_void_p),
+    ]
+
+
+class DecodeResult(C.Structure):
+    _fields_ = [
+        ("nonzero", C.c_uint64),
+        ("markers", C.c_uint64),
+        ("status", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libactc.so (raises if it is missing -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(make -C paper_2111_09562_b200/csrc)"
+            )
+        L = C.CDLL(LIB_PATH)
+        P, U64, U32, D, I = C.c_void_p, C.c_uint64, C.c_uint32, C.c_double, C.c_int
+        sig = {
+            "actc_last_error": ([], C.c_char_p),
+            "actc_version": ([], I),
+            "actc_ctx_create": ([I, C.POINTER(P)], I),
+            "actc_ctx_destroy": ([P], None),
+            "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P], I),
+            "actc_compress_encode": ([P, P, P, P, P, P, P, P, P, P], I),
+            "actc_decompress": ([P, P, P, I, P, P], I),
+            "actc_codebook_from_lengths": ([P, P, U64, P, P, P, P], I),
+            "actc_build_chunk_index": ([P, P, P, P, P], I),
+            "actc_prequantize": ([P, I, U64, D, P, P], I),
+            "actc_lorenzo_encode": ([P, U64, U32, P, P, P, P], I),
+            "actc_lorenzo_decode": ([P, U64, P, U64, U32, P, P, P], I),
+            "actc_huffman_plan": ([P, P, U64, U64, P, P, P], I),
+            "actc_huffman_encode": ([P, P, P, P, P, P, P, P], I),
+            "actc_huffman_decode": ([P, P, P, P, P], I),
+            "actc_code_lengths": ([P, P, U64, P, P, P], I),
+            "actc_count_nonzero": ([P, I, U64, P, P], I),
+            "actc_mean_abs": ([P, P, I, U64, P, P], I),
+            "actc_lbar": ([P, P, I, U64, U64, P, P, P], I),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = (
+    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_compress_plan "
+    "actc_compress_encode actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
+    "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
+    "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
+    "actc_mean_abs actc_lbar"
+).split()
+
+
+def raise_for(rc: int, default_msg: str = ""):
+    if rc == ACTC_OK:
+        return
+    msg = lib().actc_last_error().decode(errors="replace") or default_msg
+    if rc == ACTC_EPARAM:
+        raise ParameterError(msg)
+    if rc == ACTC_EDATA:
+        raise DataError(msg)
+    if rc == ACTC_EFORMAT:
+        raise FormatError(msg)
+    if rc == ACTC_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"CUDA error in libactc: {msg}")
+
+
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2111_09562_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    return torch
+
+
+_tls = threading.local()
+
+
+class Context:
+    """One libactc context per (thread, device): owns device scratch."""
+
+    def __init__(self, device: int):
+        h = C.c_void_p()
+        raise_for(lib().actc_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+        torch = torch_cuda()
+        # pinned host mailboxes for the async plan / decode-result copies
+        self.plan_buf = torch.empty(C.sizeof(Plan), dtype=torch.uint8, pin_memory=True)
+        self.dres_buf = torch.empty(C.sizeof(DecodeResult), dtype=torch.uint8, pin_memory=True)
+        self.u64_buf = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+
+    @property
+    def plan(self) -> Plan:
+        return Plan.from_address(self.plan_buf.data_ptr())
+
+    @property
+    def dres(self) -> DecodeResult:
+        return DecodeResult.from_address(self.dres_buf.data_ptr())
+
+    def __del__(self):
+        try:
+            lib().actc_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def context(device=None) -> Context:
+    torch = torch_cuda()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    c = ctxs.get(dev)
+    if c is None:
+        with torch.cuda.device(dev):
+            c = ctxs[dev] = Context(dev)
+    return c
+
+
+def stream_handle(stream=None):
+    torch = torch_cuda()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream), s

@@ -1,0 +1,554 @@
+"""Drop-in codec API over the sm_100a kernels.
+
+Mirrors /root/reference/pkg/src/actcomp/codec.py: `CodecParams` (:42-61),
+`CompressionReport` (:64-71), `CompressedActivation` with the CMTZ byte
+format (:74-179), `prequantize` (:238-251), `lorenzo_encode` (:254-272),
+`lorenzo_decode` (:275-293), `compress` (:296-340), `decompress`
+(:343-369), `write_compressed`/`read_compressed` (:372-386).
+
+Every stage runs on the GPU through libactc (include/actc.h).  A
+CompressedActivation produced by `compress` stays device-resident (payload,
+outliers, canonical code table and the decode chunk index live in CUDA
+memory); the reference's host fields (`payload`, `code_lengths`, ...) are
+materialised lazily when accessed.  `decompress` returns the reference's fp64
+host Tensor; `decompress_device` is the device path used by the training
+hooks (fp32 output, no host round trip).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import struct
+import zlib
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import FormatError, ParameterError
+from .tensor import Tensor, to_device
+
+MAGIC_COMPRESSED = b"CMTZ"
+COMPRESSED_FORMAT_VERSION = 1
+PREDICTOR_IDS = {"lorenzo-1d": 1}
+_PREDICTOR_NAMES = {v: k for k, v in PREDICTOR_IDS.items()}
+_LATTICE_LIMIT = 1 << 61
+DEFAULT_RADIUS = 1 << 15
+_MAX_RUN = 0xFFFF
+
+
+@dataclass(frozen=True)
+class CodecParams:
+    """User-facing knobs: absolute error bound and code alphabet size."""
+
+    eb: float
+    radius: int = DEFAULT_RADIUS
+    predictor: str = "lorenzo-1d"
+    preserve_zeros: bool = True
+
+    def __post_init__(self):
+        if not (self.eb > 0 and np.isfinite(self.eb)):
+            raise ParameterError(f"eb must be a positive finite real, got {self.eb}")
+        if self.radius < 2:
+            raise ParameterError(f"radius must be >= 2, got {self.radius}")
+        if self.predictor not in PREDICTOR_IDS:
+            raise ParameterError(f"unknown predictor {self.predictor!r}")
+
+    @property
+    def alphabet_size(self) -> int:
+        return 2 * self.radius
+
+
+@dataclass(frozen=True)
+class CompressionReport:
+    original_bytes: int
+    compressed_bytes: int
+    ratio: float
+    outlier_fraction: float
+    codes_entropy_bits_per_symbol: float
+    outlier_warning: bool
+
+
+def _cmtz_size(rank: int, k: int, runs: int, bits: int) -> int:
+    # header 53 + 8r, outliers 12k, RLE 4m, payload ceil(bits/8) (codec.py:95-119)
+    return 53 + 8 * rank + 12 * k + 4 * runs + (bits + 7) // 8
+
+
+def _rle_encode_lengths(lengths: np.ndarray) -> bytes:
+    """codec.py:201-226 (host serialization helper)."""
+    lengths = np.asarray(lengths, dtype=np.uint16)
+    if lengths.size == 0:
+        return struct.pack("<I", 0)
+    change = np.flatnonzero(np.diff(lengths)) + 1
+    starts = np.concatenate(([0], change))
+    ends = np.concatenate((change, [lengths.size]))
+    run_lens = ends - starts
+    values = lengths[starts]
+    if run_lens.max() > _MAX_RUN:
+        reps = (run_lens + _MAX_RUN - 1) // _MAX_RUN
+        vals = np.repeat(values, reps)
+        lens = np.full(vals.size, _MAX_RUN, dtype=np.int64)
+        last = np.cumsum(reps) - 1
+        lens[last] = run_lens - (reps - 1) * _MAX_RUN
+        run_lens, values = lens, vals
+    runs = np.empty(len(run_lens), dtype=[("l", "<u2"), ("v", "<u2")])
+    runs["l"] = run_lens
+    runs["v"] = values
+    return struct.pack("<I", len(run_lens)) + runs.tobytes()
+
+
+class _Cursor:
+    def __init__(self, buf: bytes):
+        self.buf = buf
+        self.pos = 0
+
+    def take(self, n: int) -> bytes:
+        if self.pos + n > len(self.buf):
+            raise FormatError("truncated compressed stream")
+        out = self.buf[self.pos : self.pos + n]
+        self.pos += n
+        return out
+
+    def remaining(self) -> int:
+        return len(self.buf) - self.pos
+
+
+def _rle_decode_lengths(cur: _Cursor, alphabet_size: int) -> np.ndarray:
+    (n_runs,) = struct.unpack("<I", cur.take(4))
+    runs = np.frombuffer(cur.take(4 * n_runs), dtype=[("l", "<u2"), ("v", "<u2")])
+    run_lens = runs["l"].astype(np.int64)
+    if int(run_lens.sum()) != alphabet_size:
+        raise FormatError("code-length table does not cover alphabet")
+    return np.repeat(runs["v"], run_lens).astype(np.uint16)
+
+
+def _payload_buffer_bytes(bits: int) -> int:
+    # 4-byte words for the big-endian packer + 16 B over-read pad for the decoder
+    return 4 * ((bits + 31) // 32) + 16
+
+
+class CompressedActivation:
+    """Self-describing compressed container (reference codec.py:74-179).
+
+    Constructed either from host fields (same signature as the reference's
+    frozen dataclass) or, by `compress`, from device buffers.
+    """
+
+    __slots__ = (
+        "dims", "precision", "params", "symbol_count", "payload_bits",
+        "_h_outlier_indices", "_h_outlier_values", "_h_code_lengths", "_h_payload",
+        "_dev", "_live", "_n_outliers", "_rle_runs",
+    )
+
+    def __init__(self, dims, precision, params, outlier_indices, outlier_values, symbol_count,
+                 code_lengths, payload, payload_bits):
+        self.dims = tuple(int(d) for d in dims)
+        self.precision = int(precision)
+        self.params = params
+        self.symbol_count = int(symbol_count)
+        self.payload_bits = int(payload_bits)
+        self._h_outlier_indices = np.asarray(outlier_indices, dtype=np.uint64)
+        self._h_outlier_values = np.asarray(outlier_values, dtype=np.float32)
+        self._h_code_lengths = np.asarray(code_lengths, dtype=np.uint16)
+        self._h_payload = bytes(payload)
+        self._dev = None
+        self._live = None
+        self._n_outliers = len(self._h_outlier_indices)
+        self._rle_runs = None
+
+    # ---- device-resident construction (compress) ----
+    @classmethod
+    def _from_device(cls, dims, params, dev: dict, payload_bits: int, n_outliers: int, live: int, rle_runs: int):
+        self = cls.__new__(cls)
+        self.dims = tuple(int(d) for d in dims)
+        self.precision = 4
+        self.params = params
+        self.symbol_count = int(np.prod(self.dims)) if self.dims else 0
+        self.payload_bits = int(payload_bits)
+        self._h_outlier_indices = None
+        self._h_outlier_values = None
+        self._h_code_lengths = None
+        self._h_payload = None
+        self._dev = dev
+        self._live = int(live)
+        self._n_outliers = int(n_outliers)
+        self._rle_runs = int(rle_runs)
+        return self
+
+    @property
+    def element_count(self) -> int:
+        n = 1
+        for d in self.dims:
+            n *= d
+        return n
+
+    @property
+    def is_device_resident(self) -> bool:
+        return self._dev is not None
+
+    @property
+    def device_nbytes(self) -> int:
+        """Bytes held in device memory by this container (payload + side data)."""
+        if self._dev is None:
+            return 0
+        return sum(t.numel() * t.element_size() for t in self._dev.values())
+
+    # ---- reference host fields (materialised lazily) ----
+    @property
+    def outlier_indices(self) -> np.ndarray:
+        if self._h_outlier_indices is None:
+            self._h_outlier_indices = self._dev["out_idx"].cpu().numpy().view(np.uint64).copy()
+        return self._h_outlier_indices
+
+    @property
+    def outlier_values(self) -> np.ndarray:
+        if self._h_outlier_values is None:
+            self._h_outlier_values = self._dev["out_val"].cpu().numpy().copy()
+        return self._h_outlier_values
+
+    @property
+    def code_lengths(self) -> np.ndarray:
+        if self._h_code_lengths is None:
+            canon = self._dev["canon"].cpu().numpy().astype(np.int64)
+            counts = self._dev["len_counts"].cpu().numpy().astype(np.int64)
+            lengths = np.zeros(self.params.alphabet_size, dtype=np.uint16)
+            lengths[canon] = np.repeat(np.arange(64, dtype=np.uint16), counts)
+            self._h_code_lengths = lengths
+        return self._h_code_lengths
+
+    @property
+    def payload(self) -> bytes:
+        if self._h_payload is None:
+            nbytes = (self.payload_bits + 7) // 8
+            self._h_payload = self._dev["payload"][:nbytes].cpu().numpy().tobytes()
+        return self._h_payload
+
+    # ---- device upload (containers built from host fields) ----
+    def _ensure_device(self):
+        if self._dev is not None:
+            return self._dev
+        torch = _lib.torch_cuda()
+        ctx = _lib.context()
+        sh, s = _lib.stream_handle()
+        dev = {}
+        nbytes = (self.payload_bits + 7) // 8
+        if len(self._h_payload) < nbytes:
+            raise FormatError("payload shorter than declared bit length")
+        pb = np.zeros(_payload_buffer_bytes(self.payload_bits), dtype=np.uint8)
+        pb[:nbytes] = np.frombuffer(self._h_payload, dtype=np.uint8)[:nbytes]
+        dev["payload"] = torch.from_numpy(pb).cuda()
+        dev["out_idx"] = torch.from_numpy(self._h_outlier_indices.view(np.int64).copy()).cuda()
+        dev["out_val"] = torch.from_numpy(self._h_outlier_values.copy()).cuda()
+        lengths = self._h_code_lengths
+        A = self.params.alphabet_size
+        if lengths.size != A:
+            raise FormatError("code-length table does not cover alphabet")
+        live = int(np.count_nonzero(lengths))
+        dev["canon"] = torch.empty(max(live, 1), dtype=torch.int32, device="cuda")
+        dev["len_counts"] = torch.zeros(64, dtype=torch.int32, device="cuda")
+        if live:
+            dl = torch.from_numpy(lengths.astype(np.uint16).view(np.int16).copy()).cuda()
+            live_h = C.c_uint32(0)
+            _lib.raise_for(_lib.lib().actc_codebook_from_lengths(
+                ctx.handle, C.c_void_p(dl.data_ptr()), A, C.c_void_p(dev["canon"].data_ptr()),
+                C.c_void_p(dev["len_counts"].data_ptr()), C.byref(live_h), sh))
+        self._live = live
+        self._dev = dev
+        return dev
+
+    def _desc(self, with_index=True) -> _lib.StreamDesc:
+        dev = self._dev
+        d = _lib.StreamDesc()
+        d.n = self.symbol_count
+        d.eb = float(self.params.eb)
+        d.radius = int(self.params.radius)
+        d.flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if self.params.preserve_zeros else 0
+        d.n_outliers = self._n_outliers
+        d.outlier_idx_dev = dev["out_idx"].data_ptr()
+        d.outlier_val_dev = dev["out_val"].data_ptr()
+        d.live_symbols = self._live
+        d.canon_syms_dev = dev["canon"].data_ptr()
+        d.len_counts_dev = dev["len_counts"].data_ptr()
+        d.payload_dev = dev["payload"].data_ptr()
+        d.payload_bits = self.payload_bits
+        d.chunk_offsets_dev = dev["chunk_off"].data_ptr() if (with_index and "chunk_off" in dev) else None
+        return d
+
+    def _ensure_index(self):
+        dev = self._ensure_device()
+        if "chunk_off" in dev:
+            return
+        torch = _lib.torch_cuda()
+        ctx = _lib.context()
+        sh, s = _lib.stream_handle()
+        n = self.symbol_count
+        nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
+        co = torch.zeros(max(nchunks, 1), dtype=torch.int64, device="cuda")
+        st = C.c_uint32(0)
+        d = self._desc(with_index=False)
+        _lib.raise_for(_lib.lib().actc_build_chunk_index(ctx.handle, C.byref(d), C.c_void_p(co.data_ptr()),
+                                                          C.byref(st), sh))
+        if st.value:
+            raise FormatError("bitstream does not decode to the declared symbol count")
+        dev["chunk_off"] = co
+
+    # ---- CMTZ (codec.py:95-179) ----
+    def to_bytes(self) -> bytes:
+        flags = 1 if self.params.preserve_zeros else 0
+        head = MAGIC_COMPRESSED + struct.pack(
+            "<Bd I BB", COMPRESSED_FORMAT_VERSION, self.params.eb, self.params.radius,
+            PREDICTOR_IDS[self.params.predictor], flags,
+        )
+        head += struct.pack("<BB", self.precision, len(self.dims))
+        head += struct.pack(f"<{len(self.dims)}Q", *self.dims)
+        out = bytearray(head)
+        idx = self.outlier_indices
+        out += struct.pack("<Q", len(idx))
+        if len(idx):
+            pairs = np.empty(len(idx), dtype=[("i", "<u8"), ("v", "<f4")])
+            pairs["i"] = idx
+            pairs["v"] = self.outlier_values
+            out += pairs.tobytes()
+        out += struct.pack("<Q", self.symbol_count)
+        out += _rle_encode_lengths(self.code_lengths)
+        out += struct.pack("<Q", self.payload_bits)
+        out += self.payload
+        out += struct.pack("<I", zlib.crc32(bytes(out)))
+        return bytes(out)
+
+    @classmethod
+    def from_bytes(cls, blob: bytes) -> "CompressedActivation":
+        if len(blob) < 4 + 1 + 8 + 4 + 2 + 2 + 4:
+            raise FormatError("compressed stream too short")
+        body, (stored_crc,) = blob[:-4], struct.unpack("<I", blob[-4:])
+        if zlib.crc32(body) != stored_crc:
+            raise FormatError("checksum mismatch")
+        cur = _Cursor(body)
+        if cur.take(4) != MAGIC_COMPRESSED:
+            raise FormatError("bad magic")
+        version, eb, radius, predictor_id, flags = struct.unpack("<Bd I BB", cur.take(15))
+        if version != COMPRESSED_FORMAT_VERSION:
+            raise FormatError(f"unsupported version {version}")
+        if predictor_id not in _PREDICTOR_NAMES:
+            raise FormatError(f"unknown predictor id {predictor_id}")
+        try:
+            params = CodecParams(eb=eb, radius=radius, predictor=_PREDICTOR_NAMES[predictor_id],
+                                 preserve_zeros=bool(flags & 1))
+        except ParameterError as exc:
+            raise FormatError(f"invalid codec params in header: {exc}") from exc
+        precision, rank = struct.unpack("<BB", cur.take(2))
+        if rank == 0:
+            raise FormatError("rank must be >= 1")
+        dims = struct.unpack(f"<{rank}Q", cur.take(8 * rank))
+        if any(d < 1 for d in dims):
+            raise FormatError(f"bad extents {dims}")
+        (n_out,) = struct.unpack("<Q", cur.take(8))
+        if n_out:
+            pairs = np.frombuffer(cur.take(12 * n_out), dtype=[("i", "<u8"), ("v", "<f4")])
+            out_idx = pairs["i"].astype(np.uint64)
+            out_val = pairs["v"].astype(np.float32)
+        else:
+            out_idx = np.empty(0, dtype=np.uint64)
+            out_val = np.empty(0, dtype=np.float32)
+        (symbol_count,) = struct.unpack("<Q", cur.take(8))
+        lengths = _rle_decode_lengths(cur, 2 * radius)
+        (payload_bits,) = struct.unpack("<Q", cur.take(8))
+        payload = cur.take((payload_bits + 7) // 8)
+        if cur.remaining():
+            raise FormatError("trailing bytes in compressed stream")
+        return cls(dims=tuple(int(d) for d in dims), precision=precision, params=params,
+                   outlier_indices=out_idx, outlier_values=out_val, symbol_count=int(symbol_count),
+                   code_lengths=lengths, payload=bytes(payload), payload_bits=int(payload_bits))
+
+    def __repr__(self):
+        return (f"CompressedActivation(dims={self.dims}, eb={self.params.eb}, bits={self.payload_bits}, "
+                f"outliers={self._n_outliers}, device={self.is_device_resident})")
+
+
+# ---------------------------------------------------------------------------
+# compress / decompress
+# ---------------------------------------------------------------------------
+
+
+def compress_device(x, params: CodecParams, dims=None, stream=None):
+    """Compress a contiguous fp32 CUDA tensor; returns (CompressedActivation, CompressionReport).
+
+    One host synchronisation (the compressed size is data dependent); all
+    buffers come from the torch caching allocator.
+    """
+    torch = _lib.torch_cuda()
+    if x.dtype != torch.float32:
+        raise ParameterError("compress expects a 32-bit tensor; convert explicitly with astype(4)")
+    if not x.is_contiguous():
+        x = x.contiguous()
+    dims = tuple(x.shape) if dims is None else tuple(dims)
+    if len(dims) == 0:
+        dims = (1,)
+    n = x.numel()
+    ctx = _lib.context(x.device.index)
+    sh, s = _lib.stream_handle(stream)
+    L = _lib.lib()
+    flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if params.preserve_zeros else 0
+    _lib.raise_for(L.actc_compress_plan(ctx.handle, C.c_void_p(x.data_ptr()), n, float(params.eb),
+                                        int(params.radius), flags, C.c_void_p(ctx.plan_buf.data_ptr()), sh))
+    s.synchronize()
+    plan = _lib.Plan.from_buffer_copy(ctx.plan)
+    if plan.status:
+        if plan.status == _lib.ACTC_EDATA:
+            from .errors import DataError
+            raise DataError("tensor contains NaN or Inf")
+        raise ParameterError("Huffman code length exceeds 63 bits")
+    dev = {
+        "payload": torch.empty(_payload_buffer_bytes(plan.payload_bits), dtype=torch.uint8, device=x.device),
+        "out_idx": torch.empty(plan.n_outliers, dtype=torch.int64, device=x.device),
+        "out_val": torch.empty(plan.n_outliers, dtype=torch.float32, device=x.device),
+        "canon": torch.empty(max(plan.live_symbols, 1), dtype=torch.int32, device=x.device),
+        "len_counts": torch.empty(64, dtype=torch.int32, device=x.device),
+        "chunk_off": torch.empty((n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK, dtype=torch.int64, device=x.device),
+    }
+    _lib.raise_for(L.actc_compress_encode(
+        ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev["payload"].data_ptr()),
+        C.c_void_p(dev["out_idx"].data_ptr()), C.c_void_p(dev["out_val"].data_ptr()),
+        C.c_void_p(dev["canon"].data_ptr()), C.c_void_p(dev["len_counts"].data_ptr()),
+        C.c_void_p(dev["chunk_off"].data_ptr()), sh))
+    c = CompressedActivation._from_device(dims, params, dev, plan.payload_bits, plan.n_outliers,
+                                          plan.live_symbols, plan.rle_runs)
+    blob_len = _cmtz_size(len(dims), plan.n_outliers, plan.rle_runs, plan.payload_bits)
+    frac = plan.n_outliers / n
+    report = CompressionReport(
+        original_bytes=n * 4, compressed_bytes=blob_len, ratio=(n * 4) / blob_len, outlier_fraction=frac,
+        codes_entropy_bits_per_symbol=float(plan.entropy_bits), outlier_warning=frac > 0.5,
+    )
+    return c, report
+
+
+def compress(t, params: CodecParams):
+    """Compress a 32-bit tensor; returns (CompressedActivation, report).  codec.py:296-340."""
+    torch = _lib.torch_cuda()
+    if isinstance(t, torch.Tensor):
+        return compress_device(to_device(t), params)
+    if t.precision != 4:
+        raise ParameterError("compress expects a 32-bit tensor; convert explicitly with astype(4)")
+    return compress_device(to_device(t), params, dims=t.dims)
+
+
+def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None, check=True):
+    """Reconstruct on the device.  Returns (tensor, nonzero_count or None).
+
+    dtype torch.float64 is bit-identical to the reference's output; float32
+    stores fp32 of it.  With check=False no host synchronisation happens
+    (the status and nonzero count are left in the context's mailbox).
+    """
+    torch = _lib.torch_cuda()
+    dtype = torch.float32 if dtype is None else dtype
+    n = c.element_count
+    if c.symbol_count != n:
+        raise FormatError(f"symbol count {c.symbol_count} != element count {n}")
+    c._ensure_index()
+    ctx = _lib.context()
+    sh, s = _lib.stream_handle(stream)
+    if out is None:
+        out = torch.empty(c.dims, dtype=dtype, device="cuda")
+    code = _lib.ACTC_DTYPE_F32 if out.dtype == torch.float32 else _lib.ACTC_DTYPE_F64
+    if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
+        raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
+    d = c._desc()
+    _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
+                                               C.c_void_p(ctx.dres_buf.data_ptr()), sh))
+    if not check:
+        return out, None
+    s.synchronize()
+    r = _lib.DecodeResult.from_buffer_copy(ctx.dres)
+    if r.status:
+        raise FormatError("invalid code in bitstream or outlier markers disagree with stored indices")
+    if r.markers != c._n_outliers:
+        raise FormatError("outlier markers disagree with stored indices")
+    return out, int(r.nonzero)
+
+
+def decompress(c: CompressedActivation) -> Tensor:
+    """Reconstruct the tensor a container describes (codec.py:343-369): fp64 host Tensor."""
+    torch = _lib.torch_cuda()
+    out, _ = decompress_device(c, dtype=torch.float64)
+    return Tensor(out.cpu().numpy().reshape(c.dims), precision=8)
+
+
+def write_compressed(c: CompressedActivation, sink) -> int:
+    blob = c.to_bytes()
+    if isinstance(sink, (str, bytes)) or hasattr(sink, "__fspath__"):
+        with open(sink, "wb") as fh:
+            fh.write(blob)
+    else:
+        sink.write(blob)
+    return len(blob)
+
+
+def read_compressed(source) -> CompressedActivation:
+    if isinstance(source, (str, bytes)) or hasattr(source, "__fspath__"):
+        with open(source, "rb") as fh:
+            return CompressedActivation.from_bytes(fh.read())
+    return CompressedActivation.from_bytes(source.read())
+
+
+# ---------------------------------------------------------------------------
+# pipeline internals (conformance entry points, all on the GPU)
+# ---------------------------------------------------------------------------
+
+
+def prequantize(t, eb: float) -> np.ndarray:
+    """codec.py:238-251 on the GPU (exact fp64 path)."""
+    if not (eb > 0 and np.isfinite(eb)):
+        raise ParameterError(f"eb must be a positive finite real, got {eb}")
+    torch = _lib.torch_cuda()
+    data = t.data if isinstance(t, Tensor) else np.asarray(t)
+    x = to_device(np.ascontiguousarray(data.reshape(-1)))
+    if x.dtype not in (torch.float32, torch.float64):
+        x = x.to(torch.float64)
+    q = torch.empty(x.numel(), dtype=torch.int64, device="cuda")
+    sh, s = _lib.stream_handle()
+    code = _lib.ACTC_DTYPE_F32 if x.dtype == torch.float32 else _lib.ACTC_DTYPE_F64
+    _lib.raise_for(_lib.lib().actc_prequantize(C.c_void_p(x.data_ptr()), code, x.numel(), float(eb),
+                                                C.c_void_p(q.data_ptr()), sh))
+    return q.cpu().numpy()
+
+
+def lorenzo_encode(lattice, radius: int, force_outlier=None):
+    """codec.py:254-272 on the GPU: returns (symbols, outlier_indices)."""
+    if radius < 2:
+        raise ParameterError(f"radius must be >= 2, got {radius}")
+    torch = _lib.torch_cuda()
+    lat = to_device(np.ascontiguousarray(np.asarray(lattice, dtype=np.int64).reshape(-1)))
+    n = lat.numel()
+    sym = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    force = None
+    if force_outlier is not None:
+        force = to_device(np.ascontiguousarray(np.asarray(force_outlier, dtype=np.uint8).reshape(-1)))
+    ctx = _lib.context()
+    sh, s = _lib.stream_handle()
+    _lib.raise_for(_lib.lib().actc_lorenzo_encode(
+        C.c_void_p(lat.data_ptr()), n, int(radius), C.c_void_p(force.data_ptr()) if force is not None else None,
+        C.c_void_p(sym.data_ptr()), C.c_void_p(ctx.u64_buf.data_ptr()), sh))
+    s.synchronize()
+    symbols = sym[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+    return symbols, np.flatnonzero(symbols == 0).astype(np.int64)
+
+
+def lorenzo_decode(symbols, outlier_lattice, radius: int) -> np.ndarray:
+    """codec.py:275-293 on the GPU."""
+    torch = _lib.torch_cuda()
+    s_h = np.asarray(symbols, dtype=np.int64).reshape(-1)
+    n = s_h.size
+    sym = to_device(np.ascontiguousarray(s_h.astype(np.uint32).view(np.int32)))
+    ol = np.asarray(outlier_lattice, dtype=np.int64).reshape(-1)
+    olat = to_device(np.ascontiguousarray(ol)) if ol.size else torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    ctx = _lib.context()
+    sh, s = _lib.stream_handle()
+    _lib.raise_for(_lib.lib().actc_lorenzo_decode(
+        C.c_void_p(sym.data_ptr()), n, C.c_void_p(olat.data_ptr()), ol.size, int(radius),
+        C.c_void_p(out.data_ptr()), C.c_void_p(ctx.u64_buf.data_ptr()), sh))
+    s.synchronize()
+    if int(ctx.u64_buf[:4].view(torch.int32).item()):
+        n_markers = int(np.count_nonzero(s_h == 0))
+        raise FormatError(f"outlier count mismatch: {n_markers} markers, {ol.size} stored values")
+    return out[:n].cpu().numpy()

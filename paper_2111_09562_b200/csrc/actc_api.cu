@@ -1,0 +1,612 @@
+// actc_api.cu -- the C ABI (include/actc.h): context, scratch management and
+// launch orchestration of K1..K5.  No torch types cross this boundary.
+#include <float.h>
+#include <stdarg.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+using namespace actc;
+
+namespace {
+
+thread_local char g_err[512];
+
+int set_err(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CK(call)                                                                 \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return set_err(ACTC_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKL()                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ != cudaSuccess)                                                      \
+      return set_err(ACTC_ECUDA, "launch failed: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+struct Buf {
+  void *p = nullptr;
+  size_t cap = 0;
+};
+
+int grow(Buf &b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return ACTC_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = bytes + bytes / 8 + 256;  // headroom to avoid re-growing by a few bytes
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ACTC_ENOMEM, "cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
+  }
+  b.cap = want;
+  return ACTC_OK;
+}
+
+inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+inline uint64_t pow2_ge(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+struct DecResult {
+  unsigned long long nonzero;
+  unsigned long long markers;
+  unsigned status;
+  unsigned pad;
+};
+
+}  // namespace
+
+struct actc_ctx {
+  int device = 0;
+  int num_sms = 148;
+  Buf sym, hist, cb, ctab, canon, lencnt, status, misc, lut, idx, part;
+  actc_plan_t *plan_dev = nullptr;
+  DecResult *dres_dev = nullptr;
+  // state carried from plan to encode
+  uint64_t n = 0, A = 0;
+  uint32_t radius = 0, sym_bytes = 2, win_lo = 0, win_n = 0;
+  int mode = 0;  // 1 = codec, 2 = huffman debug
+  int k1_blocks = 0, k3_blocks = 0, k4_blocks[5] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+// codebook scratch carve-up for alphabet A
+struct CbLayout {
+  size_t live_sym, live_freq, keys, vals, nf, lpar, npar, S, llen, ndepth, total;
+};
+CbLayout cb_layout(uint64_t A) {
+  CbLayout l;
+  uint64_t P = pow2_ge(A);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  l.live_sym = take(4 * A);
+  l.live_freq = take(8 * A);
+  l.keys = take(8 * P);
+  l.vals = take(4 * P);
+  l.nf = take(8 * A);
+  l.lpar = take(4 * A);
+  l.npar = take(4 * A);
+  l.S = take(8 * A);
+  l.llen = take(A);
+  l.ndepth = take(4 * A);
+  l.total = o;
+  return l;
+}
+
+constexpr size_t kK2Smem = 4096 * (8 + 8 + 4 + 4 + 4 + 8 + 4 + 1) + 64;
+
+int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const uint16_t *in_lengths,
+                 uint16_t *out_lengths, const unsigned long long *n_out, uint64_t n_symbols,
+                 uint32_t sym_bytes, cudaStream_t s, const unsigned *nonfinite = nullptr) {
+  CbLayout l = cb_layout(A);
+  int rc;
+  if ((rc = grow(c->cb, l.total))) return rc;
+  if ((rc = grow(c->ctab, 8 * A))) return rc;
+  if ((rc = grow(c->canon, 4 * A))) return rc;
+  if ((rc = grow(c->lencnt, 4 * 64))) return rc;
+  char *b = (char *)c->cb.p;
+  CodebookArgs a;
+  a.hist = hist;
+  a.A = A;
+  a.in_lengths = in_lengths;
+  a.ctab = (unsigned long long *)c->ctab.p;
+  a.canon = (uint32_t *)c->canon.p;
+  a.len_counts = (uint32_t *)c->lencnt.p;
+  a.out_lengths = out_lengths;
+  a.plan = c->plan_dev;
+  a.n_outliers = n_out;
+  a.nonfinite = nonfinite;
+  a.live_sym = (uint32_t *)(b + l.live_sym);
+  a.live_freq = (unsigned long long *)(b + l.live_freq);
+  a.keys = (unsigned long long *)(b + l.keys);
+  a.vals = (uint32_t *)(b + l.vals);
+  a.nf = (unsigned long long *)(b + l.nf);
+  a.lpar = (uint32_t *)(b + l.lpar);
+  a.npar = (uint32_t *)(b + l.npar);
+  a.S = (uint32_t *)(b + l.S);
+  a.llen = (uint8_t *)(b + l.llen);
+  a.ndepth = (uint8_t *)(b + l.ndepth);
+  a.n_symbols = n_symbols;
+  a.sym_bytes = sym_bytes;
+  CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
+  k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
+  CKL();
+  return ACTC_OK;
+}
+
+// misc counters layout (u64 slots)
+enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SLOTS = 8 };
+
+}  // namespace
+
+extern "C" {
+
+const char *actc_last_error(void) { return g_err; }
+int actc_version(void) { return 1; }
+
+int actc_ctx_create(int device, actc_ctx **out) {
+  *out = nullptr;
+  CK(cudaSetDevice(device));
+  actc_ctx *c = new actc_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&c->plan_dev, sizeof(actc_plan_t)) != cudaSuccess ||
+      cudaMalloc(&c->dres_dev, sizeof(DecResult)) != cudaSuccess) {
+    delete c;
+    return set_err(ACTC_ENOMEM, "ctx alloc failed");
+  }
+  int rc;
+  if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, 4 * kLutSize))) {
+    delete c;
+    return rc;
+  }
+  CK(cudaFuncSetAttribute(k2_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2Smem));
+  // occupancy-derived persistent grid sizes
+  int nb = 0;
+  size_t k1smem = K1_WIN * 4;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, k1smem);
+  c->k1_blocks = std::max(1, nb) * c->num_sms;
+  size_t k3smem = K3_WIN * 8 + ((size_t)K3_TILE * 56 / 32 + 4) * 4;
+  CK(cudaFuncSetAttribute(k3_encode<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3smem));
+  CK(cudaFuncSetAttribute(k3_encode<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k3_encode<uint16_t>, K3_THREADS, k3smem);
+  c->k3_blocks = std::max(1, nb) * c->num_sms;
+  size_t s16 = (size_t)K4_THREADS * (ACTC_CHUNK / 2 + 1) * 4, s32 = (size_t)K4_THREADS * (ACTC_CHUNK + 1) * 4;
+  CK(cudaFuncSetAttribute(k4_decode<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
+  CK(cudaFuncSetAttribute(k4_decode<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
+  CK(cudaFuncSetAttribute(k4_decode<0, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s32));
+  CK(cudaFuncSetAttribute(k4_decode<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s32));
+  CK(cudaFuncSetAttribute(k4_decode<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s32));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k4_decode<0, 16>, K4_THREADS, s16);
+  c->k4_blocks[0] = std::max(1, nb) * c->num_sms;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k4_decode<0, 32>, K4_THREADS, s32);
+  c->k4_blocks[1] = std::max(1, nb) * c->num_sms;
+  cudaGetLastError();
+  *out = c;
+  return ACTC_OK;
+}
+
+void actc_ctx_destroy(actc_ctx *c) {
+  if (!c) return;
+  Buf *bufs[] = {&c->sym, &c->hist, &c->cb, &c->ctab, &c->canon, &c->lencnt,
+                 &c->status, &c->misc, &c->lut, &c->idx, &c->part};
+  for (Buf *b : bufs)
+    if (b->p) cudaFree(b->p);
+  cudaFree(c->plan_dev);
+  cudaFree(c->dres_dev);
+  delete c;
+}
+
+int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius,
+                       uint32_t flags, actc_plan_t *plan_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
+  if (radius < 2) return set_err(ACTC_EPARAM, "radius must be >= 2, got %u", radius);
+  if (n == 0) return set_err(ACTC_EPARAM, "empty tensor");
+  if (n >= (1ull << 38)) return set_err(ACTC_EPARAM, "tensor too large");
+  const uint64_t A = 2ull * radius;
+  if (A > kMaxAlphabet) return set_err(ACTC_EPARAM, "radius %u too large for the device codebook (max %u)", radius, kMaxAlphabet / 2);
+  const uint32_t sb = A <= 65536 ? 2 : 4;
+  int rc;
+  if ((rc = grow(c->sym, (size_t)sb * n + 64))) return rc;
+  if ((rc = grow(c->hist, 8 * A))) return rc;
+  CK(cudaMemsetAsync(c->hist.p, 0, 8 * A, s));
+  CK(cudaMemsetAsync(c->misc.p, 0, 8 * M_SLOTS, s));
+  unsigned long long *misc = (unsigned long long *)c->misc.p;
+
+  QParams P;
+  P.eb = eb;
+  P.two_eb = 2.0 * eb;
+  double inv = 1.0 / P.two_eb;
+  float inv32 = (float)inv;
+  P.inv32 = inv32;
+  P.fast = (isfinite(inv32) && inv32 >= FLT_MIN) ? 1 : 0;
+  uint32_t win_n = (uint32_t)std::min<uint64_t>(A, K1_WIN);
+  uint32_t win_lo = A <= K1_WIN ? 0 : radius - K1_WIN / 2;
+  uint64_t ntiles = cdiv(n, K1_TILE);
+  int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)c->k1_blocks);
+  if (sb == 2)
+    k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, win_n * 4, s>>>(
+        x, n, P, radius, (uint16_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
+        (unsigned *)(misc + M_BAD));
+  else
+    k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, win_n * 4, s>>>(
+        x, n, P, radius, (uint32_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
+        (unsigned *)(misc + M_BAD));
+  CKL();
+  if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, nullptr, misc + M_NOUT, n, sb, s,
+                         (const unsigned *)(misc + M_BAD))))
+    return rc;
+  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  c->n = n;
+  c->A = A;
+  c->radius = radius;
+  c->sym_bytes = sb;
+  c->win_n = (uint32_t)std::min<uint64_t>(A, K3_WIN);
+  c->win_lo = A <= K3_WIN ? 0 : radius - K3_WIN / 2;
+  c->mode = 1;
+  return ACTC_OK;
+}
+
+static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, const float *x,
+                         uint8_t *payload, uint64_t *out_idx, float *out_val, uint64_t *chunk_off,
+                         int extract, cudaStream_t s) {
+  uint64_t ntiles = cdiv(n, K3_TILE);
+  int rc;
+  // status: flag u32 | agg_bits | agg_nz | inc_bits | inc_nz (u64) | tail u32
+  size_t need = ntiles * (4 + 8 * 4 + 4) + 1024;
+  if ((rc = grow(c->status, need))) return rc;
+  char *b = (char *)c->status.p;
+  EncStatus st;
+  st.flag = (unsigned *)b;
+  size_t o = ((ntiles * 4 + 255) / 256) * 256;
+  st.agg_bits = (unsigned long long *)(b + o); o += ntiles * 8;
+  st.agg_nz = (unsigned long long *)(b + o); o += ntiles * 8;
+  st.inc_bits = (unsigned long long *)(b + o); o += ntiles * 8;
+  st.inc_nz = (unsigned long long *)(b + o); o += ntiles * 8;
+  st.tail = (unsigned *)(b + o);
+  CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
+  unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
+  CK(cudaMemsetAsync(ticket, 0, 8, s));
+  size_t smem = (size_t)c->win_n * 8 + ((size_t)K3_TILE * 56 / 32 + 4) * 4;
+  int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)c->k3_blocks);
+  if (sb == 2)
+    k3_encode<uint16_t><<<grid, K3_THREADS, smem, s>>>(
+        (const uint16_t *)sym, n, (const unsigned long long *)c->ctab.p, c->win_lo, c->win_n, x,
+        (uint32_t *)payload, (unsigned long long *)out_idx, out_val, (unsigned long long *)chunk_off, st,
+        ticket, ntiles, extract);
+  else
+    k3_encode<uint32_t><<<grid, K3_THREADS, smem, s>>>(
+        (const uint32_t *)sym, n, (const unsigned long long *)c->ctab.p, c->win_lo, c->win_n, x,
+        (uint32_t *)payload, (unsigned long long *)out_idx, out_val, (unsigned long long *)chunk_off, st,
+        ticket, ntiles, extract);
+  CKL();
+  return ACTC_OK;
+}
+
+int actc_compress_encode(actc_ctx *c, const float *x, const actc_plan_t *plan, uint8_t *payload,
+                         uint64_t *out_idx, float *out_val, uint32_t *canon, uint32_t *len_counts,
+                         uint64_t *chunk_off, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->mode != 1 || plan->n != c->n) return set_err(ACTC_EPARAM, "actc_compress_encode without a matching plan");
+  if (plan->status != ACTC_OK) return set_err(plan->status, "Huffman code length exceeds 63 bits");
+  int rc = launch_encode(c, c->sym.p, c->sym_bytes, c->n, x, payload, out_idx, out_val, chunk_off, 1, s);
+  if (rc) return rc;
+  if (plan->live_symbols)
+    CK(cudaMemcpyAsync(canon, c->canon.p, 4ull * plan->live_symbols, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(len_counts, c->lencnt.p, 4 * 64, cudaMemcpyDeviceToDevice, s));
+  return ACTC_OK;
+}
+
+static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int mode,
+                         actc_decode_result_t *res_host, cudaStream_t s) {
+  const actc_stream_t &S = *st_in;
+  if (S.n == 0) return set_err(ACTC_EPARAM, "empty stream");
+  if (!S.chunk_offsets_dev) return set_err(ACTC_EPARAM, "stream has no chunk index (call actc_build_chunk_index)");
+  if (S.live_symbols == 0) return set_err(ACTC_EFORMAT, "empty code table with nonzero symbol count");
+  const uint64_t nchunks = cdiv(S.n, ACTC_CHUNK);
+  const uint64_t ntiles = cdiv(nchunks, K4_THREADS);
+  int rc;
+  size_t need = ntiles * (4 + 4 + 8 + 8) + 1024;
+  if ((rc = grow(c->status, need))) return rc;
+  char *b = (char *)c->status.p;
+  DecStatus st;
+  st.flag = (unsigned *)b;
+  size_t o = ((ntiles * 4 + 255) / 256) * 256;
+  st.agg_r = (int *)(b + o); o += ((ntiles * 4 + 255) / 256) * 256;
+  st.agg_v = (long long *)(b + o); o += ntiles * 8;
+  st.inc_v = (long long *)(b + o);
+  CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
+  unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
+  CK(cudaMemsetAsync(ticket, 0, 8, s));
+  CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
+  k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p);
+  CKL();
+  DecodeArgs a;
+  a.n = S.n;
+  a.eb = S.eb;
+  a.two_eb = 2.0 * S.eb;
+  a.radius = S.radius;
+  a.preserve = (S.flags & ACTC_FLAG_PRESERVE_ZEROS) ? 1 : 0;
+  a.k = S.n_outliers;
+  a.out_idx = (const unsigned long long *)S.outlier_idx_dev;
+  a.out_val = S.outlier_val_dev;
+  a.canon = S.canon_syms_dev;
+  a.len_counts = S.len_counts_dev;
+  a.lut = (const uint32_t *)c->lut.p;
+  a.payload = (const uint32_t *)S.payload_dev;
+  a.payload_bits = S.payload_bits;
+  a.chunk_off = (const unsigned long long *)S.chunk_offsets_dev;
+  a.out = out;
+  a.st = st;
+  a.ticket = ticket;
+  a.ntiles = ntiles;
+  a.nonzero = &c->dres_dev->nonzero;
+  a.markers = &c->dres_dev->markers;
+  a.status = &c->dres_dev->status;
+  const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
+  const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
+  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)(sw16 ? c->k4_blocks[0] : c->k4_blocks[1]));
+  if (mode == 0)
+    sw16 ? k4_decode<0, 16><<<grid, K4_THREADS, smem, s>>>(a) : k4_decode<0, 32><<<grid, K4_THREADS, smem, s>>>(a);
+  else if (mode == 1)
+    sw16 ? k4_decode<1, 16><<<grid, K4_THREADS, smem, s>>>(a) : k4_decode<1, 32><<<grid, K4_THREADS, smem, s>>>(a);
+  else
+    k4_decode<2, 32><<<grid, K4_THREADS, smem, s>>>(a);
+  CKL();
+  if (res_host) CK(cudaMemcpyAsync(res_host, c->dres_dev, sizeof(DecResult), cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+int actc_decompress(actc_ctx *c, const actc_stream_t *stream, void *out, int out_dtype,
+                    actc_decode_result_t *result_host, actc_stream s) {
+  if (out_dtype != ACTC_DTYPE_F32 && out_dtype != ACTC_DTYPE_F64) return set_err(ACTC_EPARAM, "bad out dtype");
+  if (!(stream->eb > 0 && isfinite(stream->eb)) || stream->radius < 2)
+    return set_err(ACTC_EFORMAT, "invalid codec params in stream");
+  if (2ull * stream->radius > kMaxAlphabet) return set_err(ACTC_EPARAM, "radius too large for the device decoder");
+  return launch_decode(c, stream, out, out_dtype == ACTC_DTYPE_F32 ? 0 : 1, result_host, (cudaStream_t)s);
+}
+
+int actc_codebook_from_lengths(actc_ctx *c, const uint16_t *lengths, uint64_t A, uint32_t *canon,
+                               uint32_t *len_counts, uint32_t *live_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (A > kMaxAlphabet || A == 0) return set_err(ACTC_EPARAM, "alphabet too large");
+  int rc = run_codebook(c, nullptr, A, lengths, nullptr, nullptr, 0, 0, s);
+  if (rc) return rc;
+  actc_plan_t plan;
+  CK(cudaMemcpyAsync(&plan, c->plan_dev, sizeof(plan), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (plan.status == ACTC_EPARAM) return set_err(ACTC_EFORMAT, "code length exceeds 63 bits");
+  if (plan.live_symbols) CK(cudaMemcpyAsync(canon, c->canon.p, 4ull * plan.live_symbols, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(len_counts, c->lencnt.p, 4 * 64, cudaMemcpyDeviceToDevice, s));
+  *live_host = plan.live_symbols;
+  return ACTC_OK;
+}
+
+int actc_build_chunk_index(actc_ctx *c, const actc_stream_t *S, uint64_t *chunk_off, uint32_t *status_host,
+                           actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  *status_host = ACTC_OK;
+  if (S->n == 0) return ACTC_OK;
+  const uint64_t seg_bits = 4096;
+  const uint64_t nseg = std::max<uint64_t>(1, cdiv(S->payload_bits, seg_bits));
+  int rc;
+  if ((rc = grow(c->idx, nseg * 8 * 4 + 1024))) return rc;
+  unsigned long long *start = (unsigned long long *)c->idx.p;
+  unsigned long long *endp = start + nseg, *cnt = endp + nseg, *base = cnt + nseg;
+  unsigned long long *misc = (unsigned long long *)c->misc.p;
+  unsigned *changed = (unsigned *)(misc + M_CHANGED);
+  unsigned *status = (unsigned *)(misc + M_STATUS);
+  CK(cudaMemsetAsync(misc + M_STATUS, 0, 8, s));
+  k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S->canon_syms_dev, S->len_counts_dev, (uint32_t *)c->lut.p);
+  CKL();
+  const int tpb = 128;
+  const int grid = (int)cdiv(nseg, tpb);
+  const uint32_t *pw = (const uint32_t *)S->payload_dev;
+  k_sync_pass<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
+                                   nseg, start, endp, cnt, changed, status, 1);
+  CKL();
+  unsigned h_changed = 1;
+  for (uint64_t it = 0; it <= nseg + 1 && h_changed; it++) {
+    CK(cudaMemsetAsync(changed, 0, 4, s));
+    k_sync_pass<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
+                                     nseg, start, endp, cnt, changed, status, 0);
+    CKL();
+    CK(cudaMemcpyAsync(&h_changed, changed, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  k_excl_scan_u64<<<1, 1024, 0, s>>>(cnt, nseg, base, misc + M_SCAN_TOT);
+  CKL();
+  unsigned long long total = 0, last_end = 0;
+  unsigned st = 0;
+  CK(cudaMemcpyAsync(&total, misc + M_SCAN_TOT, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&last_end, endp + nseg - 1, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&st, status, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (st || total < S->n || (total == S->n && last_end != S->payload_bits) || h_changed) {
+    *status_host = ACTC_EFORMAT;
+    return ACTC_OK;
+  }
+  k_index_emit<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
+                                    nseg, start, base, S->n, (unsigned long long *)chunk_off);
+  CKL();
+  return ACTC_OK;
+}
+
+int actc_prequantize(const void *x, int dtype, uint64_t n, double eb, int64_t *q, actc_stream s) {
+  if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
+  if (!n) return ACTC_OK;
+  int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 16);
+  k_prequantize<<<grid, 256, 0, (cudaStream_t)s>>>(x, dtype, n, eb, (long long *)q);
+  CKL();
+  return ACTC_OK;
+}
+
+int actc_lorenzo_encode(const int64_t *lat, uint64_t n, uint32_t radius, const uint8_t *force, uint32_t *sym,
+                        uint64_t *n_out_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (radius < 2) return set_err(ACTC_EPARAM, "radius must be >= 2, got %u", radius);
+  static thread_local unsigned long long *d_cnt = nullptr;
+  if (!d_cnt) CK(cudaMalloc(&d_cnt, 8));
+  CK(cudaMemsetAsync(d_cnt, 0, 8, s));
+  if (n) {
+    int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 16);
+    k_lorenzo_encode<<<grid, 256, 0, s>>>((const long long *)lat, n, radius, force, sym, d_cnt);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(n_out_host, d_cnt, 8, cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+int actc_lorenzo_decode(const uint32_t *sym, uint64_t n, const int64_t *olat, uint64_t k, uint32_t radius,
+                        int64_t *out, uint32_t *status_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  static thread_local unsigned *d_st = nullptr;
+  if (!d_st) CK(cudaMalloc(&d_st, 4));
+  CK(cudaMemsetAsync(d_st, 0, 4, s));
+  k_lorenzo_decode_seq<<<1, 1, 0, s>>>(sym, n, (const long long *)olat, k, radius, (long long *)out, d_st);
+  CKL();
+  CK(cudaMemcpyAsync(status_host, d_st, 4, cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+int actc_huffman_plan(actc_ctx *c, const uint32_t *sym, uint64_t n, uint64_t A, uint16_t *lengths,
+                      actc_plan_t *plan_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (A < 1) return set_err(ACTC_EPARAM, "alphabet_size must be >= 1");
+  if (A > kMaxAlphabet) return set_err(ACTC_EPARAM, "alphabet too large for the device codebook");
+  int rc;
+  if ((rc = grow(c->hist, 8 * A))) return rc;
+  CK(cudaMemsetAsync(c->hist.p, 0, 8 * A, s));
+  CK(cudaMemsetAsync(c->misc.p, 0, 8 * M_SLOTS, s));
+  unsigned long long *misc = (unsigned long long *)c->misc.p;
+  uint32_t win_n = (uint32_t)std::min<uint64_t>(A, K1_WIN);
+  if (n) {
+    int grid = (int)std::min<uint64_t>(cdiv(n, 256), (uint64_t)c->num_sms * 4);
+    k_hist_u32<<<grid, 256, win_n * 4, s>>>(sym, n, A, (unsigned long long *)c->hist.p, (unsigned *)(misc + M_BAD), win_n);
+    CKL();
+  }
+  unsigned bad = 0;
+  CK(cudaMemcpyAsync(&bad, misc + M_BAD, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) return set_err(ACTC_EPARAM, "symbol out of alphabet range");
+  if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, lengths, nullptr, n, 4, s))) return rc;
+  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  c->n = n;
+  c->A = A;
+  c->radius = 0;
+  c->sym_bytes = 4;
+  c->win_n = (uint32_t)std::min<uint64_t>(A, K3_WIN);
+  c->win_lo = 0;
+  c->mode = 2;
+  return ACTC_OK;
+}
+
+int actc_huffman_encode(actc_ctx *c, const uint32_t *sym, const actc_plan_t *plan, uint8_t *payload,
+                        uint32_t *canon, uint32_t *len_counts, uint64_t *chunk_off, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->mode != 2 || plan->n != c->n) return set_err(ACTC_EPARAM, "actc_huffman_encode without a matching plan");
+  if (plan->status != ACTC_OK) return set_err(plan->status, "Huffman code length exceeds 63 bits");
+  if (c->n) {
+    int rc = launch_encode(c, sym, 4, c->n, nullptr, payload, nullptr, nullptr, chunk_off, 0, s);
+    if (rc) return rc;
+  }
+  if (plan->live_symbols)
+    CK(cudaMemcpyAsync(canon, c->canon.p, 4ull * plan->live_symbols, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(len_counts, c->lencnt.p, 4 * 64, cudaMemcpyDeviceToDevice, s));
+  return ACTC_OK;
+}
+
+int actc_huffman_decode(actc_ctx *c, const actc_stream_t *stream, uint32_t *symbols,
+                        actc_decode_result_t *result_host, actc_stream s) {
+  return launch_decode(c, stream, symbols, 2, result_host, (cudaStream_t)s);
+}
+
+int actc_code_lengths(actc_ctx *c, const uint64_t *freqs, uint64_t A, uint16_t *lengths, actc_plan_t *plan_host,
+                      actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (A < 1 || A > kMaxAlphabet) return set_err(ACTC_EPARAM, "bad alphabet size");
+  int rc = run_codebook(c, (const unsigned long long *)freqs, A, nullptr, lengths, nullptr, 1, 4, s);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+int actc_count_nonzero(const void *x, int dtype, uint64_t n, uint64_t *out_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  static thread_local unsigned long long *d = nullptr;
+  if (!d) CK(cudaMalloc(&d, 8));
+  CK(cudaMemsetAsync(d, 0, 8, s));
+  if (n) {
+    int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 8);
+    k_count_nonzero<<<grid, 256, 0, s>>>(x, dtype, n, d);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(out_host, d, 8, cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+int actc_mean_abs(actc_ctx *c, const void *x, int dtype, uint64_t n, double *out_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return set_err(ACTC_EPARAM, "empty tensor");
+  int depth = 0;
+  while (depth < 16 && (n >> depth) > 4096) depth++;
+  int rc;
+  if ((rc = grow(c->part, 8ull * ((1ull << depth) + 1)))) return rc;
+  double *part = (double *)c->part.p;
+  uint64_t nt = 1ull << depth;
+  k_pairwise_partials<<<(int)cdiv(nt, 128), 128, 0, s>>>(x, dtype, n, depth, part);
+  CKL();
+  k_pairwise_finish<<<1, 1, 0, s>>>(part, dtype, n, depth, part + nt);
+  CKL();
+  CK(cudaMemcpyAsync(out_host, part + nt, 8, cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+int actc_lbar(actc_ctx *c, const void *g, int dtype, uint64_t N, uint64_t per, void *per_sample_max,
+              double *out_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (N == 0) return set_err(ACTC_EPARAM, "empty batch");
+  int rc;
+  if ((rc = grow(c->part, 8 * N + 8 * N + 64))) return rc;
+  unsigned long long *bits = (unsigned long long *)c->part.p;
+  double *res = (double *)(bits + N);
+  void *psm = per_sample_max ? per_sample_max : (void *)(res + 1);
+  CK(cudaMemsetAsync(bits, 0, 8 * N, s));
+  uint64_t total = N * per;
+  if (total) {
+    int grid = (int)std::min<uint64_t>(cdiv(total, 256), 148 * 8);
+    k_sample_max<<<grid, 256, 0, s>>>(g, dtype, N, per, bits);
+    CKL();
+  }
+  k_lbar_finish<<<1, 1, 0, s>>>(bits, dtype, N, psm, res);
+  CKL();
+  CK(cudaMemcpyAsync(out_host, res, 8, cudaMemcpyDeviceToHost, s));
+  return ACTC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// K1: fused prequantize + bound check + 1-D Lorenzo + outlier flag +
+// quant-code histogram (shared-memory window + global tail).
+//
+// Replaces, per element of the flattened fp32 stream:
+//   prequantize          codec.py:238-251
+//   bound check          codec.py:311-312
+//   lorenzo_encode       codec.py:254-272 (delta vs own predecessor lattice)
+//   bincount             huffman.py:183
+// Memory traffic: 4 B read + sizeof(Sym) written per element; the lattice
+// never leaves registers.  Each thread owns 16 consecutive elements
+// (4 x 128-bit loads); the predecessor lattice value of the first element
+// comes from the neighbouring lane by shuffle, lane 0 recomputes it from
+// x[i-1] (deterministic, identical result).
+#include "kernels.cuh"
+
+namespace actc {
+
+template <typename SymT>
+__global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
+    const float *__restrict__ x, uint64_t n, QParams P, uint32_t radius, SymT *__restrict__ sym,
+    unsigned long long *__restrict__ ghist, unsigned long long *__restrict__ n_outliers,
+    uint32_t win_lo, uint32_t win_n, unsigned *__restrict__ nonfinite) {
+  extern __shared__ unsigned sh_hist[];
+  for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) sh_hist[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
+  unsigned outl = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t base = tile * K1_TILE + (uint64_t)threadIdx.x * K1_EPT;
+    float xv[K1_EPT];
+    const bool full = base + K1_EPT <= n;
+    if (full) {
+      const float4 *p = reinterpret_cast<const float4 *>(x + base);
+#pragma unroll
+      for (int j = 0; j < K1_EPT / 4; j++) {
+        float4 v = __ldcs(p + j);  // streaming: read once
+        xv[4 * j] = v.x; xv[4 * j + 1] = v.y; xv[4 * j + 2] = v.z; xv[4 * j + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < K1_EPT; j++) xv[j] = (base + j < n) ? x[base + j] : 0.0f;
+    }
+    long long q[K1_EPT];
+    unsigned viol = 0;
+    bool fin = true;
+#pragma unroll
+    for (int j = 0; j < K1_EPT; j++) fin &= isfinite(xv[j]);
+    if (!fin) atomicOr(nonfinite, 1u);  // Tensor rejects NaN/Inf (tensor.py:56-57)
+#pragma unroll
+    for (int j = 0; j < K1_EPT; j++) {
+      bool vj;
+      q[j] = quant_elem(xv[j], P, vj);
+      viol |= (unsigned)vj << j;
+    }
+    long long prev = __shfl_up_sync(0xffffffffu, q[K1_EPT - 1], 1);
+    if (lane == 0) {
+      bool dummy;
+      prev = (base > 0 && base - 1 < n) ? quant_elem(x[base - 1], P, dummy) : 0;
+    }
+    SymT s[K1_EPT];
+#pragma unroll
+    for (int j = 0; j < K1_EPT; j++) {
+      long long d = q[j] - prev;
+      prev = q[j];
+      unsigned long long ad = d < 0 ? (unsigned long long)(-d) : (unsigned long long)d;
+      bool o = ad >= radius || ((viol >> j) & 1u);
+      uint32_t sj = o ? 0u : (uint32_t)(d + (long long)radius);
+      s[j] = (SymT)sj;
+      if (base + j < n) {
+        outl += o;
+        uint32_t w = sj - win_lo;
+        if (w < win_n)
+          atomicAdd(&sh_hist[w], 1u);
+        else
+          atomicAdd(&ghist[sj], 1ull);
+      }
+    }
+    if (full) {
+      if (sizeof(SymT) == 2) {
+        uint4 *d = reinterpret_cast<uint4 *>(sym + base);
+#pragma unroll
+        for (int j = 0; j < K1_EPT / 8; j++) {
+          uint4 v;
+          v.x = (uint32_t)s[8 * j + 0] | ((uint32_t)s[8 * j + 1] << 16);
+          v.y = (uint32_t)s[8 * j + 2] | ((uint32_t)s[8 * j + 3] << 16);
+          v.z = (uint32_t)s[8 * j + 4] | ((uint32_t)s[8 * j + 5] << 16);
+          v.w = (uint32_t)s[8 * j + 6] | ((uint32_t)s[8 * j + 7] << 16);
+          d[j] = v;
+        }
+      } else {
+        uint4 *d = reinterpret_cast<uint4 *>(sym + base);
+#pragma unroll
+        for (int j = 0; j < K1_EPT / 4; j++)
+          d[j] = make_uint4((uint32_t)s[4 * j], (uint32_t)s[4 * j + 1], (uint32_t)s[4 * j + 2],
+                            (uint32_t)s[4 * j + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < K1_EPT; j++)
+        if (base + j < n) sym[base + j] = s[j];
+    }
+  }
+  unsigned wsum = warp_sum(outl);
+  if (lane == 0 && wsum) atomicAdd(n_outliers, (unsigned long long)wsum);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) {
+    unsigned c = sh_hist[i];
+    if (c) atomicAdd(&ghist[win_lo + i], (unsigned long long)c);
+  }
+}
+
+template __global__ void k1_quant_lorenzo_hist<uint16_t>(const float *, uint64_t, QParams, uint32_t,
+                                                         uint16_t *, unsigned long long *,
+                                                         unsigned long long *, uint32_t, uint32_t,
+                                                         unsigned *);
+template __global__ void k1_quant_lorenzo_hist<uint32_t>(const float *, uint64_t, QParams, uint32_t,
+                                                         uint32_t *, unsigned long long *,
+                                                         unsigned long long *, uint32_t, uint32_t,
+                                                         unsigned *);
+
+// Histogram of an arbitrary u32 symbol stream (huffman_encode's bincount,
+// huffman.py:181-183) with the out-of-range check.
+__global__ void k_hist_u32(const uint32_t *__restrict__ s, uint64_t n, uint64_t alphabet,
+                           unsigned long long *__restrict__ ghist, unsigned *__restrict__ bad,
+                           uint32_t win_n) {
+  extern __shared__ unsigned sh_hist[];
+  for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) sh_hist[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = s[i];
+    if (v >= alphabet) {
+      atomicOr(bad, 1u);
+      continue;
+    }
+    if (v < win_n)
+      atomicAdd(&sh_hist[v], 1u);
+    else
+      atomicAdd(&ghist[v], 1ull);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x)
+    if (sh_hist[i]) atomicAdd(&ghist[i], (unsigned long long)sh_hist[i]);
+}
+
+// prequantize only (codec.py:238-251), fp32 or fp64 input, exact path.
+__global__ void k_prequantize(const void *__restrict__ x, int dtype, uint64_t n, double eb,
+                              long long *__restrict__ q) {
+  const double two_eb = 2.0 * eb;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    double v = dtype == ACTC_DTYPE_F32 ? (double)((const float *)x)[i] : ((const double *)x)[i];
+    bool viol;
+    q[i] = quant_exact(v, two_eb, eb, viol);
+  }
+}
+
+// lorenzo_encode over an int64 lattice (codec.py:254-272).
+__global__ void k_lorenzo_encode(const long long *__restrict__ lat, uint64_t n, uint32_t radius,
+                                 const uint8_t *__restrict__ force, uint32_t *__restrict__ sym,
+                                 unsigned long long *__restrict__ n_out) {
+  unsigned cnt = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    long long prev = i ? lat[i - 1] : 0;
+    long long d = (long long)((unsigned long long)lat[i] - (unsigned long long)prev);
+    unsigned long long ad = d < 0 ? (unsigned long long)(-d) : (unsigned long long)d;
+    bool o = ad >= radius || (force && force[i]);
+    sym[i] = o ? 0u : (uint32_t)(d + (long long)radius);
+    cnt += o;
+  }
+  cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_out, (unsigned long long)cnt);
+}
+
+}  // namespace actc

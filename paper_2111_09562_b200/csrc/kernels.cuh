@@ -1,0 +1,153 @@
+// kernels.cuh -- launch-shape constants and kernel declarations.
+#pragma once
+#include "actc_internal.cuh"
+
+namespace actc {
+
+// K1: 256 threads x 16 elements per tile
+constexpr int K1_THREADS = 256;
+constexpr int K1_EPT = 16;
+constexpr int K1_TILE = K1_THREADS * K1_EPT;
+constexpr uint32_t K1_WIN = 8192;  // shared-memory histogram window (bins)
+
+// K2: one CTA
+constexpr int K2_THREADS = 1024;
+constexpr uint32_t K2_SMEM_SORT_MAX = 8192;  // keys sorted in shared memory
+
+// K3: 256 threads x 16 symbols per tile (16 decode chunks per tile)
+constexpr int K3_THREADS = 256;
+constexpr int K3_EPT = 16;
+constexpr int K3_TILE = K3_THREADS * K3_EPT;
+constexpr uint32_t K3_WIN = 4096;  // code-table window cached in shared memory
+
+// K4: one thread decodes one ACTC_CHUNK-symbol chunk
+constexpr int K4_THREADS = 64;
+constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
+
+// lookback status for the encoder (per K3 tile)
+struct EncStatus {
+  unsigned *flag;
+  unsigned long long *agg_bits, *agg_nz, *inc_bits, *inc_nz;
+  unsigned *tail;
+};
+// lookback status for the decoder (per K4 tile)
+struct DecStatus {
+  unsigned *flag;
+  int *agg_r;
+  long long *agg_v, *inc_v;
+};
+
+template <typename SymT>
+__global__ void k1_quant_lorenzo_hist(const float *__restrict__ x, uint64_t n, QParams P,
+                                      uint32_t radius, SymT *__restrict__ sym,
+                                      unsigned long long *__restrict__ ghist,
+                                      unsigned long long *__restrict__ n_outliers, uint32_t win_lo,
+                                      uint32_t win_n, unsigned *__restrict__ nonfinite);
+__global__ void k_hist_u32(const uint32_t *__restrict__ s, uint64_t n, uint64_t alphabet,
+                           unsigned long long *__restrict__ ghist, unsigned *__restrict__ bad,
+                           uint32_t win_n);
+__global__ void k_prequantize(const void *__restrict__ x, int dtype, uint64_t n, double eb,
+                              long long *__restrict__ q);
+__global__ void k_lorenzo_encode(const long long *__restrict__ lat, uint64_t n, uint32_t radius,
+                                 const uint8_t *__restrict__ force, uint32_t *__restrict__ sym,
+                                 unsigned long long *__restrict__ n_out);
+
+// K2 codebook.  Scratch layout is owned by the host side (CodebookScratch).
+struct CodebookArgs {
+  const unsigned long long *hist;  // [A]
+  uint64_t A;
+  const uint16_t *in_lengths;      // if non-null: skip Huffman, use these lengths
+  // outputs
+  unsigned long long *ctab;        // [A] (code << 8) | len, live entries only
+  uint32_t *canon;                 // [L] canonical order
+  uint32_t *len_counts;            // [64]
+  uint16_t *out_lengths;           // optional [A] full length table
+  actc_plan_t *plan;               // device plan (fields n / n_outliers preset)
+  const unsigned long long *n_outliers;  // optional counter from K1
+  const unsigned *nonfinite;             // optional flag from K1 -> ACTC_EDATA
+  // scratch (global, used when L exceeds the shared-memory capacity)
+  uint32_t *live_sym;              // [A]
+  unsigned long long *live_freq;   // [A]
+  unsigned long long *keys;        // [pow2 >= A]
+  uint32_t *vals;                  // [pow2 >= A]
+  unsigned long long *nf;          // [A]
+  uint32_t *lpar, *npar, *S;       // [A], [A], [2A]
+  uint8_t *llen, *ndepth;          // [A], [A]
+  uint64_t n_symbols;              // total symbol count (for entropy)
+  uint32_t sym_bytes;
+};
+__global__ void k2_codebook(CodebookArgs a);
+
+template <typename SymT>
+__global__ void k3_encode(const SymT *__restrict__ sym, uint64_t n,
+                          const unsigned long long *__restrict__ ctab, uint32_t win_lo,
+                          uint32_t win_n, const float *__restrict__ x,
+                          uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
+                          float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
+                          EncStatus st, unsigned *__restrict__ ticket, uint64_t ntiles,
+                          int extract_outliers);
+
+__global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
+                            uint32_t *__restrict__ lut);
+
+struct DecodeArgs {
+  uint64_t n;
+  double eb, two_eb;
+  uint32_t radius;
+  int preserve;
+  uint64_t k;
+  const unsigned long long *out_idx;
+  const float *out_val;
+  const uint32_t *canon;
+  const uint32_t *len_counts;
+  const uint32_t *lut;
+  const uint32_t *payload;
+  uint64_t payload_bits;
+  const unsigned long long *chunk_off;
+  void *out;  // f32 / f64 values or u32 symbols
+  DecStatus st;
+  unsigned *ticket;
+  uint64_t ntiles;
+  unsigned long long *nonzero;
+  unsigned long long *markers;
+  unsigned *status;
+};
+// MODE: 0 = fp32 recon, 1 = fp64 recon, 2 = raw u32 symbols
+// SW: staging width of decoded symbols in shared memory (16 or 32 bits)
+template <int MODE, int SW>
+__global__ void k4_decode(DecodeArgs a);
+__global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
+                                unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
+
+__global__ void k_lorenzo_decode_seq(const uint32_t *__restrict__ sym, uint64_t n,
+                                     const long long *__restrict__ olat, uint64_t k,
+                                     uint32_t radius, long long *__restrict__ out,
+                                     unsigned *__restrict__ status);
+
+// index rebuild for streams without chunk offsets
+__global__ void k_sync_pass(const uint32_t *__restrict__ payload, uint64_t payload_bits,
+                            const uint32_t *__restrict__ lut, const uint32_t *__restrict__ len_counts,
+                            uint64_t seg_bits, uint64_t nseg, unsigned long long *__restrict__ start,
+                            unsigned long long *__restrict__ end_pos,
+                            unsigned long long *__restrict__ count, unsigned *__restrict__ changed,
+                            unsigned *__restrict__ status, int first);
+__global__ void k_index_emit(const uint32_t *__restrict__ payload, uint64_t payload_bits,
+                             const uint32_t *__restrict__ lut, const uint32_t *__restrict__ len_counts,
+                             uint64_t seg_bits, uint64_t nseg,
+                             const unsigned long long *__restrict__ start,
+                             const unsigned long long *__restrict__ sym_base, uint64_t n,
+                             unsigned long long *__restrict__ chunk_off);
+
+// statistics
+__global__ void k_count_nonzero(const void *__restrict__ x, int dtype, uint64_t n,
+                                unsigned long long *__restrict__ out);
+__global__ void k_pairwise_partials(const void *__restrict__ x, int dtype, uint64_t n, int depth,
+                                    double *__restrict__ partial);
+__global__ void k_pairwise_finish(const double *__restrict__ partial, int dtype, uint64_t n,
+                                  int depth, double *__restrict__ out);
+__global__ void k_sample_max(const void *__restrict__ g, int dtype, uint64_t N, uint64_t per,
+                             unsigned long long *__restrict__ bits);
+__global__ void k_lbar_finish(const unsigned long long *__restrict__ bits, int dtype, uint64_t N,
+                              void *__restrict__ per_sample_max, double *__restrict__ out);
+
+}  // namespace actc
