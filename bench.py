@@ -1,0 +1,462 @@
+"""Benchmark: activation compress+decompress on B200 (contract in the task spec).
+
+Workload (default `alexnet256`, BASELINE.json configs[1]): the five conv/ReLU
+activations of torchvision AlexNet at batch 256 on synthetic 224x224 data
+(random init), each with the ADAPTIVE error bound the controller derives from
+live statistics (R, L_bar, M_avg after two SGD-momentum steps; reference
+controller.py:196-232 / errorprop.py:104-124).  One step = compress +
+decompress of the whole activation set (124.2 M fp32 elements, 497 MB).
+
+Other workloads: `c1` (SURVEY config 1: relu-normal [32,64,56,56] at
+relative eb 1e-2) and `sweep:<MB>:<rel>`.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload W]
+
+Rank 0 prints one JSON line.  `value` = whole-job GB/s of fp32 activations
+(4n bytes per step) through compress+decompress with inputs resident in HBM;
+`e2e` = the same through host buffers (pinned H2D + D2H in the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "activation compress+decompress GB/s/GPU vs HBM peak; compression ratio; images/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+
+def alexnet_activations(batch=256, seed=0, device="cuda"):
+    """Post-ReLU outputs of AlexNet's five convs + adaptive eb per layer."""
+    import torch
+    import torchvision
+
+    from paper_2111_09562_b200 import controller as ctl
+    from paper_2111_09562_b200 import tensor as pt
+
+    torch.manual_seed(seed)
+    m = torchvision.models.alexnet(num_classes=1000).to(device)
+    for mod in m.modules():
+        if isinstance(mod, torch.nn.ReLU):
+            mod.inplace = False
+    opt = torch.optim.SGD(m.parameters(), lr=0.01, momentum=0.9)
+    convs = [m.features[i] for i in (0, 3, 6, 8, 10)]
+    relus = [m.features[i] for i in (1, 4, 7, 9, 11)]
+    consumers = [m.features[3], m.features[6], m.features[8], m.features[10], m.classifier[1]]
+    acts, grads = {}, {}
+    hooks = []
+    for i, r in enumerate(relus):
+        hooks.append(r.register_forward_hook(lambda mod, inp, out, i=i: acts.__setitem__(i, out.detach())))
+    for i, c in enumerate(consumers):
+        hooks.append(c.register_full_backward_hook(lambda mod, gi, go, i=i: grads.__setitem__(i, go[0].detach())))
+    g = torch.Generator(device=device).manual_seed(seed)
+    for _ in range(2):
+        x = torch.randn(batch, 3, 224, 224, device=device, generator=g)
+        y = torch.randint(0, 1000, (batch,), device=device, generator=g)
+        loss = torch.nn.functional.cross_entropy(m(x), y)
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        opt.step()
+    for h in hooks:
+        h.remove()
+    stats = []
+    layers = []
+    for i in range(5):
+        a = acts[i].contiguous()
+        R = pt.count_nonzero(a) / a.numel()
+        # per-sample (un-averaged) loss gradient: mean-reduced CE scales by 1/B (training.py:303)
+        _, L_bar = pt.per_sample_max(grads[i] * batch)
+        M_avg = pt.mean_abs(opt.state[consumers[i].weight]["momentum_buffer"])
+        stats.append(ctl.LayerTrainingStats(layer_id=f"conv{i + 1}", R=R, L_bar=L_bar, M_avg=M_avg, N=batch))
+        layers.append(a)
+    plan = ctl.plan_compression(stats, ctl.ControllerConfig(), interval_index=1)
+    ebs = [plan.eb[f"conv{i + 1}"] for i in range(5)]
+    info = [dict(layer=s.layer_id, shape=list(layers[i].shape), R=s.R, L_bar=s.L_bar, M_avg=s.M_avg, eb=ebs[i])
+            for i, s in enumerate(stats)]
+    del m, opt, acts, grads
+    torch.cuda.empty_cache()
+    return layers, ebs, info
+
+
+def relu_normal_tensor(shape, seed, device="cuda"):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    return torch.randn(*shape, device=device, generator=g).clamp_min_(0).contiguous()
+
+
+def build_workload(name, device="cuda"):
+    """Returns (tensors, ebs, info dict, batch)."""
+    import torch
+
+    if name == "alexnet256":
+        layers, ebs, info = alexnet_activations(256, 0, device)
+        return layers, ebs, {"workload": "alexnet_b256_conv_relu_activations", "layers": info,
+                             "eb_mode": "adaptive (controller on live R, L_bar, M_avg after 2 SGD steps)"}, 256
+    if name == "c1":
+        x = np.maximum(np.random.default_rng(0).normal(0, 1, 32 * 64 * 56 * 56), 0).astype(np.float32)
+        eb = 1e-2 * float(x.max() - x.min())
+        t = torch.from_numpy(x.reshape(32, 64, 56, 56)).to(device)
+        return [t], [eb], {"workload": "c1_relu_normal_32x64x56x56", "eb_mode": "rel 1e-2 of range", "eb": eb}, 32
+    if name.startswith("sweep:"):
+        _, mb, rel = name.split(":")
+        n = int(float(mb) * (1 << 20)) // 4
+        t = relu_normal_tensor((n,), 1234, device)
+        eb = float(rel) * float((t.max() - t.min()).item())
+        return [t], [eb], {"workload": f"sweep_{mb}MB_rel{rel}", "eb_mode": f"rel {rel} of range", "eb": eb}, 1
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (the oracle port: the reference itself is Python and
+# does not travel to the GPU box)
+# ---------------------------------------------------------------------------
+
+
+def cpu_roundtrip(tasks, threads):
+    """Run oracle compress+decompress on (array, eb) tasks with a thread pool
+    (ctypes releases the GIL).  Returns (bytes processed, wall seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as orc
+
+    orc.build()
+
+    def one(task):
+        x, eb = task
+        c = orc.compress(x, eb, debug=False)
+        orc.decompress_blob(c.blob, x.size)
+        return x.nbytes
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        total = sum(ex.map(one, tasks))
+    return total, time.perf_counter() - t0
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_tasks_for(tensors, ebs, max_elems=None):
+    tasks = []
+    for t, eb in zip(tensors, ebs):
+        a = t.detach().reshape(-1).cpu().numpy()
+        if max_elems:
+            a = a[:max_elems]
+        tasks.append((np.ascontiguousarray(a), float(eb)))
+    return tasks
+
+
+def run_reference(args, rank, world):
+    """`--impl reference`: the reference algorithm (oracle port) on host cores."""
+    import torch
+
+    if rank != 0:
+        return None
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    tensors, ebs, info, batch = build_workload(args.workload, dev)
+    tasks = cpu_tasks_for(tensors, ebs)
+    in_bytes = sum(x.nbytes for x, _ in tasks)
+    threads = host_threads()
+    # every step = the whole workload; all steps' tensors are independent, so
+    # they run concurrently across the host threads (per-tensor parallelism)
+    for _ in range(args.warmup):
+        cpu_roundtrip(tasks[-1:], 1)
+    total, wall = cpu_roundtrip(tasks * args.steps, threads)
+    gbs = total / wall / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": info,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} x full workload ({in_bytes / 1e6:.1f} MB fp32 per step), "
+                                   "oracle/actc_oracle.c (C restatement of actcomp codec.py/huffman.py), "
+                                   "one tensor per thread"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_gpu(args, rank, world):
+    import torch
+
+    import paper_2111_09562_b200 as pb
+    from paper_2111_09562_b200 import _lib
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tensors, ebs, info, batch = build_workload(args.workload, dev)
+    params = [pb.CodecParams(eb=eb) for eb in ebs]
+    n_total = sum(t.numel() for t in tensors)
+    in_bytes = 4 * n_total
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    outs = [torch.empty_like(t) for t in tensors]
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(record=None):
+        comp = []
+        for i, (t, p) in enumerate(zip(tensors, params)):
+            e0, e1, e2 = ev(), ev(), ev()
+            e0.record(stream)
+            c, rep = pb.compress_device(t, p)  # K1+K2 | sync | K3
+            e1.record(stream)
+            pb.decompress_device(c, out=outs[i], check=False)  # LUT + K4
+            e2.record(stream)
+            comp.append((c, rep, e0, e1, e2))
+        if record is not None:
+            record.append(comp)
+        return comp
+
+    # warm-up + correctness gate: device reconstruction must honour the bound
+    for _ in range(args.warmup):
+        comp = step()
+    torch.cuda.synchronize()
+    for (c, rep, *_), t, o, eb in zip(comp, tensors, outs, ebs):
+        # fp32 output = fp32(reference fp64 recon): tolerance eb + ulp(x_hat)/2
+        half_ulp = (torch.nextafter(o.abs(), torch.full_like(o, float("inf"))) - o.abs()).double() / 2
+        err = (t.double() - o.double()).abs()
+        ok = (err <= eb + half_ulp) | ((o == 0) & (t.abs().double() <= 2 * eb))
+        assert bool(ok.all()), f"bound violated: {int((~ok).sum())} elements"
+
+    # timed region: per-step events, L2 flushed between steps (untimed)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    step_ms, phase = [], {"compress": 0.0, "decompress": 0.0}
+    ratios = None
+    with ClockSampler(dev.index if os.environ.get("CUDA_VISIBLE_DEVICES") is None else 0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            s0, s1 = ev(), ev()
+            s0.record(stream)
+            rec = []
+            step(rec)
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            for c, rep, e0, e1, e2 in rec[0]:
+                phase["compress"] += e0.elapsed_time(e1)
+                phase["decompress"] += e1.elapsed_time(e2)
+            ratios = [r.ratio for _, r, *_ in rec[0]]
+            comp_bytes = [r.compressed_bytes for _, r, *_ in rec[0]]
+    torch.cuda.synchronize()
+    total_ms = sum(step_ms)
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    gbs = world * in_bytes * args.steps / (total_ms * 1e-3) / 1e9
+
+    # roofline of the dominant phase (its launch is essentially one kernel:
+    # K4 for decompress; K1 for compress' first half)
+    C = sum(comp_bytes)
+    dom = max(phase, key=phase.get)
+    per_launch_ms = phase[dom] / (args.steps * len(tensors))
+    if dom == "decompress":
+        alg = C + 4 * n_total  # read bitstream, write fp32 (K4 algorithmic bytes)
+        kname = "k4_decode (+k_build_lut)"
+    else:
+        alg = 4 * n_total + C  # read fp32, write CMTZ-equivalent bytes
+        kname = "k1_quant_lorenzo_hist + k2_codebook + k3_encode"
+    achieved = alg / len(tensors) / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh).get(args.workload, {})
+        traffic = tr.get(dom)
+    except Exception:
+        pass
+
+    # end-to-end through host buffers (pinned H2D of inputs, D2H of outputs)
+    host_in = [t.cpu().pin_memory() for t in tensors]
+    host_out = [torch.empty(t.shape, dtype=torch.float32).pin_memory() for t in tensors]
+    dev_in = [torch.empty_like(t) for t in tensors]
+
+    def e2e_step():
+        for hi, di, ho, p, o in zip(host_in, dev_in, host_out, params, outs):
+            di.copy_(hi, non_blocking=True)
+            c, _ = pb.compress_device(di, p)
+            pb.decompress_device(c, out=o, check=False)
+            ho.copy_(o, non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        s0, s1 = ev(), ev()
+        s0.record(stream)
+        e2e_step()
+        s1.record(stream)
+        s1.synchronize()
+        e2e_ms += s0.elapsed_time(s1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_gbs = world * in_bytes * args.steps / (e2e_ms * 1e-3) / 1e9
+
+    line = None
+    if rank == 0:
+        ratio_total = in_bytes / C
+        cfg = dict(info)
+        cfg.update({"parallelism": f"dp{world} (independent shards, no data-path collective)",
+                    "global_batch": batch * world, "l2": "flushed (256 MB memset) between timed steps",
+                    "per_layer_ratio": ratios, "compression_ratio": ratio_total,
+                    "bytes_in_per_step_per_gpu": in_bytes, "compressed_bytes_per_step_per_gpu": C,
+                    "phase_ms_per_step": {k: v / args.steps for k, v in phase.items()}})
+        line = {
+            "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (AlexNet random init, randn images)"
+            if args.workload == "alexnet256" else "synthetic", "config": cfg,
+            "compression_ratio": ratio_total, "images_per_s": world * batch / (ms_per_step * 1e-3),
+            "roofline_fraction_round_trip": (world * (8 * n_total + 2 * C) / (ms_per_step * 1e-3) / 1e9) / peak,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": alg / len(tensors)},
+            "e2e": {"value": e2e_gbs, "unit": "GB/s", "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": in_bytes},
+            "gpu_launches": args.steps * len(tensors) * 5,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu:
+            tasks = cpu_tasks_for(tensors, ebs)
+            threads = min(host_threads(), len(tasks))
+            nbytes, wall = cpu_roundtrip(tasks, threads)
+            line["cpu_baseline"] = {"value": nbytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+                                    "sample": f"one full step ({nbytes / 1e6:.1f} MB fp32) through oracle/actc_oracle.c, "
+                                              "one tensor per thread"}
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="alexnet256")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    try:
+        if args.impl == "reference":
+            line = run_reference(args, rank, world)
+        else:
+            line = run_gpu(args, rank, world)
+        if rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -158,3 +158,20 @@ def test_corrupt_payload_is_format_error():
         except FormatError:
             hits += 1
     assert hits >= 1
+
+
+@pytest.mark.parametrize("eb", [1.2e-6, 6.3e-6, 3.7e-5])
+def test_small_eb_outlier_heavy_vs_oracle(oracle, eb):
+    """the adaptive bounds of AlexNet's deeper layers at init: deltas exceed
+    the radius, so a large share of elements are outliers"""
+    rng = np.random.default_rng(int(eb * 1e9))
+    x = (np.maximum(rng.normal(0, 0.05, (16, 256, 13, 13)), 0)).astype(np.float32)
+    ref = oracle.compress(x, eb, debug=False)
+    c, rep = pb.compress(pb.Tensor(x), pb.CodecParams(eb=eb))
+    assert c.to_bytes() == ref.blob
+    assert rep.ratio == ref.ratio
+    want = oracle.decompress_blob(ref.blob, x.size)
+    out, nz = pb.decompress_device(c, dtype=torch.float64)
+    assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+    out32, _ = pb.decompress_device(c, dtype=torch.float32)
+    assert np.array_equal(out32.cpu().numpy().reshape(-1), want.astype(np.float32))
