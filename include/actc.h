@@ -59,6 +59,8 @@ typedef struct {
   double entropy_bits;    /* stream_entropy_bits(hist) (huffman.py:239-246) */
   uint32_t status;        /* ACTC_OK or ACTC_EPARAM (code length > 63) */
   uint32_t sym_bytes;     /* 2 (u16 symbols, radius <= 2^15) or 4 */
+  uint32_t sym_lo;        /* smallest / largest live symbol */
+  uint32_t sym_hi;
 } actc_plan_t;
 
 /* A compressed stream as the decoder sees it (all arrays on the device).

@@ -32,6 +32,8 @@ class Plan(C.Structure):
         ("entropy_bits", C.c_double),
         ("status", C.c_uint32),
         ("sym_bytes", C.c_uint32),
+        ("sym_lo", C.c_uint32),
+        ("sym_hi", C.c_uint32),
     ]
 
 

@@ -92,7 +92,7 @@ namespace {
 
 // codebook scratch carve-up for alphabet A
 struct CbLayout {
-  size_t live_sym, live_freq, keys, vals, nf, lpar, npar, S, llen, ndepth, total;
+  size_t live_sym, live_freq, keys, keys2, vals, vals2, nf, lpar, npar, llen, ndepth, total;
 };
 CbLayout cb_layout(uint64_t A) {
   CbLayout l;
@@ -103,21 +103,23 @@ CbLayout cb_layout(uint64_t A) {
     o += (bytes + 255) & ~size_t(255);
     return r;
   };
+  (void)P;
   l.live_sym = take(4 * A);
   l.live_freq = take(8 * A);
-  l.keys = take(8 * P);
-  l.vals = take(4 * P);
+  l.keys = take(8 * A);
+  l.keys2 = take(8 * A);
+  l.vals = take(4 * A);
+  l.vals2 = take(4 * A);
   l.nf = take(8 * A);
   l.lpar = take(4 * A);
   l.npar = take(4 * A);
-  l.S = take(8 * A);
   l.llen = take(A);
   l.ndepth = take(4 * A);
   l.total = o;
   return l;
 }
 
-constexpr size_t kK2Smem = 4096 * (8 + 8 + 4 + 4 + 4 + 8 + 4 + 1) + 64;
+constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
 int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const uint16_t *in_lengths,
                  uint16_t *out_lengths, const unsigned long long *n_out, uint64_t n_symbols,
@@ -143,11 +145,12 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   a.live_sym = (uint32_t *)(b + l.live_sym);
   a.live_freq = (unsigned long long *)(b + l.live_freq);
   a.keys = (unsigned long long *)(b + l.keys);
+  a.keys2 = (unsigned long long *)(b + l.keys2);
   a.vals = (uint32_t *)(b + l.vals);
+  a.vals2 = (uint32_t *)(b + l.vals2);
   a.nf = (unsigned long long *)(b + l.nf);
   a.lpar = (uint32_t *)(b + l.lpar);
   a.npar = (uint32_t *)(b + l.npar);
-  a.S = (uint32_t *)(b + l.S);
   a.llen = (uint8_t *)(b + l.llen);
   a.ndepth = (uint8_t *)(b + l.ndepth);
   a.n_symbols = n_symbols;
@@ -180,7 +183,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
     return set_err(ACTC_ENOMEM, "ctx alloc failed");
   }
   int rc;
-  if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, 4 * kLutSize))) {
+  if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, 4 * kLutWords))) {
     delete c;
     return rc;
   }
@@ -190,11 +193,15 @@ int actc_ctx_create(int device, actc_ctx **out) {
   size_t k1smem = K1_WIN * 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, k1smem);
   c->k1_blocks = std::max(1, nb) * c->num_sms;
-  size_t k3smem = K3_WIN * 8 + ((size_t)K3_TILE * 56 / 32 + 4) * 4;
-  CK(cudaFuncSetAttribute(k3_encode<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3smem));
-  CK(cudaFuncSetAttribute(k3_encode<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k3_encode<uint16_t>, K3_THREADS, k3smem);
-  c->k3_blocks = std::max(1, nb) * c->num_sms;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const void *k3s[4] = {(const void *)k3_encode<uint16_t, false>, (const void *)k3_encode<uint16_t, true>,
+                        (const void *)k3_encode<uint32_t, false>, (const void *)k3_encode<uint32_t, true>};
+  for (const void *f : k3s) {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, f));
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+  }
   size_t s16 = (size_t)K4_THREADS * (ACTC_CHUNK / 2 + 1) * 4, s32 = (size_t)K4_THREADS * (ACTC_CHUNK + 1) * 4;
   CK(cudaFuncSetAttribute(k4_decode<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
   CK(cudaFuncSetAttribute(k4_decode<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
@@ -266,15 +273,13 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
   c->A = A;
   c->radius = radius;
   c->sym_bytes = sb;
-  c->win_n = (uint32_t)std::min<uint64_t>(A, K3_WIN);
-  c->win_lo = A <= K3_WIN ? 0 : radius - K3_WIN / 2;
   c->mode = 1;
   return ACTC_OK;
 }
 
 static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, const float *x,
-                         uint8_t *payload, uint64_t *out_idx, float *out_val, uint64_t *chunk_off,
-                         int extract, cudaStream_t s) {
+                         const actc_plan_t *plan, uint8_t *payload, uint64_t *out_idx, float *out_val,
+                         uint64_t *chunk_off, int extract, cudaStream_t s) {
   uint64_t ntiles = cdiv(n, K3_TILE);
   int rc;
   // status: flag u32 | agg_bits | agg_nz | inc_bits | inc_nz (u64) | tail u32
@@ -292,18 +297,41 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
   CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
   unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
   CK(cudaMemsetAsync(ticket, 0, 8, s));
-  size_t smem = (size_t)c->win_n * 8 + ((size_t)K3_TILE * 56 / 32 + 4) * 4;
-  int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)c->k3_blocks);
+  // code-table window: the live symbol range, capped
+  const bool wide = plan->max_len > (uint32_t)K3_SHORT_MAXLEN;
+  const uint32_t cap = wide ? K3_WIN64 : K3_WIN32;
+  uint32_t lo = plan->sym_lo, hi = plan->sym_hi;
+  uint32_t span = hi >= lo ? hi - lo + 1 : 1;
+  uint32_t win_lo = lo, win_n = span;
+  if (span > cap) {
+    // centre the window on the radius (symbol of a zero delta), clamp to the live range
+    uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
+    uint32_t wl = centre > cap / 2 ? centre - cap / 2 : 0;
+    if (wl < lo) wl = lo;
+    if (wl + cap > hi + 1) wl = hi + 1 - cap;
+    win_lo = wl;
+    win_n = cap;
+  }
+  const uint32_t maxlen = plan->max_len ? plan->max_len : 1;
+  const uint32_t word_cap = (uint32_t)(((uint64_t)K3_TILE * maxlen + 31) / 32 + 4);
+  const size_t smem = (((size_t)win_n * (wide ? 8 : 4) + 15) & ~size_t(15)) + (size_t)word_cap * 4;
+  int occ = 0;
   if (sb == 2)
-    k3_encode<uint16_t><<<grid, K3_THREADS, smem, s>>>(
-        (const uint16_t *)sym, n, (const unsigned long long *)c->ctab.p, c->win_lo, c->win_n, x,
-        (uint32_t *)payload, (unsigned long long *)out_idx, out_val, (unsigned long long *)chunk_off, st,
-        ticket, ntiles, extract);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide ? (const void *)k3_encode<uint16_t, true> : (const void *)k3_encode<uint16_t, false>, K3_THREADS, smem);
   else
-    k3_encode<uint32_t><<<grid, K3_THREADS, smem, s>>>(
-        (const uint32_t *)sym, n, (const unsigned long long *)c->ctab.p, c->win_lo, c->win_n, x,
-        (uint32_t *)payload, (unsigned long long *)out_idx, out_val, (unsigned long long *)chunk_off, st,
-        ticket, ntiles, extract);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide ? (const void *)k3_encode<uint32_t, true> : (const void *)k3_encode<uint32_t, false>, K3_THREADS, smem);
+  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)std::max(1, occ) * c->num_sms);
+  const unsigned long long *ct = (const unsigned long long *)c->ctab.p;
+#define K3_LAUNCH(T, W)                                                                                   \
+  k3_encode<T, W><<<grid, K3_THREADS, smem, s>>>((const T *)sym, n, ct, win_lo, win_n, word_cap, x,      \
+                                                  (uint32_t *)payload, (unsigned long long *)out_idx, out_val, \
+                                                  (unsigned long long *)chunk_off, st, ticket, ntiles, extract)
+  if (sb == 2) {
+    if (wide) K3_LAUNCH(uint16_t, true); else K3_LAUNCH(uint16_t, false);
+  } else {
+    if (wide) K3_LAUNCH(uint32_t, true); else K3_LAUNCH(uint32_t, false);
+  }
+#undef K3_LAUNCH
   CKL();
   return ACTC_OK;
 }
@@ -314,7 +342,7 @@ int actc_compress_encode(actc_ctx *c, const float *x, const actc_plan_t *plan, u
   cudaStream_t s = (cudaStream_t)stream;
   if (c->mode != 1 || plan->n != c->n) return set_err(ACTC_EPARAM, "actc_compress_encode without a matching plan");
   if (plan->status != ACTC_OK) return set_err(plan->status, "Huffman code length exceeds 63 bits");
-  int rc = launch_encode(c, c->sym.p, c->sym_bytes, c->n, x, payload, out_idx, out_val, chunk_off, 1, s);
+  int rc = launch_encode(c, c->sym.p, c->sym_bytes, c->n, x, plan, payload, out_idx, out_val, chunk_off, 1, s);
   if (rc) return rc;
   if (plan->live_symbols)
     CK(cudaMemcpyAsync(canon, c->canon.p, 4ull * plan->live_symbols, cudaMemcpyDeviceToDevice, s));
@@ -520,8 +548,6 @@ int actc_huffman_plan(actc_ctx *c, const uint32_t *sym, uint64_t n, uint64_t A, 
   c->A = A;
   c->radius = 0;
   c->sym_bytes = 4;
-  c->win_n = (uint32_t)std::min<uint64_t>(A, K3_WIN);
-  c->win_lo = 0;
   c->mode = 2;
   return ACTC_OK;
 }
@@ -532,7 +558,7 @@ int actc_huffman_encode(actc_ctx *c, const uint32_t *sym, const actc_plan_t *pla
   if (c->mode != 2 || plan->n != c->n) return set_err(ACTC_EPARAM, "actc_huffman_encode without a matching plan");
   if (plan->status != ACTC_OK) return set_err(plan->status, "Huffman code length exceeds 63 bits");
   if (c->n) {
-    int rc = launch_encode(c, sym, 4, c->n, nullptr, payload, nullptr, nullptr, chunk_off, 0, s);
+    int rc = launch_encode(c, sym, 4, c->n, nullptr, plan, payload, nullptr, nullptr, chunk_off, 0, s);
     if (rc) return rc;
   }
   if (plan->live_symbols)

@@ -1,4 +1,4 @@
-// K2: Huffman codebook on one CTA.
+// K2: Huffman codebook on one CTA (1024 threads).
 //
 // Replaces build_code_lengths (huffman.py:37-75), canonical_codes
 // (huffman.py:78-94), the RLE record count of _rle_encode_lengths
@@ -6,94 +6,158 @@
 //
 // Bit-exactness.  heapq pops items in (freq, tiebreak) order with leaf
 // tiebreak = symbol and internal tiebreak = creation counter >= alphabet,
-// i.e. the classic two-queue algorithm where a leaf wins a frequency tie
-// and older internal nodes beat newer ones.  We run that algorithm in
+// i.e. the two-queue algorithm in which a leaf wins a frequency tie and an
+// older internal node beats a newer one.  We run that algorithm in
 // *phases*: with m the smallest remaining frequency, every item of
 // frequency < 2m is popped in merged (freq, class, index) order and paired
 // consecutively before any node created in the phase can be popped (new
 // nodes are >= 2m); an odd leftover pairs with the smallest remaining item.
 // Each phase at least doubles m, so there are <= log2(n)+1 phases, each a
-// parallel merge.  Code lengths are depths (max(1, depth)), computed by
-// walking the phases backwards.
+// merge-path parallel merge.  Code lengths are depths, computed by walking
+// the phases backwards.
+//
+// Sorting uses a stable block-wide LSD radix sort (8-bit digits, warp
+// match_any ranking), so (freq, symbol) order comes from stability.  Arrays
+// live in shared memory when the live alphabet is small, else in global
+// scratch (L2-resident).
 #include "kernels.cuh"
 
 namespace actc {
 
 namespace {
 
-// Bitonic sort of (key, val) pairs, lexicographic, in place; P is a power
-// of two, all threads of the CTA participate.
-__device__ __forceinline__ void bitonic_sort(unsigned long long *keys, uint32_t *vals, uint32_t P) {
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t p = threadIdx.x; p < P / 2; p += blockDim.x) {
-        uint32_t i = (p / j) * 2 * j + (p % j);
-        uint32_t ixj = i + j;
-        unsigned long long x = keys[i], y = keys[ixj];
-        uint32_t xv = vals[i], yv = vals[ixj];
-        bool gt = x > y || (x == y && xv > yv);
-        bool up = (i & k) == 0;
-        if (gt == up) {
-          keys[i] = y; keys[ixj] = x;
-          vals[i] = yv; vals[ixj] = xv;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// number of elements in sorted v[0..len) strictly below t
-__device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long *v, uint32_t len,
-                                                    unsigned long long t) {
-  uint32_t lo = 0, hi = len;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (v[mid] < t)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-// number of elements in sorted v[0..len) <= t
-__device__ __forceinline__ uint32_t upper_bound_u64(const unsigned long long *v, uint32_t len,
-                                                    unsigned long long t) {
-  uint32_t lo = 0, hi = len;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (v[mid] <= t)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-constexpr uint32_t kIntBit = 0x80000000u;
+constexpr int NWARP = K2_THREADS / 32;
 constexpr uint32_t kSmemL = 4096;
 constexpr int kMaxPhases = 128;
+
+struct RadixSmem {
+  uint32_t hist[NWARP][257];
+  uint32_t tot[256];
+};
+
+// One stable LSD pass on digit (key >> shift) & 0xFF, src -> dst.
+__device__ void radix_pass(const unsigned long long *__restrict__ sk, const uint32_t *__restrict__ sv,
+                           unsigned long long *__restrict__ dk, uint32_t *__restrict__ dv, uint32_t L,
+                           int shift, RadixSmem &rs) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t seg = ((L + NWARP - 1) / NWARP + 31) & ~31u;
+  const uint32_t b0 = min(L, w * seg), b1 = min(L, b0 + seg);
+  for (int d = lane; d < 257; d += 32) rs.hist[w][d] = 0;
+  __syncwarp();
+  for (uint32_t base = b0; base < b1; base += 32) {
+    uint32_t i = base + lane;
+    uint32_t d = i < b1 ? (uint32_t)((sk[i] >> shift) & 0xFF) : 256u;
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (lane == __ffs(peers) - 1) rs.hist[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps, totals
+  if (threadIdx.x < 256) {
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+    for (int ww = 0; ww < NWARP; ww++) {
+      uint32_t c = rs.hist[ww][d];
+      rs.hist[ww][d] = run;
+      run += c;
+    }
+    rs.tot[d] = run;
+  }
+  __syncthreads();
+  if (w == 0) {
+    // exclusive scan of 256 digit totals (8 per lane)
+    uint32_t v[8], s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      v[k] = rs.tot[lane * 8 + k];
+      s += v[k];
+    }
+    uint32_t inc = warp_incl_sum(s);
+    uint32_t run = inc - s;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      rs.tot[lane * 8 + k] = run;
+      run += v[k];
+    }
+  }
+  __syncthreads();
+  for (int d = lane; d < 256; d += 32) rs.hist[w][d] += rs.tot[d];
+  __syncwarp();
+  for (uint32_t base = b0; base < b1; base += 32) {
+    uint32_t i = base + lane;
+    unsigned long long k = 0;
+    uint32_t v = 0, d = 256u;
+    if (i < b1) {
+      k = sk[i];
+      v = sv[i];
+      d = (uint32_t)((k >> shift) & 0xFF);
+    }
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned lower = peers & ((1u << lane) - 1u);
+    if (d < 256) {
+      uint32_t pos = rs.hist[w][d] + __popc(lower);
+      dk[pos] = k;
+      dv[pos] = v;
+    }
+    __syncwarp();
+    if (d < 256 && lane == __ffs(peers) - 1) rs.hist[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// first index in sorted v[lo, hi) with v[i] >= T (block-wide, all threads
+// get the result).  1024-way probing, repeated on the bracketing interval.
+__device__ uint32_t block_lower_bound(const unsigned long long *v, uint32_t lo, uint32_t hi,
+                                      unsigned long long T) {
+  while (hi > lo) {
+    uint32_t len = hi - lo;
+    uint32_t step = (len + K2_THREADS - 1) / K2_THREADS;
+    uint32_t idx = lo + threadIdx.x * step;
+    bool below = idx < hi && v[idx] < T;
+    uint32_t k = (uint32_t)__syncthreads_count(below);  // probes < T form a prefix
+    if (step == 1) return lo + k;
+    if (k == 0) return lo;
+    uint32_t nlo = lo + (k - 1) * step + 1;  // probe k-1 is < T
+    uint32_t nhi = min(hi, lo + k * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
 
 }  // namespace
 
 __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ RadixSmem rs;
   __shared__ unsigned long long wbuf[33];
   __shared__ unsigned long long wbuf2[33];
-  __shared__ uint32_t s_lp, s_np, s_nn, s_a, s_b, s_nph;
+  __shared__ uint32_t s_lp, s_np, s_nn, s_nph;
   __shared__ uint32_t ph_begin[kMaxPhases], ph_pairs[kMaxPhases];
   __shared__ uint8_t ph_odd[kMaxPhases];
   __shared__ uint32_t s_cnt[64];
   __shared__ unsigned long long s_first[64];
   __shared__ uint32_t s_base[64];
   __shared__ unsigned s_err, s_maxlen;
+  __shared__ unsigned long long s_maxf;
+  __shared__ uint32_t s_odd_item;
   __shared__ double dbuf[33];
 
   const int tid = threadIdx.x;
   const uint64_t A = a.A;
 
+  if (tid == 0) {
+    s_err = 0;
+    s_maxlen = 0;
+    s_maxf = 0;
+  }
+  if (tid < 64) s_cnt[tid] = 0;
+  __syncthreads();
+
   // ---- 1. compact live symbols (symbol order) ----
   uint64_t L = 0;
+  unsigned long long maxf = 0;
   for (uint64_t c = 0; c < A; c += (uint64_t)K2_THREADS * 8) {
     uint64_t b0 = c + (uint64_t)tid * 8;
     unsigned long long f[8];
@@ -105,6 +169,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       if (s < A) v = a.in_lengths ? (unsigned long long)a.in_lengths[s] : a.hist[s];
       f[j] = v;
       cnt += v != 0;
+      maxf = v > maxf ? v : maxf;
     }
     unsigned long long tot;
     unsigned long long off = block_excl_sum<unsigned long long>(cnt, wbuf, &tot);
@@ -118,38 +183,29 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     }
     L += tot;
   }
+  atomicMax(&s_maxf, maxf);
   __syncthreads();
-
-  if (tid == 0) {
-    s_err = 0;
-    s_maxlen = 0;
-  }
-  if (tid < 64) s_cnt[tid] = 0;
+  maxf = s_maxf;
 
   // generic pointers: shared memory for small L, global scratch otherwise
-  uint32_t P = 1;
-  while (P < L) P <<= 1;
-  unsigned long long *keys = a.keys;
-  uint32_t *vals = a.vals;
-  unsigned long long *nf = a.nf;
-  uint32_t *lpar = a.lpar, *npar = a.npar, *S = a.S;
+  unsigned long long *k0 = a.keys, *k1 = a.keys2, *nf = a.nf;
+  uint32_t *v0 = a.vals, *v1 = a.vals2, *lpar = a.lpar, *npar = a.npar;
   uint32_t *ndepth = (uint32_t *)a.ndepth;
   uint8_t *llen = a.llen;
   if (L <= kSmemL) {
     unsigned char *p = smem;
-    keys = (unsigned long long *)p; p += 8 * (size_t)kSmemL;
+    k0 = (unsigned long long *)p; p += 8 * (size_t)kSmemL;
+    k1 = (unsigned long long *)p; p += 8 * (size_t)kSmemL;
     nf = (unsigned long long *)p; p += 8 * (size_t)kSmemL;
-    vals = (uint32_t *)p; p += 4 * (size_t)kSmemL;
+    v0 = (uint32_t *)p; p += 4 * (size_t)kSmemL;
+    v1 = (uint32_t *)p; p += 4 * (size_t)kSmemL;
     lpar = (uint32_t *)p; p += 4 * (size_t)kSmemL;
     npar = (uint32_t *)p; p += 4 * (size_t)kSmemL;
-    S = (uint32_t *)p; p += 8 * (size_t)kSmemL;
     ndepth = (uint32_t *)p; p += 4 * (size_t)kSmemL;
     llen = (uint8_t *)p;
   }
-  __syncthreads();
 
   if (a.in_lengths) {
-    // lengths given (codebook_from_lengths): clamp display, check range
     for (uint32_t j = tid; j < L; j += K2_THREADS) {
       unsigned l = (unsigned)a.live_freq[j];
       if (l > ACTC_MAX_CODE_LENGTH) atomicOr(&s_err, 1u);
@@ -158,14 +214,21 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   } else if (L == 1) {
     if (tid == 0) llen[0] = 1;  // huffman.py:50-52
   } else if (L > 1) {
-    // ---- 2. sort leaves by (freq, symbol) ----
-    for (uint32_t i = tid; i < P; i += K2_THREADS) {
-      keys[i] = i < L ? a.live_freq[i] : ~0ull;
-      vals[i] = i < L ? i : 0xFFFFFFFFu;
+    // ---- 2. sort leaves by (freq, symbol): stable radix on freq ----
+    for (uint32_t i = tid; i < L; i += K2_THREADS) {
+      k0[i] = a.live_freq[i];
+      v0[i] = i;
     }
     __syncthreads();
-    bitonic_sort(keys, vals, P);
-    // leaf i: freq = keys[i], live index = vals[i]
+    int passes = 0;
+    while (passes < 8 && (maxf >> (8 * passes)) != 0) passes++;
+    for (int p = 0; p < passes; p++) {
+      radix_pass(k0, v0, k1, v1, (uint32_t)L, 8 * p, rs);
+      unsigned long long *tk = k0; k0 = k1; k1 = tk;
+      uint32_t *tv = v0; v0 = v1; v1 = tv;
+    }
+    // sorted leaf i: freq k0[i], live index v0[i]
+    const unsigned long long *lf = k0;
 
     // ---- 3. phase-parallel two-queue merge ----
     if (tid == 0) {
@@ -174,37 +237,55 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     __syncthreads();
     const unsigned long long INF = ~0ull;
     while (true) {
-      uint32_t lp = s_lp, np = s_np, nn = s_nn;
+      const uint32_t lp = s_lp, np = s_np, nn = s_nn;
       if ((L - lp) + (nn - np) <= 1) break;
-      if (tid == 0) {
-        unsigned long long m = INF;
-        if (lp < L) m = keys[lp];
-        if (np < nn && nf[np] < m) m = nf[np];
-        unsigned long long T = 2 * m;
-        s_a = lower_bound_u64(keys + lp, (uint32_t)(L - lp), T);
-        s_b = lower_bound_u64(nf + np, nn - np, T);
-      }
-      __syncthreads();
-      const uint32_t na = s_a, nb = s_b;
-      for (uint32_t i = tid; i < na; i += K2_THREADS) {
-        unsigned long long f = keys[lp + i];
-        uint32_t pos = i + lower_bound_u64(nf + np, nb, f);  // internals strictly below
-        S[pos] = lp + i;
-      }
-      for (uint32_t j = tid; j < nb; j += K2_THREADS) {
-        unsigned long long f = nf[np + j];
-        uint32_t pos = j + upper_bound_u64(keys + lp, na, f);  // leaves <= win ties
-        S[pos] = kIntBit | (np + j);
-      }
-      __syncthreads();
+      unsigned long long m = INF;
+      if (lp < L) m = lf[lp];
+      if (np < nn && nf[np] < m) m = nf[np];
+      const unsigned long long T = 2 * m;
+      const uint32_t na = block_lower_bound(lf, lp, (uint32_t)L, T) - lp;
+      const uint32_t nb = block_lower_bound(nf, np, nn, T) - np;
       const uint32_t tot = na + nb, pairs = tot >> 1;
-      for (uint32_t t = tid; t < pairs; t += K2_THREADS) {
-        uint32_t x = S[2 * t], y = S[2 * t + 1];
-        unsigned long long fx = (x & kIntBit) ? nf[x & ~kIntBit] : keys[x];
-        unsigned long long fy = (y & kIntBit) ? nf[y & ~kIntBit] : keys[y];
-        nf[nn + t] = fx + fy;
-        if (x & kIntBit) npar[x & ~kIntBit] = nn + t; else lpar[x] = nn + t;
-        if (y & kIntBit) npar[y & ~kIntBit] = nn + t; else lpar[y] = nn + t;
+      // merge path: thread t owns merged positions [t*q, t*q+q), q even
+      uint32_t q = (tot + K2_THREADS - 1) / K2_THREADS;
+      q = (q + 1) & ~1u;
+      const uint32_t d0 = tid * q;
+      if (d0 < tot) {
+        // number of leaves among the first d0 merged items (leaf wins ties)
+        uint32_t lo = d0 > nb ? d0 - nb : 0, hi = min(d0, na);
+        while (lo < hi) {
+          uint32_t mid = (lo + hi + 1) >> 1;
+          uint32_t j = d0 - mid;
+          if (j >= nb || lf[lp + mid - 1] <= nf[np + j])
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        uint32_t i = lo, j = d0 - lo;
+        const uint32_t d1 = min(tot, d0 + q);
+        unsigned long long fprev = 0;
+        for (uint32_t p = d0; p < d1; p++) {
+          bool leaf = j >= nb || (i < na && lf[lp + i] <= nf[np + j]);
+          unsigned long long f;
+          uint32_t item;
+          if (leaf) {
+            f = lf[lp + i];
+            item = lp + i;
+            i++;
+          } else {
+            f = nf[np + j];
+            item = 0x80000000u | (np + j);
+            j++;
+          }
+          if (p < 2 * pairs) {
+            const uint32_t node = nn + (p >> 1);
+            if (item & 0x80000000u) npar[item & 0x7FFFFFFFu] = node; else lpar[item] = node;
+            if (p & 1) nf[node] = fprev + f;
+            fprev = f;
+          } else {
+            s_odd_item = item;  // the single leftover (tot odd)
+          }
+        }
       }
       __syncthreads();
       if (tid == 0) {
@@ -214,23 +295,21 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
         ph_odd[ph] = tot & 1;
         uint32_t nlp = lp + na, nnp = np + nb, nnn = nn + pairs;
         if (tot & 1) {
-          uint32_t z = S[tot - 1];
-          unsigned long long fz = (z & kIntBit) ? nf[z & ~kIntBit] : keys[z];
-          // candidates: next leaf, next internal (old or the first new one);
-          // leaf wins ties, and among internals the lower index wins
-          unsigned long long fl = nlp < L ? keys[nlp] : INF;
+          uint32_t z = s_odd_item;
+          unsigned long long fz = (z & 0x80000000u) ? nf[z & 0x7FFFFFFFu] : lf[z];
+          unsigned long long fl = nlp < L ? lf[nlp] : INF;
           unsigned long long fi = nnp < nnn ? nf[nnp] : INF;
           uint32_t y;
           unsigned long long fy;
           if (nlp < L && fl <= fi) {
             y = nlp; fy = fl; nlp++;
           } else {
-            y = kIntBit | nnp; fy = fi; nnp++;
+            y = 0x80000000u | nnp; fy = fi; nnp++;
           }
           uint32_t node = nnn;
           nf[node] = fz + fy;
-          if (z & kIntBit) npar[z & ~kIntBit] = node; else lpar[z] = node;
-          if (y & kIntBit) npar[y & ~kIntBit] = node; else lpar[y] = node;
+          if (z & 0x80000000u) npar[z & 0x7FFFFFFFu] = node; else lpar[z] = node;
+          if (y & 0x80000000u) npar[y & 0x7FFFFFFFu] = node; else lpar[y] = node;
           nnn++;
         }
         s_lp = nlp; s_np = nnp; s_nn = nnn;
@@ -260,21 +339,27 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     for (uint32_t i = tid; i < L; i += K2_THREADS) {
       uint32_t d = ndepth[lpar[i]] + 1;
       if (d > ACTC_MAX_CODE_LENGTH) atomicOr(&s_err, 1u);
-      llen[vals[i]] = (uint8_t)(d > 255 ? 255 : d);
+      llen[v0[i]] = (uint8_t)(d > 255 ? 255 : d);
     }
   }
   __syncthreads();
 
-  // ---- 5. canonical order: sort live symbols by (length, symbol) ----
-  for (uint32_t i = tid; i < P; i += K2_THREADS) {
-    keys[i] = i < L ? (unsigned long long)llen[i] : ~0ull;
-    vals[i] = i < L ? a.live_sym[i] : 0xFFFFFFFFu;
+  // ---- 5. canonical order: stable radix pass on length (input in symbol order) ----
+  for (uint32_t i = tid; i < L; i += K2_THREADS) {
+    k1[i] = (unsigned long long)llen[i];
+    v1[i] = a.live_sym[i];
   }
   __syncthreads();
-  if (L > 1) bitonic_sort(keys, vals, P);
+  unsigned long long *ck = k1;
+  uint32_t *cv = v1;
+  if (L > 1) {
+    radix_pass(k1, v1, k0, v0, (uint32_t)L, 0, rs);
+    ck = k0;
+    cv = v0;
+  }
   unsigned lmax = 0;
   for (uint32_t i = tid; i < L; i += K2_THREADS) {
-    unsigned l = (unsigned)keys[i];
+    unsigned l = (unsigned)ck[i];
     atomicAdd(&s_cnt[l & 63], 1u);
     lmax = max(lmax, l);
   }
@@ -294,7 +379,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   }
   __syncthreads();
   for (uint32_t i = tid; i < L; i += K2_THREADS) {
-    uint32_t l = (uint32_t)keys[i], s = vals[i];
+    uint32_t l = (uint32_t)ck[i], s = cv[i];
     a.canon[i] = s;
     if (a.ctab && l <= 56) a.ctab[s] = ((s_first[l] + (i - s_base[l])) << 8) | l;
   }
@@ -305,7 +390,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     for (uint32_t j = tid; j < L; j += K2_THREADS) a.out_lengths[a.live_sym[j]] = llen[j];
   }
 
-  // ---- 6. plan: payload bits, RLE record count, entropy ----
+  // ---- 6. plan: payload bits, RLE record count, entropy, live range ----
   unsigned long long bits = 0, recs = 0;
   double ent = 0.0;
   const double total = (double)a.n_symbols;
@@ -365,11 +450,13 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     pl->payload_bits = tb;
     pl->rle_runs = tr;
     pl->entropy_bits = L > 1 ? -te : 0.0;
-    if (pl->entropy_bits == -0.0) pl->entropy_bits = 0.0;
+    if (pl->entropy_bits == 0.0) pl->entropy_bits = 0.0;
     pl->status = (s_err & 1u) ? ACTC_EPARAM : ((s_err & 2u) ? ACTC_ECUDA : ACTC_OK);
     if (s_maxlen > 56 && !a.in_lengths) pl->status = ACTC_EPARAM;
     if (a.n_outliers) pl->n_outliers = *a.n_outliers;
     if (a.nonfinite && *a.nonfinite) pl->status = ACTC_EDATA;
+    pl->sym_lo = L ? a.live_sym[0] : 0;
+    pl->sym_hi = L ? a.live_sym[L - 1] : 0;
   }
 }
 

@@ -4,13 +4,15 @@
 // Replaces huffman_encode's bit expansion and np.packbits
 // (huffman.py:188-207) and the outlier gather of compress
 // (codec.py:321-322).  One pass over the symbol stream:
-//   * per thread: 16 symbols -> (code, len) from a shared-memory window of
-//     the code table (global fallback for the tail of the alphabet);
+//   * per thread: 16 symbols -> (code, len) from a shared-memory copy of the
+//     code table covering the live symbol range (u32 entries when every code
+//     fits 26 bits; global fallback outside the window);
 //   * block exclusive scan of (bits, outliers) packed in one u64;
 //   * decoupled look-back across tiles for the global bit offset (u64) and
 //     outlier rank;
-//   * codes OR-ed into a shared word buffer, written back as big-endian
-//     32-bit words (byte order == np.packbits' MSB-first stream).
+//   * codes packed into a shared word buffer (plain stores for words a
+//     thread owns, atomicOr only for the two it shares with neighbours),
+//     written back as big-endian 32-bit words (byte order == np.packbits).
 // The word a tile shares with its successor is not stored by the tile: its
 // bits are published in the look-back record ("tail") and merged by the
 // successor, so no output pre-zeroing and no global atomics are needed and
@@ -21,36 +23,58 @@ namespace actc {
 
 namespace {
 
-__device__ __forceinline__ void append_bits(uint32_t *words, uint32_t &w, unsigned long long &buf,
-                                            int &nb, uint32_t code, int len) {
-  // len <= 32, nb <= 31
-  buf |= (unsigned long long)code << (64 - nb - len);
-  nb += len;
-  if (nb >= 32) {
-    atomicOr(&words[w++], (uint32_t)(buf >> 32));
-    buf <<= 32;
-    nb -= 32;
+struct Packer {
+  uint32_t *words;
+  uint32_t w;        // current word index
+  uint32_t first_w;  // first word this thread touches (shared with predecessor)
+  unsigned long long buf;
+  int nb;
+  __device__ __forceinline__ void emit(uint32_t v) {
+    if (w == first_w)
+      atomicOr(&words[w], v);
+    else
+      words[w] = v;  // fully owned
+    w++;
   }
-}
+  __device__ __forceinline__ void put(uint32_t code, int len) {  // len <= 32, nb <= 31
+    buf |= (unsigned long long)code << (64 - nb - len);
+    nb += len;
+    if (nb >= 32) {
+      emit((uint32_t)(buf >> 32));
+      buf <<= 32;
+      nb -= 32;
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    if (nb > 0) atomicOr(&words[w], (uint32_t)(buf >> 32));  // shared with successor
+  }
+};
 
 }  // namespace
 
-template <typename SymT>
+template <typename SymT, bool WIDE>
 __global__ void __launch_bounds__(K3_THREADS) k3_encode(
     const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
-    uint32_t win_lo, uint32_t win_n, const float *__restrict__ x, uint32_t *__restrict__ payload,
-    unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
-    unsigned long long *__restrict__ chunk_off, EncStatus st, unsigned *__restrict__ ticket,
-    uint64_t ntiles, int extract_outliers) {
+    uint32_t win_lo, uint32_t win_n, uint32_t word_cap, const float *__restrict__ x,
+    uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
+    float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off, EncStatus st,
+    unsigned *__restrict__ ticket, uint64_t ntiles, int extract_outliers) {
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long *sh_ctab = reinterpret_cast<unsigned long long *>(smem);
-  uint32_t *sh_words = reinterpret_cast<uint32_t *>(smem + (size_t)win_n * 8);
+  using Ent = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  Ent *sh_ctab = reinterpret_cast<Ent *>(smem);
+  uint32_t *sh_words = reinterpret_cast<uint32_t *>(smem + (((size_t)win_n * sizeof(Ent) + 15) & ~size_t(15)));
   __shared__ unsigned long long wbuf[K3_THREADS / 32 + 1];
   __shared__ unsigned long long s_excl_bits, s_excl_nz;
   __shared__ unsigned s_tile;
 
   const int tid = threadIdx.x, lane = tid & 31;
-  for (uint32_t i = tid; i < win_n; i += K3_THREADS) sh_ctab[i] = ctab[win_lo + i];
+  for (uint32_t i = tid; i < win_n; i += K3_THREADS) {
+    unsigned long long e = ctab[win_lo + i];
+    if (WIDE)
+      sh_ctab[i] = (Ent)e;
+    else
+      sh_ctab[i] = (Ent)(((e >> 8) << 6) | (e & 63));  // (code << 6) | len, code <= 26 bits
+  }
   __syncthreads();
 
   while (true) {
@@ -67,11 +91,11 @@ __global__ void __launch_bounds__(K3_THREADS) k3_encode(
 #pragma unroll
         for (int j = 0; j < K3_EPT / 8; j++) {
           uint4 v = __ldcs(p + j);
-          uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int k = 0; k < 4; k++) {
-            s[8 * j + 2 * k] = w[k] & 0xFFFFu;
-            s[8 * j + 2 * k + 1] = w[k] >> 16;
+            s[8 * j + 2 * k] = w4[k] & 0xFFFFu;
+            s[8 * j + 2 * k + 1] = w4[k] >> 16;
           }
         }
       } else {
@@ -86,17 +110,34 @@ __global__ void __launch_bounds__(K3_THREADS) k3_encode(
 #pragma unroll
       for (int j = 0; j < K3_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : 0u;
     }
-    unsigned long long e[K3_EPT];
+    // (code, len) per symbol; code kept in the low bits of e
+    unsigned long long code[K3_EPT];
+    uint32_t len[K3_EPT];
     uint32_t nbits = 0, nz = 0;
 #pragma unroll
     for (int j = 0; j < K3_EPT; j++) {
       if (base + j < n) {
         uint32_t wi = s[j] - win_lo;
-        e[j] = wi < win_n ? sh_ctab[wi] : __ldg(&ctab[s[j]]);
-        nbits += (uint32_t)(e[j] & 0xFF);
+        if (WIDE) {
+          unsigned long long e = wi < win_n ? sh_ctab[wi] : __ldg(&ctab[s[j]]);
+          len[j] = (uint32_t)(e & 0xFF);
+          code[j] = e >> 8;
+        } else {
+          uint32_t e;
+          if (wi < win_n) {
+            e = (uint32_t)sh_ctab[wi];
+          } else {
+            unsigned long long g = __ldg(&ctab[s[j]]);
+            e = (uint32_t)(((g >> 8) << 6) | (g & 63));
+          }
+          len[j] = e & 63;
+          code[j] = e >> 6;
+        }
+        nbits += len[j];
         nz += s[j] == 0;
       } else {
-        e[j] = 0;
+        len[j] = 0;
+        code[j] = 0;
       }
     }
     unsigned long long tot;
@@ -129,8 +170,7 @@ __global__ void __launch_bounds__(K3_THREADS) k3_encode(
             } while (f == 0);
           }
           unsigned incm = __ballot_sync(0xffffffffu, (f & kFlagInc) != 0);
-          int stop = __ffs(incm) - 1;  // incm != 0 always? not if all 32 are AGG
-          if (!incm) stop = 32;
+          int stop = incm ? __ffs(incm) - 1 : 32;
           unsigned long long vb = 0, vn = 0;
           if (idx >= 0 && lane <= stop) {
             if (lane == stop) {
@@ -157,6 +197,9 @@ __global__ void __launch_bounds__(K3_THREADS) k3_encode(
         s_excl_nz = en;
       }
     }
+    // zero the word buffer while warp 0 looks back
+    const uint32_t zwords = min(word_cap, (uint32_t)((tile_bits + 63) >> 5));
+    for (uint32_t i = tid; i < zwords; i += K3_THREADS) sh_words[i] = 0;
     __syncthreads();
     const unsigned long long tile_bit0 = s_excl_bits;
     const unsigned long long my_bit0 = tile_bit0 + (excl >> 32);
@@ -179,26 +222,25 @@ __global__ void __launch_bounds__(K3_THREADS) k3_encode(
     // ---- pack into the shared word buffer ----
     const uint32_t start_off = (uint32_t)(tile_bit0 & 31);
     const uint32_t nwords = (uint32_t)((start_off + tile_bits + 31) >> 5);
-    for (uint32_t i = tid; i < nwords; i += K3_THREADS) sh_words[i] = 0;
-    __syncthreads();
-    {
+    if (nbits) {
       uint32_t rel = start_off + (uint32_t)(excl >> 32);
-      uint32_t w = rel >> 5;
-      int nb = rel & 31;
-      unsigned long long buf = 0;
+      Packer pk;
+      pk.words = sh_words;
+      pk.w = rel >> 5;
+      pk.first_w = pk.w;
+      pk.nb = rel & 31;
+      pk.buf = 0;
 #pragma unroll
       for (int j = 0; j < K3_EPT; j++) {
-        int len = (int)(e[j] & 0xFF);
-        if (!len) continue;
-        unsigned long long code = e[j] >> 8;
-        if (len > 32) {
-          append_bits(sh_words, w, buf, nb, (uint32_t)(code >> 32), len - 32);
-          append_bits(sh_words, w, buf, nb, (uint32_t)code, 32);
+        if (!len[j]) continue;
+        if (WIDE && len[j] > 32) {
+          pk.put((uint32_t)(code[j] >> 32), (int)len[j] - 32);
+          pk.put((uint32_t)code[j], 32);
         } else {
-          append_bits(sh_words, w, buf, nb, (uint32_t)code, len);
+          pk.put((uint32_t)code[j], (int)len[j]);
         }
       }
-      if (nb > 0) atomicOr(&sh_words[w], (uint32_t)(buf >> 32));
+      pk.finish();
     }
     __syncthreads();
 
@@ -230,13 +272,13 @@ __global__ void __launch_bounds__(K3_THREADS) k3_encode(
   }
 }
 
-template __global__ void k3_encode<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *,
-                                             uint32_t, uint32_t, const float *, uint32_t *,
-                                             unsigned long long *, float *, unsigned long long *,
-                                             EncStatus, unsigned *, uint64_t, int);
-template __global__ void k3_encode<uint32_t>(const uint32_t *, uint64_t, const unsigned long long *,
-                                             uint32_t, uint32_t, const float *, uint32_t *,
-                                             unsigned long long *, float *, unsigned long long *,
-                                             EncStatus, unsigned *, uint64_t, int);
+#define K3_INST(T, W)                                                                                        \
+  template __global__ void k3_encode<T, W>(const T *, uint64_t, const unsigned long long *, uint32_t, uint32_t, \
+                                           uint32_t, const float *, uint32_t *, unsigned long long *, float *,  \
+                                           unsigned long long *, EncStatus, unsigned *, uint64_t, int);
+K3_INST(uint16_t, false)
+K3_INST(uint16_t, true)
+K3_INST(uint32_t, false)
+K3_INST(uint32_t, true)
 
 }  // namespace actc

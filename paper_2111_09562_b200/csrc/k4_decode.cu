@@ -38,6 +38,7 @@ __device__ __forceinline__ uint64_t read_bits64(const uint32_t *__restrict__ pw,
 
 struct CodeTables {
   unsigned long long first[64];
+  unsigned long long lim[64];  // (first + count) << (32 - l), l <= 32 (left-aligned limit)
   uint32_t count[64];
   uint32_t base[64];
   uint32_t maxlen;
@@ -53,6 +54,7 @@ __device__ void build_tables(CodeTables &t, const uint32_t *len_counts) {
       t.first[l] = code;
       t.count[l] = c;
       t.base[l] = idx;
+      t.lim[l] = l <= 32 ? (code + c) << (32 - l) : 0;
       code += c;
       idx += c;
       if (c && l > 0) mx = l;
@@ -81,14 +83,32 @@ __device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint
 
 }  // namespace
 
-// LUT entry for every 12-bit prefix: (symbol << 6) | length, 0 = not a code
-// of length <= 12.  Same first-match rule as the reference's bit loop.
+// LUT entry for every 12-bit prefix: (symbol << 6) | length for a code of
+// length <= 12 (same first-match rule as the reference's bit loop); for a
+// prefix of longer codes, (l0 << 6) with l0 the first length whose
+// left-aligned limit exceeds the prefix (decoding continues from l0 on the
+// register window); 0 if no code starts with the prefix.  lut[kLutSize]
+// holds the fast-path flag: 1 if the code is prefix-free (Kraft <= 1) and
+// max length <= 32.
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
                             uint32_t *__restrict__ lut) {
   __shared__ CodeTables t;
   build_tables(t, len_counts);
   __syncthreads();
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p == 0) {
+    // Kraft sum in units of 2^-63
+    unsigned long long k = 0;
+    bool over = false;
+    for (int l = 1; l < 64 && !over; l++) {
+      unsigned long long add = (unsigned long long)t.count[l] << (63 - l);
+      if (t.count[l] >> l) over = true;  // count >= 2^l alone exceeds the budget
+      if (k + add < k) over = true;
+      k += add;
+      if (k > (1ull << 63)) over = true;
+    }
+    lut[kLutSize] = (!over && t.maxlen <= 32) ? 1u : 0u;
+  }
   if (p >= (uint32_t)kLutSize) return;
   uint32_t e = 0;
   int lim = t.maxlen < (uint32_t)kLutBits ? (int)t.maxlen : kLutBits;
@@ -98,6 +118,16 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
     if (off < t.count[l]) {
       e = (canon[t.base[l] + off] << 6) | (uint32_t)l;
       break;
+    }
+  }
+  if (!e && t.maxlen > (uint32_t)kLutBits && t.maxlen <= 32) {
+    const unsigned long long w = (unsigned long long)p << (32 - kLutBits);
+    for (int l = kLutBits + 1; l <= (int)t.maxlen; l++) {
+      unsigned long long limit = (t.first[l] + t.count[l]) << (32 - l);
+      if (limit > w) {
+        e = (uint32_t)l << 6;
+        break;
+      }
     }
   }
   lut[p] = e;
@@ -127,6 +157,7 @@ __global__ void __launch_bounds__(K4_THREADS) k4_decode(DecodeArgs a) {
 
   const uint64_t nchunks = (a.n + ACTC_CHUNK - 1) / ACTC_CHUNK;
   const long long radius = a.radius;
+  const bool fast_long = a.lut[kLutSize] != 0;
   unsigned long long nonzero = 0;
 
   while (true) {
@@ -159,37 +190,52 @@ __global__ void __launch_bounds__(K4_THREADS) k4_decode(DecodeArgs a) {
       buf <<= (pos & 31);
       int nb = 64 - (int)(pos & 31);
       wi += 2;
+      uint32_t nextw = bswap32(pw[wi++]);  // one-word lookahead hides the load latency
       long long acc = 0;
       int reset = 0;
       bool bad = false;
       uint32_t pair = 0;
       for (uint32_t i = 0; i < cnt; i++) {
         if (nb < 32) {
-          buf |= (unsigned long long)bswap32(pw[wi++]) << (32 - nb);
+          buf |= (unsigned long long)nextw << (32 - nb);
           nb += 32;
+          nextw = bswap32(pw[wi++]);
         }
-        uint32_t e = lut[buf >> (64 - kLutBits)];
+        const uint32_t W = (uint32_t)(buf >> 32);
+        uint32_t e = lut[W >> (32 - kLutBits)];
         int len = e & 63;
         uint32_t s = e >> 6;
-        if (len) {
-          buf <<= len;
-          nb -= len;
-          pos += len;
-        } else {
-          len = slow_decode(pw, pos, t, a.canon, s);
+        if (!len) {
+          if (fast_long && s) {
+            // canonical decode from the register window: first length whose
+            // left-aligned limit exceeds the window
+            int l = (int)s;
+            while (l <= (int)t.maxlen && (unsigned long long)W >= t.lim[l]) l++;
+            if (l <= (int)t.maxlen) {
+              len = l;
+              s = __ldg(&a.canon[t.base[l] + ((W >> (32 - l)) - (uint32_t)t.first[l])]);
+            }
+          }
           if (!len) {
-            bad = true;
-            s = a.radius;
+            // reference first-match rule from memory (over-subscribed tables, codes > 32 bits)
+            len = slow_decode(pw, pos, t, a.canon, s);
+            if (!len) {
+              bad = true;
+              break;
+            }
+            pos += len;
+            wi = pos >> 5;
+            buf = ((unsigned long long)bswap32(pw[wi]) << 32) | bswap32(pw[wi + 1]);
+            buf <<= (pos & 31);
+            nb = 64 - (int)(pos & 31);
+            wi += 2;
+            nextw = bswap32(pw[wi++]);
             len = 0;
           }
-          pos += len;
-          wi = pos >> 5;
-          buf = ((unsigned long long)bswap32(pw[wi]) << 32) | bswap32(pw[wi + 1]);
-          buf <<= (pos & 31);
-          nb = 64 - (int)(pos & 31);
-          wi += 2;
-          if (bad) break;
         }
+        buf <<= len;
+        nb -= len;
+        pos += len;
         if (MODE != 2) {
           if (s == 0) {
             uint32_t ord = ord0 + zc;

@@ -14,14 +14,16 @@ constexpr uint32_t K1_WIN = 8192;  // shared-memory histogram window (bins)
 constexpr int K2_THREADS = 1024;
 constexpr uint32_t K2_SMEM_SORT_MAX = 8192;  // keys sorted in shared memory
 
-// K3: 256 threads x 16 symbols per tile (16 decode chunks per tile)
-constexpr int K3_THREADS = 256;
+// K3: 512 threads x 16 symbols per tile (32 decode chunks per tile)
+constexpr int K3_THREADS = 512;
 constexpr int K3_EPT = 16;
 constexpr int K3_TILE = K3_THREADS * K3_EPT;
-constexpr uint32_t K3_WIN = 4096;  // code-table window cached in shared memory
+constexpr uint32_t K3_WIN32 = 32768;  // u32 code-table window (codes <= 26 bits)
+constexpr uint32_t K3_WIN64 = 8192;   // u64 window for longer codes
+constexpr int K3_SHORT_MAXLEN = 26;
 
 // K4: one thread decodes one ACTC_CHUNK-symbol chunk
-constexpr int K4_THREADS = 64;
+constexpr int K4_THREADS = 128;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
 // lookback status for the encoder (per K3 tile)
@@ -68,20 +70,20 @@ struct CodebookArgs {
   // scratch (global, used when L exceeds the shared-memory capacity)
   uint32_t *live_sym;              // [A]
   unsigned long long *live_freq;   // [A]
-  unsigned long long *keys;        // [pow2 >= A]
-  uint32_t *vals;                  // [pow2 >= A]
+  unsigned long long *keys, *keys2;  // [A] radix ping-pong
+  uint32_t *vals, *vals2;            // [A]
   unsigned long long *nf;          // [A]
-  uint32_t *lpar, *npar, *S;       // [A], [A], [2A]
+  uint32_t *lpar, *npar;           // [A], [A]
   uint8_t *llen, *ndepth;          // [A], [A]
   uint64_t n_symbols;              // total symbol count (for entropy)
   uint32_t sym_bytes;
 };
 __global__ void k2_codebook(CodebookArgs a);
 
-template <typename SymT>
+template <typename SymT, bool WIDE>
 __global__ void k3_encode(const SymT *__restrict__ sym, uint64_t n,
                           const unsigned long long *__restrict__ ctab, uint32_t win_lo,
-                          uint32_t win_n, const float *__restrict__ x,
+                          uint32_t win_n, uint32_t word_cap, const float *__restrict__ x,
                           uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
                           float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
                           EncStatus st, unsigned *__restrict__ ticket, uint64_t ntiles,
@@ -89,6 +91,10 @@ __global__ void k3_encode(const SymT *__restrict__ sym, uint64_t n,
 
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
                             uint32_t *__restrict__ lut);
+
+// decoder LUT: kLutSize entries + a header word (bit0: fast long-code path
+// valid, i.e. prefix-free code with max length <= 32)
+constexpr int kLutWords = kLutSize + 4;
 
 struct DecodeArgs {
   uint64_t n;
