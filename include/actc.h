@@ -81,6 +81,7 @@ typedef struct {
   const uint8_t *payload_dev;      /* MSB-first bitstream; 4-byte aligned, >=8 B tail pad */
   uint64_t payload_bits;
   const uint64_t *chunk_offsets_dev; /* [ceil(n/ACTC_CHUNK)] or NULL (rebuilt) */
+  const int64_t *chunk_lat_dev;      /* [ceil(n/ACTC_CHUNK)] lattice before each chunk, or NULL */
 } actc_stream_t;
 
 /* Result of a decompression; valid after the stream is synchronized. */
@@ -102,10 +103,12 @@ void actc_ctx_destroy(actc_ctx *ctx);
  * prequantize (:238-251), bound check (:311-312), lorenzo_encode
  * (:254-272), bincount (huffman.py:183), build_code_lengths
  * (huffman.py:37-75), canonical_codes (huffman.py:78-94).
+ * chunk_lat_dev (may be NULL) receives the decode index's lattice value
+ * before every ACTC_CHUNK-th element ([ceil(n/ACTC_CHUNK)] int64).
  * plan_host must be pinned host memory; it is written asynchronously. */
 int actc_compress_plan(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb,
-                       uint32_t radius, uint32_t flags, actc_plan_t *plan_host,
-                       actc_stream s);
+                       uint32_t radius, uint32_t flags, int64_t *chunk_lat_dev,
+                       actc_plan_t *plan_host, actc_stream s);
 
 /* compress(), phase 2 -- huffman_encode bit packing (huffman.py:188-207)
  * plus outlier extraction (codec.py:321-322) and the decode chunk index.

@@ -9,6 +9,7 @@ from .codec import (
     CompressedActivation,
     CompressionReport,
     compress,
+    compress_batch,
     compress_device,
     decompress,
     decompress_device,

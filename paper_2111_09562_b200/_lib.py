@@ -52,6 +52,7 @@ class StreamDesc(C.Structure):
         ("payload_dev", C.c_void_p),
         ("payload_bits", C.c_uint64),
         ("chunk_offsets_dev", C.c_void_p),
+        ("chunk_lat_dev", C.c_void_p),
     ]
 
 
@@ -88,7 +89,7 @@ def lib():
             "actc_version": ([], I),
             "actc_ctx_create": ([I, C.POINTER(P)], I),
             "actc_ctx_destroy": ([P], None),
-            "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P], I),
+            "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P, P], I),
             "actc_compress_encode": ([P, P, P, P, P, P, P, P, P, P], I),
             "actc_decompress": ([P, P, P, I, P, P], I),
             "actc_codebook_from_lengths": ([P, P, U64, P, P, P, P], I),
@@ -186,6 +187,22 @@ def context(device=None) -> Context:
     if c is None:
         with torch.cuda.device(dev):
             c = ctxs[dev] = Context(dev)
+    return c
+
+
+def context_for(device: int, slot: int) -> Context:
+    """Extra contexts for concurrent (multi-stream) compression: slot 0 is
+    the thread's main context, slots 1.. are private scratch sets."""
+    if slot == 0:
+        return context(device)
+    torch = torch_cuda()
+    extra = getattr(_tls, "extra", None)
+    if extra is None:
+        extra = _tls.extra = {}
+    c = extra.get((device, slot))
+    if c is None:
+        with torch.cuda.device(device):
+            c = extra[(device, slot)] = Context(device)
     return c
 
 

@@ -272,6 +272,7 @@ class CompressedActivation:
         d.payload_dev = dev["payload"].data_ptr()
         d.payload_bits = self.payload_bits
         d.chunk_offsets_dev = dev["chunk_off"].data_ptr() if (with_index and "chunk_off" in dev) else None
+        d.chunk_lat_dev = dev["chunk_lat"].data_ptr() if (with_index and "chunk_lat" in dev) else None
         return d
 
     def _ensure_index(self):
@@ -282,6 +283,8 @@ class CompressedActivation:
         ctx = _lib.context()
         sh, s = _lib.stream_handle()
         n = self.symbol_count
+        if n and not self._live:
+            raise FormatError("empty code table with nonzero symbol count")
         nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
         co = torch.zeros(max(nchunks, 1), dtype=torch.int64, device="cuda")
         st = C.c_uint32(0)
@@ -389,8 +392,11 @@ def compress_device(x, params: CodecParams, dims=None, stream=None):
     sh, s = _lib.stream_handle(stream)
     L = _lib.lib()
     flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if params.preserve_zeros else 0
+    nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
+    chunk_lat = torch.empty(nchunks, dtype=torch.int64, device=x.device)
     _lib.raise_for(L.actc_compress_plan(ctx.handle, C.c_void_p(x.data_ptr()), n, float(params.eb),
-                                        int(params.radius), flags, C.c_void_p(ctx.plan_buf.data_ptr()), sh))
+                                        int(params.radius), flags, C.c_void_p(chunk_lat.data_ptr()),
+                                        C.c_void_p(ctx.plan_buf.data_ptr()), sh))
     s.synchronize()
     plan = _lib.Plan.from_buffer_copy(ctx.plan)
     if plan.status:
@@ -404,7 +410,8 @@ def compress_device(x, params: CodecParams, dims=None, stream=None):
         "out_val": torch.empty(plan.n_outliers, dtype=torch.float32, device=x.device),
         "canon": torch.empty(max(plan.live_symbols, 1), dtype=torch.int32, device=x.device),
         "len_counts": torch.empty(64, dtype=torch.int32, device=x.device),
-        "chunk_off": torch.empty((n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK, dtype=torch.int64, device=x.device),
+        "chunk_off": torch.empty(nchunks, dtype=torch.int64, device=x.device),
+        "chunk_lat": chunk_lat,
     }
     _lib.raise_for(L.actc_compress_encode(
         ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev["payload"].data_ptr()),
@@ -420,6 +427,103 @@ def compress_device(x, params: CodecParams, dims=None, stream=None):
         codes_entropy_bits_per_symbol=float(plan.entropy_bits), outlier_warning=frac > 0.5,
     )
     return c, report
+
+
+def _finish_compress(x, params, dims, plan, dev, ctx, sh):
+    """phase 2 (K3 encode) into exact-size buffers; returns (container, report)."""
+    torch = _lib.torch_cuda()
+    n = x.numel()
+    if plan.status:
+        if plan.status == _lib.ACTC_EDATA:
+            from .errors import DataError
+            raise DataError("tensor contains NaN or Inf")
+        raise ParameterError("Huffman code length exceeds 63 bits")
+    dev["payload"] = torch.empty(_payload_buffer_bytes(plan.payload_bits), dtype=torch.uint8, device=x.device)
+    dev["out_idx"] = torch.empty(plan.n_outliers, dtype=torch.int64, device=x.device)
+    dev["out_val"] = torch.empty(plan.n_outliers, dtype=torch.float32, device=x.device)
+    dev["canon"] = torch.empty(max(plan.live_symbols, 1), dtype=torch.int32, device=x.device)
+    dev["len_counts"] = torch.empty(64, dtype=torch.int32, device=x.device)
+    dev["chunk_off"] = torch.empty(dev["chunk_lat"].numel(), dtype=torch.int64, device=x.device)
+    _lib.raise_for(_lib.lib().actc_compress_encode(
+        ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev["payload"].data_ptr()),
+        C.c_void_p(dev["out_idx"].data_ptr()), C.c_void_p(dev["out_val"].data_ptr()),
+        C.c_void_p(dev["canon"].data_ptr()), C.c_void_p(dev["len_counts"].data_ptr()),
+        C.c_void_p(dev["chunk_off"].data_ptr()), sh))
+    c = CompressedActivation._from_device(dims, params, dev, plan.payload_bits, plan.n_outliers,
+                                          plan.live_symbols, plan.rle_runs)
+    blob_len = _cmtz_size(len(dims), plan.n_outliers, plan.rle_runs, plan.payload_bits)
+    frac = plan.n_outliers / n
+    report = CompressionReport(
+        original_bytes=n * 4, compressed_bytes=blob_len, ratio=(n * 4) / blob_len, outlier_fraction=frac,
+        codes_entropy_bits_per_symbol=float(plan.entropy_bits), outlier_warning=frac > 0.5,
+    )
+    return c, report
+
+
+_side_streams: dict = {}
+
+
+def _stream_pool(device, k):
+    torch = _lib.torch_cuda()
+    pool = _side_streams.setdefault(device, [])
+    while len(pool) < k:
+        pool.append(torch.cuda.Stream(device=device))
+    return pool[:k]
+
+
+def compress_batch(xs, params, max_concurrency: int = 8):
+    """Compress several fp32 CUDA tensors with ONE host synchronisation.
+
+    Phase 1 (K1 quantize/Lorenzo/histogram + K2 codebook) of every tensor
+    runs concurrently on its own stream and context -- K2 is a single-CTA
+    kernel, so concurrent codebooks hide each other's latency behind the
+    bandwidth-bound kernels; then the plans are read once and phase 2 (K3)
+    runs.  Results are ordered on the caller's current stream.
+    """
+    torch = _lib.torch_cuda()
+    if isinstance(params, CodecParams):
+        params = [params] * len(xs)
+    xs = [x if x.is_contiguous() else x.contiguous() for x in xs]
+    for x in xs:
+        if x.dtype != torch.float32:
+            raise ParameterError("compress expects a 32-bit tensor; convert explicitly with astype(4)")
+    dev_index = xs[0].device.index if xs else torch.cuda.current_device()
+    main = torch.cuda.current_stream()
+    results = []
+    for g0 in range(0, len(xs), max_concurrency):
+        group = list(range(g0, min(len(xs), g0 + max_concurrency)))
+        streams = _stream_pool(dev_index, len(group))
+        ready = main.record_event()
+        jobs = []
+        for slot, i in enumerate(group):
+            x, p = xs[i], params[i]
+            s = streams[slot]
+            ctx = _lib.context_for(dev_index, slot)
+            n = x.numel()
+            nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
+            dev = {"chunk_lat": torch.empty(nchunks, dtype=torch.int64, device=x.device)}
+            s.wait_event(ready)
+            sh = C.c_void_p(s.cuda_stream)
+            flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
+            _lib.raise_for(_lib.lib().actc_compress_plan(
+                ctx.handle, C.c_void_p(x.data_ptr()), n, float(p.eb), int(p.radius), flags,
+                C.c_void_p(dev["chunk_lat"].data_ptr()), C.c_void_p(ctx.plan_buf.data_ptr()), sh))
+            jobs.append((i, x, p, s, ctx, sh, dev))
+        for (_, _, _, s, _, _, _) in jobs:
+            s.synchronize()
+        for (i, x, p, s, ctx, sh, dev) in jobs:
+            plan = _lib.Plan.from_buffer_copy(ctx.plan)
+            with torch.cuda.stream(s):
+                c, rep = _finish_compress(x, p, tuple(x.shape) or (1,), plan, dev, ctx, sh)
+            for t in c._dev.values():  # used on both the side and the caller's stream
+                t.record_stream(s)
+                t.record_stream(main)
+            x.record_stream(s)
+            results.append((i, c, rep))
+        for (_, _, _, s, _, _, _) in jobs:
+            main.wait_stream(s)
+    results.sort(key=lambda r: r[0])
+    return [(c, rep) for _, c, rep in results]
 
 
 def compress(t, params: CodecParams):

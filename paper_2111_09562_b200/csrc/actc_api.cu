@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -155,6 +156,12 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   a.ndepth = (uint8_t *)(b + l.ndepth);
   a.n_symbols = n_symbols;
   a.sym_bytes = sym_bytes;
+  a.dbg = nullptr;
+  if (getenv("ACTC_K2_TIMING")) {
+    int rc2 = grow(c->idx, 4096);
+    if (rc2) return rc2;
+    a.dbg = (unsigned long long *)c->idx.p;
+  }
   CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
   k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
   CKL();
@@ -162,7 +169,7 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
 }
 
 // misc counters layout (u64 slots)
-enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SLOTS = 8 };
+enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_SLOTS = 8 };
 
 }  // namespace
 
@@ -170,6 +177,14 @@ extern "C" {
 
 const char *actc_last_error(void) { return g_err; }
 int actc_version(void) { return 1; }
+
+/* debug: copy the K2 stage timestamps of the last codebook build (ACTC_K2_TIMING=1) */
+int actc_debug_k2_timing(actc_ctx *c, uint64_t *out16) {
+  if (!c->idx.p) return ACTC_EPARAM;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out16, c->idx.p, 16 * 8, cudaMemcpyDeviceToHost));
+  return ACTC_OK;
+}
 
 int actc_ctx_create(int device, actc_ctx **out) {
   *out = nullptr;
@@ -195,9 +210,14 @@ int actc_ctx_create(int device, actc_ctx **out) {
   c->k1_blocks = std::max(1, nb) * c->num_sms;
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  const void *k3s[4] = {(const void *)k3_encode<uint16_t, false>, (const void *)k3_encode<uint16_t, true>,
-                        (const void *)k3_encode<uint32_t, false>, (const void *)k3_encode<uint32_t, true>};
-  for (const void *f : k3s) {
+  const void *big[] = {(const void *)k3_count<uint16_t, false>, (const void *)k3_count<uint16_t, true>,
+                       (const void *)k3_count<uint32_t, false>, (const void *)k3_count<uint32_t, true>,
+                       (const void *)k3_pack<uint16_t, false>,  (const void *)k3_pack<uint16_t, true>,
+                       (const void *)k3_pack<uint32_t, false>,  (const void *)k3_pack<uint32_t, true>,
+                       (const void *)k4w_decode<0, 16>,         (const void *)k4w_decode<1, 16>,
+                       (const void *)k4w_decode<0, 32>,         (const void *)k4w_decode<1, 32>,
+                       (const void *)k4w_decode<2, 32>};
+  for (const void *f : big) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, f));
     CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
@@ -229,7 +249,7 @@ void actc_ctx_destroy(actc_ctx *c) {
 }
 
 int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius,
-                       uint32_t flags, actc_plan_t *plan_host, actc_stream stream) {
+                       uint32_t flags, int64_t *chunk_lat, actc_plan_t *plan_host, actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
   if (radius < 2) return set_err(ACTC_EPARAM, "radius must be >= 2, got %u", radius);
@@ -259,11 +279,11 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
   if (sb == 2)
     k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, win_n * 4, s>>>(
         x, n, P, radius, (uint16_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
-        (unsigned *)(misc + M_BAD));
+        (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
   else
     k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, win_n * 4, s>>>(
         x, n, P, radius, (uint32_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
-        (unsigned *)(misc + M_BAD));
+        (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
   CKL();
   if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, nullptr, misc + M_NOUT, n, sb, s,
                          (const unsigned *)(misc + M_BAD))))
@@ -280,23 +300,8 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
 static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, const float *x,
                          const actc_plan_t *plan, uint8_t *payload, uint64_t *out_idx, float *out_val,
                          uint64_t *chunk_off, int extract, cudaStream_t s) {
-  uint64_t ntiles = cdiv(n, K3_TILE);
+  const uint64_t ntiles = cdiv(n, K3_TILE);
   int rc;
-  // status: flag u32 | agg_bits | agg_nz | inc_bits | inc_nz (u64) | tail u32
-  size_t need = ntiles * (4 + 8 * 4 + 4) + 1024;
-  if ((rc = grow(c->status, need))) return rc;
-  char *b = (char *)c->status.p;
-  EncStatus st;
-  st.flag = (unsigned *)b;
-  size_t o = ((ntiles * 4 + 255) / 256) * 256;
-  st.agg_bits = (unsigned long long *)(b + o); o += ntiles * 8;
-  st.agg_nz = (unsigned long long *)(b + o); o += ntiles * 8;
-  st.inc_bits = (unsigned long long *)(b + o); o += ntiles * 8;
-  st.inc_nz = (unsigned long long *)(b + o); o += ntiles * 8;
-  st.tail = (unsigned *)(b + o);
-  CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
-  unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
-  CK(cudaMemsetAsync(ticket, 0, 8, s));
   // code-table window: the live symbol range, capped
   const bool wide = plan->max_len > (uint32_t)K3_SHORT_MAXLEN;
   const uint32_t cap = wide ? K3_WIN64 : K3_WIN32;
@@ -314,24 +319,48 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
   }
   const uint32_t maxlen = plan->max_len ? plan->max_len : 1;
   const uint32_t word_cap = (uint32_t)(((uint64_t)K3_TILE * maxlen + 31) / 32 + 4);
-  const size_t smem = (((size_t)win_n * (wide ? 8 : 4) + 15) & ~size_t(15)) + (size_t)word_cap * 4;
+  const size_t tbl = (((size_t)win_n * (wide ? 8 : 4) + 15) & ~size_t(15));
+  const size_t smem_pack = tbl + (size_t)word_cap * 4;
+  // the count pass only needs lengths: a byte per symbol over the whole live range
+  const uint32_t cwin_lo = lo, cwin_n = std::min<uint32_t>(span, 65536u);
+  const size_t smem_count = (cwin_n + 15) & ~15u;
+  const void *fc, *fp;
+  if (sb == 2) {
+    fc = wide ? (const void *)k3_count<uint16_t, true> : (const void *)k3_count<uint16_t, false>;
+    fp = wide ? (const void *)k3_pack<uint16_t, true> : (const void *)k3_pack<uint16_t, false>;
+  } else {
+    fc = wide ? (const void *)k3_count<uint32_t, true> : (const void *)k3_count<uint32_t, false>;
+    fp = wide ? (const void *)k3_pack<uint32_t, true> : (const void *)k3_pack<uint32_t, false>;
+  }
   int occ = 0;
-  if (sb == 2)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide ? (const void *)k3_encode<uint16_t, true> : (const void *)k3_encode<uint16_t, false>, K3_THREADS, smem);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide ? (const void *)k3_encode<uint32_t, true> : (const void *)k3_encode<uint32_t, false>, K3_THREADS, smem);
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)std::max(1, occ) * c->num_sms);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fp, K3_THREADS, smem_pack);
+  const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
+  const uint64_t tpc = cdiv(ntiles, std::min<uint64_t>(ntiles, want));
+  const uint32_t ncta = (uint32_t)cdiv(ntiles, tpc);
+  // scratch: cta_bits, cta_nz, cta_bit0, cta_nz0 (u64) + head, tail (u32)
+  if ((rc = grow(c->status, (size_t)ncta * (8 * 4 + 8) + 1024))) return rc;
+  unsigned long long *cbits = (unsigned long long *)c->status.p;
+  unsigned long long *cnz = cbits + ncta, *cbit0 = cnz + ncta, *cnz0 = cbit0 + ncta;
+  uint32_t *head = (uint32_t *)(cnz0 + ncta), *tail = head + ncta;
+  unsigned long long *misc = (unsigned long long *)c->misc.p;
   const unsigned long long *ct = (const unsigned long long *)c->ctab.p;
-#define K3_LAUNCH(T, W)                                                                                   \
-  k3_encode<T, W><<<grid, K3_THREADS, smem, s>>>((const T *)sym, n, ct, win_lo, win_n, word_cap, x,      \
-                                                  (uint32_t *)payload, (unsigned long long *)out_idx, out_val, \
-                                                  (unsigned long long *)chunk_off, st, ticket, ntiles, extract)
+#define K3_LAUNCH(T, W)                                                                                        \
+  do {                                                                                                         \
+    k3_count<T, W><<<ncta, K3_THREADS, smem_count, s>>>((const T *)sym, n, ct, cwin_lo, cwin_n, tpc, cbits, cnz); \
+    k_excl_scan_u64<<<1, 1024, 0, s>>>(cbits, ncta, cbit0, misc + M_SCAN_TOT);                                \
+    k_excl_scan_u64<<<1, 1024, 0, s>>>(cnz, ncta, cnz0, misc + M_SCAN_TOT2);                                  \
+    k3_pack<T, W><<<ncta, K3_THREADS, smem_pack, s>>>((const T *)sym, n, ct, win_lo, win_n, word_cap, tpc, x,  \
+                                                      cbit0, cnz0, (uint32_t *)payload,                        \
+                                                      (unsigned long long *)out_idx, out_val,                  \
+                                                      (unsigned long long *)chunk_off, head, tail, extract);   \
+  } while (0)
   if (sb == 2) {
     if (wide) K3_LAUNCH(uint16_t, true); else K3_LAUNCH(uint16_t, false);
   } else {
     if (wide) K3_LAUNCH(uint32_t, true); else K3_LAUNCH(uint32_t, false);
   }
 #undef K3_LAUNCH
+  k3_fixup<<<1, 1024, 0, s>>>((uint32_t *)payload, cbit0, cbits, head, tail, ncta);
   CKL();
   return ACTC_OK;
 }
@@ -396,15 +425,34 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.nonzero = &c->dres_dev->nonzero;
   a.markers = &c->dres_dev->markers;
   a.status = &c->dres_dev->status;
+  a.chunk_lat = (const long long *)S.chunk_lat_dev;
+  a.live = S.live_symbols;
   const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
-  const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)(sw16 ? c->k4_blocks[0] : c->k4_blocks[1]));
-  if (mode == 0)
-    sw16 ? k4_decode<0, 16><<<grid, K4_THREADS, smem, s>>>(a) : k4_decode<0, 32><<<grid, K4_THREADS, smem, s>>>(a);
-  else if (mode == 1)
-    sw16 ? k4_decode<1, 16><<<grid, K4_THREADS, smem, s>>>(a) : k4_decode<1, 32><<<grid, K4_THREADS, smem, s>>>(a);
-  else
-    k4_decode<2, 32><<<grid, K4_THREADS, smem, s>>>(a);
+  if (S.chunk_lat_dev || mode == 2) {
+    // warp decoder: no scan, no look-back
+    const int NW = K4W_THREADS / 32;
+    const size_t smem = (size_t)NW * 32 * (sw16 ? 33 : 65) * 4;
+    const void *f = mode == 0 ? (sw16 ? (const void *)k4w_decode<0, 16> : (const void *)k4w_decode<0, 32>)
+                  : mode == 1 ? (sw16 ? (const void *)k4w_decode<1, 16> : (const void *)k4w_decode<1, 32>)
+                              : (const void *)k4w_decode<2, 32>;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, K4W_THREADS, smem);
+    const uint64_t nwt = cdiv(nchunks, 32);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nwt, NW), (uint64_t)std::max(1, occ) * c->num_sms));
+    if (mode == 0)
+      sw16 ? k4w_decode<0, 16><<<grid, K4W_THREADS, smem, s>>>(a) : k4w_decode<0, 32><<<grid, K4W_THREADS, smem, s>>>(a);
+    else if (mode == 1)
+      sw16 ? k4w_decode<1, 16><<<grid, K4W_THREADS, smem, s>>>(a) : k4w_decode<1, 32><<<grid, K4W_THREADS, smem, s>>>(a);
+    else
+      k4w_decode<2, 32><<<grid, K4W_THREADS, smem, s>>>(a);
+  } else {
+    const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
+    const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)(sw16 ? c->k4_blocks[0] : c->k4_blocks[1]));
+    if (mode == 0)
+      sw16 ? k4_decode<0, 16><<<grid, K4_THREADS, smem, s>>>(a) : k4_decode<0, 32><<<grid, K4_THREADS, smem, s>>>(a);
+    else
+      sw16 ? k4_decode<1, 16><<<grid, K4_THREADS, smem, s>>>(a) : k4_decode<1, 32><<<grid, K4_THREADS, smem, s>>>(a);
+  }
   CKL();
   if (res_host) CK(cudaMemcpyAsync(res_host, c->dres_dev, sizeof(DecResult), cudaMemcpyDeviceToHost, s));
   return ACTC_OK;

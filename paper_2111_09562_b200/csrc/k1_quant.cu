@@ -19,7 +19,8 @@ template <typename SymT>
 __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
     const float *__restrict__ x, uint64_t n, QParams P, uint32_t radius, SymT *__restrict__ sym,
     unsigned long long *__restrict__ ghist, unsigned long long *__restrict__ n_outliers,
-    uint32_t win_lo, uint32_t win_n, unsigned *__restrict__ nonfinite) {
+    uint32_t win_lo, uint32_t win_n, unsigned *__restrict__ nonfinite,
+    long long *__restrict__ chunk_lat) {
   extern __shared__ unsigned sh_hist[];
   for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) sh_hist[i] = 0;
   __syncthreads();
@@ -52,6 +53,12 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
       bool vj;
       q[j] = quant_elem(xv[j], P, vj);
       viol |= (unsigned)vj << j;
+    }
+    // decode index: lattice value just before every ACTC_CHUNK-th element
+    // (the running value lorenzo_decode holds there, codec.py:286-292)
+    if (chunk_lat) {
+      if (base == 0) chunk_lat[0] = 0;
+      if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q[K1_EPT - 1];
     }
     long long prev = __shfl_up_sync(0xffffffffu, q[K1_EPT - 1], 1);
     if (lane == 0) {
@@ -113,11 +120,11 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
 template __global__ void k1_quant_lorenzo_hist<uint16_t>(const float *, uint64_t, QParams, uint32_t,
                                                          uint16_t *, unsigned long long *,
                                                          unsigned long long *, uint32_t, uint32_t,
-                                                         unsigned *);
+                                                         unsigned *, long long *);
 template __global__ void k1_quant_lorenzo_hist<uint32_t>(const float *, uint64_t, QParams, uint32_t,
                                                          uint32_t *, unsigned long long *,
                                                          unsigned long long *, uint32_t, uint32_t,
-                                                         unsigned *);
+                                                         unsigned *, long long *);
 
 // Histogram of an arbitrary u32 symbol stream (huffman_encode's bincount,
 // huffman.py:181-183) with the out-of-range check.

@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
 
   const int tid = threadIdx.x;
   const uint64_t A = a.A;
+#define K2_STAMP(i) \
+  if (a.dbg && tid == 0) a.dbg[i] = clock64();
+  K2_STAMP(0)
 
   if (tid == 0) {
     s_err = 0;
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   atomicMax(&s_maxf, maxf);
   __syncthreads();
   maxf = s_maxf;
+  K2_STAMP(1)
 
   // generic pointers: shared memory for small L, global scratch otherwise
   unsigned long long *k0 = a.keys, *k1 = a.keys2, *nf = a.nf;
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     }
     // sorted leaf i: freq k0[i], live index v0[i]
     const unsigned long long *lf = k0;
+    K2_STAMP(2)
 
     // ---- 3. phase-parallel two-queue merge ----
     if (tid == 0) {
@@ -320,6 +325,8 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       if (s_err & 2u) break;
     }
     // ---- 4. depths, walking phases backwards ----
+    K2_STAMP(3)
+    if (a.dbg && tid == 0) a.dbg[8] = s_nph;
     const uint32_t nn = s_nn, root = nn - 1, nph = s_nph;
     if (tid == 0) ndepth[root] = 0;
     __syncthreads();
@@ -344,6 +351,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   }
   __syncthreads();
 
+  K2_STAMP(4)
   // ---- 5. canonical order: stable radix pass on length (input in symbol order) ----
   for (uint32_t i = tid; i < L; i += K2_THREADS) {
     k1[i] = (unsigned long long)llen[i];
@@ -390,6 +398,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     for (uint32_t j = tid; j < L; j += K2_THREADS) a.out_lengths[a.live_sym[j]] = llen[j];
   }
 
+  K2_STAMP(5)
   // ---- 6. plan: payload bits, RLE record count, entropy, live range ----
   unsigned long long bits = 0, recs = 0;
   double ent = 0.0;
@@ -457,6 +466,10 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     if (a.nonfinite && *a.nonfinite) pl->status = ACTC_EDATA;
     pl->sym_lo = L ? a.live_sym[0] : 0;
     pl->sym_hi = L ? a.live_sym[L - 1] : 0;
+    if (a.dbg) {
+      a.dbg[6] = clock64();
+      a.dbg[9] = L;
+    }
   }
 }
 

@@ -22,8 +22,11 @@ constexpr uint32_t K3_WIN32 = 32768;  // u32 code-table window (codes <= 26 bits
 constexpr uint32_t K3_WIN64 = 8192;   // u64 window for longer codes
 constexpr int K3_SHORT_MAXLEN = 26;
 
-// K4: one thread decodes one ACTC_CHUNK-symbol chunk
+// K4 (scan variant, streams without a lattice index): one thread per chunk
 constexpr int K4_THREADS = 128;
+// K4 (warp variant, indexed streams): one warp per 32 chunks
+constexpr int K4W_THREADS = 256;
+constexpr int K4W_CANON_CACHE = 8192;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
 // lookback status for the encoder (per K3 tile)
@@ -44,7 +47,8 @@ __global__ void k1_quant_lorenzo_hist(const float *__restrict__ x, uint64_t n, Q
                                       uint32_t radius, SymT *__restrict__ sym,
                                       unsigned long long *__restrict__ ghist,
                                       unsigned long long *__restrict__ n_outliers, uint32_t win_lo,
-                                      uint32_t win_n, unsigned *__restrict__ nonfinite);
+                                      uint32_t win_n, unsigned *__restrict__ nonfinite,
+                                      long long *__restrict__ chunk_lat);
 __global__ void k_hist_u32(const uint32_t *__restrict__ s, uint64_t n, uint64_t alphabet,
                            unsigned long long *__restrict__ ghist, unsigned *__restrict__ bad,
                            uint32_t win_n);
@@ -77,17 +81,25 @@ struct CodebookArgs {
   uint8_t *llen, *ndepth;          // [A], [A]
   uint64_t n_symbols;              // total symbol count (for entropy)
   uint32_t sym_bytes;
+  unsigned long long *dbg;         // optional stage timestamps (clock64)
 };
 __global__ void k2_codebook(CodebookArgs a);
 
 template <typename SymT, bool WIDE>
-__global__ void k3_encode(const SymT *__restrict__ sym, uint64_t n,
-                          const unsigned long long *__restrict__ ctab, uint32_t win_lo,
-                          uint32_t win_n, uint32_t word_cap, const float *__restrict__ x,
-                          uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
-                          float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
-                          EncStatus st, unsigned *__restrict__ ticket, uint64_t ntiles,
-                          int extract_outliers);
+__global__ void k3_count(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
+                         uint32_t win_lo, uint32_t win_n, uint64_t tiles_per_cta,
+                         unsigned long long *__restrict__ cta_bits, unsigned long long *__restrict__ cta_nz);
+template <typename SymT, bool WIDE>
+__global__ void k3_pack(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
+                        uint32_t win_lo, uint32_t win_n, uint32_t word_cap, uint64_t tiles_per_cta,
+                        const float *__restrict__ x, const unsigned long long *__restrict__ cta_bit0,
+                        const unsigned long long *__restrict__ cta_nz0, uint32_t *__restrict__ payload,
+                        unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
+                        unsigned long long *__restrict__ chunk_off, uint32_t *__restrict__ head,
+                        uint32_t *__restrict__ tail, int extract_outliers);
+__global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
+                         const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
+                         const uint32_t *__restrict__ tail, uint32_t ncta);
 
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
                             uint32_t *__restrict__ lut);
@@ -110,6 +122,8 @@ struct DecodeArgs {
   const uint32_t *payload;
   uint64_t payload_bits;
   const unsigned long long *chunk_off;
+  const long long *chunk_lat;  // lattice value before every chunk (warp decoder)
+  uint32_t live;               // number of codes (canon length)
   void *out;  // f32 / f64 values or u32 symbols
   DecStatus st;
   unsigned *ticket;
@@ -122,6 +136,8 @@ struct DecodeArgs {
 // SW: staging width of decoded symbols in shared memory (16 or 32 bits)
 template <int MODE, int SW>
 __global__ void k4_decode(DecodeArgs a);
+template <int MODE, int SW>
+__global__ void k4w_decode(DecodeArgs a);
 __global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
                                 unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
 

@@ -148,6 +148,7 @@ def huffman_decode(lengths, payload: bytes, bit_length: int, count: int) -> np.n
     d.payload_dev = pd.data_ptr()
     d.payload_bits = bit_length
     d.chunk_offsets_dev = None
+    d.chunk_lat_dev = None
     ctx = _lib.context()
     sh, s = _lib.stream_handle()
     nchunks = (count + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK

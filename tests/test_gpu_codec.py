@@ -175,3 +175,20 @@ def test_small_eb_outlier_heavy_vs_oracle(oracle, eb):
     assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
     out32, _ = pb.decompress_device(c, dtype=torch.float32)
     assert np.array_equal(out32.cpu().numpy().reshape(-1), want.astype(np.float32))
+
+
+def test_compress_batch_matches_single(oracle):
+    rng = np.random.default_rng(17)
+    xs, ps = [], []
+    for k in range(11):
+        n = int(rng.integers(1, 300000))
+        xs.append(torch.from_numpy(np.maximum(rng.normal(0, 1, n), 0).astype(np.float32)).cuda())
+        ps.append(pb.CodecParams(eb=float(10 ** rng.uniform(-5, -1))))
+    out = pb.compress_batch(xs, ps, max_concurrency=4)
+    for (c, rep), x, p in zip(out, xs, ps):
+        ref = oracle.compress(x.cpu().numpy(), p.eb, debug=False)
+        assert c.to_bytes() == ref.blob
+        assert rep.ratio == ref.ratio
+        back, _ = pb.decompress_device(c, dtype=torch.float64)
+        want = oracle.decompress_blob(ref.blob, x.numel())
+        assert np.array_equal(back.cpu().numpy().view(np.uint64), want.view(np.uint64))
