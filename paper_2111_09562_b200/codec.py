@@ -508,20 +508,28 @@ def compress_batch(xs, params, max_concurrency: int = 8):
             _lib.raise_for(_lib.lib().actc_compress_plan(
                 ctx.handle, C.c_void_p(x.data_ptr()), n, float(p.eb), int(p.radius), flags,
                 C.c_void_p(dev["chunk_lat"].data_ptr()), C.c_void_p(ctx.plan_buf.data_ptr()), sh))
-            jobs.append((i, x, p, s, ctx, sh, dev))
-        for (_, _, _, s, _, _, _) in jobs:
-            s.synchronize()
-        for (i, x, p, s, ctx, sh, dev) in jobs:
-            plan = _lib.Plan.from_buffer_copy(ctx.plan)
-            with torch.cuda.stream(s):
-                c, rep = _finish_compress(x, p, tuple(x.shape) or (1,), plan, dev, ctx, sh)
-            for t in c._dev.values():  # used on both the side and the caller's stream
-                t.record_stream(s)
-                t.record_stream(main)
-            x.record_stream(s)
-            results.append((i, c, rep))
-        for (_, _, _, s, _, _, _) in jobs:
-            main.wait_stream(s)
+            jobs.append((i, x, p, s, ctx, sh, dev, s.record_event()))
+        # launch each tensor's encode as soon as its plan has landed, so
+        # encodes of early tensors overlap the codebooks of later ones
+        pending = list(jobs)
+        while pending:
+            still = []
+            for job in pending:
+                i, x, p, s, ctx, sh, dev, done = job
+                if not done.query():
+                    still.append(job)
+                    continue
+                plan = _lib.Plan.from_buffer_copy(ctx.plan)
+                with torch.cuda.stream(s):
+                    c, rep = _finish_compress(x, p, tuple(x.shape) or (1,), plan, dev, ctx, sh)
+                for t in c._dev.values():  # used on both the side and the caller's stream
+                    t.record_stream(s)
+                    t.record_stream(main)
+                x.record_stream(s)
+                results.append((i, c, rep))
+            pending = still
+        for job in jobs:
+            main.wait_stream(job[3])
     results.sort(key=lambda r: r[0])
     return [(c, rep) for _, c, rep in results]
 

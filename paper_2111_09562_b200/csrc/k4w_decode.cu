@@ -9,31 +9,28 @@
 //
 // Work unit: one warp owns 32 consecutive chunks (8192 symbols), lane l
 // decodes chunk l.  Per round each lane decodes 64 symbols of its chunk into
-// a 4 KB per-warp shared buffer (u16 pairs, rows padded to 33 words so lane
-// stores and row reads are bank-conflict free); then the warp walks the 32
-// rows: a warp inclusive scan of the deltas plus the chunk's running lattice
-// value gives 64 consecutive lattice values, reconstructed in fp64 and
-// stored coalesced (256 B / 512 B per warp store).  No block barriers, no
-// look-back: chunk start values come from the index, so warps run free.
+// a per-warp shared buffer (u16 pairs, rows padded to 33 words: conflict-free
+// lane stores and row reads); then the warp walks the 32 rows: a warp scan of
+// the deltas plus the chunk's running lattice value gives 64 consecutive
+// lattice values, reconstructed in fp64 and stored coalesced.  No block
+// barriers, no look-back: chunk start values come from the index.
+//
+// Decode step (uniform across the warp): a 12-bit LUT gives (symbol, length)
+// for codes <= 12 bits and a starting length l0 for longer prefixes; the
+// length is finished with up to three predicated comparisons against the
+// left-aligned canonical limits (skipped by warp vote when no lane needs
+// them), the symbol of a long code comes from canon[off[l] + (W >> (32-l))]
+// (shared-memory cache of the first codes in canonical order).
 #include "kernels.cuh"
 
 namespace actc {
 
 namespace {
 
-constexpr int ROUND = 64;                  // symbols per lane per round
-constexpr int ROW16 = ROUND / 2 + 1;       // words per row, u16 symbols
-constexpr int ROW32 = ROUND + 1;           // words per row, u32 symbols
+constexpr int ROUND = 64;             // symbols per lane per round
+constexpr int ROW16 = ROUND / 2 + 1;  // words per row, u16 symbols
+constexpr int ROW32 = ROUND + 1;      // words per row, u32 symbols
 constexpr int NW4 = K4W_THREADS / 32;
-
-struct Tables {
-  unsigned long long first[64];
-  unsigned long long lim[64];
-  uint32_t count[64];
-  uint32_t base[64];
-  uint32_t maxlen;
-  uint32_t n_short;  // number of codes with length <= kLutBits (canon index of the first long code)
-};
 
 __device__ __forceinline__ uint64_t read_bits64(const uint32_t *__restrict__ pw, uint64_t pos) {
   uint64_t wi = pos >> 5;
@@ -44,19 +41,33 @@ __device__ __forceinline__ uint64_t read_bits64(const uint32_t *__restrict__ pw,
   return (hi << sh) | ((uint64_t)lo >> (32 - sh));
 }
 
-// reference first-match rule from memory (over-subscribed tables, codes > 32 bits)
-__device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint64_t pos, const Tables &t,
-                                           const uint32_t *__restrict__ canon, uint32_t &sym) {
-  uint64_t win = read_bits64(pw, pos);
-  for (int l = kLutBits + 1; l <= (int)t.maxlen; l++) {
-    unsigned long long code = win >> (64 - l);
-    unsigned long long off = code - t.first[l];
-    if (off < t.count[l]) {
-      sym = canon[t.base[l] + off];
-      return l;
-    }
-  }
-  return 0;
+// 32-bit shared-window addressing: the tables and row buffers are addressed
+// through addresses computed once, so the compiler does not rematerialise the
+// shared window base (S2R SR_CgaCtaId + LEA) on every access.
+__device__ __forceinline__ uint32_t saddr(const void *p) {
+  // the opaque mov keeps the address in a register (otherwise the compiler
+  // recomputes it from SR_CgaCtaId at every use inside the decode loop)
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_row(uint32_t a) {  // row buffer: ordered w.r.t. the stores
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_row(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 }  // namespace
@@ -64,8 +75,12 @@ __device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint
 template <int MODE, int SW>
 __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
   __shared__ uint32_t lut[kLutSize];
-  __shared__ uint16_t ccache[K4W_CANON_CACHE];  // canon[n_short ...], the most frequent long codes
-  __shared__ Tables t;
+  __shared__ uint16_t ccache[K4W_CANON_CACHE];  // canon[0 .. ncache): the most frequent codes
+  __shared__ uint32_t s_limm1[64];              // ((first+count) << (32-l)) - 1, saturated
+  __shared__ int32_t s_off[64];                 // base[l] - first[l]
+  __shared__ unsigned long long s_first[64];    // for the reference-rule fallback
+  __shared__ uint32_t s_count[64], s_base[64];
+  __shared__ uint32_t s_maxlen;
   extern __shared__ __align__(16) uint32_t wbuf_all[];  // NW4 * 32 rows
   constexpr int ROW = SW == 16 ? ROW16 : ROW32;
 
@@ -74,34 +89,40 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
     reinterpret_cast<uint4 *>(lut)[i] = reinterpret_cast<const uint4 *>(a.lut)[i];
   if (tid == 0) {
     unsigned long long code = 0;
-    uint32_t idx = 0, mx = 0, ns = 0;
+    uint32_t idx = 0, mx = 0;
     for (int l = 0; l < 64; l++) {
       code <<= 1;
-      uint32_t c = a.len_counts[l];
-      t.first[l] = code;
-      t.count[l] = c;
-      t.base[l] = idx;
-      t.lim[l] = l <= 32 ? (code + c) << (32 - l) : 0;
+      const uint32_t c = a.len_counts[l];
+      s_first[l] = code;
+      s_count[l] = c;
+      s_base[l] = idx;
+      if (l >= 1 && l <= 32) {
+        const unsigned long long lim = (code + c) << (32 - l);
+        s_limm1[l] = lim == 0 ? 0u : (uint32_t)min(lim - 1, 0xFFFFFFFFull);
+        s_off[l] = (int32_t)idx - (int32_t)(uint32_t)code;
+      } else {
+        s_limm1[l] = 0xFFFFFFFFu;
+        s_off[l] = 0;
+      }
       code += c;
       idx += c;
       if (c && l > 0) mx = l;
-      if (l <= kLutBits) ns = idx;
     }
-    t.maxlen = mx;
-    t.n_short = ns;
+    s_maxlen = mx;
   }
-  __syncthreads();
-  const uint32_t n_short = t.n_short;
-  const uint32_t ncache = SW == 16 ? (uint32_t)min((long long)K4W_CANON_CACHE, (long long)a.live - (long long)n_short) : 0u;
-  for (uint32_t i = tid; i < ncache; i += K4W_THREADS) ccache[i] = (uint16_t)a.canon[n_short + i];
+  const uint32_t ncache = SW == 16 ? min((uint32_t)K4W_CANON_CACHE, a.live) : 0u;
+  for (uint32_t i = tid; i < ncache; i += K4W_THREADS) ccache[i] = (uint16_t)a.canon[i];
   __syncthreads();
 
   const bool fast_long = a.lut[kLutSize] != 0;
+  const int maxlen = (int)s_maxlen;
   const uint64_t nchunks = (a.n + ACTC_CHUNK - 1) / ACTC_CHUNK;
   const uint64_t nwt = (nchunks + 31) / 32;
   const long long radius = a.radius;
-  uint32_t *rows = wbuf_all + warp * 32 * ROW;
-  uint32_t *myrow = rows + lane * ROW;
+  const uint32_t rbase = saddr(wbuf_all) + 4u * (warp * 32 * ROW);  // this warp's rows
+  const uint32_t mbase = rbase + 4u * (lane * ROW);                    // my row
+  const uint32_t lut_s = saddr(lut), lim_s = saddr(s_limm1), off_s = saddr(s_off), cc_s = saddr(ccache);
+  const uint32_t *__restrict__ pw = a.payload;
   unsigned long long nonzero = 0, markers = 0;
   bool bad = false;
 
@@ -110,28 +131,28 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
     const bool valid = c < nchunks;
     const uint64_t e0 = c * ACTC_CHUNK;
     const uint32_t cnt = valid ? (uint32_t)min((uint64_t)ACTC_CHUNK, a.n - e0) : 0u;
-    uint64_t pos = 0, endp = 0;
-    const uint32_t *pw = a.payload;
-    uint64_t wi = 0;
+    // a full warp tile: 32 complete chunks, no bounds checks in the row loop
+    const bool full_tile = (wt + 1) * 32 * ACTC_CHUNK <= a.n;
+    uint64_t endp = 0;
+    const uint32_t *__restrict__ src = pw;  // next word to load into nextw
     unsigned long long buf = 0;
     int nb = 0;
     uint32_t nextw = 0;
-    long long P = 0;       // running lattice value of my chunk
-    uint32_t ordn = 0;     // ordinal of my chunk's next outlier
+    long long P = 0;    // running lattice value of my chunk
+    uint32_t ordn = 0;  // ordinal of my chunk's next outlier
     bool ord_known = false;
     if (valid) {
-      pos = a.chunk_off[c];
+      const uint64_t pos = a.chunk_off[c];
       endp = (c + 1 < nchunks) ? a.chunk_off[c + 1] : a.payload_bits;
-      wi = pos >> 5;
-      // pull the chunk's bitstream lines towards L1 while the first words load
-      const char *lp = reinterpret_cast<const char *>(pw + wi);
+      src = pw + (pos >> 5);
+      const char *lp = reinterpret_cast<const char *>(src);
       for (uint64_t off = 128; off < ((endp - pos) >> 3) + 16; off += 128)
         asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + off));
-      buf = ((unsigned long long)bswap32(pw[wi]) << 32) | bswap32(pw[wi + 1]);
+      buf = ((unsigned long long)bswap32(__ldg(src)) << 32) | bswap32(__ldg(src + 1));
       buf <<= (pos & 31);
       nb = 64 - (int)(pos & 31);
-      wi += 2;
-      nextw = bswap32(pw[wi++]);
+      nextw = bswap32(__ldg(src + 2));
+      src += 3;
       if (MODE != 2) P = a.chunk_lat[c];
     }
     for (int r = 0; r * ROUND < ACTC_CHUNK; r++) {
@@ -139,70 +160,76 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
       const uint32_t i0 = r * ROUND;
       const uint32_t iend = max(i0, min(cnt, i0 + ROUND));  // empty once the chunk is exhausted
       uint32_t zr = 0;
-      // One symbol, straight-line: 12-bit LUT hit, else the LUT gives the
-      // first candidate length l0 and up to 4 predicated limit steps finish it
-      // (uniform instruction stream across the warp); anything rarer takes the
-      // divergent fallback.
-#define ACTC_DEC(SYM)                                                                                  \
-  {                                                                                                    \
-    if (nb < 32) {                                                                                     \
-      buf |= (unsigned long long)nextw << (32 - nb);                                                   \
-      nb += 32;                                                                                        \
-      nextw = bswap32(pw[wi++]);                                                                       \
-    }                                                                                                  \
-    const uint32_t W = (uint32_t)(buf >> 32);                                                          \
-    const uint32_t e = lut[W >> (32 - kLutBits)];                                                      \
-    int len = e & 63;                                                                                  \
-    uint32_t sv = e >> 6;                                                                              \
-    if (len == 0) {                                                                                    \
-      int l = (int)sv;                                                                                 \
-      if (fast_long && l) {                                                                            \
-        l += (unsigned long long)W >= t.lim[l];                                                        \
-        l += (unsigned long long)W >= t.lim[l];                                                        \
-        l += (unsigned long long)W >= t.lim[l];                                                        \
-        while (l <= (int)t.maxlen && (unsigned long long)W >= t.lim[l]) l++;                            \
-        if (l <= (int)t.maxlen) {                                                                      \
-          const uint32_t ci = t.base[l] + ((W >> (32 - l)) - (uint32_t)t.first[l]);                    \
-          sv = (ci - n_short < ncache) ? (uint32_t)ccache[ci - n_short] : __ldg(&a.canon[ci]);          \
-          len = l;                                                                                     \
-        }                                                                                              \
-      }                                                                                                \
-      if (len == 0) {                                                                                  \
-        const uint64_t pos = (wi << 5) - 32 - (uint64_t)nb;                                            \
-        len = slow_decode(pw, pos, t, a.canon, sv);                                                    \
-        if (!len) {                                                                                    \
-          bad = true;                                                                                  \
-          len = 1;                                                                                     \
-          sv = a.radius;                                                                               \
-        }                                                                                              \
-        const uint64_t np = pos + len;                                                                 \
-        wi = np >> 5;                                                                                  \
-        buf = ((unsigned long long)bswap32(pw[wi]) << 32) | bswap32(pw[wi + 1]);                       \
-        buf <<= (np & 31);                                                                             \
-        nb = 64 - (int)(np & 31);                                                                      \
-        wi += 2;                                                                                       \
-        nextw = bswap32(pw[wi++]);                                                                     \
-        len = 0;                                                                                       \
-      }                                                                                                \
-    }                                                                                                  \
-    buf <<= len;                                                                                       \
-    nb -= len;                                                                                         \
-    SYM = sv;                                                                                          \
+#define ACTC_DEC(SYM)                                                                             \
+  {                                                                                               \
+    if (nb < 32) {                                                                                \
+      buf |= (unsigned long long)nextw << (32 - nb);                                              \
+      nb += 32;                                                                                   \
+      nextw = bswap32(__ldg(src));                                                                \
+      ++src;                                                                                      \
+    }                                                                                             \
+    const uint32_t W = (uint32_t)(buf >> 32);                                                     \
+    const uint32_t e = lds_u32(lut_s + ((W >> (32 - kLutBits)) << 2));                            \
+    int len = e & 63;                                                                             \
+    uint32_t sv = e >> 6;                                                                         \
+    if (__any_sync(__activemask(), len == 0)) {                                                   \
+      if (len == 0) {                                                                             \
+        /* long code: LUT gave l0; four independent limit probes finish it */                     \
+        const int l0 = (int)sv;                                                                   \
+        const uint32_t lb = lim_s + 4u * l0;                                                      \
+        const int c0 = W > lds_u32(lb), c1 = W > lds_u32(lb + 4u), c2 = W > lds_u32(lb + 8u);     \
+        const bool c3 = W > lds_u32(lb + 12u);                                                    \
+        const int l = l0 + c0 + c1 + c2;                                                          \
+        if (fast_long && l0 >= 1 && !c3 && l <= maxlen) {                                         \
+          const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                          \
+          sv = ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]);                       \
+          len = l;                                                                                \
+        } else {                                                                                  \
+          /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */        \
+          const uint64_t pos = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;                   \
+          const uint64_t win = read_bits64(pw, pos);                                              \
+          for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                       \
+            const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                \
+            if (of < s_count[ll]) {                                                               \
+              sv = a.canon[s_base[ll] + of];                                                      \
+              len = ll;                                                                           \
+              break;                                                                              \
+            }                                                                                     \
+          }                                                                                       \
+          if (!len) {                                                                             \
+            bad = true;                                                                           \
+            len = 1;                                                                              \
+            sv = a.radius;                                                                        \
+          }                                                                                       \
+          const uint64_t np = pos + len;                                                          \
+          src = pw + (np >> 5);                                                                   \
+          buf = ((unsigned long long)bswap32(src[0]) << 32) | bswap32(src[1]);                    \
+          buf <<= (np & 31);                                                                      \
+          nb = 64 - (int)(np & 31);                                                               \
+          nextw = bswap32(src[2]);                                                                \
+          src += 3;                                                                               \
+          len = 0;                                                                                \
+        }                                                                                         \
+      }                                                                                           \
+    }                                                                                             \
+    buf <<= len;                                                                                  \
+    nb -= len;                                                                                    \
+    SYM = sv;                                                                                     \
   }
-#define ACTC_ZERO(SYM, IDX)                                                                            \
-  if (MODE != 2 && SYM == 0) {                                                                         \
-    if (!ord_known) {                                                                                  \
-      uint64_t lo = 0, hi = a.k;                                                                       \
-      while (lo < hi) {                                                                                \
-        uint64_t mid = (lo + hi) >> 1;                                                                 \
-        if (a.out_idx[mid] < e0) lo = mid + 1; else hi = mid;                                          \
-      }                                                                                                \
-      ordn = (uint32_t)lo;                                                                             \
-      ord_known = true;                                                                                \
-    }                                                                                                  \
-    if (ordn >= a.k || a.out_idx[ordn] != e0 + (IDX)) bad = true;                                      \
-    ordn++;                                                                                            \
-    zr++;                                                                                              \
+#define ACTC_ZERO(SYM, IDX)                                                                       \
+  if (MODE != 2 && SYM == 0) {                                                                    \
+    if (!ord_known) {                                                                             \
+      uint64_t lo = 0, hi = a.k;                                                                  \
+      while (lo < hi) {                                                                           \
+        uint64_t mid = (lo + hi) >> 1;                                                            \
+        if (a.out_idx[mid] < e0) lo = mid + 1; else hi = mid;                                     \
+      }                                                                                           \
+      ordn = (uint32_t)lo;                                                                        \
+      ord_known = true;                                                                           \
+    }                                                                                             \
+    if (ordn >= a.k || a.out_idx[ordn] != e0 + (IDX)) bad = true;                                 \
+    ordn++;                                                                                       \
+    zr++;                                                                                         \
   }
       uint32_t i = i0;
       for (; i + 1 < iend; i += 2) {
@@ -212,10 +239,10 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
         ACTC_ZERO(sa, i)
         ACTC_ZERO(sb, i + 1)
         if (SW == 32) {
-          myrow[i - i0] = sa;
-          myrow[i - i0 + 1] = sb;
+          sts_row(mbase + 4u * (i - i0), sa);
+          sts_row(mbase + 4u * (i - i0 + 1), sb);
         } else {
-          myrow[(i - i0) >> 1] = sa | (sb << 16);
+          sts_row(mbase + 4u * ((i - i0) >> 1), sa | (sb << 16));
         }
       }
       if (i < iend) {
@@ -223,106 +250,132 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
         ACTC_DEC(sa)
         ACTC_ZERO(sa, i)
         if (SW == 32)
-          myrow[i - i0] = sa;
+          sts_row(mbase + 4u * (i - i0), sa);
         else
-          myrow[(i - i0) >> 1] = sa;
+          sts_row(mbase + 4u * ((i - i0) >> 1), sa);
       }
 #undef ACTC_DEC
 #undef ACTC_ZERO
       markers += zr;
-      // ordinal of my first outlier in this round (valid whenever zr > 0)
-      const uint32_t ordr = ordn - zr;
+      const uint32_t ordr = ordn - zr;  // ordinal of my first outlier in this round (if zr > 0)
       __syncwarp();
       const unsigned zmask = __ballot_sync(0xffffffffu, zr != 0);
 
       // ---------------- reconstruct row by row (coalesced) ----------------
-      for (int cc = 0; cc < 32; cc++) {
-        const uint64_t ch = wt * 32 + cc;
-        if (ch >= nchunks) break;
-        const uint32_t ccnt = (uint32_t)min((uint64_t)ACTC_CHUNK, a.n - ch * ACTC_CHUNK);
-        if (i0 >= ccnt) continue;
-        const uint32_t k0 = i0 + 2 * lane;  // element index inside the chunk
-        const bool v0 = k0 < ccnt, v1 = k0 + 1 < ccnt;
-        uint32_t s0, s1;
-        const uint32_t *row = rows + cc * ROW;
-        if (SW == 16) {
-          const uint32_t w = row[lane];
-          s0 = w & 0xFFFFu;
-          s1 = w >> 16;
-        } else {
-          s0 = row[2 * lane];
-          s1 = row[2 * lane + 1];
-        }
-        const uint64_t eg = ch * ACTC_CHUNK + k0;  // global element index
-        if (MODE == 2) {
-          uint32_t *out = reinterpret_cast<uint32_t *>(a.out) + eg;
-          if (v1)
-            *reinterpret_cast<uint2 *>(out) = make_uint2(s0, s1);
-          else if (v0)
-            *out = s0;
-          continue;
-        }
-        const long long Pc = __shfl_sync(0xffffffffu, P, cc);
-        long long L0, L1, Pn;
-        bool z0 = false, z1 = false;
-        uint32_t o0 = 0, o1 = 0;
-        if (SW == 16 && !((zmask >> cc) & 1u)) {
-          const int d0 = v0 ? (int)s0 - (int)radius : 0;
-          const int d1 = v1 ? (int)s1 - (int)radius : 0;
+      if (MODE != 2 && SW == 16 && full_tile && zmask == 0) {
+        // fast path: 32 complete chunks, no outliers in this round
+        for (int cc = 0; cc < 32; cc++) {
+          const uint32_t w = lds_row(rbase + 4u * (cc * ROW + lane));
+          const int d0 = (int)(w & 0xFFFFu) - (int)radius;
+          const int d1 = (int)(w >> 16) - (int)radius;
           const int inc = warp_incl_sum(d0 + d1);
-          L0 = Pc + (inc - d1);
-          L1 = L0 + d1;
-          Pn = Pc + __shfl_sync(0xffffffffu, inc, 31);
-        } else {
-          z0 = v0 && s0 == 0;
-          z1 = v1 && s1 == 0;
-          const int nzl = (int)z0 + (int)z1;
-          const int zi = warp_incl_sum(nzl);
-          o0 = __shfl_sync(0xffffffffu, ordr, cc) + (uint32_t)(zi - nzl);
-          o1 = o0 + (uint32_t)z0;
-          bool dummy;
-          const Seg e0s = z0 ? Seg{quant_exact((double)a.out_val[o0], a.two_eb, a.eb, dummy), 1}
-                             : Seg{v0 ? (long long)s0 - radius : 0, 0};
-          const Seg e1s = z1 ? Seg{quant_exact((double)a.out_val[o1], a.two_eb, a.eb, dummy), 1}
-                             : Seg{v1 ? (long long)s1 - radius : 0, 0};
-          const Seg inc = warp_incl_seg(seg_combine(e0s, e1s));
-          const long long pv = __shfl_up_sync(0xffffffffu, inc.v, 1);
-          const int pr = __shfl_up_sync(0xffffffffu, inc.r, 1);
-          const Seg ex = lane ? Seg{pv, pr} : Seg{0, 0};
-          const Seg a0 = seg_combine(ex, e0s);
-          const Seg a1 = seg_combine(a0, e1s);
-          L0 = a0.r ? a0.v : Pc + a0.v;
-          L1 = a1.r ? a1.v : Pc + a1.v;
-          const long long tv = __shfl_sync(0xffffffffu, inc.v, 31);
-          const int tr = __shfl_sync(0xffffffffu, inc.r, 31);
-          Pn = tr ? tv : Pc + tv;
+          const int tot = __shfl_sync(0xffffffffu, inc, 31);
+          const long long Pc = __shfl_sync(0xffffffffu, P, cc);
+          const long long L0 = Pc + (inc - d1);
+          const long long L1 = L0 + d1;
+          if (lane == cc) P = Pc + tot;
+          double r0 = __dmul_rn((double)L0, a.two_eb);
+          double r1 = __dmul_rn((double)L1, a.two_eb);
+          if (a.preserve) {
+            r0 = fabs(r0) <= a.eb ? 0.0 : r0;
+            r1 = fabs(r1) <= a.eb ? 0.0 : r1;
+          }
+          nonzero += (r0 != 0.0) + (r1 != 0.0);
+          const uint64_t eg = (wt * 32 + cc) * ACTC_CHUNK + i0 + 2 * lane;
+          if (MODE == 0)
+            __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.out) + eg),
+                   make_float2((float)r0, (float)r1));
+          else
+            __stcs(reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.out) + eg), make_double2(r0, r1));
         }
-        if (lane == cc) P = Pn;
-        double r0 = z0 ? (double)a.out_val[o0] : __dmul_rn((double)L0, a.two_eb);
-        double r1 = z1 ? (double)a.out_val[o1] : __dmul_rn((double)L1, a.two_eb);
-        if (a.preserve) {
-          if (fabs(r0) <= a.eb) r0 = 0.0;
-          if (fabs(r1) <= a.eb) r1 = 0.0;
-        }
-        nonzero += (v0 && r0 != 0.0) + (v1 && r1 != 0.0);
-        if (MODE == 0) {
-          float *out = reinterpret_cast<float *>(a.out) + eg;
-          if (v1)
-            __stcs(reinterpret_cast<float2 *>(out), make_float2((float)r0, (float)r1));
-          else if (v0)
-            *out = (float)r0;
-        } else {
-          double *out = reinterpret_cast<double *>(a.out) + eg;
-          if (v1)
-            __stcs(reinterpret_cast<double2 *>(out), make_double2(r0, r1));
-          else if (v0)
-            *out = r0;
+      } else {
+        for (int cc = 0; cc < 32; cc++) {
+          const uint64_t ch = wt * 32 + cc;
+          if (ch >= nchunks) break;
+          const uint32_t ccnt = (uint32_t)min((uint64_t)ACTC_CHUNK, a.n - ch * ACTC_CHUNK);
+          if (i0 >= ccnt) continue;
+          const uint32_t k0 = i0 + 2 * lane;  // element index inside the chunk
+          const bool v0 = k0 < ccnt, v1 = k0 + 1 < ccnt;
+          uint32_t s0, s1;
+          if (SW == 16) {
+            const uint32_t w = lds_row(rbase + 4u * (cc * ROW + lane));
+            s0 = w & 0xFFFFu;
+            s1 = w >> 16;
+          } else {
+            s0 = lds_row(rbase + 4u * (cc * ROW + 2 * lane));
+            s1 = lds_row(rbase + 4u * (cc * ROW + 2 * lane + 1));
+          }
+          const uint64_t eg = ch * ACTC_CHUNK + k0;  // global element index
+          if (MODE == 2) {
+            uint32_t *out = reinterpret_cast<uint32_t *>(a.out) + eg;
+            if (v1)
+              *reinterpret_cast<uint2 *>(out) = make_uint2(s0, s1);
+            else if (v0)
+              *out = s0;
+            continue;
+          }
+          const long long Pc = __shfl_sync(0xffffffffu, P, cc);
+          long long L0, L1, Pn;
+          bool z0 = false, z1 = false;
+          uint32_t o0 = 0, o1 = 0;
+          if (SW == 16 && !((zmask >> cc) & 1u)) {
+            const int d0 = v0 ? (int)s0 - (int)radius : 0;
+            const int d1 = v1 ? (int)s1 - (int)radius : 0;
+            const int inc = warp_incl_sum(d0 + d1);
+            L0 = Pc + (inc - d1);
+            L1 = L0 + d1;
+            Pn = Pc + __shfl_sync(0xffffffffu, inc, 31);
+          } else {
+            z0 = v0 && s0 == 0;
+            z1 = v1 && s1 == 0;
+            const int nzl = (int)z0 + (int)z1;
+            const int zi = warp_incl_sum(nzl);
+            o0 = __shfl_sync(0xffffffffu, ordr, cc) + (uint32_t)(zi - nzl);
+            o1 = o0 + (uint32_t)z0;
+            bool dummy;
+            const Seg e0s = z0 ? Seg{quant_exact((double)a.out_val[o0], a.two_eb, a.eb, dummy), 1}
+                               : Seg{v0 ? (long long)s0 - radius : 0, 0};
+            const Seg e1s = z1 ? Seg{quant_exact((double)a.out_val[o1], a.two_eb, a.eb, dummy), 1}
+                               : Seg{v1 ? (long long)s1 - radius : 0, 0};
+            const Seg inc = warp_incl_seg(seg_combine(e0s, e1s));
+            const long long pv = __shfl_up_sync(0xffffffffu, inc.v, 1);
+            const int pr = __shfl_up_sync(0xffffffffu, inc.r, 1);
+            const Seg ex = lane ? Seg{pv, pr} : Seg{0, 0};
+            const Seg a0 = seg_combine(ex, e0s);
+            const Seg a1 = seg_combine(a0, e1s);
+            L0 = a0.r ? a0.v : Pc + a0.v;
+            L1 = a1.r ? a1.v : Pc + a1.v;
+            const long long tv = __shfl_sync(0xffffffffu, inc.v, 31);
+            const int tr = __shfl_sync(0xffffffffu, inc.r, 31);
+            Pn = tr ? tv : Pc + tv;
+          }
+          if (lane == cc) P = Pn;
+          double r0 = z0 ? (double)a.out_val[o0] : __dmul_rn((double)L0, a.two_eb);
+          double r1 = z1 ? (double)a.out_val[o1] : __dmul_rn((double)L1, a.two_eb);
+          if (a.preserve) {
+            if (fabs(r0) <= a.eb) r0 = 0.0;
+            if (fabs(r1) <= a.eb) r1 = 0.0;
+          }
+          nonzero += (v0 && r0 != 0.0) + (v1 && r1 != 0.0);
+          if (MODE == 0) {
+            float *out = reinterpret_cast<float *>(a.out) + eg;
+            if (v1)
+              __stcs(reinterpret_cast<float2 *>(out), make_float2((float)r0, (float)r1));
+            else if (v0)
+              *out = (float)r0;
+          } else {
+            double *out = reinterpret_cast<double *>(a.out) + eg;
+            if (v1)
+              __stcs(reinterpret_cast<double2 *>(out), make_double2(r0, r1));
+            else if (v0)
+              *out = r0;
+          }
         }
       }
       __syncwarp();
     }
     if (valid) {
-      const uint64_t pos_end = (wi << 5) - 32 - (uint64_t)nb;
+      const uint64_t pos_end = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;
       if (pos_end != endp || pos_end > a.payload_bits) bad = true;
     }
   }
