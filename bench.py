@@ -309,6 +309,12 @@ def run_gpu(args, rank, world):
         ok = (err <= eb + half_ulp) | ((o == 0) & (t.abs().double() <= 2 * eb))
         assert bool(ok.all()), f"bound violated: {int((~ok).sum())} elements"
 
+    del err, ok, half_ulp
+    torch.cuda.empty_cache()  # drop the gate's fp64 temporaries before timing
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+
     # timed region: per-step events, L2 flushed between steps (untimed)
     if world > 1:
         torch.distributed.barrier()

@@ -318,7 +318,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     win_n = cap;
   }
   const uint32_t maxlen = plan->max_len ? plan->max_len : 1;
-  const uint32_t word_cap = (uint32_t)(((uint64_t)K3_TILE * maxlen + 31) / 32 + 4);
+  const uint32_t word_cap = (uint32_t)(((uint64_t)2 * K3_TILE * maxlen + 31) / 32 + 4);  // pack tile = 2*K3_TILE
   const size_t tbl = (((size_t)win_n * (wide ? 8 : 4) + 15) & ~size_t(15));
   const size_t smem_pack = tbl + (size_t)word_cap * 4;
   // the count pass only needs lengths: a byte per symbol over the whole live range
@@ -431,7 +431,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   if (S.chunk_lat_dev || mode == 2) {
     // warp decoder: no scan, no look-back
     const int NW = K4W_THREADS / 32;
-    const size_t smem = (size_t)NW * 32 * (sw16 ? 33 : 65) * 4;
+    const size_t smem = (size_t)NW * 32 * (sw16 ? 65 : 129) * 4;  // ROUND = 128 rows (+1 pad word)
     const void *f = mode == 0 ? (sw16 ? (const void *)k4w_decode<0, 16> : (const void *)k4w_decode<0, 32>)
                   : mode == 1 ? (sw16 ? (const void *)k4w_decode<1, 16> : (const void *)k4w_decode<1, 32>)
                               : (const void *)k4w_decode<2, 32>;

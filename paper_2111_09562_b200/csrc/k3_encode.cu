@@ -184,6 +184,38 @@ __global__ void __launch_bounds__(K3_THREADS) k3_count(const SymT *__restrict__ 
   }
 }
 
+constexpr int PK_EPT = 2 * K3_EPT;  // symbols per thread per pack tile
+constexpr int PK_TILE = K3_THREADS * PK_EPT;
+
+template <typename SymT>
+__device__ __forceinline__ void load_syms32(const SymT *__restrict__ sym, uint64_t base, uint64_t n,
+                                            uint32_t (&s)[PK_EPT]) {
+  if (base + PK_EPT <= n) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
+    if (sizeof(SymT) == 2) {
+#pragma unroll
+      for (int j = 0; j < PK_EPT / 8; j++) {
+        uint4 v = __ldg(p + j);
+        uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          s[8 * j + 2 * k] = w4[k] & 0xFFFFu;
+          s[8 * j + 2 * k + 1] = w4[k] >> 16;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < PK_EPT / 4; j++) {
+        uint4 v = __ldg(p + j);
+        s[4 * j] = v.x; s[4 * j + 1] = v.y; s[4 * j + 2] = v.z; s[4 * j + 3] = v.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < PK_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : 0xFFFFFFFFu;
+  }
+}
+
 template <typename SymT, bool WIDE>
 __global__ void __launch_bounds__(K3_THREADS) k3_pack(
     const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab, uint32_t win_lo,
@@ -192,6 +224,8 @@ __global__ void __launch_bounds__(K3_THREADS) k3_pack(
     uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
     unsigned long long *__restrict__ chunk_off, uint32_t *__restrict__ head, uint32_t *__restrict__ tail,
     int extract_outliers) {
+  // tiles_per_cta counts K3_TILE units (the count pass's granularity); the
+  // pack pass walks the same symbol range in PK_TILE steps
   extern __shared__ __align__(16) unsigned char smem[];
   using E = typename Ent<WIDE>::T;
   E *sh = reinterpret_cast<E *>(smem);
@@ -202,27 +236,26 @@ __global__ void __launch_bounds__(K3_THREADS) k3_pack(
   load_table<WIDE>(sh, ctab, win_lo, win_n);
   if (tid == 0) s_carry = 0;
   __syncthreads();
-  const uint64_t ntiles = (n + K3_TILE - 1) / K3_TILE;
-  const uint64_t t0 = blockIdx.x * tiles_per_cta, t1 = min(ntiles, t0 + tiles_per_cta);
+  const uint64_t r0 = min(n, blockIdx.x * tiles_per_cta * (uint64_t)K3_TILE);
+  const uint64_t r1 = min(n, (blockIdx.x + 1) * tiles_per_cta * (uint64_t)K3_TILE);
   unsigned long long bit = cta_bit0[blockIdx.x];  // start bit of the current tile
   unsigned long long nzb = cta_nz0[blockIdx.x];
   const unsigned long long cta_start = bit;
-  for (uint64_t tile = t0; tile < t1; tile++) {
-    const uint64_t base = tile * K3_TILE + (uint64_t)tid * K3_EPT;
-    uint32_t s[K3_EPT];
-    load_syms(sym, base, n, s);
-    unsigned long long code[K3_EPT];
-    uint32_t len[K3_EPT];
+  for (uint64_t tb = r0; tb < r1; tb += PK_TILE) {
+    const uint64_t base = tb + (uint64_t)tid * PK_EPT;
+    const uint64_t lim = min(r1, tb + (uint64_t)PK_TILE);
+    uint32_t s[PK_EPT];
+    load_syms32(sym, base, lim, s);
+    // pass 1: lengths (the table lookup is repeated in pass 2 to save registers)
     uint32_t nbits = 0, nz = 0;
 #pragma unroll
-    for (int j = 0; j < K3_EPT; j++) {
-      if (base + j < n) {
-        lookup<WIDE>(sh, ctab, win_lo, win_n, s[j], code[j], len[j]);
-        nbits += len[j];
+    for (int j = 0; j < PK_EPT; j++) {
+      if (s[j] != 0xFFFFFFFFu) {
+        unsigned long long code;
+        uint32_t len;
+        lookup<WIDE>(sh, ctab, win_lo, win_n, s[j], code, len);
+        nbits += len;
         nz += s[j] == 0;
-      } else {
-        len[j] = 0;
-        code[j] = 0;
       }
     }
     unsigned long long tot;
@@ -234,12 +267,13 @@ __global__ void __launch_bounds__(K3_THREADS) k3_pack(
     for (uint32_t i = tid; i < nwords && i < word_cap; i += K3_THREADS) words[i] = 0;
     __syncthreads();
     const unsigned long long my_bit0 = bit + (excl >> 32);
-    if ((base % ACTC_CHUNK) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = my_bit0;
+    // decode chunk index: bit offsets of the ACTC_CHUNK-th symbols this thread starts
+    if ((base % ACTC_CHUNK) == 0 && base < lim) chunk_off[base / ACTC_CHUNK] = my_bit0;
     if (extract_outliers && nz) {
       unsigned long long o = nzb + (excl & 0xFFFFFFFFull);
 #pragma unroll
-      for (int j = 0; j < K3_EPT; j++) {
-        if (base + j < n && s[j] == 0) {
+      for (int j = 0; j < PK_EPT; j++) {
+        if (s[j] == 0) {
           out_idx[o] = base + j;
           out_val[o] = x[base + j];
           o++;
@@ -249,20 +283,22 @@ __global__ void __launch_bounds__(K3_THREADS) k3_pack(
     if (nbits) {
       const uint32_t rel = start_off + (uint32_t)(excl >> 32);
       if (!WIDE) {
-        // codes <= 26 bits: each code completes at most one 32-bit word, so the
-        // accumulator emits with predicated stores; only the thread's first
-        // word (shared with the previous thread) and its final partial word
-        // (shared with the next) are atomic.
+        // codes <= 26 bits complete at most one word each: predicated emits;
+        // only the first (shared with the previous thread) and the final
+        // partial word (shared with the next) are atomic
         uint32_t w = rel >> 5;
         const uint32_t w0 = w;
         int nb = rel & 31;
         unsigned long long acc = 0;
 #pragma unroll
-        for (int j = 0; j < K3_EPT; j++) {
-          const int lj = (int)len[j];
-          const unsigned long long cj = code[j];
-          acc |= lj ? cj << (64 - nb - lj) : 0ull;
-          nb += lj;
+        for (int j = 0; j < PK_EPT; j++) {
+          unsigned long long cj;
+          uint32_t lj;
+          const bool pad = s[j] == 0xFFFFFFFFu;  // past the range end
+          lookup<WIDE>(sh, ctab, win_lo, win_n, pad ? win_lo : s[j], cj, lj);
+          if (pad) lj = 0;
+          acc |= lj ? cj << (64 - nb - (int)lj) : 0ull;
+          nb += (int)lj;
           const bool ready = nb >= 32;
           const uint32_t hiw = (uint32_t)(acc >> 32);
           if (ready && w == w0) atomicOr(&words[w], hiw);
@@ -280,13 +316,16 @@ __global__ void __launch_bounds__(K3_THREADS) k3_pack(
         pk.nb = rel & 31;
         pk.buf = 0;
 #pragma unroll
-        for (int j = 0; j < K3_EPT; j++) {
-          if (!len[j]) continue;
-          if (len[j] > 32) {
-            pk.put((uint32_t)(code[j] >> 32), (int)len[j] - 32);
-            pk.put((uint32_t)code[j], 32);
+        for (int j = 0; j < PK_EPT; j++) {
+          if (s[j] == 0xFFFFFFFFu) continue;
+          unsigned long long cj;
+          uint32_t lj;
+          lookup<WIDE>(sh, ctab, win_lo, win_n, s[j], cj, lj);
+          if (lj > 32) {
+            pk.put((uint32_t)(cj >> 32), (int)lj - 32);
+            pk.put((uint32_t)cj, 32);
           } else {
-            pk.put((uint32_t)code[j], (int)len[j]);
+            pk.put((uint32_t)cj, (int)lj);
           }
         }
         pk.finish();
@@ -295,7 +334,7 @@ __global__ void __launch_bounds__(K3_THREADS) k3_pack(
     __syncthreads();
     // word 0 continues the previous tile's partial word; the CTA's very first
     // word and its final partial word go to the side slots
-    const bool first_tile = tile == t0, last_tile = tile + 1 == t1;
+    const bool first_tile = tb == r0, last_tile = tb + PK_TILE >= r1;
     const uint32_t end_off = (uint32_t)((start_off + tile_bits) & 31);
     if (tid == 0 && !first_tile) words[0] |= s_carry;
     __syncthreads();

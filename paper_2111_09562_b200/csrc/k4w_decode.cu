@@ -27,7 +27,7 @@ namespace actc {
 
 namespace {
 
-constexpr int ROUND = 64;             // symbols per lane per round
+constexpr int ROUND = 128;            // symbols per lane per round
 constexpr int ROW16 = ROUND / 2 + 1;  // words per row, u16 symbols
 constexpr int ROW32 = ROUND + 1;      // words per row, u32 symbols
 constexpr int NW4 = K4W_THREADS / 32;
@@ -73,7 +73,7 @@ __device__ __forceinline__ void sts_row(uint32_t a, uint32_t v) {
 }  // namespace
 
 template <int MODE, int SW>
-__global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
+__global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   __shared__ uint32_t lut[kLutSize];
   __shared__ uint16_t ccache[K4W_CANON_CACHE];  // canon[0 .. ncache): the most frequent codes
   __shared__ uint32_t s_limm1[64];              // ((first+count) << (32-l)) - 1, saturated
@@ -263,30 +263,41 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
 
       // ---------------- reconstruct row by row (coalesced) ----------------
       if (MODE != 2 && SW == 16 && full_tile && zmask == 0) {
-        // fast path: 32 complete chunks, no outliers in this round
+        // fast path: 32 complete chunks, no outliers in this round; lane owns
+        // 4 consecutive elements of each row (ROUND = 128)
         for (int cc = 0; cc < 32; cc++) {
-          const uint32_t w = lds_row(rbase + 4u * (cc * ROW + lane));
-          const int d0 = (int)(w & 0xFFFFu) - (int)radius;
-          const int d1 = (int)(w >> 16) - (int)radius;
-          const int inc = warp_incl_sum(d0 + d1);
+          const uint32_t rw = rbase + 4u * (cc * ROW + 2 * lane);
+          const uint32_t wa = lds_row(rw), wb = lds_row(rw + 4u);
+          const int d0 = (int)(wa & 0xFFFFu) - (int)radius;
+          const int d1 = (int)(wa >> 16) - (int)radius;
+          const int d2 = (int)(wb & 0xFFFFu) - (int)radius;
+          const int d3 = (int)(wb >> 16) - (int)radius;
+          const int p1 = d0 + d1, p2 = p1 + d2, p3 = p2 + d3;
+          const int inc = warp_incl_sum(p3);
           const int tot = __shfl_sync(0xffffffffu, inc, 31);
           const long long Pc = __shfl_sync(0xffffffffu, P, cc);
-          const long long L0 = Pc + (inc - d1);
-          const long long L1 = L0 + d1;
+          const long long B = Pc + (long long)(inc - p3);
           if (lane == cc) P = Pc + tot;
-          double r0 = __dmul_rn((double)L0, a.two_eb);
-          double r1 = __dmul_rn((double)L1, a.two_eb);
+          double r0 = __dmul_rn((double)(B + d0), a.two_eb);
+          double r1 = __dmul_rn((double)(B + p1), a.two_eb);
+          double r2 = __dmul_rn((double)(B + p2), a.two_eb);
+          double r3 = __dmul_rn((double)(B + p3), a.two_eb);
           if (a.preserve) {
             r0 = fabs(r0) <= a.eb ? 0.0 : r0;
             r1 = fabs(r1) <= a.eb ? 0.0 : r1;
+            r2 = fabs(r2) <= a.eb ? 0.0 : r2;
+            r3 = fabs(r3) <= a.eb ? 0.0 : r3;
           }
-          nonzero += (r0 != 0.0) + (r1 != 0.0);
-          const uint64_t eg = (wt * 32 + cc) * ACTC_CHUNK + i0 + 2 * lane;
-          if (MODE == 0)
-            __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.out) + eg),
-                   make_float2((float)r0, (float)r1));
-          else
-            __stcs(reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.out) + eg), make_double2(r0, r1));
+          nonzero += (r0 != 0.0) + (r1 != 0.0) + (r2 != 0.0) + (r3 != 0.0);
+          const uint64_t eg = (wt * 32 + cc) * ACTC_CHUNK + i0 + 4 * lane;
+          if (MODE == 0) {
+            __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.out) + eg),
+                   make_float4((float)r0, (float)r1, (float)r2, (float)r3));
+          } else {
+            double2 *o = reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.out) + eg);
+            __stcs(o, make_double2(r0, r1));
+            __stcs(o + 1, make_double2(r2, r3));
+          }
         }
       } else {
         for (int cc = 0; cc < 32; cc++) {
@@ -294,16 +305,20 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
           if (ch >= nchunks) break;
           const uint32_t ccnt = (uint32_t)min((uint64_t)ACTC_CHUNK, a.n - ch * ACTC_CHUNK);
           if (i0 >= ccnt) continue;
-          const uint32_t k0 = i0 + 2 * lane;  // element index inside the chunk
+          // running outlier ordinal of chunk cc within this round
+          uint32_t ordc = __shfl_sync(0xffffffffu, ordr, cc);
+          for (int h = 0; h < ROUND / 64; h++) {
+          const uint32_t k0 = i0 + 64 * h + 2 * lane;  // element index inside the chunk
+          if (i0 + 64 * h >= ccnt) break;
           const bool v0 = k0 < ccnt, v1 = k0 + 1 < ccnt;
           uint32_t s0, s1;
           if (SW == 16) {
-            const uint32_t w = lds_row(rbase + 4u * (cc * ROW + lane));
+            const uint32_t w = lds_row(rbase + 4u * (cc * ROW + 32 * h + lane));
             s0 = w & 0xFFFFu;
             s1 = w >> 16;
           } else {
-            s0 = lds_row(rbase + 4u * (cc * ROW + 2 * lane));
-            s1 = lds_row(rbase + 4u * (cc * ROW + 2 * lane + 1));
+            s0 = lds_row(rbase + 4u * (cc * ROW + 64 * h + 2 * lane));
+            s1 = lds_row(rbase + 4u * (cc * ROW + 64 * h + 2 * lane + 1));
           }
           const uint64_t eg = ch * ACTC_CHUNK + k0;  // global element index
           if (MODE == 2) {
@@ -330,8 +345,9 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
             z1 = v1 && s1 == 0;
             const int nzl = (int)z0 + (int)z1;
             const int zi = warp_incl_sum(nzl);
-            o0 = __shfl_sync(0xffffffffu, ordr, cc) + (uint32_t)(zi - nzl);
+            o0 = ordc + (uint32_t)(zi - nzl);
             o1 = o0 + (uint32_t)z0;
+            ordc += (uint32_t)__shfl_sync(0xffffffffu, zi, 31);
             bool dummy;
             const Seg e0s = z0 ? Seg{quant_exact((double)a.out_val[o0], a.two_eb, a.eb, dummy), 1}
                                : Seg{v0 ? (long long)s0 - radius : 0, 0};
@@ -369,6 +385,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
               __stcs(reinterpret_cast<double2 *>(out), make_double2(r0, r1));
             else if (v0)
               *out = r0;
+          }
           }
         }
       }
