@@ -40,16 +40,24 @@ __device__ void radix_pass(const unsigned long long *__restrict__ sk, const uint
                            unsigned long long *__restrict__ dk, uint32_t *__restrict__ dv, uint32_t L,
                            int shift, RadixSmem &rs) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t seg = ((L + NWARP - 1) / NWARP + 31) & ~31u;
+  const uint32_t seg = ((L + NWARP - 1) / NWARP + 127) & ~127u;  // multiple of the 4x32 batch
   const uint32_t b0 = min(L, w * seg), b1 = min(L, b0 + seg);
   for (int d = lane; d < 257; d += 32) rs.hist[w][d] = 0;
   __syncwarp();
-  for (uint32_t base = b0; base < b1; base += 32) {
-    uint32_t i = base + lane;
-    uint32_t d = i < b1 ? (uint32_t)((sk[i] >> shift) & 0xFF) : 256u;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (lane == __ffs(peers) - 1) rs.hist[w][d] += __popc(peers);
-    __syncwarp();
+  for (uint32_t base = b0; base < b1; base += 128) {
+    // four independent loads in flight per lane
+    uint32_t d[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t i = base + 32 * u + lane;
+      d[u] = i < b1 ? (uint32_t)((sk[i] >> shift) & 0xFF) : 256u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      unsigned peers = __match_any_sync(0xffffffffu, d[u]);
+      if (lane == __ffs(peers) - 1) rs.hist[w][d[u]] += __popc(peers);
+      __syncwarp();
+    }
   }
   __syncthreads();
   // per digit: exclusive prefix over warps, totals
@@ -83,25 +91,35 @@ __device__ void radix_pass(const unsigned long long *__restrict__ sk, const uint
   __syncthreads();
   for (int d = lane; d < 256; d += 32) rs.hist[w][d] += rs.tot[d];
   __syncwarp();
-  for (uint32_t base = b0; base < b1; base += 32) {
-    uint32_t i = base + lane;
-    unsigned long long k = 0;
-    uint32_t v = 0, d = 256u;
-    if (i < b1) {
-      k = sk[i];
-      v = sv[i];
-      d = (uint32_t)((k >> shift) & 0xFF);
+  for (uint32_t base = b0; base < b1; base += 128) {
+    unsigned long long kk[4];
+    uint32_t vv[4], dd[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t i = base + 32 * u + lane;
+      kk[u] = 0;
+      vv[u] = 0;
+      dd[u] = 256u;
+      if (i < b1) {
+        kk[u] = sk[i];
+        vv[u] = sv[i];
+        dd[u] = (uint32_t)((kk[u] >> shift) & 0xFF);
+      }
     }
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    unsigned lower = peers & ((1u << lane) - 1u);
-    if (d < 256) {
-      uint32_t pos = rs.hist[w][d] + __popc(lower);
-      dk[pos] = k;
-      dv[pos] = v;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t dg = dd[u];
+      unsigned peers = __match_any_sync(0xffffffffu, dg);
+      unsigned lower = peers & ((1u << lane) - 1u);
+      if (dg < 256) {
+        uint32_t pos = rs.hist[w][dg] + __popc(lower);
+        dk[pos] = kk[u];
+        dv[pos] = vv[u];
+      }
+      __syncwarp();
+      if (dg < 256 && lane == __ffs(peers) - 1) rs.hist[w][dg] += __popc(peers);
+      __syncwarp();
     }
-    __syncwarp();
-    if (d < 256 && lane == __ffs(peers) - 1) rs.hist[w][d] += __popc(peers);
-    __syncwarp();
   }
   __syncthreads();
 }
@@ -159,32 +177,60 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   __syncthreads();
 
   // ---- 1. compact live symbols (symbol order) ----
+  // warp w owns a contiguous segment of bins, read coalesced 8 rounds at a
+  // time (all loads in flight); ballot + popc ranks live bins inside a
+  // round.  Pass 1 counts, one scan over the 32 warp counts, pass 2 writes.
   uint64_t L = 0;
   unsigned long long maxf = 0;
-  for (uint64_t c = 0; c < A; c += (uint64_t)K2_THREADS * 8) {
-    uint64_t b0 = c + (uint64_t)tid * 8;
-    unsigned long long f[8];
+  {
+    const int lane = tid & 31, w = tid >> 5;
+    const uint64_t per_w = (((A + NWARP - 1) / NWARP) + 255) & ~uint64_t(255);
+    const uint64_t wb0 = min(A, (uint64_t)w * per_w), wb1 = min(A, wb0 + per_w);
+    const unsigned lt = (1u << lane) - 1u;
     unsigned cnt = 0;
+    for (uint64_t base = wb0; base < wb1; base += 256) {
+      unsigned long long v[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      uint64_t s = b0 + j;
-      unsigned long long v = 0;
-      if (s < A) v = a.in_lengths ? (unsigned long long)a.in_lengths[s] : a.hist[s];
-      f[j] = v;
-      cnt += v != 0;
-      maxf = v > maxf ? v : maxf;
-    }
-    unsigned long long tot;
-    unsigned long long off = block_excl_sum<unsigned long long>(cnt, wbuf, &tot);
+      for (int u = 0; u < 8; u++) {
+        const uint64_t sidx = base + 32 * u + lane;
+        v[u] = sidx < wb1 ? (a.in_lengths ? (unsigned long long)a.in_lengths[sidx] : a.hist[sidx]) : 0ull;
+      }
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      if (f[j]) {
-        a.live_sym[L + off] = (uint32_t)(b0 + j);
-        a.live_freq[L + off] = f[j];
-        off++;
+      for (int u = 0; u < 8; u++) {
+        cnt += __popc(__ballot_sync(0xffffffffu, v[u] != 0));
+        maxf = v[u] > maxf ? v[u] : maxf;
       }
     }
-    L += tot;
+    __shared__ unsigned s_wcnt[NWARP + 1];
+    if (lane == 0) s_wcnt[w] = cnt;
+    __syncthreads();
+    if (w == 0) {
+      const unsigned c = s_wcnt[lane];
+      const unsigned inc = warp_incl_sum(c);
+      s_wcnt[lane] = inc - c;
+      if (lane == 31) s_wcnt[NWARP] = inc;
+    }
+    __syncthreads();
+    unsigned long long off = s_wcnt[w];
+    L = s_wcnt[NWARP];
+    for (uint64_t base = wb0; base < wb1 && cnt; base += 256) {
+      unsigned long long v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint64_t sidx = base + 32 * u + lane;
+        v[u] = sidx < wb1 ? (a.in_lengths ? (unsigned long long)a.in_lengths[sidx] : a.hist[sidx]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const unsigned m = __ballot_sync(0xffffffffu, v[u] != 0);
+        if (v[u]) {
+          const unsigned long long pos = off + __popc(m & lt);
+          a.live_sym[pos] = (uint32_t)(base + 32 * u + lane);
+          a.live_freq[pos] = v[u];
+        }
+        off += __popc(m);
+      }
+    }
   }
   atomicMax(&s_maxf, maxf);
   __syncthreads();
