@@ -432,6 +432,81 @@ def run_gpu(args, rank, world):
     return line
 
 
+def run_training(args, rank, world, batch=256, iters=8, warm=4):
+    """configs[1]: AlexNet b256 training with compressed activations vs the
+    same run uncompressed (images/s, peak memory, per-layer ratio/eb).  W is
+    shortened to 2 for a short run (the reference default is 1000)."""
+    import torch
+    import torchvision
+
+    import paper_2111_09562_b200 as pb
+    from paper_2111_09562_b200.hooks import ActivationCompressor
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = {}
+    for mode in ("baseline", "compressed"):
+        torch.manual_seed(0)
+        m = torchvision.models.alexnet(num_classes=1000).to(dev)
+        opt = torch.optim.SGD(m.parameters(), lr=0.01, momentum=0.9)
+        ddp = m
+        if world > 1:
+            ddp = torch.nn.parallel.DistributedDataParallel(m, device_ids=[dev.index])
+        comp = None
+        if mode == "compressed":
+            comp = ActivationCompressor(ActivationCompressor.conv_layer_map(m), opt,
+                                        pb.ControllerConfig(W_default=2, W_floor=1))
+        g = torch.Generator(device=dev).manual_seed(rank)
+        x = torch.randn(batch, 3, 224, 224, device=dev, generator=g)
+        y = torch.randint(0, 1000, (batch,), device=dev, generator=g)
+
+        def it():
+            opt.zero_grad(set_to_none=True)
+            if comp:
+                with comp.iteration():
+                    torch.nn.functional.cross_entropy(ddp(x), y).backward()
+            else:
+                torch.nn.functional.cross_entropy(ddp(x), y).backward()
+            opt.step()
+            if comp:
+                comp.after_step()
+
+        for _ in range(warm):
+            it()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            it()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        rec = {"images_per_s": world * batch * iters / (ms * 1e-3), "ms_per_iter": ms / iters,
+               "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
+        if comp:
+            last = [r for r in comp.records if r.compressed][-1:]
+            if last:
+                r = last[0]
+                rec["activation_bytes_raw"] = r.raw_bytes
+                rec["activation_bytes_stored"] = r.stored_bytes
+                rec["per_layer"] = {k: {"ratio": v[0], "eb": v[1]} for k, v in r.compressed.items()}
+            rec["W"] = comp.controller.W
+            comp.remove()
+        out[mode] = rec
+        del m, opt, ddp, comp, x, y
+        torch.cuda.empty_cache()
+    out["overhead_pct"] = 100.0 * (out["baseline"]["images_per_s"] / out["compressed"]["images_per_s"] - 1.0)
+    out["config"] = {"model": "alexnet", "batch_per_gpu": batch, "image": "224x224 synthetic", "W": 2,
+                     "optimizer": "SGD momentum 0.9"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -440,6 +515,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="alexnet256")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-train", action="store_true", help="skip the AlexNet training leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -458,6 +534,11 @@ def main():
             line = run_reference(args, rank, world)
         else:
             line = run_gpu(args, rank, world)
+            if not args.no_train and args.workload == "alexnet256":
+                tr = run_training(args, rank, world)
+                if line is not None:
+                    line["training"] = tr
+                    line["train_images_per_s"] = tr["compressed"]["images_per_s"]
         if rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
     finally:

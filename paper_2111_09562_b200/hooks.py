@@ -1,0 +1,336 @@
+"""Per-layer activation compression hooks for PyTorch training.
+
+Mirrors the reference's hook API and storage policy
+(/root/reference/pkg/src/actcomp/training.py):
+
+* `ActivationStore` -- per-layer slots RAW / COMPRESSED / MARKER with byte
+  accounting, put-once / pop-once (LifecycleError), training.py:105-138.
+* `ActivationCompressor` -- the train() hook sites (training.py:259-299
+  compress after forward, :335-353 lazy decompress in backward, :351-361
+  statistics, :381-418 interval boundary) re-expressed for autograd:
+  `torch.autograd.graph.saved_tensors_hooks` pack/unpack.  What autograd
+  saves for a conv layer is its (post-ReLU) output, which the next layer's
+  backward consumes; pack hands it to the GPU codec at the layer's current
+  error bound, unpack reconstructs it (fp32, on device).
+
+Policy, as in the reference:
+* no compression during the first interval (W iterations) -- there is no
+  plan yet (training.py:265-266);
+* every W iterations the collection iteration measures R (nonzero ratio of
+  the stored, i.e. decompressed, activation), L_bar (per-sample max of the
+  loss gradient at the consumer's output, un-averaged) and M_avg (mean |v|
+  of the consumer's momentum) and asks the controller for the next plan;
+* layers whose eb is None (skip set) stay raw.
+
+Packing is batched: pack hooks queue activations and `compress_batch`
+compresses the queue with one host synchronisation (concurrent codebooks).
+Under data parallelism the statistics are averaged across ranks before
+planning, so every rank compresses with identical error bounds.
+"""
+from __future__ import annotations
+
+import contextlib
+from dataclasses import dataclass, field
+
+from . import _lib
+from .codec import DEFAULT_RADIUS, CodecParams, compress_batch, decompress_device
+from .controller import AdaptiveController, ControllerConfig, LayerTrainingStats
+from .errors import LifecycleError, ParameterError
+
+
+class ActivationStore:
+    """Per-layer slots (reference training.py:105-138)."""
+
+    RAW = "raw"
+    COMPRESSED = "compressed"
+    MARKER = "marker"
+
+    def __init__(self):
+        self._slots: dict[str, tuple[str, object, int]] = {}
+        self.current_bytes = 0
+        self.peak_bytes = 0
+
+    def put(self, layer_id: str, kind: str, payload, nbytes: int):
+        if layer_id in self._slots:
+            raise LifecycleError(f"slot {layer_id!r} already filled")
+        self._slots[layer_id] = (kind, payload, nbytes)
+        self.current_bytes += nbytes
+        self.peak_bytes = max(self.peak_bytes, self.current_bytes)
+
+    def pop(self, layer_id: str):
+        entry = self._slots.pop(layer_id, None)
+        if entry is None:
+            raise LifecycleError(f"slot {layer_id!r} missing or already consumed")
+        self.current_bytes -= entry[2]
+        return entry
+
+    def clear(self):
+        self._slots.clear()
+        self.current_bytes = 0
+
+    def __contains__(self, layer_id: str) -> bool:
+        return layer_id in self._slots
+
+
+def _key(t):
+    return (t.data_ptr(), t._version, tuple(t.shape), tuple(t.stride()))
+
+
+class _Handle:
+    """One saved activation: raw until the pending queue is flushed."""
+
+    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape")
+
+    def __init__(self, t, layer, eb):
+        self.layer = layer
+        self.eb = eb
+        self.raw = t
+        self.comp = None
+        self.report = None
+        self.packs = 1
+        self.unpacks = 0
+        self.out = None
+        self.shape = tuple(t.shape)
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    compressed: dict = field(default_factory=dict)  # layer -> (ratio, eb)
+    stored_bytes: int = 0
+    raw_bytes: int = 0
+
+
+class ActivationCompressor:
+    """Adaptive activation compression for a PyTorch model.
+
+    layers: {layer_id: (producer_module, consumer_module)} -- the producer's
+    forward output is the stored activation (e.g. the ReLU after a conv), the
+    consumer is the next parameterised layer whose momentum and output
+    gradient set the error bound.  `conv_layer_map` builds this map
+    for conv nets (conv -> relu -> ... -> next conv/linear).
+    """
+
+    def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
+                 preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 8, dist_group=None,
+                 sync_stats: bool = True):
+        self.layers = dict(layers)
+        self.optimizer = optimizer
+        self.config = config or ControllerConfig()
+        self.controller = AdaptiveController(self.config)
+        self.radius = radius
+        self.preserve_zeros = preserve_zeros
+        self.grad_scale = grad_scale  # None: use the batch size (mean-reduced loss)
+        self.batch_flush = batch_flush
+        self.dist_group = dist_group
+        self.sync_stats = sync_stats
+        self.plan = None
+        self.it = 0
+        self.next_collection = self.controller.W
+        self.store = ActivationStore()
+        self.records: list[IterationRecord] = []
+        self._act_layer: dict = {}
+        self._handles: dict = {}
+        self._pending: list[_Handle] = []
+        self._collecting = False
+        self._R: dict[str, float] = {}
+        self._lbar: dict[str, float] = {}
+        self._batch = None
+        self._rec = None
+        self._hooks = []
+        for lid, (prod, cons) in self.layers.items():
+            self._hooks.append(prod.register_forward_hook(self._fwd_hook(lid)))
+            self._hooks.append(cons.register_full_backward_hook(self._bwd_hook(lid)))
+
+    # ---- construction helpers -------------------------------------------
+    @staticmethod
+    def conv_layer_map(model):
+        """{name: (activation module, consumer module)} for every Conv2d: the
+        activation is the first ReLU after it (else the conv itself), the
+        consumer the next Conv2d / Linear in module registration order
+        (reference _consumer_map, training.py:154-166)."""
+        import torch.nn as nn
+
+        # full backward hooks on the consumers forbid in-place ops on their outputs
+        for m in model.modules():
+            if isinstance(m, nn.ReLU):
+                m.inplace = False
+        mods = [(n, m) for n, m in model.named_modules() if not list(m.children())]
+        out = {}
+        for i, (name, m) in enumerate(mods):
+            if not isinstance(m, nn.Conv2d):
+                continue
+            act, cons = m, None
+            for n2, m2 in mods[i + 1:]:
+                if isinstance(m2, nn.ReLU) and act is m:
+                    act = m2
+                if isinstance(m2, (nn.Conv2d, nn.Linear)):
+                    cons = m2
+                    break
+            if cons is not None:
+                out[name] = (act, cons)
+        return out
+
+    def remove(self):
+        for h in self._hooks:
+            h.remove()
+        self._hooks.clear()
+
+    # ---- hooks ---------------------------------------------------------------
+    def _fwd_hook(self, lid):
+        def hook(mod, inp, out):
+            if self._batch is None and inp and hasattr(inp[0], "shape"):
+                self._batch = int(inp[0].shape[0])
+            self._act_layer[_key(out)] = lid
+        return hook
+
+    def _bwd_hook(self, lid):
+        def hook(mod, gin, gout):
+            if self._collecting and gout and gout[0] is not None:
+                from .tensor import per_sample_max
+
+                scale = self.grad_scale if self.grad_scale is not None else (self._batch or 1)
+                _, lbar = per_sample_max(gout[0].detach().float())
+                self._lbar[lid] = lbar * scale
+        return hook
+
+    def _pack(self, t):
+        import torch
+
+        if not (t.is_cuda and t.dtype == torch.float32) or isinstance(t, torch.nn.Parameter):
+            return ("raw", t)
+        k = _key(t)
+        lid = self._act_layer.get(k)
+        if lid is None:
+            return ("raw", t)
+        h = self._handles.get(k)
+        if h is not None:
+            h.packs += 1
+            return h
+        eb = self.plan.eb.get(lid) if self.plan is not None else None
+        h = _Handle(t, lid, eb)
+        self._handles[k] = h
+        nbytes = t.numel() * 4
+        if self._rec is not None:
+            self._rec.raw_bytes += nbytes
+        if eb is None:
+            self.store.put(lid, ActivationStore.RAW, None, nbytes)
+            if self._rec is not None:
+                self._rec.stored_bytes += nbytes
+            return h
+        self._pending.append(h)
+        if len(self._pending) >= self.batch_flush:
+            self.flush()
+        return h
+
+    def flush(self):
+        """Compress every queued activation (one host sync for the batch)."""
+        if not self._pending:
+            return
+        pend, self._pending = self._pending, []
+        params = [CodecParams(eb=h.eb, radius=self.radius, preserve_zeros=self.preserve_zeros) for h in pend]
+        out = compress_batch([h.raw for h in pend], params)
+        for h, (c, rep) in zip(pend, out):
+            h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
+            self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
+            if self._rec is not None:
+                self._rec.stored_bytes += rep.compressed_bytes
+                self._rec.compressed[h.layer] = (rep.ratio, h.eb)
+
+    def _unpack(self, h):
+        import torch
+
+        if isinstance(h, tuple):
+            return h[1]
+        if h.out is None:
+            if h.comp is None and h.raw is None:
+                raise LifecycleError(f"activation of {h.layer!r} already released")
+            if h.raw is not None and h in self._pending:
+                self.flush()
+            if h.comp is not None:
+                out, nz = decompress_device(h.comp, dtype=torch.float32, check=self._collecting)
+                h.out = out.view(h.shape)
+                if self._collecting:
+                    self._R[h.layer] = nz / out.numel()
+                self.store.pop(h.layer)
+                h.comp = None
+            else:
+                h.out = h.raw
+                if self._collecting:
+                    from .tensor import count_nonzero
+
+                    self._R[h.layer] = count_nonzero(h.raw) / h.raw.numel()
+                self.store.pop(h.layer)
+                h.raw = None
+        h.unpacks += 1
+        out = h.out
+        if h.unpacks >= h.packs:
+            h.out = None
+        return out
+
+    # ---- iteration protocol --------------------------------------------------
+    @contextlib.contextmanager
+    def iteration(self):
+        """Wrap forward + backward of one training iteration."""
+        import torch
+
+        self._collecting = (self.it + 1) == self.next_collection
+        self._act_layer.clear()
+        self._handles.clear()
+        self._R.clear()
+        self._lbar.clear()
+        self.store.clear()
+        self._rec = IterationRecord(self.it)
+        with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack):
+            yield self
+            self.flush()
+        self._handles.clear()
+        self._act_layer.clear()
+
+    def after_step(self):
+        """Call after optimizer.step(): interval boundary -> new plan."""
+        self.records.append(self._rec)
+        if self._collecting:
+            self.plan = self.controller.new_interval(self._collect_stats())
+            self.next_collection = (self.it + 1) + self.plan.W
+        self.it += 1
+        self._collecting = False
+        return self.plan
+
+    def _collect_stats(self):
+        from .tensor import mean_abs
+
+        ids = list(self.layers)
+        N = self._batch or 1
+        R = [self._R.get(l, 0.0) for l in ids]
+        Lb = [self._lbar.get(l, 0.0) for l in ids]
+        M = []
+        for l in ids:
+            cons = self.layers[l][1]
+            st = self.optimizer.state.get(cons.weight, {})
+            v = st.get("momentum_buffer")
+            M.append(mean_abs(v) if v is not None else 0.0)
+        if self.sync_stats:
+            R, Lb, M = sync_layer_stats(R, Lb, M, self.dist_group)
+        return [LayerTrainingStats(layer_id=l, R=min(1.0, max(0.0, r)), L_bar=lb, M_avg=m, N=N)
+                for l, r, lb, m in zip(ids, R, Lb, M)]
+
+
+def sync_layer_stats(R, L_bar, M_avg, group=None):
+    """Average per-layer statistics across data-parallel ranks (identical eb
+    everywhere).  No-op without an initialised process group."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return R, L_bar, M_avg
+    world = dist.get_world_size(group)
+    if world == 1:
+        return R, L_bar, M_avg
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    v = torch.tensor(list(R) + list(L_bar) + list(M_avg), dtype=torch.float64, device=dev)
+    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+    v = (v / world).cpu().tolist()
+    k = len(R)
+    return v[:k], v[k:2 * k], v[2 * k:]

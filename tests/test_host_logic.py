@@ -1,0 +1,151 @@
+"""CPU tests of the host-side logic: the reference's controller arithmetic
+(against reference-generated values and the reference's own known answers),
+the ActivationStore lifecycle, the layer map, and the cross-rank statistics
+sync (gloo, world size 2)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_2111_09562_b200 import controller as ctl
+from paper_2111_09562_b200.errors import LifecycleError, MemoryInfeasibleError, ParameterError
+from paper_2111_09562_b200.hooks import ActivationCompressor, ActivationStore, sync_layer_stats
+
+
+def stats(layer_id="conv1", R=0.5, L_bar=2.0, M_avg=1.0, N=64, **kw):
+    return ctl.LayerTrainingStats(layer_id=layer_id, R=R, L_bar=L_bar, M_avg=M_avg, N=N, **kw)
+
+
+def plan_of(eb_map, W=1000, interval=1):
+    return ctl.CompressionPlan(eb=eb_map, W=W, interval_index=interval, skip=frozenset())
+
+
+def test_hand_computed_eb():
+    # reference test_controller.py:101-105
+    plan = ctl.plan_compression([stats()], ctl.ControllerConfig())
+    assert plan.eb["conv1"] == pytest.approx(2.7621358640099365e-3, rel=1e-12)
+
+
+def test_eb_matches_reference_golden(golden_meta):
+    s = golden_meta["stats"]
+    st = ctl.LayerTrainingStats("conv1", R=s["collect"]["R"], L_bar=s["collect"]["L_bar"], M_avg=s["collect"]["M_avg"], N=8)
+    assert ctl.plan_compression([st], ctl.ControllerConfig()).eb["conv1"] == s["plan_eb"]
+
+
+def test_estimate_eb_inverse():
+    for a, L, N, R, eb in [(0.32, 2.0, 64, 0.5, 1e-3), (0.1, 0.3, 7, 0.9, 3e-5)]:
+        sig = ctl.predict_sigma(a, L, N, R, eb)
+        assert ctl.estimate_eb(sig, a, L, N, R) == pytest.approx(eb, rel=1e-14)
+    assert ctl.estimate_eb(1.0, 0.32, 0.0, 8, 0.5) is None
+    assert ctl.estimate_eb(1.0, 0.32, 1.0, 8, 0.0) is None
+
+
+def test_update_interval_cases():
+    # reference test_controller.py:144-197
+    cfg = ctl.ControllerConfig()
+    assert ctl.update_interval(plan_of({"c": 1e-3}), plan_of({"c": 2.5e-3}), 1000, cfg) == (500, 0)
+    assert ctl.update_interval(plan_of({"c": 1e-3}), plan_of({"c": 2e-3}), 1000, cfg)[0] == 1000
+    assert ctl.update_interval(plan_of({"c": 1e-3}), plan_of({"c": 1e-3 / 2.5}), 1000, cfg)[0] == 500
+    W, k = ctl.update_interval(plan_of({"c": 1e-3}), plan_of({"c": 1.1e-3}), 250, cfg, 0)
+    assert (W, k) == (250, 1)
+    assert ctl.update_interval(plan_of({"c": 1.1e-3}), plan_of({"c": 1e-3}), W, cfg, k) == (1000, 0)
+    W = 250
+    for _ in range(4):
+        W, _ = ctl.update_interval(plan_of({"c": 1e-3}), plan_of({"c": 1e-1}), W, cfg)
+    assert W == 125
+    assert ctl.update_interval(None, plan_of({"c": 1e-3}), 1000, cfg) == (1000, 0)
+    assert ctl.update_interval(plan_of({"c": 1e-3}), plan_of({"c": 1.5e-3}), 500, cfg, 1) == (500, 0)
+
+
+def test_skip_and_validation():
+    plan = ctl.plan_compression([stats("a", R=0.0), stats("b", M_avg=0.0), stats("c")], ctl.ControllerConfig())
+    assert plan.skip == frozenset({"a", "b"}) and set(plan.eb) == {"c"}
+    with pytest.raises(ParameterError):
+        ctl.LayerTrainingStats("x", R=1.5, L_bar=1.0, M_avg=1.0, N=1)
+    with pytest.raises(ParameterError):
+        ctl.CompressionPlan(eb={"x": 0.0}, W=10, interval_index=0, skip=frozenset())
+
+
+def test_batch_planner():
+    cfg = ctl.ControllerConfig(memory_budget_bytes=10 ** 9)
+    b = ctl.choose_batch_size({"l1": 1e6, "l2": 2e6}, {"l1": 4.0, "l2": 8.0}, cfg)
+    assert b == 1024 or b * (1e6 / 4 + 2e6 / 8) <= 10 ** 9 * 0.95
+    with pytest.raises(MemoryInfeasibleError):
+        ctl.choose_batch_size({"l1": 1e12}, {}, cfg)
+
+
+def test_adaptive_controller_W():
+    cfg = ctl.ControllerConfig(W_default=8, W_floor=2)
+    c = ctl.AdaptiveController(cfg)
+    p1 = c.new_interval([stats(M_avg=1.0)])
+    p2 = c.new_interval([stats(M_avg=3.0)])  # eb x3 -> halve W
+    assert p1.W == 8 and p2.W == 4 and c.intervals_planned == 2
+
+
+def test_kv_config():
+    m = ctl.parse_kv_lines("W_default = 200  # comment\n\nW_floor=10\n")
+    cfg = ctl.controller_config_from_mapping(m)
+    assert cfg.W_default == 200 and cfg.W_floor == 10
+    with pytest.raises(ParameterError):
+        ctl.controller_config_from_mapping({"bogus": "1"})
+
+
+def test_activation_store_lifecycle():
+    s = ActivationStore()
+    s.put("conv1", ActivationStore.COMPRESSED, object(), 100)
+    s.put("conv2", ActivationStore.RAW, object(), 400)
+    assert s.current_bytes == 500 and s.peak_bytes == 500
+    with pytest.raises(LifecycleError):
+        s.put("conv1", ActivationStore.RAW, None, 1)
+    kind, _, nb = s.pop("conv1")
+    assert kind == ActivationStore.COMPRESSED and nb == 100 and s.current_bytes == 400
+    with pytest.raises(LifecycleError):
+        s.pop("conv1")
+
+
+def test_conv_layer_map():
+    torch = pytest.importorskip("torch")
+    import torch.nn as nn
+
+    net = nn.Sequential(nn.Conv2d(3, 8, 3), nn.ReLU(inplace=True), nn.MaxPool2d(2), nn.Conv2d(8, 8, 3), nn.ReLU(),
+                        nn.Flatten(), nn.Linear(8, 4))
+    m = ActivationCompressor.conv_layer_map(net)
+    assert list(m) == ["0", "3"]
+    assert m["0"] == (net[1], net[3]) and m["3"] == (net[4], net[6])
+    assert not net[1].inplace
+
+
+def _sync_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    R, L, M = sync_layer_stats([0.5 + 0.1 * rank, 0.2], [1.0 * (rank + 1), 0.0], [0.01, 0.02])
+    plan = ctl.plan_compression([ctl.LayerTrainingStats(f"c{i}", R=R[i], L_bar=L[i], M_avg=M[i], N=16)
+                                 for i in range(2)], ctl.ControllerConfig())
+    q.put((rank, R, L, M, dict(plan.eb), sorted(plan.skip)))
+    dist.destroy_process_group()
+
+
+def test_stats_sync_two_ranks_gloo():
+    """world_size 2 on gloo: both ranks see averaged stats and identical eb."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_sync_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    (_, R0, L0, M0, eb0, sk0), (_, R1, L1, M1, eb1, sk1) = res
+    assert R0 == R1 == [pytest.approx(0.55), pytest.approx(0.2)]
+    assert L0 == L1 == [pytest.approx(1.5), 0.0]
+    assert eb0 == eb1 and sk0 == sk1 == ["c1"]
