@@ -29,6 +29,7 @@ namespace {
 constexpr int NWARP = K2_THREADS / 32;
 constexpr uint32_t kSmemL = 4096;
 constexpr int kMaxPhases = 128;
+constexpr uint32_t kWin = 22528;  // merged positions per staged window (180 KB of u64)
 
 struct RadixSmem {
   uint32_t hist[NWARP][257];
@@ -144,6 +145,74 @@ __device__ uint32_t block_lower_bound(const unsigned long long *v, uint32_t lo, 
   return lo;
 }
 
+// number of leaves among the first d merged items of (leaves lf[0,na),
+// internals nf[0,nb)), leaf wins ties -- block-wide 1024-way probing
+__device__ uint32_t merge_split_block(const unsigned long long *lf, const unsigned long long *nf, uint32_t na,
+                                      uint32_t nb, uint32_t d) {
+  uint32_t lo = d > nb ? d - nb : 0, hi = min(d, na);  // answer in [lo, hi]
+  while (lo < hi) {
+    const uint32_t len = hi - lo;
+    const uint32_t step = (len + K2_THREADS - 1) / K2_THREADS;
+    // candidate i = lo + 1 + t*step: predicate "leaf i-1 precedes internal d-i"
+    const uint32_t i = lo + 1 + threadIdx.x * step;
+    bool p = false;
+    if (i <= hi) {
+      const uint32_t j = d - i;
+      p = j >= nb || lf[i - 1] <= nf[j];
+    }
+    const uint32_t k = (uint32_t)__syncthreads_count(p);  // true probes form a prefix
+    if (step == 1) return lo + k;
+    // answer in [c_{k-1}, c_k - 1] with c_t = lo + 1 + t*step, c_{-1} = lo
+    const uint32_t nlo = k ? lo + 1 + (k - 1) * step : lo;
+    const uint32_t nhi = min(hi, lo + k * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+// Sequentially merge merged positions [d0, d1) of (a[0,na), b[0,nb)) (leaf
+// wins ties), creating pair nodes nn + p/2 for p < 2*pairs (positions are
+// relative to the window) and recording the odd leftover.
+__device__ __forceinline__ void merge_range(const unsigned long long *a, const unsigned long long *b, uint32_t na,
+                                            uint32_t nb, uint32_t d0, uint32_t d1, uint32_t abase, uint32_t bbase,
+                                            uint32_t nn, uint32_t pairs, uint32_t *lpar, uint32_t *npar,
+                                            unsigned long long *nf, uint32_t &odd_item) {
+  uint32_t lo = d0 > nb ? d0 - nb : 0, hi = min(d0, na);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    const uint32_t j = d0 - mid;
+    if (j >= nb || a[mid - 1] <= b[j])
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  uint32_t i = lo, j = d0 - lo;
+  unsigned long long fprev = 0;
+  for (uint32_t p = d0; p < d1; p++) {
+    const bool leaf = j >= nb || (i < na && a[i] <= b[j]);
+    unsigned long long f;
+    uint32_t item;
+    if (leaf) {
+      f = a[i];
+      item = abase + i;
+      i++;
+    } else {
+      f = b[j];
+      item = 0x80000000u | (bbase + j);
+      j++;
+    }
+    if (p < 2 * pairs) {
+      const uint32_t node = nn + (p >> 1);
+      if (item & 0x80000000u) npar[item & 0x7FFFFFFFu] = node; else lpar[item] = node;
+      if (p & 1) nf[node] = fprev + f;
+      fprev = f;
+    } else {
+      odd_item = item;  // the single leftover (tot odd)
+    }
+  }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
@@ -242,7 +311,8 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   uint32_t *v0 = a.vals, *v1 = a.vals2, *lpar = a.lpar, *npar = a.npar;
   uint32_t *ndepth = (uint32_t *)a.ndepth;
   uint8_t *llen = a.llen;
-  if (L <= kSmemL) {
+  const bool big = L > kSmemL;
+  if (!big) {
     unsigned char *p = smem;
     k0 = (unsigned long long *)p; p += 8 * (size_t)kSmemL;
     k1 = (unsigned long long *)p; p += 8 * (size_t)kSmemL;
@@ -297,45 +367,35 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       const uint32_t na = block_lower_bound(lf, lp, (uint32_t)L, T) - lp;
       const uint32_t nb = block_lower_bound(nf, np, nn, T) - np;
       const uint32_t tot = na + nb, pairs = tot >> 1;
-      // merge path: thread t owns merged positions [t*q, t*q+q), q even
-      uint32_t q = (tot + K2_THREADS - 1) / K2_THREADS;
-      q = (q + 1) & ~1u;
-      const uint32_t d0 = tid * q;
-      if (d0 < tot) {
-        // number of leaves among the first d0 merged items (leaf wins ties)
-        uint32_t lo = d0 > nb ? d0 - nb : 0, hi = min(d0, na);
-        while (lo < hi) {
-          uint32_t mid = (lo + hi + 1) >> 1;
-          uint32_t j = d0 - mid;
-          if (j >= nb || lf[lp + mid - 1] <= nf[np + j])
-            lo = mid;
-          else
-            hi = mid - 1;
-        }
-        uint32_t i = lo, j = d0 - lo;
-        const uint32_t d1 = min(tot, d0 + q);
-        unsigned long long fprev = 0;
-        for (uint32_t p = d0; p < d1; p++) {
-          bool leaf = j >= nb || (i < na && lf[lp + i] <= nf[np + j]);
-          unsigned long long f;
-          uint32_t item;
-          if (leaf) {
-            f = lf[lp + i];
-            item = lp + i;
-            i++;
-          } else {
-            f = nf[np + j];
-            item = 0x80000000u | (np + j);
-            j++;
-          }
-          if (p < 2 * pairs) {
-            const uint32_t node = nn + (p >> 1);
-            if (item & 0x80000000u) npar[item & 0x7FFFFFFFu] = node; else lpar[item] = node;
-            if (p & 1) nf[node] = fprev + f;
-            fprev = f;
-          } else {
-            s_odd_item = item;  // the single leftover (tot odd)
-          }
+      if (!big) {
+        // merge path on the (shared-memory) arrays: thread t owns merged
+        // positions [t*q, t*q+q), q even so pairs never straddle threads
+        uint32_t q = (tot + K2_THREADS - 1) / K2_THREADS;
+        q = (q + 1) & ~1u;
+        const uint32_t d0 = tid * q;
+        if (d0 < tot)
+          merge_range(lf + lp, nf + np, na, nb, d0, min(tot, d0 + q), lp, np, nn, pairs, lpar, npar, nf, s_odd_item);
+      } else {
+        // global arrays: stage the phase's inputs through shared memory in
+        // windows of kWin merged positions
+        for (uint32_t wa = 0; wa < tot; wa += kWin) {
+          const uint32_t wb = min(tot, wa + kWin);
+          const uint32_t ia = merge_split_block(lf + lp, nf + np, na, nb, wa);
+          const uint32_t ib = merge_split_block(lf + lp, nf + np, na, nb, wb);
+          const uint32_t ja = wa - ia, jb = wb - ib;
+          unsigned long long *sl = reinterpret_cast<unsigned long long *>(smem);
+          unsigned long long *sn = sl + (ib - ia);
+          for (uint32_t i = tid; i < ib - ia; i += K2_THREADS) sl[i] = lf[lp + ia + i];
+          for (uint32_t j = tid; j < jb - ja; j += K2_THREADS) sn[j] = nf[np + ja + j];
+          __syncthreads();
+          const uint32_t wt = wb - wa;
+          uint32_t q = (wt + K2_THREADS - 1) / K2_THREADS;
+          q = (q + 1) & ~1u;  // wa is even (kWin even), so pairs stay inside a thread
+          const uint32_t d0 = tid * q;
+          if (d0 < wt)
+            merge_range(sl, sn, ib - ia, jb - ja, d0, min(wt, d0 + q), lp + ia, np + ja, nn + wa / 2,
+                        pairs > wa / 2 ? pairs - wa / 2 : 0, lpar, npar, nf, s_odd_item);
+          __syncthreads();
         }
       }
       __syncthreads();
@@ -371,26 +431,31 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       if (s_err & 2u) break;
     }
     // ---- 4. depths, walking phases backwards ----
+    // internal-node depths as bytes in shared memory (saturating at 255;
+    // anything > 63 is an error anyway)
     K2_STAMP(3)
     if (a.dbg && tid == 0) a.dbg[8] = s_nph;
     const uint32_t nn = s_nn, root = nn - 1, nph = s_nph;
-    if (tid == 0) ndepth[root] = 0;
+    uint8_t *dep = big ? reinterpret_cast<uint8_t *>(smem) : reinterpret_cast<uint8_t *>(ndepth);
+    __syncthreads();
+    if (tid == 0) dep[root] = 0;
     __syncthreads();
     for (int ph = (int)nph - 1; ph >= 0; ph--) {
       const uint32_t b = ph_begin[ph], pr = ph_pairs[ph];
       if (ph_odd[ph]) {
         if (tid == 0) {
-          uint32_t o = b + pr;
-          if (o != root) ndepth[o] = ndepth[npar[o]] + 1;
+          const uint32_t o = b + pr;
+          if (o != root) dep[o] = (uint8_t)min(255, dep[npar[o]] + 1);
         }
         __syncthreads();
       }
       for (uint32_t t = b + tid; t < b + pr; t += K2_THREADS)
-        if (t != root) ndepth[t] = ndepth[npar[t]] + 1;
+        if (t != root) dep[t] = (uint8_t)min(255, dep[npar[t]] + 1);
       __syncthreads();
     }
+#pragma unroll 4
     for (uint32_t i = tid; i < L; i += K2_THREADS) {
-      uint32_t d = ndepth[lpar[i]] + 1;
+      const uint32_t d = (uint32_t)dep[lpar[i]] + 1;
       if (d > ACTC_MAX_CODE_LENGTH) atomicOr(&s_err, 1u);
       llen[v0[i]] = (uint8_t)(d > 255 ? 255 : d);
     }
