@@ -268,10 +268,9 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
   QParams P;
   P.eb = eb;
   P.two_eb = 2.0 * eb;
-  double inv = 1.0 / P.two_eb;
-  float inv32 = (float)inv;
-  P.inv32 = inv32;
-  P.fast = (isfinite(inv32) && inv32 >= FLT_MIN) ? 1 : 0;
+  const double inv = 1.0 / P.two_eb;
+  P.inv = inv;
+  P.fast = (isfinite(inv) && inv >= DBL_MIN) ? 1 : 0;
   uint32_t win_n = (uint32_t)std::min<uint64_t>(A, K1_WIN);
   uint32_t win_lo = A <= K1_WIN ? 0 : radius - K1_WIN / 2;
   uint64_t ntiles = cdiv(n, K1_TILE);

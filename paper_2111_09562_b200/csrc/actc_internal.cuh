@@ -24,8 +24,8 @@ constexpr uint32_t kMaxAlphabet = 1u << kSymKeyBits;
 struct QParams {
   double eb;
   double two_eb;   // 2.0 * eb (exact scaling; may be +inf like numpy)
-  float inv32;     // fl32(fl64(1 / two_eb)) -- fast-path multiplier
-  int fast;        // inv32 is a finite normal float
+  double inv;      // fl64(1 / two_eb) -- fast-path multiplier
+  int fast;        // inv is finite and normal
 };
 
 // Exact restatement: v = x / (2eb); q = sign(v)*floor(fl(|v| + 0.5));
@@ -40,19 +40,20 @@ __device__ __forceinline__ long long quant_exact(double x, double two_eb, double
   return (long long)q;
 }
 
-// Fast path in fp32.  v32 = x*inv32 has relative error <= 2^-22.9 of the
-// true quotient; when the fractional distance of |v32| to the rounding
-// boundary exceeds m = (|v32|+1)*2^-20 the exact fp64 path provably yields
-// the same q, and |x - q*2eb| <= eb*(1 - m) so the bound check cannot
-// fire.  Returns false when the caller must take quant_exact.
-__device__ __forceinline__ bool quant_fast(float xf, float inv32, long long &q) {
-  float v = __fmul_rn(xf, inv32);
-  float a = fabsf(v);
-  float f = floorf(__fadd_rn(a, 0.5f));
-  float r = __fsub_rn(a, f);
-  float m = __fmul_rn(__fadd_rn(a, 1.0f), 0x1p-20f);
-  bool safe = (a < 0x1p19f) && (fabsf(r) < __fsub_rn(0.5f, m));
-  int qi = (int)f;
+// Fast path in fp64 with a multiply instead of the division.
+// v' = x * fl64(1/(2eb)) is within |v|*2^-51 of the true quotient; when the
+// distance of |v'| to the rounding boundary exceeds m = (|v'|+1)*2^-44 the
+// exact path (x / 2eb, floor(fl(|v|+0.5))) provably yields the same q, and
+// |x - q*2eb| <= eb*(1 - m) so the bound check cannot fire.  |v'| < 2^29
+// keeps q in int32.  Returns false when the caller must take quant_exact.
+__device__ __forceinline__ bool quant_fast(float xf, double inv, long long &q) {
+  const double v = __dmul_rn((double)xf, inv);
+  const double a = fabs(v);
+  const double f = floor(__dadd_rn(a, 0.5));
+  const double r = __dsub_rn(a, f);
+  const double m = __dmul_rn(__dadd_rn(a, 1.0), 0x1p-44);
+  const bool safe = (a < 0x1p29) && (fabs(r) < __dsub_rn(0.5, m));
+  const int qi = (int)f;
   q = xf > 0.0f ? qi : -qi;
   return safe;
 }
@@ -60,7 +61,7 @@ __device__ __forceinline__ bool quant_fast(float xf, float inv32, long long &q) 
 __device__ __forceinline__ long long quant_elem(float xf, const QParams &P, bool &viol) {
   long long q;
   viol = false;
-  if (P.fast && quant_fast(xf, P.inv32, q)) return q;
+  if (P.fast && quant_fast(xf, P.inv, q)) return q;
   return quant_exact((double)xf, P.two_eb, P.eb, viol);
 }
 

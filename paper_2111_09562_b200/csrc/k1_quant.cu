@@ -15,6 +15,36 @@
 
 namespace actc {
 
+__device__ __forceinline__ uint32_t k1_saddr(const void *p) {
+  // opaque: keeps the shared base in a register (no SR_CgaCtaId rematerialisation)
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ void k1_hist_add(uint32_t hbase, uint32_t win_lo, uint32_t win_n,
+                                            unsigned long long *__restrict__ ghist, uint32_t sj) {
+  const uint32_t w = sj - win_lo;
+  if (w < win_n)
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * w) : "memory");
+  else
+    atomicAdd(&ghist[sj], 1ull);
+}
+
+template <typename SymT>
+__device__ __forceinline__ void k1_store(SymT *__restrict__ sym, uint64_t base, const uint32_t (&s)[K1_EPT]) {
+  if (sizeof(SymT) == 2) {
+    uint4 *d = reinterpret_cast<uint4 *>(sym + base);
+#pragma unroll
+    for (int j = 0; j < K1_EPT / 8; j++)
+      d[j] = make_uint4(s[8 * j] | (s[8 * j + 1] << 16), s[8 * j + 2] | (s[8 * j + 3] << 16),
+                        s[8 * j + 4] | (s[8 * j + 5] << 16), s[8 * j + 6] | (s[8 * j + 7] << 16));
+  } else {
+    uint4 *d = reinterpret_cast<uint4 *>(sym + base);
+#pragma unroll
+    for (int j = 0; j < K1_EPT / 4; j++) d[j] = make_uint4(s[4 * j], s[4 * j + 1], s[4 * j + 2], s[4 * j + 3]);
+  }
+}
+
 template <typename SymT>
 __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
     const float *__restrict__ x, uint64_t n, QParams P, uint32_t radius, SymT *__restrict__ sym,
@@ -24,14 +54,18 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
   extern __shared__ unsigned sh_hist[];
   for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) sh_hist[i] = 0;
   __syncthreads();
+  const uint32_t hbase = k1_saddr(sh_hist);
   const int lane = threadIdx.x & 31;
   const uint64_t ntiles = (n + K1_TILE - 1) / K1_TILE;
+  const uint64_t nfull = n / K1_TILE;  // tiles with no element past n
+  const int R = (int)min(radius, 0x40000000u);
   unsigned outl = 0;
+  bool fin_all = true;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t base = tile * K1_TILE + (uint64_t)threadIdx.x * K1_EPT;
+    const bool full_tile = tile < nfull;  // warp-uniform
     float xv[K1_EPT];
-    const bool full = base + K1_EPT <= n;
-    if (full) {
+    if (full_tile) {
       const float4 *p = reinterpret_cast<const float4 *>(x + base);
 #pragma unroll
       for (int j = 0; j < K1_EPT / 4; j++) {
@@ -42,72 +76,94 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) xv[j] = (base + j < n) ? x[base + j] : 0.0f;
     }
-    long long q[K1_EPT];
-    unsigned viol = 0;
     bool fin = true;
 #pragma unroll
     for (int j = 0; j < K1_EPT; j++) fin &= isfinite(xv[j]);
-    if (!fin) atomicOr(nonfinite, 1u);  // Tensor rejects NaN/Inf (tensor.py:56-57)
+    fin_all &= fin;
+    // fp32 fast quantizer for all 16 elements; exact fp64 only where needed
+    int q32[K1_EPT];
+    unsigned slow = 0;
 #pragma unroll
     for (int j = 0; j < K1_EPT; j++) {
-      bool vj;
-      q[j] = quant_elem(xv[j], P, vj);
-      viol |= (unsigned)vj << j;
+      long long qq;
+      const bool ok = P.fast && quant_fast(xv[j], P.inv, qq);
+      q32[j] = (int)qq;
+      slow |= (unsigned)!ok << j;
     }
-    // decode index: lattice value just before every ACTC_CHUNK-th element
-    // (the running value lorenzo_decode holds there, codec.py:286-292)
-    if (chunk_lat) {
-      if (base == 0) chunk_lat[0] = 0;
-      if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q[K1_EPT - 1];
+    long long prev64;
+    {
+      long long lastq = q32[K1_EPT - 1];
+      if (slow >> (K1_EPT - 1)) {
+        bool v;
+        lastq = quant_exact((double)xv[K1_EPT - 1], P.two_eb, P.eb, v);
+      }
+      prev64 = __shfl_up_sync(0xffffffffu, lastq, 1);
+      if (lane == 0) {
+        bool dummy;
+        prev64 = (base > 0 && base - 1 < n) ? quant_elem(x[base - 1], P, dummy) : 0;
+      }
     }
-    long long prev = __shfl_up_sync(0xffffffffu, q[K1_EPT - 1], 1);
-    if (lane == 0) {
-      bool dummy;
-      prev = (base > 0 && base - 1 < n) ? quant_elem(x[base - 1], P, dummy) : 0;
-    }
-    SymT s[K1_EPT];
+    uint32_t s[K1_EPT];
+    const bool fast32 = __all_sync(0xffffffffu, slow == 0 && prev64 >= -(1ll << 29) && prev64 <= (1ll << 29));
+    if (fast32 && full_tile) {
+      // every lattice value fits int32 (|q| < 2^19): 32-bit Lorenzo + histogram
+      if (chunk_lat) {
+        if (base == 0) chunk_lat[0] = 0;
+        if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q32[K1_EPT - 1];
+      }
+      int prev = (int)prev64;
 #pragma unroll
-    for (int j = 0; j < K1_EPT; j++) {
-      long long d = q[j] - prev;
-      prev = q[j];
-      unsigned long long ad = d < 0 ? (unsigned long long)(-d) : (unsigned long long)d;
-      bool o = ad >= radius || ((viol >> j) & 1u);
-      uint32_t sj = o ? 0u : (uint32_t)(d + (long long)radius);
-      s[j] = (SymT)sj;
-      if (base + j < n) {
+      for (int j = 0; j < K1_EPT; j++) {
+        const int d = q32[j] - prev;
+        prev = q32[j];
+        const bool o = (uint32_t)(d + R - 1) >= (uint32_t)(2 * R - 1);  // |d| >= radius
+        const uint32_t sj = o ? 0u : (uint32_t)(d + R);
+        s[j] = sj;
         outl += o;
-        uint32_t w = sj - win_lo;
-        if (w < win_n)
-          atomicAdd(&sh_hist[w], 1u);
-        else
-          atomicAdd(&ghist[sj], 1ull);
+        k1_hist_add(hbase, win_lo, win_n, ghist, sj);
       }
-    }
-    if (full) {
-      if (sizeof(SymT) == 2) {
-        uint4 *d = reinterpret_cast<uint4 *>(sym + base);
-#pragma unroll
-        for (int j = 0; j < K1_EPT / 8; j++) {
-          uint4 v;
-          v.x = (uint32_t)s[8 * j + 0] | ((uint32_t)s[8 * j + 1] << 16);
-          v.y = (uint32_t)s[8 * j + 2] | ((uint32_t)s[8 * j + 3] << 16);
-          v.z = (uint32_t)s[8 * j + 4] | ((uint32_t)s[8 * j + 5] << 16);
-          v.w = (uint32_t)s[8 * j + 6] | ((uint32_t)s[8 * j + 7] << 16);
-          d[j] = v;
-        }
-      } else {
-        uint4 *d = reinterpret_cast<uint4 *>(sym + base);
-#pragma unroll
-        for (int j = 0; j < K1_EPT / 4; j++)
-          d[j] = make_uint4((uint32_t)s[4 * j], (uint32_t)s[4 * j + 1], (uint32_t)s[4 * j + 2],
-                            (uint32_t)s[4 * j + 3]);
-      }
+      k1_store<SymT>(sym, base, s);
     } else {
+      // general path: exact fp64 where the fast path declined, int64 deltas
+      long long q[K1_EPT];
+      unsigned viol = 0;
 #pragma unroll
-      for (int j = 0; j < K1_EPT; j++)
-        if (base + j < n) sym[base + j] = s[j];
+      for (int j = 0; j < K1_EPT; j++) {
+        q[j] = q32[j];
+        if ((slow >> j) & 1u) {
+          bool vj;
+          q[j] = quant_exact((double)xv[j], P.two_eb, P.eb, vj);
+          viol |= (unsigned)vj << j;
+        }
+      }
+      if (chunk_lat) {
+        if (base == 0) chunk_lat[0] = 0;
+        if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q[K1_EPT - 1];
+      }
+      long long prev = prev64;
+#pragma unroll
+      for (int j = 0; j < K1_EPT; j++) {
+        long long d = q[j] - prev;
+        prev = q[j];
+        unsigned long long ad = d < 0 ? (unsigned long long)(-d) : (unsigned long long)d;
+        bool o = ad >= radius || ((viol >> j) & 1u);
+        uint32_t sj = o ? 0u : (uint32_t)(d + (long long)radius);
+        s[j] = sj;
+        if (base + j < n) {
+          outl += o;
+          k1_hist_add(hbase, win_lo, win_n, ghist, sj);
+        }
+      }
+      if (full_tile) {
+        k1_store<SymT>(sym, base, s);
+      } else {
+#pragma unroll
+        for (int j = 0; j < K1_EPT; j++)
+          if (base + j < n) sym[base + j] = (SymT)s[j];
+      }
     }
   }
+  if (!__all_sync(0xffffffffu, fin_all) && !fin_all) atomicOr(nonfinite, 1u);  // tensor.py:56-57
   unsigned wsum = warp_sum(outl);
   if (lane == 0 && wsum) atomicAdd(n_outliers, (unsigned long long)wsum);
   __syncthreads();
