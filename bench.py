@@ -36,6 +36,11 @@ sys.path.insert(0, ROOT)
 METRIC = "activation compress+decompress GB/s/GPU vs HBM peak; compression ratio; images/s"
 
 
+KERNEL_NAMES = {"quant": "k1_quant_lorenzo_hist", "codebook": "k2_codebook", "count": "k3_count",
+                "scan": "k_excl_scan_u64", "pack": "k3_pack", "fixup": "k3_fixup", "lut": "k_build_lut",
+                "decode": "k4w_decode"}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -321,6 +326,8 @@ def run_gpu(args, rank, world):
     torch.cuda.synchronize()
     step_ms, phase = [], {"compress": 0.0, "decompress": 0.0}
     ratios = None
+    _lib.kernel_stats()  # reset the per-kind launch counters / timers
+    _lib.timing_enable(True)  # per-launch CUDA events on each kernel's own stream
     with ClockSampler(dev.index if os.environ.get("CUDA_VISIBLE_DEVICES") is None else 0) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -337,6 +344,8 @@ def run_gpu(args, rank, world):
             ratios = [r.ratio for _, r in comp]
             comp_bytes = [r.compressed_bytes for _, r in comp]
     torch.cuda.synchronize()
+    _lib.timing_enable(False)
+    kstats = _lib.kernel_stats()
     total_ms = sum(step_ms)
     if world > 1:
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -345,26 +354,37 @@ def run_gpu(args, rank, world):
     ms_per_step = total_ms / args.steps
     gbs = world * in_bytes * args.steps / (total_ms * 1e-3) / 1e9
 
-    # roofline of the dominant phase (its launch is essentially one kernel:
-    # K4 for decompress; K1 for compress' first half)
+    # roofline of the dominant kernel: the kind with the largest summed live
+    # duration (CUDA events on the launching stream, timed region only);
+    # algorithmic bytes per step per kind as stated in DESIGN.md section 4
     C = sum(comp_bytes)
-    dom = max(phase, key=phase.get)
-    per_launch_ms = phase[dom] / (args.steps * len(tensors))
-    if dom == "decompress":
-        alg = C + 4 * n_total  # read bitstream, write fp32 (K4 algorithmic bytes)
-        kname = "k4w_decode (+k_build_lut)"
-    else:
-        alg = 4 * n_total + C  # read fp32, write CMTZ-equivalent bytes
-        kname = "compress_batch: k1_quant_lorenzo_hist + k2_codebook + k3_count/k3_pack"
-    achieved = alg / len(tensors) / (per_launch_ms * 1e-3) / 1e9
+    sb = 2  # u16 symbols (radius <= 2^15)
+    alg_step = {
+        "quant": 4 * n_total + sb * n_total + 8 * n_total // 256,  # read fp32, write symbols + chunk lattice
+        "codebook": 8 * 65536 * len(tensors),  # read the histogram (latency-bound, single CTA)
+        "count": sb * n_total,  # read symbols
+        "pack": sb * n_total + C,  # read symbols, write bitstream + outliers
+        "decode": C + 16 * n_total // 256 + 4 * n_total,  # read bitstream + chunk index, write fp32
+    }
+    kernels = {}
+    for kind, (nl, ms) in kstats.items():
+        if nl == 0:
+            continue
+        ent = {"launches_per_step": nl / args.steps, "ms_per_step": ms / args.steps}
+        if kind in alg_step and ms > 0:
+            ent["alg_bytes_per_launch"] = alg_step[kind] * args.steps / nl
+            ent["achieved_gbs"] = alg_step[kind] * args.steps / (ms * 1e-3) / 1e9
+        kernels[kind] = ent
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     peak, peak_kind = _peaks()
+    achieved = kernels[dom].get("achieved_gbs", 0.0)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            tr = json.load(fh).get(args.workload, {})
-        traffic = tr.get(dom)
+            traffic = json.load(fh).get(args.workload, {}).get(dom)
     except Exception:
         pass
+    gpu_launches = sum(nl for nl, _ in kstats.values())
 
     # end-to-end through host buffers (pinned H2D of inputs, D2H of outputs)
     host_in = [t.cpu().pin_memory() for t in tensors]
@@ -415,11 +435,14 @@ def run_gpu(args, rank, world):
             if args.workload == "alexnet256" else "synthetic", "config": cfg,
             "compression_ratio": ratio_total, "images_per_s": world * batch / (ms_per_step * 1e-3),
             "roofline_fraction_round_trip": (world * (8 * n_total + 2 * C) / (ms_per_step * 1e-3) / 1e9) / peak,
-            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": alg / len(tensors)},
+            "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES.get(dom, dom), "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": kernels[dom].get("alg_bytes_per_launch"),
+                         "avg_launch_ms": kernels[dom]["ms_per_step"] / kernels[dom]["launches_per_step"],
+                         "timing": "CUDA events around every launch on its own stream, timed region"},
+            "kernels": kernels,
             "e2e": {"value": e2e_gbs, "unit": "GB/s", "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": in_bytes},
-            "gpu_launches": args.steps * len(tensors) * 9,  # k1,k2,k3_count,2x scan,k3_pack,k3_fixup,lut,k4w
+            "gpu_launches": gpu_launches,  # counted by libactc (actc_kernel_stats) over the timed region
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu:

@@ -188,6 +188,29 @@ int actc_mean_abs(actc_ctx *ctx, const void *x_dev, int dtype, uint64_t n, doubl
 int actc_lbar(actc_ctx *ctx, const void *g_dev, int dtype, uint64_t N, uint64_t per_sample,
               void *per_sample_max_dev, double *out_host, actc_stream s);
 
+/* ---- instrumentation (not part of the reference interface) ----
+ * Every kernel launch the library makes is counted per kind; with timing
+ * enabled each launch is also bracketed by CUDA events recorded on the
+ * stream it is launched on.  actc_kernel_stats synchronizes the pending
+ * events, writes per-kind totals (launches, summed kernel ms) for up to
+ * `nkinds` kinds and resets the accumulators.  Process-wide. */
+enum {
+  ACTC_KIND_QUANT = 0,    /* K1 quantize + Lorenzo + histogram */
+  ACTC_KIND_CODEBOOK = 1, /* K2 Huffman codebook */
+  ACTC_KIND_COUNT = 2,    /* K3 per-CTA bit count */
+  ACTC_KIND_SCAN = 3,     /* exclusive scans of per-CTA totals */
+  ACTC_KIND_PACK = 4,     /* K3 bit packing + outlier extraction */
+  ACTC_KIND_FIXUP = 5,    /* K3 boundary-word fixup */
+  ACTC_KIND_LUT = 6,      /* decoder prefix table */
+  ACTC_KIND_DECODE = 7,   /* K4 decode + inverse Lorenzo + recon */
+  ACTC_KIND_INDEX = 8,    /* chunk-index rebuild (from_bytes streams) */
+  ACTC_KIND_STATS = 9,    /* K5 statistics */
+  ACTC_KIND_DEBUG = 10,   /* conformance entry points */
+  ACTC_KIND_NKINDS = 11
+};
+int actc_timing_enable(int on);
+int actc_kernel_stats(uint64_t *launches, double *ms, int nkinds);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,6 +104,8 @@ def lib():
             "actc_count_nonzero": ([P, I, U64, P, P], I),
             "actc_mean_abs": ([P, P, I, U64, P, P], I),
             "actc_lbar": ([P, P, I, U64, U64, P, P, P], I),
+            "actc_timing_enable": ([I], I),
+            "actc_kernel_stats": ([P, P, I], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -118,8 +120,26 @@ EXPORTED_SYMBOLS = (
     "actc_compress_encode actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
-    "actc_mean_abs actc_lbar"
+    "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats"
 ).split()
+
+# instrumentation kinds (include/actc.h ACTC_KIND_*)
+KERNEL_KINDS = ("quant", "codebook", "count", "scan", "pack", "fixup", "lut", "decode", "index", "stats", "debug")
+
+
+def timing_enable(on: bool = True):
+    """Bracket every library kernel launch with CUDA events on its stream."""
+    lib().actc_timing_enable(1 if on else 0)
+
+
+def kernel_stats() -> dict:
+    """{kind: (launches, summed kernel ms)} since the last call; resets.
+    Synchronizes the pending timing events."""
+    n = len(KERNEL_KINDS)
+    launches = (C.c_uint64 * n)()
+    ms = (C.c_double * n)()
+    raise_for(lib().actc_kernel_stats(C.cast(launches, C.c_void_p), C.cast(ms, C.c_void_p), n))
+    return {k: (int(launches[i]), float(ms[i])) for i, k in enumerate(KERNEL_KINDS)}
 
 
 def raise_for(rc: int, default_msg: str = ""):

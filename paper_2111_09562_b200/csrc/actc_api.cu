@@ -8,6 +8,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -59,6 +62,58 @@ int grow(Buf &b, size_t bytes) {
   b.cap = want;
   return ACTC_OK;
 }
+
+// ---- launch instrumentation (actc_timing_enable / actc_kernel_stats) ----
+struct KRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::atomic<unsigned long long> g_launches[ACTC_KIND_NKINDS];
+std::atomic<bool> g_timing{false};
+std::mutex g_tmu;
+std::vector<KRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t pool_event() {
+  cudaEvent_t e = nullptr;
+  if (!g_pool.empty()) {
+    e = g_pool.back();
+    g_pool.pop_back();
+  } else if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    e = nullptr;
+  }
+  return e;
+}
+
+// Scope guard around one kernel launch: counts it and, when timing is on,
+// brackets it with events on its own stream.
+struct KTimer {
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KTimer(int k, cudaStream_t st) : kind(k), s(st) {
+    g_launches[k].fetch_add(1, std::memory_order_relaxed);
+    if (g_timing.load(std::memory_order_relaxed)) {
+      std::lock_guard<std::mutex> g(g_tmu);
+      a = pool_event();
+      b = pool_event();
+      if (a && b) cudaEventRecord(a, s);
+    }
+  }
+  ~KTimer() {
+    if (a && b) {
+      cudaEventRecord(b, s);
+      std::lock_guard<std::mutex> g(g_tmu);
+      g_recs.push_back({kind, a, b});
+    } else {
+      std::lock_guard<std::mutex> g(g_tmu);
+      if (a) g_pool.push_back(a);
+      if (b) g_pool.push_back(b);
+    }
+  }
+};
+#define KT(kind) KTimer kt_guard_(kind, s)
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t pow2_ge(uint64_t x) {
@@ -163,7 +218,10 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
     a.dbg = (unsigned long long *)c->idx.p;
   }
   CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
-  k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
+  {
+    KT(ACTC_KIND_CODEBOOK);
+    k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
+  }
   CKL();
   return ACTC_OK;
 }
@@ -184,6 +242,43 @@ int actc_debug_k2_timing(actc_ctx *c, uint64_t *out16) {
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(out16, c->idx.p, 16 * 8, cudaMemcpyDeviceToHost));
   return ACTC_OK;
+}
+
+int actc_timing_enable(int on) {
+  g_timing.store(on != 0);
+  return ACTC_OK;
+}
+
+int actc_kernel_stats(uint64_t *launches, double *ms, int nkinds) {
+  double acc[ACTC_KIND_NKINDS] = {0};
+  std::vector<KRec> recs;
+  {
+    std::lock_guard<std::mutex> g(g_tmu);
+    recs.swap(g_recs);
+  }
+  int rc = ACTC_OK;
+  for (const KRec &r : recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess)
+      acc[r.kind] += t;
+    else
+      rc = set_err(ACTC_ECUDA, "kernel timing event failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    std::lock_guard<std::mutex> g(g_tmu);
+    for (const KRec &r : recs) {
+      g_pool.push_back(r.a);
+      g_pool.push_back(r.b);
+    }
+  }
+  for (int k = 0; k < ACTC_KIND_NKINDS; k++) {
+    unsigned long long l = g_launches[k].exchange(0);
+    if (k < nkinds) {
+      if (launches) launches[k] = l;
+      if (ms) ms[k] = acc[k];
+    }
+  }
+  return rc;
 }
 
 int actc_ctx_create(int device, actc_ctx **out) {
@@ -275,14 +370,17 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
   uint32_t win_lo = A <= K1_WIN ? 0 : radius - K1_WIN / 2;
   uint64_t ntiles = cdiv(n, K1_TILE);
   int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)c->k1_blocks);
-  if (sb == 2)
-    k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, win_n * 4, s>>>(
-        x, n, P, radius, (uint16_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
-        (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
-  else
-    k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, win_n * 4, s>>>(
-        x, n, P, radius, (uint32_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
-        (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
+  {
+    KT(ACTC_KIND_QUANT);
+    if (sb == 2)
+      k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, win_n * 4, s>>>(
+          x, n, P, radius, (uint16_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
+          (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
+    else
+      k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, win_n * 4, s>>>(
+          x, n, P, radius, (uint32_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
+          (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
+  }
   CKL();
   if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, nullptr, misc + M_NOUT, n, sb, s,
                          (const unsigned *)(misc + M_BAD))))
@@ -345,9 +443,13 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
   const unsigned long long *ct = (const unsigned long long *)c->ctab.p;
 #define K3_LAUNCH(T, W)                                                                                        \
   do {                                                                                                         \
-    k3_count<T, W><<<ncta, K3_THREADS, smem_count, s>>>((const T *)sym, n, ct, cwin_lo, cwin_n, tpc, cbits, cnz); \
-    k_excl_scan_u64<<<1, 1024, 0, s>>>(cbits, ncta, cbit0, misc + M_SCAN_TOT);                                \
-    k_excl_scan_u64<<<1, 1024, 0, s>>>(cnz, ncta, cnz0, misc + M_SCAN_TOT2);                                  \
+    { KT(ACTC_KIND_COUNT);                                                                                     \
+      k3_count<T, W><<<ncta, K3_THREADS, smem_count, s>>>((const T *)sym, n, ct, cwin_lo, cwin_n, tpc, cbits, cnz); } \
+    { KT(ACTC_KIND_SCAN);                                                                                      \
+      k_excl_scan_u64<<<1, 1024, 0, s>>>(cbits, ncta, cbit0, misc + M_SCAN_TOT); }                             \
+    { KT(ACTC_KIND_SCAN);                                                                                      \
+      k_excl_scan_u64<<<1, 1024, 0, s>>>(cnz, ncta, cnz0, misc + M_SCAN_TOT2); }                               \
+    KT(ACTC_KIND_PACK);                                                                                        \
     k3_pack<T, W><<<ncta, K3_THREADS, smem_pack, s>>>((const T *)sym, n, ct, win_lo, win_n, word_cap, tpc, x,  \
                                                       cbit0, cnz0, (uint32_t *)payload,                        \
                                                       (unsigned long long *)out_idx, out_val,                  \
@@ -359,7 +461,10 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     if (wide) K3_LAUNCH(uint32_t, true); else K3_LAUNCH(uint32_t, false);
   }
 #undef K3_LAUNCH
-  k3_fixup<<<1, 1024, 0, s>>>((uint32_t *)payload, cbit0, cbits, head, tail, ncta);
+  {
+    KT(ACTC_KIND_FIXUP);
+    k3_fixup<<<1, 1024, 0, s>>>((uint32_t *)payload, cbit0, cbits, head, tail, ncta);
+  }
   CKL();
   return ACTC_OK;
 }
@@ -400,7 +505,10 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
   CK(cudaMemsetAsync(ticket, 0, 8, s));
   CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
-  k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p);
+  {
+    KT(ACTC_KIND_LUT);
+    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p);
+  }
   CKL();
   DecodeArgs a;
   a.n = S.n;
@@ -427,6 +535,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.chunk_lat = (const long long *)S.chunk_lat_dev;
   a.live = S.live_symbols;
   const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
+  KT(ACTC_KIND_DECODE);
   if (S.chunk_lat_dev || mode == 2) {
     // warp decoder: no scan, no look-back
     const int NW = K4W_THREADS / 32;
@@ -497,24 +606,36 @@ int actc_build_chunk_index(actc_ctx *c, const actc_stream_t *S, uint64_t *chunk_
   unsigned *changed = (unsigned *)(misc + M_CHANGED);
   unsigned *status = (unsigned *)(misc + M_STATUS);
   CK(cudaMemsetAsync(misc + M_STATUS, 0, 8, s));
-  k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S->canon_syms_dev, S->len_counts_dev, (uint32_t *)c->lut.p);
+  {
+    KT(ACTC_KIND_LUT);
+    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S->canon_syms_dev, S->len_counts_dev, (uint32_t *)c->lut.p);
+  }
   CKL();
   const int tpb = 128;
   const int grid = (int)cdiv(nseg, tpb);
   const uint32_t *pw = (const uint32_t *)S->payload_dev;
-  k_sync_pass<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
-                                   nseg, start, endp, cnt, changed, status, 1);
+  {
+    KT(ACTC_KIND_INDEX);
+    k_sync_pass<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
+                                     nseg, start, endp, cnt, changed, status, 1);
+  }
   CKL();
   unsigned h_changed = 1;
   for (uint64_t it = 0; it <= nseg + 1 && h_changed; it++) {
     CK(cudaMemsetAsync(changed, 0, 4, s));
-    k_sync_pass<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
-                                     nseg, start, endp, cnt, changed, status, 0);
+    {
+      KT(ACTC_KIND_INDEX);
+      k_sync_pass<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
+                                       nseg, start, endp, cnt, changed, status, 0);
+    }
     CKL();
     CK(cudaMemcpyAsync(&h_changed, changed, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }
-  k_excl_scan_u64<<<1, 1024, 0, s>>>(cnt, nseg, base, misc + M_SCAN_TOT);
+  {
+    KT(ACTC_KIND_INDEX);
+    k_excl_scan_u64<<<1, 1024, 0, s>>>(cnt, nseg, base, misc + M_SCAN_TOT);
+  }
   CKL();
   unsigned long long total = 0, last_end = 0;
   unsigned st = 0;
@@ -526,17 +647,22 @@ int actc_build_chunk_index(actc_ctx *c, const actc_stream_t *S, uint64_t *chunk_
     *status_host = ACTC_EFORMAT;
     return ACTC_OK;
   }
-  k_index_emit<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
-                                    nseg, start, base, S->n, (unsigned long long *)chunk_off);
+  {
+    KT(ACTC_KIND_INDEX);
+    k_index_emit<<<grid, tpb, 0, s>>>(pw, S->payload_bits, (const uint32_t *)c->lut.p, S->len_counts_dev, seg_bits,
+                                      nseg, start, base, S->n, (unsigned long long *)chunk_off);
+  }
   CKL();
   return ACTC_OK;
 }
 
-int actc_prequantize(const void *x, int dtype, uint64_t n, double eb, int64_t *q, actc_stream s) {
+int actc_prequantize(const void *x, int dtype, uint64_t n, double eb, int64_t *q, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
   if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
   if (!n) return ACTC_OK;
   int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 16);
-  k_prequantize<<<grid, 256, 0, (cudaStream_t)s>>>(x, dtype, n, eb, (long long *)q);
+  KT(ACTC_KIND_DEBUG);
+  k_prequantize<<<grid, 256, 0, s>>>(x, dtype, n, eb, (long long *)q);
   CKL();
   return ACTC_OK;
 }
@@ -550,6 +676,7 @@ int actc_lorenzo_encode(const int64_t *lat, uint64_t n, uint32_t radius, const u
   CK(cudaMemsetAsync(d_cnt, 0, 8, s));
   if (n) {
     int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 16);
+    KT(ACTC_KIND_DEBUG);
     k_lorenzo_encode<<<grid, 256, 0, s>>>((const long long *)lat, n, radius, force, sym, d_cnt);
     CKL();
   }
@@ -563,7 +690,10 @@ int actc_lorenzo_decode(const uint32_t *sym, uint64_t n, const int64_t *olat, ui
   static thread_local unsigned *d_st = nullptr;
   if (!d_st) CK(cudaMalloc(&d_st, 4));
   CK(cudaMemsetAsync(d_st, 0, 4, s));
-  k_lorenzo_decode_seq<<<1, 1, 0, s>>>(sym, n, (const long long *)olat, k, radius, (long long *)out, d_st);
+  {
+    KT(ACTC_KIND_DEBUG);
+    k_lorenzo_decode_seq<<<1, 1, 0, s>>>(sym, n, (const long long *)olat, k, radius, (long long *)out, d_st);
+  }
   CKL();
   CK(cudaMemcpyAsync(status_host, d_st, 4, cudaMemcpyDeviceToHost, s));
   return ACTC_OK;
@@ -582,6 +712,7 @@ int actc_huffman_plan(actc_ctx *c, const uint32_t *sym, uint64_t n, uint64_t A, 
   uint32_t win_n = (uint32_t)std::min<uint64_t>(A, K1_WIN);
   if (n) {
     int grid = (int)std::min<uint64_t>(cdiv(n, 256), (uint64_t)c->num_sms * 4);
+    KT(ACTC_KIND_DEBUG);
     k_hist_u32<<<grid, 256, win_n * 4, s>>>(sym, n, A, (unsigned long long *)c->hist.p, (unsigned *)(misc + M_BAD), win_n);
     CKL();
   }
@@ -636,6 +767,7 @@ int actc_count_nonzero(const void *x, int dtype, uint64_t n, uint64_t *out_host,
   CK(cudaMemsetAsync(d, 0, 8, s));
   if (n) {
     int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 8);
+    KT(ACTC_KIND_STATS);
     k_count_nonzero<<<grid, 256, 0, s>>>(x, dtype, n, d);
     CKL();
   }
@@ -652,9 +784,15 @@ int actc_mean_abs(actc_ctx *c, const void *x, int dtype, uint64_t n, double *out
   if ((rc = grow(c->part, 8ull * ((1ull << depth) + 1)))) return rc;
   double *part = (double *)c->part.p;
   uint64_t nt = 1ull << depth;
-  k_pairwise_partials<<<(int)cdiv(nt, 128), 128, 0, s>>>(x, dtype, n, depth, part);
+  {
+    KT(ACTC_KIND_STATS);
+    k_pairwise_partials<<<(int)cdiv(nt, 128), 128, 0, s>>>(x, dtype, n, depth, part);
+  }
   CKL();
-  k_pairwise_finish<<<1, 1, 0, s>>>(part, dtype, n, depth, part + nt);
+  {
+    KT(ACTC_KIND_STATS);
+    k_pairwise_finish<<<1, 1, 0, s>>>(part, dtype, n, depth, part + nt);
+  }
   CKL();
   CK(cudaMemcpyAsync(out_host, part + nt, 8, cudaMemcpyDeviceToHost, s));
   return ACTC_OK;
@@ -673,10 +811,14 @@ int actc_lbar(actc_ctx *c, const void *g, int dtype, uint64_t N, uint64_t per, v
   uint64_t total = N * per;
   if (total) {
     int grid = (int)std::min<uint64_t>(cdiv(total, 256), 148 * 8);
+    KT(ACTC_KIND_STATS);
     k_sample_max<<<grid, 256, 0, s>>>(g, dtype, N, per, bits);
     CKL();
   }
-  k_lbar_finish<<<1, 1, 0, s>>>(bits, dtype, N, psm, res);
+  {
+    KT(ACTC_KIND_STATS);
+    k_lbar_finish<<<1, 1, 0, s>>>(bits, dtype, N, psm, res);
+  }
   CKL();
   CK(cudaMemcpyAsync(out_host, res, 8, cudaMemcpyDeviceToHost, s));
   return ACTC_OK;
