@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
   const uint64_t nfull = n / K1_TILE;  // tiles with no element past n
   const int R = (int)min(radius, 0x40000000u);
   unsigned outl = 0;
+  unsigned zc = 0;  // zero deltas (symbol `radius`, the dominant one): counted in a register
   bool fin_all = true;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t base = tile * K1_TILE + (uint64_t)threadIdx.x * K1_EPT;
@@ -120,7 +121,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
         const uint32_t sj = o ? 0u : (uint32_t)(d + R);
         s[j] = sj;
         outl += o;
-        k1_hist_add(hbase, win_lo, win_n, ghist, sj);
+        if (d == 0)
+          zc++;
+        else
+          k1_hist_add(hbase, win_lo, win_n, ghist, sj);
       }
       k1_store<SymT>(sym, base, s);
     } else {
@@ -151,7 +155,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
         s[j] = sj;
         if (base + j < n) {
           outl += o;
-          k1_hist_add(hbase, win_lo, win_n, ghist, sj);
+          if (sj == radius)
+            zc++;
+          else
+            k1_hist_add(hbase, win_lo, win_n, ghist, sj);
         }
       }
       if (full_tile) {
@@ -166,6 +173,14 @@ __global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
   if (!__all_sync(0xffffffffu, fin_all) && !fin_all) atomicOr(nonfinite, 1u);  // tensor.py:56-57
   unsigned wsum = warp_sum(outl);
   if (lane == 0 && wsum) atomicAdd(n_outliers, (unsigned long long)wsum);
+  const unsigned zsum = warp_sum(zc);
+  if (lane == 0 && zsum) {
+    const uint32_t w = radius - win_lo;
+    if (w < win_n)
+      atomicAdd(&sh_hist[w], zsum);
+    else
+      atomicAdd(&ghist[radius], (unsigned long long)zsum);
+  }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) {
     unsigned c = sh_hist[i];

@@ -16,4 +16,13 @@ timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k1_|k2_|k3_|k_excl|k_build|k4w_" -s 45 -c 45 \
    -o gpurun_out/${TAG}_step -f python tools/prof_workload.py --steps 2 > gpurun_out/${TAG}_ncu_full.log 2>&1
 ncu -i gpurun_out/${TAG}_step.ncu-rep --page raw --csv > gpurun_out/${TAG}_step_raw.csv 2>/dev/null
+ncu -i gpurun_out/${TAG}_step.ncu-rep --page details --csv > gpurun_out/${TAG}_step_details.csv 2>/dev/null
+for k in k4w_decode k1_quant_lorenzo_hist k3_pack k2_codebook; do
+  ncu -i gpurun_out/${TAG}_step.ncu-rep --page source --csv --print-source sass -k regex:$k -c 1 > gpurun_out/${TAG}_src_$k.csv 2>/dev/null
+done
+# the copy-back limit is 64 MiB: keep the report only when small
+sz=$(stat -c %s gpurun_out/${TAG}_step.ncu-rep 2>/dev/null || echo 0)
+if [ "$sz" -gt 30000000 ]; then mv gpurun_out/${TAG}_step.ncu-rep /tmp/; fi
+gzip -f gpurun_out/${TAG}_src_*.csv gpurun_out/${TAG}_step_raw.csv gpurun_out/${TAG}_step_details.csv
+du -sh gpurun_out
 ls -la gpurun_out | tail -20
