@@ -311,7 +311,8 @@ int actc_ctx_create(int device, actc_ctx **out) {
                        (const void *)k3_pack<uint32_t, false>,  (const void *)k3_pack<uint32_t, true>,
                        (const void *)k4w_decode<0, 16>,         (const void *)k4w_decode<1, 16>,
                        (const void *)k4w_decode<0, 32>,         (const void *)k4w_decode<1, 32>,
-                       (const void *)k4w_decode<2, 32>};
+                       (const void *)k4w_decode<2, 32>,         (const void *)k3_encode_lb<uint16_t>,
+                       (const void *)k3_encode_lb<uint32_t>};
   for (const void *f : big) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, f));
@@ -413,6 +414,50 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     if (wl + cap > hi + 1) wl = hi + 1 - cap;
     win_lo = wl;
     win_n = cap;
+  }
+  if (!wide && !getenv("ACTC_K3_TWO_PASS")) {
+    // single pass: warp per 1024-symbol segment, decoupled look-back
+    const uint64_t nseg = cdiv(n, K3L_SEG);
+    uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
+    if (span > K3L_WIN) {
+      uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
+      uint32_t wl = centre > K3L_WIN / 2 ? centre - K3L_WIN / 2 : 0;
+      if (wl < lo) wl = lo;
+      if (wl + K3L_WIN > hi + 1) wl = hi + 1 - K3L_WIN;
+      lwin_lo = wl;
+    }
+    const size_t smem = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
+    if ((rc = grow(c->status, nseg * 24 + 1024))) return rc;
+    char *b = (char *)c->status.p;
+    EncLB st;
+    st.inc_bits = (unsigned long long *)b;
+    st.inc_nz = st.inc_bits + nseg;
+    st.flag = (unsigned *)(st.inc_nz + nseg);
+    st.agg = st.flag + nseg;
+    unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
+    CK(cudaMemsetAsync(st.flag, 0, nseg * 4, s));
+    CK(cudaMemsetAsync(ticket, 0, 4, s));
+    CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
+    const void *f = sb == 2 ? (const void *)k3_encode_lb<uint16_t> : (const void *)k3_encode_lb<uint32_t>;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, K3L_THREADS, smem);
+    const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), want));
+    {
+      KT(ACTC_KIND_PACK);
+      if (sb == 2)
+        k3_encode_lb<uint16_t><<<grid, K3L_THREADS, smem, s>>>((const uint16_t *)sym, n, (const unsigned long long *)c->ctab.p,
+                                                               lwin_lo, lwin_n, x, (uint32_t *)payload,
+                                                               (unsigned long long *)out_idx, out_val,
+                                                               (unsigned long long *)chunk_off, st, ticket, extract);
+      else
+        k3_encode_lb<uint32_t><<<grid, K3L_THREADS, smem, s>>>((const uint32_t *)sym, n, (const unsigned long long *)c->ctab.p,
+                                                               lwin_lo, lwin_n, x, (uint32_t *)payload,
+                                                               (unsigned long long *)out_idx, out_val,
+                                                               (unsigned long long *)chunk_off, st, ticket, extract);
+    }
+    CKL();
+    return ACTC_OK;
   }
   const uint32_t maxlen = plan->max_len ? plan->max_len : 1;
   const uint32_t word_cap = (uint32_t)(((uint64_t)2 * K3_TILE * maxlen + 31) / 32 + 4);  // pack tile = 2*K3_TILE

@@ -1,0 +1,220 @@
+// K3 (single pass): canonical-Huffman encode + MSB-first bit packing +
+// outlier extraction + decode chunk index, one warp per segment.
+//
+// Replaces huffman.py:188-207 (code lookup, np.packbits) and codec.py:321-322
+// (outlier indices / values) for codes of at most K3_SHORT_MAXLEN bits.
+//
+// A segment is 1024 consecutive symbols: lane l owns 32 of them.  The warp
+//   1. loads its symbols (read once), sums code lengths / outlier markers,
+//   2. publishes the segment aggregate, then finds its exclusive bit prefix by
+//      decoupled look-back over the preceding segments (32 per probe, summing
+//      aggregates until an inclusive prefix is met), publishes the inclusive
+//      prefix,
+//   3. packs its codes into a per-warp shared word buffer (plain stores for
+//      words a lane owns, shared atomicOr for the two it shares with its
+//      neighbours) and stores the words coalesced, big-endian; the two words
+//      it shares with the neighbouring segments are OR-ed into the
+//      zero-initialised payload.
+// Segments are claimed in order through a global ticket, so every segment's
+// predecessors are already running: the look-back always terminates.
+// No block barrier after the table load; warps are fully independent.
+#include "kernels.cuh"
+
+namespace actc {
+
+namespace {
+
+constexpr uint32_t kSent = 0xFFFFFFFFu;  // symbol past the end of the stream
+
+template <typename SymT>
+__device__ __forceinline__ void lb_load(const SymT *__restrict__ sym, uint64_t base, uint64_t n,
+                                        uint32_t (&s)[K3L_EPT]) {
+  if (base + K3L_EPT <= n) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
+    if (sizeof(SymT) == 2) {
+#pragma unroll
+      for (int j = 0; j < K3L_EPT / 8; j++) {
+        const uint4 v = __ldcs(p + j);  // streaming: the symbol buffer is read once
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          s[8 * j + 2 * k] = w4[k] & 0xFFFFu;
+          s[8 * j + 2 * k + 1] = w4[k] >> 16;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < K3L_EPT / 4; j++) {
+        const uint4 v = __ldcs(p + j);
+        s[4 * j] = v.x; s[4 * j + 1] = v.y; s[4 * j + 2] = v.z; s[4 * j + 3] = v.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < K3L_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : kSent;
+  }
+}
+
+// (code << 6) | len from the shared window, else from the global table
+__device__ __forceinline__ uint32_t lb_entry(const uint32_t *tab, const unsigned long long *__restrict__ ctab,
+                                             uint32_t win_lo, uint32_t win_n, uint32_t s) {
+  const uint32_t wi = s - win_lo;
+  if (wi < win_n) return tab[wi];
+  const unsigned long long g = __ldg(&ctab[s]);
+  return (uint32_t)(((g >> 8) << 6) | (g & 63));
+}
+
+}  // namespace
+
+template <typename SymT>
+__global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
+    const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab, uint32_t win_lo,
+    uint32_t win_n, const float *__restrict__ x, uint32_t *__restrict__ payload,
+    unsigned long long *__restrict__ out_idx, float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
+    EncLB st, unsigned *__restrict__ ticket, int extract_outliers) {
+  extern __shared__ __align__(16) uint32_t k3l_sm[];
+  uint32_t *tab = k3l_sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < win_n; i += K3L_THREADS) {
+    const unsigned long long e = ctab[win_lo + i];
+    tab[i] = (uint32_t)(((e >> 8) << 6) | (e & 63));
+  }
+  __syncthreads();
+  uint32_t *wb = k3l_sm + ((win_n + 3) & ~3u) + warp * K3L_WORDS;
+  const uint64_t nseg = (n + K3L_SEG - 1) / K3L_SEG;
+
+  while (true) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    const uint64_t seg = __shfl_sync(0xffffffffu, t, 0);
+    if (seg >= nseg) break;
+    const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
+    uint32_t s[K3L_EPT];
+    lb_load(sym, base, n, s);
+
+    // ---- 1. code lengths and outlier markers ----
+    uint32_t bits = 0, nz = 0;
+#pragma unroll
+    for (int j = 0; j < K3L_EPT; j++) {
+      if (s[j] != kSent) {
+        bits += lb_entry(tab, ctab, win_lo, win_n, s[j]) & 63;
+        nz += s[j] == 0;
+      }
+    }
+    const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nz);
+    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31), seg_nz = __shfl_sync(0xffffffffu, iz, 31);
+
+    // ---- 2. publish, look back, publish the inclusive prefix ----
+    unsigned long long pb = 0, pz = 0;
+    if (seg == 0) {
+      if (lane == 0) {
+        st.inc_bits[0] = seg_bits;
+        st.inc_nz[0] = seg_nz;
+        st_release(&st.flag[0], kFlagInc);
+      }
+    } else {
+      if (lane == 0) {
+        st.agg[seg] = (seg_bits << 11) | seg_nz;
+        st_release(&st.flag[seg], kFlagAgg);
+      }
+      long long p = (long long)seg - 1;
+      while (true) {
+        const long long idx = p - lane;
+        unsigned f = kFlagInc;  // before segment 0: an inclusive prefix of zero
+        if (idx >= 0) {
+          do {
+            f = ld_acquire(&st.flag[idx]);
+          } while (f == 0);
+        }
+        const unsigned im = __ballot_sync(0xffffffffu, f == kFlagInc);
+        const int stop = im ? __ffs(im) - 1 : 32;
+        unsigned long long vb = 0, vz = 0;
+        if (idx >= 0 && lane <= stop) {
+          if (lane == stop) {
+            vb = st.inc_bits[idx];
+            vz = st.inc_nz[idx];
+          } else {
+            const unsigned g = st.agg[idx];
+            vb = g >> 11;
+            vz = g & 2047u;
+          }
+        }
+        pb += warp_sum(vb);
+        pz += warp_sum(vz);
+        if (im) break;
+        p -= 32;
+      }
+      if (lane == 0) {
+        st.inc_bits[seg] = pb + seg_bits;
+        st.inc_nz[seg] = pz + seg_nz;
+        st_release(&st.flag[seg], kFlagInc);
+      }
+    }
+
+    // ---- 3. pack ----
+    const uint32_t off0 = (uint32_t)(pb & 31);
+    const uint32_t nw = (off0 + seg_bits + 31) >> 5;
+    for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
+    __syncwarp();
+    const uint32_t lane_ex = ib - bits;
+    if ((lane & 7) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
+    if (extract_outliers && nz) {
+      unsigned long long o = pz + (iz - nz);
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] == 0) {
+          out_idx[o] = base + j;
+          out_val[o] = x[base + j];
+          o++;
+        }
+      }
+    }
+    if (bits) {
+      // codes <= 26 bits complete at most one word each: predicated emits;
+      // the lane's first word and final partial word may be shared -> atomic
+      const uint32_t rel = off0 + lane_ex;
+      uint32_t w = rel >> 5;
+      const uint32_t w0 = w;
+      int nb = rel & 31;
+      unsigned long long acc = 0;
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const bool pad = s[j] == kSent;
+        const uint32_t e = lb_entry(tab, ctab, win_lo, win_n, pad ? win_lo : s[j]);
+        const int lj = pad ? 0 : (int)(e & 63);
+        const unsigned long long cj = e >> 6;
+        acc |= lj ? cj << (64 - nb - lj) : 0ull;
+        nb += lj;
+        const bool ready = nb >= 32;
+        const uint32_t hiw = (uint32_t)(acc >> 32);
+        if (ready && w == w0) atomicOr(&wb[w], hiw);
+        if (ready && w != w0) wb[w] = hiw;
+        acc = ready ? (acc << 32) : acc;
+        nb = ready ? nb - 32 : nb;
+        w += ready;
+      }
+      if (nb > 0) atomicOr(&wb[w], (uint32_t)(acc >> 32));
+    }
+    __syncwarp();
+    const uint64_t gw0 = pb >> 5;
+    const uint32_t end_off = (off0 + seg_bits) & 31;
+    for (uint32_t i = lane; i < nw; i += 32) {
+      const uint32_t v = bswap32(wb[i]);
+      const bool shared_word = (i == 0 && off0 != 0) || (i == nw - 1 && end_off != 0);
+      if (shared_word)
+        atomicOr(&payload[gw0 + i], v);
+      else
+        payload[gw0 + i] = v;
+    }
+    __syncwarp();
+  }
+}
+
+template __global__ void k3_encode_lb<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *, uint32_t,
+                                                uint32_t, const float *, uint32_t *, unsigned long long *, float *,
+                                                unsigned long long *, EncLB, unsigned *, int);
+template __global__ void k3_encode_lb<uint32_t>(const uint32_t *, uint64_t, const unsigned long long *, uint32_t,
+                                                uint32_t, const float *, uint32_t *, unsigned long long *, float *,
+                                                unsigned long long *, EncLB, unsigned *, int);
+
+}  // namespace actc

@@ -21,6 +21,13 @@ constexpr int K3_TILE = K3_THREADS * K3_EPT;
 constexpr uint32_t K3_WIN32 = 32768;  // u32 code-table window (codes <= 26 bits)
 constexpr uint32_t K3_WIN64 = 8192;   // u64 window for longer codes
 constexpr int K3_SHORT_MAXLEN = 26;
+// K3 single-pass encoder (codes <= K3_SHORT_MAXLEN): one warp per segment of
+// 32 lanes x 32 symbols, decoupled look-back over segments
+constexpr int K3L_THREADS = 256;
+constexpr int K3L_EPT = 32;
+constexpr int K3L_SEG = 32 * K3L_EPT;                                     // symbols per segment
+constexpr uint32_t K3L_WIN = 8192;                                        // u32 code-table window
+constexpr int K3L_WORDS = (K3L_SEG * K3_SHORT_MAXLEN + 31) / 32 + 2;      // packed words per segment (max)
 
 // K4 (scan variant, streams without a lattice index): one thread per chunk
 constexpr int K4_THREADS = 128;
@@ -97,6 +104,18 @@ __global__ void k3_pack(const SymT *__restrict__ sym, uint64_t n, const unsigned
                         unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
                         unsigned long long *__restrict__ chunk_off, uint32_t *__restrict__ head,
                         uint32_t *__restrict__ tail, int extract_outliers);
+// single-pass encoder look-back state (per segment)
+struct EncLB {
+  unsigned *flag;                     // 0 = empty, kFlagAgg, kFlagInc
+  unsigned *agg;                      // (bits << 11) | outliers of the segment
+  unsigned long long *inc_bits, *inc_nz;  // inclusive prefixes
+};
+template <typename SymT>
+__global__ void k3_encode_lb(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
+                             uint32_t win_lo, uint32_t win_n, const float *__restrict__ x,
+                             uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
+                             float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off, EncLB st,
+                             unsigned *__restrict__ ticket, int extract_outliers);
 __global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
                          const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
                          const uint32_t *__restrict__ tail, uint32_t ncta);
