@@ -417,7 +417,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
   }
   if (!wide && !getenv("ACTC_K3_TWO_PASS")) {
     // single pass: warp per 1024-symbol segment, decoupled look-back
-    const uint64_t nseg = cdiv(n, K3L_SEG);
+    const uint64_t nseg = cdiv(n, (uint64_t)K3L_SEG * (K3L_THREADS / 32));  // look-back tiles
     uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
     if (span > K3L_WIN) {
       uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
@@ -442,7 +442,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, K3L_THREADS, smem);
     const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), want));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nseg, want));
     {
       KT(ACTC_KIND_PACK);
       if (sb == 2)

@@ -6,18 +6,19 @@
 //
 // A segment is 1024 consecutive symbols: lane l owns 32 of them.  The warp
 //   1. loads its symbols (read once), sums code lengths / outlier markers,
-//   2. publishes the segment aggregate, then finds its exclusive bit prefix by
-//      decoupled look-back over the preceding segments (32 per probe, summing
-//      aggregates until an inclusive prefix is met), publishes the inclusive
-//      prefix,
+//   2. the CTA publishes its tile aggregate, then finds the tile's exclusive
+//      bit prefix by decoupled look-back over the preceding tiles (summing
+//      aggregates until an inclusive prefix is met) and publishes the
+//      inclusive prefix,
 //   3. packs its codes into a per-warp shared word buffer (plain stores for
 //      words a lane owns, shared atomicOr for the two it shares with its
 //      neighbours) and stores the words coalesced, big-endian; the two words
 //      it shares with the neighbouring segments are OR-ed into the
 //      zero-initialised payload.
-// Segments are claimed in order through a global ticket, so every segment's
-// predecessors are already running: the look-back always terminates.
-// No block barrier after the table load; warps are fully independent.
+// The look-back runs per CTA tile (8 segments, one per warp; warp 0 probes
+// 128 predecessor tiles per round trip).  Tiles are claimed in order through
+// a global ticket, so every tile's predecessors are already running: the
+// look-back always terminates.
 #include "kernels.cuh"
 
 namespace actc {
@@ -72,22 +73,26 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
     uint32_t win_n, const float *__restrict__ x, uint32_t *__restrict__ payload,
     unsigned long long *__restrict__ out_idx, float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
     EncLB st, unsigned *__restrict__ ticket, int extract_outliers) {
+  constexpr int NW = K3L_THREADS / 32;
   extern __shared__ __align__(16) uint32_t k3l_sm[];
+  __shared__ uint32_t s_wbits[NW], s_wnz[NW];
+  __shared__ unsigned long long s_pb, s_pz;
+  __shared__ unsigned s_tile;
   uint32_t *tab = k3l_sm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < win_n; i += K3L_THREADS) {
     const unsigned long long e = ctab[win_lo + i];
     tab[i] = (uint32_t)(((e >> 8) << 6) | (e & 63));
   }
-  __syncthreads();
   uint32_t *wb = k3l_sm + ((win_n + 3) & ~3u) + warp * K3L_WORDS;
-  const uint64_t nseg = (n + K3L_SEG - 1) / K3L_SEG;
+  const uint64_t ntiles = (n + (uint64_t)K3L_SEG * NW - 1) / ((uint64_t)K3L_SEG * NW);
 
   while (true) {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1u);
-    const uint64_t seg = __shfl_sync(0xffffffffu, t, 0);
-    if (seg >= nseg) break;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();  // also orders the table load / the previous tile's smem use
+    const uint64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint64_t seg = tile * NW + warp;
     const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
     uint32_t s[K3L_EPT];
     lb_load(sym, base, n, s);
@@ -102,54 +107,88 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
       }
     }
     const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nz);
-    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31), seg_nz = __shfl_sync(0xffffffffu, iz, 31);
+    if (lane == 31) {
+      s_wbits[warp] = ib;
+      s_wnz[warp] = iz;
+    }
+    __syncthreads();
 
-    // ---- 2. publish, look back, publish the inclusive prefix ----
-    unsigned long long pb = 0, pz = 0;
-    if (seg == 0) {
-      if (lane == 0) {
-        st.inc_bits[0] = seg_bits;
-        st.inc_nz[0] = seg_nz;
-        st_release(&st.flag[0], kFlagInc);
-      }
-    } else {
-      if (lane == 0) {
-        st.agg[seg] = (seg_bits << 11) | seg_nz;
-        st_release(&st.flag[seg], kFlagAgg);
-      }
-      long long p = (long long)seg - 1;
-      while (true) {
-        const long long idx = p - lane;
-        unsigned f = kFlagInc;  // before segment 0: an inclusive prefix of zero
-        if (idx >= 0) {
-          do {
-            f = ld_acquire(&st.flag[idx]);
-          } while (f == 0);
+    // ---- 2. tile aggregate, look-back over tiles (warp 0), inclusive prefix ----
+    if (warp == 0) {
+      const uint32_t wbv = lane < NW ? s_wbits[lane] : 0u, wzv = lane < NW ? s_wnz[lane] : 0u;
+      const uint32_t tb = warp_sum(wbv), tz = warp_sum(wzv);
+      unsigned long long pb = 0, pz = 0;
+      if (tile == 0) {
+        if (lane == 0) {
+          st.inc_bits[0] = tb;
+          st.inc_nz[0] = tz;
+          st_release(&st.flag[0], kFlagInc);
         }
-        const unsigned im = __ballot_sync(0xffffffffu, f == kFlagInc);
-        const int stop = im ? __ffs(im) - 1 : 32;
-        unsigned long long vb = 0, vz = 0;
-        if (idx >= 0 && lane <= stop) {
-          if (lane == stop) {
-            vb = st.inc_bits[idx];
-            vz = st.inc_nz[idx];
-          } else {
-            const unsigned g = st.agg[idx];
-            vb = g >> 11;
-            vz = g & 2047u;
+      } else {
+        if (lane == 0) {
+          st.agg[tile] = (tb << 14) | tz;  // tb < 2^18, tz <= 8192
+          st_release(&st.flag[tile], kFlagAgg);
+        }
+        // probe 128 predecessors per round trip: lane l owns p-l, p-l-32, ...
+        long long p = (long long)tile - 1;
+        while (true) {
+          unsigned f[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const long long idx = p - lane - 32 * k;
+            f[k] = kFlagInc;
+            if (idx >= 0) {
+              do {
+                f[k] = ld_acquire(&st.flag[idx]);
+              } while (f[k] == 0);
+            }
           }
+          // nearest inclusive prefix: smallest distance d = lane + 32k
+          int stop = 128;
+#pragma unroll
+          for (int k = 3; k >= 0; k--) {
+            const unsigned im = __ballot_sync(0xffffffffu, f[k] == kFlagInc);
+            if (im) stop = 32 * k + __ffs(im) - 1;
+          }
+          unsigned long long vb = 0, vz = 0;
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int d = lane + 32 * k;
+            const long long idx = p - d;
+            if (idx >= 0 && d <= stop) {
+              if (d == stop) {
+                vb += st.inc_bits[idx];
+                vz += st.inc_nz[idx];
+              } else {
+                const unsigned g = st.agg[idx];
+                vb += g >> 14;
+                vz += g & 16383u;
+              }
+            }
+          }
+          pb += warp_sum(vb);
+          pz += warp_sum(vz);
+          if (stop < 128) break;
+          p -= 128;
         }
-        pb += warp_sum(vb);
-        pz += warp_sum(vz);
-        if (im) break;
-        p -= 32;
+        if (lane == 0) {
+          st.inc_bits[tile] = pb + tb;
+          st.inc_nz[tile] = pz + tz;
+          st_release(&st.flag[tile], kFlagInc);
+        }
       }
       if (lane == 0) {
-        st.inc_bits[seg] = pb + seg_bits;
-        st.inc_nz[seg] = pz + seg_nz;
-        st_release(&st.flag[seg], kFlagInc);
+        s_pb = pb;
+        s_pz = pz;
       }
     }
+    __syncthreads();
+    unsigned long long pb = s_pb, pz = s_pz;
+    for (int w = 0; w < warp; w++) {
+      pb += s_wbits[w];
+      pz += s_wnz[w];
+    }
+    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31);
 
     // ---- 3. pack ----
     const uint32_t off0 = (uint32_t)(pb & 31);
@@ -171,7 +210,8 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
     }
     if (bits) {
       // codes <= 26 bits complete at most one word each: predicated emits;
-      // the lane's first word and final partial word may be shared -> atomic
+      // the lane's first word and final partial word may be shared -> atomic.
+      // A pad symbol has len 0: the 64-bit shift by >= 64 yields 0.
       const uint32_t rel = off0 + lane_ex;
       uint32_t w = rel >> 5;
       const uint32_t w0 = w;
@@ -180,8 +220,8 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
         const bool pad = s[j] == kSent;
-        const uint32_t e = lb_entry(tab, ctab, win_lo, win_n, pad ? win_lo : s[j]);
-        const int lj = pad ? 0 : (int)(e & 63);
+        const uint32_t e = pad ? 0u : lb_entry(tab, ctab, win_lo, win_n, s[j]);
+        const int lj = (int)(e & 63);
         const unsigned long long cj = e >> 6;
         acc |= lj ? cj << (64 - nb - lj) : 0ull;
         nb += lj;
@@ -206,7 +246,6 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
       else
         payload[gw0 + i] = v;
     }
-    __syncwarp();
   }
 }
 
