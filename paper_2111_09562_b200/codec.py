@@ -464,10 +464,12 @@ _side_streams: dict = {}
 
 
 def _stream_pool(device, k):
+    """Side streams; slot r has a higher priority than slot r+1 (torch maps
+    the request onto the device's priority range)."""
     torch = _lib.torch_cuda()
     pool = _side_streams.setdefault(device, [])
     while len(pool) < k:
-        pool.append(torch.cuda.Stream(device=device))
+        pool.append(torch.cuda.Stream(device=device, priority=-(8 - len(pool))))
     return pool[:k]
 
 
@@ -490,8 +492,12 @@ def compress_batch(xs, params, max_concurrency: int = 8):
     dev_index = xs[0].device.index if xs else torch.cuda.current_device()
     main = torch.cuda.current_stream()
     results = []
+    # smallest tensors first, on the highest-priority streams: their K1 ends
+    # early, so the (single-CTA) codebooks start while the large tensors are
+    # still being quantized
+    order = sorted(range(len(xs)), key=lambda i: xs[i].numel())
     for g0 in range(0, len(xs), max_concurrency):
-        group = list(range(g0, min(len(xs), g0 + max_concurrency)))
+        group = order[g0:g0 + max_concurrency]
         streams = _stream_pool(dev_index, len(group))
         ready = main.record_event()
         jobs = []

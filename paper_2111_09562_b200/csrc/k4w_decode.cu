@@ -15,12 +15,14 @@
 // lattice values, reconstructed in fp64 and stored coalesced.  No block
 // barriers, no look-back: chunk start values come from the index.
 //
-// Decode step (uniform across the warp): a 12-bit LUT gives (symbol, length)
-// for codes <= 12 bits and a starting length l0 for longer prefixes; the
-// length is finished with up to three predicated comparisons against the
-// left-aligned canonical limits (skipped by warp vote when no lane needs
-// them), the symbol of a long code comes from canon[off[l] + (W >> (32-l))]
-// (shared-memory cache of the first codes in canonical order).
+// Decode step (one path for every lane): a 12-bit LUT gives (symbol, length)
+// for codes <= 12 bits and a starting length l0 for longer prefixes; three
+// comparisons against the left-aligned canonical limits finish the length
+// (for a short code they are all false: the limits are non-decreasing), and
+// the symbol of a long code comes from canon[off[l] + (W >> (32-l))] (shared
+// cache of the first codes in canonical order).  Only invalid streams and
+// codes longer than l0+3 take the warp-voted bit-serial fallback.  The next
+// payload word is loaded one refill ahead and byte-swapped when consumed.
 #include "kernels.cuh"
 
 namespace actc {
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
       buf = ((unsigned long long)bswap32(__ldg(src)) << 32) | bswap32(__ldg(src + 1));
       buf <<= (pos & 31);
       nb = 64 - (int)(pos & 31);
-      nextw = bswap32(__ldg(src + 2));
+      nextw = __ldg(src + 2);  // kept raw (big-endian); swapped when consumed
       src += 3;
       if (MODE != 2) P = a.chunk_lat[c];
     }
@@ -164,53 +166,54 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
 #define ACTC_DEC(SYM)                                                                             \
   {                                                                                               \
     if (nb < 32) {                                                                                \
-      buf |= (unsigned long long)nextw << (32 - nb);                                              \
+      buf |= (unsigned long long)bswap32(nextw) << (32 - nb);                                     \
       nb += 32;                                                                                   \
-      nextw = bswap32(__ldg(src));                                                                \
+      nextw = __ldg(src); /* raw: swapped at the next refill, so the load latency is hidden */   \
       ++src;                                                                                      \
     }                                                                                             \
     const uint32_t W = (uint32_t)(buf >> 32);                                                     \
     const uint32_t e = lds_u32(lut_s + ((W >> (32 - kLutBits)) << 2));                            \
-    int len = e & 63;                                                                             \
+    const uint32_t le = e & 63;                                                                   \
+    /* uniform step: short codes (le > 0) start the limit probes at their own length and */       \
+    /* stay there (limits are non-decreasing); long codes start at the LUT's l0 */                \
+    const uint32_t l0 = le ? le : (e >> 6);                                                       \
+    const uint32_t lb = lim_s + 4u * l0;                                                          \
+    const uint32_t l = l0 + (W > lds_u32(lb)) + (W > lds_u32(lb + 4u)) + (W > lds_u32(lb + 8u));  \
+    const bool c3 = W > lds_u32(lb + 12u);                                                        \
+    const bool ok = le || (fast_long && l0 >= 1 && !c3 && (int)l <= maxlen);                      \
+    int len = le ? (int)le : (int)l;                                                              \
     uint32_t sv = e >> 6;                                                                         \
-    if (__any_sync(__activemask(), len == 0)) {                                                   \
-      if (len == 0) {                                                                             \
-        /* long code: LUT gave l0; four independent limit probes finish it */                     \
-        const int l0 = (int)sv;                                                                   \
-        const uint32_t lb = lim_s + 4u * l0;                                                      \
-        const int c0 = W > lds_u32(lb), c1 = W > lds_u32(lb + 4u), c2 = W > lds_u32(lb + 8u);     \
-        const bool c3 = W > lds_u32(lb + 12u);                                                    \
-        const int l = l0 + c0 + c1 + c2;                                                          \
-        if (fast_long && l0 >= 1 && !c3 && l <= maxlen) {                                         \
-          const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                          \
-          sv = ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]);                       \
-          len = l;                                                                                \
-        } else {                                                                                  \
-          /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */        \
-          const uint64_t pos = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;                   \
-          const uint64_t win = read_bits64(pw, pos);                                              \
-          for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                       \
-            const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                \
-            if (of < s_count[ll]) {                                                               \
-              sv = a.canon[s_base[ll] + of];                                                      \
-              len = ll;                                                                           \
-              break;                                                                              \
-            }                                                                                     \
+    if (ok && !le) {                                                                              \
+      const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                              \
+      sv = ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]);                           \
+    }                                                                                             \
+    if (__any_sync(__activemask(), !ok)) {                                                        \
+      if (!ok) {                                                                                  \
+        /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */          \
+        const uint64_t pos = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;                     \
+        const uint64_t win = read_bits64(pw, pos);                                                \
+        len = 0;                                                                                  \
+        for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                         \
+          const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                  \
+          if (of < s_count[ll]) {                                                                 \
+            sv = a.canon[s_base[ll] + of];                                                        \
+            len = ll;                                                                             \
+            break;                                                                                \
           }                                                                                       \
-          if (!len) {                                                                             \
-            bad = true;                                                                           \
-            len = 1;                                                                              \
-            sv = a.radius;                                                                        \
-          }                                                                                       \
-          const uint64_t np = pos + len;                                                          \
-          src = pw + (np >> 5);                                                                   \
-          buf = ((unsigned long long)bswap32(src[0]) << 32) | bswap32(src[1]);                    \
-          buf <<= (np & 31);                                                                      \
-          nb = 64 - (int)(np & 31);                                                               \
-          nextw = bswap32(src[2]);                                                                \
-          src += 3;                                                                               \
-          len = 0;                                                                                \
         }                                                                                         \
+        if (!len) {                                                                               \
+          bad = true;                                                                             \
+          len = 1;                                                                                \
+          sv = a.radius;                                                                          \
+        }                                                                                         \
+        const uint64_t np = pos + len;                                                            \
+        src = pw + (np >> 5);                                                                     \
+        buf = ((unsigned long long)bswap32(src[0]) << 32) | bswap32(src[1]);                      \
+        buf <<= (np & 31);                                                                        \
+        nb = 64 - (int)(np & 31);                                                                 \
+        nextw = src[2];                                                                           \
+        src += 3;                                                                                 \
+        len = 0;                                                                                  \
       }                                                                                           \
     }                                                                                             \
     buf <<= len;                                                                                  \
