@@ -46,7 +46,7 @@ __device__ __forceinline__ void k1_store(SymT *__restrict__ sym, uint64_t base, 
 }
 
 template <typename SymT>
-__global__ void __launch_bounds__(K1_THREADS) k1_quant_lorenzo_hist(
+__global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
     const float *__restrict__ x, uint64_t n, QParams P, uint32_t radius, SymT *__restrict__ sym,
     unsigned long long *__restrict__ ghist, unsigned long long *__restrict__ n_outliers,
     uint32_t win_lo, uint32_t win_n, unsigned *__restrict__ nonfinite,
