@@ -127,6 +127,61 @@ def _payload_buffer_bytes(bits: int) -> int:
     return 4 * ((bits + 31) // 32) + 16
 
 
+class _DevBufs:
+    """Device arrays of one container.  Arrays produced by the encoder are
+    carved out of ONE uint8 allocation (`carve`); typed views are created
+    only when a caller indexes them -- the hot path uses `ptr()`.  Arrays
+    added individually (uploads, the lazily rebuilt index) are plain
+    tensors.  Mapping-like: [], in, values(), ptr()."""
+
+    __slots__ = ("_bufs", "_slots", "_views")
+
+    _DT = {"payload": "uint8", "out_idx": "int64", "out_val": "float32", "canon": "int32",
+           "len_counts": "int32", "chunk_off": "int64", "chunk_lat": "int64"}
+
+    def __init__(self):
+        self._bufs = []      # backing tensors (carved bases and plain arrays)
+        self._slots = {}     # name -> (base tensor, byte offset, numel, itemsize)
+        self._views = {}
+
+    def carve(self, device, layout):
+        """layout: [(name, numel, itemsize)] -> one allocation, 16-byte aligned slots."""
+        torch = _lib.torch_cuda()
+        offs, o = [], 0
+        for name, numel, isz in layout:
+            offs.append(o)
+            o += (numel * isz + 15) & ~15
+        base = torch.empty(max(o, 16), dtype=torch.uint8, device=device)
+        self._bufs.append(base)
+        for (name, numel, isz), off in zip(layout, offs):
+            self._slots[name] = (base, off, numel, isz)
+        return base
+
+    def __setitem__(self, name, t):
+        self._bufs.append(t)
+        self._slots[name] = (t, 0, t.numel(), t.element_size())
+        self._views[name] = t
+
+    def __getitem__(self, name):
+        v = self._views.get(name)
+        if v is None:
+            torch = _lib.torch_cuda()
+            base, off, numel, isz = self._slots[name]
+            v = base[off:off + numel * isz].view(getattr(torch, self._DT[name]))
+            self._views[name] = v
+        return v
+
+    def __contains__(self, name):
+        return name in self._slots
+
+    def ptr(self, name) -> int:
+        base, off, _, _ = self._slots[name]
+        return base.data_ptr() + off
+
+    def values(self):
+        return list(self._bufs)
+
+
 class CompressedActivation:
     """Self-describing compressed container (reference codec.py:74-179).
 
@@ -230,7 +285,7 @@ class CompressedActivation:
         torch = _lib.torch_cuda()
         ctx = _lib.context()
         sh, s = _lib.stream_handle()
-        dev = {}
+        dev = _DevBufs()
         nbytes = (self.payload_bits + 7) // 8
         if len(self._h_payload) < nbytes:
             raise FormatError("payload shorter than declared bit length")
@@ -250,8 +305,8 @@ class CompressedActivation:
             dl = torch.from_numpy(lengths.astype(np.uint16).view(np.int16).copy()).cuda()
             live_h = C.c_uint32(0)
             _lib.raise_for(_lib.lib().actc_codebook_from_lengths(
-                ctx.handle, C.c_void_p(dl.data_ptr()), A, C.c_void_p(dev["canon"].data_ptr()),
-                C.c_void_p(dev["len_counts"].data_ptr()), C.byref(live_h), sh))
+                ctx.handle, C.c_void_p(dl.data_ptr()), A, C.c_void_p(dev.ptr("canon")),
+                C.c_void_p(dev.ptr("len_counts")), C.byref(live_h), sh))
         self._live = live
         self._dev = dev
         return dev
@@ -264,15 +319,15 @@ class CompressedActivation:
         d.radius = int(self.params.radius)
         d.flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if self.params.preserve_zeros else 0
         d.n_outliers = self._n_outliers
-        d.outlier_idx_dev = dev["out_idx"].data_ptr()
-        d.outlier_val_dev = dev["out_val"].data_ptr()
+        d.outlier_idx_dev = dev.ptr("out_idx")
+        d.outlier_val_dev = dev.ptr("out_val")
         d.live_symbols = self._live
-        d.canon_syms_dev = dev["canon"].data_ptr()
-        d.len_counts_dev = dev["len_counts"].data_ptr()
-        d.payload_dev = dev["payload"].data_ptr()
+        d.canon_syms_dev = dev.ptr("canon")
+        d.len_counts_dev = dev.ptr("len_counts")
+        d.payload_dev = dev.ptr("payload")
         d.payload_bits = self.payload_bits
-        d.chunk_offsets_dev = dev["chunk_off"].data_ptr() if (with_index and "chunk_off" in dev) else None
-        d.chunk_lat_dev = dev["chunk_lat"].data_ptr() if (with_index and "chunk_lat" in dev) else None
+        d.chunk_offsets_dev = dev.ptr("chunk_off") if (with_index and "chunk_off" in dev) else None
+        d.chunk_lat_dev = dev.ptr("chunk_lat") if (with_index and "chunk_lat" in dev) else None
         return d
 
     def _ensure_index(self):
@@ -399,34 +454,9 @@ def compress_device(x, params: CodecParams, dims=None, stream=None):
                                         C.c_void_p(ctx.plan_buf.data_ptr()), sh))
     s.synchronize()
     plan = _lib.Plan.from_buffer_copy(ctx.plan)
-    if plan.status:
-        if plan.status == _lib.ACTC_EDATA:
-            from .errors import DataError
-            raise DataError("tensor contains NaN or Inf")
-        raise ParameterError("Huffman code length exceeds 63 bits")
-    dev = {
-        "payload": torch.empty(_payload_buffer_bytes(plan.payload_bits), dtype=torch.uint8, device=x.device),
-        "out_idx": torch.empty(plan.n_outliers, dtype=torch.int64, device=x.device),
-        "out_val": torch.empty(plan.n_outliers, dtype=torch.float32, device=x.device),
-        "canon": torch.empty(max(plan.live_symbols, 1), dtype=torch.int32, device=x.device),
-        "len_counts": torch.empty(64, dtype=torch.int32, device=x.device),
-        "chunk_off": torch.empty(nchunks, dtype=torch.int64, device=x.device),
-        "chunk_lat": chunk_lat,
-    }
-    _lib.raise_for(L.actc_compress_encode(
-        ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev["payload"].data_ptr()),
-        C.c_void_p(dev["out_idx"].data_ptr()), C.c_void_p(dev["out_val"].data_ptr()),
-        C.c_void_p(dev["canon"].data_ptr()), C.c_void_p(dev["len_counts"].data_ptr()),
-        C.c_void_p(dev["chunk_off"].data_ptr()), sh))
-    c = CompressedActivation._from_device(dims, params, dev, plan.payload_bits, plan.n_outliers,
-                                          plan.live_symbols, plan.rle_runs)
-    blob_len = _cmtz_size(len(dims), plan.n_outliers, plan.rle_runs, plan.payload_bits)
-    frac = plan.n_outliers / n
-    report = CompressionReport(
-        original_bytes=n * 4, compressed_bytes=blob_len, ratio=(n * 4) / blob_len, outlier_fraction=frac,
-        codes_entropy_bits_per_symbol=float(plan.entropy_bits), outlier_warning=frac > 0.5,
-    )
-    return c, report
+    dev = _DevBufs()
+    dev["chunk_lat"] = chunk_lat
+    return _finish_compress(x, params, dims, plan, dev, ctx, sh)
 
 
 def _finish_compress(x, params, dims, plan, dev, ctx, sh):
@@ -438,17 +468,18 @@ def _finish_compress(x, params, dims, plan, dev, ctx, sh):
             from .errors import DataError
             raise DataError("tensor contains NaN or Inf")
         raise ParameterError("Huffman code length exceeds 63 bits")
-    dev["payload"] = torch.empty(_payload_buffer_bytes(plan.payload_bits), dtype=torch.uint8, device=x.device)
-    dev["out_idx"] = torch.empty(plan.n_outliers, dtype=torch.int64, device=x.device)
-    dev["out_val"] = torch.empty(plan.n_outliers, dtype=torch.float32, device=x.device)
-    dev["canon"] = torch.empty(max(plan.live_symbols, 1), dtype=torch.int32, device=x.device)
-    dev["len_counts"] = torch.empty(64, dtype=torch.int32, device=x.device)
-    dev["chunk_off"] = torch.empty(dev["chunk_lat"].numel(), dtype=torch.int64, device=x.device)
+    # one allocation per container, carved (the host cost per tensor is on
+    # the critical path of compress_batch)
+    dev.carve(x.device, [("chunk_off", (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK, 8),
+                         ("out_idx", plan.n_outliers, 8),
+                         ("payload", _payload_buffer_bytes(plan.payload_bits), 1),
+                         ("out_val", plan.n_outliers, 4), ("canon", max(plan.live_symbols, 1), 4),
+                         ("len_counts", 64, 4)])
     _lib.raise_for(_lib.lib().actc_compress_encode(
-        ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev["payload"].data_ptr()),
-        C.c_void_p(dev["out_idx"].data_ptr()), C.c_void_p(dev["out_val"].data_ptr()),
-        C.c_void_p(dev["canon"].data_ptr()), C.c_void_p(dev["len_counts"].data_ptr()),
-        C.c_void_p(dev["chunk_off"].data_ptr()), sh))
+        ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev.ptr("payload")),
+        C.c_void_p(dev.ptr("out_idx")), C.c_void_p(dev.ptr("out_val")),
+        C.c_void_p(dev.ptr("canon")), C.c_void_p(dev.ptr("len_counts")),
+        C.c_void_p(dev.ptr("chunk_off")), sh))
     c = CompressedActivation._from_device(dims, params, dev, plan.payload_bits, plan.n_outliers,
                                           plan.live_symbols, plan.rle_runs)
     blob_len = _cmtz_size(len(dims), plan.n_outliers, plan.rle_runs, plan.payload_bits)
@@ -507,13 +538,14 @@ def compress_batch(xs, params, max_concurrency: int = 8):
             ctx = _lib.context_for(dev_index, slot)
             n = x.numel()
             nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
-            dev = {"chunk_lat": torch.empty(nchunks, dtype=torch.int64, device=x.device)}
+            dev = _DevBufs()
+            dev["chunk_lat"] = torch.empty(nchunks, dtype=torch.int64, device=x.device)
             s.wait_event(ready)
             sh = C.c_void_p(s.cuda_stream)
             flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
             _lib.raise_for(_lib.lib().actc_compress_plan(
                 ctx.handle, C.c_void_p(x.data_ptr()), n, float(p.eb), int(p.radius), flags,
-                C.c_void_p(dev["chunk_lat"].data_ptr()), C.c_void_p(ctx.plan_buf.data_ptr()), sh))
+                C.c_void_p(dev.ptr("chunk_lat")), C.c_void_p(ctx.plan_buf.data_ptr()), sh))
             jobs.append((i, x, p, s, ctx, sh, dev, s.record_event()))
         # launch each tensor's encode as soon as its plan has landed, so
         # encodes of early tensors overlap the codebooks of later ones

@@ -125,6 +125,82 @@ __device__ void radix_pass(const unsigned long long *__restrict__ sk, const uint
   __syncthreads();
 }
 
+// Stable LSD pass on keys only (digit (key >> shift) & 0xFF), src -> dst,
+// with 16 loads in flight per lane: a warp walks its segment in batches of
+// 512 keys (lane owns every 32nd), so one L2 round trip covers 512 keys.
+constexpr int KB = 16;
+__device__ void radix_pass_keys(const unsigned long long *__restrict__ sk, unsigned long long *__restrict__ dk,
+                                uint32_t L, int shift, RadixSmem &rs) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t seg = ((L + NWARP - 1) / NWARP + 32 * KB - 1) & ~uint32_t(32 * KB - 1);
+  const uint32_t b0 = min(L, w * seg), b1 = min(L, b0 + seg);
+  for (int d = lane; d < 257; d += 32) rs.hist[w][d] = 0;
+  __syncwarp();
+  for (uint32_t base = b0; base < b1; base += 32 * KB) {
+    uint32_t d[KB];
+#pragma unroll
+    for (int u = 0; u < KB; u++) {
+      const uint32_t i = base + 32 * u + lane;
+      d[u] = i < b1 ? (uint32_t)((sk[i] >> shift) & 0xFF) : 256u;
+    }
+#pragma unroll
+    for (int u = 0; u < KB; u++) {
+      const unsigned peers = __match_any_sync(0xffffffffu, d[u]);
+      if (lane == __ffs(peers) - 1) rs.hist[w][d[u]] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+    for (int ww = 0; ww < NWARP; ww++) {
+      const uint32_t c = rs.hist[ww][d];
+      rs.hist[ww][d] = run;
+      run += c;
+    }
+    rs.tot[d] = run;
+  }
+  __syncthreads();
+  if (w == 0) {
+    uint32_t v[8], t = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      v[k] = rs.tot[lane * 8 + k];
+      t += v[k];
+    }
+    const uint32_t inc = warp_incl_sum(t);
+    uint32_t run = inc - t;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      rs.tot[lane * 8 + k] = run;
+      run += v[k];
+    }
+  }
+  __syncthreads();
+  for (int d = lane; d < 256; d += 32) rs.hist[w][d] += rs.tot[d];
+  __syncwarp();
+  for (uint32_t base = b0; base < b1; base += 32 * (KB / 2)) {
+    unsigned long long kk[KB / 2];
+#pragma unroll
+    for (int u = 0; u < KB / 2; u++) {
+      const uint32_t i = base + 32 * u + lane;
+      kk[u] = i < b1 ? sk[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < KB / 2; u++) {
+      const uint32_t i = base + 32 * u + lane;
+      const uint32_t dg = i < b1 ? (uint32_t)((kk[u] >> shift) & 0xFF) : 256u;
+      const unsigned peers = __match_any_sync(0xffffffffu, dg);
+      if (dg < 256) dk[rs.hist[w][dg] + __popc(peers & ((1u << lane) - 1u))] = kk[u];
+      __syncwarp();
+      if (dg < 256 && lane == __ffs(peers) - 1) rs.hist[w][dg] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
 // first index in sorted v[lo, hi) with v[i] >= T (block-wide, all threads
 // get the result).  1024-way probing, repeated on the bracketing interval.
 __device__ uint32_t block_lower_bound(const unsigned long long *v, uint32_t lo, uint32_t hi,
@@ -143,6 +219,61 @@ __device__ uint32_t block_lower_bound(const unsigned long long *v, uint32_t lo, 
     hi = nhi;
   }
   return lo;
+}
+
+// Both lower bounds of a phase at once: threads [0, 512) probe v1[lo1, hi1),
+// threads [512, 1024) probe v2[lo2, hi2) -- one memory round trip per
+// refinement step for the pair.  Results: first index with v >= T.
+__device__ void block_lower_bound2(const unsigned long long *v1, uint32_t lo1, uint32_t hi1,
+                                   const unsigned long long *v2, uint32_t lo2, uint32_t hi2,
+                                   unsigned long long T, uint32_t &r1, uint32_t &r2) {
+  constexpr uint32_t H = K2_THREADS / 2;
+  const bool second = threadIdx.x >= H;
+  const uint32_t t = threadIdx.x & (H - 1);
+  bool d1 = hi1 <= lo1, d2 = hi2 <= lo2;
+  r1 = lo1;
+  r2 = lo2;
+  while (!(d1 && d2)) {
+    const uint32_t s1 = d1 ? 1 : (hi1 - lo1 + H - 1) / H, s2 = d2 ? 1 : (hi2 - lo2 + H - 1) / H;
+    bool below = false;
+    if (!second && !d1) {
+      const uint32_t idx = lo1 + t * s1;
+      below = idx < hi1 && v1[idx] < T;
+    } else if (second && !d2) {
+      const uint32_t idx = lo2 + t * s2;
+      below = idx < hi2 && v2[idx] < T;
+    }
+    const uint32_t k1 = (uint32_t)__syncthreads_count(below && !second);
+    const uint32_t k2 = (uint32_t)__syncthreads_count(below && second);
+    if (!d1) {
+      if (s1 == 1 || k1 == 0) {
+        r1 = lo1 + (s1 == 1 ? k1 : 0);
+        d1 = true;
+      } else {
+        const uint32_t nlo = lo1 + (k1 - 1) * s1 + 1, nhi = min(hi1, lo1 + k1 * s1);
+        lo1 = nlo;
+        hi1 = nhi;
+        if (hi1 <= lo1) {
+          r1 = lo1;
+          d1 = true;
+        }
+      }
+    }
+    if (!d2) {
+      if (s2 == 1 || k2 == 0) {
+        r2 = lo2 + (s2 == 1 ? k2 : 0);
+        d2 = true;
+      } else {
+        const uint32_t nlo = lo2 + (k2 - 1) * s2 + 1, nhi = min(hi2, lo2 + k2 * s2);
+        lo2 = nlo;
+        hi2 = nhi;
+        if (hi2 <= lo2) {
+          r2 = lo2;
+          d2 = true;
+        }
+      }
+    }
+  }
 }
 
 // number of leaves among the first d merged items of (leaves lf[0,na),
@@ -335,17 +466,36 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     if (tid == 0) llen[0] = 1;  // huffman.py:50-52
   } else if (L > 1) {
     // ---- 2. sort leaves by (freq, symbol): stable radix on freq ----
-    for (uint32_t i = tid; i < L; i += K2_THREADS) {
-      k0[i] = a.live_freq[i];
-      v0[i] = i;
-    }
-    __syncthreads();
     int passes = 0;
     while (passes < 8 && (maxf >> (8 * passes)) != 0) passes++;
-    for (int p = 0; p < passes; p++) {
-      radix_pass(k0, v0, k1, v1, (uint32_t)L, 8 * p, rs);
-      unsigned long long *tk = k0; k0 = k1; k1 = tk;
-      uint32_t *tv = v0; v0 = v1; v1 = tv;
+    if (big && (maxf >> 38) == 0) {
+      // packed keys (freq << 26 | live index), unique, sorted on the freq
+      // digits only (stability keeps the index order); then split
+#pragma unroll 8
+      for (uint32_t i = tid; i < L; i += K2_THREADS) k0[i] = (a.live_freq[i] << kSymKeyBits) | i;
+      __syncthreads();
+      for (int p = 0; p < passes; p++) {
+        radix_pass_keys(k0, k1, (uint32_t)L, kSymKeyBits + 8 * p, rs);
+        unsigned long long *tk = k0; k0 = k1; k1 = tk;
+      }
+#pragma unroll 8
+      for (uint32_t i = tid; i < L; i += K2_THREADS) {
+        const unsigned long long key = k0[i];
+        k0[i] = key >> kSymKeyBits;
+        v0[i] = (uint32_t)(key & (kMaxAlphabet - 1));
+      }
+      __syncthreads();
+    } else {
+      for (uint32_t i = tid; i < L; i += K2_THREADS) {
+        k0[i] = a.live_freq[i];
+        v0[i] = i;
+      }
+      __syncthreads();
+      for (int p = 0; p < passes; p++) {
+        radix_pass(k0, v0, k1, v1, (uint32_t)L, 8 * p, rs);
+        unsigned long long *tk = k0; k0 = k1; k1 = tk;
+        uint32_t *tv = v0; v0 = v1; v1 = tv;
+      }
     }
     // sorted leaf i: freq k0[i], live index v0[i]
     const unsigned long long *lf = k0;
@@ -364,8 +514,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       if (lp < L) m = lf[lp];
       if (np < nn && nf[np] < m) m = nf[np];
       const unsigned long long T = 2 * m;
-      const uint32_t na = block_lower_bound(lf, lp, (uint32_t)L, T) - lp;
-      const uint32_t nb = block_lower_bound(nf, np, nn, T) - np;
+      uint32_t ea, eb2;
+      block_lower_bound2(lf, lp, (uint32_t)L, nf, np, nn, T, ea, eb2);
+      const uint32_t na = ea - lp, nb = eb2 - np;
       const uint32_t tot = na + nb, pairs = tot >> 1;
       if (!big) {
         // merge path on the (shared-memory) arrays: thread t owns merged
@@ -449,36 +600,63 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
         }
         __syncthreads();
       }
-      for (uint32_t t = b + tid; t < b + pr; t += K2_THREADS)
-        if (t != root) dep[t] = (uint8_t)min(255, dep[npar[t]] + 1);
+      // parents of this phase's nodes are all newer: gather 8 at a time
+      for (uint32_t t0 = b + tid; t0 < b + pr; t0 += 8 * K2_THREADS) {
+        uint32_t par[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const uint32_t t = t0 + u * K2_THREADS;
+          par[u] = (t < b + pr && t != root) ? npar[t] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const uint32_t t = t0 + u * K2_THREADS;
+          if (par[u] != 0xFFFFFFFFu) dep[t] = (uint8_t)min(255, dep[par[u]] + 1);
+        }
+      }
       __syncthreads();
     }
-#pragma unroll 4
-    for (uint32_t i = tid; i < L; i += K2_THREADS) {
-      const uint32_t d = (uint32_t)dep[lpar[i]] + 1;
-      if (d > ACTC_MAX_CODE_LENGTH) atomicOr(&s_err, 1u);
-      llen[v0[i]] = (uint8_t)(d > 255 ? 255 : d);
+    for (uint32_t i0 = tid; i0 < L; i0 += 8 * K2_THREADS) {
+      uint32_t lp8[8], vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t i = i0 + u * K2_THREADS;
+        lp8[u] = i < L ? lpar[i] : 0u;
+        vv[u] = i < L ? v0[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t i = i0 + u * K2_THREADS;
+        if (i < L) {
+          const uint32_t d = (uint32_t)dep[lp8[u]] + 1;
+          if (d > ACTC_MAX_CODE_LENGTH) atomicOr(&s_err, 1u);
+          llen[vv[u]] = (uint8_t)(d > 255 ? 255 : d);
+        }
+      }
     }
   }
   __syncthreads();
 
   K2_STAMP(4)
   // ---- 5. canonical order: stable radix pass on length (input in symbol order) ----
-  for (uint32_t i = tid; i < L; i += K2_THREADS) {
-    k1[i] = (unsigned long long)llen[i];
-    v1[i] = a.live_sym[i];
-  }
+  // keys (len << 26 | live index): one keys-only pass on the length digit
+#pragma unroll 8
+  for (uint32_t i = tid; i < L; i += K2_THREADS) k1[i] = ((unsigned long long)llen[i] << kSymKeyBits) | i;
   __syncthreads();
   unsigned long long *ck = k1;
-  uint32_t *cv = v1;
   if (L > 1) {
-    radix_pass(k1, v1, k0, v0, (uint32_t)L, 0, rs);
+    if (big)
+      radix_pass_keys(k1, k0, (uint32_t)L, kSymKeyBits, rs);
+    else {
+      for (uint32_t i = tid; i < L; i += K2_THREADS) v1[i] = i;
+      __syncthreads();
+      radix_pass(k1, v1, k0, v0, (uint32_t)L, kSymKeyBits, rs);
+    }
     ck = k0;
-    cv = v0;
   }
   unsigned lmax = 0;
   for (uint32_t i = tid; i < L; i += K2_THREADS) {
-    unsigned l = (unsigned)ck[i];
+    unsigned l = (unsigned)(ck[i] >> kSymKeyBits);
     atomicAdd(&s_cnt[l & 63], 1u);
     lmax = max(lmax, l);
   }
@@ -497,10 +675,28 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     }
   }
   __syncthreads();
-  for (uint32_t i = tid; i < L; i += K2_THREADS) {
-    uint32_t l = (uint32_t)ck[i], s = cv[i];
-    a.canon[i] = s;
-    if (a.ctab && l <= 56) a.ctab[s] = ((s_first[l] + (i - s_base[l])) << 8) | l;
+  for (uint32_t i0 = tid; i0 < L; i0 += 8 * K2_THREADS) {
+    unsigned long long kk[8];
+    uint32_t sy[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t i = i0 + u * K2_THREADS;
+      kk[u] = i < L ? ck[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t i = i0 + u * K2_THREADS;
+      sy[u] = i < L ? a.live_sym[kk[u] & (kMaxAlphabet - 1)] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t i = i0 + u * K2_THREADS;
+      if (i < L) {
+        const uint32_t l = (uint32_t)(kk[u] >> kSymKeyBits), s = sy[u];
+        a.canon[i] = s;
+        if (a.ctab && l <= 56) a.ctab[s] = ((s_first[l] + (i - s_base[l])) << 8) | l;
+      }
+    }
   }
   if (tid < 64) a.len_counts[tid] = s_cnt[tid];
   if (a.out_lengths) {
@@ -511,21 +707,44 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
 
   K2_STAMP(5)
   // ---- 6. plan: payload bits, RLE record count, entropy, live range ----
+  // p*log2(p) = (f/T) * (log2 f - log2 T) with log2 f from a shared table for
+  // f < kLgTab (the shared arrays of stages 2-5 are dead here); the
+  // summation order differs from numpy's anyway (report value, rel. 1e-12)
+  constexpr uint32_t kLgTab = 4096;
+  double *lgtab = reinterpret_cast<double *>(smem);
+  const double total = (double)a.n_symbols;
+  if (!a.in_lengths) {
+    for (uint32_t f = tid; f < kLgTab; f += K2_THREADS) lgtab[f] = f ? log2((double)f) : 0.0;
+  }
+  __syncthreads();
+  const double lgT = log2(total);
   unsigned long long bits = 0, recs = 0;
   double ent = 0.0;
-  const double total = (double)a.n_symbols;
-  for (uint32_t j = tid; j < L; j += K2_THREADS) {
-    uint32_t s = a.live_sym[j];
-    unsigned long long f = a.live_freq[j];
-    if (!a.in_lengths) {
-      bits += f * llen[j];
-      double p = (double)f / total;
-      ent += p * log2(p);
+  for (uint32_t j0 = tid; j0 < L; j0 += 8 * K2_THREADS) {
+    uint32_t sy[8], pe[8];
+    unsigned long long fr[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t j = j0 + u * K2_THREADS;
+      sy[u] = j < L ? a.live_sym[j] : 0u;
+      pe[u] = (j < L && j) ? a.live_sym[j - 1] + 1 : 0u;
+      fr[u] = j < L ? a.live_freq[j] : 0ull;
     }
-    uint32_t prev_end = j ? a.live_sym[j - 1] + 1 : 0;
-    uint64_t g = s - prev_end;
-    if (g) recs += (g + 65534) / 65535;
-    if (j == 0 || g || llen[j] != llen[j - 1]) recs += 1;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t j = j0 + u * K2_THREADS;
+      if (j >= L) continue;
+      const unsigned long long f = fr[u];
+      const uint32_t lj = llen[j];
+      if (!a.in_lengths) {
+        bits += f * lj;
+        const double pp = (double)f / total;
+        ent += pp * (f < kLgTab ? lgtab[f] - lgT : log2(pp));
+      }
+      const uint64_t g = sy[u] - pe[u];
+      if (g) recs += (g + 65534) / 65535;
+      if (j == 0 || g || lj != llen[j - 1]) recs += 1;
+    }
   }
   unsigned long long tb;
   block_excl_sum<unsigned long long>(bits, wbuf, &tb);
