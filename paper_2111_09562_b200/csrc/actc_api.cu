@@ -237,10 +237,10 @@ const char *actc_last_error(void) { return g_err; }
 int actc_version(void) { return 1; }
 
 /* debug: copy the K2 stage timestamps of the last codebook build (ACTC_K2_TIMING=1) */
-int actc_debug_k2_timing(actc_ctx *c, uint64_t *out16) {
+int actc_debug_k2_timing(actc_ctx *c, uint64_t *out32) {
   if (!c->idx.p) return ACTC_EPARAM;
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(out16, c->idx.p, 16 * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out32, c->idx.p, 32 * 8, cudaMemcpyDeviceToHost));
   return ACTC_OK;
 }
 

@@ -474,9 +474,11 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
 #pragma unroll 8
       for (uint32_t i = tid; i < L; i += K2_THREADS) k0[i] = (a.live_freq[i] << kSymKeyBits) | i;
       __syncthreads();
+      K2_STAMP(10)
       for (int p = 0; p < passes; p++) {
         radix_pass_keys(k0, k1, (uint32_t)L, kSymKeyBits + 8 * p, rs);
         unsigned long long *tk = k0; k0 = k1; k1 = tk;
+        if (p < 3) { K2_STAMP(11 + p) }
       }
 #pragma unroll 8
       for (uint32_t i = tid; i < L; i += K2_THREADS) {
@@ -507,7 +509,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     }
     __syncthreads();
     const unsigned long long INF = ~0ull;
+    unsigned long long t_lb = 0, t_merge = 0, t_book = 0, t_c0 = 0;
     while (true) {
+      if (a.dbg && tid == 0) t_c0 = clock64();
       const uint32_t lp = s_lp, np = s_np, nn = s_nn;
       if ((L - lp) + (nn - np) <= 1) break;
       unsigned long long m = INF;
@@ -517,6 +521,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       uint32_t ea, eb2;
       block_lower_bound2(lf, lp, (uint32_t)L, nf, np, nn, T, ea, eb2);
       const uint32_t na = ea - lp, nb = eb2 - np;
+      if (a.dbg && tid == 0) { const unsigned long long c = clock64(); t_lb += c - t_c0; t_c0 = c; }
       const uint32_t tot = na + nb, pairs = tot >> 1;
       if (!big) {
         // merge path on the (shared-memory) arrays: thread t owns merged
@@ -531,8 +536,9 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
         // windows of kWin merged positions
         for (uint32_t wa = 0; wa < tot; wa += kWin) {
           const uint32_t wb = min(tot, wa + kWin);
-          const uint32_t ia = merge_split_block(lf + lp, nf + np, na, nb, wa);
-          const uint32_t ib = merge_split_block(lf + lp, nf + np, na, nb, wb);
+          // a phase that fits one window needs no merge-path split
+          const uint32_t ia = wa == 0 ? 0u : merge_split_block(lf + lp, nf + np, na, nb, wa);
+          const uint32_t ib = wb == tot ? na : merge_split_block(lf + lp, nf + np, na, nb, wb);
           const uint32_t ja = wa - ia, jb = wb - ib;
           unsigned long long *sl = reinterpret_cast<unsigned long long *>(smem);
           unsigned long long *sn = sl + (ib - ia);
@@ -550,6 +556,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
         }
       }
       __syncthreads();
+      if (a.dbg && tid == 0) { const unsigned long long c = clock64(); t_merge += c - t_c0; t_c0 = c; }
       if (tid == 0) {
         uint32_t ph = s_nph;
         ph_begin[ph] = nn;
@@ -579,7 +586,13 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
         if (ph + 1 >= kMaxPhases) s_err |= 2u;  // cannot happen for n < 2^38
       }
       __syncthreads();
+      if (a.dbg && tid == 0) { const unsigned long long c = clock64(); t_book += c - t_c0; t_c0 = c; }
       if (s_err & 2u) break;
+    }
+    if (a.dbg && tid == 0) {
+      a.dbg[16] = t_lb;
+      a.dbg[17] = t_merge;
+      a.dbg[18] = t_book;
     }
     // ---- 4. depths, walking phases backwards ----
     // internal-node depths as bytes in shared memory (saturating at 255;
@@ -654,13 +667,29 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     }
     ck = k0;
   }
-  unsigned lmax = 0;
-  for (uint32_t i = tid; i < L; i += K2_THREADS) {
-    unsigned l = (unsigned)(ck[i] >> kSymKeyBits);
-    atomicAdd(&s_cnt[l & 63], 1u);
-    lmax = max(lmax, l);
+  if (big && L > 1) {
+    // per-length counts = the digit totals of the pass (exclusive prefix in rs.tot)
+    if (tid < 64) {
+      const uint32_t hi = tid + 1 < 256 ? rs.tot[tid + 1] : (uint32_t)L;
+      s_cnt[tid] = hi - rs.tot[tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned mx = 0;
+      for (int l = 0; l < 64; l++)
+        if (s_cnt[l]) mx = l;
+      // lengths >= 64 (saturated depths) only occur with an error already flagged
+      s_maxlen = (rs.tot[64] < (uint32_t)L) ? 255u : mx;
+    }
+  } else {
+    unsigned lmax = 0;
+    for (uint32_t i = tid; i < L; i += K2_THREADS) {
+      unsigned l = (unsigned)(ck[i] >> kSymKeyBits);
+      atomicAdd(&s_cnt[l & 63], 1u);
+      lmax = max(lmax, l);
+    }
+    atomicMax(&s_maxlen, lmax);
   }
-  atomicMax(&s_maxlen, lmax);
   __syncthreads();
   if (tid == 0) {
     // huffman.py:97-117 (first_code per length, base index per length)
@@ -717,7 +746,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
     for (uint32_t f = tid; f < kLgTab; f += K2_THREADS) lgtab[f] = f ? log2((double)f) : 0.0;
   }
   __syncthreads();
-  const double lgT = log2(total);
+  const double lgT = log2(total), invT = 1.0 / total;
   unsigned long long bits = 0, recs = 0;
   double ent = 0.0;
   for (uint32_t j0 = tid; j0 < L; j0 += 8 * K2_THREADS) {
@@ -738,7 +767,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
       const uint32_t lj = llen[j];
       if (!a.in_lengths) {
         bits += f * lj;
-        const double pp = (double)f / total;
+        const double pp = (double)f * invT;
         ent += pp * (f < kLgTab ? lgtab[f] - lgT : log2(pp));
       }
       const uint64_t g = sy[u] - pe[u];

@@ -18,10 +18,13 @@ L.actc_debug_k2_timing.argtypes = [C.c_void_p, C.c_void_p]
 for rep in range(2):
     for t, eb in zip(tensors, ebs):
         pb.compress_device(t, pb.CodecParams(eb=eb))
-        out = (C.c_uint64 * 16)()
+        out = (C.c_uint64 * 32)()
         L.actc_debug_k2_timing(_lib.context().handle, out)
         v = list(out)
         st = ["compact", "sort", "phases", "depth", "canon", "plan"]
         d = {st[i]: v[i + 1] - v[i] for i in range(6) if v[i + 1] >= v[i]}
         if rep:
-            print(f"L={v[9]} phases={v[8]} total={v[6]-v[0]} cycles", {k: int(x) for k, x in d.items()})
+            sub = {"init": v[10] - v[1], "pass0": v[11] - v[10], "pass1": v[12] - v[11], "pass2": v[13] - v[12],
+                   "lb": v[16], "merge": v[17], "book": v[18]}
+            print(f"L={v[9]} phases={v[8]} total={v[6]-v[0]} cycles", {k: int(x) for k, x in d.items()},
+                  {k: int(x) for k, x in sub.items() if x < 1 << 40})
