@@ -427,15 +427,12 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       lwin_lo = wl;
     }
     const size_t smem = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
-    if ((rc = grow(c->status, nseg * 24 + 1024))) return rc;
-    char *b = (char *)c->status.p;
+    if ((rc = grow(c->status, nseg * 16 + 1024))) return rc;
     EncLB st;
-    st.inc_bits = (unsigned long long *)b;
-    st.inc_nz = st.inc_bits + nseg;
-    st.flag = (unsigned *)(st.inc_nz + nseg);
-    st.agg = st.flag + nseg;
+    st.stat = (unsigned long long *)c->status.p;
+    st.incnz = st.stat + nseg;
     unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
-    CK(cudaMemsetAsync(st.flag, 0, nseg * 4, s));
+    CK(cudaMemsetAsync(st.stat, 0, nseg * 16, s));
     CK(cudaMemsetAsync(ticket, 0, 4, s));
     CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
     const void *f = sb == 2 ? (const void *)k3_encode_lb<uint16_t> : (const void *)k3_encode_lb<uint32_t>;

@@ -107,47 +107,45 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
       }
     }
     const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nz);
+    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31);
     if (lane == 31) {
       s_wbits[warp] = ib;
       s_wnz[warp] = iz;
     }
     __syncthreads();
 
-    // ---- 2. tile aggregate, look-back over tiles (warp 0), inclusive prefix ----
+    // ---- 2. warp 0: tile aggregate, look-back, inclusive prefix ----
     if (warp == 0) {
       const uint32_t wbv = lane < NW ? s_wbits[lane] : 0u, wzv = lane < NW ? s_wnz[lane] : 0u;
       const uint32_t tb = warp_sum(wbv), tz = warp_sum(wzv);
       unsigned long long pb = 0, pz = 0;
       if (tile == 0) {
         if (lane == 0) {
-          st.inc_bits[0] = tb;
-          st.inc_nz[0] = tz;
-          st_release(&st.flag[0], kFlagInc);
+          st_relaxed_u64(&st.incnz[0], kLbInc | tz);
+          __threadfence();
+          st_relaxed_u64(&st.stat[0], kLbInc | tb);
         }
       } else {
-        if (lane == 0) {
-          st.agg[tile] = (tb << 14) | tz;  // tb < 2^18, tz <= 8192
-          st_release(&st.flag[tile], kFlagAgg);
-        }
+        if (lane == 0) st_relaxed_u64(&st.stat[tile], kLbAgg | ((unsigned long long)tb << 14) | tz);
         // probe 128 predecessors per round trip: lane l owns p-l, p-l-32, ...
         long long p = (long long)tile - 1;
         while (true) {
-          unsigned f[4];
+          unsigned long long v[4];
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const long long idx = p - lane - 32 * k;
-            f[k] = kFlagInc;
+            v[k] = kLbInc;  // before tile 0: an inclusive prefix of zero
             if (idx >= 0) {
               do {
-                f[k] = ld_acquire(&st.flag[idx]);
-              } while (f[k] == 0);
+                v[k] = ld_relaxed_u64(&st.stat[idx]);
+              } while ((v[k] >> 62) == 0);
             }
           }
           // nearest inclusive prefix: smallest distance d = lane + 32k
           int stop = 128;
 #pragma unroll
           for (int k = 3; k >= 0; k--) {
-            const unsigned im = __ballot_sync(0xffffffffu, f[k] == kFlagInc);
+            const unsigned im = __ballot_sync(0xffffffffu, (v[k] >> 62) == 2);
             if (im) stop = 32 * k + __ffs(im) - 1;
           }
           unsigned long long vb = 0, vz = 0;
@@ -157,10 +155,14 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
             const long long idx = p - d;
             if (idx >= 0 && d <= stop) {
               if (d == stop) {
-                vb += st.inc_bits[idx];
-                vz += st.inc_nz[idx];
+                vb += v[k] & kLbVal;
+                unsigned long long z;
+                do {
+                  z = ld_relaxed_u64(&st.incnz[idx]);
+                } while ((z >> 62) != 2);
+                vz += z & kLbVal;
               } else {
-                const unsigned g = st.agg[idx];
+                const unsigned long long g = v[k] & kLbVal;
                 vb += g >> 14;
                 vz += g & 16383u;
               }
@@ -172,9 +174,9 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
           p -= 128;
         }
         if (lane == 0) {
-          st.inc_bits[tile] = pb + tb;
-          st.inc_nz[tile] = pz + tz;
-          st_release(&st.flag[tile], kFlagInc);
+          st_relaxed_u64(&st.incnz[tile], kLbInc | (pz + tz));
+          __threadfence();
+          st_relaxed_u64(&st.stat[tile], kLbInc | (pb + tb));
         }
       }
       if (lane == 0) {
@@ -182,40 +184,18 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
         s_pz = pz;
       }
     }
-    __syncthreads();
-    unsigned long long pb = s_pb, pz = s_pz;
-    for (int w = 0; w < warp; w++) {
-      pb += s_wbits[w];
-      pz += s_wnz[w];
-    }
-    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31);
 
-    // ---- 3. pack ----
-    const uint32_t off0 = (uint32_t)(pb & 31);
-    const uint32_t nw = (off0 + seg_bits + 31) >> 5;
-    for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
+    // ---- 3. pack locally (segment bit 0 at word 0, bit 31) while warp 0 looks back ----
+    const uint32_t nl = (seg_bits + 31) >> 5;
+    for (uint32_t i = lane; i <= nl; i += 32) wb[i] = 0;
     __syncwarp();
     const uint32_t lane_ex = ib - bits;
-    if ((lane & 7) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
-    if (extract_outliers && nz) {
-      unsigned long long o = pz + (iz - nz);
-#pragma unroll
-      for (int j = 0; j < K3L_EPT; j++) {
-        if (s[j] == 0) {
-          out_idx[o] = base + j;
-          out_val[o] = x[base + j];
-          o++;
-        }
-      }
-    }
-    if (bits) {
+    {
       // codes <= 26 bits complete at most one word each: predicated emits;
       // the lane's first word and final partial word may be shared -> atomic.
-      // A pad symbol has len 0: the 64-bit shift by >= 64 yields 0.
-      const uint32_t rel = off0 + lane_ex;
-      uint32_t w = rel >> 5;
+      uint32_t w = lane_ex >> 5;
       const uint32_t w0 = w;
-      int nb = rel & 31;
+      int nb = lane_ex & 31;
       unsigned long long acc = 0;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
@@ -235,12 +215,34 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
       }
       if (nb > 0) atomicOr(&wb[w], (uint32_t)(acc >> 32));
     }
-    __syncwarp();
+    __syncthreads();  // s_pb / s_pz ready; every warp's buffer complete
+
+    // ---- 4. write out at the absolute bit offset ----
+    unsigned long long pb = s_pb, pz = s_pz;
+    for (int w = 0; w < warp; w++) {  // s_wbits[w]: segment w's total (lane 31's inclusive sum)
+      pb += s_wbits[w];
+      pz += s_wnz[w];
+    }
+    if ((lane & 7) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
+    if (extract_outliers && nz) {
+      unsigned long long o = pz + (iz - nz);
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] == 0) {
+          out_idx[o] = base + j;
+          out_val[o] = x[base + j];
+          o++;
+        }
+      }
+    }
+    const uint32_t sh = (uint32_t)(pb & 31);
     const uint64_t gw0 = pb >> 5;
-    const uint32_t end_off = (off0 + seg_bits) & 31;
+    const uint32_t nw = (sh + seg_bits + 31) >> 5;
+    const uint32_t end_off = (sh + seg_bits) & 31;
     for (uint32_t i = lane; i < nw; i += 32) {
-      const uint32_t v = bswap32(wb[i]);
-      const bool shared_word = (i == 0 && off0 != 0) || (i == nw - 1 && end_off != 0);
+      const uint32_t cur = i < nl ? wb[i] : 0u, prev = i ? wb[i - 1] : 0u;
+      const uint32_t v = bswap32(sh ? (cur >> sh) | (prev << (32 - sh)) : cur);
+      const bool shared_word = (i == 0 && sh != 0) || (i == nw - 1 && end_off != 0);
       if (shared_word)
         atomicOr(&payload[gw0 + i], v);
       else

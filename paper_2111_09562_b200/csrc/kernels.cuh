@@ -104,12 +104,18 @@ __global__ void k3_pack(const SymT *__restrict__ sym, uint64_t n, const unsigned
                         unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
                         unsigned long long *__restrict__ chunk_off, uint32_t *__restrict__ head,
                         uint32_t *__restrict__ tail, int extract_outliers);
-// single-pass encoder look-back state (per segment)
+// single-pass encoder look-back state (per tile).  Self-validating 64-bit
+// words (flag in the top bits, value below) so pollers need no acquire:
+//   stat[t]  = kLbAgg | (tile bits << 14 | tile outliers)   or
+//              kLbInc | inclusive bits (< 2^44)
+//   incnz[t] = kLbInc | inclusive outlier count (written before stat's INC)
 struct EncLB {
-  unsigned *flag;                     // 0 = empty, kFlagAgg, kFlagInc
-  unsigned *agg;                      // (bits << 11) | outliers of the segment
-  unsigned long long *inc_bits, *inc_nz;  // inclusive prefixes
+  unsigned long long *stat;
+  unsigned long long *incnz;
 };
+constexpr unsigned long long kLbAgg = 1ull << 62;
+constexpr unsigned long long kLbInc = 2ull << 62;
+constexpr unsigned long long kLbVal = (1ull << 62) - 1;
 template <typename SymT>
 __global__ void k3_encode_lb(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
                              uint32_t win_lo, uint32_t win_n, const float *__restrict__ x,
