@@ -80,9 +80,19 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
   __shared__ unsigned s_tile;
   uint32_t *tab = k3l_sm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t i = threadIdx.x; i < win_n; i += K3L_THREADS) {
-    const unsigned long long e = ctab[win_lo + i];
-    tab[i] = (uint32_t)(((e >> 8) << 6) | (e & 63));
+  // table copy: 16 loads in flight per thread (one L2 round trip per 4096 entries)
+  for (uint32_t i0 = threadIdx.x; i0 < win_n; i0 += 16 * K3L_THREADS) {
+    unsigned long long e[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t i = i0 + u * K3L_THREADS;
+      e[u] = i < win_n ? __ldg(&ctab[win_lo + i]) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t i = i0 + u * K3L_THREADS;
+      if (i < win_n) tab[i] = (uint32_t)(((e[u] >> 8) << 6) | (e[u] & 63));
+    }
   }
   uint32_t *wb = k3l_sm + ((win_n + 3) & ~3u) + warp * K3L_WORDS;
   const uint64_t ntiles = (n + (uint64_t)K3L_SEG * NW - 1) / ((uint64_t)K3L_SEG * NW);

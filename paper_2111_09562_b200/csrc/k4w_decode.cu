@@ -87,8 +87,14 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   constexpr int ROW = SW == 16 ? ROW16 : ROW32;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kLutSize / 4; i += K4W_THREADS)
-    reinterpret_cast<uint4 *>(lut)[i] = reinterpret_cast<const uint4 *>(a.lut)[i];
+  {
+    constexpr int PER = kLutSize / 4 / K4W_THREADS;  // 16-byte loads per thread, all in flight
+    uint4 l4[PER];
+#pragma unroll
+    for (int u = 0; u < PER; u++) l4[u] = __ldg(reinterpret_cast<const uint4 *>(a.lut) + tid + u * K4W_THREADS);
+#pragma unroll
+    for (int u = 0; u < PER; u++) reinterpret_cast<uint4 *>(lut)[tid + u * K4W_THREADS] = l4[u];
+  }
   if (tid == 0) {
     unsigned long long code = 0;
     uint32_t idx = 0, mx = 0;
@@ -113,7 +119,28 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     s_maxlen = mx;
   }
   const uint32_t ncache = SW == 16 ? min((uint32_t)K4W_CANON_CACHE, a.live) : 0u;
-  for (uint32_t i = tid; i < ncache; i += K4W_THREADS) ccache[i] = (uint16_t)a.canon[i];
+  // canonical-symbol cache: 8 x 16-byte loads in flight per thread
+  for (uint32_t i0 = 4 * tid; i0 < ncache; i0 += 4 * 8 * K4W_THREADS) {
+    uint4 c4[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t i = i0 + 4 * u * K4W_THREADS;
+      c4[u] = i + 3 < ncache ? __ldg(reinterpret_cast<const uint4 *>(a.canon + i)) : make_uint4(0, 0, 0, 0);
+      if (i < ncache && i + 3 >= ncache) {  // ragged tail
+        c4[u].x = a.canon[i];
+        if (i + 1 < ncache) c4[u].y = a.canon[i + 1];
+        if (i + 2 < ncache) c4[u].z = a.canon[i + 2];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const uint32_t i = i0 + 4 * u * K4W_THREADS;
+      if (i < ncache) ccache[i] = (uint16_t)c4[u].x;
+      if (i + 1 < ncache) ccache[i + 1] = (uint16_t)c4[u].y;
+      if (i + 2 < ncache) ccache[i + 2] = (uint16_t)c4[u].z;
+      if (i + 3 < ncache) ccache[i + 3] = (uint16_t)c4[u].w;
+    }
+  }
   __syncthreads();
 
   const bool fast_long = a.lut[kLutSize] != 0;
