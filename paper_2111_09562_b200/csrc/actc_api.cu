@@ -312,7 +312,8 @@ int actc_ctx_create(int device, actc_ctx **out) {
                        (const void *)k4w_decode<0, 16>,         (const void *)k4w_decode<1, 16>,
                        (const void *)k4w_decode<0, 32>,         (const void *)k4w_decode<1, 32>,
                        (const void *)k4w_decode<2, 32>,         (const void *)k3_encode_lb<uint16_t>,
-                       (const void *)k3_encode_lb<uint32_t>};
+                       (const void *)k3_encode_lb<uint32_t>,    (const void *)k3_seg_pack<uint16_t>,
+                       (const void *)k3_seg_pack<uint32_t>};
   for (const void *f : big) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, f));
@@ -416,8 +417,6 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     win_n = cap;
   }
   if (!wide && !getenv("ACTC_K3_TWO_PASS")) {
-    // single pass: warp per 1024-symbol segment, decoupled look-back
-    const uint64_t nseg = cdiv(n, (uint64_t)K3L_SEG * (K3L_THREADS / 32));  // look-back tiles
     uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
     if (span > K3L_WIN) {
       uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
@@ -426,6 +425,52 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       if (wl + K3L_WIN > hi + 1) wl = hi + 1 - K3L_WIN;
       lwin_lo = wl;
     }
+    if (!getenv("ACTC_K3_LB")) {
+      // two passes over 1024-symbol segments, no inter-warp waiting
+      const uint64_t nseg = cdiv(n, K3L_SEG);
+      const size_t tsm = (size_t)((lwin_n + 3) & ~3u) * 4;
+      const size_t psm = tsm + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
+      if ((rc = grow(c->status, nseg * 24 + 1024))) return rc;
+      unsigned long long *bit0 = (unsigned long long *)c->status.p, *nz0 = bit0 + nseg;
+      uint32_t *sbits = (uint32_t *)(nz0 + nseg), *snz = sbits + nseg;
+      unsigned long long *misc = (unsigned long long *)c->misc.p;
+      CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
+      const void *fc = sb == 2 ? (const void *)k3_seg_count<uint16_t> : (const void *)k3_seg_count<uint32_t>;
+      const void *fp = sb == 2 ? (const void *)k3_seg_pack<uint16_t> : (const void *)k3_seg_pack<uint32_t>;
+      int occ_c = 0, occ_p = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, fc, K3L_THREADS, tsm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, fp, K3L_THREADS, psm);
+      const uint64_t wseg = cdiv(nseg, K3L_THREADS / 32);
+      const int gc = (int)std::max<uint64_t>(1, std::min<uint64_t>(wseg, (uint64_t)std::max(1, occ_c) * c->num_sms));
+      const int gp = (int)std::max<uint64_t>(1, std::min<uint64_t>(wseg, (uint64_t)std::max(1, occ_p) * c->num_sms));
+      const unsigned long long *ct = (const unsigned long long *)c->ctab.p;
+      {
+        KT(ACTC_KIND_COUNT);
+        if (sb == 2)
+          k3_seg_count<uint16_t><<<gc, K3L_THREADS, tsm, s>>>((const uint16_t *)sym, n, ct, lwin_lo, lwin_n, sbits, snz);
+        else
+          k3_seg_count<uint32_t><<<gc, K3L_THREADS, tsm, s>>>((const uint32_t *)sym, n, ct, lwin_lo, lwin_n, sbits, snz);
+      }
+      {
+        KT(ACTC_KIND_SCAN);
+        k3_seg_scan<<<1, 1024, 0, s>>>(sbits, snz, nseg, bit0, nz0, misc + M_SCAN_TOT);
+      }
+      {
+        KT(ACTC_KIND_PACK);
+        if (sb == 2)
+          k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, n, ct, lwin_lo, lwin_n, x, bit0, nz0,
+                                                             (uint32_t *)payload, (unsigned long long *)out_idx,
+                                                             out_val, (unsigned long long *)chunk_off, extract);
+        else
+          k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, n, ct, lwin_lo, lwin_n, x, bit0, nz0,
+                                                             (uint32_t *)payload, (unsigned long long *)out_idx,
+                                                             out_val, (unsigned long long *)chunk_off, extract);
+      }
+      CKL();
+      return ACTC_OK;
+    }
+    // single pass: decoupled look-back over 8-segment tiles
+    const uint64_t nseg = cdiv(n, (uint64_t)K3L_SEG * (K3L_THREADS / 32));  // look-back tiles
     const size_t smem = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
     if ((rc = grow(c->status, nseg * 16 + 1024))) return rc;
     EncLB st;

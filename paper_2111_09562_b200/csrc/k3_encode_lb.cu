@@ -261,6 +261,197 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
   }
 }
 
+// ===========================================================================
+// Two-pass, barrier-free variant (the production path for codes <= 26 bits):
+//   k3_seg_count  warp per 1024-symbol segment: code bits + outlier markers
+//   k3_seg_scan   one CTA: exclusive prefixes (u64) over the segments
+//   k3_seg_pack   warp per segment at its known bit offset: pack + store
+// Symbols are read twice (2 x 2 B), but no warp ever waits for another.
+// ===========================================================================
+
+__device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned long long *__restrict__ ctab,
+                                               uint32_t win_lo, uint32_t win_n, int nthreads) {
+  for (uint32_t i0 = threadIdx.x; i0 < win_n; i0 += 16 * nthreads) {
+    unsigned long long e[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t i = i0 + u * nthreads;
+      e[u] = i < win_n ? __ldg(&ctab[win_lo + i]) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t i = i0 + u * nthreads;
+      if (i < win_n) tab[i] = (uint32_t)(((e[u] >> 8) << 6) | (e[u] & 63));
+    }
+  }
+}
+
+template <typename SymT>
+__global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restrict__ sym, uint64_t n,
+                                                            const unsigned long long *__restrict__ ctab,
+                                                            uint32_t win_lo, uint32_t win_n,
+                                                            uint32_t *__restrict__ seg_bits,
+                                                            uint32_t *__restrict__ seg_nz) {
+  extern __shared__ __align__(16) uint32_t k3c_sm[];
+  k3_load_window(k3c_sm, ctab, win_lo, win_n, K3L_THREADS);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nseg = (n + K3L_SEG - 1) / K3L_SEG;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
+  for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + (threadIdx.x >> 5); seg < nseg; seg += nwarps) {
+    const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
+    uint32_t s[K3L_EPT];
+    lb_load(sym, base, n, s);
+    uint32_t bits = 0, nz = 0;
+#pragma unroll
+    for (int j = 0; j < K3L_EPT; j++) {
+      if (s[j] != kSent) {
+        bits += lb_entry(k3c_sm, ctab, win_lo, win_n, s[j]) & 63;
+        nz += s[j] == 0;
+      }
+    }
+    bits = warp_sum(bits);
+    nz = warp_sum(nz);
+    if (lane == 0) {
+      seg_bits[seg] = bits;
+      seg_nz[seg] = nz;
+    }
+  }
+}
+
+// exclusive prefixes of (bits, outliers) over the segments; one CTA of 1024,
+// 8 consecutive segments per thread per round
+__global__ void __launch_bounds__(1024) k3_seg_scan(const uint32_t *__restrict__ seg_bits,
+                                                    const uint32_t *__restrict__ seg_nz, uint64_t nseg,
+                                                    unsigned long long *__restrict__ bit0,
+                                                    unsigned long long *__restrict__ nz0,
+                                                    unsigned long long *__restrict__ totals) {
+  __shared__ unsigned long long wb[33], wz[33];
+  unsigned long long runb = 0, runz = 0;
+  for (uint64_t c0 = 0; c0 < nseg; c0 += 8 * 1024) {
+    const uint64_t i0 = c0 + 8ull * threadIdx.x;
+    uint32_t b[8], z[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      b[u] = i0 + u < nseg ? seg_bits[i0 + u] : 0u;
+      z[u] = i0 + u < nseg ? seg_nz[i0 + u] : 0u;
+    }
+    unsigned long long tb = 0, tz = 0;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      tb += b[u];
+      tz += z[u];
+    }
+    unsigned long long allb, allz;
+    const unsigned long long eb = block_excl_sum<unsigned long long>(tb, wb, &allb);
+    const unsigned long long ez = block_excl_sum<unsigned long long>(tz, wz, &allz);
+    unsigned long long rb = runb + eb, rz = runz + ez;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      if (i0 + u < nseg) {
+        bit0[i0 + u] = rb;
+        nz0[i0 + u] = rz;
+      }
+      rb += b[u];
+      rz += z[u];
+    }
+    runb += allb;
+    runz += allz;
+  }
+  if (threadIdx.x == 0) {
+    totals[0] = runb;
+    totals[1] = runz;
+  }
+}
+
+template <typename SymT>
+__global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(
+    const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab, uint32_t win_lo,
+    uint32_t win_n, const float *__restrict__ x, const unsigned long long *__restrict__ bit0,
+    const unsigned long long *__restrict__ nz0, uint32_t *__restrict__ payload,
+    unsigned long long *__restrict__ out_idx, float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
+    int extract_outliers) {
+  extern __shared__ __align__(16) uint32_t k3p_sm[];
+  uint32_t *tab = k3p_sm;
+  k3_load_window(tab, ctab, win_lo, win_n, K3L_THREADS);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t *wb = k3p_sm + ((win_n + 3) & ~3u) + warp * K3L_WORDS;
+  const uint64_t nseg = (n + K3L_SEG - 1) / K3L_SEG;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
+  for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + warp; seg < nseg; seg += nwarps) {
+    const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
+    uint32_t s[K3L_EPT];
+    lb_load(sym, base, n, s);
+    const unsigned long long pb = bit0[seg], pz = nz0[seg];
+    uint32_t bits = 0, nz = 0;
+#pragma unroll
+    for (int j = 0; j < K3L_EPT; j++) {
+      if (s[j] != kSent) {
+        bits += lb_entry(tab, ctab, win_lo, win_n, s[j]) & 63;
+        nz += s[j] == 0;
+      }
+    }
+    const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nz);
+    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31);
+    const uint32_t lane_ex = ib - bits;
+    const uint32_t off0 = (uint32_t)(pb & 31);
+    const uint32_t nw = (off0 + seg_bits + 31) >> 5;
+    for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
+    __syncwarp();
+    if ((lane & 7) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
+    if (extract_outliers && nz) {
+      unsigned long long o = pz + (iz - nz);
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] == 0) {
+          out_idx[o] = base + j;
+          out_val[o] = x[base + j];
+          o++;
+        }
+      }
+    }
+    {
+      // codes <= 26 bits complete at most one word each: predicated emits;
+      // the lane's first word and final partial word may be shared -> atomic
+      const uint32_t rel = off0 + lane_ex;
+      uint32_t w = rel >> 5;
+      const uint32_t w0 = w;
+      int nb = rel & 31;
+      unsigned long long acc = 0;
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const bool pad = s[j] == kSent;
+        const uint32_t e = pad ? 0u : lb_entry(tab, ctab, win_lo, win_n, s[j]);
+        const int lj = (int)(e & 63);
+        const unsigned long long cj = e >> 6;
+        acc |= lj ? cj << (64 - nb - lj) : 0ull;
+        nb += lj;
+        const bool ready = nb >= 32;
+        const uint32_t hiw = (uint32_t)(acc >> 32);
+        if (ready && w == w0) atomicOr(&wb[w], hiw);
+        if (ready && w != w0) wb[w] = hiw;
+        acc = ready ? (acc << 32) : acc;
+        nb = ready ? nb - 32 : nb;
+        w += ready;
+      }
+      if (nb > 0) atomicOr(&wb[w], (uint32_t)(acc >> 32));
+    }
+    __syncwarp();
+    const uint64_t gw0 = pb >> 5;
+    const uint32_t end_off = (off0 + seg_bits) & 31;
+    for (uint32_t i = lane; i < nw; i += 32) {
+      const uint32_t v = bswap32(wb[i]);
+      const bool shared_word = (i == 0 && off0 != 0) || (i == nw - 1 && end_off != 0);
+      if (shared_word)
+        atomicOr(&payload[gw0 + i], v);
+      else
+        payload[gw0 + i] = v;
+    }
+    __syncwarp();
+  }
+}
+
 template __global__ void k3_encode_lb<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *, uint32_t,
                                                 uint32_t, const float *, uint32_t *, unsigned long long *, float *,
                                                 unsigned long long *, EncLB, unsigned *, int);
@@ -268,4 +459,19 @@ template __global__ void k3_encode_lb<uint32_t>(const uint32_t *, uint64_t, cons
                                                 uint32_t, const float *, uint32_t *, unsigned long long *, float *,
                                                 unsigned long long *, EncLB, unsigned *, int);
 
+}  // namespace actc
+
+namespace actc {
+template __global__ void k3_seg_count<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *, uint32_t,
+                                                uint32_t, uint32_t *, uint32_t *);
+template __global__ void k3_seg_count<uint32_t>(const uint32_t *, uint64_t, const unsigned long long *, uint32_t,
+                                                uint32_t, uint32_t *, uint32_t *);
+template __global__ void k3_seg_pack<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *, uint32_t,
+                                               uint32_t, const float *, const unsigned long long *,
+                                               const unsigned long long *, uint32_t *, unsigned long long *, float *,
+                                               unsigned long long *, int);
+template __global__ void k3_seg_pack<uint32_t>(const uint32_t *, uint64_t, const unsigned long long *, uint32_t,
+                                               uint32_t, const float *, const unsigned long long *,
+                                               const unsigned long long *, uint32_t *, unsigned long long *, float *,
+                                               unsigned long long *, int);
 }  // namespace actc

@@ -122,6 +122,20 @@ __global__ void k3_encode_lb(const SymT *__restrict__ sym, uint64_t n, const uns
                              uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
                              float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off, EncLB st,
                              unsigned *__restrict__ ticket, int extract_outliers);
+template <typename SymT>
+__global__ void k3_seg_count(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
+                             uint32_t win_lo, uint32_t win_n, uint32_t *__restrict__ seg_bits,
+                             uint32_t *__restrict__ seg_nz);
+__global__ void k3_seg_scan(const uint32_t *__restrict__ seg_bits, const uint32_t *__restrict__ seg_nz, uint64_t nseg,
+                            unsigned long long *__restrict__ bit0, unsigned long long *__restrict__ nz0,
+                            unsigned long long *__restrict__ totals);
+template <typename SymT>
+__global__ void k3_seg_pack(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
+                            uint32_t win_lo, uint32_t win_n, const float *__restrict__ x,
+                            const unsigned long long *__restrict__ bit0, const unsigned long long *__restrict__ nz0,
+                            uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
+                            float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
+                            int extract_outliers);
 __global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
                          const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
                          const uint32_t *__restrict__ tail, uint32_t ncta);
