@@ -134,7 +134,7 @@ struct DecResult {
 struct actc_ctx {
   int device = 0;
   int num_sms = 148;
-  Buf sym, hist, cb, ctab, canon, lencnt, status, misc, lut, idx, part;
+  Buf sym, hist, cb, ctab, len8, canon, lencnt, status, misc, lut, idx, part;
   actc_plan_t *plan_dev = nullptr;
   DecResult *dres_dev = nullptr;
   // state carried from plan to encode
@@ -184,6 +184,7 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   int rc;
   if ((rc = grow(c->cb, l.total))) return rc;
   if ((rc = grow(c->ctab, 8 * A))) return rc;
+  if ((rc = grow(c->len8, A + 64))) return rc;
   if ((rc = grow(c->canon, 4 * A))) return rc;
   if ((rc = grow(c->lencnt, 4 * 64))) return rc;
   char *b = (char *)c->cb.p;
@@ -192,6 +193,7 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   a.A = A;
   a.in_lengths = in_lengths;
   a.ctab = (unsigned long long *)c->ctab.p;
+  a.len8 = (uint8_t *)c->len8.p;
   a.canon = (uint32_t *)c->canon.p;
   a.len_counts = (uint32_t *)c->lencnt.p;
   a.out_lengths = out_lengths;
@@ -313,7 +315,8 @@ int actc_ctx_create(int device, actc_ctx **out) {
                        (const void *)k4w_decode<0, 32>,         (const void *)k4w_decode<1, 32>,
                        (const void *)k4w_decode<2, 32>,         (const void *)k3_encode_lb<uint16_t>,
                        (const void *)k3_encode_lb<uint32_t>,    (const void *)k3_seg_pack<uint16_t>,
-                       (const void *)k3_seg_pack<uint32_t>};
+                       (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
+                       (const void *)k3_seg_count<uint32_t>};
   for (const void *f : big) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, f));
@@ -336,7 +339,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
 
 void actc_ctx_destroy(actc_ctx *c) {
   if (!c) return;
-  Buf *bufs[] = {&c->sym, &c->hist, &c->cb, &c->ctab, &c->canon, &c->lencnt,
+  Buf *bufs[] = {&c->sym, &c->hist, &c->cb, &c->ctab, &c->len8, &c->canon, &c->lencnt,
                  &c->status, &c->misc, &c->lut, &c->idx, &c->part};
   for (Buf *b : bufs)
     if (b->p) cudaFree(b->p);
@@ -428,43 +431,56 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     if (!getenv("ACTC_K3_LB")) {
       // two passes over 1024-symbol segments, no inter-warp waiting
       const uint64_t nseg = cdiv(n, K3L_SEG);
-      const size_t tsm = (size_t)((lwin_n + 3) & ~3u) * 4;
-      const size_t psm = tsm + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
-      if ((rc = grow(c->status, nseg * 24 + 1024))) return rc;
-      unsigned long long *bit0 = (unsigned long long *)c->status.p, *nz0 = bit0 + nseg;
-      uint32_t *sbits = (uint32_t *)(nz0 + nseg), *snz = sbits + nseg;
-      unsigned long long *misc = (unsigned long long *)c->misc.p;
-      CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
+      SegArgs g;
+      g.n = n;
+      g.ctab = (const unsigned long long *)c->ctab.p;
+      g.len8 = (const uint8_t *)c->len8.p;
+      g.lo = lo;
+      g.span = span;
+      g.win_lo = lwin_lo;
+      g.win_n = lwin_n;
+      const bool l8 = span <= 65536;
+      const size_t csm = l8 ? (size_t)((((lo & 15u) + span + 15) & ~15u)) : 16;
+      const size_t psm = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
       const void *fc = sb == 2 ? (const void *)k3_seg_count<uint16_t> : (const void *)k3_seg_count<uint32_t>;
       const void *fp = sb == 2 ? (const void *)k3_seg_pack<uint16_t> : (const void *)k3_seg_pack<uint32_t>;
       int occ_c = 0, occ_p = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, fc, K3L_THREADS, tsm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, fc, K3L_THREADS, csm);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, fp, K3L_THREADS, psm);
-      const uint64_t wseg = cdiv(nseg, K3L_THREADS / 32);
-      const int gc = (int)std::max<uint64_t>(1, std::min<uint64_t>(wseg, (uint64_t)std::max(1, occ_c) * c->num_sms));
-      const int gp = (int)std::max<uint64_t>(1, std::min<uint64_t>(wseg, (uint64_t)std::max(1, occ_p) * c->num_sms));
-      const unsigned long long *ct = (const unsigned long long *)c->ctab.p;
+      const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
+      g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
+      g.ncta = (uint32_t)cdiv(nseg, g.spc);
+      if ((rc = grow(c->status, nseg * 8 + (size_t)g.ncta * 16 + 1024))) return rc;
+      g.cta_bits = (unsigned long long *)c->status.p;
+      g.cta_nz = g.cta_bits + g.ncta;
+      g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
+      g.seg_nz = g.seg_bits + nseg;
+      g.x = x;
+      g.payload = (uint32_t *)payload;
+      g.out_idx = (unsigned long long *)out_idx;
+      g.out_val = out_val;
+      g.chunk_off = (unsigned long long *)chunk_off;
+      g.extract = extract;
+      CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
+      const int gp = (int)std::max<uint64_t>(
+          1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), (uint64_t)std::max(1, occ_p) * c->num_sms));
       {
         KT(ACTC_KIND_COUNT);
         if (sb == 2)
-          k3_seg_count<uint16_t><<<gc, K3L_THREADS, tsm, s>>>((const uint16_t *)sym, n, ct, lwin_lo, lwin_n, sbits, snz);
+          k3_seg_count<uint16_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint16_t *)sym, g);
         else
-          k3_seg_count<uint32_t><<<gc, K3L_THREADS, tsm, s>>>((const uint32_t *)sym, n, ct, lwin_lo, lwin_n, sbits, snz);
+          k3_seg_count<uint32_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint32_t *)sym, g);
       }
       {
         KT(ACTC_KIND_SCAN);
-        k3_seg_scan<<<1, 1024, 0, s>>>(sbits, snz, nseg, bit0, nz0, misc + M_SCAN_TOT);
+        k3_cta_scan<<<1, 1024, 0, s>>>(g);
       }
       {
         KT(ACTC_KIND_PACK);
         if (sb == 2)
-          k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, n, ct, lwin_lo, lwin_n, x, bit0, nz0,
-                                                             (uint32_t *)payload, (unsigned long long *)out_idx,
-                                                             out_val, (unsigned long long *)chunk_off, extract);
+          k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, g);
         else
-          k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, n, ct, lwin_lo, lwin_n, x, bit0, nz0,
-                                                             (uint32_t *)payload, (unsigned long long *)out_idx,
-                                                             out_val, (unsigned long long *)chunk_off, extract);
+          k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
       }
       CKL();
       return ACTC_OK;

@@ -724,6 +724,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
         const uint32_t l = (uint32_t)(kk[u] >> kSymKeyBits), s = sy[u];
         a.canon[i] = s;
         if (a.ctab && l <= 56) a.ctab[s] = ((s_first[l] + (i - s_base[l])) << 8) | l;
+        if (a.len8) a.len8[s] = (uint8_t)l;
       }
     }
   }

@@ -263,11 +263,18 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
 
 // ===========================================================================
 // Two-pass, barrier-free variant (the production path for codes <= 26 bits):
-//   k3_seg_count  warp per 1024-symbol segment: code bits + outlier markers
-//   k3_seg_scan   one CTA: exclusive prefixes (u64) over the segments
-//   k3_seg_pack   warp per segment at its known bit offset: pack + store
+//   k3_seg_count  CTA b owns segments [b*spc, (b+1)*spc); warp per 1024-symbol
+//                 segment sums code lengths (byte table of the live range in
+//                 shared memory) and outlier markers; the CTA then turns its
+//                 segment counts into exclusive in-CTA prefixes and writes its
+//                 totals
+//   k3_cta_scan   one CTA: exclusive prefixes of the CTA totals (in place)
+//   k3_seg_pack   warp per segment at bit cta_prefix + in-CTA prefix: one
+//                 (code, len) lookup per symbol into registers, pack, store
 // Symbols are read twice (2 x 2 B), but no warp ever waits for another.
 // ===========================================================================
+
+constexpr uint32_t K3S_L8MAX = 65536;  // byte length table in shared memory (u16 symbol range)
 
 __device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned long long *__restrict__ ctab,
                                                uint32_t win_lo, uint32_t win_n, int nthreads) {
@@ -287,111 +294,142 @@ __device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned lon
 }
 
 template <typename SymT>
-__global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restrict__ sym, uint64_t n,
-                                                            const unsigned long long *__restrict__ ctab,
-                                                            uint32_t win_lo, uint32_t win_n,
-                                                            uint32_t *__restrict__ seg_bits,
-                                                            uint32_t *__restrict__ seg_nz) {
-  extern __shared__ __align__(16) uint32_t k3c_sm[];
-  k3_load_window(k3c_sm, ctab, win_lo, win_n, K3L_THREADS);
+__global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restrict__ sym, SegArgs a) {
+  extern __shared__ __align__(16) uint8_t k3c_l8[];
+  __shared__ unsigned long long wsum_b[K3L_THREADS / 32 + 1], wsum_z[K3L_THREADS / 32 + 1];
+  const bool smem_tab = a.span <= K3S_L8MAX;
+  uint32_t shift = 0;
+  if (smem_tab) {
+    // len8[lo, lo+span) -> shared, 16-byte loads from an aligned start (the
+    // global table is padded by 64 bytes), 16 in flight per thread
+    const uint32_t a0 = a.lo & ~15u;
+    shift = a.lo - a0;
+    const uint32_t nv = (shift + a.span + 15) >> 4;
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.len8 + a0);
+    for (uint32_t i0 = threadIdx.x; i0 < nv; i0 += 16 * K3L_THREADS) {
+      uint4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; u++) {
+        const uint32_t i = i0 + u * K3L_THREADS;
+        v[u] = i < nv ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; u++) {
+        const uint32_t i = i0 + u * K3L_THREADS;
+        if (i < nv) reinterpret_cast<uint4 *>(k3c_l8)[i] = v[u];
+      }
+    }
+  }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint64_t nseg = (n + K3L_SEG - 1) / K3L_SEG;
-  const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
-  for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + (threadIdx.x >> 5); seg < nseg; seg += nwarps) {
+  const uint8_t *l8 = k3c_l8 + shift;  // l8[s - lo]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
+  const uint64_t s0 = (uint64_t)blockIdx.x * a.spc, s1 = min(nseg, s0 + a.spc);
+  unsigned long long tb = 0, tz = 0;
+  for (uint64_t seg = s0 + warp; seg < s1; seg += K3L_THREADS / 32) {
     const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
     uint32_t s[K3L_EPT];
-    lb_load(sym, base, n, s);
+    lb_load(sym, base, a.n, s);
     uint32_t bits = 0, nz = 0;
 #pragma unroll
     for (int j = 0; j < K3L_EPT; j++) {
       if (s[j] != kSent) {
-        bits += lb_entry(k3c_sm, ctab, win_lo, win_n, s[j]) & 63;
+        bits += smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
         nz += s[j] == 0;
       }
     }
     bits = warp_sum(bits);
     nz = warp_sum(nz);
     if (lane == 0) {
-      seg_bits[seg] = bits;
-      seg_nz[seg] = nz;
+      a.seg_bits[seg] = bits;
+      a.seg_nz[seg] = nz;
+      tb += bits;
+      tz += nz;
     }
   }
-}
-
-// exclusive prefixes of (bits, outliers) over the segments; one CTA of 1024,
-// 8 consecutive segments per thread per round
-__global__ void __launch_bounds__(1024) k3_seg_scan(const uint32_t *__restrict__ seg_bits,
-                                                    const uint32_t *__restrict__ seg_nz, uint64_t nseg,
-                                                    unsigned long long *__restrict__ bit0,
-                                                    unsigned long long *__restrict__ nz0,
-                                                    unsigned long long *__restrict__ totals) {
-  __shared__ unsigned long long wb[33], wz[33];
+  __syncthreads();  // this CTA's segment counts are visible to the whole CTA
+  // in-CTA exclusive prefixes (u32: spc * 1024 * 26 bits < 2^32 for spc < 2^17)
   unsigned long long runb = 0, runz = 0;
-  for (uint64_t c0 = 0; c0 < nseg; c0 += 8 * 1024) {
-    const uint64_t i0 = c0 + 8ull * threadIdx.x;
-    uint32_t b[8], z[8];
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      b[u] = i0 + u < nseg ? seg_bits[i0 + u] : 0u;
-      z[u] = i0 + u < nseg ? seg_nz[i0 + u] : 0u;
-    }
-    unsigned long long tb = 0, tz = 0;
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      tb += b[u];
-      tz += z[u];
-    }
+  for (uint64_t c0 = s0; c0 < s1; c0 += K3L_THREADS) {
+    const uint64_t i = c0 + threadIdx.x;
+    const uint32_t vb = i < s1 ? a.seg_bits[i] : 0u, vz = i < s1 ? a.seg_nz[i] : 0u;
     unsigned long long allb, allz;
-    const unsigned long long eb = block_excl_sum<unsigned long long>(tb, wb, &allb);
-    const unsigned long long ez = block_excl_sum<unsigned long long>(tz, wz, &allz);
-    unsigned long long rb = runb + eb, rz = runz + ez;
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      if (i0 + u < nseg) {
-        bit0[i0 + u] = rb;
-        nz0[i0 + u] = rz;
-      }
-      rb += b[u];
-      rz += z[u];
+    const unsigned long long eb = block_excl_sum<unsigned long long>(vb, wsum_b, &allb);
+    const unsigned long long ez = block_excl_sum<unsigned long long>(vz, wsum_z, &allz);
+    if (i < s1) {
+      a.seg_bits[i] = (uint32_t)(runb + eb);
+      a.seg_nz[i] = (uint32_t)(runz + ez);
     }
     runb += allb;
     runz += allz;
   }
   if (threadIdx.x == 0) {
-    totals[0] = runb;
-    totals[1] = runz;
+    a.cta_bits[blockIdx.x] = runb;
+    a.cta_nz[blockIdx.x] = runz;
+  }
+}
+
+// exclusive prefixes of the per-CTA totals, in place (one CTA of 1024)
+__global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
+  __shared__ unsigned long long wb[33], wz[33];
+  unsigned long long runb = 0, runz = 0;
+  for (uint32_t c0 = 0; c0 < a.ncta; c0 += 1024) {
+    const uint32_t i = c0 + threadIdx.x;
+    const unsigned long long vb = i < a.ncta ? a.cta_bits[i] : 0ull, vz = i < a.ncta ? a.cta_nz[i] : 0ull;
+    unsigned long long allb, allz;
+    const unsigned long long eb = block_excl_sum<unsigned long long>(vb, wb, &allb);
+    const unsigned long long ez = block_excl_sum<unsigned long long>(vz, wz, &allz);
+    if (i < a.ncta) {
+      a.cta_bits[i] = runb + eb;
+      a.cta_nz[i] = runz + ez;
+    }
+    runb += allb;
+    runz += allz;
   }
 }
 
 template <typename SymT>
-__global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(
-    const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab, uint32_t win_lo,
-    uint32_t win_n, const float *__restrict__ x, const unsigned long long *__restrict__ bit0,
-    const unsigned long long *__restrict__ nz0, uint32_t *__restrict__ payload,
-    unsigned long long *__restrict__ out_idx, float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
-    int extract_outliers) {
+__global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint32_t k3p_sm[];
   uint32_t *tab = k3p_sm;
-  k3_load_window(tab, ctab, win_lo, win_n, K3L_THREADS);
+  k3_load_window(tab, a.ctab, a.win_lo, a.win_n, K3L_THREADS);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t *wb = k3p_sm + ((win_n + 3) & ~3u) + warp * K3L_WORDS;
-  const uint64_t nseg = (n + K3L_SEG - 1) / K3L_SEG;
+  uint32_t *wb = k3p_sm + ((a.win_n + 3) & ~3u) + warp * K3L_WORDS;
+  const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
   const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
+  const uint32_t wlast = a.win_n - 1;
   for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + warp; seg < nseg; seg += nwarps) {
     const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
     uint32_t s[K3L_EPT];
-    lb_load(sym, base, n, s);
-    const unsigned long long pb = bit0[seg], pz = nz0[seg];
-    uint32_t bits = 0, nz = 0;
+    lb_load(sym, base, a.n, s);
+    const uint64_t r = seg / a.spc;
+    const unsigned long long pb = a.cta_bits[r] + a.seg_bits[seg], pz = a.cta_nz[r] + a.seg_nz[seg];
+    // one (code << 6 | len) lookup per symbol: clamped into the shared window,
+    // symbols outside it (rare, long codes) fixed up from the global table
+    uint32_t e[K3L_EPT];
+    uint32_t oow = 0, zmask = 0;
 #pragma unroll
     for (int j = 0; j < K3L_EPT; j++) {
-      if (s[j] != kSent) {
-        bits += lb_entry(tab, ctab, win_lo, win_n, s[j]) & 63;
-        nz += s[j] == 0;
+      const uint32_t wi = s[j] - a.win_lo;
+      const bool sent = s[j] == kSent;
+      e[j] = sent ? 0u : tab[min(wi, wlast)];
+      oow |= (uint32_t)(wi > wlast && !sent) << j;
+      zmask |= (uint32_t)(s[j] == 0) << j;
+    }
+    if (oow) {
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        if ((oow >> j) & 1u) {  // re-read the symbol: s[] is dead here (register pressure)
+          const unsigned long long g = __ldg(&a.ctab[(uint32_t)sym[base + j]]);
+          e[j] = (uint32_t)(((g >> 8) << 6) | (g & 63));
+        }
       }
     }
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < K3L_EPT; j++) bits += e[j] & 63;
+    const uint32_t nz = __popc(zmask);
     const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nz);
     const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31);
     const uint32_t lane_ex = ib - bits;
@@ -399,21 +437,20 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(
     const uint32_t nw = (off0 + seg_bits + 31) >> 5;
     for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
     __syncwarp();
-    if ((lane & 7) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
-    if (extract_outliers && nz) {
+    if ((lane & 7) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
+    if (a.extract && nz) {
       unsigned long long o = pz + (iz - nz);
-#pragma unroll
-      for (int j = 0; j < K3L_EPT; j++) {
-        if (s[j] == 0) {
-          out_idx[o] = base + j;
-          out_val[o] = x[base + j];
-          o++;
-        }
+      for (uint32_t m = zmask; m; m &= m - 1) {
+        const uint64_t e_idx = base + (uint32_t)(__ffs(m) - 1);
+        a.out_idx[o] = e_idx;
+        a.out_val[o] = a.x[e_idx];
+        o++;
       }
     }
     {
       // codes <= 26 bits complete at most one word each: predicated emits;
-      // the lane's first word and final partial word may be shared -> atomic
+      // the lane's first word and final partial word may be shared -> atomic.
+      // A length-0 entry (past the end) has code 0.
       const uint32_t rel = off0 + lane_ex;
       uint32_t w = rel >> 5;
       const uint32_t w0 = w;
@@ -421,11 +458,8 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(
       unsigned long long acc = 0;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        const bool pad = s[j] == kSent;
-        const uint32_t e = pad ? 0u : lb_entry(tab, ctab, win_lo, win_n, s[j]);
-        const int lj = (int)(e & 63);
-        const unsigned long long cj = e >> 6;
-        acc |= lj ? cj << (64 - nb - lj) : 0ull;
+        const int lj = (int)(e[j] & 63);
+        acc |= (unsigned long long)(e[j] >> 6) << ((64 - nb - lj) & 63);  // len 0 -> code 0
         nb += lj;
         const bool ready = nb >= 32;
         const uint32_t hiw = (uint32_t)(acc >> 32);
@@ -444,9 +478,9 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(
       const uint32_t v = bswap32(wb[i]);
       const bool shared_word = (i == 0 && off0 != 0) || (i == nw - 1 && end_off != 0);
       if (shared_word)
-        atomicOr(&payload[gw0 + i], v);
+        atomicOr(&a.payload[gw0 + i], v);
       else
-        payload[gw0 + i] = v;
+        a.payload[gw0 + i] = v;
     }
     __syncwarp();
   }
@@ -462,16 +496,8 @@ template __global__ void k3_encode_lb<uint32_t>(const uint32_t *, uint64_t, cons
 }  // namespace actc
 
 namespace actc {
-template __global__ void k3_seg_count<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *, uint32_t,
-                                                uint32_t, uint32_t *, uint32_t *);
-template __global__ void k3_seg_count<uint32_t>(const uint32_t *, uint64_t, const unsigned long long *, uint32_t,
-                                                uint32_t, uint32_t *, uint32_t *);
-template __global__ void k3_seg_pack<uint16_t>(const uint16_t *, uint64_t, const unsigned long long *, uint32_t,
-                                               uint32_t, const float *, const unsigned long long *,
-                                               const unsigned long long *, uint32_t *, unsigned long long *, float *,
-                                               unsigned long long *, int);
-template __global__ void k3_seg_pack<uint32_t>(const uint32_t *, uint64_t, const unsigned long long *, uint32_t,
-                                               uint32_t, const float *, const unsigned long long *,
-                                               const unsigned long long *, uint32_t *, unsigned long long *, float *,
-                                               unsigned long long *, int);
+template __global__ void k3_seg_count<uint16_t>(const uint16_t *, SegArgs);
+template __global__ void k3_seg_count<uint32_t>(const uint32_t *, SegArgs);
+template __global__ void k3_seg_pack<uint16_t>(const uint16_t *, SegArgs);
+template __global__ void k3_seg_pack<uint32_t>(const uint32_t *, SegArgs);
 }  // namespace actc

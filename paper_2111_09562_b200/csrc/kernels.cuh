@@ -72,6 +72,7 @@ struct CodebookArgs {
   const uint16_t *in_lengths;      // if non-null: skip Huffman, use these lengths
   // outputs
   unsigned long long *ctab;        // [A] (code << 8) | len, live entries only
+  uint8_t *len8;                   // [A] code length per symbol, live entries only (may be null)
   uint32_t *canon;                 // [L] canonical order
   uint32_t *len_counts;            // [64]
   uint16_t *out_lengths;           // optional [A] full length table
@@ -122,20 +123,29 @@ __global__ void k3_encode_lb(const SymT *__restrict__ sym, uint64_t n, const uns
                              uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
                              float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off, EncLB st,
                              unsigned *__restrict__ ticket, int extract_outliers);
+// segment encoder (codes <= 26 bits): per-CTA ranges of segments
+struct SegArgs {
+  uint64_t n;
+  const unsigned long long *ctab;  // [A] (code << 8) | len
+  const uint8_t *len8;             // [A] lengths
+  uint32_t lo, span;               // live symbol range (len8 window)
+  uint32_t win_lo, win_n;          // (code, len) window for the pack pass
+  uint64_t spc;                    // segments per count CTA
+  uint32_t *seg_bits, *seg_nz;     // [nseg]
+  unsigned long long *cta_bits, *cta_nz;  // [ncta] totals, then exclusive prefixes (in place)
+  uint32_t ncta;
+  const float *x;
+  uint32_t *payload;
+  unsigned long long *out_idx;
+  float *out_val;
+  unsigned long long *chunk_off;
+  int extract;
+};
 template <typename SymT>
-__global__ void k3_seg_count(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
-                             uint32_t win_lo, uint32_t win_n, uint32_t *__restrict__ seg_bits,
-                             uint32_t *__restrict__ seg_nz);
-__global__ void k3_seg_scan(const uint32_t *__restrict__ seg_bits, const uint32_t *__restrict__ seg_nz, uint64_t nseg,
-                            unsigned long long *__restrict__ bit0, unsigned long long *__restrict__ nz0,
-                            unsigned long long *__restrict__ totals);
+__global__ void k3_seg_count(const SymT *__restrict__ sym, SegArgs a);
+__global__ void k3_cta_scan(SegArgs a);
 template <typename SymT>
-__global__ void k3_seg_pack(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
-                            uint32_t win_lo, uint32_t win_n, const float *__restrict__ x,
-                            const unsigned long long *__restrict__ bit0, const unsigned long long *__restrict__ nz0,
-                            uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
-                            float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off,
-                            int extract_outliers);
+__global__ void k3_seg_pack(const SymT *__restrict__ sym, SegArgs a);
 __global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
                          const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
                          const uint32_t *__restrict__ tail, uint32_t ncta);
