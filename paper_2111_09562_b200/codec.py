@@ -134,7 +134,7 @@ class _DevBufs:
     added individually (uploads, the lazily rebuilt index) are plain
     tensors.  Mapping-like: [], in, values(), ptr()."""
 
-    __slots__ = ("_bufs", "_slots", "_views")
+    __slots__ = ("_bufs", "_slots", "_views", "offsets")
 
     _DT = {"payload": "uint8", "out_idx": "int64", "out_val": "float32", "canon": "int32",
            "len_counts": "int32", "chunk_off": "int64", "chunk_lat": "int64"}
@@ -143,18 +143,22 @@ class _DevBufs:
         self._bufs = []      # backing tensors (carved bases and plain arrays)
         self._slots = {}     # name -> (base tensor, byte offset, numel, itemsize)
         self._views = {}
+        self.offsets = {}
 
     def carve(self, device, layout):
         """layout: [(name, numel, itemsize)] -> one allocation, 16-byte aligned slots."""
-        torch = _lib.torch_cuda()
-        offs, o = [], 0
+        import torch
+
+        offs, o = {}, 0
         for name, numel, isz in layout:
-            offs.append(o)
+            offs[name] = o
             o += (numel * isz + 15) & ~15
         base = torch.empty(max(o, 16), dtype=torch.uint8, device=device)
         self._bufs.append(base)
-        for (name, numel, isz), off in zip(layout, offs):
-            self._slots[name] = (base, off, numel, isz)
+        slots = self._slots
+        for name, numel, isz in layout:
+            slots[name] = (base, offs[name], numel, isz)
+        self.offsets = offs
         return base
 
     def __setitem__(self, name, t):
@@ -470,16 +474,17 @@ def _finish_compress(x, params, dims, plan, dev, ctx, sh):
         raise ParameterError("Huffman code length exceeds 63 bits")
     # one allocation per container, carved (the host cost per tensor is on
     # the critical path of compress_batch)
-    dev.carve(x.device, [("chunk_off", (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK, 8),
-                         ("out_idx", plan.n_outliers, 8),
-                         ("payload", _payload_buffer_bytes(plan.payload_bits), 1),
-                         ("out_val", plan.n_outliers, 4), ("canon", max(plan.live_symbols, 1), 4),
-                         ("len_counts", 64, 4)])
-    _lib.raise_for(_lib.lib().actc_compress_encode(
-        ctx.handle, C.c_void_p(x.data_ptr()), C.byref(plan), C.c_void_p(dev.ptr("payload")),
-        C.c_void_p(dev.ptr("out_idx")), C.c_void_p(dev.ptr("out_val")),
-        C.c_void_p(dev.ptr("canon")), C.c_void_p(dev.ptr("len_counts")),
-        C.c_void_p(dev.ptr("chunk_off")), sh))
+    k, live = plan.n_outliers, max(plan.live_symbols, 1)
+    base = dev.carve(x.device, [("chunk_off", (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK, 8),
+                                ("out_idx", k, 8), ("payload", _payload_buffer_bytes(plan.payload_bits), 1),
+                                ("out_val", k, 4), ("canon", live, 4), ("len_counts", 64, 4)])
+    bp = base.data_ptr()
+    o = dev.offsets
+    rc = _lib.lib().actc_compress_encode(ctx.handle, x.data_ptr(), C.byref(plan), bp + o["payload"],
+                                         bp + o["out_idx"], bp + o["out_val"], bp + o["canon"],
+                                         bp + o["len_counts"], bp + o["chunk_off"], sh)
+    if rc:
+        _lib.raise_for(rc)
     c = CompressedActivation._from_device(dims, params, dev, plan.payload_bits, plan.n_outliers,
                                           plan.live_symbols, plan.rle_runs)
     blob_len = _cmtz_size(len(dims), plan.n_outliers, plan.rle_runs, plan.payload_bits)
@@ -558,11 +563,10 @@ def compress_batch(xs, params, max_concurrency: int = 8):
                     still.append(job)
                     continue
                 plan = _lib.Plan.from_buffer_copy(ctx.plan)
-                with torch.cuda.stream(s):
-                    c, rep = _finish_compress(x, p, tuple(x.shape) or (1,), plan, dev, ctx, sh)
-                for t in c._dev.values():  # used on both the side and the caller's stream
+                # buffers are allocated on the caller's stream and written on s
+                c, rep = _finish_compress(x, p, tuple(x.shape) or (1,), plan, dev, ctx, sh)
+                for t in dev._bufs:
                     t.record_stream(s)
-                    t.record_stream(main)
                 x.record_stream(s)
                 results.append((i, c, rep))
             pending = still
