@@ -148,7 +148,7 @@ namespace {
 
 // codebook scratch carve-up for alphabet A
 struct CbLayout {
-  size_t live_sym, live_freq, keys, keys2, vals, vals2, nf, lpar, npar, llen, ndepth, total;
+  size_t live_sym, live_freq, keys, keys2, vals, vals2, nf, lpar, npar, llen, ndepth, cls16, total;
 };
 CbLayout cb_layout(uint64_t A) {
   CbLayout l;
@@ -171,9 +171,13 @@ CbLayout cb_layout(uint64_t A) {
   l.npar = take(4 * A);
   l.llen = take(A);
   l.ndepth = take(4 * A);
+  l.cls16 = take(2 * A);
   l.total = o;
   return l;
 }
+
+// misc counters layout (u64 slots)
+enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SLOTS = 8 };
 
 constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
@@ -214,12 +218,24 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   a.n_symbols = n_symbols;
   a.sym_bytes = sym_bytes;
   a.dbg = nullptr;
+  a.cls16 = (uint16_t *)(b + l.cls16);
+  a.fallback = (unsigned *)((unsigned long long *)c->misc.p + M_K2GATE);
+  a.gate = nullptr;
   if (getenv("ACTC_K2_TIMING")) {
     int rc2 = grow(c->idx, 4096);
     if (rc2) return rc2;
     a.dbg = (unsigned long long *)c->idx.p;
   }
   CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
+  // frequency-class codebook first; it hands over to k2_codebook (gated)
+  // when its capacities are exceeded
+  static const bool no_k2r = getenv("ACTC_K2_OLD") != nullptr;
+  if (!in_lengths && A <= 65536 && n_symbols < (1ull << 32) && !no_k2r) {
+    KT(ACTC_KIND_CODEBOOK);
+    CK(cudaMemsetAsync(a.fallback, 0xFF, 4, s));
+    k2r_codebook<<<1, K2_THREADS, kK2rSmem, s>>>(a);
+    a.gate = a.fallback;
+  }
   {
     KT(ACTC_KIND_CODEBOOK);
     k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
@@ -228,8 +244,6 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   return ACTC_OK;
 }
 
-// misc counters layout (u64 slots)
-enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_SLOTS = 8 };
 
 }  // namespace
 
@@ -244,6 +258,14 @@ int actc_debug_k2_timing(actc_ctx *c, uint64_t *out32) {
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(out32, c->idx.p, 32 * 8, cudaMemcpyDeviceToHost));
   return ACTC_OK;
+}
+
+// 1 if the last codebook on this ctx came from the frequency-class kernel (synchronizes)
+int actc_debug_k2r_used(actc_ctx *c) {
+  unsigned v = 0xFFFFFFFFu;
+  cudaDeviceSynchronize();
+  cudaMemcpy(&v, (unsigned long long *)c->misc.p + M_K2GATE, 4, cudaMemcpyDeviceToHost);
+  return v == 0u ? 1 : 0;
 }
 
 int actc_timing_enable(int on) {
@@ -300,6 +322,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
     return rc;
   }
   CK(cudaFuncSetAttribute(k2_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2Smem));
+  CK(cudaFuncSetAttribute(k2r_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2rSmem));
   // occupancy-derived persistent grid sizes
   int nb = 0;
   size_t k1smem = K1_WIN * 4;

@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_codebook(CodebookArgs a) {
   __shared__ uint32_t s_odd_item;
   __shared__ double dbuf[33];
 
+  if (a.gate && *a.gate == 0u) return;  // k2r produced the codebook
   const int tid = threadIdx.x;
   const uint64_t A = a.A;
 #define K2_STAMP(i) \

@@ -90,8 +90,16 @@ struct CodebookArgs {
   uint64_t n_symbols;              // total symbol count (for entropy)
   uint32_t sym_bytes;
   unsigned long long *dbg;         // optional stage timestamps (clock64)
+  uint16_t *cls16;                 // [A] class id per symbol (k2r scratch)
+  unsigned *fallback;              // k2r: 1 = caps exceeded, run k2_codebook
+  const unsigned *gate;            // k2_codebook: if non-null and *gate == 0, do nothing
 };
 __global__ void k2_codebook(CodebookArgs a);
+// K2r (frequency-class codebook) capacities; dynamic shared memory size
+constexpr uint32_t kRCap = 6144;
+constexpr uint32_t kICap = 11264;
+constexpr size_t kK2rSmem = (size_t)(3 * (kRCap + 1) + 3 * (kICap + 1)) * 4;
+__global__ void k2r_codebook(CodebookArgs a);
 
 template <typename SymT, bool WIDE>
 __global__ void k3_count(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
