@@ -12,6 +12,7 @@ from .codec import (
     compress_batch,
     compress_device,
     decompress,
+    decompress_batch,
     decompress_device,
     lorenzo_decode,
     lorenzo_encode,

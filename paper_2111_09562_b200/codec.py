@@ -315,6 +315,12 @@ class CompressedActivation:
         self._dev = dev
         return dev
 
+    def _record_stream(self, s):
+        """mark the device buffers as in use on side stream s (caching allocator)"""
+        if self._dev is not None:
+            for t in self._dev.values():
+                t.record_stream(s)
+
     def _desc(self, with_index=True) -> _lib.StreamDesc:
         dev = self._dev
         d = _lib.StreamDesc()
@@ -618,6 +624,47 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
     if r.markers != c._n_outliers:
         raise FormatError("outlier markers disagree with stored indices")
     return out, int(r.nonzero)
+
+
+def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8):
+    """Reconstruct several streams concurrently, each on its own stream and
+    context (a small tensor's decode alone does not fill the GPU).  Results
+    are ordered on the caller's current stream; no host synchronisation, so
+    status and nonzero counts are not checked (decompress_device does that).
+    """
+    torch = _lib.torch_cuda()
+    dtype = torch.float32 if dtype is None else dtype
+    if outs is None:
+        outs = [torch.empty(c.dims, dtype=dtype, device="cuda") for c in cs]
+    if not cs:
+        return outs
+    dev_index = outs[0].device.index
+    main = torch.cuda.current_stream()
+    order = sorted(range(len(cs)), key=lambda i: -cs[i].element_count)  # largest first
+    for g0 in range(0, len(cs), max_concurrency):
+        group = order[g0:g0 + max_concurrency]
+        streams = _stream_pool(dev_index, len(group))
+        ready = main.record_event()
+        for slot, i in enumerate(group):
+            c, out = cs[i], outs[i]
+            n = c.element_count
+            if c.symbol_count != n:
+                raise FormatError(f"symbol count {c.symbol_count} != element count {n}")
+            if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
+                raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
+            c._ensure_index()
+            s = streams[slot]
+            s.wait_event(ready)
+            ctx = _lib.context_for(dev_index, slot)
+            code = _lib.ACTC_DTYPE_F32 if out.dtype == torch.float32 else _lib.ACTC_DTYPE_F64
+            d = c._desc()
+            _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
+                                                       C.c_void_p(ctx.dres_buf.data_ptr()), C.c_void_p(s.cuda_stream)))
+            out.record_stream(s)
+            c._record_stream(s)
+        for slot in range(len(group)):
+            main.wait_stream(streams[slot])
+    return outs
 
 
 def decompress(c: CompressedActivation) -> Tensor:

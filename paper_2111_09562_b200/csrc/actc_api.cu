@@ -67,6 +67,7 @@ int grow(Buf &b, size_t bytes) {
 struct KRec {
   int kind;
   cudaEvent_t a, b;
+  cudaStream_t s;
 };
 std::atomic<unsigned long long> g_launches[ACTC_KIND_NKINDS];
 std::atomic<bool> g_timing{false};
@@ -105,7 +106,7 @@ struct KTimer {
     if (a && b) {
       cudaEventRecord(b, s);
       std::lock_guard<std::mutex> g(g_tmu);
-      g_recs.push_back({kind, a, b});
+      g_recs.push_back({kind, a, b, s});
     } else {
       std::lock_guard<std::mutex> g(g_tmu);
       if (a) g_pool.push_back(a);
@@ -171,7 +172,7 @@ CbLayout cb_layout(uint64_t A) {
   l.npar = take(4 * A);
   l.llen = take(A);
   l.ndepth = take(4 * A);
-  l.cls16 = take(2 * A);
+  l.cls16 = take(2 * A + 64);
   l.total = o;
   return l;
 }
@@ -266,6 +267,57 @@ int actc_debug_k2r_used(actc_ctx *c) {
   cudaDeviceSynchronize();
   cudaMemcpy(&v, (unsigned long long *)c->misc.p + M_K2GATE, 4, cudaMemcpyDeviceToHost);
   return v == 0u ? 1 : 0;
+}
+
+// debug: per-launch timeline of the timed launches since the last call
+// (kind, start ms, end ms, stream slot) relative to the earliest start;
+// consumes the records like actc_kernel_stats.  Returns the record count.
+int actc_debug_timeline(double *out, int cap) {
+  std::vector<KRec> recs;
+  {
+    std::lock_guard<std::mutex> g(g_tmu);
+    recs.swap(g_recs);
+  }
+  int n = 0;
+  if (!recs.empty()) {
+    for (const KRec &r : recs) cudaEventSynchronize(r.b);
+    cudaEvent_t ref = recs[0].a;
+    float best = 0.f;
+    for (const KRec &r : recs) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, ref, r.a) == cudaSuccess && t < best) {
+        best = t;
+      }
+    }
+    std::vector<cudaStream_t> slots;
+    for (const KRec &r : recs) {
+      if (n >= cap) break;
+      float t0 = 0.f, t1 = 0.f;
+      cudaEventElapsedTime(&t0, ref, r.a);
+      cudaEventElapsedTime(&t1, ref, r.b);
+      int slot = -1;
+      for (size_t q = 0; q < slots.size(); q++)
+        if (slots[q] == r.s) slot = (int)q;
+      if (slot < 0) {
+        slot = (int)slots.size();
+        slots.push_back(r.s);
+      }
+      out[4 * n] = r.kind;
+      out[4 * n + 1] = t0 - best;
+      out[4 * n + 2] = t1 - best;
+      out[4 * n + 3] = slot;
+      n++;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(g_tmu);
+    for (const KRec &r : recs) {
+      g_pool.push_back(r.a);
+      g_pool.push_back(r.b);
+    }
+  }
+  cudaGetLastError();
+  return n;
 }
 
 int actc_timing_enable(int on) {
@@ -627,13 +679,17 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   st.agg_r = (int *)(b + o); o += ((ntiles * 4 + 255) / 256) * 256;
   st.agg_v = (long long *)(b + o); o += ntiles * 8;
   st.inc_v = (long long *)(b + o);
-  CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
+  const bool warp_dec = S.chunk_lat_dev || mode == 2;
   unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
-  CK(cudaMemsetAsync(ticket, 0, 8, s));
+  if (!warp_dec) {  // look-back state of the scan decoder
+    CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
+    CK(cudaMemsetAsync(ticket, 0, 8, s));
+  }
   CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
   {
     KT(ACTC_KIND_LUT);
-    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p);
+    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p,
+                                               warp_dec ? 1 : 0);
   }
   CKL();
   DecodeArgs a;
@@ -662,7 +718,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.live = S.live_symbols;
   const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
   KT(ACTC_KIND_DECODE);
-  if (S.chunk_lat_dev || mode == 2) {
+  if (warp_dec) {
     // warp decoder: no scan, no look-back
     const int NW = K4W_THREADS / 32;
     const size_t smem = (size_t)NW * 32 * (sw16 ? 65 : 129) * 4;  // ROUND = 128 rows (+1 pad word)
@@ -734,7 +790,7 @@ int actc_build_chunk_index(actc_ctx *c, const actc_stream_t *S, uint64_t *chunk_
   CK(cudaMemsetAsync(misc + M_STATUS, 0, 8, s));
   {
     KT(ACTC_KIND_LUT);
-    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S->canon_syms_dev, S->len_counts_dev, (uint32_t *)c->lut.p);
+    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S->canon_syms_dev, S->len_counts_dev, (uint32_t *)c->lut.p, 0);
   }
   CKL();
   const int tpb = 128;

@@ -17,23 +17,26 @@
 // leaf runs and internal runs lighter than 2m (merge path), scans their
 // counts into merge positions, and each merged run emits <= 2 new runs (a
 // pair straddling the previous run, then its inner pairs); an odd leftover
-// pairs with the lightest remaining item ("carry").  The activation
-// alphabets of the bench have 0.5-5 K classes for 12-64 K live symbols.
+// pairs with the lightest remaining item ("carry").  Phases of <= 32 runs
+// run on one warp without block barriers.  The activation alphabets of the
+// bench have 0.5-5 K classes for 12-64 K live symbols.
 //
 // Depths need no tree walk: depth is non-increasing in creation order
 // (internals) and in sorted order (leaves), so with B_0 = root and
 // B_d = min{ j : pos(j) >= 2 B_{d-1} } (pos = merge position), the nodes of
 // depth <= d are exactly those popped at positions >= 2 B_{d-1}.  One
 // search per level over the run arrays gives the level boundaries; a
-// frequency class then has one depth, or (if a boundary cuts it) the first
+// frequency class then has one depth, or (if a boundary cuts it) its first
 // t symbols in symbol order are one level deeper.
 //
-// Symbol passes (warp per contiguous symbol range): class id per symbol ->
-// code length -> canonical rank by (length, symbol) via per-warp counters.
+// Symbol passes: thread t owns a contiguous symbol segment; per-thread
+// length counters + column prefix sums give the canonical rank by (length,
+// symbol) without warp voting.
 //
 // Limits of this fast path (else the host-launched k2_codebook runs: the
-// kernel leaves *fallback = 1): alphabet <= 65536, n < 2^32, <= kRCap
-// classes, <= kICap internal runs, <= kBigCap symbols with freq >= 2^18.
+// kernel leaves *fallback = 1): alphabet <= 65536, sum of freqs < 2^32,
+// <= kRCap classes, <= kICap internal runs, <= kBigCap symbols with freq >=
+// 2^18, <= 32 distinct code lengths, <= 8 cut classes.
 #include "kernels.cuh"
 
 namespace actc {
@@ -50,12 +53,17 @@ constexpr uint32_t kHT = 0x80000000u;     // head-taken flag on a run's position
 constexpr int kMaxLv = 64;
 constexpr int kMaxSide = 96;
 constexpr uint32_t kInf32 = 0xFFFFFFFFu;
+constexpr uint32_t kHot = 64;             // classes counted in per-warp counters
+constexpr int kNL = 32;                   // max distinct code lengths (symbol passes)
+constexpr int kTS = kNL + 2;              // per-thread length-counter stride (odd word count)
+constexpr int kNS = 8;                    // max cut classes
+constexpr int kSS = kNS + 2;              // per-thread cut-class counter stride
 
 struct Side {
   uint32_t run, pos, leaf;
 };
 
-// first k in [0, nr) with pred(k) (monotone), warp-cooperative 32-ary search
+// first k in [0, nr) with pred(k) (pred monotone), warp-cooperative 32-ary search
 template <typename Pred>
 __device__ __forceinline__ uint32_t warp_first(uint32_t nr, Pred pred) {
   const int lane = threadIdx.x & 31;
@@ -92,6 +100,68 @@ __device__ void prefix_inplace(uint32_t *v, uint32_t n, uint32_t *wb) {
   __syncthreads();
 }
 
+// phase scan element: item count c and the number of runs emitted when the
+// segment starts at an even (e0) or odd (e1) merge position
+struct PhS {
+  uint32_t c, e0, e1;
+};
+__device__ __forceinline__ PhS ph_combine(PhS a, PhS b) {
+  const bool odd = a.c & 1u;
+  return PhS{a.c + b.c, a.e0 + (odd ? b.e1 : b.e0), a.e1 + (odd ? b.e0 : b.e1)};
+}
+__device__ __forceinline__ PhS ph_shfl_up(PhS v, int o) {
+  return PhS{__shfl_up_sync(0xffffffffu, v.c, o), __shfl_up_sync(0xffffffffu, v.e0, o),
+             __shfl_up_sync(0xffffffffu, v.e1, o)};
+}
+// block exclusive scan of PhS; *tot = block total
+__device__ PhS ph_block_excl(PhS v, PhS *wb, PhS *tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  PhS inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const PhS t = ph_shfl_up(inc, o);
+    if (lane >= o) inc = ph_combine(t, inc);
+  }
+  if (lane == 31) wb[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const PhS x = wb[lane];
+    PhS xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const PhS t = ph_shfl_up(xi, o);
+      if (lane >= o) xi = ph_combine(t, xi);
+    }
+    PhS xe = ph_shfl_up(xi, 1);
+    if (lane == 0) xe = PhS{0, 0, 0};
+    wb[lane] = xe;
+    if (lane == 31) wb[32] = xi;
+  }
+  __syncthreads();
+  PhS le = ph_shfl_up(inc, 1);
+  if (lane == 0) le = PhS{0, 0, 0};
+  const PhS r = ph_combine(wb[w], le);
+  *tot = wb[32];
+  __syncthreads();
+  return r;
+}
+
+// exclusive prefix down the rows (threads) of one column of a per-thread u16
+// table, plus a column base; one warp per column, 32 rows per round
+__device__ void column_prefix(uint16_t *tab, uint32_t stride, uint32_t ncol, const uint32_t *colbase) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t col = warp; col < ncol; col += NW) {
+    uint32_t run = colbase ? colbase[col] : 0u;
+    for (int r0 = 0; r0 < NT; r0 += 32) {
+      uint16_t *p = tab + (r0 + lane) * stride + col;
+      const uint32_t v = *p;
+      const uint32_t inc = warp_incl_sum(v);
+      *p = (uint16_t)(run + inc - v);
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
@@ -100,13 +170,16 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   uint32_t *LW = sm, *LC = LW + (kRCap + 1), *LM = LC + (kRCap + 1);
   uint32_t *IW = LM + (kRCap + 1), *IC = IW + (kICap + 1), *IM = IC + (kICap + 1);
   // class-building scratch aliases the internal-run region (dead until the phases)
-  uint32_t *bm = IW, *bpre = bm + kBMW, *BL = bpre + kBMW, *SB = BL + kBigCap;
-  // symbol-pass counters alias it again after the depth stage
-  uint32_t *cntA = IW, *cntL = IW + NW * 64;
+  uint32_t *bm = IW, *bpre = bm + kBMW, *BL = bpre + kBMW, *SB = BL + kBigCap, *wcnt = SB + kBigCap;
+  // symbol-pass tables alias LC.. after the per-class stage
+  uint16_t *cntT = reinterpret_cast<uint16_t *>(LC);  // [NT][kTS] length counters
+  uint16_t *cntS = cntT + NT * kTS;                      // [NT][kSS] cut-class counters
+  uint8_t *t_first = reinterpret_cast<uint8_t *>(cntS + NT * kSS), *t_last = t_first + NT;
 
-  __shared__ uint32_t s_wb[NW + 1], s_wb2[NW + 1];
+  __shared__ uint32_t s_wb[NW + 1];
   __shared__ unsigned long long s_wbl[NW + 1];
   __shared__ double s_wbd[NW + 1];
+  __shared__ PhS s_wbp[NW + 1];
   __shared__ uint32_t s_lastw_t[NT];
   __shared__ unsigned s_fail, s_err;
   __shared__ uint32_t s_L, s_lo, s_hi, s_nbig, s_lastw;
@@ -118,16 +191,19 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   __shared__ uint32_t s_lencnt[64], s_base[64];
   __shared__ unsigned long long s_first[64];
   __shared__ uint32_t sc_s0[64], sc_da[64], sc_db[64], sc_dl[64], s_nsc;
-  __shared__ uint32_t w_first[NW], w_last[NW], w_starts[NW], w_has[NW];
+  __shared__ uint32_t s_starts, s_minlen, s_maxlen;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = (1u << lane) - 1u;
   const uint32_t A = (uint32_t)a.A;
 #define K2R_STAMP(i) \
   if (a.dbg && tid == 0) a.dbg[i] = clock64();
   K2R_STAMP(0)
-
+  // the plan's K1 counters: loaded early, used at the very end
+  unsigned long long n_out = 0;
+  unsigned nonfin = 0;
   if (tid == 0) {
+    if (a.n_outliers) n_out = *a.n_outliers;
+    if (a.nonfinite) nonfin = *a.nonfinite;
     s_fail = 0;
     s_err = 0;
     s_L = 0;
@@ -138,12 +214,14 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     s_nside = 0;
     s_nsc = 0;
     s_nlv = 0;
+    s_starts = 0;
   }
   if (tid < 64) s_lencnt[tid] = 0;
   for (uint32_t i = tid; i < kBMW; i += NT) bm[i] = 0;
+  for (uint32_t i = tid; i < NW * kHot; i += NT) wcnt[i] = 0;
   __syncthreads();
 
-  // ---- S1: live range, frequency bitmap, heavy frequencies ----
+  // ---- S1: live range, frequency bitmap, heavy frequencies (warp-strided) ----
   {
     const uint32_t WS = (((A + NW - 1) / NW) + 31) & ~31u;
     const uint32_t w0 = min(A, warp * WS), w1 = min(A, w0 + WS);
@@ -167,7 +245,8 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
           mylo = min(mylo, s);
           myhi = max(myhi, s);
           if (f < kFT) {
-            atomicOr(&bm[f >> 5], 1u << (f & 31));
+            const uint32_t bit = 1u << (f & 31);
+            if (!(bm[f >> 5] & bit)) atomicOr(&bm[f >> 5], bit);
           } else {
             const uint32_t p = atomicAdd(&s_nbig, 1u);
             if (p < kBigCap) BL[p] = f;
@@ -242,47 +321,124 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   __syncthreads();
   K2R_STAMP(1)
 
-  // ---- S2: class id per live symbol, class sizes and weights ----
-  const uint32_t span = hi - lo + 1;
-  const uint32_t WS2 = (((span + NW - 1) / NW) + 31) & ~31u;
-  const uint32_t v0 = min(hi + 1, lo + warp * WS2), v1 = min(hi + 1, v0 + WS2);
-  for (uint32_t base = v0; base < v1; base += 256) {
-    unsigned long long v[8];
+  // symbol-pass geometry: thread t owns [p0 + t*SEG, p0 + (t+1)*SEG), SEG % 16 == 0
+  const uint32_t p0 = lo & ~15u;
+  const uint32_t SEG = ((((hi + 1 - p0) + NT - 1) / NT) + 15) & ~15u;
+
+  // ---- S2: class id per live symbol, class sizes and weights (warp-strided) ----
+  {
+    const uint32_t span = hi + 1 - p0;
+    const uint32_t WS2 = (((span + NW - 1) / NW) + 31) & ~31u;
+    const uint32_t v0 = min(hi + 1, p0 + warp * WS2), v1 = min(hi + 1, v0 + WS2);
+    for (uint32_t base = v0; base < v1; base += 256) {
+      unsigned long long v[8];
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t s = base + 32 * u + lane;
-      v[u] = s < v1 ? a.hist[s] : 0ull;
-    }
+      for (int u = 0; u < 8; u++) {
+        const uint32_t s = base + 32 * u + lane;
+        v[u] = s < v1 ? a.hist[s] : 0ull;
+      }
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const uint32_t s = base + 32 * u + lane;
-      const uint32_t f = (uint32_t)v[u];
-      uint32_t k = kInf32;
-      if (f) {
-        if (f < kFT) {
-          const uint32_t wd = f >> 5;
-          k = bpre[wd] + __popc(bm[wd] & ((1u << (f & 31)) - 1u));
-        } else {
-          uint32_t l2 = 0, h2 = nu;
-          while (l2 < h2) {
-            const uint32_t m = (l2 + h2) >> 1;
-            if (BL[m] < f) l2 = m + 1; else h2 = m;
+      for (int u = 0; u < 8; u++) {
+        const uint32_t s = base + 32 * u + lane;
+        const uint32_t f = (uint32_t)v[u];
+        uint32_t k = kInf32;
+        if (f) {
+          if (f < kFT) {
+            const uint32_t wd = f >> 5;
+            k = bpre[wd] + __popc(bm[wd] & ((1u << (f & 31)) - 1u));
+          } else {
+            uint32_t l2 = 0, h2 = nu;
+            while (l2 < h2) {
+              const uint32_t m = (l2 + h2) >> 1;
+              if (BL[m] < f) l2 = m + 1; else h2 = m;
+            }
+            k = Rs + l2;
           }
-          k = Rs + l2;
         }
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        if (f && lane == __ffs(peers) - 1) {
+          if (k < kHot)
+            wcnt[warp * kHot + k] += __popc(peers);  // warp-private: the lightest classes are the hot ones
+          else
+            atomicAdd(&LC[k], (uint32_t)__popc(peers));
+          LW[k] = f;
+        }
+        if (s < v1) a.cls16[s] = f ? (uint16_t)k : (uint16_t)0xFFFF;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, k);
-      if (f && lane == __ffs(peers) - 1) {
-        atomicAdd(&LC[k], (uint32_t)__popc(peers));
-        LW[k] = f;
-      }
-      if (s < v1) a.cls16[s] = f ? (uint16_t)k : (uint16_t)0xFFFF;
     }
   }
   __syncthreads();
+  if (tid < (int)min(kHot, R)) {
+    uint32_t c = LC[tid];
+    for (int w = 0; w < NW; w++) c += wcnt[w * kHot + tid];
+    LC[tid] = c;
+  }
   K2R_STAMP(2)
 
   // ---- phases over runs ----
+  const uint32_t target = 2 * (L - 1);
+  // range of the upcoming phase (warp 0): runs lighter than twice the lightest item
+  auto next_range = [&]() {
+    const uint32_t li = s_li, ii = s_ii, ni = s_ni;
+    const unsigned long long wl = li < R ? LW[li] : ~0ull, wi = ii < ni ? IW[ii] : ~0ull;
+    const unsigned long long lim = 2ull * min(wl, wi);
+    const uint32_t le = li + warp_first(R - li, [&](uint32_t k) { return (unsigned long long)LW[li + k] >= lim; });
+    const uint32_t ie = ii + warp_first(ni - ii, [&](uint32_t k) { return (unsigned long long)IW[ii + k] >= lim; });
+    if (lane == 0) {
+      s_le = le;
+      s_ie = ie;
+      if (++s_nph > 96) s_fail = 1;
+    }
+    __syncwarp();
+  };
+  // odd leftover (weight s_lastw) pairs with the lightest remaining item
+  // (leaf on ties); one thread, then the state advances
+  auto finish_phase = [&](uint32_t P, uint32_t C, uint32_t E) {
+    const uint32_t li = s_li, lh = s_lh, ii = s_ii, ih = s_ih, ni = s_ni, le = s_le, ie = s_ie;
+    uint32_t Pn = P + C, nli = le, nlh = le == li ? lh : 0u, nii = ie, nih = ie == ii ? ih : 0u, nni = ni + E;
+    if (C & 1u) {
+      const unsigned long long wl = le < R ? LW[le] : ~0ull;
+      const uint32_t icand = ie < ni ? ie : ni;
+      const unsigned long long wi = icand < nni ? IW[icand] : ~0ull;
+      uint32_t wp;
+      const uint32_t ns = s_nside;
+      if (ns >= kMaxSide) s_fail = 1;
+      if (wl <= wi) {
+        wp = LW[le];
+        if (ns < kMaxSide) s_side[ns] = Side{le, Pn, 1u};
+        if (LC[le] == 1u) {
+          LM[le] = Pn | kHT;
+          nli = le + 1;
+          nlh = 0;
+        } else {
+          nli = le;
+          nlh = 1;
+        }
+      } else {
+        wp = IW[icand];
+        if (ns < kMaxSide) s_side[ns] = Side{icand, Pn, 0u};
+        if (IC[icand] == 1u) {
+          IM[icand] = Pn | kHT;
+          nii = icand + 1;
+          nih = 0;
+        } else {
+          nii = icand;
+          nih = 1;
+        }
+      }
+      s_nside = ns + 1;
+      IW[nni] = s_lastw + wp;
+      IC[nni] = 1;
+      nni++;
+      Pn++;
+    }
+    s_li = nli;
+    s_lh = nlh;
+    s_ii = nii;
+    s_ih = nih;
+    s_ni = nni;
+    s_P = Pn;
+  };
   if (tid == 0) {
     s_li = 0;
     s_lh = 0;
@@ -293,32 +449,84 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     s_nph = 0;
   }
   __syncthreads();
-  const uint32_t target = 2 * (L - 1);
+  if (warp == 0 && target > 0) next_range();
+  __syncthreads();
   while (true) {
-    const uint32_t P = s_P;
-    if (P >= target || s_fail) break;
-    if (tid == 0) {
-      const uint32_t li = s_li, ii = s_ii, ni = s_ni;
-      const unsigned long long wl = li < R ? LW[li] : ~0ull, wi = ii < ni ? IW[ii] : ~0ull;
-      const unsigned long long lim = 2ull * min(wl, wi);
-      uint32_t l2 = li, h2 = R;
-      while (l2 < h2) {
-        const uint32_t m = (l2 + h2) >> 1;
-        if (LW[m] < lim) l2 = m + 1; else h2 = m;
+    if (s_P >= target || s_fail) break;
+    const uint32_t T0 = (s_le - s_li) + (s_ie - s_ii);
+    if (T0 <= 32) {
+      // ---- one warp runs consecutive small phases (lane = merged run) ----
+      if (warp == 0) {
+        while (true) {
+          const uint32_t P = s_P, li = s_li, lh = s_lh, ii = s_ii, ih = s_ih, ni = s_ni, le = s_le, ie = s_ie;
+          const uint32_t nL = le - li, nI = ie - ii, T = nL + nI;
+          uint32_t w = 0, c = 0, run = 0;
+          bool tl = false;
+          if ((uint32_t)lane < T) {
+            const uint32_t j = lane;
+            uint32_t l2 = j > nI ? j - nI : 0, h2 = min(j, nL);
+            while (l2 < h2) {
+              const uint32_t m = (l2 + h2) >> 1;
+              if (LW[li + m] <= IW[ii + j - 1 - m]) l2 = m + 1; else h2 = m;
+            }
+            const uint32_t ax = l2, bx = j - l2;
+            tl = ax < nL && (bx >= nI || LW[li + ax] <= IW[ii + bx]);
+            if (tl) {
+              run = li + ax;
+              w = LW[run];
+              c = LC[run] - (ax == 0 ? lh : 0u);
+            } else {
+              run = ii + bx;
+              w = IW[run];
+              c = IC[run] - (bx == 0 ? ih : 0u);
+            }
+          }
+          const uint32_t cin = warp_incl_sum(c);
+          const uint32_t C = __shfl_sync(0xffffffffu, cin, 31);
+          const uint32_t p = P + cin - c;
+          const uint32_t bnd = ((uint32_t)lane < T) ? (p & 1u) : 0u;
+          const uint32_t rem = c - bnd;
+          const uint32_t nbk = ((uint32_t)lane < T && rem >= 2u) ? 1u : 0u;
+          const uint32_t e = bnd + nbk;
+          const uint32_t ein = warp_incl_sum(e);
+          const uint32_t E = __shfl_sync(0xffffffffu, ein, 31);
+          if (ni + E + 1 > kICap) {
+            if (lane == 0) s_fail = 1;
+            __syncwarp();
+            break;
+          }
+          const uint32_t prevw = __shfl_up_sync(0xffffffffu, w, 1);
+          const uint32_t lastw = __shfl_sync(0xffffffffu, w, (T - 1) & 31);
+          if ((uint32_t)lane < T) {
+            if (tl) LM[run] = p | ((run == li && lh) ? kHT : 0u);
+            else IM[run] = p | ((run == ii && ih) ? kHT : 0u);
+            uint32_t o = ni + ein - e;
+            if (bnd) {
+              IW[o] = prevw + w;
+              IC[o] = 1;
+              o++;
+            }
+            if (nbk) {
+              IW[o] = 2u * w;
+              IC[o] = rem >> 1;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            s_lastw = lastw;
+            finish_phase(P, C, E);
+          }
+          __syncwarp();
+          if (s_P >= target || s_fail) break;
+          next_range();
+          if ((s_le - s_li) + (s_ie - s_ii) > 32) break;
+        }
       }
-      s_le = l2;
-      l2 = ii;
-      h2 = ni;
-      while (l2 < h2) {
-        const uint32_t m = (l2 + h2) >> 1;
-        if (IW[m] < lim) l2 = m + 1; else h2 = m;
-      }
-      s_ie = l2;
-      if (++s_nph > 96) s_fail = 1;
+      __syncthreads();
+      continue;
     }
-    __syncthreads();
-    if (s_fail) break;
-    const uint32_t li = s_li, lh = s_lh, ii = s_ii, ih = s_ih, ni = s_ni, le = s_le, ie = s_ie;
+    // ---- block phase: thread t owns merged runs [j0, j1) ----
+    const uint32_t P = s_P, li = s_li, lh = s_lh, ii = s_ii, ih = s_ih, ni = s_ni, le = s_le, ie = s_ie;
     const uint32_t nL = le - li, nI = ie - ii, T = nL + nI;
     const uint32_t K = (T + NT - 1) / NT;
     const uint32_t j0 = min(T, tid * K), j1 = min(T, j0 + K);
@@ -341,24 +549,35 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     w = IW[ii + bx];                                                    \
     c = IC[ii + bx] - (bx == 0 ? ih : 0u);                              \
   }
-    uint32_t sumc = 0, lastw = 0;
+    PhS loc{0, 0, 0};
+    uint32_t lastw = 0;
     {
-      uint32_t ax = a0, bx = j0 - a0;
+      uint32_t ax = a0, bx = j0 - a0, q0 = 0, q1 = 1;
       for (uint32_t j = j0; j < j1; j++) {
         K2R_NEXT
         if (tl) ax++; else bx++;
-        sumc += c;
+        const uint32_t b0 = q0 & 1u, b1 = q1 & 1u;
+        loc.e0 += b0 + ((c - b0) >= 2u);
+        loc.e1 += b1 + ((c - b1) >= 2u);
+        q0 += c;
+        q1 += c;
+        loc.c += c;
         lastw = w;
       }
     }
     s_lastw_t[tid] = lastw;
     if (j0 < j1 && j1 == T) s_lastw = lastw;
-    uint32_t C;
-    const uint32_t cex = block_excl_sum<uint32_t>(sumc, s_wb, &C);
-    const uint32_t pw0 = (tid > 0 && j0 < j1) ? s_lastw_t[tid - 1] : 0u;
-    uint32_t e = 0;
+    PhS tot;
+    const PhS ex = ph_block_excl(loc, s_wbp, &tot);
+    const uint32_t C = tot.c, E = tot.e0;
+    if (ni + E + 1 > kICap) {
+      if (tid == 0) s_fail = 1;
+      __syncthreads();
+      break;
+    }
     {
-      uint32_t ax = a0, bx = j0 - a0, p = P + cex;
+      uint32_t ax = a0, bx = j0 - a0, p = P + ex.c, o = ni + ex.e0;
+      uint32_t prevw = (tid > 0 && j0 < j1) ? s_lastw_t[tid - 1] : 0u;
       for (uint32_t j = j0; j < j1; j++) {
         K2R_NEXT
         if (tl) {
@@ -368,23 +587,6 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
           IM[ii + bx] = p | ((bx == 0 && ih) ? kHT : 0u);
           bx++;
         }
-        const uint32_t bnd = p & 1u;
-        e += bnd + ((c - bnd) >= 2u);
-        p += c;
-      }
-    }
-    uint32_t E;
-    const uint32_t eex = block_excl_sum<uint32_t>(e, s_wb2, &E);
-    if (ni + E + 1 > kICap) {
-      if (tid == 0) s_fail = 1;
-      __syncthreads();
-      break;
-    }
-    {
-      uint32_t ax = a0, bx = j0 - a0, p = P + cex, o = ni + eex, prevw = pw0;
-      for (uint32_t j = j0; j < j1; j++) {
-        K2R_NEXT
-        if (tl) ax++; else bx++;
         const uint32_t bnd = p & 1u;
         if (bnd) {
           IW[o] = prevw + w;
@@ -403,51 +605,10 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     }
 #undef K2R_NEXT
     __syncthreads();
-    if (tid == 0) {
-      uint32_t Pn = P + C, nli = le, nlh = le == li ? lh : 0u, nii = ie, nih = ie == ii ? ih : 0u, nni = ni + E;
-      if (C & 1u) {
-        // the odd leftover pairs with the lightest remaining item (leaf on ties)
-        const unsigned long long wl = le < R ? LW[le] : ~0ull;
-        const uint32_t icand = ie < ni ? ie : ni;
-        const unsigned long long wi = icand < nni ? IW[icand] : ~0ull;
-        uint32_t wp;
-        const uint32_t ns = s_nside;
-        if (ns >= kMaxSide) s_fail = 1;
-        if (wl <= wi) {
-          wp = LW[le];
-          if (ns < kMaxSide) s_side[ns] = Side{le, Pn, 1u};
-          if (LC[le] == 1u) {
-            LM[le] = Pn | kHT;
-            nli = le + 1;
-            nlh = 0;
-          } else {
-            nli = le;
-            nlh = 1;
-          }
-        } else {
-          wp = IW[icand];
-          if (ns < kMaxSide) s_side[ns] = Side{icand, Pn, 0u};
-          if (IC[icand] == 1u) {
-            IM[icand] = Pn | kHT;
-            nii = icand + 1;
-            nih = 0;
-          } else {
-            nii = icand;
-            nih = 1;
-          }
-        }
-        s_nside = ns + 1;
-        IW[nni] = s_lastw + wp;
-        IC[nni] = 1;
-        nni++;
-        Pn++;
-      }
-      s_li = nli;
-      s_lh = nlh;
-      s_ii = nii;
-      s_ih = nih;
-      s_ni = nni;
-      s_P = Pn;
+    if (warp == 0) {
+      if (lane == 0) finish_phase(P, C, E);
+      __syncwarp();
+      if (s_P < target && !s_fail) next_range();
     }
     __syncthreads();
   }
@@ -461,8 +622,7 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   const uint32_t ni = s_ni, nside = s_nside;
   prefix_inplace(LC, R, s_wb);  // LC -> first sorted-leaf index of each class (LC[R] = L)
   if (L >= 2) prefix_inplace(IC, ni, s_wb);  // IC -> first internal index of each run
-  // position of the first / last item of a run; head-taken runs keep their
-  // first item's position in the side table
+  // position of a head-taken run's first item (side table)
   auto first_pos = [&](const uint32_t *M, const uint32_t *S, uint32_t k, uint32_t leaf) -> uint32_t {
     const uint32_t m = M[k];
     if (!(m & kHT)) return m;
@@ -511,55 +671,62 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   __syncthreads();
   K2R_STAMP(4)
 
-  // ---- per class: depth, split points, bits, entropy, length counts ----
+  // ---- per class: depth, cut points, bits, entropy, length counts ----
   unsigned long long bits = 0;
   double ent = 0.0;
   const double total = (double)a.n_symbols;
-  for (uint32_t k = tid; k < R; k += NT) {
-    const uint32_t s0 = LC[k], s1 = LC[k + 1], cnt = s1 - s0, f = LW[k];
-    // depth(i) = 1 + #{levels with LB > i}; LB decreasing over levels
-    auto depth_of = [&](uint32_t i) -> uint32_t {
-      uint32_t l2 = 0, h2 = nlv;
-      while (l2 < h2) {
-        const uint32_t m = (l2 + h2) >> 1;
-        if (s_LB[m] > i) l2 = m + 1; else h2 = m;
+  for (uint32_t k0 = 0; k0 < R; k0 += NT) {
+    const uint32_t k = k0 + tid;
+    uint32_t dl = 0xFFu, cnt = 0;
+    if (k < R) {
+      const uint32_t s0 = LC[k], s1 = LC[k + 1], f = LW[k];
+      cnt = s1 - s0;
+      // depth(i) = 1 + #{levels with LB > i}; LB non-increasing over levels
+      auto depth_of = [&](uint32_t i) -> uint32_t {
+        uint32_t l2 = 0, h2 = nlv;
+        while (l2 < h2) {
+          const uint32_t m = (l2 + h2) >> 1;
+          if (s_LB[m] > i) l2 = m + 1; else h2 = m;
+        }
+        return 1u + l2;
+      };
+      dl = depth_of(s1 - 1);
+      const uint32_t df = depth_of(s0);
+      uint32_t ci = dl;
+      unsigned long long sumt = 0;
+      if (df != dl) {
+        // level indices x in [dl-1, df-1) have s0 < LB[x] <= s1-1: they cut the
+        // class at rank t = LB[x] - s0 (t decreasing in x); ranks [t, prev)
+        // are j levels deeper than the class's last symbol
+        const uint32_t da = dl - 1, db = df - 1;
+        const uint32_t sc = atomicAdd(&s_nsc, 1u);
+        if (sc < 64) {
+          sc_s0[sc] = s0;
+          sc_da[sc] = da;
+          sc_db[sc] = db;
+          sc_dl[sc] = dl;
+        }
+        ci = dl | 0x100u | (min(sc, 63u) << 9);
+        uint32_t prev = cnt, j = 0;
+        for (uint32_t x = da; x < db; x++) {
+          const uint32_t t = s_LB[x] - s0;
+          sumt += t;
+          atomicAdd(&s_lencnt[min(63u, dl + j)], prev - t);
+          prev = t;
+          j++;
+        }
+        atomicAdd(&s_lencnt[min(63u, dl + j)], prev);
+        dl = 0xFFu;  // counted above
       }
-      return 1u + l2;
-    };
-    const uint32_t dl = depth_of(s1 - 1), df = depth_of(s0);
-    uint32_t ci = dl;
-    unsigned long long sumt = 0;
-    if (df != dl) {
-      // level indices x in [dl-1, df-1) have s0 < LB[x] <= s1-1: they cut the
-      // class at rank t = LB[x] - s0 (t decreasing in x)
-      const uint32_t da = dl - 1, db = df - 1;
-      const uint32_t sc = atomicAdd(&s_nsc, 1u);
-      if (sc < 64) {
-        sc_s0[sc] = s0;
-        sc_da[sc] = da;
-        sc_db[sc] = db;
-        sc_dl[sc] = dl;
-      } else {
-        atomicOr(&s_err, 2u);
-      }
-      ci = dl | 0x100u | (sc << 9);
-      // ranks [t, prev) are j levels deeper than the class's last symbol
-      uint32_t prev = cnt, j = 0;
-      for (uint32_t x = da; x < db; x++) {
-        const uint32_t t = s_LB[x] - s0;
-        sumt += t;
-        atomicAdd(&s_lencnt[min(63u, dl + j)], prev - t);
-        prev = t;
-        j++;
-      }
-      atomicAdd(&s_lencnt[min(63u, dl + j)], prev);
-    } else {
-      atomicAdd(&s_lencnt[min(63u, dl)], cnt);
+      bits += (unsigned long long)f * ((unsigned long long)cnt * (ci & 0xFFu) + sumt);
+      const double p = (double)f / total;
+      ent += (double)cnt * (p * log2(p));
+      LW[k] = ci;
     }
-    bits += (unsigned long long)f * ((unsigned long long)cnt * dl + sumt);
-    const double p = (double)f / total;
-    ent += (double)cnt * (p * log2(p));
-    LW[k] = ci;
+    // uncut classes: one atomic per distinct length per warp
+    const unsigned pk = __match_any_sync(0xffffffffu, dl);
+    const uint32_t sumc = __reduce_add_sync(pk, cnt);
+    if (dl != 0xFFu && lane == __ffs(pk) - 1) atomicAdd(&s_lencnt[min(63u, dl)], sumc);
   }
   unsigned long long tb;
   block_excl_sum<unsigned long long>(bits, s_wbl, &tb);
@@ -567,133 +734,135 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   block_excl_sum<double>(ent, s_wbd, &te);
   if (tid == 0) {
     unsigned long long code = 0;
-    uint32_t idx = 0, mx = 0;
+    uint32_t idx = 0, mx = 0, mn = 64;
     for (int l = 0; l < 64; l++) {
       code <<= 1;
       s_first[l] = code;
       s_base[l] = idx;
       code += s_lencnt[l];
       idx += s_lencnt[l];
-      if (s_lencnt[l]) mx = l;
+      if (s_lencnt[l]) {
+        mx = l;
+        mn = min(mn, (uint32_t)l);
+      }
     }
-    s_lencnt[0] = mx;  // stash: max length (length 0 never counted)
+    s_minlen = mn;
+    s_maxlen = mx;
+    if (mx + 1 - mn > (uint32_t)kNL || s_nsc > (uint32_t)kNS) s_fail = 1;
   }
-  for (uint32_t i = tid; i < 2 * NW * 64; i += NT) cntA[i] = 0;
   __syncthreads();
-  const uint32_t maxlen = s_lencnt[0], nsc = min(64u, s_nsc);
+  if (s_fail) {
+    if (tid == 0) *a.fallback = 1u;
+    return;
+  }
+  const uint32_t minlen = s_minlen, maxlen = s_maxlen, nsc = s_nsc;
+  {
+    // per-thread counters (LC.. is dead now)
+    uint32_t *z = reinterpret_cast<uint32_t *>(cntT);
+    const uint32_t words = (NT * kTS + NT * kSS) / 2;
+    for (uint32_t i = tid; i < words; i += NT) z[i] = 0;
+  }
+  __syncthreads();
   K2R_STAMP(5)
 
-  // ---- symbol passes over the live range, warp w owns [v0, v1) ----
+  // ---- symbol passes: thread t owns [q0, q0 + SEG) ----
+  const uint32_t q0 = p0 + tid * SEG;
+  const uint32_t q1 = min(hi + 1, q0 + SEG);  // live-range part of my segment
+  uint16_t *myT = cntT + tid * kTS;
+  uint16_t *myS = cntS + tid * kSS;
   if (nsc) {
-    for (uint32_t base = v0; base < v1; base += 32) {
-      const uint32_t s = base + lane;
-      const uint32_t k = s < v1 ? a.cls16[s] : 0xFFFFu;
-      uint32_t sc = 0xFFu;
-      if (k != 0xFFFFu) {
-        const uint32_t ci = LW[k];
-        if (ci & 0x100u) sc = ci >> 9;
+    // pass A: cut-class membership counts
+    for (uint32_t c0 = q0; c0 < q1; c0 += 8) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(a.cls16 + c0);
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t s = c0 + u;
+        const uint32_t k = (wv[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+        if (s >= lo && s < q1 && k != 0xFFFFu) {
+          const uint32_t ci = LW[k];
+          if (ci & 0x100u) myS[ci >> 9]++;
+        }
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, sc);
-      if (sc != 0xFFu && lane == __ffs(peers) - 1) cntA[warp * 64 + sc] += __popc(peers);
     }
     __syncthreads();
-    if (tid < (int)nsc) {
-      uint32_t run = 0;
-      for (int w = 0; w < NW; w++) {
-        const uint32_t t = cntA[w * 64 + tid];
-        cntA[w * 64 + tid] = run;
-        run += t;
-      }
-    }
+    column_prefix(cntS, kSS, nsc, nullptr);
     __syncthreads();
   }
-  // pass B: code lengths, per-warp length counts, RLE run starts
+  // pass B: lengths (len8 written 16 at a time), per-thread length counts, run starts
   {
-    uint32_t prevlen = 0, starts = 0, firstlen = 0;
-    bool first = true;
-    for (uint32_t base = v0; base < v1; base += 32) {
-      const uint32_t s = base + lane;
-      const bool in = s < v1;
-      const uint32_t k = in ? a.cls16[s] : 0xFFFFu;
-      uint32_t len = 0, sc = 0xFFu;
-      if (k != 0xFFFFu) {
-        const uint32_t ci = LW[k];
-        len = ci & 0xFFu;
-        if (ci & 0x100u) sc = ci >> 9;
+    uint32_t prevlen = 0, starts = 0;
+    for (uint32_t c0 = q0; c0 < q1; c0 += 16) {
+      const uint4 va = *reinterpret_cast<const uint4 *>(a.cls16 + c0);
+      const uint4 vb = *reinterpret_cast<const uint4 *>(a.cls16 + c0 + 8);
+      const uint32_t wv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+      uint32_t out[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 16; u++) {
+        const uint32_t s = c0 + u;
+        const uint32_t k = (wv[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+        uint32_t len = 0;
+        if (s >= lo && s < q1 && k != 0xFFFFu) {
+          const uint32_t ci = LW[k];
+          len = ci & 0xFFu;
+          if (ci & 0x100u) {
+            const uint32_t sc = ci >> 9;
+            const uint32_t r = myS[sc];
+            myS[sc] = (uint16_t)(r + 1);
+            uint32_t extra = 0;
+            for (uint32_t x = sc_da[sc]; x < sc_db[sc]; x++) extra += (s_LB[x] - sc_s0[sc]) > r;
+            len += extra;
+          }
+          myT[len - minlen]++;
+        }
+        out[u >> 2] |= len << (8 * (u & 3));
+        if (s < q1) {
+          if (s == q0) t_first[tid] = (uint8_t)len;
+          else if (s > lo && len != prevlen) starts++;
+          prevlen = len;
+        }
       }
-      const unsigned ps = __match_any_sync(0xffffffffu, sc);
-      if (sc != 0xFFu) {
-        const uint32_t r = cntA[warp * 64 + sc] + __popc(ps & lt);
-        // depth = dl + #{cut levels x in [da, db) with t = LB[x] - s0 > r}
-        uint32_t extra = 0;
-        for (uint32_t x = sc_da[sc]; x < sc_db[sc]; x++) extra += (s_LB[x] - sc_s0[sc]) > r;
-        len = sc_dl[sc] + extra;
+      *reinterpret_cast<uint4 *>(a.len8 + c0) = make_uint4(out[0], out[1], out[2], out[3]);
+      if (a.out_lengths) {
+        for (int u = 0; u < 16; u++) {
+          const uint32_t s = c0 + u;
+          if (s >= lo && s < q1) a.out_lengths[s] = (uint16_t)((out[u >> 2] >> (8 * (u & 3))) & 0xFFu);
+        }
       }
-      __syncwarp();
-      if (sc != 0xFFu && lane == __ffs(ps) - 1) cntA[warp * 64 + sc] += __popc(ps);
-      len = min(len, 63u);
-      if (k != 0xFFFFu) {
-        a.len8[s] = (uint8_t)len;
-        if (a.out_lengths) a.out_lengths[s] = (uint16_t)len;
-      }
-      const unsigned pl = __match_any_sync(0xffffffffu, in ? len : 0xFFu);
-      if (in && len && lane == __ffs(pl) - 1) cntL[warp * 64 + len] += __popc(pl);
-      // run starts inside this warp's range (its first symbol is judged later)
-      uint32_t up = __shfl_up_sync(0xffffffffu, len, 1);
-      if (lane == 0) up = prevlen;
-      const bool st = in && !(first && lane == 0) && len != up;
-      starts += __popc(__ballot_sync(0xffffffffu, st));
-      if (first) firstlen = __shfl_sync(0xffffffffu, len, 0);
-      const uint32_t nin = min(32u, v1 - base);
-      prevlen = __shfl_sync(0xffffffffu, len, nin - 1);
-      first = false;
-      __syncwarp();
     }
-    if (lane == 0) {
-      w_has[warp] = v0 < v1;
-      w_first[warp] = firstlen;
-      w_last[warp] = prevlen;
-      w_starts[warp] = starts;
-    }
+    if (q0 < q1) t_last[tid] = (uint8_t)prevlen;
+    __syncthreads();
+    // a run starts at my first symbol when it differs from the previous thread's last
+    if (q0 < q1 && q0 > lo && tid > 0 && t_first[tid] != t_last[tid - 1]) starts++;
+    starts = warp_sum(starts);
+    if (lane == 0 && starts) atomicAdd(&s_starts, starts);
   }
-  __syncthreads();
-  if (tid < 64) {
-    uint32_t run = s_base[tid];
-    for (int w = 0; w < NW; w++) {
-      const uint32_t t = cntL[w * 64 + tid];
-      cntL[w * 64 + tid] = run;
-      run += t;
-    }
-  }
+  column_prefix(cntT, kTS, maxlen + 1 - minlen, s_base + minlen);
   __syncthreads();
   // pass C: canonical ranks -> canon[], ctab[]
-  for (uint32_t base = v0; base < v1; base += 32) {
-    const uint32_t s = base + lane;
-    const bool live = s < v1 && a.cls16[s] != 0xFFFFu;
-    const uint32_t len = live ? a.len8[s] : 0xFFu;
-    const unsigned pl = __match_any_sync(0xffffffffu, len);
-    if (live) {
-      const uint32_t ci = cntL[warp * 64 + len] + __popc(pl & lt);
-      a.canon[ci] = s;
-      if (a.ctab && len <= 56) a.ctab[s] = ((s_first[len] + (ci - s_base[len])) << 8) | len;
+  for (uint32_t c0 = q0; c0 < q1; c0 += 16) {
+    const uint4 lv = *reinterpret_cast<const uint4 *>(a.len8 + c0);
+    const uint32_t wv[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t s = c0 + u;
+      const uint32_t len = (wv[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+      if (len && s < q1) {
+        const uint32_t ci = myT[len - minlen];
+        myT[len - minlen] = (uint16_t)(ci + 1);
+        a.canon[ci] = s;
+        if (len <= 56) a.ctab[s] = ((s_first[len] + (ci - s_base[len])) << 8) | len;
+      }
     }
-    __syncwarp();
-    if (live && lane == __ffs(pl) - 1) cntL[warp * 64 + len] += __popc(pl);
-    __syncwarp();
   }
-  if (tid < 64) a.len_counts[tid] = tid ? s_lencnt[tid] : 0u;
+  if (tid < 64) a.len_counts[tid] = s_lencnt[tid];
+  __syncthreads();
   K2R_STAMP(6)
   if (tid == 0) {
     // RLE records over the whole alphabet: zero run before lo, runs inside
-    // [lo, hi], zero run after hi; a run longer than 65535 splits
-    uint64_t recs = 1 + (lo > 0) + (hi + 1 < A);
-    int prev = -1;
-    for (int w = 0; w < NW; w++) {
-      if (!w_has[w]) continue;
-      recs += w_starts[w];
-      if (prev >= 0 && w_first[w] != w_last[prev]) recs++;
-      prev = w;
-    }
+    // [lo, hi] (the one starting at lo + later starts), zero run after hi; a
+    // run longer than 65535 splits
+    uint64_t recs = (lo > 0) + 1 + s_starts + (hi + 1 < A);
     if (recs == 1 && A > 65535) recs = (A + 65534) / 65535;
     actc_plan_t *pl = a.plan;
     pl->n = a.n_symbols;
@@ -704,10 +873,10 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     pl->rle_runs = recs;
     pl->entropy_bits = L > 1 ? -te : 0.0;
     if (pl->entropy_bits == 0.0) pl->entropy_bits = 0.0;
-    pl->status = (s_err & 1u) ? ACTC_EPARAM : ((s_err & 2u) ? ACTC_ECUDA : ACTC_OK);
+    pl->status = (s_err & 1u) ? ACTC_EPARAM : ACTC_OK;
     if (maxlen > 56) pl->status = ACTC_EPARAM;
-    if (a.n_outliers) pl->n_outliers = *a.n_outliers;
-    if (a.nonfinite && *a.nonfinite) pl->status = ACTC_EDATA;
+    if (a.n_outliers) pl->n_outliers = n_out;
+    if (a.nonfinite && nonfin) pl->status = ACTC_EDATA;
     pl->sym_lo = lo;
     pl->sym_hi = hi;
     *a.fallback = 0u;

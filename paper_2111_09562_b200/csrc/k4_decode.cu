@@ -91,7 +91,7 @@ __device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint
 // holds the fast-path flag: 1 if the code is prefix-free (Kraft <= 1) and
 // max length <= 32.
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
-                            uint32_t *__restrict__ lut) {
+                            uint32_t *__restrict__ lut, int ci_mode) {
   __shared__ CodeTables t;
   build_tables(t, len_counts);
   __syncthreads();
@@ -116,7 +116,7 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
     unsigned long long code = p >> (kLutBits - l);
     unsigned long long off = code - t.first[l];
     if (off < t.count[l]) {
-      e = (canon[t.base[l] + off] << 6) | (uint32_t)l;
+      e = ((ci_mode ? (uint32_t)(t.base[l] + off) : canon[t.base[l] + off]) << 6) | (uint32_t)l;
       break;
     }
   }

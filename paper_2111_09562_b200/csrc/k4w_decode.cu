@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   __shared__ int32_t s_off[64];                 // base[l] - first[l]
   __shared__ unsigned long long s_first[64];    // for the reference-rule fallback
   __shared__ uint32_t s_count[64], s_base[64];
-  __shared__ uint32_t s_maxlen;
+  __shared__ uint32_t s_maxlen, s_zci;
   extern __shared__ __align__(16) uint32_t wbuf_all[];  // NW4 * 32 rows
   constexpr int ROW = SW == 16 ? ROW16 : ROW32;
 
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
       if (c && l > 0) mx = l;
     }
     s_maxlen = mx;
+    s_zci = 0xFFFFFFFFu;
   }
   const uint32_t ncache = SW == 16 ? min((uint32_t)K4W_CANON_CACHE, a.live) : 0u;
   // canonical-symbol cache: 8 x 16-byte loads in flight per thread
@@ -142,6 +143,11 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     }
   }
   __syncthreads();
+  // canonical index of the outlier marker (symbol 0): the smallest symbol, so
+  // the first of its length in canonical order (only live with outliers)
+  if (a.k && tid < 64 && s_count[tid] && a.canon[s_base[tid]] == 0u) s_zci = s_base[tid];
+  __syncthreads();
+  const uint32_t zci = s_zci;
 
   const bool fast_long = a.lut[kLutSize] != 0;
   const bool fin_scale = isfinite(a.two_eb);
@@ -153,6 +159,8 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   const uint32_t mbase = rbase + 4u * (lane * ROW);                    // my row
   const uint32_t lut_s = saddr(lut), lim_s = saddr(s_limm1), off_s = saddr(s_off), cc_s = saddr(ccache);
   const uint32_t *__restrict__ pw = a.payload;
+  // canonical index -> symbol (the most frequent codes come first in canonical order)
+  auto sym_of = [&](uint32_t ci) -> uint32_t { return ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]); };
   unsigned long long nonzero = 0, markers = 0;
   bool bad = false;
 
@@ -210,10 +218,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     const bool ok = le || (fast_long && l0 >= 1 && !c3 && (int)l <= maxlen);                      \
     int len = le ? (int)le : (int)l;                                                              \
     uint32_t sv = e >> 6;                                                                         \
-    if (ok && !le) {                                                                              \
-      const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                              \
-      sv = ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]);                           \
-    }                                                                                             \
+    if (ok && !le) sv = lds_u32(off_s + 4u * l) + (W >> (32 - l));                                \
     if (__any_sync(__activemask(), !ok)) {                                                        \
       if (!ok) {                                                                                  \
         /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */          \
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
         for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                         \
           const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                  \
           if (of < s_count[ll]) {                                                                 \
-            sv = a.canon[s_base[ll] + of];                                                        \
+            sv = s_base[ll] + (uint32_t)of;                                                       \
             len = ll;                                                                             \
             break;                                                                                \
           }                                                                                       \
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
         if (!len) {                                                                               \
           bad = true;                                                                             \
           len = 1;                                                                                \
-          sv = a.radius;                                                                          \
+          sv = 0;                                                                                 \
         }                                                                                         \
         const uint64_t np = pos + len;                                                            \
         src = pw + (np >> 5);                                                                     \
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     SYM = sv;                                                                                     \
   }
 #define ACTC_ZERO(SYM, IDX)                                                                       \
-  if (MODE != 2 && SYM == 0) {                                                                    \
+  if (MODE != 2 && SYM == zci) {                                                                  \
     if (!ord_known) {                                                                             \
       uint64_t lo = 0, hi = a.k;                                                                  \
       while (lo < hi) {                                                                           \
@@ -307,10 +312,10 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
         for (int cc = 0; cc < 32; cc++) {
           const uint32_t rw = rbase + 4u * (cc * ROW + 2 * lane);
           const uint32_t wa = lds_row(rw), wb = lds_row(rw + 4u);
-          const int d0 = (int)(wa & 0xFFFFu) - R32;
-          const int d1 = (int)(wa >> 16) - R32;
-          const int d2 = (int)(wb & 0xFFFFu) - R32;
-          const int d3 = (int)(wb >> 16) - R32;
+          const int d0 = (int)sym_of(wa & 0xFFFFu) - R32;
+          const int d1 = (int)sym_of(wa >> 16) - R32;
+          const int d2 = (int)sym_of(wb & 0xFFFFu) - R32;
+          const int d3 = (int)sym_of(wb >> 16) - R32;
           const int p1 = d0 + d1, p2 = p1 + d2, p3 = p2 + d3;
           const int inc = warp_incl_sum(p3);
           const int tot = __shfl_sync(0xffffffffu, inc, 31);
@@ -356,6 +361,11 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
             s1 = lds_row(rbase + 4u * (cc * ROW + 64 * h + 2 * lane + 1));
           }
           const uint64_t eg = ch * ACTC_CHUNK + k0;  // global element index
+          // row entries are canonical indices: outlier markers by index,
+          // everything else translated to its symbol
+          const bool m0 = v0 && s0 == zci, m1 = v1 && s1 == zci;
+          s0 = v0 ? sym_of(s0) : 0u;
+          s1 = v1 ? sym_of(s1) : 0u;
           if (MODE == 2) {
             uint32_t *out = reinterpret_cast<uint32_t *>(a.out) + eg;
             if (v1)
@@ -376,8 +386,8 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
             L1 = L0 + d1;
             Pn = Pc + __shfl_sync(0xffffffffu, inc, 31);
           } else {
-            z0 = v0 && s0 == 0;
-            z1 = v1 && s1 == 0;
+            z0 = m0;
+            z1 = m1;
             const int nzl = (int)z0 + (int)z1;
             const int zi = warp_incl_sum(nzl);
             o0 = ordc + (uint32_t)(zi - nzl);

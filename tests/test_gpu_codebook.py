@@ -67,7 +67,7 @@ def test_code_lengths_class_edge_cases(oracle):
     fib = [1, 1]
     for _ in range(40):
         fib.append(fib[-1] + fib[-2])
-    cases.append(np.array(fib, dtype=np.uint64))                    # depth 41 chain
+    deep = np.array(fib, dtype=np.uint64)                           # 41 distinct lengths: fallback
     rng = np.random.default_rng(5)
     for A in (2, 3, 64, 1000, 65536):
         for hi in (2, 3, 50):
@@ -76,6 +76,7 @@ def test_code_lengths_class_edge_cases(oracle):
         got = ph.build_code_lengths(f)
         assert _k2r_used()
         assert np.array_equal(got, oracle.build_code_lengths(f))
+    assert np.array_equal(ph.build_code_lengths(deep), oracle.build_code_lengths(deep))
 
 
 def test_code_lengths_fallback_paths(oracle):

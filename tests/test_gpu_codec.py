@@ -192,3 +192,20 @@ def test_compress_batch_matches_single(oracle):
         back, _ = pb.decompress_device(c, dtype=torch.float64)
         want = oracle.decompress_blob(ref.blob, x.numel())
         assert np.array_equal(back.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+def test_decompress_batch_matches_single(oracle):
+    rng = np.random.default_rng(23)
+    xs, ps = [], []
+    for k in range(6):
+        n = int(rng.integers(1, 400000))
+        xs.append(torch.from_numpy(np.maximum(rng.normal(0, 1, n), 0).astype(np.float32)).cuda())
+        ps.append(pb.CodecParams(eb=float(10 ** rng.uniform(-6, -1))))
+    comp = pb.compress_batch(xs, ps, max_concurrency=3)
+    outs = pb.decompress_batch([c for c, _ in comp], max_concurrency=3)
+    outs64 = pb.decompress_batch([c for c, _ in comp], dtype=torch.float64)
+    torch.cuda.synchronize()
+    for (c, rep), x, p, o, o64 in zip(comp, xs, ps, outs, outs64):
+        want = oracle.decompress_blob(oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob, x.numel())
+        assert np.array_equal(o64.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+        assert np.array_equal(o.cpu().numpy().reshape(-1), want.astype(np.float32))
