@@ -403,13 +403,28 @@ def run_gpu(args, rank, world):
     host_out = [torch.empty(t.shape, dtype=torch.float32).pin_memory() for t in tensors]
     dev_in = [torch.empty_like(t) for t in tensors]
 
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    e2e_order = sorted(range(len(tensors)), key=lambda i: -tensors[i].numel())
+
     def e2e_step():
-        for hi, di in zip(host_in, dev_in):
-            di.copy_(hi, non_blocking=True)
-        comp = pb.compress_batch(dev_in, params)
-        pb.decompress_batch([c for c, _ in comp], outs)
-        for o, ho in zip(outs, host_out):
-            ho.copy_(o, non_blocking=True)
+        # per-tensor pipeline through the public API: all host->device copies
+        # are queued up front (largest first); each tensor is compressed as
+        # soon as its copy lands, reconstructed, and copied back while later
+        # tensors are still crossing PCIe in the other direction
+        h2d_s.wait_stream(stream)
+        ready = {}
+        for i in e2e_order:
+            with torch.cuda.stream(h2d_s):
+                dev_in[i].copy_(host_in[i], non_blocking=True)
+            ready[i] = h2d_s.record_event()
+        for i in e2e_order:
+            (c, _), = pb.compress_batch([dev_in[i]], [params[i]], ready=[ready[i]])
+            done = []
+            pb.decompress_batch([c], [outs[i]], done=done)
+            d2h_s.wait_event(done[0])
+            with torch.cuda.stream(d2h_s):
+                host_out[i].copy_(outs[i], non_blocking=True)
+        stream.wait_stream(d2h_s)
 
     for _ in range(max(1, args.warmup // 2)):
         e2e_step()

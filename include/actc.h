@@ -78,7 +78,7 @@ typedef struct {
   uint32_t live_symbols;
   const uint32_t *canon_syms_dev;  /* [live_symbols] */
   const uint32_t *len_counts_dev;  /* [64]: number of codes of each length */
-  const uint8_t *payload_dev;      /* MSB-first bitstream; 4-byte aligned, >=8 B tail pad */
+  const uint8_t *payload_dev;      /* MSB-first bitstream; 4-byte aligned, >=32 B tail pad */
   uint64_t payload_bits;
   const uint64_t *chunk_offsets_dev; /* [ceil(n/ACTC_CHUNK)] or NULL (rebuilt) */
   const int64_t *chunk_lat_dev;      /* [ceil(n/ACTC_CHUNK)] lattice before each chunk, or NULL */
@@ -113,7 +113,7 @@ int actc_compress_plan(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb,
 /* compress(), phase 2 -- huffman_encode bit packing (huffman.py:188-207)
  * plus outlier extraction (codec.py:321-322) and the decode chunk index.
  * `plan` is the synchronized phase-1 result; buffers are sized from it:
- *   payload_dev      >= 4*ceil(payload_bits/32) + 8 bytes, 4-byte aligned
+ *   payload_dev      >= 4*ceil(payload_bits/32) + 32 bytes, 4-byte aligned
  *   outlier_idx_dev  [n_outliers], outlier_val_dev [n_outliers]
  *   canon_syms_dev   [live_symbols], len_counts_dev [64]
  *   chunk_offsets_dev [ceil(n/ACTC_CHUNK)]
@@ -123,6 +123,25 @@ int actc_compress_encode(actc_ctx *ctx, const float *x_dev, const actc_plan_t *p
                          float *outlier_val_dev, uint32_t *canon_syms_dev,
                          uint32_t *len_counts_dev, uint64_t *chunk_offsets_dev,
                          actc_stream s);
+
+/* compress(), both phases without a host round trip (for batches): K1,
+ * the codebook and the K3 segment encoder are launched back to back, the
+ * encoder taking its live symbol range from the device plan.  Output
+ * buffers are sized by caps instead of the plan:
+ *   payload_dev >= payload_cap_bytes (a Huffman payload is at most
+ *     n*ceil(log2 L) bits for L live symbols; the caller passes that bound + 32)
+ *   outlier_idx_dev / outlier_val_dev [k_cap]
+ *   canon_syms_dev [min(alphabet, n)], len_counts_dev [64], chunk_offsets_dev
+ * The plan lands in plan_host (pinned) when the stream reaches it.  If the
+ * stream needs the wide (> 26-bit) encoder, exceeds a cap, or the plan
+ * status is not ACTC_OK, nothing is encoded and the caller redoes the
+ * tensor with actc_compress_plan/actc_compress_encode.  Same inputs and
+ * ownership rules as actc_compress_plan. */
+int actc_compress_async(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb, uint32_t radius,
+                        uint32_t flags, int64_t *chunk_lat_dev, uint8_t *payload_dev,
+                        uint64_t payload_cap_bytes, uint64_t *outlier_idx_dev, float *outlier_val_dev,
+                        uint64_t k_cap, uint32_t *canon_syms_dev, uint32_t *len_counts_dev,
+                        uint64_t *chunk_offsets_dev, actc_plan_t *plan_host, actc_stream s);
 
 /* decompress() -- replaces codec.py:343-369: huffman_decode
  * (huffman.py:210-236), marker check (codec.py:356-359), lorenzo_decode

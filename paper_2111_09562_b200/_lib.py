@@ -91,6 +91,7 @@ def lib():
             "actc_ctx_destroy": ([P], None),
             "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P, P], I),
             "actc_compress_encode": ([P, P, P, P, P, P, P, P, P, P], I),
+            "actc_compress_async": ([P, P, U64, D, U32, U32, P, P, U64, P, P, U64, P, P, P, P, P], I),
             "actc_decompress": ([P, P, P, I, P, P], I),
             "actc_codebook_from_lengths": ([P, P, U64, P, P, P, P], I),
             "actc_build_chunk_index": ([P, P, P, P, P], I),
@@ -117,7 +118,7 @@ def lib():
 
 EXPORTED_SYMBOLS = (
     "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_compress_plan "
-    "actc_compress_encode actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
+    "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
     "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats"

@@ -123,8 +123,9 @@ def _rle_decode_lengths(cur: _Cursor, alphabet_size: int) -> np.ndarray:
 
 
 def _payload_buffer_bytes(bits: int) -> int:
-    # 4-byte words for the big-endian packer + 16 B over-read pad for the decoder
-    return 4 * ((bits + 31) // 32) + 16
+    # 4-byte words for the big-endian packer + 32 B over-read pad (the lane
+    # decoder keeps six words of look-ahead)
+    return 4 * ((bits + 31) // 32) + 32
 
 
 class _DevBufs:
@@ -177,6 +178,12 @@ class _DevBufs:
 
     def __contains__(self, name):
         return name in self._slots
+
+    def shrink(self, name, numel):
+        """the slot's exact extent once the device plan is known (capped buffers)"""
+        base, off, _, isz = self._slots[name]
+        self._slots[name] = (base, off, int(numel), isz)
+        self._views.pop(name, None)
 
     def ptr(self, name) -> int:
         base, off, _, _ = self._slots[name]
@@ -469,15 +476,18 @@ def compress_device(x, params: CodecParams, dims=None, stream=None):
     return _finish_compress(x, params, dims, plan, dev, ctx, sh)
 
 
-def _finish_compress(x, params, dims, plan, dev, ctx, sh):
-    """phase 2 (K3 encode) into exact-size buffers; returns (container, report)."""
-    torch = _lib.torch_cuda()
-    n = x.numel()
+def _check_plan(plan):
     if plan.status:
         if plan.status == _lib.ACTC_EDATA:
             from .errors import DataError
             raise DataError("tensor contains NaN or Inf")
         raise ParameterError("Huffman code length exceeds 63 bits")
+
+
+def _finish_compress(x, params, dims, plan, dev, ctx, sh):
+    """phase 2 (K3 encode) into exact-size buffers; returns (container, report)."""
+    n = x.numel()
+    _check_plan(plan)
     # one allocation per container, carved (the host cost per tensor is on
     # the critical path of compress_batch)
     k, live = plan.n_outliers, max(plan.live_symbols, 1)
@@ -491,6 +501,10 @@ def _finish_compress(x, params, dims, plan, dev, ctx, sh):
                                          bp + o["len_counts"], bp + o["chunk_off"], sh)
     if rc:
         _lib.raise_for(rc)
+    return _container(n, params, dims, plan, dev)
+
+
+def _container(n, params, dims, plan, dev):
     c = CompressedActivation._from_device(dims, params, dev, plan.payload_bits, plan.n_outliers,
                                           plan.live_symbols, plan.rle_runs)
     blob_len = _cmtz_size(len(dims), plan.n_outliers, plan.rle_runs, plan.payload_bits)
@@ -515,14 +529,19 @@ def _stream_pool(device, k):
     return pool[:k]
 
 
-def compress_batch(xs, params, max_concurrency: int = 8):
+def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
     """Compress several fp32 CUDA tensors with ONE host synchronisation.
 
-    Phase 1 (K1 quantize/Lorenzo/histogram + K2 codebook) of every tensor
-    runs concurrently on its own stream and context -- K2 is a single-CTA
-    kernel, so concurrent codebooks hide each other's latency behind the
-    bandwidth-bound kernels; then the plans are read once and phase 2 (K3)
-    runs.  Results are ordered on the caller's current stream.
+    Every tensor runs K1 (quantize/Lorenzo/histogram), K2 (codebook) and K3
+    (encode) back to back on its own stream and context with no host round
+    trip (actc_compress_async: the encoder reads its live symbol range from
+    the device plan and writes into buffers sized by caps), so the
+    single-CTA codebooks of some tensors overlap the bandwidth-bound kernels
+    of others.  The plans are read after one synchronisation; a tensor that
+    overflows a cap (or needs the > 26-bit encoder) is redone through the
+    two-phase path.  Results are ordered on the caller's current stream.
+    `ready` (optional, one CUDA event per tensor) lets each tensor start as
+    soon as its own producer (e.g. its host-to-device copy) is done.
     """
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
@@ -533,49 +552,61 @@ def compress_batch(xs, params, max_concurrency: int = 8):
             raise ParameterError("compress expects a 32-bit tensor; convert explicitly with astype(4)")
     dev_index = xs[0].device.index if xs else torch.cuda.current_device()
     main = torch.cuda.current_stream()
+    L = _lib.lib()
     results = []
-    # smallest tensors first, on the highest-priority streams: their K1 ends
-    # early, so the (single-CTA) codebooks start while the large tensors are
-    # still being quantized
-    order = sorted(range(len(xs)), key=lambda i: xs[i].numel())
+    # largest tensors first: the longest K1 -> K2 -> K3 chain starts earliest
+    order = sorted(range(len(xs)), key=lambda i: -xs[i].numel())
     for g0 in range(0, len(xs), max_concurrency):
         group = order[g0:g0 + max_concurrency]
         streams = _stream_pool(dev_index, len(group))
-        ready = main.record_event()
+        ready_ev = main.record_event()
         jobs = []
         for slot, i in enumerate(group):
             x, p = xs[i], params[i]
             s = streams[slot]
             ctx = _lib.context_for(dev_index, slot)
             n = x.numel()
+            if n == 0:
+                raise ParameterError("empty tensor")
             nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
+            lmax = min(p.alphabet_size, n)
+            cap = _payload_buffer_bytes(n * max(1, (lmax - 1).bit_length()))  # Huffman <= fixed-length code
+            k_cap = max(4096, n // 64)
             dev = _DevBufs()
-            dev["chunk_lat"] = torch.empty(nchunks, dtype=torch.int64, device=x.device)
-            s.wait_event(ready)
-            sh = C.c_void_p(s.cuda_stream)
+            base = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("out_idx", k_cap, 8),
+                                        ("payload", cap, 1), ("out_val", k_cap, 4), ("canon", lmax, 4),
+                                        ("len_counts", 64, 4)])
+            bp, o = base.data_ptr(), dev.offsets
+            s.wait_event(ready_ev)
+            if ready is not None:
+                s.wait_event(ready[i])
             flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
-            _lib.raise_for(_lib.lib().actc_compress_plan(
-                ctx.handle, C.c_void_p(x.data_ptr()), n, float(p.eb), int(p.radius), flags,
-                C.c_void_p(dev.ptr("chunk_lat")), C.c_void_p(ctx.plan_buf.data_ptr()), sh))
-            jobs.append((i, x, p, s, ctx, sh, dev, s.record_event()))
-        # launch each tensor's encode as soon as its plan has landed, so
-        # encodes of early tensors overlap the codebooks of later ones
-        pending = list(jobs)
-        while pending:
-            still = []
-            for job in pending:
-                i, x, p, s, ctx, sh, dev, done = job
-                if not done.query():
-                    still.append(job)
-                    continue
-                plan = _lib.Plan.from_buffer_copy(ctx.plan)
-                # buffers are allocated on the caller's stream and written on s
-                c, rep = _finish_compress(x, p, tuple(x.shape) or (1,), plan, dev, ctx, sh)
-                for t in dev._bufs:
-                    t.record_stream(s)
-                x.record_stream(s)
-                results.append((i, c, rep))
-            pending = still
+            _lib.raise_for(L.actc_compress_async(
+                ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, bp + o["chunk_lat"],
+                bp + o["payload"], cap, bp + o["out_idx"], bp + o["out_val"], k_cap, bp + o["canon"],
+                bp + o["len_counts"], bp + o["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream))
+            base.record_stream(s)
+            x.record_stream(s)
+            jobs.append((i, x, p, s, ctx, dev, cap, k_cap))
+        for job in jobs:
+            job[3].synchronize()
+        for i, x, p, s, ctx, dev, cap, k_cap in jobs:
+            plan = _lib.Plan.from_buffer_copy(ctx.plan)
+            n = x.numel()
+            dims = tuple(x.shape) or (1,)
+            fits = (plan.status == 0 and plan.max_len <= 26 and plan.n_outliers <= k_cap
+                    and plan.payload_bits <= 8 * (cap - 32))
+            if fits:
+                k = plan.n_outliers
+                dev.shrink("out_idx", k)
+                dev.shrink("out_val", k)
+                dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
+                dev.shrink("canon", max(plan.live_symbols, 1))
+                c, rep = _container(n, p, dims, plan, dev)
+            else:
+                _check_plan(plan)
+                c, rep = compress_device(x, p, stream=s)
+            results.append((i, c, rep))
         for job in jobs:
             main.wait_stream(job[3])
     results.sort(key=lambda r: r[0])
@@ -626,11 +657,13 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
     return out, int(r.nonzero)
 
 
-def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8):
+def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=None):
     """Reconstruct several streams concurrently, each on its own stream and
     context (a small tensor's decode alone does not fill the GPU).  Results
     are ordered on the caller's current stream; no host synchronisation, so
     status and nonzero counts are not checked (decompress_device does that).
+    If `done` is a list, it receives one CUDA event per stream (input order)
+    recorded when that reconstruction is complete.
     """
     torch = _lib.torch_cuda()
     dtype = torch.float32 if dtype is None else dtype
@@ -641,6 +674,7 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8):
     dev_index = outs[0].device.index
     main = torch.cuda.current_stream()
     order = sorted(range(len(cs)), key=lambda i: -cs[i].element_count)  # largest first
+    evs = [None] * len(cs)
     for g0 in range(0, len(cs), max_concurrency):
         group = order[g0:g0 + max_concurrency]
         streams = _stream_pool(dev_index, len(group))
@@ -662,8 +696,12 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8):
                                                        C.c_void_p(ctx.dres_buf.data_ptr()), C.c_void_p(s.cuda_stream)))
             out.record_stream(s)
             c._record_stream(s)
+            if done is not None:
+                evs[i] = s.record_event()
         for slot in range(len(group)):
             main.wait_stream(streams[slot])
+    if done is not None:
+        done.extend(evs)
     return outs
 
 

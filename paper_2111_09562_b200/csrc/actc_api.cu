@@ -116,6 +116,29 @@ struct KTimer {
 };
 #define KT(kind) KTimer kt_guard_(kind, s)
 
+// memoised cudaOccupancyMaxActiveBlocksPerMultiprocessor (the query costs
+// microseconds of host time and sits on every encode/decode launch)
+int occupancy(const void *f, int threads, size_t smem) {
+  struct Key {
+    const void *f;
+    int t;
+    size_t s;
+    int v;
+  };
+  static std::mutex mu;
+  static std::vector<Key> memo;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (const Key &k : memo)
+      if (k.f == f && k.t == threads && k.s == smem) return k.v;
+  }
+  int v = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, f, threads, smem);
+  std::lock_guard<std::mutex> g(mu);
+  if (memo.size() < 256) memo.push_back({f, threads, smem, v});
+  return v;
+}
+
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t pow2_ge(uint64_t x) {
   uint64_t p = 1;
@@ -386,9 +409,10 @@ int actc_ctx_create(int device, actc_ctx **out) {
                        (const void *)k3_count<uint32_t, false>, (const void *)k3_count<uint32_t, true>,
                        (const void *)k3_pack<uint16_t, false>,  (const void *)k3_pack<uint16_t, true>,
                        (const void *)k3_pack<uint32_t, false>,  (const void *)k3_pack<uint32_t, true>,
-                       (const void *)k4w_decode<0, 16>,         (const void *)k4w_decode<1, 16>,
-                       (const void *)k4w_decode<0, 32>,         (const void *)k4w_decode<1, 32>,
-                       (const void *)k4w_decode<2, 32>,         (const void *)k3_encode_lb<uint16_t>,
+                       (const void *)k4w_decode<0, 16, false>,  (const void *)k4w_decode<1, 16, false>,
+                       (const void *)k4w_decode<0, 32, false>,  (const void *)k4w_decode<1, 32, false>,
+                       (const void *)k4w_decode<2, 32, false>,  (const void *)k4w_decode<0, 16, true>,
+                       (const void *)k4w_decode<1, 16, true>,   (const void *)k3_encode_lb<uint16_t>,
                        (const void *)k3_encode_lb<uint32_t>,    (const void *)k3_seg_pack<uint16_t>,
                        (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
                        (const void *)k3_seg_count<uint32_t>};
@@ -423,9 +447,8 @@ void actc_ctx_destroy(actc_ctx *c) {
   delete c;
 }
 
-int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius,
-                       uint32_t flags, int64_t *chunk_lat, actc_plan_t *plan_host, actc_stream stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+static int launch_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius, int64_t *chunk_lat,
+                       cudaStream_t s) {
   if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
   if (radius < 2) return set_err(ACTC_EPARAM, "radius must be >= 2, got %u", radius);
   if (n == 0) return set_err(ACTC_EPARAM, "empty tensor");
@@ -465,12 +488,21 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
   if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, nullptr, misc + M_NOUT, n, sb, s,
                          (const unsigned *)(misc + M_BAD))))
     return rc;
-  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
   c->n = n;
   c->A = A;
   c->radius = radius;
   c->sym_bytes = sb;
   c->mode = 1;
+  return ACTC_OK;
+}
+
+int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius,
+                       uint32_t flags, int64_t *chunk_lat, actc_plan_t *plan_host, actc_stream stream) {
+  (void)flags;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_plan(c, x, n, eb, radius, chunk_lat, s);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
   return ACTC_OK;
 }
 
@@ -494,7 +526,9 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     win_lo = wl;
     win_n = cap;
   }
-  if (!wide && !getenv("ACTC_K3_TWO_PASS")) {
+  static const bool k3_two_pass = getenv("ACTC_K3_TWO_PASS") != nullptr;
+  static const bool k3_lb = getenv("ACTC_K3_LB") != nullptr;
+  if (!wide && !k3_two_pass) {
     uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
     if (span > K3L_WIN) {
       uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
@@ -503,10 +537,10 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       if (wl + K3L_WIN > hi + 1) wl = hi + 1 - K3L_WIN;
       lwin_lo = wl;
     }
-    if (!getenv("ACTC_K3_LB")) {
+    if (!k3_lb) {
       // two passes over 1024-symbol segments, no inter-warp waiting
       const uint64_t nseg = cdiv(n, K3L_SEG);
-      SegArgs g;
+      SegArgs g{};
       g.n = n;
       g.ctab = (const unsigned long long *)c->ctab.p;
       g.len8 = (const uint8_t *)c->len8.p;
@@ -520,8 +554,8 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       const void *fc = sb == 2 ? (const void *)k3_seg_count<uint16_t> : (const void *)k3_seg_count<uint32_t>;
       const void *fp = sb == 2 ? (const void *)k3_seg_pack<uint16_t> : (const void *)k3_seg_pack<uint32_t>;
       int occ_c = 0, occ_p = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, fc, K3L_THREADS, csm);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, fp, K3L_THREADS, psm);
+      occ_c = occupancy(fc, K3L_THREADS, csm);
+      occ_p = occupancy(fp, K3L_THREADS, psm);
       const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
       g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
       g.ncta = (uint32_t)cdiv(nseg, g.spc);
@@ -573,7 +607,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
     const void *f = sb == 2 ? (const void *)k3_encode_lb<uint16_t> : (const void *)k3_encode_lb<uint32_t>;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, K3L_THREADS, smem);
+    occ = occupancy(f, K3L_THREADS, smem);
     const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nseg, want));
     {
@@ -608,7 +642,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
     fp = wide ? (const void *)k3_pack<uint32_t, true> : (const void *)k3_pack<uint32_t, false>;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fp, K3_THREADS, smem_pack);
+  occ = occupancy(fp, K3_THREADS, smem_pack);
   const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
   const uint64_t tpc = cdiv(ntiles, std::min<uint64_t>(ntiles, want));
   const uint32_t ncta = (uint32_t)cdiv(ntiles, tpc);
@@ -661,6 +695,76 @@ int actc_compress_encode(actc_ctx *c, const float *x, const actc_plan_t *plan, u
   return ACTC_OK;
 }
 
+int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius, uint32_t flags,
+                        int64_t *chunk_lat, uint8_t *payload, uint64_t payload_cap_bytes, uint64_t *out_idx,
+                        float *out_val, uint64_t k_cap, uint32_t *canon, uint32_t *len_counts, uint64_t *chunk_off,
+                        actc_plan_t *plan_host, actc_stream stream) {
+  (void)flags;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_plan(c, x, n, eb, radius, chunk_lat, s);
+  if (rc) return rc;
+  // K3 segment encoder planned on the device: live range / windows from the
+  // device plan, shared-memory sizes and grids at their caps
+  const uint32_t sb = c->sym_bytes;
+  const void *sym = c->sym.p;
+  const uint64_t nseg = cdiv(n, K3L_SEG);
+  SegArgs g{};
+  g.n = n;
+  g.ctab = (const unsigned long long *)c->ctab.p;
+  g.len8 = (const uint8_t *)c->len8.p;
+  g.dplan = c->plan_dev;
+  g.radius = radius;
+  g.cap_bits = payload_cap_bytes >= 32 ? 8 * (payload_cap_bytes - 32) : 0;
+  g.k_cap = k_cap;
+  g.canon_src = (const uint32_t *)c->canon.p;
+  g.lencnt_src = (const uint32_t *)c->lencnt.p;
+  g.canon_out = canon;
+  g.lencnt_out = len_counts;
+  const size_t csm = 65536 + 16;
+  const size_t psm = (size_t)K3L_WIN * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
+  const void *fc = sb == 2 ? (const void *)k3_seg_count<uint16_t> : (const void *)k3_seg_count<uint32_t>;
+  const void *fp = sb == 2 ? (const void *)k3_seg_pack<uint16_t> : (const void *)k3_seg_pack<uint32_t>;
+  const int occ_c = occupancy(fc, K3L_THREADS, csm), occ_p = occupancy(fp, K3L_THREADS, psm);
+  const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
+  g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
+  g.ncta = (uint32_t)cdiv(nseg, g.spc);
+  if ((rc = grow(c->status, nseg * 8 + (size_t)g.ncta * 16 + 1024))) return rc;
+  g.cta_bits = (unsigned long long *)c->status.p;
+  g.cta_nz = g.cta_bits + g.ncta;
+  g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
+  g.seg_nz = g.seg_bits + nseg;
+  g.x = x;
+  g.payload = (uint32_t *)payload;
+  g.out_idx = (unsigned long long *)out_idx;
+  g.out_val = out_val;
+  g.chunk_off = (unsigned long long *)chunk_off;
+  g.extract = 1;
+  const int gp = (int)std::max<uint64_t>(
+      1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), (uint64_t)std::max(1, occ_p) * c->num_sms));
+  {
+    KT(ACTC_KIND_COUNT);
+    if (sb == 2)
+      k3_seg_count<uint16_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint16_t *)sym, g);
+    else
+      k3_seg_count<uint32_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint32_t *)sym, g);
+  }
+  {
+    KT(ACTC_KIND_SCAN);
+    k3_cta_scan<<<1, 1024, 0, s>>>(g);
+  }
+  {
+    KT(ACTC_KIND_PACK);
+    if (sb == 2)
+      k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, g);
+    else
+      k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
+  }
+  CKL();
+  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  c->mode = 0;  // the ctx holds no pending plan for actc_compress_encode
+  return ACTC_OK;
+}
+
 static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int mode,
                          actc_decode_result_t *res_host, cudaStream_t s) {
   const actc_stream_t &S = *st_in;
@@ -686,10 +790,24 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     CK(cudaMemsetAsync(ticket, 0, 8, s));
   }
   CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
+  // decoder choice for indexed streams: the warp decoder with symbols
+  // resolved in the decode chain while the canonical table fits its shared
+  // cache; the lane decoder (sequential reconstruction, canonical indices
+  // translated off the chain) for wide alphabets.  ACTC_DEC=k4w|k4wci|k4x
+  // forces one (measurements).
+  static const char *force = getenv("ACTC_DEC");
+  const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
+  int kind = (sw16 && S.live_symbols <= 24576u) ? 0 : 2;  // 0 k4w, 1 k4w ci rows, 2 k4x
+  if (force) kind = !strcmp(force, "k4w") ? 0 : !strcmp(force, "k4wci") ? 1 : 2;
+  if (kind == 1 && !(sw16 && mode != 2)) kind = 0;
+  const bool lane_dec = warp_dec && kind == 2;
   {
     KT(ACTC_KIND_LUT);
-    k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p,
-                                               warp_dec ? 1 : 0);
+    if (lane_dec)
+      k_build_lut8<<<16, 256, 0, s>>>(S.len_counts_dev, (uint8_t *)c->lut.p);
+    else
+      k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p,
+                                                 (warp_dec && kind == 1) ? 1 : 0);
   }
   CKL();
   DecodeArgs a;
@@ -716,25 +834,34 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.status = &c->dres_dev->status;
   a.chunk_lat = (const long long *)S.chunk_lat_dev;
   a.live = S.live_symbols;
-  const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
   KT(ACTC_KIND_DECODE);
-  if (warp_dec) {
+  if (lane_dec) {
+    const void *f = mode == 0 ? (const void *)k4x_decode<0> : mode == 1 ? (const void *)k4x_decode<1>
+                                                                        : (const void *)k4x_decode<2>;
+    const int occ = occupancy(f, K4X_THREADS, 0);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nchunks, K4X_THREADS),
+                                                                      (uint64_t)std::max(1, occ) * c->num_sms));
+    if (mode == 0)
+      k4x_decode<0><<<grid, K4X_THREADS, 0, s>>>(a);
+    else if (mode == 1)
+      k4x_decode<1><<<grid, K4X_THREADS, 0, s>>>(a);
+    else
+      k4x_decode<2><<<grid, K4X_THREADS, 0, s>>>(a);
+  } else if (warp_dec) {
     // warp decoder: no scan, no look-back
     const int NW = K4W_THREADS / 32;
     const size_t smem = (size_t)NW * 32 * (sw16 ? 65 : 129) * 4;  // ROUND = 128 rows (+1 pad word)
-    const void *f = mode == 0 ? (sw16 ? (const void *)k4w_decode<0, 16> : (const void *)k4w_decode<0, 32>)
-                  : mode == 1 ? (sw16 ? (const void *)k4w_decode<1, 16> : (const void *)k4w_decode<1, 32>)
-                              : (const void *)k4w_decode<2, 32>;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, K4W_THREADS, smem);
+    const bool cir = kind == 1;
+    const void *f = mode == 0 ? (cir ? (const void *)k4w_decode<0, 16, true>
+                                     : sw16 ? (const void *)k4w_decode<0, 16, false> : (const void *)k4w_decode<0, 32, false>)
+                  : mode == 1 ? (cir ? (const void *)k4w_decode<1, 16, true>
+                                     : sw16 ? (const void *)k4w_decode<1, 16, false> : (const void *)k4w_decode<1, 32, false>)
+                              : (const void *)k4w_decode<2, 32, false>;
+    const int occ = occupancy(f, K4W_THREADS, smem);
     const uint64_t nwt = cdiv(nchunks, 32);
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nwt, NW), (uint64_t)std::max(1, occ) * c->num_sms));
-    if (mode == 0)
-      sw16 ? k4w_decode<0, 16><<<grid, K4W_THREADS, smem, s>>>(a) : k4w_decode<0, 32><<<grid, K4W_THREADS, smem, s>>>(a);
-    else if (mode == 1)
-      sw16 ? k4w_decode<1, 16><<<grid, K4W_THREADS, smem, s>>>(a) : k4w_decode<1, 32><<<grid, K4W_THREADS, smem, s>>>(a);
-    else
-      k4w_decode<2, 32><<<grid, K4W_THREADS, smem, s>>>(a);
+    void *args[] = {&a};
+    CK(cudaLaunchKernel(f, dim3(grid), dim3(K4W_THREADS), args, smem, s));
   } else {
     const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
     const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)(sw16 ? c->k4_blocks[0] : c->k4_blocks[1]));

@@ -297,6 +297,13 @@ template <typename SymT>
 __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint8_t k3c_l8[];
   __shared__ unsigned long long wsum_b[K3L_THREADS / 32 + 1], wsum_z[K3L_THREADS / 32 + 1];
+  if (!seg_resolve(a)) return;
+  if (a.dplan) {
+    // device-planned: zero the payload (the pack ORs boundary words)
+    const uint64_t nw = (a.dplan->payload_bits + 31) / 32 + 2;
+    for (uint64_t i = (uint64_t)blockIdx.x * K3L_THREADS + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * K3L_THREADS)
+      a.payload[i] = 0u;
+  }
   const bool smem_tab = a.span <= K3S_L8MAX;
   uint32_t shift = 0;
   if (smem_tab) {
@@ -372,6 +379,13 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
 // exclusive prefixes of the per-CTA totals, in place (one CTA of 1024)
 __global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
   __shared__ unsigned long long wb[33], wz[33];
+  if (!seg_resolve(a)) return;
+  if (a.dplan) {
+    // device-planned: the canonical table goes to the caller's buffers
+    const uint32_t live = a.dplan->live_symbols;
+    for (uint32_t i = threadIdx.x; i < live; i += 1024) a.canon_out[i] = a.canon_src[i];
+    if (threadIdx.x < 64) a.lencnt_out[threadIdx.x] = a.lencnt_src[threadIdx.x];
+  }
   unsigned long long runb = 0, runz = 0;
   for (uint32_t c0 = 0; c0 < a.ncta; c0 += 1024) {
     const uint32_t i = c0 + threadIdx.x;
@@ -391,6 +405,7 @@ __global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
 template <typename SymT>
 __global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint32_t k3p_sm[];
+  if (!seg_resolve(a)) return;
   uint32_t *tab = k3p_sm;
   k3_load_window(tab, a.ctab, a.win_lo, a.win_n, K3L_THREADS);
   __syncthreads();

@@ -74,7 +74,7 @@ __device__ __forceinline__ void sts_row(uint32_t a, uint32_t v) {
 
 }  // namespace
 
-template <int MODE, int SW>
+template <int MODE, int SW, bool CIR>
 __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   __shared__ uint32_t lut[kLutSize];
   __shared__ uint16_t ccache[K4W_CANON_CACHE];  // canon[0 .. ncache): the most frequent codes
@@ -160,7 +160,13 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   const uint32_t lut_s = saddr(lut), lim_s = saddr(s_limm1), off_s = saddr(s_off), cc_s = saddr(ccache);
   const uint32_t *__restrict__ pw = a.payload;
   // canonical index -> symbol (the most frequent codes come first in canonical order)
-  auto sym_of = [&](uint32_t ci) -> uint32_t { return ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]); };
+  // CIR: rows hold canonical indices (translated in the reconstruct, off the
+  // decode chain); otherwise the decode chain resolves symbols itself
+  auto sym_of = [&](uint32_t ci) -> uint32_t {
+    if (!CIR) return ci;
+    return ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]);
+  };
+  const uint32_t zmark = CIR ? zci : 0u;
   unsigned long long nonzero = 0, markers = 0;
   bool bad = false;
 
@@ -218,7 +224,10 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     const bool ok = le || (fast_long && l0 >= 1 && !c3 && (int)l <= maxlen);                      \
     int len = le ? (int)le : (int)l;                                                              \
     uint32_t sv = e >> 6;                                                                         \
-    if (ok && !le) sv = lds_u32(off_s + 4u * l) + (W >> (32 - l));                                \
+    if (ok && !le) {                                                                              \
+      const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                              \
+      sv = CIR ? ci : (ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]));              \
+    }                                                                                             \
     if (__any_sync(__activemask(), !ok)) {                                                        \
       if (!ok) {                                                                                  \
         /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */          \
@@ -228,7 +237,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
         for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                         \
           const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                  \
           if (of < s_count[ll]) {                                                                 \
-            sv = s_base[ll] + (uint32_t)of;                                                       \
+            sv = CIR ? s_base[ll] + (uint32_t)of : a.canon[s_base[ll] + of];                      \
             len = ll;                                                                             \
             break;                                                                                \
           }                                                                                       \
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
         if (!len) {                                                                               \
           bad = true;                                                                             \
           len = 1;                                                                                \
-          sv = 0;                                                                                 \
+          sv = CIR ? 0u : a.radius;                                                               \
         }                                                                                         \
         const uint64_t np = pos + len;                                                            \
         src = pw + (np >> 5);                                                                     \
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     SYM = sv;                                                                                     \
   }
 #define ACTC_ZERO(SYM, IDX)                                                                       \
-  if (MODE != 2 && SYM == zci) {                                                                  \
+  if (MODE != 2 && SYM == zmark) {                                                                \
     if (!ord_known) {                                                                             \
       uint64_t lo = 0, hi = a.k;                                                                  \
       while (lo < hi) {                                                                           \
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
           const uint64_t eg = ch * ACTC_CHUNK + k0;  // global element index
           // row entries are canonical indices: outlier markers by index,
           // everything else translated to its symbol
-          const bool m0 = v0 && s0 == zci, m1 = v1 && s1 == zci;
+          const bool m0 = v0 && s0 == zmark, m1 = v1 && s1 == zmark;
           s0 = v0 ? sym_of(s0) : 0u;
           s1 = v1 ? sym_of(s1) : 0u;
           if (MODE == 2) {
@@ -449,10 +458,12 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
   }
 }
 
-template __global__ void k4w_decode<0, 16>(DecodeArgs);
-template __global__ void k4w_decode<1, 16>(DecodeArgs);
-template __global__ void k4w_decode<0, 32>(DecodeArgs);
-template __global__ void k4w_decode<1, 32>(DecodeArgs);
-template __global__ void k4w_decode<2, 32>(DecodeArgs);
+template __global__ void k4w_decode<0, 16, false>(DecodeArgs);
+template __global__ void k4w_decode<1, 16, false>(DecodeArgs);
+template __global__ void k4w_decode<0, 32, false>(DecodeArgs);
+template __global__ void k4w_decode<1, 32, false>(DecodeArgs);
+template __global__ void k4w_decode<2, 32, false>(DecodeArgs);
+template __global__ void k4w_decode<0, 16, true>(DecodeArgs);
+template __global__ void k4w_decode<1, 16, true>(DecodeArgs);
 
 }  // namespace actc

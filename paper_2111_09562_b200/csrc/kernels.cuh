@@ -148,7 +148,38 @@ struct SegArgs {
   float *out_val;
   unsigned long long *chunk_off;
   int extract;
+  // device-planned launch (actc_compress_async): when dplan is set the kernels
+  // take the live range / window from the device plan, skip everything when
+  // the stream does not fit the caps (the host redoes it synchronously), the
+  // count pass zeroes the payload and the scan copies the canonical table
+  const actc_plan_t *dplan;
+  uint32_t radius;
+  uint64_t cap_bits, k_cap;
+  const uint32_t *canon_src, *lencnt_src;
+  uint32_t *canon_out, *lencnt_out;
 };
+// resolve a device-planned SegArgs; false = this stream takes the host path
+__device__ __forceinline__ bool seg_resolve(SegArgs &a) {
+  if (!a.dplan) return true;
+  const actc_plan_t &p = *a.dplan;
+  if (p.status != ACTC_OK || p.max_len > (uint32_t)K3_SHORT_MAXLEN || p.payload_bits > a.cap_bits ||
+      p.n_outliers > a.k_cap)
+    return false;
+  const uint32_t lo = p.sym_lo, hi = p.sym_hi;
+  const uint32_t span = hi >= lo ? hi - lo + 1 : 1;
+  a.lo = lo;
+  a.span = span;
+  a.win_lo = lo;
+  a.win_n = min(span, K3L_WIN);
+  if (span > K3L_WIN) {
+    const uint32_t centre = a.radius ? a.radius : (lo + hi) / 2;
+    uint32_t wl = centre > K3L_WIN / 2 ? centre - K3L_WIN / 2 : 0;
+    if (wl < lo) wl = lo;
+    if (wl + K3L_WIN > hi + 1) wl = hi + 1 - K3L_WIN;
+    a.win_lo = wl;
+  }
+  return true;
+}
 template <typename SymT>
 __global__ void k3_seg_count(const SymT *__restrict__ sym, SegArgs a);
 __global__ void k3_cta_scan(SegArgs a);
@@ -194,8 +225,13 @@ struct DecodeArgs {
 // SW: staging width of decoded symbols in shared memory (16 or 32 bits)
 template <int MODE, int SW>
 __global__ void k4_decode(DecodeArgs a);
-template <int MODE, int SW>
+template <int MODE, int SW, bool CIR>
 __global__ void k4w_decode(DecodeArgs a);
+// K4x: lane per chunk, sequential inverse Lorenzo in registers
+constexpr int K4X_THREADS = 256;
+__global__ void k_build_lut8(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8);
+template <int MODE>
+__global__ void k4x_decode(DecodeArgs a);
 __global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
                                 unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
 

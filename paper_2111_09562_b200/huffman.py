@@ -105,7 +105,7 @@ def huffman_encode(symbols, alphabet_size: int):
     lens_h = lengths.cpu().numpy().view(np.uint16)
     if n == 0:
         return lens_h, b"", 0
-    payload = torch.empty(4 * ((plan.payload_bits + 31) // 32) + 16, dtype=torch.uint8, device="cuda")
+    payload = torch.empty(4 * ((plan.payload_bits + 31) // 32) + 32, dtype=torch.uint8, device="cuda")
     canon = torch.empty(max(plan.live_symbols, 1), dtype=torch.int32, device="cuda")
     counts = torch.empty(64, dtype=torch.int32, device="cuda")
     chunk = torch.empty((n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK, dtype=torch.int64, device="cuda")
@@ -129,7 +129,7 @@ def huffman_decode(lengths, payload: bytes, bit_length: int, count: int) -> np.n
     if lengths.max() > MAX_CODE_LENGTH:
         raise FormatError("invalid code in bitstream")
     canon, counts, live = _canon_tables(lengths.astype(np.uint16))
-    pb = np.zeros(4 * ((bit_length + 31) // 32) + 16, dtype=np.uint8)
+    pb = np.zeros(4 * ((bit_length + 31) // 32) + 32, dtype=np.uint8)
     nbytes = (bit_length + 7) // 8
     pb[:nbytes] = np.frombuffer(payload, dtype=np.uint8)[:nbytes]
     pd = torch.from_numpy(pb).cuda()
