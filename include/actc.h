@@ -137,6 +137,8 @@ int actc_compress_encode(actc_ctx *ctx, const float *x_dev, const actc_plan_t *p
  * status is not ACTC_OK, nothing is encoded and the caller redoes the
  * tensor with actc_compress_plan/actc_compress_encode.  Same inputs and
  * ownership rules as actc_compress_plan. */
+#define ACTC_ASYNC_K1_ONLY 0x100u /* flags: launch only K1 (quantize/Lorenzo/histogram) */
+#define ACTC_ASYNC_REST 0x200u    /* flags: launch the codebook + encoder after a K1_ONLY call */
 int actc_compress_async(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb, uint32_t radius,
                         uint32_t flags, int64_t *chunk_lat_dev, uint8_t *payload_dev,
                         uint64_t payload_cap_bytes, uint64_t *outlier_idx_dev, float *outlier_val_dev,

@@ -17,6 +17,8 @@ LIB_PATH = os.path.join(HERE, "libactc.so")
 
 ACTC_OK, ACTC_EPARAM, ACTC_EDATA, ACTC_EFORMAT, ACTC_ENOMEM, ACTC_ECUDA = range(6)
 ACTC_FLAG_PRESERVE_ZEROS = 1
+ACTC_ASYNC_K1_ONLY = 0x100
+ACTC_ASYNC_REST = 0x200
 ACTC_DTYPE_F32, ACTC_DTYPE_F64 = 0, 1
 ACTC_CHUNK = 256
 

@@ -581,16 +581,20 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
             if ready is not None:
                 s.wait_event(ready[i])
             flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
-            _lib.raise_for(L.actc_compress_async(
-                ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, bp + o["chunk_lat"],
-                bp + o["payload"], cap, bp + o["out_idx"], bp + o["out_val"], k_cap, bp + o["canon"],
-                bp + o["len_counts"], bp + o["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream))
+            args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, bp + o["chunk_lat"],
+                    bp + o["payload"], cap, bp + o["out_idx"], bp + o["out_val"], k_cap, bp + o["canon"],
+                    bp + o["len_counts"], bp + o["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
+            # every tensor's K1 goes out before any codebook/encoder launch
+            _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
             base.record_stream(s)
             x.record_stream(s)
-            jobs.append((i, x, p, s, ctx, dev, cap, k_cap))
+            jobs.append((i, x, p, s, ctx, dev, cap, k_cap, args))
+        for job in jobs:
+            args = job[8]
+            _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
         for job in jobs:
             job[3].synchronize()
-        for i, x, p, s, ctx, dev, cap, k_cap in jobs:
+        for i, x, p, s, ctx, dev, cap, k_cap, _ in jobs:
             plan = _lib.Plan.from_buffer_copy(ctx.plan)
             n = x.numel()
             dims = tuple(x.shape) or (1,)

@@ -166,13 +166,16 @@ struct actc_ctx {
   uint32_t radius = 0, sym_bytes = 2, win_lo = 0, win_n = 0;
   int mode = 0;  // 1 = codec, 2 = huffman debug
   int k1_blocks = 0, k3_blocks = 0, k4_blocks[5] = {0, 0, 0, 0, 0};
+  // when set (actc_compress_async), the codebook writes the canonical table
+  // straight into the caller's buffers instead of the ctx scratch
+  uint32_t *canon_out = nullptr, *lencnt_out = nullptr;
 };
 
 namespace {
 
 // codebook scratch carve-up for alphabet A
 struct CbLayout {
-  size_t live_sym, live_freq, keys, keys2, vals, vals2, nf, lpar, npar, llen, ndepth, cls16, total;
+  size_t live_sym, live_freq, keys, keys2, vals, vals2, nf, lpar, npar, llen, ndepth, cls16, rank_tab, total;
 };
 CbLayout cb_layout(uint64_t A) {
   CbLayout l;
@@ -196,6 +199,7 @@ CbLayout cb_layout(uint64_t A) {
   l.llen = take(A);
   l.ndepth = take(4 * A);
   l.cls16 = take(2 * A + 64);
+  l.rank_tab = take(1024 * 34 * 2);
   l.total = o;
   return l;
 }
@@ -222,8 +226,8 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   a.in_lengths = in_lengths;
   a.ctab = (unsigned long long *)c->ctab.p;
   a.len8 = (uint8_t *)c->len8.p;
-  a.canon = (uint32_t *)c->canon.p;
-  a.len_counts = (uint32_t *)c->lencnt.p;
+  a.canon = c->canon_out ? c->canon_out : (uint32_t *)c->canon.p;
+  a.len_counts = c->lencnt_out ? c->lencnt_out : (uint32_t *)c->lencnt.p;
   a.out_lengths = out_lengths;
   a.plan = c->plan_dev;
   a.n_outliers = n_out;
@@ -243,6 +247,7 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   a.sym_bytes = sym_bytes;
   a.dbg = nullptr;
   a.cls16 = (uint16_t *)(b + l.cls16);
+  a.rank_tab = (uint16_t *)(b + l.rank_tab);
   a.fallback = (unsigned *)((unsigned long long *)c->misc.p + M_K2GATE);
   a.gate = nullptr;
   if (getenv("ACTC_K2_TIMING")) {
@@ -256,13 +261,16 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   static const bool no_k2r = getenv("ACTC_K2_OLD") != nullptr;
   if (!in_lengths && A <= 65536 && n_symbols < (1ull << 32) && !no_k2r) {
     KT(ACTC_KIND_CODEBOOK);
-    CK(cudaMemsetAsync(a.fallback, 0xFF, 4, s));
     k2r_codebook<<<1, K2_THREADS, kK2rSmem, s>>>(a);
     a.gate = a.fallback;
   }
   {
     KT(ACTC_KIND_CODEBOOK);
     k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
+  }
+  if (a.gate) {
+    KT(ACTC_KIND_CODEBOOK);
+    k2s_emit<<<K2_THREADS / 32, 32, 0, s>>>(a);
   }
   CKL();
   return ACTC_OK;
@@ -447,8 +455,8 @@ void actc_ctx_destroy(actc_ctx *c) {
   delete c;
 }
 
-static int launch_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius, int64_t *chunk_lat,
-                       cudaStream_t s) {
+static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius, int64_t *chunk_lat,
+                     cudaStream_t s) {
   if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
   if (radius < 2) return set_err(ACTC_EPARAM, "radius must be >= 2, got %u", radius);
   if (n == 0) return set_err(ACTC_EPARAM, "empty tensor");
@@ -485,15 +493,28 @@ static int launch_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
           (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
   }
   CKL();
-  if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, nullptr, misc + M_NOUT, n, sb, s,
-                         (const unsigned *)(misc + M_BAD))))
-    return rc;
   c->n = n;
   c->A = A;
   c->radius = radius;
   c->sym_bytes = sb;
+  return ACTC_OK;
+}
+
+// codebook for the histogram the last launch_k1 on this ctx produced
+static int launch_cb(actc_ctx *c, cudaStream_t s) {
+  unsigned long long *misc = (unsigned long long *)c->misc.p;
+  int rc = run_codebook(c, (const unsigned long long *)c->hist.p, c->A, nullptr, nullptr, misc + M_NOUT, c->n,
+                        c->sym_bytes, s, (const unsigned *)(misc + M_BAD));
+  if (rc) return rc;
   c->mode = 1;
   return ACTC_OK;
+}
+
+static int launch_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius, int64_t *chunk_lat,
+                       cudaStream_t s) {
+  int rc = launch_k1(c, x, n, eb, radius, chunk_lat, s);
+  if (rc) return rc;
+  return launch_cb(c, s);
 }
 
 int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius,
@@ -570,6 +591,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       g.out_val = out_val;
       g.chunk_off = (unsigned long long *)chunk_off;
       g.extract = extract;
+      g.k = plan->n_outliers;
       CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
       const int gp = (int)std::max<uint64_t>(
           1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), (uint64_t)std::max(1, occ_p) * c->num_sms));
@@ -699,9 +721,20 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
                         int64_t *chunk_lat, uint8_t *payload, uint64_t payload_cap_bytes, uint64_t *out_idx,
                         float *out_val, uint64_t k_cap, uint32_t *canon, uint32_t *len_counts, uint64_t *chunk_off,
                         actc_plan_t *plan_host, actc_stream stream) {
-  (void)flags;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = launch_plan(c, x, n, eb, radius, chunk_lat, s);
+  int rc;
+  // ACTC_ASYNC_K1_ONLY / ACTC_ASYNC_REST split the launch in two so a batch
+  // can put every tensor's K1 on the GPU before the rest of any chain
+  if (!(flags & ACTC_ASYNC_REST)) {
+    if ((rc = launch_k1(c, x, n, eb, radius, chunk_lat, s))) return rc;
+    if (flags & ACTC_ASYNC_K1_ONLY) return ACTC_OK;
+  } else if (c->n != n) {
+    return set_err(ACTC_EPARAM, "actc_compress_async(REST) without a matching K1 launch");
+  }
+  c->canon_out = canon;
+  c->lencnt_out = len_counts;
+  rc = launch_cb(c, s);
+  c->canon_out = c->lencnt_out = nullptr;
   if (rc) return rc;
   // K3 segment encoder planned on the device: live range / windows from the
   // device plan, shared-memory sizes and grids at their caps
@@ -716,8 +749,8 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   g.radius = radius;
   g.cap_bits = payload_cap_bytes >= 32 ? 8 * (payload_cap_bytes - 32) : 0;
   g.k_cap = k_cap;
-  g.canon_src = (const uint32_t *)c->canon.p;
-  g.lencnt_src = (const uint32_t *)c->lencnt.p;
+  g.canon_src = nullptr;  // the codebook wrote the caller's table directly
+  g.lencnt_src = nullptr;
   g.canon_out = canon;
   g.lencnt_out = len_counts;
   const size_t csm = 65536 + 16;

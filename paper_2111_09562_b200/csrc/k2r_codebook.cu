@@ -839,21 +839,14 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   }
   column_prefix(cntT, kTS, maxlen + 1 - minlen, s_base + minlen);
   __syncthreads();
-  // pass C: canonical ranks -> canon[], ctab[]
-  for (uint32_t c0 = q0; c0 < q1; c0 += 16) {
-    const uint4 lv = *reinterpret_cast<const uint4 *>(a.len8 + c0);
-    const uint32_t wv[4] = {lv.x, lv.y, lv.z, lv.w};
+  // pass C (canonical ranks -> canon[], ctab[]) is k2s_emit's: one SM's
+  // store pipe is too narrow for ~2 scattered stores per symbol.  Hand over
+  // this thread's starting rank per length (column prefix + base).
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(myT);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(a.rank_tab + (size_t)tid * kTS);
 #pragma unroll
-    for (int u = 0; u < 16; u++) {
-      const uint32_t s = c0 + u;
-      const uint32_t len = (wv[u >> 2] >> (8 * (u & 3))) & 0xFFu;
-      if (len && s < q1) {
-        const uint32_t ci = myT[len - minlen];
-        myT[len - minlen] = (uint16_t)(ci + 1);
-        a.canon[ci] = s;
-        if (len <= 56) a.ctab[s] = ((s_first[len] + (ci - s_base[len])) << 8) | len;
-      }
-    }
+    for (int u = 0; u < kTS / 2; u++) dst[u] = src[u];
   }
   if (tid < 64) a.len_counts[tid] = s_lencnt[tid];
   __syncthreads();
@@ -890,6 +883,61 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     }
   }
 #undef K2R_STAMP
+}
+
+// K2s: canonical codes for the symbols of the k2r threads' segments
+// (huffman.py:78-94 rule: code = first[len] + rank among the symbols of that
+// length in symbol order); thread t of the grid replays k2r thread t's
+// segment with the starting ranks k2r left in rank_tab.  32 CTAs of one warp:
+// the scattered stores spread over 32 SMs.
+__global__ void __launch_bounds__(32) k2s_emit(CodebookArgs a) {
+  if (*a.fallback) return;  // k2_codebook built the tables
+  __shared__ uint16_t s_row[32 * kTS];
+  __shared__ unsigned long long s_first[64];
+  __shared__ uint32_t s_base[64];
+  const int lane = threadIdx.x;
+  const uint32_t t = blockIdx.x * 32 + lane;
+  if (lane == 0) {
+    unsigned long long code = 0;
+    uint32_t idx = 0;
+    for (int l = 0; l < 64; l++) {
+      code <<= 1;
+      s_first[l] = code;
+      s_base[l] = idx;
+      code += a.len_counts[l];
+      idx += a.len_counts[l];
+    }
+  }
+  uint32_t minlen = 64;
+  for (int l = 63; l >= 1; l--)
+    if (a.len_counts[l]) minlen = l;
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(a.rank_tab + (size_t)t * kTS);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(s_row + lane * kTS);
+#pragma unroll
+    for (int u = 0; u < kTS / 2; u++) dst[u] = src[u];
+  }
+  __syncwarp();
+  const uint32_t lo = a.plan->sym_lo, hi = a.plan->sym_hi;
+  const uint32_t p0 = lo & ~15u;
+  const uint32_t SEG = ((((hi + 1 - p0) + NT - 1) / NT) + 15) & ~15u;
+  const uint32_t q0 = p0 + t * SEG, q1 = min(hi + 1, q0 + SEG);
+  uint16_t *row = s_row + lane * kTS;
+  for (uint32_t c0 = q0; c0 < q1; c0 += 16) {
+    const uint4 lv = *reinterpret_cast<const uint4 *>(a.len8 + c0);
+    const uint32_t wv[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t s = c0 + u;
+      const uint32_t len = (wv[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+      if (len && s < q1) {
+        const uint32_t ci = row[len - minlen];
+        row[len - minlen] = (uint16_t)(ci + 1);
+        a.canon[ci] = s;
+        if (len <= 56) a.ctab[s] = ((s_first[len] + (ci - s_base[len])) << 8) | len;
+      }
+    }
+  }
 }
 
 }  // namespace actc

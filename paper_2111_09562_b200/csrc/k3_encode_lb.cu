@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
 __global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
   __shared__ unsigned long long wb[33], wz[33];
   if (!seg_resolve(a)) return;
-  if (a.dplan) {
-    // device-planned: the canonical table goes to the caller's buffers
+  if (a.dplan && a.canon_src) {
+    // device-planned with the table in ctx scratch: copy it to the caller's buffers
     const uint32_t live = a.dplan->live_symbols;
     for (uint32_t i = threadIdx.x; i < live; i += 1024) a.canon_out[i] = a.canon_src[i];
     if (threadIdx.x < 64) a.lencnt_out[threadIdx.x] = a.lencnt_src[threadIdx.x];
@@ -402,8 +402,23 @@ __global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
   }
 }
 
+__device__ __forceinline__ uint32_t k3_saddr(const void *p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t k3_lds(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v, uint32_t p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
+               ::"r"(addr), "r"(v), "r"(p) : "memory");
+}
+
 template <typename SymT>
-__global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
+__global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint32_t k3p_sm[];
   if (!seg_resolve(a)) return;
   uint32_t *tab = k3p_sm;
@@ -414,30 +429,45 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(const SymT *__rest
   const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
   const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
   const uint32_t wlast = a.win_n - 1;
+  const bool fast_tab = a.span <= a.win_n;
+  const uint32_t tab_rel = k3_saddr(tab) - 4u * a.win_lo;  // tab[s - win_lo] at tab_rel + 4s (mod 2^32)
+  const uint32_t wb_s = k3_saddr(wb);
   for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + warp; seg < nseg; seg += nwarps) {
     const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
     uint32_t s[K3L_EPT];
     lb_load(sym, base, a.n, s);
     const uint64_t r = seg / a.spc;
     const unsigned long long pb = a.cta_bits[r] + a.seg_bits[seg], pz = a.cta_nz[r] + a.seg_nz[seg];
-    // one (code << 6 | len) lookup per symbol: clamped into the shared window,
-    // symbols outside it (rare, long codes) fixed up from the global table
+    // one (code << 6 | len) lookup per symbol
     uint32_t e[K3L_EPT];
-    uint32_t oow = 0, zmask = 0;
+    uint32_t zmask = 0;
+    if (fast_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
+      // every live symbol is inside the window and the segment is full
 #pragma unroll
-    for (int j = 0; j < K3L_EPT; j++) {
-      const uint32_t wi = s[j] - a.win_lo;
-      const bool sent = s[j] == kSent;
-      e[j] = sent ? 0u : tab[min(wi, wlast)];
-      oow |= (uint32_t)(wi > wlast && !sent) << j;
-      zmask |= (uint32_t)(s[j] == 0) << j;
-    }
-    if (oow) {
+      for (int j = 0; j < K3L_EPT; j++) e[j] = k3_lds(tab_rel + 4u * s[j]);
+      if (a.k) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) zmask |= (uint32_t)(s[j] == 0) << j;
+      }
+    } else {
+      // clamped into the shared window, symbols outside it (rare, long
+      // codes) fixed up from the global table; sentinels past the end
+      uint32_t oow = 0;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        if ((oow >> j) & 1u) {  // re-read the symbol: s[] is dead here (register pressure)
-          const unsigned long long g = __ldg(&a.ctab[(uint32_t)sym[base + j]]);
-          e[j] = (uint32_t)(((g >> 8) << 6) | (g & 63));
+        const uint32_t wi = s[j] - a.win_lo;
+        const bool sent = s[j] == kSent;
+        e[j] = sent ? 0u : tab[min(wi, wlast)];
+        oow |= (uint32_t)(wi > wlast && !sent) << j;
+        zmask |= (uint32_t)(s[j] == 0) << j;
+      }
+      if (oow) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) {
+          if ((oow >> j) & 1u) {  // re-read the symbol: s[] is dead here (register pressure)
+            const unsigned long long g = __ldg(&a.ctab[(uint32_t)sym[base + j]]);
+            e[j] = (uint32_t)(((g >> 8) << 6) | (g & 63));
+          }
         }
       }
     }
@@ -463,28 +493,26 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_seg_pack(const SymT *__rest
       }
     }
     {
-      // codes <= 26 bits complete at most one word each: predicated emits;
-      // the lane's first word and final partial word may be shared -> atomic.
-      // A length-0 entry (past the end) has code 0.
+      // codes <= 26 bits complete at most one word each.  Every word goes
+      // into the (zeroed) warp buffer by a predicated shared OR, so the
+      // lane's first and last words -- shared with its neighbours -- need
+      // no special case.  A length-0 entry (past the end) has code 0.
       const uint32_t rel = off0 + lane_ex;
-      uint32_t w = rel >> 5;
-      const uint32_t w0 = w;
-      int nb = rel & 31;
+      uint32_t addr = wb_s + 4u * (rel >> 5);
+      uint32_t nb = rel & 31;
       unsigned long long acc = 0;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        const int lj = (int)(e[j] & 63);
-        acc |= (unsigned long long)(e[j] >> 6) << ((64 - nb - lj) & 63);  // len 0 -> code 0
+        const uint32_t lj = e[j] & 63;
+        acc |= (unsigned long long)(e[j] >> 6) << ((64 - nb - lj) & 63);
         nb += lj;
-        const bool ready = nb >= 32;
-        const uint32_t hiw = (uint32_t)(acc >> 32);
-        if (ready && w == w0) atomicOr(&wb[w], hiw);
-        if (ready && w != w0) wb[w] = hiw;
+        const uint32_t ready = nb >= 32;
+        k3_red_or(addr, (uint32_t)(acc >> 32), ready);
         acc = ready ? (acc << 32) : acc;
-        nb = ready ? nb - 32 : nb;
-        w += ready;
+        nb -= ready << 5;
+        addr += ready << 2;
       }
-      if (nb > 0) atomicOr(&wb[w], (uint32_t)(acc >> 32));
+      k3_red_or(addr, (uint32_t)(acc >> 32), nb > 0);
     }
     __syncwarp();
     const uint64_t gw0 = pb >> 5;

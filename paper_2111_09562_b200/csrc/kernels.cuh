@@ -26,7 +26,7 @@ constexpr int K3_SHORT_MAXLEN = 26;
 constexpr int K3L_THREADS = 256;
 constexpr int K3L_EPT = 32;
 constexpr int K3L_SEG = 32 * K3L_EPT;                                     // symbols per segment
-constexpr uint32_t K3L_WIN = 8192;                                        // u32 code-table window
+constexpr uint32_t K3L_WIN = 16384;                                       // u32 code-table window
 constexpr int K3L_WORDS = (K3L_SEG * K3_SHORT_MAXLEN + 31) / 32 + 2;      // packed words per segment (max)
 
 // K4 (scan variant, streams without a lattice index): one thread per chunk
@@ -93,6 +93,7 @@ struct CodebookArgs {
   uint16_t *cls16;                 // [A] class id per symbol (k2r scratch)
   unsigned *fallback;              // k2r: 1 = caps exceeded, run k2_codebook
   const unsigned *gate;            // k2_codebook: if non-null and *gate == 0, do nothing
+  uint16_t *rank_tab;              // [1024 x 34] k2r -> k2s starting canonical ranks
 };
 __global__ void k2_codebook(CodebookArgs a);
 // K2r (frequency-class codebook) capacities; dynamic shared memory size
@@ -100,6 +101,7 @@ constexpr uint32_t kRCap = 6144;
 constexpr uint32_t kICap = 11264;
 constexpr size_t kK2rSmem = (size_t)(3 * (kRCap + 1) + 3 * (kICap + 1)) * 4;
 __global__ void k2r_codebook(CodebookArgs a);
+__global__ void k2s_emit(CodebookArgs a);
 
 template <typename SymT, bool WIDE>
 __global__ void k3_count(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
@@ -153,6 +155,7 @@ struct SegArgs {
   // the stream does not fit the caps (the host redoes it synchronously), the
   // count pass zeroes the payload and the scan copies the canonical table
   const actc_plan_t *dplan;
+  uint64_t k;  // outlier count (from the plan); 0 skips the marker scan
   uint32_t radius;
   uint64_t cap_bits, k_cap;
   const uint32_t *canon_src, *lencnt_src;
@@ -167,6 +170,7 @@ __device__ __forceinline__ bool seg_resolve(SegArgs &a) {
     return false;
   const uint32_t lo = p.sym_lo, hi = p.sym_hi;
   const uint32_t span = hi >= lo ? hi - lo + 1 : 1;
+  a.k = p.n_outliers;
   a.lo = lo;
   a.span = span;
   a.win_lo = lo;

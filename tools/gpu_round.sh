@@ -11,13 +11,13 @@ if [ -z "$2" ]; then
 fi
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2>> gpurun_out/${TAG}_bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:"k1_|k2_|k3_|k_excl|k_build|k4w_|k4_" -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:"k1_|k2|k3_|k_build|k4w_|k4x_|k4_" -c 400 --csv \
    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-train > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k1_|k2_|k3_|k_excl|k_build|k4w_" -s 45 -c 45 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k1_|k2|k3_|k_build|k4w_|k4x_" -s 45 -c 45 \
    -o gpurun_out/${TAG}_step -f python tools/prof_workload.py --steps 2 > gpurun_out/${TAG}_ncu_full.log 2>&1
 ncu -i gpurun_out/${TAG}_step.ncu-rep --page raw --csv > gpurun_out/${TAG}_step_raw.csv 2>/dev/null
 ncu -i gpurun_out/${TAG}_step.ncu-rep --page details --csv > gpurun_out/${TAG}_step_details.csv 2>/dev/null
-for k in k4w_decode k1_quant_lorenzo_hist k3_pack k2_codebook; do
+for k in k4w_decode k4x_decode k1_quant_lorenzo_hist k3_seg_pack k3_seg_count k2r_codebook; do
   ncu -i gpurun_out/${TAG}_step.ncu-rep --page source --csv --print-source sass -k regex:$k -c 1 > gpurun_out/${TAG}_src_$k.csv 2>/dev/null
 done
 # the copy-back limit is 64 MiB: keep the report only when small
