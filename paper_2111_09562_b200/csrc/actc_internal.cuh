@@ -42,19 +42,26 @@ __device__ __forceinline__ long long quant_exact(double x, double two_eb, double
 
 // Fast path in fp64 with a multiply instead of the division.
 // v' = x * fl64(1/(2eb)) is within |v|*2^-51 of the true quotient; when the
-// distance of |v'| to the rounding boundary exceeds m = (|v'|+1)*2^-44 the
-// exact path (x / 2eb, floor(fl(|v|+0.5))) provably yields the same q, and
-// |x - q*2eb| <= eb*(1 - m) so the bound check cannot fire.  |v'| < 2^29
-// keeps q in int32.  Returns false when the caller must take quant_exact.
-__device__ __forceinline__ bool quant_fast(float xf, double inv, long long &q) {
+// distance of |v'| to the rounding boundary exceeds (|v'|+1)*2^-44 the exact
+// path (x / 2eb, floor(fl(|v|+0.5))) provably yields the same q, and
+// |x - q*2eb| <= eb*(1 - m) so the bound check cannot fire.  With |v'| <
+// 2^29 that margin is below 2^-14, which is used as a constant (three fp64
+// operations fewer per element; ~1e-4 of elements take the exact path
+// instead).  Returns false when the caller must take quant_exact.
+__device__ __forceinline__ bool quant_fast32(float xf, double inv, int &q) {
   const double v = __dmul_rn((double)xf, inv);
   const double a = fabs(v);
   const double f = floor(__dadd_rn(a, 0.5));
   const double r = __dsub_rn(a, f);
-  const double m = __dmul_rn(__dadd_rn(a, 1.0), 0x1p-44);
-  const bool safe = (a < 0x1p29) && (fabs(r) < __dsub_rn(0.5, m));
+  const bool safe = (a < 0x1p29) && (fabs(r) < 0.49993896484375);  // 0.5 - 2^-14
   const int qi = (int)f;
   q = xf > 0.0f ? qi : -qi;
+  return safe;
+}
+__device__ __forceinline__ bool quant_fast(float xf, double inv, long long &q) {
+  int q32;
+  const bool safe = quant_fast32(xf, inv, q32);
+  q = q32;
   return safe;
 }
 

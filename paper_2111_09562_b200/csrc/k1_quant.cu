@@ -84,12 +84,13 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
     // fp32 fast quantizer for all 16 elements; exact fp64 only where needed
     int q32[K1_EPT];
     unsigned slow = 0;
+    if (P.fast) {
 #pragma unroll
-    for (int j = 0; j < K1_EPT; j++) {
-      long long qq;
-      const bool ok = P.fast && quant_fast(xv[j], P.inv, qq);
-      q32[j] = (int)qq;
-      slow |= (unsigned)!ok << j;
+      for (int j = 0; j < K1_EPT; j++) slow |= (unsigned)!quant_fast32(xv[j], P.inv, q32[j]) << j;
+    } else {
+      slow = (1u << K1_EPT) - 1;
+#pragma unroll
+      for (int j = 0; j < K1_EPT; j++) q32[j] = 0;
     }
     long long prev64;
     {

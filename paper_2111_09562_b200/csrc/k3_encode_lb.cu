@@ -293,6 +293,17 @@ __device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned lon
   }
 }
 
+__device__ __forceinline__ uint32_t k3c_saddr(const void *p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t k3c_ldsb(uint32_t a) {
+  unsigned short v;
+  asm("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+
 template <typename SymT>
 __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint8_t k3c_l8[];
@@ -329,6 +340,7 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
   }
   __syncthreads();
   const uint8_t *l8 = k3c_l8 + shift;  // l8[s - lo]
+  const uint32_t l8_rel = k3c_saddr(k3c_l8) + shift - a.lo;  // l8[s - lo] at l8_rel + s (mod 2^32)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
   const uint64_t s0 = (uint64_t)blockIdx.x * a.spc, s1 = min(nseg, s0 + a.spc);
@@ -338,15 +350,25 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
     uint32_t s[K3L_EPT];
     lb_load(sym, base, a.n, s);
     uint32_t bits = 0, nz = 0;
+    if (smem_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
+      // full segment, byte table in shared memory: one LDS.U8 per symbol
 #pragma unroll
-    for (int j = 0; j < K3L_EPT; j++) {
-      if (s[j] != kSent) {
-        bits += smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
-        nz += s[j] == 0;
+      for (int j = 0; j < K3L_EPT; j++) bits += k3c_ldsb(l8_rel + s[j]);
+      if (a.k) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) nz += s[j] == 0;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] != kSent) {
+          bits += smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
+          nz += s[j] == 0;
+        }
       }
     }
     bits = warp_sum(bits);
-    nz = warp_sum(nz);
+    if (a.k || !__all_sync(0xffffffffu, nz == 0)) nz = warp_sum(nz);
     if (lane == 0) {
       a.seg_bits[seg] = bits;
       a.seg_nz[seg] = nz;
