@@ -214,22 +214,20 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
     }                                                                                             \
     const uint32_t W = (uint32_t)(buf >> 32);                                                     \
     const uint32_t e = lds_u32(lut_s + ((W >> (32 - kLutBits)) << 2));                            \
-    const uint32_t le = e & 63;                                                                   \
-    /* uniform step: short codes (le > 0) start the limit probes at their own length and */       \
-    /* stay there (limits are non-decreasing); long codes start at the LUT's l0 */                \
-    const uint32_t l0 = le ? le : (e >> 6);                                                       \
-    const uint32_t lb = lim_s + 4u * l0;                                                          \
-    const uint32_t l = l0 + (W > lds_u32(lb)) + (W > lds_u32(lb + 4u)) + (W > lds_u32(lb + 8u));  \
-    const bool c3 = W > lds_u32(lb + 12u);                                                        \
-    const bool ok = le || (fast_long && l0 >= 1 && !c3 && (int)l <= maxlen);                      \
-    int len = le ? (int)le : (int)l;                                                              \
+    int len = (int)(e & 63);                                                                      \
     uint32_t sv = e >> 6;                                                                         \
-    if (ok && !le) {                                                                              \
-      const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                              \
-      sv = CIR ? ci : (ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]));              \
-    }                                                                                             \
-    if (__any_sync(__activemask(), !ok)) {                                                        \
-      if (!ok) {                                                                                  \
+    if (len == 0) {                                                                               \
+      /* long code (divergent): the LUT gives the shortest length l0 behind the prefix; */        \
+      /* three comparisons with the left-aligned canonical limits finish the length */           \
+      const uint32_t l0 = sv;                                                                     \
+      const uint32_t lb = lim_s + 4u * l0;                                                        \
+      const uint32_t l = l0 + (W > lds_u32(lb)) + (W > lds_u32(lb + 4u)) + (W > lds_u32(lb + 8u)); \
+      const bool ok = fast_long && l0 >= 1 && !(W > lds_u32(lb + 12u)) && (int)l <= maxlen;      \
+      if (ok) {                                                                                   \
+        const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                            \
+        sv = CIR ? ci : (ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]));            \
+        len = (int)l;                                                                             \
+      } else {                                                                                    \
         /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */          \
         const uint64_t pos = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;                     \
         const uint64_t win = read_bits64(pw, pos);                                                \
