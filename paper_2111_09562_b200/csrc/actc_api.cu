@@ -883,7 +883,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   } else if (warp_dec) {
     // warp decoder: no scan, no look-back
     const int NW = K4W_THREADS / 32;
-    const size_t smem = (size_t)NW * 32 * (sw16 ? 65 : 129) * 4;  // ROUND = 128 rows (+1 pad word)
+    const size_t smem = (size_t)NW * 32 * (sw16 ? 33 : 65) * 4;  // ROUND = 64 rows (+1 pad word)
     const bool cir = kind == 1;
     const void *f = mode == 0 ? (cir ? (const void *)k4w_decode<0, 16, true>
                                      : sw16 ? (const void *)k4w_decode<0, 16, false> : (const void *)k4w_decode<0, 32, false>)

@@ -29,7 +29,7 @@ namespace actc {
 
 namespace {
 
-constexpr int ROUND = 128;            // symbols per lane per round
+constexpr int ROUND = 64;             // symbols per lane per round
 constexpr int ROW16 = ROUND / 2 + 1;  // words per row, u16 symbols
 constexpr int ROW32 = ROUND + 1;      // words per row, u32 symbols
 constexpr int NW4 = K4W_THREADS / 32;
@@ -75,7 +75,7 @@ __device__ __forceinline__ void sts_row(uint32_t a, uint32_t v) {
 }  // namespace
 
 template <int MODE, int SW, bool CIR>
-__global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
+__global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
   __shared__ uint32_t lut[kLutSize];
   __shared__ uint16_t ccache[K4W_CANON_CACHE];  // canon[0 .. ncache): the most frequent codes
   __shared__ uint32_t s_limm1[64];              // ((first+count) << (32-l)) - 1, saturated
@@ -317,32 +317,25 @@ __global__ void __launch_bounds__(K4W_THREADS, 2) k4w_decode(DecodeArgs a) {
         int P32 = (int)P;
         const int R32 = (int)radius;
         for (int cc = 0; cc < 32; cc++) {
-          const uint32_t rw = rbase + 4u * (cc * ROW + 2 * lane);
-          const uint32_t wa = lds_row(rw), wb = lds_row(rw + 4u);
+          // lane owns elements 2*lane, 2*lane+1 of row cc (ROUND = 64)
+          const uint32_t wa = lds_row(rbase + 4u * (cc * ROW + lane));
           const int d0 = (int)sym_of(wa & 0xFFFFu) - R32;
           const int d1 = (int)sym_of(wa >> 16) - R32;
-          const int d2 = (int)sym_of(wb & 0xFFFFu) - R32;
-          const int d3 = (int)sym_of(wb >> 16) - R32;
-          const int p1 = d0 + d1, p2 = p1 + d2, p3 = p2 + d3;
-          const int inc = warp_incl_sum(p3);
+          const int p1 = d0 + d1;
+          const int inc = warp_incl_sum(p1);
           const int tot = __shfl_sync(0xffffffffu, inc, 31);
           const int Pc = __shfl_sync(0xffffffffu, P32, cc);
-          const int B = Pc + (inc - p3);
+          const int B = Pc + (inc - p1);
           if (lane == cc) P32 = Pc + tot;
-          const int L0 = B + d0, L1 = B + p1, L2 = B + p2, L3 = B + p3;
+          const int L0 = B + d0, L1 = B + p1;
           const double r0 = __dmul_rn((double)L0, a.two_eb);
           const double r1 = __dmul_rn((double)L1, a.two_eb);
-          const double r2 = __dmul_rn((double)L2, a.two_eb);
-          const double r3 = __dmul_rn((double)L3, a.two_eb);
-          nonzero += (L0 != 0) + (L1 != 0) + (L2 != 0) + (L3 != 0);
-          const uint64_t eg = (wt * 32 + cc) * ACTC_CHUNK + i0 + 4 * lane;
+          nonzero += (L0 != 0) + (L1 != 0);
+          const uint64_t eg = (wt * 32 + cc) * ACTC_CHUNK + i0 + 2 * lane;
           if (MODE == 0) {
-            __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.out) + eg),
-                   make_float4((float)r0, (float)r1, (float)r2, (float)r3));
+            __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.out) + eg), make_float2((float)r0, (float)r1));
           } else {
-            double2 *o = reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.out) + eg);
-            __stcs(o, make_double2(r0, r1));
-            __stcs(o + 1, make_double2(r2, r3));
+            __stcs(reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.out) + eg), make_double2(r0, r1));
           }
         }
         P = P32;

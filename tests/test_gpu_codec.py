@@ -209,3 +209,27 @@ def test_decompress_batch_matches_single(oracle):
         want = oracle.decompress_blob(oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob, x.numel())
         assert np.array_equal(o64.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
         assert np.array_equal(o.cpu().numpy().reshape(-1), want.astype(np.float32))
+
+
+def test_compress_batch_cap_overflow_takes_two_phase_path(oracle):
+    """actc_compress_async sizes outlier buffers by a cap (max(4096, n/64));
+    a tensor with more outliers must come back through the two-phase path,
+    bit-exact either way"""
+    rng = np.random.default_rng(29)
+    n = 200_000
+    x = (rng.standard_normal(n) * 1e4).astype(np.float32)  # deltas >> radius at this eb: ~all outliers
+    small = np.maximum(rng.normal(0, 1, 50_000), 0).astype(np.float32)
+    xs = [torch.from_numpy(x).cuda(), torch.from_numpy(small).cuda()]
+    ps = [pb.CodecParams(eb=1e-3, radius=64), pb.CodecParams(eb=1e-2)]
+    out = pb.compress_batch(xs, ps)
+    for (c, rep), xt, p in zip(out, xs, ps):
+        ref = oracle.compress(xt.cpu().numpy(), p.eb, radius=p.radius, debug=False)
+        assert c.to_bytes() == ref.blob
+        assert rep.ratio == ref.ratio
+    assert out[0][1].outlier_fraction > 0.5
+    back = pb.decompress_batch([c for c, _ in out], dtype=torch.float64)
+    torch.cuda.synchronize()
+    for o, xt, p in zip(back, xs, ps):
+        want = oracle.decompress_blob(oracle.compress(xt.cpu().numpy(), p.eb, radius=p.radius, debug=False).blob,
+                                      xt.numel())
+        assert np.array_equal(o.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
