@@ -41,7 +41,7 @@ extern "C" {
 
 /* Symbols per decode chunk: the encoder records the bit offset of every
  * ACTC_CHUNK-th symbol in a device-side index (not part of CMTZ). */
-#define ACTC_CHUNK 256
+#define ACTC_CHUNK 128
 #define ACTC_MAX_CODE_LENGTH 63 /* huffman.py:34 */
 
 typedef void *actc_stream; /* a cudaStream_t */

@@ -20,7 +20,7 @@ ACTC_FLAG_PRESERVE_ZEROS = 1
 ACTC_ASYNC_K1_ONLY = 0x100
 ACTC_ASYNC_REST = 0x200
 ACTC_DTYPE_F32, ACTC_DTYPE_F64 = 0, 1
-ACTC_CHUNK = 256
+ACTC_CHUNK = 128
 
 
 class Plan(C.Structure):

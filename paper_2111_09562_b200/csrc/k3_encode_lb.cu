@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
       pb += s_wbits[w];
       pz += s_wnz[w];
     }
-    if ((lane & 7) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
+    if (((lane * K3L_EPT) % ACTC_CHUNK) == 0 && base < n) chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every ACTC_CHUNK-th symbol
     if (extract_outliers && nz) {
       unsigned long long o = pz + (iz - nz);
 #pragma unroll
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
     const uint32_t nw = (off0 + seg_bits + 31) >> 5;
     for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
     __syncwarp();
-    if ((lane & 7) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every 256th symbol
+    if (((lane * K3L_EPT) % ACTC_CHUNK) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every ACTC_CHUNK-th symbol
     if (a.extract && nz) {
       unsigned long long o = pz + (iz - nz);
       for (uint32_t m = zmask; m; m &= m - 1) {
