@@ -203,7 +203,7 @@ class CompressedActivation:
     __slots__ = (
         "dims", "precision", "params", "symbol_count", "payload_bits",
         "_h_outlier_indices", "_h_outlier_values", "_h_code_lengths", "_h_payload",
-        "_dev", "_live", "_n_outliers", "_rle_runs",
+        "_dev", "_live", "_n_outliers", "_rle_runs", "_desc_cache",
     )
 
     def __init__(self, dims, precision, params, outlier_indices, outlier_values, symbol_count,
@@ -221,6 +221,7 @@ class CompressedActivation:
         self._live = None
         self._n_outliers = len(self._h_outlier_indices)
         self._rle_runs = None
+        self._desc_cache = None
 
     # ---- device-resident construction (compress) ----
     @classmethod
@@ -239,6 +240,7 @@ class CompressedActivation:
         self._live = int(live)
         self._n_outliers = int(n_outliers)
         self._rle_runs = int(rle_runs)
+        self._desc_cache = None
         return self
 
     @property
@@ -329,6 +331,8 @@ class CompressedActivation:
                 t.record_stream(s)
 
     def _desc(self, with_index=True) -> _lib.StreamDesc:
+        if with_index and self._desc_cache is not None:
+            return self._desc_cache
         dev = self._dev
         d = _lib.StreamDesc()
         d.n = self.symbol_count
@@ -345,6 +349,8 @@ class CompressedActivation:
         d.payload_bits = self.payload_bits
         d.chunk_offsets_dev = dev.ptr("chunk_off") if (with_index and "chunk_off" in dev) else None
         d.chunk_lat_dev = dev.ptr("chunk_lat") if (with_index and "chunk_lat" in dev) else None
+        if with_index and d.chunk_offsets_dev:
+            self._desc_cache = d  # device buffers are fixed for the container's lifetime
         return d
 
     def _ensure_index(self):
@@ -592,9 +598,11 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
         for job in jobs:
             args = job[8]
             _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
-        for job in jobs:
-            job[3].synchronize()
+        # containers are built as each stream finishes (the host work of the
+        # early tensors overlaps the GPU tail of the late ones), and each
+        # container's stream descriptor is built once here
         for i, x, p, s, ctx, dev, cap, k_cap, _ in jobs:
+            s.synchronize()
             plan = _lib.Plan.from_buffer_copy(ctx.plan)
             n = x.numel()
             dims = tuple(x.shape) or (1,)
@@ -607,6 +615,7 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
                 dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
                 dev.shrink("canon", max(plan.live_symbols, 1))
                 c, rep = _container(n, p, dims, plan, dev)
+                c._desc()
             else:
                 _check_plan(plan)
                 c, rep = compress_device(x, p, stream=s)
@@ -683,21 +692,27 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
         group = order[g0:g0 + max_concurrency]
         streams = _stream_pool(dev_index, len(group))
         ready = main.record_event()
+        L = _lib.lib()
+        f32 = torch.float32
         for slot, i in enumerate(group):
             c, out = cs[i], outs[i]
-            n = c.element_count
-            if c.symbol_count != n:
-                raise FormatError(f"symbol count {c.symbol_count} != element count {n}")
-            if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
+            n = c.symbol_count
+            if out.numel() != n or out.dtype not in (f32, torch.float64) or not out.is_contiguous():
                 raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
-            c._ensure_index()
+            d = c._desc_cache
+            if d is None:
+                if n != c.element_count:
+                    raise FormatError(f"symbol count {n} != element count {c.element_count}")
+                c._ensure_index()
+                d = c._desc()
             s = streams[slot]
             s.wait_event(ready)
             ctx = _lib.context_for(dev_index, slot)
-            code = _lib.ACTC_DTYPE_F32 if out.dtype == torch.float32 else _lib.ACTC_DTYPE_F64
-            d = c._desc()
-            _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
-                                                       C.c_void_p(ctx.dres_buf.data_ptr()), C.c_void_p(s.cuda_stream)))
+            rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(),
+                                   _lib.ACTC_DTYPE_F32 if out.dtype == f32 else _lib.ACTC_DTYPE_F64,
+                                   None, s.cuda_stream)  # no result mailbox: nothing is read back
+            if rc:
+                _lib.raise_for(rc)
             out.record_stream(s)
             c._record_stream(s)
             if done is not None:

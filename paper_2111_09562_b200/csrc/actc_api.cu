@@ -822,7 +822,8 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
     CK(cudaMemsetAsync(ticket, 0, 8, s));
   }
-  CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
+  // the result mailbox is only read back when the caller asks for it
+  if (res_host || !warp_dec) CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
   // decoder choice for indexed streams: the warp decoder with symbols
   // resolved in the decode chain while the canonical table fits its shared
   // cache; the lane decoder (sequential reconstruction, canonical indices
