@@ -53,7 +53,7 @@ constexpr uint32_t kHT = 0x80000000u;     // head-taken flag on a run's position
 constexpr int kMaxLv = 64;
 constexpr int kMaxSide = 96;
 constexpr uint32_t kInf32 = 0xFFFFFFFFu;
-constexpr uint32_t kHot = 64;             // classes counted in per-warp counters
+constexpr uint32_t kHot = 384;            // classes counted in per-warp counters
 constexpr int kNL = 32;                   // max distinct code lengths (symbol passes)
 constexpr int kTS = kNL + 2;              // per-thread length-counter stride (odd word count)
 constexpr int kNS = 8;                    // max cut classes
@@ -786,9 +786,11 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
       }
     }
     __syncthreads();
+    K2R_STAMP(13)
     column_prefix(cntS, kSS, nsc, nullptr);
     __syncthreads();
   }
+  K2R_STAMP(14)
   // pass B: lengths (len8 written 16 at a time), per-thread length counts, run starts
   {
     uint32_t prevlen = 0, starts = 0;
@@ -837,16 +839,19 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     starts = warp_sum(starts);
     if (lane == 0 && starts) atomicAdd(&s_starts, starts);
   }
+  K2R_STAMP(15)
   column_prefix(cntT, kTS, maxlen + 1 - minlen, s_base + minlen);
+  K2R_STAMP(16)
   __syncthreads();
   // pass C (canonical ranks -> canon[], ctab[]) is k2s_emit's: one SM's
   // store pipe is too narrow for ~2 scattered stores per symbol.  Hand over
   // this thread's starting rank per length (column prefix + base).
   {
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(myT);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(a.rank_tab + (size_t)tid * kTS);
-#pragma unroll
-    for (int u = 0; u < kTS / 2; u++) dst[u] = src[u];
+    // the [thread][length] table is contiguous in shared memory: copy it coalesced
+    __syncthreads();
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(cntT);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(a.rank_tab);
+    for (uint32_t i = tid; i < (uint32_t)(NT * kTS / 2); i += NT) dst[i] = src[i];
   }
   if (tid < 64) a.len_counts[tid] = s_lencnt[tid];
   __syncthreads();

@@ -31,6 +31,9 @@ for rep in range(2):
             d = {st[i]: v[i + 1] - v[i] for i in range(7)}
             print(f"k2r L={v[9]} classes={v[10]} iruns={v[11]} phases={v[8]} cut_classes={v[12]} "
                   f"total={v[7]-v[0]} cycles", d)
+            if v[14] > v[5]:
+                print("    symbols:", {"passA": (v[13] - v[5]) if v[13] > v[5] else 0, "prefixA": (v[14] - v[13]) if v[13] > v[5] else 0,
+                                     "passB": v[15] - v[14], "prefixB": v[16] - v[15], "handover": v[6] - v[16]})
         else:
             st = ["compact", "sort", "phases", "depth", "canon", "plan"]
             d = {st[i]: v[i + 1] - v[i] for i in range(6) if v[i + 1] >= v[i]}
