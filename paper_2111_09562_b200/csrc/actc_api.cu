@@ -406,11 +406,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
   }
   CK(cudaFuncSetAttribute(k2_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2Smem));
   CK(cudaFuncSetAttribute(k2r_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2rSmem));
-  // occupancy-derived persistent grid sizes
   int nb = 0;
-  size_t k1smem = K1_WIN * 4;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, k1smem);
-  c->k1_blocks = std::max(1, nb) * c->num_sms;
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   const void *big[] = {(const void *)k3_count<uint16_t, false>, (const void *)k3_count<uint16_t, true>,
@@ -423,12 +419,16 @@ int actc_ctx_create(int device, actc_ctx **out) {
                        (const void *)k4w_decode<1, 16, true>,   (const void *)k3_encode_lb<uint16_t>,
                        (const void *)k3_encode_lb<uint32_t>,    (const void *)k3_seg_pack<uint16_t>,
                        (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
-                       (const void *)k3_seg_count<uint32_t>};
+                       (const void *)k3_seg_count<uint32_t>,    (const void *)k1_quant_lorenzo_hist<uint16_t>,
+                       (const void *)k1_quant_lorenzo_hist<uint32_t>, (const void *)k_hist_u32};
   for (const void *f : big) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, f));
     CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
   }
+  // occupancy-derived persistent grid sizes
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, (size_t)K1_WIN * 4);
+  c->k1_blocks = std::max(1, nb) * c->num_sms;
   size_t s16 = (size_t)K4_THREADS * (ACTC_CHUNK / 2 + 1) * 4, s32 = (size_t)K4_THREADS * (ACTC_CHUNK + 1) * 4;
   CK(cudaFuncSetAttribute(k4_decode<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
   CK(cudaFuncSetAttribute(k4_decode<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
