@@ -179,6 +179,29 @@ class _DevBufs:
     def __contains__(self, name):
         return name in self._slots
 
+    def compact(self, names, stream):
+        """Move the named slots into one exact-size allocation (copies on
+        `stream`); their old backing allocation is released once unused."""
+        torch = _lib.torch_cuda()
+        olds = {self._slots[nm][0] for nm in names}
+        layout = [(nm, self._slots[nm][2], self._slots[nm][3]) for nm in names]
+        offs, o = {}, 0
+        for nm, numel, isz in layout:
+            offs[nm] = o
+            o += (numel * isz + 15) & ~15
+        base = torch.empty(max(o, 16), dtype=torch.uint8, device=next(iter(olds)).device)
+        with torch.cuda.stream(stream):
+            for nm, numel, isz in layout:
+                src, soff, _, _ = self._slots[nm]
+                nb = numel * isz
+                if nb:
+                    base[offs[nm]:offs[nm] + nb].copy_(src[soff:soff + nb])
+                self._slots[nm] = (base, offs[nm], numel, isz)
+                self._views.pop(nm, None)
+        base.record_stream(stream)
+        still = {self._slots[nm][0] for nm in self._slots}
+        self._bufs = [b for b in self._bufs if b not in olds or b in still] + [base]
+
     def shrink(self, name, numel):
         """the slot's exact extent once the device plan is known (capped buffers)"""
         base, off, _, isz = self._slots[name]
@@ -535,7 +558,7 @@ def _stream_pool(device, k):
     return pool[:k]
 
 
-def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
+def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bool = False, bit_hints=None):
     """Compress several fp32 CUDA tensors with ONE host synchronisation.
 
     Every tensor runs K1 (quantize/Lorenzo/histogram), K2 (codebook) and K3
@@ -548,6 +571,11 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
     two-phase path.  Results are ordered on the caller's current stream.
     `ready` (optional, one CUDA event per tensor) lets each tensor start as
     soon as its own producer (e.g. its host-to-device copy) is done.
+    `compact` copies the payload and outliers into exact-size buffers and
+    releases the capped ones (stored activations, where memory is the point).
+    `bit_hints` (optional, per tensor: expected payload bits or None) caps
+    the payload at 1.25x the hint instead of n*ceil(log2 L) bits -- e.g. the
+    same layer's previous size in training; an overflow is redone exactly.
     """
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
@@ -576,23 +604,30 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
                 raise ParameterError("empty tensor")
             nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
             lmax = min(p.alphabet_size, n)
-            cap = _payload_buffer_bytes(n * max(1, (lmax - 1).bit_length()))  # Huffman <= fixed-length code
+            cap_bits = n * max(1, (lmax - 1).bit_length())  # Huffman <= fixed-length code
+            if bit_hints is not None and bit_hints[i]:
+                cap_bits = min(cap_bits, int(bit_hints[i] * 1.25) + 4096)
+            cap = _payload_buffer_bytes(cap_bits)
             k_cap = max(4096, n // 64)
             dev = _DevBufs()
-            base = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("out_idx", k_cap, 8),
-                                        ("payload", cap, 1), ("out_val", k_cap, 4), ("canon", lmax, 4),
-                                        ("len_counts", 64, 4)])
-            bp, o = base.data_ptr(), dev.offsets
+            # fixed-size arrays, and the capped (data-dependent) ones apart so
+            # `compact` can replace the latter by exact-size copies
+            fixed = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("canon", lmax, 4),
+                                         ("len_counts", 64, 4)])
+            fp, of = fixed.data_ptr(), dev.offsets
+            capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4)])
+            cp, oc = capped.data_ptr(), dev.offsets
             s.wait_event(ready_ev)
             if ready is not None:
                 s.wait_event(ready[i])
             flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
-            args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, bp + o["chunk_lat"],
-                    bp + o["payload"], cap, bp + o["out_idx"], bp + o["out_val"], k_cap, bp + o["canon"],
-                    bp + o["len_counts"], bp + o["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
+            args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
+                    cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, fp + of["canon"],
+                    fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
             # every tensor's K1 goes out before any codebook/encoder launch
             _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
-            base.record_stream(s)
+            fixed.record_stream(s)
+            capped.record_stream(s)
             x.record_stream(s)
             jobs.append((i, x, p, s, ctx, dev, cap, k_cap, args))
         for job in jobs:
@@ -614,6 +649,8 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None):
                 dev.shrink("out_val", k)
                 dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
                 dev.shrink("canon", max(plan.live_symbols, 1))
+                if compact:
+                    dev.compact(("out_idx", "payload", "out_val"), s)
                 c, rep = _container(n, p, dims, plan, dev)
                 c._desc()
             else:

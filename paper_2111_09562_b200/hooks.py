@@ -101,6 +101,15 @@ class IterationRecord:
     raw_bytes: int = 0
 
 
+class _LayerMap(dict):
+    """conv_layer_map's result: the layer map plus the model it came from
+    (whose in-place ReLUs run out of place in collection iterations)."""
+
+    def __init__(self, d, model):
+        super().__init__(d)
+        self.model = model
+
+
 class ActivationCompressor:
     """Adaptive activation compression for a PyTorch model.
 
@@ -115,6 +124,7 @@ class ActivationCompressor:
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 8, dist_group=None,
                  sync_stats: bool = True):
         self.layers = dict(layers)
+        self._model = getattr(layers, "model", None)
         self.optimizer = optimizer
         self.config = config or ControllerConfig()
         self.controller = AdaptiveController(self.config)
@@ -134,13 +144,14 @@ class ActivationCompressor:
         self._pending: list[_Handle] = []
         self._collecting = False
         self._R: dict[str, float] = {}
+        self._bits: dict[str, int] = {}
         self._lbar: dict[str, float] = {}
         self._batch = None
         self._rec = None
         self._hooks = []
+        self._bwd_hooks = []
         for lid, (prod, cons) in self.layers.items():
             self._hooks.append(prod.register_forward_hook(self._fwd_hook(lid)))
-            self._hooks.append(cons.register_full_backward_hook(self._bwd_hook(lid)))
 
     # ---- construction helpers -------------------------------------------
     @staticmethod
@@ -151,10 +162,6 @@ class ActivationCompressor:
         (reference _consumer_map, training.py:154-166)."""
         import torch.nn as nn
 
-        # full backward hooks on the consumers forbid in-place ops on their outputs
-        for m in model.modules():
-            if isinstance(m, nn.ReLU):
-                m.inplace = False
         mods = [(n, m) for n, m in model.named_modules() if not list(m.children())]
         out = {}
         for i, (name, m) in enumerate(mods):
@@ -169,12 +176,21 @@ class ActivationCompressor:
                     break
             if cons is not None:
                 out[name] = (act, cons)
-        return out
+        return _LayerMap(out, model)
+
+    def _modules(self):
+        seen = []
+        for prod, cons in self.layers.values():
+            for m in (prod, cons):
+                if all(m is not x for x in seen):
+                    seen.append(m)
+        return seen
 
     def remove(self):
-        for h in self._hooks:
+        for h in self._hooks + self._bwd_hooks:
             h.remove()
         self._hooks.clear()
+        self._bwd_hooks.clear()
 
     # ---- hooks ---------------------------------------------------------------
     def _fwd_hook(self, lid):
@@ -229,9 +245,11 @@ class ActivationCompressor:
             return
         pend, self._pending = self._pending, []
         params = [CodecParams(eb=h.eb, radius=self.radius, preserve_zeros=self.preserve_zeros) for h in pend]
-        out = compress_batch([h.raw for h in pend], params)
+        hints = [self._bits.get(h.layer) for h in pend]
+        out = compress_batch([h.raw for h in pend], params, compact=True, bit_hints=hints)
         for h, (c, rep) in zip(pend, out):
             h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
+            self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
             self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
             if self._rec is not None:
                 self._rec.stored_bytes += rep.compressed_bytes
@@ -281,9 +299,32 @@ class ActivationCompressor:
         self._lbar.clear()
         self.store.clear()
         self._rec = IterationRecord(self.it)
-        with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack):
-            yield self
-            self.flush()
+        # the consumers' output-gradient hooks (L_bar) exist only in collection
+        # iterations: full backward hooks wrap every call of their module
+        relus = []
+        if self._collecting:
+            import torch.nn as nn
+
+            # full backward hooks forbid in-place ops on their modules' outputs:
+            # in-place ReLUs run out of place in collection iterations only
+            scope = self._model.modules() if self._model is not None else (
+                m for mod in self._modules() for m in mod.modules())
+            for m in scope:
+                if isinstance(m, nn.ReLU) and m.inplace:
+                    m.inplace = False
+                    relus.append(m)
+            for lid, (prod, cons) in self.layers.items():
+                self._bwd_hooks.append(cons.register_full_backward_hook(self._bwd_hook(lid)))
+        try:
+            with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack):
+                yield self
+                self.flush()
+        finally:
+            for h in self._bwd_hooks:
+                h.remove()
+            self._bwd_hooks.clear()
+            for m in relus:
+                m.inplace = True
         self._handles.clear()
         self._act_layer.clear()
 

@@ -233,3 +233,21 @@ def test_compress_batch_cap_overflow_takes_two_phase_path(oracle):
         want = oracle.decompress_blob(oracle.compress(xt.cpu().numpy(), p.eb, radius=p.radius, debug=False).blob,
                                       xt.numel())
         assert np.array_equal(o.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+
+
+def test_compress_batch_compact(oracle):
+    """compact=True: payload/outliers moved to exact-size buffers; same bytes"""
+    rng = np.random.default_rng(31)
+    xs = [torch.from_numpy(np.maximum(rng.normal(0, 1, n), 0).astype(np.float32)).cuda() for n in (70000, 300000)]
+    ps = [pb.CodecParams(eb=1e-3), pb.CodecParams(eb=1e-5)]  # the second overflows the outlier cap
+    loose = pb.compress_batch(xs, ps)
+    tight = pb.compress_batch(xs, ps, compact=True)
+    for (c0, r0), (c1, r1), x, p in zip(loose, tight, xs, ps):
+        assert c1.to_bytes() == c0.to_bytes() == oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob
+        assert c1.device_nbytes <= c0.device_nbytes
+    assert tight[0][0].device_nbytes < loose[0][0].device_nbytes
+    outs = pb.decompress_batch([c for c, _ in tight], dtype=torch.float64)
+    torch.cuda.synchronize()
+    for o, x, p in zip(outs, xs, ps):
+        want = oracle.decompress_blob(oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob, x.numel())
+        assert np.array_equal(o.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
