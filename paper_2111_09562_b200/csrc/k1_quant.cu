@@ -77,10 +77,6 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) xv[j] = (base + j < n) ? x[base + j] : 0.0f;
     }
-    bool fin = true;
-#pragma unroll
-    for (int j = 0; j < K1_EPT; j++) fin &= isfinite(xv[j]);
-    fin_all &= fin;
     // fp32 fast quantizer for all 16 elements; exact fp64 only where needed
     int q32[K1_EPT];
     unsigned slow = 0;
@@ -91,6 +87,12 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
       slow = (1u << K1_EPT) - 1;
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) q32[j] = 0;
+    }
+    // non-finite inputs always fail the fast path (|v| < 2^29 is false for
+    // inf and NaN), so only the lanes that took the slow path are checked
+    if (slow) {
+#pragma unroll
+      for (int j = 0; j < K1_EPT; j++) fin_all &= !((slow >> j) & 1u) || isfinite(xv[j]);
     }
     long long prev64;
     {
