@@ -841,7 +841,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
       k_build_lut8<<<16, 256, 0, s>>>(S.len_counts_dev, (uint8_t *)c->lut.p);
     else
       k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p,
-                                                 (warp_dec && kind == 1) ? 1 : 0);
+                                                 warp_dec ? ((kind == 1 ? 1 : 0) | 2) : 0);
   }
   CKL();
   DecodeArgs a;

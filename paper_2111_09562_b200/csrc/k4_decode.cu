@@ -91,12 +91,14 @@ __device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint
 // holds the fast-path flag: 1 if the code is prefix-free (Kraft <= 1) and
 // max length <= 32.
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
-                            uint32_t *__restrict__ lut, int ci_mode) {
+                            uint32_t *__restrict__ lut, int mode) {
   __shared__ CodeTables t;
+  __shared__ unsigned s_ok;
   build_tables(t, len_counts);
   __syncthreads();
+  const int ci_mode = mode & 1;
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p == 0) {
+  if (threadIdx.x == 0) {
     // Kraft sum in units of 2^-63
     unsigned long long k = 0;
     bool over = false;
@@ -107,8 +109,10 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
       k += add;
       if (k > (1ull << 63)) over = true;
     }
-    lut[kLutSize] = (!over && t.maxlen <= 32) ? 1u : 0u;
+    s_ok = (!over && t.maxlen <= 32) ? 1u : 0u;
+    if (p == 0) lut[kLutSize] = s_ok;
   }
+  __syncthreads();
   if (p >= (uint32_t)kLutSize) return;
   uint32_t e = 0;
   int lim = t.maxlen < (uint32_t)kLutBits ? (int)t.maxlen : kLutBits;
@@ -122,13 +126,17 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
   }
   if (!e && t.maxlen > (uint32_t)kLutBits && t.maxlen <= 32) {
     const unsigned long long w = (unsigned long long)p << (32 - kLutBits);
+    const unsigned long long w1 = w | ((1ull << (32 - kLutBits)) - 1);
+    int l0 = 0, l1 = 0;
     for (int l = kLutBits + 1; l <= (int)t.maxlen; l++) {
       unsigned long long limit = (t.first[l] + t.count[l]) << (32 - l);
-      if (limit > w) {
-        e = (uint32_t)l << 6;
-        break;
-      }
+      if (!l0 && limit > w) l0 = l;
+      if (!l1 && limit > w1) l1 = l;
     }
+    if (l0) e = (uint32_t)l0 << 6;
+    // mode bit1: every code behind the prefix has the same length -> "exact
+    // long" entry (length field 63): the decoder skips the limit probes
+    if ((mode & 2) && s_ok && l0 && l1 == l0) e |= 63u;
   }
   lut[p] = e;
 }

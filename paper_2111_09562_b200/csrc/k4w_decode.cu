@@ -216,7 +216,12 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
     const uint32_t e = lds_u32(lut_s + ((W >> (32 - kLutBits)) << 2));                            \
     int len = (int)(e & 63);                                                                      \
     uint32_t sv = e >> 6;                                                                         \
-    if (len == 0) {                                                                               \
+    if (len == 63) {                                                                              \
+      /* long code, one length behind this prefix: canonical index directly */                    \
+      const uint32_t ci = lds_u32(off_s + 4u * sv) + (W >> (32 - sv));                            \
+      len = (int)sv;                                                                              \
+      sv = CIR ? ci : (ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]));              \
+    } else if (len == 0) {                                                                        \
       /* long code (divergent): the LUT gives the shortest length l0 behind the prefix; */        \
       /* three comparisons with the left-aligned canonical limits finish the length */           \
       const uint32_t l0 = sv;                                                                     \

@@ -193,9 +193,11 @@ __global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long lon
                          const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
                          const uint32_t *__restrict__ tail, uint32_t ncta);
 
-// ci_mode: short-code entries carry the canonical index instead of the symbol
+// mode bit0: short-code entries carry the canonical index instead of the
+// symbol; bit1: long prefixes with a single code length get "exact" entries
+// (length field 63, length above it) -- k4w only
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
-                            uint32_t *__restrict__ lut, int ci_mode);
+                            uint32_t *__restrict__ lut, int mode);
 
 // decoder LUT: kLutSize entries + a header word (bit0: fast long-code path
 // valid, i.e. prefix-free code with max length <= 32)
