@@ -641,7 +641,7 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
             plan = _lib.Plan.from_buffer_copy(ctx.plan)
             n = x.numel()
             dims = tuple(x.shape) or (1,)
-            fits = (plan.status == 0 and plan.max_len <= 26 and plan.n_outliers <= k_cap
+            fits = (plan.status == 0 and plan.max_len <= 56 and plan.n_outliers <= k_cap
                     and plan.payload_bits <= 8 * (cap - 32))
             if fits:
                 k = plan.n_outliers

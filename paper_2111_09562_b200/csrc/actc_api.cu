@@ -549,7 +549,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
   }
   static const bool k3_two_pass = getenv("ACTC_K3_TWO_PASS") != nullptr;
   static const bool k3_lb = getenv("ACTC_K3_LB") != nullptr;
-  if (!wide && !k3_two_pass) {
+  if (!k3_two_pass && (!wide || !k3_lb)) {
     uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
     if (span > K3L_WIN) {
       uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
@@ -580,11 +580,12 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
       g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
       g.ncta = (uint32_t)cdiv(nseg, g.spc);
-      if ((rc = grow(c->status, nseg * 8 + (size_t)g.ncta * 16 + 1024))) return rc;
+      if ((rc = grow(c->status, nseg * 9 + (size_t)g.ncta * 16 + 1024))) return rc;
       g.cta_bits = (unsigned long long *)c->status.p;
       g.cta_nz = g.cta_bits + g.ncta;
       g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
       g.seg_nz = g.seg_bits + nseg;
+      g.seg_long = (uint8_t *)(g.seg_nz + nseg);
       g.x = x;
       g.payload = (uint32_t *)payload;
       g.out_idx = (unsigned long long *)out_idx;
@@ -761,11 +762,12 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
   g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
   g.ncta = (uint32_t)cdiv(nseg, g.spc);
-  if ((rc = grow(c->status, nseg * 8 + (size_t)g.ncta * 16 + 1024))) return rc;
+  if ((rc = grow(c->status, nseg * 9 + (size_t)g.ncta * 16 + 1024))) return rc;
   g.cta_bits = (unsigned long long *)c->status.p;
   g.cta_nz = g.cta_bits + g.ncta;
   g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
   g.seg_nz = g.seg_bits + nseg;
+  g.seg_long = (uint8_t *)(g.seg_nz + nseg);
   g.x = x;
   g.payload = (uint32_t *)payload;
   g.out_idx = (unsigned long long *)out_idx;

@@ -349,11 +349,15 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
     const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
     uint32_t s[K3L_EPT];
     lb_load(sym, base, a.n, s);
-    uint32_t bits = 0, nz = 0;
+    uint32_t bits = 0, nz = 0, mx = 0;
     if (smem_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
       // full segment, byte table in shared memory: one LDS.U8 per symbol
 #pragma unroll
-      for (int j = 0; j < K3L_EPT; j++) bits += k3c_ldsb(l8_rel + s[j]);
+      for (int j = 0; j < K3L_EPT; j++) {
+        const uint32_t l = k3c_ldsb(l8_rel + s[j]);
+        bits += l;
+        mx = max(mx, l);
+      }
       if (a.k) {
 #pragma unroll
         for (int j = 0; j < K3L_EPT; j++) nz += s[j] == 0;
@@ -362,14 +366,18 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
         if (s[j] != kSent) {
-          bits += smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
+          const uint32_t l = smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
+          bits += l;
+          mx = max(mx, l);
           nz += s[j] == 0;
         }
       }
     }
     bits = warp_sum(bits);
     if (a.k || !__all_sync(0xffffffffu, nz == 0)) nz = warp_sum(nz);
+    mx = __reduce_max_sync(0xffffffffu, mx);
     if (lane == 0) {
+      a.seg_long[seg] = mx > (uint32_t)K3_SHORT_MAXLEN;  // the pack takes its u64 path
       a.seg_bits[seg] = bits;
       a.seg_nz[seg] = nz;
       tb += bits;
@@ -460,6 +468,50 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
     lb_load(sym, base, a.n, s);
     const uint64_t r = seg / a.spc;
     const unsigned long long pb = a.cta_bits[r] + a.seg_bits[seg], pz = a.cta_nz[r] + a.seg_nz[seg];
+    if (a.seg_long[seg]) {
+      // rare: a code longer than 26 bits in this segment.  u64 (code, len)
+      // entries from the global table, every word OR-ed straight into the
+      // (zeroed) payload, codes fed in <= 32-bit chunks.
+      uint32_t bits = 0, zm = 0;
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] != kSent) bits += (uint32_t)(__ldg(&a.ctab[s[j]]) & 0xFF);
+        zm |= (uint32_t)(s[j] == 0) << j;
+      }
+      const uint32_t nzl = __popc(zm);
+      const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nzl);
+      const uint32_t lane_ex = ib - bits;
+      if (((lane * K3L_EPT) % ACTC_CHUNK) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;
+      if (a.extract && nzl) {
+        unsigned long long o = pz + (iz - nzl);
+        for (uint32_t m = zm; m; m &= m - 1) {
+          const uint64_t e_idx = base + (uint32_t)(__ffs(m) - 1);
+          a.out_idx[o] = e_idx;
+          a.out_val[o] = a.x[e_idx];
+          o++;
+        }
+      }
+      unsigned long long P = pb + lane_ex;
+#pragma unroll 1
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] == kSent) continue;
+        const unsigned long long g = __ldg(&a.ctab[s[j]]);
+        const unsigned long long code = g >> 8;
+        int len = (int)(g & 0xFF);
+        while (len > 0) {
+          const int c = len > 32 ? 32 : len;
+          const uint32_t chunk = (uint32_t)((code >> (len - c)) & ((1ull << c) - 1));
+          const uint32_t off = (uint32_t)(P & 31);
+          const unsigned long long v = (unsigned long long)chunk << (64 - off - c);
+          uint32_t *w = a.payload + (P >> 5);
+          atomicOr(w, bswap32((uint32_t)(v >> 32)));
+          if (off + c > 32) atomicOr(w + 1, bswap32((uint32_t)v));
+          P += c;
+          len -= c;
+        }
+      }
+      continue;
+    }
     // one (code << 6 | len) lookup per symbol
     uint32_t e[K3L_EPT];
     uint32_t zmask = 0;

@@ -142,6 +142,7 @@ struct SegArgs {
   uint32_t win_lo, win_n;          // (code, len) window for the pack pass
   uint64_t spc;                    // segments per count CTA
   uint32_t *seg_bits, *seg_nz;     // [nseg]
+  uint8_t *seg_long;               // [nseg] segment holds a code longer than K3_SHORT_MAXLEN
   unsigned long long *cta_bits, *cta_nz;  // [ncta] totals, then exclusive prefixes (in place)
   uint32_t ncta;
   const float *x;
@@ -165,7 +166,7 @@ struct SegArgs {
 __device__ __forceinline__ bool seg_resolve(SegArgs &a) {
   if (!a.dplan) return true;
   const actc_plan_t &p = *a.dplan;
-  if (p.status != ACTC_OK || p.max_len > (uint32_t)K3_SHORT_MAXLEN || p.payload_bits > a.cap_bits ||
+  if (p.status != ACTC_OK || p.max_len > 56u || p.payload_bits > a.cap_bits ||
       p.n_outliers > a.k_cap)
     return false;
   const uint32_t lo = p.sym_lo, hi = p.sym_hi;

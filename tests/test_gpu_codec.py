@@ -251,3 +251,36 @@ def test_compress_batch_compact(oracle):
     for o, x, p in zip(outs, xs, ps):
         want = oracle.decompress_blob(oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob, x.numel())
         assert np.array_equal(o.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+
+
+def _fibonacci_deltas(rng, depth):
+    """integer-valued signal whose Lorenzo deltas 0, 1, -1, 2, -2, ... occur
+    with Fibonacci counts: a Huffman tree ~depth levels deep, its longest
+    codes (> 26 bits) confined to a few segments"""
+    fib = [1, 1]
+    while len(fib) < depth:
+        fib.append(fib[-1] + fib[-2])
+    vals = [((i + 1) // 2) * (1 if i % 2 else -1) for i in range(depth)]
+    d = np.repeat(np.array(vals, dtype=np.int64), fib[::-1])
+    rng.shuffle(d)
+    return np.cumsum(d).astype(np.float32)  # eb = 0.5: x / (2 eb) is exact
+
+
+@pytest.mark.parametrize("depth", [29, 33])
+def test_long_codes_bit_exact(oracle, depth):
+    """codes longer than 26 bits take the segment encoder's u64 path (single
+    and batched compress) and the decoders' long-code entries"""
+    x = _fibonacci_deltas(np.random.default_rng(depth), depth)
+    p = pb.CodecParams(eb=0.5)
+    ref = oracle.compress(x, p.eb, debug=False)
+    c, rep = pb.compress(pb.Tensor(x), p)
+    assert 26 < int(c.code_lengths.max()) <= 56
+    assert c.to_bytes() == ref.blob
+    assert rep.ratio == ref.ratio
+    xt = torch.from_numpy(x).cuda()
+    (cb, _), = pb.compress_batch([xt], [p])
+    assert cb.to_bytes() == ref.blob
+    want = oracle.decompress_blob(ref.blob, x.size)
+    for cc in (c, cb, pc.CompressedActivation.from_bytes(ref.blob)):
+        out, _ = pb.decompress_device(cc, dtype=torch.float64)
+        assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
