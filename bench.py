@@ -36,8 +36,8 @@ sys.path.insert(0, ROOT)
 METRIC = "activation compress+decompress GB/s/GPU vs HBM peak; compression ratio; images/s"
 
 
-KERNEL_NAMES = {"quant": "k1_quant_lorenzo_hist", "codebook": "k2r_codebook + k2s_emit", "count": "k3_seg_count",
-                "scan": "k3_cta_scan", "pack": "k3_seg_pack", "fixup": "k3_fixup", "lut": "k_build_lut(8)",
+KERNEL_NAMES = {"quant": "k1_quant_lorenzo_hist", "codebook": "k2r_codebook + k2s_emit", "count": "k3_seg_count (+ CTA-total scan in its last CTA)",
+                "scan": "k_excl_scan_u64 (non-default encoders)", "pack": "k3_seg_pack", "fixup": "k3_fixup", "lut": "k_build_lut(8)",
                 "decode": "k4w_decode (<= 24K live symbols) / k4x_decode"}
 
 

@@ -150,9 +150,22 @@ int actc_compress_async(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb
  * (codec.py:275-293), recon/splice/re-zero (codec.py:364-368).
  * out_dtype ACTC_DTYPE_F64 is bit-identical to the reference's fp64
  * output; ACTC_DTYPE_F32 stores fp32(that value).  result_host is pinned
- * host memory written asynchronously. */
+ * host memory written asynchronously.  out_dtype may carry
+ * ACTC_DEC_LUT_ONLY (build only the decode table into ctx) or ACTC_DEC_REST
+ * (launch only the decoder, after a LUT_ONLY call with the same ctx, stream
+ * and actc_stream_t): a batch puts every table build on the GPU before any
+ * decoder fills it. */
+#define ACTC_DEC_LUT_ONLY 0x100
+#define ACTC_DEC_REST 0x200
 int actc_decompress(actc_ctx *ctx, const actc_stream_t *stream, void *out_dev,
                     int out_dtype, actc_decode_result_t *result_host, actc_stream s);
+
+/* zlib.crc32(data, crc_in) of a device buffer -- the CMTZ checksum
+ * (codec.py:118 writes it over every preceding byte, codec.py:126 checks it).
+ * A running value continues a checksum begun elsewhere (the host-built
+ * header), exactly as zlib.crc32's second argument.  Synchronizes. */
+int actc_crc32(actc_ctx *ctx, const void *data_dev, uint64_t len, uint32_t crc_in,
+               uint32_t *crc_out_host, actc_stream s);
 
 /* Build the canonical code table from a per-symbol length table (the
  * form CMTZ stores, codec.py:164) -- used after from_bytes
@@ -227,7 +240,8 @@ enum {
   ACTC_KIND_INDEX = 8,    /* chunk-index rebuild (from_bytes streams) */
   ACTC_KIND_STATS = 9,    /* K5 statistics */
   ACTC_KIND_DEBUG = 10,   /* conformance entry points */
-  ACTC_KIND_NKINDS = 11
+  ACTC_KIND_CRC = 11,     /* K6 CRC-32 */
+  ACTC_KIND_NKINDS = 12
 };
 int actc_timing_enable(int on);
 int actc_kernel_stats(uint64_t *launches, double *ms, int nkinds);

@@ -19,6 +19,8 @@ ACTC_OK, ACTC_EPARAM, ACTC_EDATA, ACTC_EFORMAT, ACTC_ENOMEM, ACTC_ECUDA = range(
 ACTC_FLAG_PRESERVE_ZEROS = 1
 ACTC_ASYNC_K1_ONLY = 0x100
 ACTC_ASYNC_REST = 0x200
+ACTC_DEC_LUT_ONLY = 0x100
+ACTC_DEC_REST = 0x200
 ACTC_DTYPE_F32, ACTC_DTYPE_F64 = 0, 1
 ACTC_CHUNK = 128
 
@@ -97,6 +99,7 @@ def lib():
             "actc_decompress": ([P, P, P, I, P, P], I),
             "actc_codebook_from_lengths": ([P, P, U64, P, P, P, P], I),
             "actc_build_chunk_index": ([P, P, P, P, P], I),
+            "actc_crc32": ([P, P, U64, U32, P, P], I),
             "actc_prequantize": ([P, I, U64, D, P, P], I),
             "actc_lorenzo_encode": ([P, U64, U32, P, P, P, P], I),
             "actc_lorenzo_decode": ([P, U64, P, U64, U32, P, P, P], I),
@@ -123,11 +126,11 @@ EXPORTED_SYMBOLS = (
     "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
-    "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats"
+    "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats actc_crc32"
 ).split()
 
 # instrumentation kinds (include/actc.h ACTC_KIND_*)
-KERNEL_KINDS = ("quant", "codebook", "count", "scan", "pack", "fixup", "lut", "decode", "index", "stats", "debug")
+KERNEL_KINDS = ("quant", "codebook", "count", "scan", "pack", "fixup", "lut", "decode", "index", "stats", "debug", "crc")
 
 
 def timing_enable(on: bool = True):
@@ -158,6 +161,14 @@ def raise_for(rc: int, default_msg: str = ""):
     if rc == ACTC_ENOMEM:
         raise MemoryError(msg)
     raise RuntimeError(f"CUDA error in libactc: {msg}")
+
+
+def cuda_available() -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return torch.cuda.is_available()
 
 
 def torch_cuda():

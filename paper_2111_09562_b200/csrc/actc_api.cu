@@ -158,7 +158,7 @@ struct DecResult {
 struct actc_ctx {
   int device = 0;
   int num_sms = 148;
-  Buf sym, hist, cb, ctab, len8, canon, lencnt, status, misc, lut, idx, part;
+  Buf sym, hist, cb, ctab, len8, canon, lencnt, status, misc, lut, idx, part, crc, crc_copy;
   actc_plan_t *plan_dev = nullptr;
   DecResult *dres_dev = nullptr;
   // state carried from plan to encode
@@ -169,6 +169,10 @@ struct actc_ctx {
   // when set (actc_compress_async), the codebook writes the canonical table
   // straight into the caller's buffers instead of the ctx scratch
   uint32_t *canon_out = nullptr, *lencnt_out = nullptr;
+  // when set (actc_compress_async), the codebook leaves the canonical-code
+  // emission to the segment count pass that follows it
+  bool defer_emit = false;
+  EmitArgs emit{};
 };
 
 namespace {
@@ -205,7 +209,7 @@ CbLayout cb_layout(uint64_t A) {
 }
 
 // misc counters layout (u64 slots)
-enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SLOTS = 8 };
+enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SEGTICKET = 8, M_SLOTS = 9 };
 
 constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
@@ -268,7 +272,10 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
     KT(ACTC_KIND_CODEBOOK);
     k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
   }
-  if (a.gate) {
+  c->emit = EmitArgs{};
+  if (a.gate && c->defer_emit) {
+    c->emit = EmitArgs{a.fallback, a.rank_tab, a.len_counts, a.len8, a.plan, a.canon, a.ctab};
+  } else if (a.gate) {
     KT(ACTC_KIND_CODEBOOK);
     k2s_emit<<<K2_THREADS / 32, 32, 0, s>>>(a);
   }
@@ -447,7 +454,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
 void actc_ctx_destroy(actc_ctx *c) {
   if (!c) return;
   Buf *bufs[] = {&c->sym, &c->hist, &c->cb, &c->ctab, &c->len8, &c->canon, &c->lencnt,
-                 &c->status, &c->misc, &c->lut, &c->idx, &c->part};
+                 &c->status, &c->misc, &c->lut, &c->idx, &c->part, &c->crc, &c->crc_copy};
   for (Buf *b : bufs)
     if (b->p) cudaFree(b->p);
   cudaFree(c->plan_dev);
@@ -586,6 +593,7 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
       g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
       g.seg_nz = g.seg_bits + nseg;
       g.seg_long = (uint8_t *)(g.seg_nz + nseg);
+      g.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_SEGTICKET);
       g.x = x;
       g.payload = (uint32_t *)payload;
       g.out_idx = (unsigned long long *)out_idx;
@@ -602,10 +610,6 @@ static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, 
           k3_seg_count<uint16_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint16_t *)sym, g);
         else
           k3_seg_count<uint32_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint32_t *)sym, g);
-      }
-      {
-        KT(ACTC_KIND_SCAN);
-        k3_cta_scan<<<1, 1024, 0, s>>>(g);
       }
       {
         KT(ACTC_KIND_PACK);
@@ -734,8 +738,10 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   }
   c->canon_out = canon;
   c->lencnt_out = len_counts;
+  c->defer_emit = true;
   rc = launch_cb(c, s);
   c->canon_out = c->lencnt_out = nullptr;
+  c->defer_emit = false;
   if (rc) return rc;
   // K3 segment encoder planned on the device: live range / windows from the
   // device plan, shared-memory sizes and grids at their caps
@@ -768,6 +774,9 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
   g.seg_nz = g.seg_bits + nseg;
   g.seg_long = (uint8_t *)(g.seg_nz + nseg);
+  g.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_SEGTICKET);
+  g.emit = c->emit;  // the count pass emits the canonical codes
+  c->emit = EmitArgs{};
   g.x = x;
   g.payload = (uint32_t *)payload;
   g.out_idx = (unsigned long long *)out_idx;
@@ -784,10 +793,6 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
       k3_seg_count<uint32_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint32_t *)sym, g);
   }
   {
-    KT(ACTC_KIND_SCAN);
-    k3_cta_scan<<<1, 1024, 0, s>>>(g);
-  }
-  {
     KT(ACTC_KIND_PACK);
     if (sb == 2)
       k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, g);
@@ -800,8 +805,9 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   return ACTC_OK;
 }
 
+// phase: 0 = table + decoder, 1 = table only, 2 = decoder only (table built by a phase-1 call)
 static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int mode,
-                         actc_decode_result_t *res_host, cudaStream_t s) {
+                         actc_decode_result_t *res_host, cudaStream_t s, int phase = 0) {
   const actc_stream_t &S = *st_in;
   if (S.n == 0) return set_err(ACTC_EPARAM, "empty stream");
   if (!S.chunk_offsets_dev) return set_err(ACTC_EPARAM, "stream has no chunk index (call actc_build_chunk_index)");
@@ -820,12 +826,12 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   st.inc_v = (long long *)(b + o);
   const bool warp_dec = S.chunk_lat_dev || mode == 2;
   unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
-  if (!warp_dec) {  // look-back state of the scan decoder
+  if (!warp_dec && phase != 1) {  // look-back state of the scan decoder
     CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
     CK(cudaMemsetAsync(ticket, 0, 8, s));
   }
   // the result mailbox is only read back when the caller asks for it
-  if (res_host || !warp_dec) CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
+  if ((res_host || !warp_dec) && phase != 1) CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
   // decoder choice for indexed streams: the warp decoder with symbols
   // resolved in the decode chain while the canonical table fits its shared
   // cache; the lane decoder (sequential reconstruction, canonical indices
@@ -837,7 +843,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   if (force) kind = !strcmp(force, "k4w") ? 0 : !strcmp(force, "k4wci") ? 1 : 2;
   if (kind == 1 && !(sw16 && mode != 2)) kind = 0;
   const bool lane_dec = warp_dec && kind == 2;
-  {
+  if (phase != 2) {
     KT(ACTC_KIND_LUT);
     if (lane_dec)
       k_build_lut8<<<16, 256, 0, s>>>(S.len_counts_dev, (uint8_t *)c->lut.p);
@@ -846,6 +852,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
                                                  warp_dec ? ((kind == 1 ? 1 : 0) | 2) : 0);
   }
   CKL();
+  if (phase == 1) return ACTC_OK;
   DecodeArgs a;
   a.n = S.n;
   a.eb = S.eb;
@@ -913,11 +920,39 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
 
 int actc_decompress(actc_ctx *c, const actc_stream_t *stream, void *out, int out_dtype,
                     actc_decode_result_t *result_host, actc_stream s) {
+  const int phase = (out_dtype & ACTC_DEC_LUT_ONLY) ? 1 : (out_dtype & ACTC_DEC_REST) ? 2 : 0;
+  out_dtype &= ~(ACTC_DEC_LUT_ONLY | ACTC_DEC_REST);
   if (out_dtype != ACTC_DTYPE_F32 && out_dtype != ACTC_DTYPE_F64) return set_err(ACTC_EPARAM, "bad out dtype");
   if (!(stream->eb > 0 && isfinite(stream->eb)) || stream->radius < 2)
     return set_err(ACTC_EFORMAT, "invalid codec params in stream");
   if (2ull * stream->radius > kMaxAlphabet) return set_err(ACTC_EPARAM, "radius too large for the device decoder");
-  return launch_decode(c, stream, out, out_dtype == ACTC_DTYPE_F32 ? 0 : 1, result_host, (cudaStream_t)s);
+  return launch_decode(c, stream, out, out_dtype == ACTC_DTYPE_F32 ? 0 : 1, result_host, (cudaStream_t)s, phase);
+}
+
+int actc_crc32(actc_ctx *c, const void *data_dev, uint64_t len, uint32_t crc_in, uint32_t *crc_out_host,
+               actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (len && !data_dev) return set_err(ACTC_EPARAM, "null buffer");
+  const uint64_t nb = crc32_blocks(len);
+  int rc;
+  // [ticket][result][pad][per-CTA values]
+  if ((rc = grow(c->crc, 16 + 4 * nb))) return rc;
+  uint32_t *w = (uint32_t *)c->crc.p;
+  const uint8_t *src = (const uint8_t *)data_dev;
+  if (len && ((uintptr_t)src & 15u)) {  // the kernel loads 16-byte words
+    if ((rc = grow(c->crc_copy, len + 16))) return rc;
+    CK(cudaMemcpyAsync(c->crc_copy.p, src, len, cudaMemcpyDeviceToDevice, s));
+    src = (const uint8_t *)c->crc_copy.p;
+  }
+  CK(cudaMemsetAsync(w, 0, 4, s));
+  {
+    KT(ACTC_KIND_CRC);
+    if (crc32_launch(src, len, crc_in, w + 4, (unsigned *)w, w + 1, s))
+      return set_err(ACTC_ECUDA, "crc32 launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  CK(cudaMemcpyAsync(crc_out_host, w + 1, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return ACTC_OK;
 }
 
 int actc_codebook_from_lengths(actc_ctx *c, const uint16_t *lengths, uint64_t A, uint32_t *canon,

@@ -54,8 +54,8 @@ constexpr int kMaxLv = 64;
 constexpr int kMaxSide = 96;
 constexpr uint32_t kInf32 = 0xFFFFFFFFu;
 constexpr uint32_t kHot = 384;            // classes counted in per-warp counters
-constexpr int kNL = 32;                   // max distinct code lengths (symbol passes)
-constexpr int kTS = kNL + 2;              // per-thread length-counter stride (odd word count)
+constexpr int kNL = K2R_NL;               // max distinct code lengths (symbol passes)
+constexpr int kTS = K2R_TS;               // per-thread length-counter stride (odd word count)
 constexpr int kNS = 8;                    // max cut classes
 constexpr int kSS = kNS + 2;              // per-thread cut-class counter stride
 
@@ -900,49 +900,8 @@ __global__ void __launch_bounds__(32) k2s_emit(CodebookArgs a) {
   __shared__ uint16_t s_row[32 * kTS];
   __shared__ unsigned long long s_first[64];
   __shared__ uint32_t s_base[64];
-  const int lane = threadIdx.x;
-  const uint32_t t = blockIdx.x * 32 + lane;
-  if (lane == 0) {
-    unsigned long long code = 0;
-    uint32_t idx = 0;
-    for (int l = 0; l < 64; l++) {
-      code <<= 1;
-      s_first[l] = code;
-      s_base[l] = idx;
-      code += a.len_counts[l];
-      idx += a.len_counts[l];
-    }
-  }
-  uint32_t minlen = 64;
-  for (int l = 63; l >= 1; l--)
-    if (a.len_counts[l]) minlen = l;
-  {
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(a.rank_tab + (size_t)t * kTS);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(s_row + lane * kTS);
-#pragma unroll
-    for (int u = 0; u < kTS / 2; u++) dst[u] = src[u];
-  }
-  __syncwarp();
-  const uint32_t lo = a.plan->sym_lo, hi = a.plan->sym_hi;
-  const uint32_t p0 = lo & ~15u;
-  const uint32_t SEG = ((((hi + 1 - p0) + NT - 1) / NT) + 15) & ~15u;
-  const uint32_t q0 = p0 + t * SEG, q1 = min(hi + 1, q0 + SEG);
-  uint16_t *row = s_row + lane * kTS;
-  for (uint32_t c0 = q0; c0 < q1; c0 += 16) {
-    const uint4 lv = *reinterpret_cast<const uint4 *>(a.len8 + c0);
-    const uint32_t wv[4] = {lv.x, lv.y, lv.z, lv.w};
-#pragma unroll
-    for (int u = 0; u < 16; u++) {
-      const uint32_t s = c0 + u;
-      const uint32_t len = (wv[u >> 2] >> (8 * (u & 3))) & 0xFFu;
-      if (len && s < q1) {
-        const uint32_t ci = row[len - minlen];
-        row[len - minlen] = (uint16_t)(ci + 1);
-        a.canon[ci] = s;
-        if (len <= 56) a.ctab[s] = ((s_first[len] + (ci - s_base[len])) << 8) | len;
-      }
-    }
-  }
+  const EmitArgs e{a.fallback, a.rank_tab, a.len_counts, a.len8, a.plan, a.canon, a.ctab};
+  k2s_emit_warp(e, blockIdx.x, s_row, s_first, s_base);
 }
 
 }  // namespace actc

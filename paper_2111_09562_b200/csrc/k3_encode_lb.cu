@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(K3L_THREADS, 3) k3_encode_lb(
 //                 shared memory) and outlier markers; the CTA then turns its
 //                 segment counts into exclusive in-CTA prefixes and writes its
 //                 totals
-//   k3_cta_scan   one CTA: exclusive prefixes of the CTA totals (in place)
+//                 (the last count CTA turns the CTA totals into exclusive prefixes)
 //   k3_seg_pack   warp per segment at bit cta_prefix + in-CTA prefix: one
 //                 (code, len) lookup per symbol into registers, pack, store
 // Symbols are read twice (2 x 2 B), but no warp ever waits for another.
@@ -314,6 +314,21 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
     const uint64_t nw = (a.dplan->payload_bits + 31) / 32 + 2;
     for (uint64_t i = (uint64_t)blockIdx.x * K3L_THREADS + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * K3L_THREADS)
       a.payload[i] = 0u;
+    if (a.canon_src) {
+      // the table is in ctx scratch: copy it to the caller's buffers
+      const uint32_t live = a.dplan->live_symbols;
+      for (uint32_t i = blockIdx.x * K3L_THREADS + threadIdx.x; i < live; i += gridDim.x * K3L_THREADS)
+        a.canon_out[i] = a.canon_src[i];
+      if (blockIdx.x == 0 && threadIdx.x < 64) a.lencnt_out[threadIdx.x] = a.lencnt_src[threadIdx.x];
+    }
+  }
+  if (a.emit.rank_tab && threadIdx.x < 32 && !*a.emit.fallback) {
+    // the codebook's canonical-code emission (k2s_emit's work), warp 0 of
+    // the first CTAs: this pass reads only len8; the pack reads ctab
+    __shared__ uint16_t e_row[32 * K2R_TS];
+    __shared__ unsigned long long e_first[64];
+    __shared__ uint32_t e_base[64];
+    for (uint32_t wb = blockIdx.x; wb < K2_THREADS / 32; wb += gridDim.x) k2s_emit_warp(a.emit, wb, e_row, e_first, e_base);
   }
   const bool smem_tab = a.span <= K3S_L8MAX;
   uint32_t shift = 0;
@@ -400,29 +415,26 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
     runb += allb;
     runz += allz;
   }
+  // the last CTA to finish turns the per-CTA totals into exclusive prefixes
+  // (in place) -- no separate scan launch waiting for a free SM
+  __shared__ unsigned k3c_last;
   if (threadIdx.x == 0) {
     a.cta_bits[blockIdx.x] = runb;
     a.cta_nz[blockIdx.x] = runz;
+    __threadfence();
+    k3c_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
   }
-}
-
-// exclusive prefixes of the per-CTA totals, in place (one CTA of 1024)
-__global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
-  __shared__ unsigned long long wb[33], wz[33];
-  if (!seg_resolve(a)) return;
-  if (a.dplan && a.canon_src) {
-    // device-planned with the table in ctx scratch: copy it to the caller's buffers
-    const uint32_t live = a.dplan->live_symbols;
-    for (uint32_t i = threadIdx.x; i < live; i += 1024) a.canon_out[i] = a.canon_src[i];
-    if (threadIdx.x < 64) a.lencnt_out[threadIdx.x] = a.lencnt_src[threadIdx.x];
-  }
-  unsigned long long runb = 0, runz = 0;
-  for (uint32_t c0 = 0; c0 < a.ncta; c0 += 1024) {
+  __syncthreads();
+  if (!k3c_last) return;
+  __threadfence();
+  runb = runz = 0;
+  for (uint32_t c0 = 0; c0 < a.ncta; c0 += K3L_THREADS) {
     const uint32_t i = c0 + threadIdx.x;
-    const unsigned long long vb = i < a.ncta ? a.cta_bits[i] : 0ull, vz = i < a.ncta ? a.cta_nz[i] : 0ull;
+    const unsigned long long vb = i < a.ncta ? __ldcg(&a.cta_bits[i]) : 0ull;
+    const unsigned long long vz = i < a.ncta ? __ldcg(&a.cta_nz[i]) : 0ull;
     unsigned long long allb, allz;
-    const unsigned long long eb = block_excl_sum<unsigned long long>(vb, wb, &allb);
-    const unsigned long long ez = block_excl_sum<unsigned long long>(vz, wz, &allz);
+    const unsigned long long eb = block_excl_sum<unsigned long long>(vb, wsum_b, &allb);
+    const unsigned long long ez = block_excl_sum<unsigned long long>(vz, wsum_z, &allz);
     if (i < a.ncta) {
       a.cta_bits[i] = runb + eb;
       a.cta_nz[i] = runz + ez;
@@ -430,6 +442,7 @@ __global__ void __launch_bounds__(1024) k3_cta_scan(SegArgs a) {
     runb += allb;
     runz += allz;
   }
+  if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
 }
 
 __device__ __forceinline__ uint32_t k3_saddr(const void *p) {
@@ -492,7 +505,7 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
         }
       }
       unsigned long long P = pb + lane_ex;
-#pragma unroll 1
+#pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
         if (s[j] == kSent) continue;
         const unsigned long long g = __ldg(&a.ctab[s[j]]);

@@ -97,6 +97,72 @@ struct CodebookArgs {
 };
 __global__ void k2_codebook(CodebookArgs a);
 // K2r (frequency-class codebook) capacities; dynamic shared memory size
+constexpr int K2R_NL = 32;            // k2r: max distinct code lengths
+constexpr int K2R_TS = K2R_NL + 2;     // k2r: per-thread length-counter stride (u16, odd word count)
+
+// Canonical-code emission for the symbols of k2r's per-thread segments
+// (huffman.py:78-94 rule: code = first[len] + rank among the symbols of that
+// length in symbol order).  Thread t (0..K2_THREADS-1) replays k2r thread t's
+// segment from the starting ranks k2r left in rank_tab.  Run by k2s_emit, or
+// -- on the batched path -- folded into the first warps of k3_seg_count.
+struct EmitArgs {
+  const unsigned *fallback;  // nonzero: k2_codebook built the tables, nothing to emit
+  const uint16_t *rank_tab;  // [K2_THREADS][K2R_TS]; null = no emission pending
+  const uint32_t *len_counts;
+  const uint8_t *len8;
+  const actc_plan_t *plan;
+  uint32_t *canon;
+  unsigned long long *ctab;
+};
+// one warp emits k2r threads 32*wblk .. 32*wblk+31; s_row holds 32*K2R_TS u16
+__device__ __forceinline__ void k2s_emit_warp(const EmitArgs &e, uint32_t wblk, uint16_t *s_row,
+                                              unsigned long long *s_first, uint32_t *s_base) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t t = wblk * 32 + lane;
+  if (lane == 0) {
+    unsigned long long code = 0;
+    uint32_t idx = 0;
+    for (int l = 0; l < 64; l++) {
+      code <<= 1;
+      s_first[l] = code;
+      s_base[l] = idx;
+      code += e.len_counts[l];
+      idx += e.len_counts[l];
+    }
+  }
+  uint32_t minlen = 64;
+  for (int l = 63; l >= 1; l--)
+    if (e.len_counts[l]) minlen = l;
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(e.rank_tab + (size_t)t * K2R_TS);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(s_row + lane * K2R_TS);
+#pragma unroll
+    for (int u = 0; u < K2R_TS / 2; u++) dst[u] = src[u];
+  }
+  __syncwarp();
+  const uint32_t lo = e.plan->sym_lo, hi = e.plan->sym_hi;
+  const uint32_t p0 = lo & ~15u;
+  const uint32_t SEG = ((((hi + 1 - p0) + K2_THREADS - 1) / K2_THREADS) + 15) & ~15u;
+  const uint32_t q0 = p0 + t * SEG, q1 = min(hi + 1, q0 + SEG);
+  uint16_t *row = s_row + lane * K2R_TS;
+  for (uint32_t c0 = q0; c0 < q1; c0 += 16) {
+    const uint4 lv = *reinterpret_cast<const uint4 *>(e.len8 + c0);
+    const uint32_t wv[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t s = c0 + u;
+      const uint32_t len = (wv[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+      if (len && s < q1) {
+        const uint32_t ci = row[len - minlen];
+        row[len - minlen] = (uint16_t)(ci + 1);
+        e.canon[ci] = s;
+        if (len <= 56) e.ctab[s] = ((s_first[len] + (ci - s_base[len])) << 8) | len;
+      }
+    }
+  }
+  __syncwarp();
+}
+
 constexpr uint32_t kRCap = 6144;
 constexpr uint32_t kICap = 11264;
 constexpr size_t kK2rSmem = (size_t)(3 * (kRCap + 1) + 3 * (kICap + 1)) * 4;
@@ -145,6 +211,7 @@ struct SegArgs {
   uint8_t *seg_long;               // [nseg] segment holds a code longer than K3_SHORT_MAXLEN
   unsigned long long *cta_bits, *cta_nz;  // [ncta] totals, then exclusive prefixes (in place)
   uint32_t ncta;
+  unsigned *ticket;                // count CTAs done (zero before the launch; the last CTA resets it)
   const float *x;
   uint32_t *payload;
   unsigned long long *out_idx;
@@ -161,6 +228,7 @@ struct SegArgs {
   uint64_t cap_bits, k_cap;
   const uint32_t *canon_src, *lencnt_src;
   uint32_t *canon_out, *lencnt_out;
+  EmitArgs emit;  // deferred k2s emission (rank_tab null: none)
 };
 // resolve a device-planned SegArgs; false = this stream takes the host path
 __device__ __forceinline__ bool seg_resolve(SegArgs &a) {
@@ -187,7 +255,6 @@ __device__ __forceinline__ bool seg_resolve(SegArgs &a) {
 }
 template <typename SymT>
 __global__ void k3_seg_count(const SymT *__restrict__ sym, SegArgs a);
-__global__ void k3_cta_scan(SegArgs a);
 template <typename SymT>
 __global__ void k3_seg_pack(const SymT *__restrict__ sym, SegArgs a);
 __global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
@@ -272,5 +339,10 @@ __global__ void k_sample_max(const void *__restrict__ g, int dtype, uint64_t N, 
                              unsigned long long *__restrict__ bits);
 __global__ void k_lbar_finish(const unsigned long long *__restrict__ bits, int dtype, uint64_t N,
                               void *__restrict__ per_sample_max, double *__restrict__ out);
+
+// K6 CRC-32 (k6_crc.cu)
+uint64_t crc32_blocks(uint64_t len);
+int crc32_launch(const uint8_t *data, uint64_t len, uint32_t crc_in, uint32_t *part, unsigned *ticket,
+                 uint32_t *out_dev, cudaStream_t s);
 
 }  // namespace actc
