@@ -13,7 +13,7 @@ import threading
 from .errors import DataError, FormatError, ParameterError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libactc.so")
+LIB_PATH = os.environ.get("ACTC_LIB_PATH") or os.path.join(HERE, "libactc.so")  # override: A/B builds
 
 ACTC_OK, ACTC_EPARAM, ACTC_EDATA, ACTC_EFORMAT, ACTC_ENOMEM, ACTC_ECUDA = range(6)
 ACTC_FLAG_PRESERVE_ZEROS = 1

@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
     return ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]);
   };
   const uint32_t zmark = CIR ? zci : 0u;
+  const uint32_t ncm1 = ncache ? ncache - 1 : 0u;
   unsigned long long nonzero = 0, markers = 0;
   bool bad = false;
 
@@ -214,50 +215,61 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
     }                                                                                             \
     const uint32_t W = (uint32_t)(buf >> 32);                                                     \
     const uint32_t e = lds_u32(lut_s + ((W >> (32 - kLutBits)) << 2));                            \
-    int len = (int)(e & 63);                                                                      \
-    uint32_t sv = e >> 6;                                                                         \
-    if (len == 63) {                                                                              \
-      /* long code, one length behind this prefix: canonical index directly */                    \
-      const uint32_t ci = lds_u32(off_s + 4u * sv) + (W >> (32 - sv));                            \
-      len = (int)sv;                                                                              \
-      sv = CIR ? ci : (ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]));              \
-    } else if (len == 0) {                                                                        \
-      /* long code (divergent): the LUT gives the shortest length l0 behind the prefix; */        \
-      /* three comparisons with the left-aligned canonical limits finish the length */           \
-      const uint32_t l0 = sv;                                                                     \
-      const uint32_t lb = lim_s + 4u * l0;                                                        \
-      const uint32_t l = l0 + (W > lds_u32(lb)) + (W > lds_u32(lb + 4u)) + (W > lds_u32(lb + 8u)); \
-      const bool ok = fast_long && l0 >= 1 && !(W > lds_u32(lb + 12u)) && (int)l <= maxlen;      \
-      if (ok) {                                                                                   \
-        const uint32_t ci = lds_u32(off_s + 4u * l) + (W >> (32 - l));                            \
-        sv = CIR ? ci : (ci < ncache ? lds_u16(cc_s + 2u * ci) : __ldg(&a.canon[ci]));            \
-        len = (int)l;                                                                             \
-      } else {                                                                                    \
-        /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */          \
-        const uint64_t pos = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;                     \
-        const uint64_t win = read_bits64(pw, pos);                                                \
-        len = 0;                                                                                  \
-        for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                         \
-          const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                  \
-          if (of < s_count[ll]) {                                                                 \
-            sv = CIR ? s_base[ll] + (uint32_t)of : a.canon[s_base[ll] + of];                      \
-            len = ll;                                                                             \
-            break;                                                                                \
+    const uint32_t l6 = e & 63u, hv = e >> 6;                                                     \
+    const bool lng = l6 == 63u;                                                                   \
+    /* a long code behind an exact-length prefix resolves without a branch: every lane */         \
+    /* forms the canonical index (with a dummy length 1 for short codes) and reads the */         \
+    /* symbol cache, so the warp never splits on the common long codes */                         \
+    const uint32_t lc = lng ? hv : 1u;                                                            \
+    const uint32_t ci = lds_u32(off_s + 4u * lc) + (W >> (32 - lc));                              \
+    int len = lng ? (int)hv : (int)l6;                                                            \
+    uint32_t sv;                                                                                  \
+    if (CIR) {                                                                                    \
+      sv = lng ? ci : hv;                                                                         \
+    } else {                                                                                      \
+      const uint32_t sl = lds_u16(cc_s + 2u * min(ci, ncm1));                                     \
+      sv = lng ? sl : hv;                                                                         \
+    }                                                                                             \
+    if (__any_sync(__activemask(), l6 == 0u || (!CIR && lng && ci >= ncache))) {                  \
+      if (!CIR && lng && ci >= ncache) sv = __ldg(&a.canon[ci]);                                  \
+      if (l6 == 0u) {                                                                             \
+        /* long code behind a mixed prefix: the LUT gives the shortest length l0; */              \
+        /* three comparisons with the left-aligned canonical limits finish it */                  \
+        const uint32_t l0 = hv;                                                                   \
+        const uint32_t lb = lim_s + 4u * l0;                                                      \
+        const uint32_t l = l0 + (W > lds_u32(lb)) + (W > lds_u32(lb + 4u)) + (W > lds_u32(lb + 8u)); \
+        const bool ok = fast_long && l0 >= 1 && !(W > lds_u32(lb + 12u)) && (int)l <= maxlen;    \
+        if (ok) {                                                                                 \
+          const uint32_t cj = lds_u32(off_s + 4u * l) + (W >> (32 - l));                         \
+          sv = CIR ? cj : (cj < ncache ? lds_u16(cc_s + 2u * cj) : __ldg(&a.canon[cj]));          \
+          len = (int)l;                                                                           \
+        } else {                                                                                  \
+          /* rare: longer than l0+3, over-subscribed table, codes > 32 bits, or invalid */        \
+          const uint64_t pos = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;                   \
+          const uint64_t win = read_bits64(pw, pos);                                              \
+          len = 0;                                                                                \
+          for (int ll = kLutBits + 1; ll <= maxlen; ll++) {                                       \
+            const unsigned long long cd = win >> (64 - ll), of = cd - s_first[ll];                \
+            if (of < s_count[ll]) {                                                               \
+              sv = CIR ? s_base[ll] + (uint32_t)of : a.canon[s_base[ll] + of];                    \
+              len = ll;                                                                           \
+              break;                                                                              \
+            }                                                                                     \
           }                                                                                       \
+          if (!len) {                                                                             \
+            bad = true;                                                                           \
+            len = 1;                                                                              \
+            sv = CIR ? 0u : a.radius;                                                             \
+          }                                                                                       \
+          const uint64_t np = pos + len;                                                          \
+          src = pw + (np >> 5);                                                                   \
+          buf = ((unsigned long long)bswap32(src[0]) << 32) | bswap32(src[1]);                    \
+          buf <<= (np & 31);                                                                      \
+          nb = 64 - (int)(np & 31);                                                               \
+          nextw = src[2];                                                                         \
+          src += 3;                                                                               \
+          len = 0;                                                                                \
         }                                                                                         \
-        if (!len) {                                                                               \
-          bad = true;                                                                             \
-          len = 1;                                                                                \
-          sv = CIR ? 0u : a.radius;                                                               \
-        }                                                                                         \
-        const uint64_t np = pos + len;                                                            \
-        src = pw + (np >> 5);                                                                     \
-        buf = ((unsigned long long)bswap32(src[0]) << 32) | bswap32(src[1]);                      \
-        buf <<= (np & 31);                                                                        \
-        nb = 64 - (int)(np & 31);                                                                 \
-        nextw = src[2];                                                                           \
-        src += 3;                                                                                 \
-        len = 0;                                                                                  \
       }                                                                                           \
     }                                                                                             \
     buf <<= len;                                                                                  \
