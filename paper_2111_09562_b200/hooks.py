@@ -34,7 +34,7 @@ from dataclasses import dataclass, field
 
 from . import _lib
 from .codec import DEFAULT_RADIUS, CodecParams, compress_batch, decompress_device
-from .controller import AdaptiveController, ControllerConfig, LayerTrainingStats
+from .controller import AdaptiveController, ControllerConfig, LayerTrainingStats, choose_batch_size
 from .errors import LifecycleError, ParameterError
 
 
@@ -122,7 +122,7 @@ class ActivationCompressor:
 
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 8, dist_group=None,
-                 sync_stats: bool = True):
+                 sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None):
         self.layers = dict(layers)
         self._model = getattr(layers, "model", None)
         self.optimizer = optimizer
@@ -150,6 +150,17 @@ class ActivationCompressor:
         self._rec = None
         self._hooks = []
         self._bwd_hooks = []
+        # memory-budget batch planner (reference training.py:401-426): per-
+        # sample bytes of each stored activation, the ratios observed in the
+        # current interval, the model's fixed bytes (weights + velocity)
+        self.input_sample_bytes = input_sample_bytes
+        if fixed_bytes is None:
+            fixed_bytes = 2.0 * sum(p.numel() * p.element_size()
+                                    for g in optimizer.param_groups for p in g["params"])
+        self.fixed_bytes = float(fixed_bytes)
+        self.batch_size = None  # recommended batch (choose_batch_size), once planned
+        self._per_sample: dict[str, float] = {}
+        self._interval_ratios: dict[str, list] = {lid: [] for lid in self.layers}
         for lid, (prod, cons) in self.layers.items():
             self._hooks.append(prod.register_forward_hook(self._fwd_hook(lid)))
 
@@ -227,6 +238,8 @@ class ActivationCompressor:
         h = _Handle(t, lid, eb)
         self._handles[k] = h
         nbytes = t.numel() * 4
+        if self._batch:
+            self._per_sample[lid] = nbytes / self._batch
         if self._rec is not None:
             self._rec.raw_bytes += nbytes
         if eb is None:
@@ -251,6 +264,7 @@ class ActivationCompressor:
             h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
             self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
             self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
+            self._interval_ratios.setdefault(h.layer, []).append(rep.ratio)
             if self._rec is not None:
                 self._rec.stored_bytes += rep.compressed_bytes
                 self._rec.compressed[h.layer] = (rep.ratio, h.eb)
@@ -298,6 +312,7 @@ class ActivationCompressor:
         self._R.clear()
         self._lbar.clear()
         self.store.clear()
+        self.store.peak_bytes = 0
         self._rec = IterationRecord(self.it)
         # the consumers' output-gradient hooks (L_bar) exist only in collection
         # iterations: full backward hooks wrap every call of their module
@@ -331,12 +346,40 @@ class ActivationCompressor:
     def after_step(self):
         """Call after optimizer.step(): interval boundary -> new plan."""
         self.records.append(self._rec)
+        budget = self.config.memory_budget_bytes
         if self._collecting:
             self.plan = self.controller.new_interval(self._collect_stats())
             self.next_collection = (self.it + 1) + self.plan.W
+            if budget is not None and self.controller.intervals_planned >= 2:
+                self.batch_size = self.plan_batch_size()
+            self._interval_ratios = {lid: [] for lid in self.layers}
+        if budget is not None and (self.store.peak_bytes + self.fixed_bytes
+                                   > budget * (1.0 - self.config.reserve_fraction)):
+            self.controller.note_reserve_breach()  # training.py:420-426
         self.it += 1
         self._collecting = False
         return self.plan
+
+    def plan_batch_size(self) -> int:
+        """Largest power-of-two batch whose projected activation bytes (per-
+        sample cost / observed ratio per layer, plus the input) and the
+        model's fixed bytes fit the memory budget minus the reserve
+        (controller.choose_batch_size; reference training.py:401-416)."""
+        costs = {}
+        if self.input_sample_bytes:
+            costs["input"] = float(self.input_sample_bytes)
+        ratios = {}
+        for lid in self.layers:
+            if lid in self._per_sample:
+                costs[lid] = self._per_sample[lid]
+            r = self._interval_ratios.get(lid)
+            if r:
+                ratios[lid] = sum(r) / len(r)
+        return choose_batch_size(costs, ratios, self.config, fixed_bytes=self.fixed_bytes)
+
+    @property
+    def reserve_breaches(self) -> int:
+        return self.controller.reserve_breach_count
 
     def _collect_stats(self):
         from .tensor import mean_abs
@@ -355,6 +398,15 @@ class ActivationCompressor:
             R, Lb, M = sync_layer_stats(R, Lb, M, self.dist_group)
         return [LayerTrainingStats(layer_id=l, R=min(1.0, max(0.0, r)), L_bar=lb, M_avg=m, N=N)
                 for l, r, lb, m in zip(ids, R, Lb, M)]
+
+
+def device_memory_budget(device=None, headroom_bytes: int = 0) -> int:
+    """Bytes this process may plan against on `device`: what the allocator
+    already holds plus what the driver reports free (torch.cuda.mem_get_info),
+    minus a headroom -- a value for ControllerConfig.memory_budget_bytes."""
+    torch = _lib.torch_cuda()
+    free, _total = torch.cuda.mem_get_info(device)
+    return int(free + torch.cuda.memory_reserved(device) - headroom_bytes)
 
 
 def sync_layer_stats(R, L_bar, M_avg, group=None):

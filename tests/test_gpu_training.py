@@ -19,13 +19,14 @@ def _net():
                          nn.Flatten(), nn.Linear(64 * 8 * 8, 10)).cuda()
 
 
-def _run(compress, iters=8):
+def _run(compress, iters=8, budget=None):
     net = _net()
     opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
     comp = None
     if compress:
         comp = ActivationCompressor(ActivationCompressor.conv_layer_map(net), opt,
-                                    pb.ControllerConfig(W_default=2, W_floor=1))
+                                    pb.ControllerConfig(W_default=2, W_floor=1, memory_budget_bytes=budget),
+                                    input_sample_bytes=3 * 32 * 32 * 4)
     g = torch.Generator(device="cuda").manual_seed(1)
     losses = []
     for it in range(iters):
@@ -69,3 +70,21 @@ def test_hooks_handle_shared_saved_tensors():
     # ReLU output saved by both relu backward and maxpool -> compressed once, unpacked twice
     net, comp, _ = _run(True, iters=5)
     assert comp.store.current_bytes == 0  # every slot consumed exactly once
+
+
+def test_memory_budget_batch_planner_on_device():
+    """with a budget, the compressor recommends a batch from the observed
+    ratios once two intervals are planned (training.py:401-416); a budget
+    below the stored bytes counts reserve breaches (:420-426)"""
+    from paper_2111_09562_b200.hooks import device_memory_budget
+
+    budget = device_memory_budget()
+    assert budget > 0
+    _, comp, _ = _run(True, iters=7, budget=budget)
+    assert comp.controller.intervals_planned >= 2 and comp.batch_size is not None
+    assert comp.batch_size >= 16 and comp.reserve_breaches == 0
+    # per-sample costs of the three stored activations, measured in the pack hook
+    assert set(comp._per_sample) == set(comp.layers)
+    tight = comp.fixed_bytes + 1  # fixed bytes alone fill the usable budget
+    _, comp2, _ = _run(True, iters=3, budget=int(tight / 0.95) + 1)
+    assert comp2.reserve_breaches >= 1

@@ -116,6 +116,36 @@ def test_conv_layer_map():
     assert m.model is net and net[1].inplace  # in-place ReLUs are switched off only while collecting
 
 
+def test_compressor_batch_planner_and_reserve_breaches():
+    """ActivationCompressor's memory-budget planner (reference training.py:
+    401-426): per-sample layer costs / interval ratios + fixed model bytes
+    -> choose_batch_size; store peak + fixed over the usable budget counts
+    a reserve breach."""
+    torch = pytest.importorskip("torch")
+    import torch.nn as nn
+
+    net = nn.Sequential(nn.Conv2d(3, 8, 3), nn.ReLU(), nn.Conv2d(8, 8, 3), nn.ReLU(), nn.Flatten(), nn.Linear(8, 4))
+    opt = torch.optim.SGD(net.parameters(), lr=0.1, momentum=0.9)
+    cfg = ctl.ControllerConfig(memory_budget_bytes=10 ** 6, reserve_fraction=0.1)
+    comp = ActivationCompressor(ActivationCompressor.conv_layer_map(net), opt, cfg, input_sample_bytes=3 * 32 * 32 * 4)
+    nparams = sum(p.numel() for p in net.parameters())
+    assert comp.fixed_bytes == 2 * 4 * nparams  # weights + velocity, fp32 (training.py:200)
+    comp._per_sample = {"0": 8 * 30 * 30 * 4.0, "2": 8 * 28 * 28 * 4.0}
+    comp._interval_ratios = {"0": [4.0, 6.0], "2": [8.0]}
+    want = ctl.choose_batch_size({"input": 3 * 32 * 32 * 4.0, "0": 8 * 30 * 30 * 4.0, "2": 8 * 28 * 28 * 4.0},
+                                 {"0": 5.0, "2": 8.0}, cfg, fixed_bytes=comp.fixed_bytes)
+    assert comp.plan_batch_size() == want
+    per_b = 3 * 32 * 32 * 4 + 8 * 30 * 30 * 4 / 5 + 8 * 28 * 28 * 4 / 8
+    assert want * per_b + comp.fixed_bytes <= 0.9 * 10 ** 6 < 2 * want * per_b + comp.fixed_bytes
+    # reserve breach accounting on after_step
+    comp._rec = None
+    comp.store.peak_bytes = 10 ** 6
+    comp.after_step()
+    comp.store.peak_bytes = 0
+    comp.after_step()
+    assert comp.reserve_breaches == 1 and comp.it == 2
+
+
 def _sync_worker(rank, world, port, q):
     import torch.distributed as dist
 
