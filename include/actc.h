@@ -222,6 +222,14 @@ int actc_mean_abs(actc_ctx *ctx, const void *x_dev, int dtype, uint64_t n, doubl
 int actc_lbar(actc_ctx *ctx, const void *g_dev, int dtype, uint64_t N, uint64_t per_sample,
               void *per_sample_max_dev, double *out_host, actc_stream s);
 
+/* inject_uniform_error (errorprop.py:127-139): out = f64(x) + U[-eb, eb]
+ * noise (zeros keep 0 noise when preserve_zeros), bit-identical to numpy's
+ * default_rng(seed).uniform draws.  pcg_state = {state_hi, state_lo, inc_hi,
+ * inc_lo}: the PCG64 state numpy derives from the seed (host SeedSequence).
+ * x is fp32 or fp64 (dtype), out is fp64[n]. */
+int actc_inject_uniform(actc_ctx *ctx, const void *x_dev, int dtype, uint64_t n, double eb,
+                        int preserve_zeros, const uint64_t *pcg_state, double *out_dev, actc_stream s);
+
 /* ---- instrumentation (not part of the reference interface) ----
  * Every kernel launch the library makes is counted per kind; with timing
  * enabled each launch is also bracketed by CUDA events recorded on the
@@ -241,7 +249,8 @@ enum {
   ACTC_KIND_STATS = 9,    /* K5 statistics */
   ACTC_KIND_DEBUG = 10,   /* conformance entry points */
   ACTC_KIND_CRC = 11,     /* K6 CRC-32 */
-  ACTC_KIND_NKINDS = 12
+  ACTC_KIND_INJECT = 12,  /* K7 uniform error injection */
+  ACTC_KIND_NKINDS = 13
 };
 int actc_timing_enable(int on);
 int actc_kernel_stats(uint64_t *launches, double *ms, int nkinds);

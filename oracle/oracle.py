@@ -212,3 +212,15 @@ def lbar(g):
         return lib().orc_lbar_f32(_p(g), N, per)
     g = np.ascontiguousarray(g, dtype=np.float64)
     return lib().orc_lbar_f64(_p(g), N, per)
+
+
+def inject_uniform_error(x, eb, preserve_zeros=True, seed=0):
+    """errorprop.py:127-139 restated: numpy default_rng(seed) (PCG64) draws
+    U[-eb, eb] noise for every element, zeroed where the input is 0 when
+    preserve_zeros; returns f64(x) + noise (flat fp64)."""
+    rng = np.random.default_rng(seed)
+    data = np.asarray(x).astype(np.float64).reshape(-1)
+    noise = rng.uniform(-eb, eb, size=data.size)
+    if preserve_zeros:
+        noise[data == 0.0] = 0.0
+    return data + noise

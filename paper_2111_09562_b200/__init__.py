@@ -43,6 +43,7 @@ from .errors import (
     ParameterError,
     SchemaError,
 )
+from .errorprop import inject_uniform_error
 from .tensor import Tensor, TensorStats, compute_stats, make_tensor
 
 __version__ = "0.1.0"

@@ -347,6 +347,7 @@ int actc_debug_timeline(double *out, int cap) {
       n++;
     }
   }
+  cudaGetLastError();
   {
     std::lock_guard<std::mutex> g(g_tmu);
     for (const KRec &r : recs) {
@@ -354,7 +355,6 @@ int actc_debug_timeline(double *out, int cap) {
       g_pool.push_back(r.b);
     }
   }
-  cudaGetLastError();
   return n;
 }
 
@@ -952,6 +952,19 @@ int actc_crc32(actc_ctx *c, const void *data_dev, uint64_t len, uint32_t crc_in,
   }
   CK(cudaMemcpyAsync(crc_out_host, w + 1, 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return ACTC_OK;
+}
+
+int actc_inject_uniform(actc_ctx *c, const void *x_dev, int dtype, uint64_t n, double eb, int preserve_zeros,
+                        const uint64_t *pcg_state, double *out_dev, actc_stream stream) {
+  (void)c;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(eb > 0.0) || !isfinite(eb)) return set_err(ACTC_EPARAM, "eb must be > 0 and finite");
+  if (dtype != ACTC_DTYPE_F32 && dtype != ACTC_DTYPE_F64) return set_err(ACTC_EPARAM, "bad dtype");
+  if (n && (!x_dev || !out_dev || !pcg_state)) return set_err(ACTC_EPARAM, "null buffer");
+  KT(ACTC_KIND_INJECT);
+  if (inject_launch(x_dev, dtype, n, eb, preserve_zeros, pcg_state, out_dev, s))
+    return set_err(ACTC_ECUDA, "inject launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return ACTC_OK;
 }
 

@@ -345,4 +345,8 @@ uint64_t crc32_blocks(uint64_t len);
 int crc32_launch(const uint8_t *data, uint64_t len, uint32_t crc_in, uint32_t *part, unsigned *ticket,
                  uint32_t *out_dev, cudaStream_t s);
 
+// K7 uniform error injection (k7_inject.cu); state = {st_hi, st_lo, inc_hi, inc_lo}
+int inject_launch(const void *x, int dtype, uint64_t n, double eb, int preserve, const uint64_t state[4],
+                  double *out, cudaStream_t s);
+
 }  // namespace actc

@@ -76,6 +76,22 @@ def _key(t):
     return (t.data_ptr(), t._version, tuple(t.shape), tuple(t.stride()))
 
 
+class _Marker:
+    """A cheap layer's saved output (pooling after a stored activation):
+    nothing is kept; unpack recomputes it from the stored predecessor
+    (reference MARKER slots, training.py:295-296, recompute_cheap :344-347)."""
+
+    __slots__ = ("slot", "mod", "src", "packs", "unpacks", "out")
+
+    def __init__(self, slot, mod, src):
+        self.slot = slot
+        self.mod = mod
+        self.src = src
+        self.packs = 1
+        self.unpacks = 0
+        self.out = None
+
+
 class _Handle:
     """One saved activation: raw until the pending queue is flushed."""
 
@@ -99,6 +115,7 @@ class IterationRecord:
     compressed: dict = field(default_factory=dict)  # layer -> (ratio, eb)
     stored_bytes: int = 0
     raw_bytes: int = 0
+    markers: int = 0  # cheap-layer outputs recomputed instead of stored
 
 
 class _LayerMap(dict):
@@ -122,7 +139,8 @@ class ActivationCompressor:
 
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 8, dist_group=None,
-                 sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None):
+                 sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
+                 recompute_cheap: bool = True):
         self.layers = dict(layers)
         self._model = getattr(layers, "model", None)
         self.optimizer = optimizer
@@ -163,6 +181,16 @@ class ActivationCompressor:
         self._interval_ratios: dict[str, list] = {lid: [] for lid in self.layers}
         for lid, (prod, cons) in self.layers.items():
             self._hooks.append(prod.register_forward_hook(self._fwd_hook(lid)))
+        # cheap layers (pooling) fed by a stored activation: their saved
+        # outputs become MARKER slots, recomputed in backward
+        self._cheap: dict = {}
+        self._markers: dict = {}
+        if recompute_cheap and self._model is not None:
+            import torch.nn as nn
+
+            for name, m in self._model.named_modules():
+                if isinstance(m, (nn.MaxPool2d, nn.AvgPool2d)):
+                    self._hooks.append(m.register_forward_hook(self._cheap_hook(name)))
 
     # ---- construction helpers -------------------------------------------
     @staticmethod
@@ -211,6 +239,14 @@ class ActivationCompressor:
             self._act_layer[_key(out)] = lid
         return hook
 
+    def _cheap_hook(self, name):
+        def hook(mod, inp, out):
+            if inp and hasattr(inp[0], "data_ptr") and hasattr(out, "data_ptr"):
+                k = _key(inp[0])
+                if k in self._act_layer:
+                    self._cheap[_key(out)] = (name, mod, k)
+        return hook
+
     def _bwd_hook(self, lid):
         def hook(mod, gin, gout):
             if self._collecting and gout and gout[0] is not None:
@@ -229,7 +265,21 @@ class ActivationCompressor:
         k = _key(t)
         lid = self._act_layer.get(k)
         if lid is None:
-            return ("raw", t)
+            cheap = self._cheap.get(k)
+            src = self._handles.get(cheap[2]) if cheap is not None else None
+            if src is None:
+                return ("raw", t)
+            m = self._markers.get(k)
+            if m is not None:
+                m.packs += 1
+                return m
+            m = _Marker(f"{cheap[0]}@{src.layer}", cheap[1], src)
+            src.packs += 1  # the recompute reads the predecessor once more
+            self._markers[k] = m
+            self.store.put(m.slot, ActivationStore.MARKER, None, 0)
+            if self._rec is not None:
+                self._rec.markers += 1
+            return m
         h = self._handles.get(k)
         if h is not None:
             h.packs += 1
@@ -274,6 +324,20 @@ class ActivationCompressor:
 
         if isinstance(h, tuple):
             return h[1]
+        if isinstance(h, _Marker):
+            if h.out is None:
+                if h.src is None:
+                    raise LifecycleError(f"marker {h.slot!r} already released")
+                x = self._unpack(h.src)
+                with torch.no_grad():
+                    h.out = h.mod(x)
+                self.store.pop(h.slot)
+                h.src = None
+            h.unpacks += 1
+            out = h.out
+            if h.unpacks >= h.packs:
+                h.out = None
+            return out
         if h.out is None:
             if h.comp is None and h.raw is None:
                 raise LifecycleError(f"activation of {h.layer!r} already released")
@@ -309,6 +373,8 @@ class ActivationCompressor:
         self._collecting = (self.it + 1) == self.next_collection
         self._act_layer.clear()
         self._handles.clear()
+        self._cheap.clear()
+        self._markers.clear()
         self._R.clear()
         self._lbar.clear()
         self.store.clear()
@@ -342,6 +408,8 @@ class ActivationCompressor:
                 m.inplace = True
         self._handles.clear()
         self._act_layer.clear()
+        self._cheap.clear()
+        self._markers.clear()
 
     def after_step(self):
         """Call after optimizer.step(): interval boundary -> new plan."""

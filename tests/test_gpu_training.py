@@ -70,6 +70,9 @@ def test_hooks_handle_shared_saved_tensors():
     # ReLU output saved by both relu backward and maxpool -> compressed once, unpacked twice
     net, comp, _ = _run(True, iters=5)
     assert comp.store.current_bytes == 0  # every slot consumed exactly once
+    # the two max-pools after stored ReLU outputs are MARKER slots (recomputed
+    # in backward from the decompressed ReLU output), every iteration
+    assert all(r.markers == 2 for r in comp.records)
 
 
 def test_memory_budget_batch_planner_on_device():

@@ -13,7 +13,7 @@ import bench  # noqa: E402
 import paper_2111_09562_b200 as pb  # noqa: E402
 from paper_2111_09562_b200 import _lib  # noqa: E402
 
-KIND = ["K1", "K2", "K3cnt", "scan", "K3pack", "fix", "lut", "K4dec", "idx", "stats", "dbg", "crc"]
+KIND = ["K1", "K2", "K3cnt", "scan", "K3pack", "fix", "lut", "K4dec", "idx", "stats", "dbg", "crc", "inject"]
 torch.cuda.set_device(0)
 ts, ebs, info, _ = bench.build_workload(sys.argv[1] if len(sys.argv) > 1 else "alexnet256", "cuda")
 ps = [pb.CodecParams(eb=e) for e in ebs]
