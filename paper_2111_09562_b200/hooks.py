@@ -30,6 +30,7 @@ planning, so every rank compresses with identical error bounds.
 from __future__ import annotations
 
 import contextlib
+import weakref
 from dataclasses import dataclass, field
 
 from . import _lib
@@ -81,21 +82,27 @@ class _Marker:
     nothing is kept; unpack recomputes it from the stored predecessor
     (reference MARKER slots, training.py:295-296, recompute_cheap :344-347)."""
 
-    __slots__ = ("slot", "mod", "src", "packs", "unpacks", "out")
+    __slots__ = ("slot", "mod", "src", "packs", "unpacks", "out", "ref")
 
-    def __init__(self, slot, mod, src):
+    def __init__(self, slot, mod, src, t):
         self.slot = slot
         self.mod = mod
         self.src = src
         self.packs = 1
         self.unpacks = 0
         self.out = None
+        self.ref = weakref.ref(t)
 
 
 class _Handle:
-    """One saved activation: raw until the pending queue is flushed."""
+    """One saved fp32 tensor.  Autograd saves a module's output while the op
+    runs, before the module's forward hook names it, so every saved tensor
+    gets a handle; the producer's forward hook then promotes the handle of
+    its output to a stored activation (layer set): raw until the pending
+    queue is flushed, compressed after.  Handles nobody promotes pass the
+    tensor through."""
 
-    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape")
+    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref")
 
     def __init__(self, t, layer, eb):
         self.layer = layer
@@ -107,6 +114,9 @@ class _Handle:
         self.unpacks = 0
         self.out = None
         self.shape = tuple(t.shape)
+        # the tensor's identity: a key (pointer, version, shape, stride) is
+        # only unique while the tensor lives -- freed memory is reused
+        self.ref = weakref.ref(t)
 
 
 @dataclass
@@ -236,16 +246,34 @@ class ActivationCompressor:
         def hook(mod, inp, out):
             if self._batch is None and inp and hasattr(inp[0], "shape"):
                 self._batch = int(inp[0].shape[0])
-            self._act_layer[_key(out)] = lid
+            if not hasattr(out, "data_ptr"):
+                return
+            k = _key(out)
+            self._act_layer[k] = (lid, weakref.ref(out))
+            h = self._live(self._handles, k)
+            if h is not None and h.layer is None:
+                self._promote(h, lid)  # saved by the op itself, before this hook
         return hook
 
     def _cheap_hook(self, name):
         def hook(mod, inp, out):
             if inp and hasattr(inp[0], "data_ptr") and hasattr(out, "data_ptr"):
-                k = _key(inp[0])
-                if k in self._act_layer:
-                    self._cheap[_key(out)] = (name, mod, k)
+                src = self._live(self._handles, _key(inp[0]))
+                if src is not None and src.layer is not None:
+                    self._cheap[_key(out)] = (name, mod, src, weakref.ref(out))
         return hook
+
+    @staticmethod
+    def _live(table, k):
+        """table[k] if the tensor it was registered for is still alive."""
+        e = table.get(k)
+        if e is None:
+            return None
+        ref = e[-1] if isinstance(e, tuple) else e.ref
+        if ref() is None:
+            del table[k]
+            return None
+        return e
 
     def _bwd_hook(self, lid):
         def hook(mod, gin, gout):
@@ -263,30 +291,37 @@ class ActivationCompressor:
         if not (t.is_cuda and t.dtype == torch.float32) or isinstance(t, torch.nn.Parameter):
             return ("raw", t)
         k = _key(t)
-        lid = self._act_layer.get(k)
-        if lid is None:
-            cheap = self._cheap.get(k)
-            src = self._handles.get(cheap[2]) if cheap is not None else None
-            if src is None:
-                return ("raw", t)
-            m = self._markers.get(k)
-            if m is not None:
-                m.packs += 1
-                return m
-            m = _Marker(f"{cheap[0]}@{src.layer}", cheap[1], src)
+        h = self._live(self._handles, k)
+        if h is not None:
+            h.packs += 1
+            return h
+        m = self._live(self._markers, k)
+        if m is not None:
+            m.packs += 1
+            return m
+        cheap = self._live(self._cheap, k)
+        if cheap is not None and cheap[2].ref() is not None:
+            src = cheap[2]
+            m = _Marker(f"{cheap[0]}@{src.layer}", cheap[1], src, t)
             src.packs += 1  # the recompute reads the predecessor once more
             self._markers[k] = m
             self.store.put(m.slot, ActivationStore.MARKER, None, 0)
             if self._rec is not None:
                 self._rec.markers += 1
             return m
-        h = self._handles.get(k)
-        if h is not None:
-            h.packs += 1
-            return h
-        eb = self.plan.eb.get(lid) if self.plan is not None else None
-        h = _Handle(t, lid, eb)
+        h = _Handle(t, None, None)
         self._handles[k] = h
+        a = self._live(self._act_layer, k)
+        if a is not None:
+            self._promote(h, a[0])
+        return h
+
+    def _promote(self, h, lid):
+        """Make h the stored activation of layer lid (raw, or queued for the
+        codec at the layer's planned error bound)."""
+        eb = self.plan.eb.get(lid) if self.plan is not None else None
+        h.layer, h.eb = lid, eb
+        t = h.raw
         nbytes = t.numel() * 4
         if self._batch:
             self._per_sample[lid] = nbytes / self._batch
@@ -296,11 +331,10 @@ class ActivationCompressor:
             self.store.put(lid, ActivationStore.RAW, None, nbytes)
             if self._rec is not None:
                 self._rec.stored_bytes += nbytes
-            return h
+            return
         self._pending.append(h)
         if len(self._pending) >= self.batch_flush:
             self.flush()
-        return h
 
     def flush(self):
         """Compress every queued activation (one host sync for the batch)."""
@@ -338,6 +372,8 @@ class ActivationCompressor:
             if h.unpacks >= h.packs:
                 h.out = None
             return out
+        if h.layer is None:
+            return h.raw  # a saved tensor that is not a stored activation
         if h.out is None:
             if h.comp is None and h.raw is None:
                 raise LifecycleError(f"activation of {h.layer!r} already released")
