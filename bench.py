@@ -556,7 +556,7 @@ def run_training(args, rank, world, batch=256, iters=8, warm=4):
         if mode == "compressed":
             comp = ActivationCompressor(ActivationCompressor.conv_layer_map(m), opt,
                                         pb.ControllerConfig(W_default=2, W_floor=1),
-                                        batch_flush=int(os.environ.get("ACTC_FLUSH", "8")))
+                                        batch_flush=int(os.environ.get("ACTC_FLUSH", "1")))
         g = torch.Generator(device=dev).manual_seed(rank)
         x = torch.randn(batch, 3, 224, 224, device=dev, generator=g)
         y = torch.randint(0, 1000, (batch,), device=dev, generator=g)

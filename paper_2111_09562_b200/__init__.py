@@ -10,6 +10,8 @@ from .codec import (
     CompressionReport,
     compress,
     compress_batch,
+    compress_begin,
+    compress_end,
     compress_device,
     decompress,
     decompress_batch,

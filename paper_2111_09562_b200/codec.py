@@ -190,8 +190,12 @@ class _DevBufs:
         for nm, numel, isz in layout:
             offs[nm] = o
             o += (numel * isz + 15) & ~15
-        base = torch.empty(max(o, 16), dtype=torch.uint8, device=next(iter(olds)).device)
+        cur = torch.cuda.current_stream()
+        # allocated on the copying stream: a block handed out for the caller's
+        # stream could still be in use by that stream's queued work, which
+        # `stream` is not ordered after
         with torch.cuda.stream(stream):
+            base = torch.empty(max(o, 16), dtype=torch.uint8, device=next(iter(olds)).device)
             for nm, numel, isz in layout:
                 src, soff, _, _ = self._slots[nm]
                 nb = numel * isz
@@ -199,7 +203,8 @@ class _DevBufs:
                     base[offs[nm]:offs[nm] + nb].copy_(src[soff:soff + nb])
                 self._slots[nm] = (base, offs[nm], numel, isz)
                 self._views.pop(nm, None)
-        base.record_stream(stream)
+        if cur != stream:
+            base.record_stream(cur)  # read later on the caller's stream (decoders)
         still = {self._slots[nm][0] for nm in self._slots}
         self._bufs = [b for b in self._bufs if b not in olds or b in still] + [base]
 
@@ -626,6 +631,41 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
         params = [params] * len(xs)
+    results = [None] * len(xs)
+    # largest tensors first: the longest K1 -> K2 -> K3 chain starts earliest
+    order = sorted(range(len(xs)), key=lambda i: -xs[i].numel())
+    del torch
+    for g0 in range(0, len(xs), max_concurrency):
+        group = order[g0:g0 + max_concurrency]
+        pend = compress_begin([xs[i] for i in group], [params[i] for i in group],
+                              ready=None if ready is None else [ready[i] for i in group],
+                              bit_hints=None if bit_hints is None else [bit_hints[i] for i in group])
+        for i, r in zip(group, compress_end(pend, compact=compact)):
+            results[i] = r
+    return results
+
+
+class PendingCompress:
+    """Launched, not yet synchronised compressions (compress_begin)."""
+
+    __slots__ = ("jobs", "main", "done")
+
+    def __init__(self, jobs, main):
+        self.jobs = jobs
+        self.main = main
+        self.done = False
+
+
+def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None) -> PendingCompress:
+    """Launch the compression of xs (each on its own side stream and context,
+    slots slot_base .. slot_base+len-1) and return without synchronising;
+    compress_end reads the plans and builds the containers.  The inputs are
+    kept alive (and recorded on the side streams) until then, and the slots'
+    contexts are busy: nothing else may use them (slot 0 is the thread's main
+    context, used by compress_device / decompress_device) before compress_end."""
+    torch = _lib.torch_cuda()
+    if isinstance(params, CodecParams):
+        params = [params] * len(xs)
     xs = [x if x.is_contiguous() else x.contiguous() for x in xs]
     for x in xs:
         if x.dtype != torch.float32:
@@ -633,80 +673,92 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
     dev_index = xs[0].device.index if xs else torch.cuda.current_device()
     main = torch.cuda.current_stream()
     L = _lib.lib()
-    results = []
-    # largest tensors first: the longest K1 -> K2 -> K3 chain starts earliest
-    order = sorted(range(len(xs)), key=lambda i: -xs[i].numel())
-    for g0 in range(0, len(xs), max_concurrency):
-        group = order[g0:g0 + max_concurrency]
-        streams = _stream_pool(dev_index, len(group))
-        ready_ev = main.record_event()
-        jobs = []
-        for slot, i in enumerate(group):
-            x, p = xs[i], params[i]
-            s = streams[slot]
-            ctx = _lib.context_for(dev_index, slot)
-            n = x.numel()
-            if n == 0:
-                raise ParameterError("empty tensor")
-            nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
-            lmax = min(p.alphabet_size, n)
-            cap_bits = n * max(1, (lmax - 1).bit_length())  # Huffman <= fixed-length code
-            if bit_hints is not None and bit_hints[i]:
-                cap_bits = min(cap_bits, int(bit_hints[i] * 1.25) + 4096)
-            cap = _payload_buffer_bytes(cap_bits)
-            k_cap = max(4096, n // 64)
-            dev = _DevBufs()
-            # fixed-size arrays, and the capped (data-dependent) ones apart so
-            # `compact` can replace the latter by exact-size copies
-            fixed = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("canon", lmax, 4),
-                                         ("len_counts", 64, 4)])
-            fp, of = fixed.data_ptr(), dev.offsets
-            capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4)])
-            cp, oc = capped.data_ptr(), dev.offsets
-            s.wait_event(ready_ev)
-            if ready is not None:
-                s.wait_event(ready[i])
-            flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
-            args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
-                    cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, fp + of["canon"],
-                    fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
-            # every tensor's K1 goes out before any codebook/encoder launch
-            _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
-            fixed.record_stream(s)
-            capped.record_stream(s)
-            x.record_stream(s)
-            jobs.append((i, x, p, s, ctx, dev, cap, k_cap, args))
-        for job in jobs:
-            args = job[8]
-            _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
-        # containers are built as each stream finishes (the host work of the
-        # early tensors overlaps the GPU tail of the late ones), and each
-        # container's stream descriptor is built once here
-        for i, x, p, s, ctx, dev, cap, k_cap, _ in jobs:
-            s.synchronize()
-            plan = _lib.Plan.from_buffer_copy(ctx.plan)
-            n = x.numel()
-            dims = tuple(x.shape) or (1,)
-            fits = (plan.status == 0 and plan.max_len <= 56 and plan.n_outliers <= k_cap
-                    and plan.payload_bits <= 8 * (cap - 32))
-            if fits:
-                k = plan.n_outliers
-                dev.shrink("out_idx", k)
-                dev.shrink("out_val", k)
-                dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
-                dev.shrink("canon", max(plan.live_symbols, 1))
-                if compact:
-                    dev.compact(("out_idx", "payload", "out_val"), s)
-                c, rep = _container(n, p, dims, plan, dev)
-                c._desc()
-            else:
-                _check_plan(plan)
-                c, rep = compress_device(x, p, stream=s)
-            results.append((i, c, rep))
-        for job in jobs:
-            main.wait_stream(job[3])
-    results.sort(key=lambda r: r[0])
-    return [(c, rep) for _, c, rep in results]
+    streams = _stream_pool(dev_index, slot_base + len(xs))[slot_base:]
+    jobs = []
+    for j, (x, p) in enumerate(zip(xs, params)):
+        s = streams[j]
+        ctx = _lib.context_for(dev_index, slot_base + j)
+        n = x.numel()
+        if n == 0:
+            raise ParameterError("empty tensor")
+        nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
+        lmax = min(p.alphabet_size, n)
+        cap_bits = n * max(1, (lmax - 1).bit_length())  # Huffman <= fixed-length code
+        if bit_hints is not None and bit_hints[j]:
+            cap_bits = min(cap_bits, int(bit_hints[j] * 1.25) + 4096)
+        cap = _payload_buffer_bytes(cap_bits)
+        k_cap = max(4096, n // 64)
+        dev = _DevBufs()
+        # fixed-size arrays, and the capped (data-dependent) ones apart so
+        # `compact` can replace the latter by exact-size copies
+        fixed = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("canon", lmax, 4),
+                                     ("len_counts", 64, 4)])
+        fp, of = fixed.data_ptr(), dev.offsets
+        capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4)])
+        cp, oc = capped.data_ptr(), dev.offsets
+        # recorded after this tensor's allocations: its side stream is ordered
+        # after all caller-stream work that used the blocks the allocator reused
+        s.wait_event(main.record_event())
+        if ready is not None:
+            s.wait_event(ready[j])
+        flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
+        args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
+                cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, fp + of["canon"],
+                fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
+        # every tensor's K1 goes out before any codebook/encoder launch
+        _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
+        fixed.record_stream(s)
+        capped.record_stream(s)
+        x.record_stream(s)
+        jobs.append((x, p, s, ctx, dev, cap, k_cap, args))
+    for job in jobs:
+        args = job[7]
+        _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
+    return PendingCompress(jobs, main)
+
+
+def compress_end(pend: PendingCompress, compact: bool = False):
+    """Synchronise a compress_begin batch: [(CompressedActivation, report)]
+    in input order.  A tensor whose plan overflowed a cap is redone through
+    the two-phase path (its input is still held)."""
+    if pend.done:
+        raise ParameterError("compress_end called twice on the same batch")
+    pend.done = True
+    out = []
+    # containers are built as each stream finishes (the host work of the
+    # early tensors overlaps the GPU tail of the late ones), and each
+    # container's stream descriptor is built once here
+    for x, p, s, ctx, dev, cap, k_cap, _ in pend.jobs:
+        s.synchronize()
+        plan = _lib.Plan.from_buffer_copy(ctx.plan)
+        n = x.numel()
+        dims = tuple(x.shape) or (1,)
+        fits = (plan.status == 0 and plan.max_len <= 56 and plan.n_outliers <= k_cap
+                and plan.payload_bits <= 8 * (cap - 32))
+        if fits:
+            k = plan.n_outliers
+            dev.shrink("out_idx", k)
+            dev.shrink("out_val", k)
+            dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
+            dev.shrink("canon", max(plan.live_symbols, 1))
+            if compact:
+                dev.compact(("out_idx", "payload", "out_val"), s)
+            c, rep = _container(n, p, dims, plan, dev)
+            c._desc()
+        else:
+            _check_plan(plan)
+            # the two-phase redo runs on the thread's main context: order it
+            # after the caller's queued work (which may use that context) and
+            # allocate on the stream it runs on
+            torch = _lib.torch_cuda()
+            s.wait_stream(pend.main)
+            with torch.cuda.stream(s):
+                c, rep = compress_device(x, p)
+        out.append((c, rep))
+    for job in pend.jobs:
+        pend.main.wait_stream(job[2])
+    pend.jobs = []
+    return out
 
 
 def compress(t, params: CodecParams):

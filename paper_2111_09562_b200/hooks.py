@@ -22,8 +22,12 @@ Policy, as in the reference:
   of the consumer's momentum) and asks the controller for the next plan;
 * layers whose eb is None (skip set) stay raw.
 
-Packing is batched: pack hooks queue activations and `compress_batch`
-compresses the queue with one host synchronisation (concurrent codebooks).
+Packing is asynchronous: a stored activation's compression is launched on a
+side stream as soon as its producer has run (`compress_begin`, no host
+sync); the oldest in-flight compression is finished (`compress_end`: plan
+read, exact-size container, original released) once more than `batch_flush`
+are in flight, so the raw activations of at most that many layers coexist
+with their compressed copies.
 Under data parallelism the statistics are averaged across ranks before
 planning, so every rank compresses with identical error bounds.
 """
@@ -34,7 +38,7 @@ import weakref
 from dataclasses import dataclass, field
 
 from . import _lib
-from .codec import DEFAULT_RADIUS, CodecParams, compress_batch, decompress_device
+from .codec import DEFAULT_RADIUS, CodecParams, compress_begin, compress_end, decompress_device
 from .controller import AdaptiveController, ControllerConfig, LayerTrainingStats, choose_batch_size
 from .errors import LifecycleError, ParameterError
 
@@ -102,7 +106,7 @@ class _Handle:
     queue is flushed, compressed after.  Handles nobody promotes pass the
     tensor through."""
 
-    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref")
+    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref", "job")
 
     def __init__(self, t, layer, eb):
         self.layer = layer
@@ -114,6 +118,7 @@ class _Handle:
         self.unpacks = 0
         self.out = None
         self.shape = tuple(t.shape)
+        self.job = None  # compress_begin batch while the compression is in flight
         # the tensor's identity: a key (pointer, version, shape, stride) is
         # only unique while the tensor lives -- freed memory is reused
         self.ref = weakref.ref(t)
@@ -148,7 +153,7 @@ class ActivationCompressor:
     """
 
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
-                 preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 8, dist_group=None,
+                 preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 1, dist_group=None,
                  sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
                  recompute_cheap: bool = True):
         self.layers = dict(layers)
@@ -169,7 +174,8 @@ class ActivationCompressor:
         self.records: list[IterationRecord] = []
         self._act_layer: dict = {}
         self._handles: dict = {}
-        self._pending: list[_Handle] = []
+        self._pending: list[_Handle] = []  # compressions launched, not yet synchronised (oldest first)
+        self._slot = 0
         self._collecting = False
         self._R: dict[str, float] = {}
         self._bits: dict[str, int] = {}
@@ -332,26 +338,35 @@ class ActivationCompressor:
             if self._rec is not None:
                 self._rec.stored_bytes += nbytes
             return
+        # launch now (side stream, no host sync); the oldest in-flight
+        # compressions are finished -- container built, original released --
+        # once more than `batch_flush` are in flight, so at most that many
+        # raw activations outlive their compression
+        params = CodecParams(eb=eb, radius=self.radius, preserve_zeros=self.preserve_zeros)
+        # slots 1.. (never the thread's main context, which the decoders use
+        # in backward while the last compressions may still be in flight)
+        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(lid)])
+        self._slot = (self._slot + 1) % (self.batch_flush + 1)
         self._pending.append(h)
-        if len(self._pending) >= self.batch_flush:
-            self.flush()
+        while len(self._pending) > self.batch_flush:
+            self._finish(self._pending.pop(0))
+
+    def _finish(self, h):
+        (c, rep), = compress_end(h.job, compact=True)
+        h.job = None
+        h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
+        self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
+        self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
+        self._interval_ratios.setdefault(h.layer, []).append(rep.ratio)
+        if self._rec is not None:
+            self._rec.stored_bytes += rep.compressed_bytes
+            self._rec.compressed[h.layer] = (rep.ratio, h.eb)
 
     def flush(self):
-        """Compress every queued activation (one host sync for the batch)."""
-        if not self._pending:
-            return
+        """Finish every in-flight compression."""
         pend, self._pending = self._pending, []
-        params = [CodecParams(eb=h.eb, radius=self.radius, preserve_zeros=self.preserve_zeros) for h in pend]
-        hints = [self._bits.get(h.layer) for h in pend]
-        out = compress_batch([h.raw for h in pend], params, compact=True, bit_hints=hints)
-        for h, (c, rep) in zip(pend, out):
-            h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
-            self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
-            self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
-            self._interval_ratios.setdefault(h.layer, []).append(rep.ratio)
-            if self._rec is not None:
-                self._rec.stored_bytes += rep.compressed_bytes
-                self._rec.compressed[h.layer] = (rep.ratio, h.eb)
+        for h in pend:
+            self._finish(h)
 
     def _unpack(self, h):
         import torch
@@ -377,8 +392,9 @@ class ActivationCompressor:
         if h.out is None:
             if h.comp is None and h.raw is None:
                 raise LifecycleError(f"activation of {h.layer!r} already released")
-            if h.raw is not None and h in self._pending:
-                self.flush()
+            if h.job is not None:
+                self._pending.remove(h)
+                self._finish(h)
             if h.comp is not None:
                 out, nz = decompress_device(h.comp, dtype=torch.float32, check=self._collecting)
                 h.out = out.view(h.shape)
