@@ -541,9 +541,11 @@ def run_training(args, rank, world, batch=256, iters=8, warm=4):
     import torchvision
 
     import paper_2111_09562_b200 as pb
+    from paper_2111_09562_b200 import _lib
     from paper_2111_09562_b200.hooks import ActivationCompressor
 
     dev = torch.device("cuda", torch.cuda.current_device())
+    _lib.release_contexts()  # the codec legs' scratch is not the training's
     out = {}
     for mode in ("baseline", "compressed"):
         torch.manual_seed(0)
@@ -596,6 +598,12 @@ def run_training(args, rank, world, batch=256, iters=8, warm=4):
             ms = float(t.item())
         rec = {"images_per_s": world * batch * iters / (ms * 1e-3), "ms_per_iter": ms / iters,
                "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
+        if comp:
+            # the codec contexts' scratch is cudaMalloc'ed by the library,
+            # outside torch's allocator: reported beside the allocator peak
+            sb = _lib.scratch_bytes(slots=range(comp.batch_flush + 2))  # main + the hooks' side slots
+            rec["codec_scratch_gb"] = sb / 1e9
+            rec["peak_mem_gb_incl_codec_scratch"] = rec["peak_mem_gb"] + sb / 1e9
         if comp:
             last = [r for r in comp.records if r.compressed][-1:]
             if last:

@@ -98,6 +98,15 @@ int actc_version(void);
 /* One context per stream: owns grow-on-demand device scratch. */
 int actc_ctx_create(int device, actc_ctx **out);
 void actc_ctx_destroy(actc_ctx *ctx);
+/* device bytes the context's scratch currently holds (cudaMalloc'ed by the
+ * library, outside the caller's allocator) */
+uint64_t actc_ctx_device_bytes(const actc_ctx *ctx);
+/* symbol scratch for the NEXT compress launch on this context (K1 writes
+ * the n symbols, u16 when 2*radius <= 65536 else u32, plus 64 bytes; the
+ * encoder reads them): lets a caller hand in stream-ordered memory from its
+ * own allocator instead of the context's persistent buffer.  Consumed by
+ * that launch; must stay valid until the compression completes. */
+int actc_ctx_set_scratch(actc_ctx *ctx, void *sym_dev, uint64_t bytes);
 
 /* compress(), phase 1 -- replaces codec.py:296-316 up to the codebook:
  * prequantize (:238-251), bound check (:311-312), lorenzo_encode

@@ -93,6 +93,8 @@ def lib():
             "actc_version": ([], I),
             "actc_ctx_create": ([I, C.POINTER(P)], I),
             "actc_ctx_destroy": ([P], None),
+            "actc_ctx_device_bytes": ([P], U64),
+            "actc_ctx_set_scratch": ([P, P, U64], I),
             "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P, P], I),
             "actc_compress_encode": ([P, P, P, P, P, P, P, P, P, P], I),
             "actc_compress_async": ([P, P, U64, D, U32, U32, P, P, U64, P, P, U64, P, P, P, P, P], I),
@@ -123,7 +125,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = (
-    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_compress_plan "
+    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_ctx_device_bytes actc_ctx_set_scratch actc_compress_plan "
     "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
@@ -223,6 +225,27 @@ def context(device=None) -> Context:
         with torch.cuda.device(dev):
             c = ctxs[dev] = Context(dev)
     return c
+
+
+def release_contexts():
+    """Destroy this thread's library contexts and their scratch (after a
+    device synchronisation); they are recreated on next use."""
+    torch = torch_cuda()
+    torch.cuda.synchronize()
+    for name in ("ctxs", "extra"):
+        d = getattr(_tls, name, None)
+        if d:
+            d.clear()
+
+
+def scratch_bytes(slots=None) -> int:
+    """Device bytes held by this thread's library contexts (scratch the
+    library cudaMalloc's itself, invisible to torch's allocator); `slots`
+    restricts the sum to those context slots (0 = the main context)."""
+    L = lib()
+    ctxs = [(0, c) for c in getattr(_tls, "ctxs", {}).values()]
+    ctxs += [(k[1], c) for k, c in getattr(_tls, "extra", {}).items()]
+    return sum(int(L.actc_ctx_device_bytes(c.handle)) for sl, c in ctxs if slots is None or sl in slots)
 
 
 def context_for(device: int, slot: int) -> Context:

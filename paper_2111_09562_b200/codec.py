@@ -656,13 +656,17 @@ class PendingCompress:
         self.done = False
 
 
-def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None) -> PendingCompress:
+def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
+                   own_scratch: bool = False) -> PendingCompress:
     """Launch the compression of xs (each on its own side stream and context,
     slots slot_base .. slot_base+len-1) and return without synchronising;
     compress_end reads the plans and builds the containers.  The inputs are
     kept alive (and recorded on the side streams) until then, and the slots'
     contexts are busy: nothing else may use them (slot 0 is the thread's main
-    context, used by compress_device / decompress_device) before compress_end."""
+    context, used by compress_device / decompress_device) before compress_end.
+    `own_scratch`: the symbol scratch (2-4 bytes per element) comes from
+    torch's allocator per call and is released at compress_end, instead of
+    the context's persistent buffer (memory-bound callers such as the hooks)."""
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
         params = [params] * len(xs)
@@ -701,6 +705,12 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None) -
         s.wait_event(main.record_event())
         if ready is not None:
             s.wait_event(ready[j])
+        symbuf = None
+        if own_scratch:
+            sb = 2 if 2 * int(p.radius) <= 65536 else 4
+            with torch.cuda.stream(s):  # stream-ordered for the side stream
+                symbuf = torch.empty(sb * n + 64, dtype=torch.uint8, device=x.device)
+            _lib.raise_for(L.actc_ctx_set_scratch(ctx.handle, symbuf.data_ptr(), symbuf.numel()))
         flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
         args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
                 cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, fp + of["canon"],
@@ -710,7 +720,7 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None) -
         fixed.record_stream(s)
         capped.record_stream(s)
         x.record_stream(s)
-        jobs.append((x, p, s, ctx, dev, cap, k_cap, args))
+        jobs.append((x, p, s, ctx, dev, cap, k_cap, args, symbuf))
     for job in jobs:
         args = job[7]
         _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
@@ -728,7 +738,7 @@ def compress_end(pend: PendingCompress, compact: bool = False):
     # containers are built as each stream finishes (the host work of the
     # early tensors overlaps the GPU tail of the late ones), and each
     # container's stream descriptor is built once here
-    for x, p, s, ctx, dev, cap, k_cap, _ in pend.jobs:
+    for x, p, s, ctx, dev, cap, k_cap, _, _sym in pend.jobs:
         s.synchronize()
         plan = _lib.Plan.from_buffer_copy(ctx.plan)
         n = x.numel()

@@ -173,6 +173,11 @@ struct actc_ctx {
   // emission to the segment count pass that follows it
   bool defer_emit = false;
   EmitArgs emit{};
+  // caller-provided symbol scratch for the next K1 (actc_ctx_set_scratch;
+  // consumed by that launch), and the buffer the current stream's symbols live in
+  void *sym_ext = nullptr;
+  size_t sym_ext_bytes = 0;
+  void *sym_cur = nullptr;
 };
 
 namespace {
@@ -451,6 +456,21 @@ int actc_ctx_create(int device, actc_ctx **out) {
   return ACTC_OK;
 }
 
+int actc_ctx_set_scratch(actc_ctx *c, void *sym_dev, uint64_t bytes) {
+  c->sym_ext = sym_dev;
+  c->sym_ext_bytes = sym_dev ? bytes : 0;
+  return ACTC_OK;
+}
+
+uint64_t actc_ctx_device_bytes(const actc_ctx *c) {
+  if (!c) return 0;
+  const Buf *bufs[] = {&c->sym, &c->hist, &c->cb, &c->ctab, &c->len8, &c->canon, &c->lencnt,
+                       &c->status, &c->misc, &c->lut, &c->idx, &c->part, &c->crc, &c->crc_copy};
+  uint64_t t = sizeof(actc_plan_t) + sizeof(DecResult);
+  for (const Buf *b : bufs) t += b->p ? b->cap : 0;
+  return t;
+}
+
 void actc_ctx_destroy(actc_ctx *c) {
   if (!c) return;
   Buf *bufs[] = {&c->sym, &c->hist, &c->cb, &c->ctab, &c->len8, &c->canon, &c->lencnt,
@@ -472,7 +492,15 @@ static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_
   if (A > kMaxAlphabet) return set_err(ACTC_EPARAM, "radius %u too large for the device codebook (max %u)", radius, kMaxAlphabet / 2);
   const uint32_t sb = A <= 65536 ? 2 : 4;
   int rc;
-  if ((rc = grow(c->sym, (size_t)sb * n + 64))) return rc;
+  const size_t sym_need = (size_t)sb * n + 64;
+  if (c->sym_ext && c->sym_ext_bytes >= sym_need) {
+    c->sym_cur = c->sym_ext;
+  } else {
+    if ((rc = grow(c->sym, sym_need))) return rc;
+    c->sym_cur = c->sym.p;
+  }
+  c->sym_ext = nullptr;  // one launch only
+  c->sym_ext_bytes = 0;
   if ((rc = grow(c->hist, 8 * A))) return rc;
   CK(cudaMemsetAsync(c->hist.p, 0, 8 * A, s));
   CK(cudaMemsetAsync(c->misc.p, 0, 8 * M_SLOTS, s));
@@ -492,11 +520,11 @@ static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_
     KT(ACTC_KIND_QUANT);
     if (sb == 2)
       k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, win_n * 4, s>>>(
-          x, n, P, radius, (uint16_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
+          x, n, P, radius, (uint16_t *)c->sym_cur, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
           (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
     else
       k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, win_n * 4, s>>>(
-          x, n, P, radius, (uint32_t *)c->sym.p, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
+          x, n, P, radius, (uint32_t *)c->sym_cur, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
           (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
   }
   CKL();
@@ -714,7 +742,7 @@ int actc_compress_encode(actc_ctx *c, const float *x, const actc_plan_t *plan, u
   cudaStream_t s = (cudaStream_t)stream;
   if (c->mode != 1 || plan->n != c->n) return set_err(ACTC_EPARAM, "actc_compress_encode without a matching plan");
   if (plan->status != ACTC_OK) return set_err(plan->status, "Huffman code length exceeds 63 bits");
-  int rc = launch_encode(c, c->sym.p, c->sym_bytes, c->n, x, plan, payload, out_idx, out_val, chunk_off, 1, s);
+  int rc = launch_encode(c, c->sym_cur, c->sym_bytes, c->n, x, plan, payload, out_idx, out_val, chunk_off, 1, s);
   if (rc) return rc;
   if (plan->live_symbols)
     CK(cudaMemcpyAsync(canon, c->canon.p, 4ull * plan->live_symbols, cudaMemcpyDeviceToDevice, s));
@@ -746,7 +774,7 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   // K3 segment encoder planned on the device: live range / windows from the
   // device plan, shared-memory sizes and grids at their caps
   const uint32_t sb = c->sym_bytes;
-  const void *sym = c->sym.p;
+  const void *sym = c->sym_cur;
   const uint64_t nseg = cdiv(n, K3L_SEG);
   SegArgs g{};
   g.n = n;

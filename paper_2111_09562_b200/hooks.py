@@ -345,7 +345,8 @@ class ActivationCompressor:
         params = CodecParams(eb=eb, radius=self.radius, preserve_zeros=self.preserve_zeros)
         # slots 1.. (never the thread's main context, which the decoders use
         # in backward while the last compressions may still be in flight)
-        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(lid)])
+        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(lid)],
+                               own_scratch=True)
         self._slot = (self._slot + 1) % (self.batch_flush + 1)
         self._pending.append(h)
         while len(self._pending) > self.batch_flush:
