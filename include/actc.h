@@ -82,6 +82,7 @@ typedef struct {
   uint64_t payload_bits;
   const uint64_t *chunk_offsets_dev; /* [ceil(n/ACTC_CHUNK)] or NULL (rebuilt) */
   const int64_t *chunk_lat_dev;      /* [ceil(n/ACTC_CHUNK)] lattice before each chunk, or NULL */
+  const void *table_dev;             /* decode table built at compress time (actc_ctx_set_table_out), or NULL */
 } actc_stream_t;
 
 /* Result of a decompression; valid after the stream is synchronized. */
@@ -107,6 +108,13 @@ uint64_t actc_ctx_device_bytes(const actc_ctx *ctx);
  * own allocator instead of the context's persistent buffer.  Consumed by
  * that launch; must stay valid until the compression completes. */
 int actc_ctx_set_scratch(actc_ctx *ctx, void *sym_dev, uint64_t bytes);
+/* buffer (ACTC_TABLE_BYTES) for the decode table of the NEXT compression on
+ * this context: the codebook's tail builds the table actc_decompress will
+ * pick for the stream (prefix LUT, or the u8 length table for wide
+ * alphabets), so decompression launches only the decoder (pass it back as
+ * actc_stream_t.table_dev).  Consumed by that launch. */
+#define ACTC_TABLE_BYTES 16400
+int actc_ctx_set_table_out(actc_ctx *ctx, void *table_dev, uint64_t bytes);
 
 /* compress(), phase 1 -- replaces codec.py:296-316 up to the codebook:
  * prequantize (:238-251), bound check (:311-312), lorenzo_encode

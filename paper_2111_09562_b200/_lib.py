@@ -19,6 +19,7 @@ ACTC_OK, ACTC_EPARAM, ACTC_EDATA, ACTC_EFORMAT, ACTC_ENOMEM, ACTC_ECUDA = range(
 ACTC_FLAG_PRESERVE_ZEROS = 1
 ACTC_ASYNC_K1_ONLY = 0x100
 ACTC_ASYNC_REST = 0x200
+ACTC_TABLE_BYTES = 16400  # include/actc.h
 ACTC_DEC_LUT_ONLY = 0x100
 ACTC_DEC_REST = 0x200
 ACTC_DTYPE_F32, ACTC_DTYPE_F64 = 0, 1
@@ -57,6 +58,7 @@ class StreamDesc(C.Structure):
         ("payload_bits", C.c_uint64),
         ("chunk_offsets_dev", C.c_void_p),
         ("chunk_lat_dev", C.c_void_p),
+        ("table_dev", C.c_void_p),
     ]
 
 
@@ -95,6 +97,7 @@ def lib():
             "actc_ctx_destroy": ([P], None),
             "actc_ctx_device_bytes": ([P], U64),
             "actc_ctx_set_scratch": ([P, P, U64], I),
+            "actc_ctx_set_table_out": ([P, P, U64], I),
             "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P, P], I),
             "actc_compress_encode": ([P, P, P, P, P, P, P, P, P, P], I),
             "actc_compress_async": ([P, P, U64, D, U32, U32, P, P, U64, P, P, U64, P, P, P, P, P], I),
@@ -125,7 +128,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = (
-    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_ctx_device_bytes actc_ctx_set_scratch actc_compress_plan "
+    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_ctx_device_bytes actc_ctx_set_scratch actc_ctx_set_table_out actc_compress_plan "
     "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "

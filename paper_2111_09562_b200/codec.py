@@ -378,6 +378,7 @@ class CompressedActivation:
         d.payload_bits = self.payload_bits
         d.chunk_offsets_dev = dev.ptr("chunk_off") if (with_index and "chunk_off" in dev) else None
         d.chunk_lat_dev = dev.ptr("chunk_lat") if (with_index and "chunk_lat" in dev) else None
+        d.table_dev = dev.ptr("table") if (with_index and "table" in dev) else None
         if with_index and d.chunk_offsets_dev:
             self._desc_cache = d  # device buffers are fixed for the container's lifetime
         return d
@@ -696,7 +697,7 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         # fixed-size arrays, and the capped (data-dependent) ones apart so
         # `compact` can replace the latter by exact-size copies
         fixed = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("canon", lmax, 4),
-                                     ("len_counts", 64, 4)])
+                                     ("len_counts", 64, 4), ("table", _lib.ACTC_TABLE_BYTES, 1)])
         fp, of = fixed.data_ptr(), dev.offsets
         capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4)])
         cp, oc = capped.data_ptr(), dev.offsets
@@ -722,7 +723,9 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         x.record_stream(s)
         jobs.append((x, p, s, ctx, dev, cap, k_cap, args, symbuf))
     for job in jobs:
-        args = job[7]
+        args, dev = job[7], job[4]
+        # the chain's tail builds the stream's decode table into the container
+        _lib.raise_for(L.actc_ctx_set_table_out(args[0], dev.ptr("table"), _lib.ACTC_TABLE_BYTES))
         _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
     return PendingCompress(jobs, main)
 

@@ -178,6 +178,8 @@ struct actc_ctx {
   void *sym_ext = nullptr;
   size_t sym_ext_bytes = 0;
   void *sym_cur = nullptr;
+  // decode-table output for the next async compression (actc_ctx_set_table_out)
+  void *table_out = nullptr;
 };
 
 namespace {
@@ -453,6 +455,13 @@ int actc_ctx_create(int device, actc_ctx **out) {
   c->k4_blocks[1] = std::max(1, nb) * c->num_sms;
   cudaGetLastError();
   *out = c;
+  return ACTC_OK;
+}
+
+int actc_ctx_set_table_out(actc_ctx *c, void *table_dev, uint64_t bytes) {
+  if (table_dev && bytes < ACTC_TABLE_BYTES) return set_err(ACTC_EPARAM, "decode table buffer too small");
+  if (((uintptr_t)table_dev & 15u) != 0) return set_err(ACTC_EPARAM, "decode table buffer must be 16-byte aligned");
+  c->table_out = table_dev;
   return ACTC_OK;
 }
 
@@ -827,6 +836,13 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
     else
       k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
   }
+  if (c->table_out) {
+    // the decode table the decoder will pick, built now (off the decompress path)
+    KT(ACTC_KIND_LUT);
+    k_build_table_plan<<<kLutSize / 256, 256, 0, s>>>(canon, len_counts, c->plan_dev, c->table_out,
+                                                      2ull * radius <= 65536 ? 1 : 0);
+    c->table_out = nullptr;
+  }
   CKL();
   CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
   c->mode = 0;  // the ctx holds no pending plan for actc_compress_encode
@@ -871,7 +887,11 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   if (force) kind = !strcmp(force, "k4w") ? 0 : !strcmp(force, "k4wci") ? 1 : 2;
   if (kind == 1 && !(sw16 && mode != 2)) kind = 0;
   const bool lane_dec = warp_dec && kind == 2;
-  if (phase != 2) {
+  // a table built at compress time (k_build_table_plan) follows the same
+  // choice rule; an ACTC_DEC override or the debug mode builds its own
+  const bool prebuilt = S.table_dev && warp_dec && !force && mode != 2 && kind != 1;
+  if (prebuilt && phase == 1) return ACTC_OK;
+  if (phase != 2 && !prebuilt) {
     KT(ACTC_KIND_LUT);
     if (lane_dec)
       k_build_lut8<<<16, 256, 0, s>>>(S.len_counts_dev, (uint8_t *)c->lut.p);
@@ -892,7 +912,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.out_val = S.outlier_val_dev;
   a.canon = S.canon_syms_dev;
   a.len_counts = S.len_counts_dev;
-  a.lut = (const uint32_t *)c->lut.p;
+  a.lut = prebuilt ? (const uint32_t *)S.table_dev : (const uint32_t *)c->lut.p;
   a.payload = (const uint32_t *)S.payload_dev;
   a.payload_bits = S.payload_bits;
   a.chunk_off = (const unsigned long long *)S.chunk_offsets_dev;

@@ -90,8 +90,8 @@ __device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint
 // register window); 0 if no code starts with the prefix.  lut[kLutSize]
 // holds the fast-path flag: 1 if the code is prefix-free (Kraft <= 1) and
 // max length <= 32.
-__global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
-                            uint32_t *__restrict__ lut, int mode) {
+__device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
+                                           uint32_t *__restrict__ lut, int mode) {
   __shared__ CodeTables t;
   __shared__ unsigned s_ok;
   build_tables(t, len_counts);
@@ -139,6 +139,24 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
     if ((mode & 2) && s_ok && l0 && l1 == l0) e |= 63u;
   }
   lut[p] = e;
+}
+
+__global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
+                            uint32_t *__restrict__ lut, int mode) {
+  lut32_body(canon, len_counts, lut, mode);
+}
+
+// The decode table of a stream compressed by actc_compress_async, built at
+// the end of its chain from the device plan: the k4w prefix LUT (symbols,
+// exact-long entries) when launch_decode will pick k4w for it (16-bit
+// symbols and <= 24576 live symbols), else the k4x u8 length table.
+__global__ void k_build_table_plan(const uint32_t *canon, const uint32_t *len_counts, const actc_plan_t *plan,
+                                   void *table, int sw16) {
+  if (plan->status != ACTC_OK || plan->live_symbols == 0) return;
+  if (sw16 && plan->live_symbols <= 24576u)
+    lut32_body(canon, len_counts, (uint32_t *)table, 2);
+  else
+    lut8_body(len_counts, (uint8_t *)table);
 }
 
 template <int MODE, int SW>

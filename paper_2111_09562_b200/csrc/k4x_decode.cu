@@ -29,7 +29,7 @@ namespace actc {
 
 namespace {
 
-constexpr int kXBits = 12;
+static_assert(kXBits == 12, "k4x prefix width");
 constexpr int kXCache = 16384;
 
 __device__ __forceinline__ uint64_t x_read_bits64(const uint32_t *__restrict__ pw, uint64_t pos) {
@@ -71,36 +71,7 @@ __device__ __forceinline__ uint32_t x_lds_u32(uint32_t a) {
 // value starts with the 12-bit prefix p has length in [l0, l0+3] (maxlen <=
 // 32); 0 otherwise (long spread, invalid prefix, or codes > 32 bits).
 __global__ void k_build_lut8(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8) {
-  __shared__ unsigned long long lim[65];  // (first + count) << (32 - l): exclusive left-aligned limit
-  __shared__ uint32_t s_max;
-  if (threadIdx.x == 0) {
-    unsigned long long code = 0;
-    uint32_t mx = 0;
-    for (int l = 0; l < 64; l++) {
-      code <<= 1;
-      const uint32_t c = len_counts[l];
-      lim[l] = l <= 32 ? (code + c) << (32 - l) : 0ull;
-      code += c;
-      if (c && l > 0) mx = l;
-    }
-    s_max = mx;
-  }
-  __syncthreads();
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (1u << kXBits)) return;
-  uint8_t e = 0;
-  if (s_max >= 1 && s_max <= 32) {
-    const unsigned long long w0 = (unsigned long long)p << (32 - kXBits);
-    const unsigned long long w1 = w0 | ((1ull << (32 - kXBits)) - 1);
-    // shortest length whose codes cover w0, and the one covering w1
-    int l0 = 0, l1 = 0;
-    for (int l = 1; l <= (int)s_max; l++)
-      if (!l0 && lim[l] > w0) l0 = l;
-    for (int l = 1; l <= (int)s_max; l++)
-      if (!l1 && lim[l] > w1) l1 = l;
-    if (l0 && l1 && l1 - l0 <= 3) e = (uint8_t)l0;
-  }
-  lut8[p] = e;
+  lut8_body(len_counts, lut8);
 }
 
 template <int MODE>

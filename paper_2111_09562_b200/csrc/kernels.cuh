@@ -345,6 +345,49 @@ uint64_t crc32_blocks(uint64_t len);
 int crc32_launch(const uint8_t *data, uint64_t len, uint32_t crc_in, uint32_t *part, unsigned *ticket,
                  uint32_t *out_dev, cudaStream_t s);
 
+// K4x u8 length table: lut8[p] = l0 when every code whose left-aligned
+// 32-bit value starts with the kXBits-bit prefix p has a length in
+// [l0, l0+3] (max length <= 32); 0 otherwise.  16 x 256 threads.
+constexpr int kXBits = 12;
+__device__ __forceinline__ void lut8_body(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8) {
+  __shared__ unsigned long long lim[65];  // (first + count) << (32 - l): exclusive left-aligned limit
+  __shared__ uint32_t s_max;
+  if (threadIdx.x == 0) {
+    unsigned long long code = 0;
+    uint32_t mx = 0;
+    for (int l = 0; l < 64; l++) {
+      code <<= 1;
+      const uint32_t c = len_counts[l];
+      lim[l] = l <= 32 ? (code + c) << (32 - l) : 0ull;
+      code += c;
+      if (c && l > 0) mx = l;
+    }
+    s_max = mx;
+  }
+  __syncthreads();
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (1u << kXBits)) return;
+  uint8_t e = 0;
+  if (s_max >= 1 && s_max <= 32) {
+    const unsigned long long w0 = (unsigned long long)p << (32 - kXBits);
+    const unsigned long long w1 = w0 | ((1ull << (32 - kXBits)) - 1);
+    // shortest length whose codes cover w0, and the one covering w1
+    int l0 = 0, l1 = 0;
+    for (int l = 1; l <= (int)s_max; l++)
+      if (!l0 && lim[l] > w0) l0 = l;
+    for (int l = 1; l <= (int)s_max; l++)
+      if (!l1 && lim[l] > w1) l1 = l;
+    if (l0 && l1 && l1 - l0 <= 3) e = (uint8_t)l0;
+  }
+  lut8[p] = e;
+}
+
+
+// decode table at compress time (k4_decode.cu): the table launch_decode
+// would build for this stream, chosen on the device from the plan
+__global__ void k_build_table_plan(const uint32_t *canon, const uint32_t *len_counts, const actc_plan_t *plan,
+                                   void *table, int sw16);
+
 // K7 uniform error injection (k7_inject.cu); state = {st_hi, st_lo, inc_hi, inc_lo}
 int inject_launch(const void *x, int dtype, uint64_t n, double eb, int preserve, const uint64_t state[4],
                   double *out, cudaStream_t s);
