@@ -38,7 +38,7 @@ METRIC = "activation compress+decompress GB/s/GPU vs HBM peak; compression ratio
 
 KERNEL_NAMES = {"quant": "k1_quant_lorenzo_hist", "codebook": "k2r_codebook + k2s_emit", "count": "k3_seg_count (+ CTA-total scan in its last CTA)",
                 "scan": "k_excl_scan_u64 (non-default encoders)", "pack": "k3_seg_pack", "fixup": "k3_fixup", "lut": "k_build_lut(8)",
-                "decode": "k4w_decode (<= 24K live symbols) / k4x_decode"}
+                "decode": "k4w_decode (<= 16K live symbols) / k4x_decode"}
 
 
 def _timeline():

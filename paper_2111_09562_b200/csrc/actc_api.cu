@@ -883,7 +883,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   // forces one (measurements).
   static const char *force = getenv("ACTC_DEC");
   const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
-  int kind = (sw16 && S.live_symbols <= 24576u) ? 0 : 2;  // 0 k4w, 1 k4w ci rows, 2 k4x
+  int kind = (sw16 && S.live_symbols <= K4W_MAX_LIVE) ? 0 : 2;  // 0 k4w, 1 k4w ci rows, 2 k4x
   if (force) kind = !strcmp(force, "k4w") ? 0 : !strcmp(force, "k4wci") ? 1 : 2;
   if (kind == 1 && !(sw16 && mode != 2)) kind = 0;
   const bool lane_dec = warp_dec && kind == 2;

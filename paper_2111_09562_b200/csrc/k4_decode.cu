@@ -149,11 +149,11 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
 // The decode table of a stream compressed by actc_compress_async, built at
 // the end of its chain from the device plan: the k4w prefix LUT (symbols,
 // exact-long entries) when launch_decode will pick k4w for it (16-bit
-// symbols and <= 24576 live symbols), else the k4x u8 length table.
+// symbols and <= K4W_MAX_LIVE live symbols), else the k4x u8 length table.
 __global__ void k_build_table_plan(const uint32_t *canon, const uint32_t *len_counts, const actc_plan_t *plan,
                                    void *table, int sw16) {
   if (plan->status != ACTC_OK || plan->live_symbols == 0) return;
-  if (sw16 && plan->live_symbols <= 24576u)
+  if (sw16 && plan->live_symbols <= K4W_MAX_LIVE)
     lut32_body(canon, len_counts, (uint32_t *)table, 2);
   else
     lut8_body(len_counts, (uint8_t *)table);
