@@ -858,11 +858,13 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
             s.wait_event(ready)
             ctx = _lib.context_for(dev_index, slot)
             dt = _lib.ACTC_DTYPE_F32 if out.dtype == f32 else _lib.ACTC_DTYPE_F64
-            # every decode table goes out before any decoder fills the GPU
-            rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(), dt | _lib.ACTC_DEC_LUT_ONLY,
-                                   None, s.cuda_stream)
-            if rc:
-                _lib.raise_for(rc)
+            if not d.table_dev:
+                # every decode table goes out before any decoder fills the GPU
+                # (streams from compress_batch carry theirs already)
+                rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(), dt | _lib.ACTC_DEC_LUT_ONLY,
+                                       None, s.cuda_stream)
+                if rc:
+                    _lib.raise_for(rc)
             jobs.append((i, c, out, d, s, ctx, dt))
         for i, c, out, d, s, ctx, dt in jobs:
             rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(), dt | _lib.ACTC_DEC_REST,

@@ -891,7 +891,9 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   // choice rule; an ACTC_DEC override or the debug mode builds its own
   const bool prebuilt = S.table_dev && warp_dec && !force && mode != 2 && kind != 1;
   if (prebuilt && phase == 1) return ACTC_OK;
-  if (phase != 2 && !prebuilt) {
+  // batches skip the table-only call for streams that carry a table; if the
+  // table cannot be used here (decoder override), the decoder call builds one
+  if (!prebuilt && (phase != 2 || S.table_dev)) {
     KT(ACTC_KIND_LUT);
     if (lane_dec)
       k_build_lut8<<<16, 256, 0, s>>>(S.len_counts_dev, (uint8_t *)c->lut.p);
