@@ -33,6 +33,7 @@ extern "C" {
 #define ACTC_EFORMAT 3 /* -> FormatError    (errors.py:20) */
 #define ACTC_ENOMEM 4
 #define ACTC_ECUDA 5
+#define ACTC_EAGAIN 6  /* plan status only: the async codebook needs its fallback, redo (actc_compress_async) */
 
 #define ACTC_FLAG_PRESERVE_ZEROS 1u /* CMTZ flags bit0 (codec.py:96) */
 
@@ -153,9 +154,14 @@ int actc_compress_encode(actc_ctx *ctx, const float *x_dev, const actc_plan_t *p
  * stream needs the wide (> 26-bit) encoder, exceeds a cap, or the plan
  * status is not ACTC_OK, nothing is encoded and the caller redoes the
  * tensor with actc_compress_plan/actc_compress_encode.  Same inputs and
- * ownership rules as actc_compress_plan. */
+ * ownership rules as actc_compress_plan.
+ * ACTC_ASYNC_NO_FALLBACK: do not queue the symbol-level fallback codebook
+ * behind the frequency-class one (its launch needs a whole SM and waits for
+ * one to drain); if the fast codebook's capacities are exceeded the plan
+ * status is ACTC_EAGAIN and the caller redoes the tensor. */
 #define ACTC_ASYNC_K1_ONLY 0x100u /* flags: launch only K1 (quantize/Lorenzo/histogram) */
 #define ACTC_ASYNC_REST 0x200u    /* flags: launch the codebook + encoder after a K1_ONLY call */
+#define ACTC_ASYNC_NO_FALLBACK 0x400u
 int actc_compress_async(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb, uint32_t radius,
                         uint32_t flags, int64_t *chunk_lat_dev, uint8_t *payload_dev,
                         uint64_t payload_cap_bytes, uint64_t *outlier_idx_dev, float *outlier_val_dev,

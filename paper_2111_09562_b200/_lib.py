@@ -19,6 +19,8 @@ ACTC_OK, ACTC_EPARAM, ACTC_EDATA, ACTC_EFORMAT, ACTC_ENOMEM, ACTC_ECUDA = range(
 ACTC_FLAG_PRESERVE_ZEROS = 1
 ACTC_ASYNC_K1_ONLY = 0x100
 ACTC_ASYNC_REST = 0x200
+ACTC_ASYNC_NO_FALLBACK = 0x400
+ACTC_EAGAIN = 6
 ACTC_TABLE_BYTES = 16400  # include/actc.h
 ACTC_DEC_LUT_ONLY = 0x100
 ACTC_DEC_REST = 0x200

@@ -646,6 +646,12 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
     return results
 
 
+# tensors (element count, radius) whose frequency-class codebook needed the
+# symbol-level fallback in an earlier async compression: they queue the
+# fallback behind it; all others skip that launch (ACTC_ASYNC_NO_FALLBACK)
+_FALLBACK_SEEN: set = set()
+
+
 class PendingCompress:
     """Launched, not yet synchronised compressions (compress_begin)."""
 
@@ -713,6 +719,8 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
                 symbuf = torch.empty(sb * n + 64, dtype=torch.uint8, device=x.device)
             _lib.raise_for(L.actc_ctx_set_scratch(ctx.handle, symbuf.data_ptr(), symbuf.numel()))
         flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
+        if (n, int(p.radius)) not in _FALLBACK_SEEN:
+            flags |= _lib.ACTC_ASYNC_NO_FALLBACK
         args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
                 cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, fp + of["canon"],
                 fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
@@ -759,7 +767,10 @@ def compress_end(pend: PendingCompress, compact: bool = False):
             c, rep = _container(n, p, dims, plan, dev)
             c._desc()
         else:
-            _check_plan(plan)
+            if plan.status == _lib.ACTC_EAGAIN:
+                _FALLBACK_SEEN.add((n, int(p.radius)))  # next time: queue the fallback codebook
+            else:
+                _check_plan(plan)
             # the two-phase redo runs on the thread's main context: order it
             # after the caller's queued work (which may use that context) and
             # allocate on the stream it runs on

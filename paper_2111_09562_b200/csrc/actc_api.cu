@@ -172,6 +172,7 @@ struct actc_ctx {
   // when set (actc_compress_async), the codebook leaves the canonical-code
   // emission to the segment count pass that follows it
   bool defer_emit = false;
+  bool no_fallback = false;  // actc_compress_async ACTC_ASYNC_NO_FALLBACK
   EmitArgs emit{};
   // caller-provided symbol scratch for the next K1 (actc_ctx_set_scratch;
   // consumed by that launch), and the buffer the current stream's symbols live in
@@ -275,7 +276,7 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
     k2r_codebook<<<1, K2_THREADS, kK2rSmem, s>>>(a);
     a.gate = a.fallback;
   }
-  {
+  if (!(a.gate && c->no_fallback)) {
     KT(ACTC_KIND_CODEBOOK);
     k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
   }
@@ -776,9 +777,11 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   c->canon_out = canon;
   c->lencnt_out = len_counts;
   c->defer_emit = true;
+  c->no_fallback = (flags & ACTC_ASYNC_NO_FALLBACK) != 0;
   rc = launch_cb(c, s);
   c->canon_out = c->lencnt_out = nullptr;
   c->defer_emit = false;
+  c->no_fallback = false;
   if (rc) return rc;
   // K3 segment encoder planned on the device: live range / windows from the
   // device plan, shared-memory sizes and grids at their caps

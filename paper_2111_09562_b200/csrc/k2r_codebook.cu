@@ -269,7 +269,10 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   const uint32_t L = s_L;
   const uint32_t nbig = s_nbig;
   if (L == 0 || nbig > kBigCap || s_sum >= (1ull << 32)) {
-    if (tid == 0) *a.fallback = 1u;
+    if (tid == 0) {
+      *a.fallback = 1u;
+      a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
+    }
     return;
   }
   const uint32_t lo = s_lo, hi = s_hi;
@@ -314,7 +317,10 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   }
   const uint32_t R = Rs + nu;
   if (R > kRCap) {
-    if (tid == 0) *a.fallback = 1u;
+    if (tid == 0) {
+      *a.fallback = 1u;
+      a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
+    }
     return;
   }
   for (uint32_t i = tid; i < R; i += NT) LC[i] = 0;
@@ -613,7 +619,10 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     __syncthreads();
   }
   if (s_fail) {
-    if (tid == 0) *a.fallback = 1u;
+    if (tid == 0) {
+      *a.fallback = 1u;
+      a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
+    }
     return;
   }
   K2R_STAMP(3)
@@ -752,7 +761,10 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   }
   __syncthreads();
   if (s_fail) {
-    if (tid == 0) *a.fallback = 1u;
+    if (tid == 0) {
+      *a.fallback = 1u;
+      a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
+    }
     return;
   }
   const uint32_t minlen = s_minlen, maxlen = s_maxlen, nsc = s_nsc;

@@ -284,3 +284,30 @@ def test_long_codes_bit_exact(oracle, depth):
     for cc in (c, cb, pc.CompressedActivation.from_bytes(ref.blob)):
         out, _ = pb.decompress_device(cc, dtype=torch.float64)
         assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+
+
+def test_async_codebook_fallback_redo_and_memory(oracle):
+    """> 6144 distinct symbol frequencies exceed the frequency-class codebook:
+    the first batched compression runs without the fallback launch, sees
+    ACTC_EAGAIN and redoes the tensor; the next one queues the fallback
+    codebook on the device.  Both bit-exact."""
+    K = 6500
+    rng = np.random.default_rng(1)
+    vals = np.array([((i + 1) // 2) * (1 if i % 2 else -1) for i in range(K)], dtype=np.int64)
+    d = np.repeat(vals, np.arange(K, 0, -1))
+    rng.shuffle(d)
+    x = np.cumsum(d).astype(np.float32)  # eb = 0.5: exact lattice values
+    p = pb.CodecParams(eb=0.5)
+    ref = oracle.compress(x, p.eb, debug=False)
+    xt = torch.from_numpy(x).cuda()
+    key = (x.size, p.radius)
+    pc._FALLBACK_SEEN.discard(key)
+    (c1, r1), = pb.compress_batch([xt], [p])
+    assert key in pc._FALLBACK_SEEN
+    (c2, r2), = pb.compress_batch([xt], [p])
+    for c, r in ((c1, r1), (c2, r2)):
+        assert c.to_bytes() == ref.blob
+        assert r.ratio == ref.ratio
+    out = pb.decompress_batch([c2], dtype=torch.float64)[0]
+    want = oracle.decompress_blob(ref.blob, x.size)
+    assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
