@@ -817,6 +817,9 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   g.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_SEGTICKET);
   g.emit = c->emit;  // the count pass emits the canonical codes
   c->emit = EmitArgs{};
+  g.table = c->table_out;  // the first pack CTAs build the decode table
+  g.sw16 = 2ull * radius <= 65536 ? 1 : 0;
+  c->table_out = nullptr;
   g.x = x;
   g.payload = (uint32_t *)payload;
   g.out_idx = (unsigned long long *)out_idx;
@@ -838,13 +841,6 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
       k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, g);
     else
       k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
-  }
-  if (c->table_out) {
-    // the decode table the decoder will pick, built now (off the decompress path)
-    KT(ACTC_KIND_LUT);
-    k_build_table_plan<<<kLutSize / 256, 256, 0, s>>>(canon, len_counts, c->plan_dev, c->table_out,
-                                                      2ull * radius <= 65536 ? 1 : 0);
-    c->table_out = nullptr;
   }
   CKL();
   CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));

@@ -464,6 +464,14 @@ template <typename SymT>
 __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint32_t k3p_sm[];
   if (!seg_resolve(a)) return;
+  if (a.table && a.dplan) {
+    // the stream's decode table (kLutSize entries, 16 rows of 256), built
+    // here by the first CTAs instead of a launch of its own
+    for (uint32_t b = blockIdx.x; b < (uint32_t)(kLutSize / K3L_THREADS); b += gridDim.x) {
+      table_rows_plan(a.canon_out, a.lencnt_out, a.dplan, a.table, a.sw16, b);
+      __syncthreads();
+    }
+  }
   uint32_t *tab = k3p_sm;
   k3_load_window(tab, a.ctab, a.win_lo, a.win_n, K3L_THREADS);
   __syncthreads();

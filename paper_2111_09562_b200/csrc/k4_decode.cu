@@ -36,33 +36,6 @@ __device__ __forceinline__ uint64_t read_bits64(const uint32_t *__restrict__ pw,
   return (hi << sh) | ((uint64_t)lo >> (32 - sh));
 }
 
-struct CodeTables {
-  unsigned long long first[64];
-  unsigned long long lim[64];  // (first + count) << (32 - l), l <= 32 (left-aligned limit)
-  uint32_t count[64];
-  uint32_t base[64];
-  uint32_t maxlen;
-};
-
-__device__ void build_tables(CodeTables &t, const uint32_t *len_counts) {
-  if (threadIdx.x == 0) {
-    unsigned long long code = 0;
-    uint32_t idx = 0, mx = 0;
-    for (int l = 0; l < 64; l++) {
-      code <<= 1;
-      uint32_t c = len_counts[l];
-      t.first[l] = code;
-      t.count[l] = c;
-      t.base[l] = idx;
-      t.lim[l] = l <= 32 ? (code + c) << (32 - l) : 0;
-      code += c;
-      idx += c;
-      if (c && l > 0) mx = l;
-    }
-    t.maxlen = mx;
-  }
-}
-
 // Canonical decode of one code starting at absolute bit `pos` for lengths
 // beyond the LUT (huffman.py:127-141 rule: the first length whose code
 // offset is in range).  Returns length or 0 if invalid.
@@ -83,67 +56,9 @@ __device__ __forceinline__ int slow_decode(const uint32_t *__restrict__ pw, uint
 
 }  // namespace
 
-// LUT entry for every 12-bit prefix: (symbol << 6) | length for a code of
-// length <= 12 (same first-match rule as the reference's bit loop); for a
-// prefix of longer codes, (l0 << 6) with l0 the first length whose
-// left-aligned limit exceeds the prefix (decoding continues from l0 on the
-// register window); 0 if no code starts with the prefix.  lut[kLutSize]
-// holds the fast-path flag: 1 if the code is prefix-free (Kraft <= 1) and
-// max length <= 32.
-__device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
-                                           uint32_t *__restrict__ lut, int mode) {
-  __shared__ CodeTables t;
-  __shared__ unsigned s_ok;
-  build_tables(t, len_counts);
-  __syncthreads();
-  const int ci_mode = mode & 1;
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (threadIdx.x == 0) {
-    // Kraft sum in units of 2^-63
-    unsigned long long k = 0;
-    bool over = false;
-    for (int l = 1; l < 64 && !over; l++) {
-      unsigned long long add = (unsigned long long)t.count[l] << (63 - l);
-      if (t.count[l] >> l) over = true;  // count >= 2^l alone exceeds the budget
-      if (k + add < k) over = true;
-      k += add;
-      if (k > (1ull << 63)) over = true;
-    }
-    s_ok = (!over && t.maxlen <= 32) ? 1u : 0u;
-    if (p == 0) lut[kLutSize] = s_ok;
-  }
-  __syncthreads();
-  if (p >= (uint32_t)kLutSize) return;
-  uint32_t e = 0;
-  int lim = t.maxlen < (uint32_t)kLutBits ? (int)t.maxlen : kLutBits;
-  for (int l = 1; l <= lim; l++) {
-    unsigned long long code = p >> (kLutBits - l);
-    unsigned long long off = code - t.first[l];
-    if (off < t.count[l]) {
-      e = ((ci_mode ? (uint32_t)(t.base[l] + off) : canon[t.base[l] + off]) << 6) | (uint32_t)l;
-      break;
-    }
-  }
-  if (!e && t.maxlen > (uint32_t)kLutBits && t.maxlen <= 32) {
-    const unsigned long long w = (unsigned long long)p << (32 - kLutBits);
-    const unsigned long long w1 = w | ((1ull << (32 - kLutBits)) - 1);
-    int l0 = 0, l1 = 0;
-    for (int l = kLutBits + 1; l <= (int)t.maxlen; l++) {
-      unsigned long long limit = (t.first[l] + t.count[l]) << (32 - l);
-      if (!l0 && limit > w) l0 = l;
-      if (!l1 && limit > w1) l1 = l;
-    }
-    if (l0) e = (uint32_t)l0 << 6;
-    // mode bit1: every code behind the prefix has the same length -> "exact
-    // long" entry (length field 63): the decoder skips the limit probes
-    if ((mode & 2) && s_ok && l0 && l1 == l0) e |= 63u;
-  }
-  lut[p] = e;
-}
-
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
                             uint32_t *__restrict__ lut, int mode) {
-  lut32_body(canon, len_counts, lut, mode);
+  lut32_body(canon, len_counts, lut, mode, blockIdx.x);
 }
 
 // The decode table of a stream compressed by actc_compress_async, built at
@@ -153,10 +68,7 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
 __global__ void k_build_table_plan(const uint32_t *canon, const uint32_t *len_counts, const actc_plan_t *plan,
                                    void *table, int sw16) {
   if (plan->status != ACTC_OK || plan->live_symbols == 0) return;
-  if (sw16 && plan->live_symbols <= K4W_MAX_LIVE)
-    lut32_body(canon, len_counts, (uint32_t *)table, 2);
-  else
-    lut8_body(len_counts, (uint8_t *)table);
+  table_rows_plan(canon, len_counts, plan, table, sw16, blockIdx.x);
 }
 
 template <int MODE, int SW>

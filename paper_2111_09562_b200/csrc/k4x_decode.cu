@@ -71,7 +71,7 @@ __device__ __forceinline__ uint32_t x_lds_u32(uint32_t a) {
 // value starts with the 12-bit prefix p has length in [l0, l0+3] (maxlen <=
 // 32); 0 otherwise (long spread, invalid prefix, or codes > 32 bits).
 __global__ void k_build_lut8(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8) {
-  lut8_body(len_counts, lut8);
+  lut8_body(len_counts, lut8, blockIdx.x);
 }
 
 template <int MODE>

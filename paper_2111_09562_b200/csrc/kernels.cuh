@@ -233,6 +233,8 @@ struct SegArgs {
   const uint32_t *canon_src, *lencnt_src;
   uint32_t *canon_out, *lencnt_out;
   EmitArgs emit;  // deferred k2s emission (rank_tab null: none)
+  void *table;    // decode table built by the first pack CTAs (null: none)
+  int sw16;       // 16-bit symbols (the k4w / k4x choice of the table)
 };
 // resolve a device-planned SegArgs; false = this stream takes the host path
 __device__ __forceinline__ bool seg_resolve(SegArgs &a) {
@@ -349,11 +351,98 @@ uint64_t crc32_blocks(uint64_t len);
 int crc32_launch(const uint8_t *data, uint64_t len, uint32_t crc_in, uint32_t *part, unsigned *ticket,
                  uint32_t *out_dev, cudaStream_t s);
 
+// canonical code tables from the per-length counts (huffman.py:97-117)
+struct CodeTables {
+  unsigned long long first[64];
+  unsigned long long lim[64];  // (first + count) << (32 - l), l <= 32 (left-aligned limit)
+  uint32_t count[64];
+  uint32_t base[64];
+  uint32_t maxlen;
+};
+
+__device__ __forceinline__ void build_tables(CodeTables &t, const uint32_t *len_counts) {
+  if (threadIdx.x == 0) {
+    unsigned long long code = 0;
+    uint32_t idx = 0, mx = 0;
+    for (int l = 0; l < 64; l++) {
+      code <<= 1;
+      uint32_t c = len_counts[l];
+      t.first[l] = code;
+      t.count[l] = c;
+      t.base[l] = idx;
+      t.lim[l] = l <= 32 ? (code + c) << (32 - l) : 0;
+      code += c;
+      idx += c;
+      if (c && l > 0) mx = l;
+    }
+    t.maxlen = mx;
+  }
+}
+
+// LUT entry for every 12-bit prefix: (symbol << 6) | length for a code of
+// length <= 12 (same first-match rule as the reference's bit loop); for a
+// prefix of longer codes, (l0 << 6) with l0 the first length whose
+// left-aligned limit exceeds the prefix (decoding continues from l0 on the
+// register window); 0 if no code starts with the prefix.  lut[kLutSize]
+// holds the fast-path flag: 1 if the code is prefix-free (Kraft <= 1) and
+// max length <= 32.
+__device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
+                                           uint32_t *__restrict__ lut, int mode, uint32_t blk) {
+  __shared__ CodeTables t;
+  __shared__ unsigned s_ok;
+  build_tables(t, len_counts);
+  __syncthreads();
+  const int ci_mode = mode & 1;
+  uint32_t p = blk * blockDim.x + threadIdx.x;
+  if (threadIdx.x == 0) {
+    // Kraft sum in units of 2^-63
+    unsigned long long k = 0;
+    bool over = false;
+    for (int l = 1; l < 64 && !over; l++) {
+      unsigned long long add = (unsigned long long)t.count[l] << (63 - l);
+      if (t.count[l] >> l) over = true;  // count >= 2^l alone exceeds the budget
+      if (k + add < k) over = true;
+      k += add;
+      if (k > (1ull << 63)) over = true;
+    }
+    s_ok = (!over && t.maxlen <= 32) ? 1u : 0u;
+    if (p == 0) lut[kLutSize] = s_ok;
+  }
+  __syncthreads();
+  if (p >= (uint32_t)kLutSize) return;
+  uint32_t e = 0;
+  int lim = t.maxlen < (uint32_t)kLutBits ? (int)t.maxlen : kLutBits;
+  for (int l = 1; l <= lim; l++) {
+    unsigned long long code = p >> (kLutBits - l);
+    unsigned long long off = code - t.first[l];
+    if (off < t.count[l]) {
+      e = ((ci_mode ? (uint32_t)(t.base[l] + off) : canon[t.base[l] + off]) << 6) | (uint32_t)l;
+      break;
+    }
+  }
+  if (!e && t.maxlen > (uint32_t)kLutBits && t.maxlen <= 32) {
+    const unsigned long long w = (unsigned long long)p << (32 - kLutBits);
+    const unsigned long long w1 = w | ((1ull << (32 - kLutBits)) - 1);
+    int l0 = 0, l1 = 0;
+    for (int l = kLutBits + 1; l <= (int)t.maxlen; l++) {
+      unsigned long long limit = (t.first[l] + t.count[l]) << (32 - l);
+      if (!l0 && limit > w) l0 = l;
+      if (!l1 && limit > w1) l1 = l;
+    }
+    if (l0) e = (uint32_t)l0 << 6;
+    // mode bit1: every code behind the prefix has the same length -> "exact
+    // long" entry (length field 63): the decoder skips the limit probes
+    if ((mode & 2) && s_ok && l0 && l1 == l0) e |= 63u;
+  }
+  lut[p] = e;
+}
+
 // K4x u8 length table: lut8[p] = l0 when every code whose left-aligned
 // 32-bit value starts with the kXBits-bit prefix p has a length in
 // [l0, l0+3] (max length <= 32); 0 otherwise.  16 x 256 threads.
 constexpr int kXBits = 12;
-__device__ __forceinline__ void lut8_body(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8) {
+__device__ __forceinline__ void lut8_body(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8,
+                                          uint32_t blk) {
   __shared__ unsigned long long lim[65];  // (first + count) << (32 - l): exclusive left-aligned limit
   __shared__ uint32_t s_max;
   if (threadIdx.x == 0) {
@@ -369,7 +458,7 @@ __device__ __forceinline__ void lut8_body(const uint32_t *__restrict__ len_count
     s_max = mx;
   }
   __syncthreads();
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t p = blk * blockDim.x + threadIdx.x;
   if (p >= (1u << kXBits)) return;
   uint8_t e = 0;
   if (s_max >= 1 && s_max <= 32) {
@@ -386,6 +475,16 @@ __device__ __forceinline__ void lut8_body(const uint32_t *__restrict__ len_count
   lut8[p] = e;
 }
 
+
+// decode table rows [256*b, 256*b + 256) of a stream with plan p (the pack
+// kernel's first CTAs run it; same choice as launch_decode)
+__device__ __forceinline__ void table_rows_plan(const uint32_t *canon, const uint32_t *len_counts,
+                                                const actc_plan_t *p, void *table, int sw16, uint32_t blk) {
+  if (sw16 && p->live_symbols <= K4W_MAX_LIVE)
+    lut32_body(canon, len_counts, (uint32_t *)table, 2, blk);
+  else
+    lut8_body(len_counts, (uint8_t *)table, blk);
+}
 
 // decode table at compress time (k4_decode.cu): the table launch_decode
 // would build for this stream, chosen on the device from the plan
