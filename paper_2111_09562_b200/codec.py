@@ -863,8 +863,9 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
             if d is None:
                 if n != c.element_count:
                     raise FormatError(f"symbol count {n} != element count {c.element_count}")
-                c._ensure_index()
+                c._ensure_index()  # uploads / index rebuild on the caller's stream
                 d = c._desc()
+                ready = main.record_event()  # ... which the side stream must follow
             s = streams[slot]
             s.wait_event(ready)
             ctx = _lib.context_for(dev_index, slot)

@@ -311,3 +311,28 @@ def test_async_codebook_fallback_redo_and_memory(oracle):
     out = pb.decompress_batch([c2], dtype=torch.float64)[0]
     want = oracle.decompress_blob(ref.blob, x.size)
     assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+
+
+def test_compress_begin_end_with_caller_scratch(oracle):
+    """compress_begin/compress_end (the hooks' path): launched without a host
+    sync, symbol scratch from torch's allocator, private side slots; same
+    bytes as the reference, and the decode table carried by the container
+    reconstructs like a table built at decode time (from_bytes)."""
+    rng = np.random.default_rng(41)
+    xs = [np.maximum(rng.normal(0, 1, n), 0).astype(np.float32) for n in (300_001, 70_000, 5)]
+    ps = [pb.CodecParams(eb=e) for e in (1e-3, 1e-5, 1e-2)]
+    pend = [pc.compress_begin([torch.from_numpy(x).cuda()], [p], slot_base=1 + k, own_scratch=True)
+            for k, (x, p) in enumerate(zip(xs, ps))]
+    outs = [pc.compress_end(q, compact=True)[0] for q in pend]
+    for (c, rep), x, p in zip(outs, xs, ps):
+        ref = oracle.compress(x, p.eb, debug=False)
+        assert c.to_bytes() == ref.blob and rep.ratio == ref.ratio
+        want = oracle.decompress_blob(ref.blob, x.size)
+        got = pb.decompress_batch([c], dtype=torch.float64)[0]
+        again = pb.decompress_batch([pc.CompressedActivation.from_bytes(ref.blob)], dtype=torch.float64)[0]
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+        assert np.array_equal(again.cpu().numpy().reshape(-1).view(np.uint64), want.view(np.uint64))
+    assert outs[0][0]._desc().table_dev  # decode table built with the stream (async path)
+    with pytest.raises(ParameterError):
+        pc.compress_end(pend[0])
