@@ -453,7 +453,8 @@ def run_gpu(args, rank, world):
         # are queued up front (largest first); each tensor is compressed as
         # soon as its copy lands, reconstructed, and copied back while later
         # tensors are still crossing PCIe in the other direction
-        h2d_s.wait_stream(stream)
+        cur = torch.cuda.current_stream()
+        h2d_s.wait_stream(cur)
         ready = {}
         for i in e2e_order:
             with torch.cuda.stream(h2d_s):
@@ -466,20 +467,27 @@ def run_gpu(args, rank, world):
             d2h_s.wait_event(done[0])
             with torch.cuda.stream(d2h_s):
                 host_out[i].copy_(outs[i], non_blocking=True)
-        stream.wait_stream(d2h_s)
+        cur.wait_stream(d2h_s)
 
+    # the pipeline runs on its own (non-default) stream: work on the legacy
+    # default stream would serialise with the copy streams
+    e2e_main = torch.cuda.Stream()
     for _ in range(max(1, args.warmup // 2)):
-        e2e_step()
+        e2e_main.wait_stream(stream)
+        with torch.cuda.stream(e2e_main):
+            e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     e2e_ms = 0.0
     for _ in range(args.steps):
         flush.zero_()
+        e2e_main.wait_stream(stream)
         s0, s1 = ev(), ev()
-        s0.record(stream)
-        e2e_step()
-        s1.record(stream)
+        with torch.cuda.stream(e2e_main):
+            s0.record(e2e_main)
+            e2e_step()
+            s1.record(e2e_main)
         s1.synchronize()
         e2e_ms += s0.elapsed_time(s1)
     if world > 1:

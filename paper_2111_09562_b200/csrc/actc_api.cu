@@ -221,6 +221,39 @@ enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STA
 
 constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
+// Plan hand-off to pinned host memory.  A cudaMemcpyAsync D2H would queue
+// behind every earlier device-to-host copy on the copy engine (e.g. a
+// caller's 200 MB D2H of a reconstructed tensor on another stream); a kernel
+// storing into the mapped pinned buffer (UVA) lands as soon as the stream
+// reaches it.  Falls back to the copy for host memory the device cannot map.
+__global__ void k_plan_out(const actc_plan_t *__restrict__ src, actc_plan_t *dst) {
+  constexpr int W = (int)(sizeof(actc_plan_t) / 4);
+  static_assert(sizeof(actc_plan_t) % 4 == 0, "plan size");
+  if (threadIdx.x < W) reinterpret_cast<volatile uint32_t *>(dst)[threadIdx.x] = reinterpret_cast<const uint32_t *>(src)[threadIdx.x];
+  __threadfence_system();
+}
+
+int plan_to_host(actc_ctx *c, actc_plan_t *plan_host, cudaStream_t s) {
+  static thread_local const void *last_host = nullptr;
+  static thread_local void *last_dev = nullptr;
+  if (plan_host != last_host) {
+    cudaPointerAttributes at{};
+    void *dev = nullptr;
+    if (cudaPointerGetAttributes(&at, plan_host) == cudaSuccess && at.type == cudaMemoryTypeHost)
+      dev = at.devicePointer;
+    cudaGetLastError();
+    last_host = plan_host;
+    last_dev = dev;
+  }
+  if (last_dev) {
+    k_plan_out<<<1, 32, 0, s>>>(c->plan_dev, (actc_plan_t *)last_dev);
+    CKL();
+  } else {
+    CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  }
+  return ACTC_OK;
+}
+
 int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const uint16_t *in_lengths,
                  uint16_t *out_lengths, const unsigned long long *n_out, uint64_t n_symbols,
                  uint32_t sym_bytes, cudaStream_t s, const unsigned *nonfinite = nullptr) {
@@ -568,7 +601,7 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
   cudaStream_t s = (cudaStream_t)stream;
   int rc = launch_plan(c, x, n, eb, radius, chunk_lat, s);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  if ((rc = plan_to_host(c, plan_host, s))) return rc;
   return ACTC_OK;
 }
 
@@ -843,7 +876,7 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
       k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
   }
   CKL();
-  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  if ((rc = plan_to_host(c, plan_host, s))) return rc;
   c->mode = 0;  // the ctx holds no pending plan for actc_compress_encode
   return ACTC_OK;
 }
@@ -1163,7 +1196,7 @@ int actc_huffman_plan(actc_ctx *c, const uint32_t *sym, uint64_t n, uint64_t A, 
   CK(cudaStreamSynchronize(s));
   if (bad) return set_err(ACTC_EPARAM, "symbol out of alphabet range");
   if ((rc = run_codebook(c, (const unsigned long long *)c->hist.p, A, nullptr, lengths, nullptr, n, 4, s))) return rc;
-  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  if ((rc = plan_to_host(c, plan_host, s))) return rc;
   c->n = n;
   c->A = A;
   c->radius = 0;
@@ -1198,7 +1231,7 @@ int actc_code_lengths(actc_ctx *c, const uint64_t *freqs, uint64_t A, uint16_t *
   if (A < 1 || A > kMaxAlphabet) return set_err(ACTC_EPARAM, "bad alphabet size");
   int rc = run_codebook(c, (const unsigned long long *)freqs, A, nullptr, lengths, nullptr, 1, 4, s);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(plan_host, c->plan_dev, sizeof(actc_plan_t), cudaMemcpyDeviceToHost, s));
+  if ((rc = plan_to_host(c, plan_host, s))) return rc;
   return ACTC_OK;
 }
 
