@@ -246,6 +246,7 @@ int plan_to_host(actc_ctx *c, actc_plan_t *plan_host, cudaStream_t s) {
     last_dev = dev;
   }
   if (last_dev) {
+    KT(ACTC_KIND_CODEBOOK);  // the plan hand-off is the codebook's output
     k_plan_out<<<1, 32, 0, s>>>(c->plan_dev, (actc_plan_t *)last_dev);
     CKL();
   } else {
