@@ -307,7 +307,30 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   static const bool no_k2r = getenv("ACTC_K2_OLD") != nullptr;
   if (!in_lengths && A <= 65536 && n_symbols < (1ull << 32) && !no_k2r) {
     KT(ACTC_KIND_CODEBOOK);
-    k2r_codebook<<<1, K2_THREADS, kK2rSmem, s>>>(a);
+    // the single-CTA codebook sits on the critical path of its tensor's
+    // chain: highest execution priority, so a freed SM goes to it before the
+    // pending CTAs of other tensors' bandwidth kernels (ACTC_K2R_PRIO=0: off)
+    static const bool prio_off = getenv("ACTC_K2R_PRIO") && !strcmp(getenv("ACTC_K2R_PRIO"), "0");
+    if (!prio_off) {
+      static int hi = [] {
+        int lo = 0, h = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &h);
+        return h;
+      }();
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(1);
+      cfg.blockDim = dim3(K2_THREADS);
+      cfg.dynamicSmemBytes = kK2rSmem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributePriority;
+      at[0].val.priority = hi;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, k2r_codebook, a));
+    } else {
+      k2r_codebook<<<1, K2_THREADS, kK2rSmem, s>>>(a);
+    }
     a.gate = a.fallback;
   }
   if (!(a.gate && c->no_fallback)) {
