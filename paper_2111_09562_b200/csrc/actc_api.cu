@@ -217,7 +217,7 @@ CbLayout cb_layout(uint64_t A) {
 }
 
 // misc counters layout (u64 slots)
-enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SEGTICKET = 8, M_SLOTS = 9 };
+enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SEGTICKET = 8, M_PACKTICKET = 9, M_SLOTS = 10 };
 
 constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
@@ -233,18 +233,24 @@ __global__ void k_plan_out(const actc_plan_t *__restrict__ src, actc_plan_t *dst
   __threadfence_system();
 }
 
-int plan_to_host(actc_ctx *c, actc_plan_t *plan_host, cudaStream_t s) {
+// device alias of a pinned host buffer (UVA-mapped), or null
+void *mapped_alias(const void *host) {
   static thread_local const void *last_host = nullptr;
   static thread_local void *last_dev = nullptr;
-  if (plan_host != last_host) {
+  if (host != last_host) {
     cudaPointerAttributes at{};
     void *dev = nullptr;
-    if (cudaPointerGetAttributes(&at, plan_host) == cudaSuccess && at.type == cudaMemoryTypeHost)
+    if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost)
       dev = at.devicePointer;
     cudaGetLastError();
-    last_host = plan_host;
+    last_host = host;
     last_dev = dev;
   }
+  return last_dev;
+}
+
+int plan_to_host(actc_ctx *c, actc_plan_t *plan_host, cudaStream_t s) {
+  void *last_dev = mapped_alias(plan_host);
   if (last_dev) {
     KT(ACTC_KIND_CODEBOOK);  // the plan hand-off is the codebook's output
     k_plan_out<<<1, 32, 0, s>>>(c->plan_dev, (actc_plan_t *)last_dev);
@@ -874,6 +880,11 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   g.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_SEGTICKET);
   g.emit = c->emit;  // the count pass emits the canonical codes
   c->emit = EmitArgs{};
+  // the pack's last CTA hands the plan to the mapped mailbox (one launch
+  // less per tensor than the plan_to_host kernel); ACTC_PLAN_IN_PACK=0: off
+  static const bool plan_in_pack = !(getenv("ACTC_PLAN_IN_PACK") && !strcmp(getenv("ACTC_PLAN_IN_PACK"), "0"));
+  g.plan_host = plan_in_pack ? (actc_plan_t *)mapped_alias(plan_host) : nullptr;
+  g.pack_ticket = (unsigned *)((unsigned long long *)c->misc.p + M_PACKTICKET);
   g.table = c->table_out;  // the first pack CTAs build the decode table
   g.sw16 = 2ull * radius <= 65536 ? 1 : 0;
   c->table_out = nullptr;
@@ -900,7 +911,7 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
       k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
   }
   CKL();
-  if ((rc = plan_to_host(c, plan_host, s))) return rc;
+  if (!g.plan_host && (rc = plan_to_host(c, plan_host, s))) return rc;
   c->mode = 0;  // the ctx holds no pending plan for actc_compress_encode
   return ACTC_OK;
 }

@@ -460,10 +460,20 @@ __device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v, uint32_t p)
                ::"r"(addr), "r"(v), "r"(p) : "memory");
 }
 
+__device__ __forceinline__ void k3_plan_out(const SegArgs &a) {
+  constexpr int W = (int)(sizeof(actc_plan_t) / 4);
+  if (threadIdx.x < W)
+    reinterpret_cast<volatile uint32_t *>(a.plan_host)[threadIdx.x] = reinterpret_cast<const uint32_t *>(a.dplan)[threadIdx.x];
+  __threadfence_system();
+}
+
 template <typename SymT>
 __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
   extern __shared__ __align__(16) uint32_t k3p_sm[];
-  if (!seg_resolve(a)) return;
+  if (!seg_resolve(a)) {
+    if (a.plan_host && blockIdx.x == 0) k3_plan_out(a);  // the host redoes this stream: it needs the plan
+    return;
+  }
   if (a.table && a.dplan) {
     // the stream's decode table (kLutSize entries, 16 rows of 256), built
     // here by the first CTAs instead of a launch of its own
@@ -621,6 +631,20 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
         a.payload[gw0 + i] = v;
     }
     __syncwarp();
+  }
+  if (a.plan_host) {
+    // the last CTA to finish hands the plan to the mapped host mailbox
+    __shared__ unsigned k3p_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      k3p_last = atomicAdd(a.pack_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (k3p_last) {
+      k3_plan_out(a);
+      if (threadIdx.x == 0) *a.pack_ticket = 0u;
+    }
   }
 }
 

@@ -234,6 +234,8 @@ struct SegArgs {
   uint32_t *canon_out, *lencnt_out;
   EmitArgs emit;  // deferred k2s emission (rank_tab null: none)
   void *table;    // decode table built by the first pack CTAs (null: none)
+  actc_plan_t *plan_host;  // mapped pinned plan mailbox the pack's last CTA fills (null: none)
+  unsigned *pack_ticket;   // pack CTAs done (zero, reset by the last)
   int sw16;       // 16-bit symbols (the k4w / k4x choice of the table)
 };
 // resolve a device-planned SegArgs; false = this stream takes the host path
