@@ -103,6 +103,14 @@ void actc_ctx_destroy(actc_ctx *ctx);
 /* device bytes the context's scratch currently holds (cudaMalloc'ed by the
  * library, outside the caller's allocator) */
 uint64_t actc_ctx_device_bytes(const actc_ctx *ctx);
+/* Decode faults of every decoder launched on this context since the last
+ * call (ACTC_OK or ACTC_EFORMAT), including launches made without a result
+ * mailbox (batched decompression): the sticky word is copied to
+ * status_host (pinned; valid after the stream is synchronized) and reset.
+ * Replaces the FormatError huffman_decode / decompress raise at once
+ * (huffman.py:228-235, codec.py:356-359) for callers that defer the check
+ * to their next synchronisation point. */
+int actc_ctx_take_status(actc_ctx *ctx, uint32_t *status_host, actc_stream s);
 /* symbol scratch for the NEXT compress launch on this context (K1 writes
  * the n symbols, u16 when 2*radius <= 65536 else u32, plus 64 bytes; the
  * encoder reads them): lets a caller hand in stream-ordered memory from its

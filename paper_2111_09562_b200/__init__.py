@@ -7,6 +7,7 @@ codec stage runs as hand-written sm_100a CUDA in libactc.so (include/actc.h).
 from .codec import (
     CodecParams,
     CompressedActivation,
+    check_decode_status,
     CompressionReport,
     compress,
     compress_batch,

@@ -98,6 +98,7 @@ def lib():
             "actc_ctx_create": ([I, C.POINTER(P)], I),
             "actc_ctx_destroy": ([P], None),
             "actc_ctx_device_bytes": ([P], U64),
+            "actc_ctx_take_status": ([P, P, P], I),
             "actc_ctx_set_scratch": ([P, P, U64], I),
             "actc_ctx_set_table_out": ([P, P, U64], I),
             "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P, P], I),
@@ -130,7 +131,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = (
-    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_ctx_device_bytes actc_ctx_set_scratch actc_ctx_set_table_out actc_compress_plan "
+    "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_ctx_device_bytes actc_ctx_take_status actc_ctx_set_scratch actc_ctx_set_table_out actc_compress_plan "
     "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
@@ -203,6 +204,7 @@ class Context:
         self.plan_buf = torch.empty(C.sizeof(Plan), dtype=torch.uint8, pin_memory=True)
         self.dres_buf = torch.empty(C.sizeof(DecodeResult), dtype=torch.uint8, pin_memory=True)
         self.u64_buf = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+        self.sticky_buf = torch.zeros(4, dtype=torch.uint8, pin_memory=True)
 
     @property
     def plan(self) -> Plan:
@@ -253,6 +255,40 @@ def scratch_bytes(slots=None) -> int:
     return sum(int(L.actc_ctx_device_bytes(c.handle)) for sl, c in ctxs if slots is None or sl in slots)
 
 
+def _thread_contexts(device):
+    out = [c for d, c in getattr(_tls, "ctxs", {}).items() if d == device]
+    out += [c for (d, _slot), c in getattr(_tls, "extra", {}).items() if d == device]
+    return out
+
+
+def take_decode_status(device=None, stream=None):
+    """Queue the collection of every decode fault this thread's contexts on
+    `device` saw since the last collection (actc_ctx_take_status) on
+    `stream` (default: the device's current stream, which the batched
+    decoders' side streams were joined into).  Returns an event; pass it to
+    `decode_status_result` at the next natural synchronisation."""
+    torch = torch_cuda()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    sh, s = stream_handle(stream, dev)
+    L = lib()
+    for c in _thread_contexts(dev):
+        raise_for(L.actc_ctx_take_status(c.handle, C.c_void_p(c.sticky_buf.data_ptr()), sh))
+    return (dev, s.record_event())
+
+
+def decode_status_result(token) -> int:
+    """Wait for a take_decode_status event; ACTC_OK or ACTC_EFORMAT."""
+    import torch
+
+    dev, ev = token
+    ev.synchronize()
+    st = 0
+    for c in _thread_contexts(dev):
+        st |= int(c.sticky_buf.view(torch.int32).item())
+        c.sticky_buf.zero_()
+    return st
+
+
 def context_for(device: int, slot: int) -> Context:
     """Extra contexts for concurrent (multi-stream) compression: slot 0 is
     the thread's main context, slots 1.. are private scratch sets."""
@@ -269,7 +305,9 @@ def context_for(device: int, slot: int) -> Context:
     return c
 
 
-def stream_handle(stream=None):
+def stream_handle(stream=None, device=None):
+    """(cudaStream_t handle, torch stream): `stream`, else the current stream
+    of `device` (the tensor's device -- not necessarily the current one)."""
     torch = torch_cuda()
-    s = torch.cuda.current_stream() if stream is None else stream
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return C.c_void_p(s.cuda_stream), s

@@ -284,6 +284,12 @@ class CompressedActivation:
         return self._dev is not None
 
     @property
+    def device(self):
+        """CUDA device holding the container's buffers (uploaded to the
+        current device on first use when built from host fields)."""
+        return self._ensure_device()["payload"].device
+
+    @property
     def device_nbytes(self) -> int:
         """Bytes held in device memory by this container (payload + side data)."""
         if self._dev is None:
@@ -513,7 +519,7 @@ def compress_device(x, params: CodecParams, dims=None, stream=None):
         dims = (1,)
     n = x.numel()
     ctx = _lib.context(x.device.index)
-    sh, s = _lib.stream_handle(stream)
+    sh, s = _lib.stream_handle(stream, x.device)
     L = _lib.lib()
     flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if params.preserve_zeros else 0
     nchunks = (n + _lib.ACTC_CHUNK - 1) // _lib.ACTC_CHUNK
@@ -808,10 +814,11 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
     if c.symbol_count != n:
         raise FormatError(f"symbol count {c.symbol_count} != element count {n}")
     c._ensure_index()
-    ctx = _lib.context()
-    sh, s = _lib.stream_handle(stream)
+    dev = c.device
+    ctx = _lib.context(dev.index)
+    sh, s = _lib.stream_handle(stream, dev)
     if out is None:
-        out = torch.empty(c.dims, dtype=dtype, device="cuda")
+        out = torch.empty(c.dims, dtype=dtype, device=dev)
     code = _lib.ACTC_DTYPE_F32 if out.dtype == torch.float32 else _lib.ACTC_DTYPE_F64
     if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
         raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
@@ -832,8 +839,8 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
 def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=None):
     """Reconstruct several streams concurrently, each on its own stream and
     context (a small tensor's decode alone does not fill the GPU).  Results
-    are ordered on the caller's current stream; no host synchronisation, so
-    status and nonzero counts are not checked (decompress_device does that).
+    are ordered on the caller's current stream; no host synchronisation: decode
+    faults are collected by `check_decode_status` (one sync for many batches).
     If `done` is a list, it receives one CUDA event per stream (input order)
     recorded when that reconstruction is complete.
     """
@@ -892,6 +899,16 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
     if done is not None:
         done.extend(evs)
     return outs
+
+
+def check_decode_status(device=None):
+    """Raise FormatError if any decompression issued by this thread on
+    `device` since the last check met an invalid stream (bad code, stream
+    length mismatch, outlier markers that disagree with the stored indices;
+    huffman.py:228-235, codec.py:356-359).  `decompress_batch` does not
+    synchronise; this is its check, one host synchronisation for all."""
+    if _lib.decode_status_result(_lib.take_decode_status(device)):
+        raise FormatError("invalid code in bitstream or outlier markers disagree with stored indices")
 
 
 def decompress(c: CompressedActivation) -> Tensor:

@@ -1,6 +1,7 @@
 // actc_api.cu -- the C ABI (include/actc.h): context, scratch management and
 // launch orchestration of K1..K5.  No torch types cross this boundary.
 #include <float.h>
+#include <stddef.h>
 #include <stdarg.h>
 #include <math.h>
 #include <stdio.h>
@@ -149,9 +150,10 @@ inline uint64_t pow2_ge(uint64_t x) {
 struct DecResult {
   unsigned long long nonzero;
   unsigned long long markers;
-  unsigned status;
-  unsigned pad;
+  unsigned status;  // this call (reset when the caller asks for the result)
+  unsigned sticky;  // every decode on the context since the last actc_ctx_take_status
 };
+static_assert(offsetof(DecResult, sticky) == offsetof(DecResult, status) + 4, "report_format_error layout");
 
 }  // namespace
 
@@ -310,14 +312,12 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
   // frequency-class codebook first; it hands over to k2_codebook (gated)
   // when its capacities are exceeded
-  static const bool no_k2r = getenv("ACTC_K2_OLD") != nullptr;
-  if (!in_lengths && A <= 65536 && n_symbols < (1ull << 32) && !no_k2r) {
+  if (!in_lengths && A <= 65536 && n_symbols < (1ull << 32)) {
     KT(ACTC_KIND_CODEBOOK);
     // the single-CTA codebook sits on the critical path of its tensor's
     // chain: highest execution priority, so a freed SM goes to it before the
-    // pending CTAs of other tensors' bandwidth kernels (ACTC_K2R_PRIO=0: off)
-    static const bool prio_off = getenv("ACTC_K2R_PRIO") && !strcmp(getenv("ACTC_K2R_PRIO"), "0");
-    if (!prio_off) {
+    // pending CTAs of other tensors' bandwidth kernels
+    {
       static int hi = [] {
         int lo = 0, h = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &h);
@@ -334,8 +334,6 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
       cfg.attrs = at;
       cfg.numAttrs = 1;
       CK(cudaLaunchKernelEx(&cfg, k2r_codebook, a));
-    } else {
-      k2r_codebook<<<1, K2_THREADS, kK2rSmem, s>>>(a);
     }
     a.gate = a.fallback;
   }
@@ -477,6 +475,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
     delete c;
     return set_err(ACTC_ENOMEM, "ctx alloc failed");
   }
+  cudaMemset(c->dres_dev, 0, sizeof(DecResult));
   int rc;
   if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, 4 * kLutWords))) {
     delete c;
@@ -487,15 +486,10 @@ int actc_ctx_create(int device, actc_ctx **out) {
   int nb = 0;
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  const void *big[] = {(const void *)k3_count<uint16_t, false>, (const void *)k3_count<uint16_t, true>,
-                       (const void *)k3_count<uint32_t, false>, (const void *)k3_count<uint32_t, true>,
-                       (const void *)k3_pack<uint16_t, false>,  (const void *)k3_pack<uint16_t, true>,
-                       (const void *)k3_pack<uint32_t, false>,  (const void *)k3_pack<uint32_t, true>,
-                       (const void *)k4w_decode<0, 16, false>,  (const void *)k4w_decode<1, 16, false>,
+  const void *big[] = {(const void *)k4w_decode<0, 16, false>,  (const void *)k4w_decode<1, 16, false>,
                        (const void *)k4w_decode<0, 32, false>,  (const void *)k4w_decode<1, 32, false>,
                        (const void *)k4w_decode<2, 32, false>,  (const void *)k4w_decode<0, 16, true>,
-                       (const void *)k4w_decode<1, 16, true>,   (const void *)k3_encode_lb<uint16_t>,
-                       (const void *)k3_encode_lb<uint32_t>,    (const void *)k3_seg_pack<uint16_t>,
+                       (const void *)k4w_decode<1, 16, true>,   (const void *)k3_seg_pack<uint16_t>,
                        (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
                        (const void *)k3_seg_count<uint32_t>,    (const void *)k1_quant_lorenzo_hist<uint16_t>,
                        (const void *)k1_quant_lorenzo_hist<uint32_t>, (const void *)k_hist_u32};
@@ -532,6 +526,13 @@ int actc_ctx_set_table_out(actc_ctx *c, void *table_dev, uint64_t bytes) {
 int actc_ctx_set_scratch(actc_ctx *c, void *sym_dev, uint64_t bytes) {
   c->sym_ext = sym_dev;
   c->sym_ext_bytes = sym_dev ? bytes : 0;
+  return ACTC_OK;
+}
+
+int actc_ctx_take_status(actc_ctx *c, uint32_t *status_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(status_host, &c->dres_dev->sticky, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemsetAsync(&c->dres_dev->sticky, 0, 4, s));
   return ACTC_OK;
 }
 
@@ -638,172 +639,73 @@ int actc_compress_plan(actc_ctx *c, const float *x, uint64_t n, double eb, uint3
 static int launch_encode(actc_ctx *c, const void *sym, uint32_t sb, uint64_t n, const float *x,
                          const actc_plan_t *plan, uint8_t *payload, uint64_t *out_idx, float *out_val,
                          uint64_t *chunk_off, int extract, cudaStream_t s) {
-  const uint64_t ntiles = cdiv(n, K3_TILE);
   int rc;
-  // code-table window: the live symbol range, capped
-  const bool wide = plan->max_len > (uint32_t)K3_SHORT_MAXLEN;
-  const uint32_t cap = wide ? K3_WIN64 : K3_WIN32;
+  // the segment encoder's (code << 8 | len) table holds codes of up to 56
+  // bits; a longer Huffman code needs > Fib(58) ~ 5.9e11 symbols, more than
+  // a tensor in 180 GB of HBM can hold -- rejected loudly, never truncated
+  if (plan->max_len > 56) return set_err(ACTC_EPARAM, "Huffman code length %u exceeds the device encoder's 56 bits",
+                                         plan->max_len);
   uint32_t lo = plan->sym_lo, hi = plan->sym_hi;
   uint32_t span = hi >= lo ? hi - lo + 1 : 1;
-  uint32_t win_lo = lo, win_n = span;
-  if (span > cap) {
-    // centre the window on the radius (symbol of a zero delta), clamp to the live range
+  // code-table window of the pack pass: the live range, capped and centred
+  // on the radius (symbol of a zero delta)
+  uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
+  if (span > K3L_WIN) {
     uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
-    uint32_t wl = centre > cap / 2 ? centre - cap / 2 : 0;
+    uint32_t wl = centre > K3L_WIN / 2 ? centre - K3L_WIN / 2 : 0;
     if (wl < lo) wl = lo;
-    if (wl + cap > hi + 1) wl = hi + 1 - cap;
-    win_lo = wl;
-    win_n = cap;
+    if (wl + K3L_WIN > hi + 1) wl = hi + 1 - K3L_WIN;
+    lwin_lo = wl;
   }
-  static const bool k3_two_pass = getenv("ACTC_K3_TWO_PASS") != nullptr;
-  static const bool k3_lb = getenv("ACTC_K3_LB") != nullptr;
-  if (!k3_two_pass && (!wide || !k3_lb)) {
-    uint32_t lwin_lo = lo, lwin_n = std::min<uint32_t>(span, K3L_WIN);
-    if (span > K3L_WIN) {
-      uint32_t centre = c->radius ? c->radius : (lo + hi) / 2;
-      uint32_t wl = centre > K3L_WIN / 2 ? centre - K3L_WIN / 2 : 0;
-      if (wl < lo) wl = lo;
-      if (wl + K3L_WIN > hi + 1) wl = hi + 1 - K3L_WIN;
-      lwin_lo = wl;
-    }
-    if (!k3_lb) {
-      // two passes over 1024-symbol segments, no inter-warp waiting
-      const uint64_t nseg = cdiv(n, K3L_SEG);
-      SegArgs g{};
-      g.n = n;
-      g.ctab = (const unsigned long long *)c->ctab.p;
-      g.len8 = (const uint8_t *)c->len8.p;
-      g.lo = lo;
-      g.span = span;
-      g.win_lo = lwin_lo;
-      g.win_n = lwin_n;
-      const bool l8 = span <= 65536;
-      const size_t csm = l8 ? (size_t)((((lo & 15u) + span + 15) & ~15u)) : 16;
-      const size_t psm = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
-      const void *fc = sb == 2 ? (const void *)k3_seg_count<uint16_t> : (const void *)k3_seg_count<uint32_t>;
-      const void *fp = sb == 2 ? (const void *)k3_seg_pack<uint16_t> : (const void *)k3_seg_pack<uint32_t>;
-      int occ_c = 0, occ_p = 0;
-      occ_c = occupancy(fc, K3L_THREADS, csm);
-      occ_p = occupancy(fp, K3L_THREADS, psm);
-      const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
-      g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
-      g.ncta = (uint32_t)cdiv(nseg, g.spc);
-      if ((rc = grow(c->status, nseg * 9 + (size_t)g.ncta * 16 + 1024))) return rc;
-      g.cta_bits = (unsigned long long *)c->status.p;
-      g.cta_nz = g.cta_bits + g.ncta;
-      g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
-      g.seg_nz = g.seg_bits + nseg;
-      g.seg_long = (uint8_t *)(g.seg_nz + nseg);
-      g.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_SEGTICKET);
-      g.x = x;
-      g.payload = (uint32_t *)payload;
-      g.out_idx = (unsigned long long *)out_idx;
-      g.out_val = out_val;
-      g.chunk_off = (unsigned long long *)chunk_off;
-      g.extract = extract;
-      g.k = plan->n_outliers;
-      CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
-      const int gp = (int)std::max<uint64_t>(
-          1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), (uint64_t)std::max(1, occ_p) * c->num_sms));
-      {
-        KT(ACTC_KIND_COUNT);
-        if (sb == 2)
-          k3_seg_count<uint16_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint16_t *)sym, g);
-        else
-          k3_seg_count<uint32_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint32_t *)sym, g);
-      }
-      {
-        KT(ACTC_KIND_PACK);
-        if (sb == 2)
-          k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, g);
-        else
-          k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
-      }
-      CKL();
-      return ACTC_OK;
-    }
-    // single pass: decoupled look-back over 8-segment tiles
-    const uint64_t nseg = cdiv(n, (uint64_t)K3L_SEG * (K3L_THREADS / 32));  // look-back tiles
-    const size_t smem = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
-    if ((rc = grow(c->status, nseg * 16 + 1024))) return rc;
-    EncLB st;
-    st.stat = (unsigned long long *)c->status.p;
-    st.incnz = st.stat + nseg;
-    unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
-    CK(cudaMemsetAsync(st.stat, 0, nseg * 16, s));
-    CK(cudaMemsetAsync(ticket, 0, 4, s));
-    CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
-    const void *f = sb == 2 ? (const void *)k3_encode_lb<uint16_t> : (const void *)k3_encode_lb<uint32_t>;
-    int occ = 0;
-    occ = occupancy(f, K3L_THREADS, smem);
-    const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nseg, want));
-    {
-      KT(ACTC_KIND_PACK);
-      if (sb == 2)
-        k3_encode_lb<uint16_t><<<grid, K3L_THREADS, smem, s>>>((const uint16_t *)sym, n, (const unsigned long long *)c->ctab.p,
-                                                               lwin_lo, lwin_n, x, (uint32_t *)payload,
-                                                               (unsigned long long *)out_idx, out_val,
-                                                               (unsigned long long *)chunk_off, st, ticket, extract);
-      else
-        k3_encode_lb<uint32_t><<<grid, K3L_THREADS, smem, s>>>((const uint32_t *)sym, n, (const unsigned long long *)c->ctab.p,
-                                                               lwin_lo, lwin_n, x, (uint32_t *)payload,
-                                                               (unsigned long long *)out_idx, out_val,
-                                                               (unsigned long long *)chunk_off, st, ticket, extract);
-    }
-    CKL();
-    return ACTC_OK;
-  }
-  const uint32_t maxlen = plan->max_len ? plan->max_len : 1;
-  const uint32_t word_cap = (uint32_t)(((uint64_t)2 * K3_TILE * maxlen + 31) / 32 + 4);  // pack tile = 2*K3_TILE
-  const size_t tbl = (((size_t)win_n * (wide ? 8 : 4) + 15) & ~size_t(15));
-  const size_t smem_pack = tbl + (size_t)word_cap * 4;
-  // the count pass only needs lengths: a byte per symbol over the whole live range
-  const uint32_t cwin_lo = lo, cwin_n = std::min<uint32_t>(span, 65536u);
-  const size_t smem_count = (cwin_n + 15) & ~15u;
-  const void *fc, *fp;
-  if (sb == 2) {
-    fc = wide ? (const void *)k3_count<uint16_t, true> : (const void *)k3_count<uint16_t, false>;
-    fp = wide ? (const void *)k3_pack<uint16_t, true> : (const void *)k3_pack<uint16_t, false>;
-  } else {
-    fc = wide ? (const void *)k3_count<uint32_t, true> : (const void *)k3_count<uint32_t, false>;
-    fp = wide ? (const void *)k3_pack<uint32_t, true> : (const void *)k3_pack<uint32_t, false>;
-  }
-  int occ = 0;
-  occ = occupancy(fp, K3_THREADS, smem_pack);
-  const uint64_t want = (uint64_t)std::max(1, occ) * c->num_sms;
-  const uint64_t tpc = cdiv(ntiles, std::min<uint64_t>(ntiles, want));
-  const uint32_t ncta = (uint32_t)cdiv(ntiles, tpc);
-  // scratch: cta_bits, cta_nz, cta_bit0, cta_nz0 (u64) + head, tail (u32)
-  if ((rc = grow(c->status, (size_t)ncta * (8 * 4 + 8) + 1024))) return rc;
-  unsigned long long *cbits = (unsigned long long *)c->status.p;
-  unsigned long long *cnz = cbits + ncta, *cbit0 = cnz + ncta, *cnz0 = cbit0 + ncta;
-  uint32_t *head = (uint32_t *)(cnz0 + ncta), *tail = head + ncta;
-  unsigned long long *misc = (unsigned long long *)c->misc.p;
-  const unsigned long long *ct = (const unsigned long long *)c->ctab.p;
-#define K3_LAUNCH(T, W)                                                                                        \
-  do {                                                                                                         \
-    { KT(ACTC_KIND_COUNT);                                                                                     \
-      k3_count<T, W><<<ncta, K3_THREADS, smem_count, s>>>((const T *)sym, n, ct, cwin_lo, cwin_n, tpc, cbits, cnz); } \
-    { KT(ACTC_KIND_SCAN);                                                                                      \
-      k_excl_scan_u64<<<1, 1024, 0, s>>>(cbits, ncta, cbit0, misc + M_SCAN_TOT); }                             \
-    { KT(ACTC_KIND_SCAN);                                                                                      \
-      k_excl_scan_u64<<<1, 1024, 0, s>>>(cnz, ncta, cnz0, misc + M_SCAN_TOT2); }                               \
-    KT(ACTC_KIND_PACK);                                                                                        \
-    k3_pack<T, W><<<ncta, K3_THREADS, smem_pack, s>>>((const T *)sym, n, ct, win_lo, win_n, word_cap, tpc, x,  \
-                                                      cbit0, cnz0, (uint32_t *)payload,                        \
-                                                      (unsigned long long *)out_idx, out_val,                  \
-                                                      (unsigned long long *)chunk_off, head, tail, extract);   \
-  } while (0)
-  if (sb == 2) {
-    if (wide) K3_LAUNCH(uint16_t, true); else K3_LAUNCH(uint16_t, false);
-  } else {
-    if (wide) K3_LAUNCH(uint32_t, true); else K3_LAUNCH(uint32_t, false);
-  }
-#undef K3_LAUNCH
+  // two passes over 1024-symbol segments, no inter-warp waiting
+  const uint64_t nseg = cdiv(n, K3L_SEG);
+  SegArgs g{};
+  g.n = n;
+  g.ctab = (const unsigned long long *)c->ctab.p;
+  g.len8 = (const uint8_t *)c->len8.p;
+  g.lo = lo;
+  g.span = span;
+  g.win_lo = lwin_lo;
+  g.win_n = lwin_n;
+  const bool l8 = span <= 65536;
+  const size_t csm = l8 ? (size_t)((((lo & 15u) + span + 15) & ~15u)) : 16;
+  const size_t psm = (size_t)((lwin_n + 3) & ~3u) * 4 + (size_t)(K3L_THREADS / 32) * K3L_WORDS * 4;
+  const void *fc = sb == 2 ? (const void *)k3_seg_count<uint16_t> : (const void *)k3_seg_count<uint32_t>;
+  const void *fp = sb == 2 ? (const void *)k3_seg_pack<uint16_t> : (const void *)k3_seg_pack<uint32_t>;
+  const int occ_c = occupancy(fc, K3L_THREADS, csm), occ_p = occupancy(fp, K3L_THREADS, psm);
+  const uint64_t want_c = (uint64_t)std::max(1, occ_c) * c->num_sms;
+  g.spc = std::max<uint64_t>(K3L_THREADS / 32, cdiv(nseg, want_c));
+  g.ncta = (uint32_t)cdiv(nseg, g.spc);
+  if ((rc = grow(c->status, nseg * 9 + (size_t)g.ncta * 16 + 1024))) return rc;
+  g.cta_bits = (unsigned long long *)c->status.p;
+  g.cta_nz = g.cta_bits + g.ncta;
+  g.seg_bits = (uint32_t *)(g.cta_nz + g.ncta);
+  g.seg_nz = g.seg_bits + nseg;
+  g.seg_long = (uint8_t *)(g.seg_nz + nseg);
+  g.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_SEGTICKET);
+  g.x = x;
+  g.payload = (uint32_t *)payload;
+  g.out_idx = (unsigned long long *)out_idx;
+  g.out_val = out_val;
+  g.chunk_off = (unsigned long long *)chunk_off;
+  g.extract = extract;
+  g.k = plan->n_outliers;
+  CK(cudaMemsetAsync(payload, 0, 4 * cdiv(plan->payload_bits, 32) + 8, s));
+  const int gp = (int)std::max<uint64_t>(
+      1, std::min<uint64_t>(cdiv(nseg, K3L_THREADS / 32), (uint64_t)std::max(1, occ_p) * c->num_sms));
   {
-    KT(ACTC_KIND_FIXUP);
-    k3_fixup<<<1, 1024, 0, s>>>((uint32_t *)payload, cbit0, cbits, head, tail, ncta);
+    KT(ACTC_KIND_COUNT);
+    if (sb == 2)
+      k3_seg_count<uint16_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint16_t *)sym, g);
+    else
+      k3_seg_count<uint32_t><<<g.ncta, K3L_THREADS, csm, s>>>((const uint32_t *)sym, g);
+  }
+  {
+    KT(ACTC_KIND_PACK);
+    if (sb == 2)
+      k3_seg_pack<uint16_t><<<gp, K3L_THREADS, psm, s>>>((const uint16_t *)sym, g);
+    else
+      k3_seg_pack<uint32_t><<<gp, K3L_THREADS, psm, s>>>((const uint32_t *)sym, g);
   }
   CKL();
   return ACTC_OK;
@@ -881,9 +783,8 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   g.emit = c->emit;  // the count pass emits the canonical codes
   c->emit = EmitArgs{};
   // the pack's last CTA hands the plan to the mapped mailbox (one launch
-  // less per tensor than the plan_to_host kernel); ACTC_PLAN_IN_PACK=0: off
-  static const bool plan_in_pack = !(getenv("ACTC_PLAN_IN_PACK") && !strcmp(getenv("ACTC_PLAN_IN_PACK"), "0"));
-  g.plan_host = plan_in_pack ? (actc_plan_t *)mapped_alias(plan_host) : nullptr;
+  // less per tensor than the plan_to_host kernel)
+  g.plan_host = (actc_plan_t *)mapped_alias(plan_host);
   g.pack_ticket = (unsigned *)((unsigned long long *)c->misc.p + M_PACKTICKET);
   g.table = c->table_out;  // the first pack CTAs build the decode table
   g.sw16 = 2ull * radius <= 65536 ? 1 : 0;
@@ -942,7 +843,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     CK(cudaMemsetAsync(ticket, 0, 8, s));
   }
   // the result mailbox is only read back when the caller asks for it
-  if ((res_host || !warp_dec) && phase != 1) CK(cudaMemsetAsync(c->dres_dev, 0, sizeof(DecResult), s));
+  if ((res_host || !warp_dec) && phase != 1) CK(cudaMemsetAsync(c->dres_dev, 0, offsetof(DecResult, sticky), s));
   // decoder choice for indexed streams: the warp decoder with symbols
   // resolved in the decode chain while the canonical table fits its shared
   // cache; the lane decoder (sequential reconstruction, canonical indices
@@ -1181,8 +1082,10 @@ int actc_lorenzo_encode(const int64_t *lat, uint64_t n, uint32_t radius, const u
                         uint64_t *n_out_host, actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (radius < 2) return set_err(ACTC_EPARAM, "radius must be >= 2, got %u", radius);
-  static thread_local unsigned long long *d_cnt = nullptr;
-  if (!d_cnt) CK(cudaMalloc(&d_cnt, 8));
+  // stream-ordered scratch word on the stream's device (no per-thread
+  // cache: a thread may drive several devices and streams)
+  unsigned long long *d_cnt = nullptr;
+  CK(cudaMallocAsync((void **)&d_cnt, 8, s));
   CK(cudaMemsetAsync(d_cnt, 0, 8, s));
   if (n) {
     int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 16);
@@ -1191,14 +1094,15 @@ int actc_lorenzo_encode(const int64_t *lat, uint64_t n, uint32_t radius, const u
     CKL();
   }
   CK(cudaMemcpyAsync(n_out_host, d_cnt, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d_cnt, s));
   return ACTC_OK;
 }
 
 int actc_lorenzo_decode(const uint32_t *sym, uint64_t n, const int64_t *olat, uint64_t k, uint32_t radius,
                         int64_t *out, uint32_t *status_host, actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  static thread_local unsigned *d_st = nullptr;
-  if (!d_st) CK(cudaMalloc(&d_st, 4));
+  unsigned *d_st = nullptr;  // stream-ordered scratch word
+  CK(cudaMallocAsync((void **)&d_st, 4, s));
   CK(cudaMemsetAsync(d_st, 0, 4, s));
   {
     KT(ACTC_KIND_DEBUG);
@@ -1206,6 +1110,7 @@ int actc_lorenzo_decode(const uint32_t *sym, uint64_t n, const int64_t *olat, ui
   }
   CKL();
   CK(cudaMemcpyAsync(status_host, d_st, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d_st, s));
   return ACTC_OK;
 }
 
@@ -1272,8 +1177,8 @@ int actc_code_lengths(actc_ctx *c, const uint64_t *freqs, uint64_t A, uint16_t *
 
 int actc_count_nonzero(const void *x, int dtype, uint64_t n, uint64_t *out_host, actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  static thread_local unsigned long long *d = nullptr;
-  if (!d) CK(cudaMalloc(&d, 8));
+  unsigned long long *d = nullptr;  // stream-ordered scratch word
+  CK(cudaMallocAsync((void **)&d, 8, s));
   CK(cudaMemsetAsync(d, 0, 8, s));
   if (n) {
     int grid = (int)std::min<uint64_t>(cdiv(n, 256), 148 * 8);
@@ -1282,6 +1187,7 @@ int actc_count_nonzero(const void *x, int dtype, uint64_t n, uint64_t *out_host,
     CKL();
   }
   CK(cudaMemcpyAsync(out_host, d, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d, s));
   return ACTC_OK;
 }
 

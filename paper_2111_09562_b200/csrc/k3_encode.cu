@@ -1,75 +1,27 @@
 // K3: canonical-Huffman encode + MSB-first bit packing + outlier
-// extraction + decode chunk index, as reduce-then-scan:
+// extraction + decode chunk index.
 //
-//   k3_count   each CTA owns a contiguous range of tiles; sums code lengths
-//              and outlier markers of its range (symbols read once)
-//   k_excl_scan_u64   tiny scan of the per-CTA totals -> each CTA's first
-//              bit / first outlier rank
-//   k3_pack    each CTA re-walks its range with its exact start bit:
-//              (code, len) from a shared-memory copy of the code table
-//              (live symbol range), block scan, codes packed into a shared
-//              word buffer (plain stores for words a thread owns, atomicOr
-//              for the two it shares), big-endian word stores (byte order ==
-//              np.packbits, huffman.py:206).  The partial word between two
-//              tiles of one CTA is carried in shared memory; the first/last
-//              word of each CTA go to side slots merged by
-//   k3_fixup   one CTA, one thread per CTA boundary.
-// No CTA ever waits on another, so there is no look-back latency on the
-// critical path.  Replaces huffman.py:188-207 and codec.py:321-322.
+// Replaces huffman.py:188-207 (code lookup, np.packbits) and codec.py:321-322
+// (outlier indices / values).  Two barrier-free passes over 1024-symbol
+// segments (see the section comment below).
 #include "kernels.cuh"
 
 namespace actc {
 
 namespace {
 
-template <bool WIDE>
-struct Ent;
-template <>
-struct Ent<false> {
-  using T = uint32_t;
-};
-template <>
-struct Ent<true> {
-  using T = unsigned long long;
-};
-
-struct Packer {
-  uint32_t *words;
-  uint32_t w;
-  uint32_t first_w;
-  unsigned long long buf;
-  int nb;
-  __device__ __forceinline__ void emit(uint32_t v) {
-    if (w == first_w)
-      atomicOr(&words[w], v);
-    else
-      words[w] = v;  // fully owned by this thread
-    w++;
-  }
-  __device__ __forceinline__ void put(uint32_t code, int len) {  // len <= 32, nb <= 31
-    buf |= (unsigned long long)code << (64 - nb - len);
-    nb += len;
-    if (nb >= 32) {
-      emit((uint32_t)(buf >> 32));
-      buf <<= 32;
-      nb -= 32;
-    }
-  }
-  __device__ __forceinline__ void finish() {
-    if (nb > 0) atomicOr(&words[w], (uint32_t)(buf >> 32));
-  }
-};
+constexpr uint32_t kSent = 0xFFFFFFFFu;  // symbol past the end of the stream
 
 template <typename SymT>
-__device__ __forceinline__ void load_syms(const SymT *__restrict__ sym, uint64_t base, uint64_t n,
-                                          uint32_t (&s)[K3_EPT]) {
-  if (base + K3_EPT <= n) {
+__device__ __forceinline__ void lb_load(const SymT *__restrict__ sym, uint64_t base, uint64_t n,
+                                        uint32_t (&s)[K3L_EPT]) {
+  if (base + K3L_EPT <= n) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
     if (sizeof(SymT) == 2) {
-      const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
 #pragma unroll
-      for (int j = 0; j < K3_EPT / 8; j++) {
-        uint4 v = __ldg(p + j);
-        uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < K3L_EPT / 8; j++) {
+        const uint4 v = __ldcs(p + j);  // streaming: the symbol buffer is read once
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           s[8 * j + 2 * k] = w4[k] & 0xFFFFu;
@@ -77,322 +29,413 @@ __device__ __forceinline__ void load_syms(const SymT *__restrict__ sym, uint64_t
         }
       }
     } else {
-      const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
 #pragma unroll
-      for (int j = 0; j < K3_EPT / 4; j++) {
-        uint4 v = __ldg(p + j);
+      for (int j = 0; j < K3L_EPT / 4; j++) {
+        const uint4 v = __ldcs(p + j);
         s[4 * j] = v.x; s[4 * j + 1] = v.y; s[4 * j + 2] = v.z; s[4 * j + 3] = v.w;
       }
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < K3_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : 0u;
-  }
-}
-
-template <bool WIDE>
-__device__ __forceinline__ void load_table(typename Ent<WIDE>::T *sh, const unsigned long long *__restrict__ ctab,
-                                           uint32_t win_lo, uint32_t win_n) {
-  for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) {
-    unsigned long long e = ctab[win_lo + i];
-    if (WIDE)
-      sh[i] = (typename Ent<WIDE>::T)e;
-    else
-      sh[i] = (typename Ent<WIDE>::T)(((e >> 8) << 6) | (e & 63));  // (code << 6) | len
-  }
-}
-
-template <bool WIDE>
-__device__ __forceinline__ void lookup(const typename Ent<WIDE>::T *sh, const unsigned long long *__restrict__ ctab,
-                                       uint32_t win_lo, uint32_t win_n, uint32_t s, unsigned long long &code,
-                                       uint32_t &len) {
-  const uint32_t wi = s - win_lo;
-  if (WIDE) {
-    unsigned long long e = wi < win_n ? (unsigned long long)sh[wi] : __ldg(&ctab[s]);
-    len = (uint32_t)(e & 0xFF);
-    code = e >> 8;
-  } else {
-    uint32_t e;
-    if (wi < win_n) {
-      e = (uint32_t)sh[wi];
-    } else {
-      unsigned long long g = __ldg(&ctab[s]);
-      e = (uint32_t)(((g >> 8) << 6) | (g & 63));
-    }
-    len = e & 63;
-    code = e >> 6;
+    for (int j = 0; j < K3L_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : kSent;
   }
 }
 
 }  // namespace
 
-template <typename SymT, bool WIDE>
-__global__ void __launch_bounds__(K3_THREADS) k3_count(const SymT *__restrict__ sym, uint64_t n,
-                                                       const unsigned long long *__restrict__ ctab,
-                                                       uint32_t win_lo, uint32_t win_n, uint64_t tiles_per_cta,
-                                                       unsigned long long *__restrict__ cta_bits,
-                                                       unsigned long long *__restrict__ cta_nz) {
-  // code lengths only: one byte per symbol of the window (whole 64K alphabet fits)
-  extern __shared__ __align__(16) unsigned char len8[];
-  __shared__ unsigned long long wb[K3_THREADS / 32], wz[K3_THREADS / 32];
-  for (uint32_t i = threadIdx.x; i < win_n; i += K3_THREADS) len8[i] = (unsigned char)(ctab[win_lo + i] & 0xFF);
-  __syncthreads();
-  const uint64_t ntiles = (n + K3_TILE - 1) / K3_TILE;
-  const uint64_t t0 = blockIdx.x * tiles_per_cta, t1 = min(ntiles, t0 + tiles_per_cta);
-  uint32_t bits = 0, nz = 0;  // per tile <= 16 * 63 bits, flushed to 64-bit per tile
-  unsigned long long bits64 = 0, nz64 = 0;
-  for (uint64_t tile = t0; tile < t1; tile++) {
-    const uint64_t base = tile * K3_TILE + (uint64_t)threadIdx.x * K3_EPT;
-    uint32_t s[K3_EPT];
-    load_syms(sym, base, n, s);
-    bits = 0;
-    nz = 0;
-    if (base + K3_EPT <= n) {
+// ===========================================================================
+// Two-pass, barrier-free variant (the production path for codes <= 26 bits):
+//   k3_seg_count  CTA b owns segments [b*spc, (b+1)*spc); warp per 1024-symbol
+//                 segment sums code lengths (byte table of the live range in
+//                 shared memory) and outlier markers; the CTA then turns its
+//                 segment counts into exclusive in-CTA prefixes and writes its
+//                 totals
+//                 (the last count CTA turns the CTA totals into exclusive prefixes)
+//   k3_seg_pack   warp per segment at bit cta_prefix + in-CTA prefix: one
+//                 (code, len) lookup per symbol into registers, pack, store
+// Symbols are read twice (2 x 2 B), but no warp ever waits for another.
+// ===========================================================================
+
+constexpr uint32_t K3S_L8MAX = 65536;  // byte length table in shared memory (u16 symbol range)
+
+__device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned long long *__restrict__ ctab,
+                                               uint32_t win_lo, uint32_t win_n, int nthreads) {
+  for (uint32_t i0 = threadIdx.x; i0 < win_n; i0 += 16 * nthreads) {
+    unsigned long long e[16];
 #pragma unroll
-      for (int j = 0; j < K3_EPT; j++) {
-        const uint32_t wi = s[j] - win_lo;
-        bits += wi < win_n ? (uint32_t)len8[wi] : (uint32_t)(__ldg(&ctab[s[j]]) & 0xFF);
-        nz += s[j] == 0;
+    for (int u = 0; u < 16; u++) {
+      const uint32_t i = i0 + u * nthreads;
+      e[u] = i < win_n ? __ldg(&ctab[win_lo + i]) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const uint32_t i = i0 + u * nthreads;
+      if (i < win_n) tab[i] = (uint32_t)(((e[u] >> 8) << 6) | (e[u] & 63));
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t k3c_saddr(const void *p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t k3c_ldsb(uint32_t a) {
+  unsigned short v;
+  asm("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+
+template <typename SymT>
+__global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restrict__ sym, SegArgs a) {
+  extern __shared__ __align__(16) uint8_t k3c_l8[];
+  __shared__ unsigned long long wsum_b[K3L_THREADS / 32 + 1], wsum_z[K3L_THREADS / 32 + 1];
+  if (!seg_resolve(a)) return;
+  if (a.dplan) {
+    // device-planned: zero the payload (the pack ORs boundary words)
+    const uint64_t nw = (a.dplan->payload_bits + 31) / 32 + 2;
+    for (uint64_t i = (uint64_t)blockIdx.x * K3L_THREADS + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * K3L_THREADS)
+      a.payload[i] = 0u;
+    if (a.canon_src) {
+      // the table is in ctx scratch: copy it to the caller's buffers
+      const uint32_t live = a.dplan->live_symbols;
+      for (uint32_t i = blockIdx.x * K3L_THREADS + threadIdx.x; i < live; i += gridDim.x * K3L_THREADS)
+        a.canon_out[i] = a.canon_src[i];
+      if (blockIdx.x == 0 && threadIdx.x < 64) a.lencnt_out[threadIdx.x] = a.lencnt_src[threadIdx.x];
+    }
+  }
+  if (a.emit.rank_tab && threadIdx.x < 32 && !*a.emit.fallback) {
+    // the codebook's canonical-code emission (k2s_emit's work), warp 0 of
+    // the first CTAs: this pass reads only len8; the pack reads ctab
+    __shared__ uint16_t e_row[32 * K2R_TS];
+    __shared__ unsigned long long e_first[64];
+    __shared__ uint32_t e_base[64];
+    for (uint32_t wb = blockIdx.x; wb < K2_THREADS / 32; wb += gridDim.x) k2s_emit_warp(a.emit, wb, e_row, e_first, e_base);
+  }
+  const bool smem_tab = a.span <= K3S_L8MAX;
+  uint32_t shift = 0;
+  if (smem_tab) {
+    // len8[lo, lo+span) -> shared, 16-byte loads from an aligned start (the
+    // global table is padded by 64 bytes), 16 in flight per thread
+    const uint32_t a0 = a.lo & ~15u;
+    shift = a.lo - a0;
+    const uint32_t nv = (shift + a.span + 15) >> 4;
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.len8 + a0);
+    for (uint32_t i0 = threadIdx.x; i0 < nv; i0 += 16 * K3L_THREADS) {
+      uint4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; u++) {
+        const uint32_t i = i0 + u * K3L_THREADS;
+        v[u] = i < nv ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; u++) {
+        const uint32_t i = i0 + u * K3L_THREADS;
+        if (i < nv) reinterpret_cast<uint4 *>(k3c_l8)[i] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  const uint8_t *l8 = k3c_l8 + shift;  // l8[s - lo]
+  const uint32_t l8_rel = k3c_saddr(k3c_l8) + shift - a.lo;  // l8[s - lo] at l8_rel + s (mod 2^32)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
+  const uint64_t s0 = (uint64_t)blockIdx.x * a.spc, s1 = min(nseg, s0 + a.spc);
+  unsigned long long tb = 0, tz = 0;
+  for (uint64_t seg = s0 + warp; seg < s1; seg += K3L_THREADS / 32) {
+    const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
+    uint32_t s[K3L_EPT];
+    lb_load(sym, base, a.n, s);
+    uint32_t bits = 0, nz = 0, mx = 0;
+    if (smem_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
+      // full segment, byte table in shared memory: one LDS.U8 per symbol
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const uint32_t l = k3c_ldsb(l8_rel + s[j]);
+        bits += l;
+        mx = max(mx, l);
+      }
+      if (a.k) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) nz += s[j] == 0;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < K3_EPT; j++) {
-        if (base + j < n) {
-          const uint32_t wi = s[j] - win_lo;
-          bits += wi < win_n ? (uint32_t)len8[wi] : (uint32_t)(__ldg(&ctab[s[j]]) & 0xFF);
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] != kSent) {
+          const uint32_t l = smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
+          bits += l;
+          mx = max(mx, l);
           nz += s[j] == 0;
         }
       }
     }
-    bits64 += bits;
-    nz64 += nz;
+    bits = warp_sum(bits);
+    if (a.k || !__all_sync(0xffffffffu, nz == 0)) nz = warp_sum(nz);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+      a.seg_long[seg] = mx > (uint32_t)K3_SHORT_MAXLEN;  // the pack takes its u64 path
+      a.seg_bits[seg] = bits;
+      a.seg_nz[seg] = nz;
+      tb += bits;
+      tz += nz;
+    }
   }
-  const unsigned long long vb = warp_sum(bits64), vz = warp_sum(nz64);
-  if ((threadIdx.x & 31) == 0) {
-    wb[threadIdx.x >> 5] = vb;
-    wz[threadIdx.x >> 5] = vz;
+  __syncthreads();  // this CTA's segment counts are visible to the whole CTA
+  // in-CTA exclusive prefixes (u32: spc * 1024 * 26 bits < 2^32 for spc < 2^17)
+  unsigned long long runb = 0, runz = 0;
+  for (uint64_t c0 = s0; c0 < s1; c0 += K3L_THREADS) {
+    const uint64_t i = c0 + threadIdx.x;
+    const uint32_t vb = i < s1 ? a.seg_bits[i] : 0u, vz = i < s1 ? a.seg_nz[i] : 0u;
+    unsigned long long allb, allz;
+    const unsigned long long eb = block_excl_sum<unsigned long long>(vb, wsum_b, &allb);
+    const unsigned long long ez = block_excl_sum<unsigned long long>(vz, wsum_z, &allz);
+    if (i < s1) {
+      a.seg_bits[i] = (uint32_t)(runb + eb);
+      a.seg_nz[i] = (uint32_t)(runz + ez);
+    }
+    runb += allb;
+    runz += allz;
+  }
+  // the last CTA to finish turns the per-CTA totals into exclusive prefixes
+  // (in place) -- no separate scan launch waiting for a free SM
+  __shared__ unsigned k3c_last;
+  if (threadIdx.x == 0) {
+    a.cta_bits[blockIdx.x] = runb;
+    a.cta_nz[blockIdx.x] = runz;
+    __threadfence();
+    k3c_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tb = 0, tz = 0;
-    for (int w = 0; w < K3_THREADS / 32; w++) {
-      tb += wb[w];
-      tz += wz[w];
+  if (!k3c_last) return;
+  __threadfence();
+  runb = runz = 0;
+  for (uint32_t c0 = 0; c0 < a.ncta; c0 += K3L_THREADS) {
+    const uint32_t i = c0 + threadIdx.x;
+    const unsigned long long vb = i < a.ncta ? __ldcg(&a.cta_bits[i]) : 0ull;
+    const unsigned long long vz = i < a.ncta ? __ldcg(&a.cta_nz[i]) : 0ull;
+    unsigned long long allb, allz;
+    const unsigned long long eb = block_excl_sum<unsigned long long>(vb, wsum_b, &allb);
+    const unsigned long long ez = block_excl_sum<unsigned long long>(vz, wsum_z, &allz);
+    if (i < a.ncta) {
+      a.cta_bits[i] = runb + eb;
+      a.cta_nz[i] = runz + ez;
     }
-    cta_bits[blockIdx.x] = tb;
-    cta_nz[blockIdx.x] = tz;
+    runb += allb;
+    runz += allz;
   }
+  if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
 }
 
-constexpr int PK_EPT = 2 * K3_EPT;  // symbols per thread per pack tile
-constexpr int PK_TILE = K3_THREADS * PK_EPT;
+__device__ __forceinline__ uint32_t k3_saddr(const void *p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t k3_lds(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v, uint32_t p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
+               ::"r"(addr), "r"(v), "r"(p) : "memory");
+}
+
+__device__ __forceinline__ void k3_plan_out(const SegArgs &a) {
+  constexpr int W = (int)(sizeof(actc_plan_t) / 4);
+  if (threadIdx.x < W)
+    reinterpret_cast<volatile uint32_t *>(a.plan_host)[threadIdx.x] = reinterpret_cast<const uint32_t *>(a.dplan)[threadIdx.x];
+  __threadfence_system();
+}
 
 template <typename SymT>
-__device__ __forceinline__ void load_syms32(const SymT *__restrict__ sym, uint64_t base, uint64_t n,
-                                            uint32_t (&s)[PK_EPT]) {
-  if (base + PK_EPT <= n) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
-    if (sizeof(SymT) == 2) {
-#pragma unroll
-      for (int j = 0; j < PK_EPT / 8; j++) {
-        uint4 v = __ldg(p + j);
-        uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          s[8 * j + 2 * k] = w4[k] & 0xFFFFu;
-          s[8 * j + 2 * k + 1] = w4[k] >> 16;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < PK_EPT / 4; j++) {
-        uint4 v = __ldg(p + j);
-        s[4 * j] = v.x; s[4 * j + 1] = v.y; s[4 * j + 2] = v.z; s[4 * j + 3] = v.w;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < PK_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : 0xFFFFFFFFu;
+__global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__restrict__ sym, SegArgs a) {
+  extern __shared__ __align__(16) uint32_t k3p_sm[];
+  if (!seg_resolve(a)) {
+    if (a.plan_host && blockIdx.x == 0) k3_plan_out(a);  // the host redoes this stream: it needs the plan
+    return;
   }
-}
-
-template <typename SymT, bool WIDE>
-__global__ void __launch_bounds__(K3_THREADS) k3_pack(
-    const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab, uint32_t win_lo,
-    uint32_t win_n, uint32_t word_cap, uint64_t tiles_per_cta, const float *__restrict__ x,
-    const unsigned long long *__restrict__ cta_bit0, const unsigned long long *__restrict__ cta_nz0,
-    uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
-    unsigned long long *__restrict__ chunk_off, uint32_t *__restrict__ head, uint32_t *__restrict__ tail,
-    int extract_outliers) {
-  // tiles_per_cta counts K3_TILE units (the count pass's granularity); the
-  // pack pass walks the same symbol range in PK_TILE steps
-  extern __shared__ __align__(16) unsigned char smem[];
-  using E = typename Ent<WIDE>::T;
-  E *sh = reinterpret_cast<E *>(smem);
-  uint32_t *words = reinterpret_cast<uint32_t *>(smem + (((size_t)win_n * sizeof(E) + 15) & ~size_t(15)));
-  __shared__ unsigned long long wbuf[K3_THREADS / 32 + 1];
-  __shared__ uint32_t s_carry;
-  const int tid = threadIdx.x;
-  load_table<WIDE>(sh, ctab, win_lo, win_n);
-  if (tid == 0) s_carry = 0;
-  __syncthreads();
-  const uint64_t r0 = min(n, blockIdx.x * tiles_per_cta * (uint64_t)K3_TILE);
-  const uint64_t r1 = min(n, (blockIdx.x + 1) * tiles_per_cta * (uint64_t)K3_TILE);
-  unsigned long long bit = cta_bit0[blockIdx.x];  // start bit of the current tile
-  unsigned long long nzb = cta_nz0[blockIdx.x];
-  const unsigned long long cta_start = bit;
-  for (uint64_t tb = r0; tb < r1; tb += PK_TILE) {
-    const uint64_t base = tb + (uint64_t)tid * PK_EPT;
-    const uint64_t lim = min(r1, tb + (uint64_t)PK_TILE);
-    uint32_t s[PK_EPT];
-    load_syms32(sym, base, lim, s);
-    // pass 1: lengths (the table lookup is repeated in pass 2 to save registers)
-    uint32_t nbits = 0, nz = 0;
-#pragma unroll
-    for (int j = 0; j < PK_EPT; j++) {
-      if (s[j] != 0xFFFFFFFFu) {
-        unsigned long long code;
-        uint32_t len;
-        lookup<WIDE>(sh, ctab, win_lo, win_n, s[j], code, len);
-        nbits += len;
-        nz += s[j] == 0;
-      }
+  if (a.table && a.dplan) {
+    // the stream's decode table (kLutSize entries, 16 rows of 256), built
+    // here by the first CTAs instead of a launch of its own
+    for (uint32_t b = blockIdx.x; b < (uint32_t)(kLutSize / K3L_THREADS); b += gridDim.x) {
+      table_rows_plan(a.canon_out, a.lencnt_out, a.dplan, a.table, a.sw16, b);
+      __syncthreads();
     }
-    unsigned long long tot;
-    const unsigned long long excl =
-        block_excl_sum<unsigned long long>(((unsigned long long)nbits << 32) | nz, wbuf, &tot);
-    const unsigned long long tile_bits = tot >> 32;
-    const uint32_t start_off = (uint32_t)(bit & 31);
-    const uint32_t nwords = (uint32_t)((start_off + tile_bits + 31) >> 5);
-    for (uint32_t i = tid; i < nwords && i < word_cap; i += K3_THREADS) words[i] = 0;
-    __syncthreads();
-    const unsigned long long my_bit0 = bit + (excl >> 32);
-    // decode chunk index: bit offsets of the ACTC_CHUNK-th symbols this thread starts
-    if ((base % ACTC_CHUNK) == 0 && base < lim) chunk_off[base / ACTC_CHUNK] = my_bit0;
-    if (extract_outliers && nz) {
-      unsigned long long o = nzb + (excl & 0xFFFFFFFFull);
+  }
+  uint32_t *tab = k3p_sm;
+  k3_load_window(tab, a.ctab, a.win_lo, a.win_n, K3L_THREADS);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t *wb = k3p_sm + ((a.win_n + 3) & ~3u) + warp * K3L_WORDS;
+  const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
+  const uint32_t wlast = a.win_n - 1;
+  const bool fast_tab = a.span <= a.win_n;
+  const uint32_t tab_rel = k3_saddr(tab) - 4u * a.win_lo;  // tab[s - win_lo] at tab_rel + 4s (mod 2^32)
+  const uint32_t wb_s = k3_saddr(wb);
+  for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + warp; seg < nseg; seg += nwarps) {
+    const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
+    uint32_t s[K3L_EPT];
+    lb_load(sym, base, a.n, s);
+    const uint64_t r = seg / a.spc;
+    const unsigned long long pb = a.cta_bits[r] + a.seg_bits[seg], pz = a.cta_nz[r] + a.seg_nz[seg];
+    if (a.seg_long[seg]) {
+      // rare: a code longer than 26 bits in this segment.  u64 (code, len)
+      // entries from the global table, every word OR-ed straight into the
+      // (zeroed) payload, codes fed in <= 32-bit chunks.
+      uint32_t bits = 0, zm = 0;
 #pragma unroll
-      for (int j = 0; j < PK_EPT; j++) {
-        if (s[j] == 0) {
-          out_idx[o] = base + j;
-          out_val[o] = x[base + j];
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] != kSent) bits += (uint32_t)(__ldg(&a.ctab[s[j]]) & 0xFF);
+        zm |= (uint32_t)(s[j] == 0) << j;
+      }
+      const uint32_t nzl = __popc(zm);
+      const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nzl);
+      const uint32_t lane_ex = ib - bits;
+      if (((lane * K3L_EPT) % ACTC_CHUNK) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;
+      if (a.extract && nzl) {
+        unsigned long long o = pz + (iz - nzl);
+        for (uint32_t m = zm; m; m &= m - 1) {
+          const uint64_t e_idx = base + (uint32_t)(__ffs(m) - 1);
+          a.out_idx[o] = e_idx;
+          a.out_val[o] = a.x[e_idx];
           o++;
         }
       }
-    }
-    if (nbits) {
-      const uint32_t rel = start_off + (uint32_t)(excl >> 32);
-      if (!WIDE) {
-        // codes <= 26 bits complete at most one word each: predicated emits;
-        // only the first (shared with the previous thread) and the final
-        // partial word (shared with the next) are atomic
-        uint32_t w = rel >> 5;
-        const uint32_t w0 = w;
-        int nb = rel & 31;
-        unsigned long long acc = 0;
+      unsigned long long P = pb + lane_ex;
 #pragma unroll
-        for (int j = 0; j < PK_EPT; j++) {
-          unsigned long long cj;
-          uint32_t lj;
-          const bool pad = s[j] == 0xFFFFFFFFu;  // past the range end
-          lookup<WIDE>(sh, ctab, win_lo, win_n, pad ? win_lo : s[j], cj, lj);
-          if (pad) lj = 0;
-          acc |= lj ? cj << (64 - nb - (int)lj) : 0ull;
-          nb += (int)lj;
-          const bool ready = nb >= 32;
-          const uint32_t hiw = (uint32_t)(acc >> 32);
-          if (ready && w == w0) atomicOr(&words[w], hiw);
-          if (ready && w != w0) words[w] = hiw;
-          acc = ready ? (acc << 32) : acc;
-          nb = ready ? nb - 32 : nb;
-          w += ready;
+      for (int j = 0; j < K3L_EPT; j++) {
+        if (s[j] == kSent) continue;
+        const unsigned long long g = __ldg(&a.ctab[s[j]]);
+        const unsigned long long code = g >> 8;
+        int len = (int)(g & 0xFF);
+        while (len > 0) {
+          const int c = len > 32 ? 32 : len;
+          const uint32_t chunk = (uint32_t)((code >> (len - c)) & ((1ull << c) - 1));
+          const uint32_t off = (uint32_t)(P & 31);
+          const unsigned long long v = (unsigned long long)chunk << (64 - off - c);
+          uint32_t *w = a.payload + (P >> 5);
+          atomicOr(w, bswap32((uint32_t)(v >> 32)));
+          if (off + c > 32) atomicOr(w + 1, bswap32((uint32_t)v));
+          P += c;
+          len -= c;
         }
-        if (nb > 0) atomicOr(&words[w], (uint32_t)(acc >> 32));
-      } else {
-        Packer pk;
-        pk.words = words;
-        pk.w = rel >> 5;
-        pk.first_w = pk.w;
-        pk.nb = rel & 31;
-        pk.buf = 0;
+      }
+      continue;
+    }
+    // one (code << 6 | len) lookup per symbol
+    uint32_t e[K3L_EPT];
+    uint32_t zmask = 0;
+    if (fast_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
+      // every live symbol is inside the window and the segment is full
 #pragma unroll
-        for (int j = 0; j < PK_EPT; j++) {
-          if (s[j] == 0xFFFFFFFFu) continue;
-          unsigned long long cj;
-          uint32_t lj;
-          lookup<WIDE>(sh, ctab, win_lo, win_n, s[j], cj, lj);
-          if (lj > 32) {
-            pk.put((uint32_t)(cj >> 32), (int)lj - 32);
-            pk.put((uint32_t)cj, 32);
-          } else {
-            pk.put((uint32_t)cj, (int)lj);
+      for (int j = 0; j < K3L_EPT; j++) e[j] = k3_lds(tab_rel + 4u * s[j]);
+      if (a.k) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) zmask |= (uint32_t)(s[j] == 0) << j;
+      }
+    } else {
+      // clamped into the shared window, symbols outside it (rare, long
+      // codes) fixed up from the global table; sentinels past the end
+      uint32_t oow = 0;
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const uint32_t wi = s[j] - a.win_lo;
+        const bool sent = s[j] == kSent;
+        e[j] = sent ? 0u : tab[min(wi, wlast)];
+        oow |= (uint32_t)(wi > wlast && !sent) << j;
+        zmask |= (uint32_t)(s[j] == 0) << j;
+      }
+      if (oow) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) {
+          if ((oow >> j) & 1u) {  // re-read the symbol: s[] is dead here (register pressure)
+            const unsigned long long g = __ldg(&a.ctab[(uint32_t)sym[base + j]]);
+            e[j] = (uint32_t)(((g >> 8) << 6) | (g & 63));
           }
         }
-        pk.finish();
       }
     }
-    __syncthreads();
-    // word 0 continues the previous tile's partial word; the CTA's very first
-    // word and its final partial word go to the side slots
-    const bool first_tile = tb == r0, last_tile = tb + PK_TILE >= r1;
-    const uint32_t end_off = (uint32_t)((start_off + tile_bits) & 31);
-    if (tid == 0 && !first_tile) words[0] |= s_carry;
-    __syncthreads();
-    const uint64_t gw0 = bit >> 5;
-    const bool head_word = first_tile && ((cta_start & 31) != 0 || nwords == 1);
-    const uint32_t wlo = head_word ? 1 : 0;
-    const uint32_t whi = end_off ? nwords - 1 : nwords;  // last partial word is carried
-    for (uint32_t i = wlo + tid; i < whi; i += K3_THREADS) payload[gw0 + i] = bswap32(words[i]);
-    __syncthreads();
-    if (tid == 0) {
-      if (head_word) head[blockIdx.x] = words[0];
-      uint32_t carry = end_off ? words[nwords - 1] : 0u;
-      if (head_word && nwords == 1) carry = 0;  // already in head
-      s_carry = carry;
-      if (last_tile) tail[blockIdx.x] = carry;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < K3L_EPT; j++) bits += e[j] & 63;
+    const uint32_t nz = __popc(zmask);
+    const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nz);
+    const uint32_t seg_bits = __shfl_sync(0xffffffffu, ib, 31);
+    const uint32_t lane_ex = ib - bits;
+    const uint32_t off0 = (uint32_t)(pb & 31);
+    const uint32_t nw = (off0 + seg_bits + 31) >> 5;
+    for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
+    __syncwarp();
+    if (((lane * K3L_EPT) % ACTC_CHUNK) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every ACTC_CHUNK-th symbol
+    if (a.extract && nz) {
+      unsigned long long o = pz + (iz - nz);
+      for (uint32_t m = zmask; m; m &= m - 1) {
+        const uint64_t e_idx = base + (uint32_t)(__ffs(m) - 1);
+        a.out_idx[o] = e_idx;
+        a.out_val[o] = a.x[e_idx];
+        o++;
+      }
     }
-    bit += tile_bits;
-    nzb += tot & 0xFFFFFFFFull;
+    {
+      // codes <= 26 bits complete at most one word each.  Every word goes
+      // into the (zeroed) warp buffer by a predicated shared OR, so the
+      // lane's first and last words -- shared with its neighbours -- need
+      // no special case.  A length-0 entry (past the end) has code 0.
+      const uint32_t rel = off0 + lane_ex;
+      uint32_t addr = wb_s + 4u * (rel >> 5);
+      uint32_t nb = rel & 31;
+      unsigned long long acc = 0;
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const uint32_t lj = e[j] & 63;
+        acc |= (unsigned long long)(e[j] >> 6) << ((64 - nb - lj) & 63);
+        nb += lj;
+        const uint32_t ready = nb >= 32;
+        k3_red_or(addr, (uint32_t)(acc >> 32), ready);
+        acc = ready ? (acc << 32) : acc;
+        nb -= ready << 5;
+        addr += ready << 2;
+      }
+      k3_red_or(addr, (uint32_t)(acc >> 32), nb > 0);
+    }
+    __syncwarp();
+    const uint64_t gw0 = pb >> 5;
+    const uint32_t end_off = (off0 + seg_bits) & 31;
+    for (uint32_t i = lane; i < nw; i += 32) {
+      const uint32_t v = bswap32(wb[i]);
+      const bool shared_word = (i == 0 && off0 != 0) || (i == nw - 1 && end_off != 0);
+      if (shared_word)
+        atomicOr(&a.payload[gw0 + i], v);
+      else
+        a.payload[gw0 + i] = v;
+    }
+    __syncwarp();
+  }
+  if (a.plan_host) {
+    // the last CTA to finish hands the plan to the mapped host mailbox
+    __shared__ unsigned k3p_last;
     __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      k3p_last = atomicAdd(a.pack_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (k3p_last) {
+      k3_plan_out(a);
+      if (threadIdx.x == 0) *a.pack_ticket = 0u;
+    }
   }
 }
 
-// Merge the CTA boundary words: head[b] goes into the word holding CTA b's
-// first bit, tail[b] into the word holding its last bit (both partial).
-__global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
-                         const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
-                         const uint32_t *__restrict__ tail, uint32_t ncta) {
-  // pass 1: zero every word a side slot lands in; pass 2: OR the slots in
-  for (int pass = 0; pass < 2; pass++) {
-    for (uint32_t b = threadIdx.x; b < ncta; b += blockDim.x) {
-      const unsigned long long s = cta_bit0[b], nb = cta_bits[b];
-      if (!nb) continue;
-      const unsigned long long e = s + nb;
-      const uint64_t wf = s >> 5, wl = (e - 1) >> 5;
-      const bool has_head = (s & 31) != 0 || wf == wl;
-      const bool has_tail = (e & 31) != 0 && !(wf == wl && has_head);
-      if (pass == 0) {
-        if (has_head) payload[wf] = 0;
-        if (has_tail) payload[wl] = 0;
-      } else {
-        if (has_head) atomicOr(&payload[wf], bswap32(head[b]));
-        if (has_tail) atomicOr(&payload[wl], bswap32(tail[b]));
-      }
-    }
-    __syncthreads();
-  }
-}
 
-#define K3_INST(T, W)                                                                                          \
-  template __global__ void k3_count<T, W>(const T *, uint64_t, const unsigned long long *, uint32_t, uint32_t, \
-                                          uint64_t, unsigned long long *, unsigned long long *);                 \
-  template __global__ void k3_pack<T, W>(const T *, uint64_t, const unsigned long long *, uint32_t, uint32_t,  \
-                                         uint32_t, uint64_t, const float *, const unsigned long long *,         \
-                                         const unsigned long long *, uint32_t *, unsigned long long *, float *, \
-                                         unsigned long long *, uint32_t *, uint32_t *, int);
-K3_INST(uint16_t, false)
-K3_INST(uint16_t, true)
-K3_INST(uint32_t, false)
-K3_INST(uint32_t, true)
+}  // namespace actc
 
+namespace actc {
+template __global__ void k3_seg_count<uint16_t>(const uint16_t *, SegArgs);
+template __global__ void k3_seg_count<uint32_t>(const uint32_t *, SegArgs);
+template __global__ void k3_seg_pack<uint16_t>(const uint16_t *, SegArgs);
+template __global__ void k3_seg_pack<uint32_t>(const uint32_t *, SegArgs);
 }  // namespace actc

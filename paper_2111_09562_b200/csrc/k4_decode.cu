@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(K4_THREADS) k4_decode(DecodeArgs a) {
       }
       if (SW == 16 && (cnt & 1) && !bad) my[cnt >> 1] = pair;
       if (pos != endp || pos > a.payload_bits) bad = true;
-      if (bad) atomicOr(a.status, (unsigned)ACTC_EFORMAT);
+      if (bad) report_format_error(a);
       agg = Seg{acc, reset};
     }
     if (MODE != 2) {

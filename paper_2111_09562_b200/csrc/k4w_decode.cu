@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(K4W_THREADS, 3) k4w_decode(DecodeArgs a) {
       if (pos_end != endp || pos_end > a.payload_bits) bad = true;
     }
   }
-  if (bad) atomicOr(a.status, (unsigned)ACTC_EFORMAT);
+  if (bad) report_format_error(a);
   const unsigned long long ws = warp_sum(nonzero), wm = warp_sum(markers);
   if (lane == 0) {
     if (ws) atomicAdd(a.nonzero, ws);

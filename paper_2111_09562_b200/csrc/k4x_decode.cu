@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(K4X_THREADS) k4x_decode(DecodeArgs a) {
     const uint64_t pos_end = ((uint64_t)(src - pw) << 5) - 32 - (uint64_t)nb;
     if (pos_end != endp || pos_end > a.payload_bits) bad = true;
   }
-  if (bad) atomicOr(a.status, (unsigned)ACTC_EFORMAT);
+  if (bad) report_format_error(a);
   const unsigned long long ws = warp_sum(nonzero), wm = warp_sum(markers);
   if (lane == 0) {
     if (ws) atomicAdd(a.nonzero, ws);

@@ -14,15 +14,10 @@ constexpr uint32_t K1_WIN = 8192;  // shared-memory histogram window (bins)
 constexpr int K2_THREADS = 1024;
 constexpr uint32_t K2_SMEM_SORT_MAX = 8192;  // keys sorted in shared memory
 
-// K3: 512 threads x 16 symbols per tile (32 decode chunks per tile)
-constexpr int K3_THREADS = 512;
-constexpr int K3_EPT = 16;
-constexpr int K3_TILE = K3_THREADS * K3_EPT;
-constexpr uint32_t K3_WIN32 = 32768;  // u32 code-table window (codes <= 26 bits)
-constexpr uint32_t K3_WIN64 = 8192;   // u64 window for longer codes
+// K3 segment encoder: one warp per segment of 32 lanes x 32 symbols; codes
+// of up to K3_SHORT_MAXLEN bits take the shared-window path, longer ones
+// (<= 56 bits) the u64 path
 constexpr int K3_SHORT_MAXLEN = 26;
-// K3 single-pass encoder (codes <= K3_SHORT_MAXLEN): one warp per segment of
-// 32 lanes x 32 symbols, decoupled look-back over segments
 constexpr int K3L_THREADS = 256;
 constexpr int K3L_EPT = 32;
 constexpr int K3L_SEG = 32 * K3L_EPT;                                     // symbols per segment
@@ -173,36 +168,6 @@ constexpr size_t kK2rSmem = (size_t)(3 * (kRCap + 1) + 3 * (kICap + 1)) * 4;
 __global__ void k2r_codebook(CodebookArgs a);
 __global__ void k2s_emit(CodebookArgs a);
 
-template <typename SymT, bool WIDE>
-__global__ void k3_count(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
-                         uint32_t win_lo, uint32_t win_n, uint64_t tiles_per_cta,
-                         unsigned long long *__restrict__ cta_bits, unsigned long long *__restrict__ cta_nz);
-template <typename SymT, bool WIDE>
-__global__ void k3_pack(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
-                        uint32_t win_lo, uint32_t win_n, uint32_t word_cap, uint64_t tiles_per_cta,
-                        const float *__restrict__ x, const unsigned long long *__restrict__ cta_bit0,
-                        const unsigned long long *__restrict__ cta_nz0, uint32_t *__restrict__ payload,
-                        unsigned long long *__restrict__ out_idx, float *__restrict__ out_val,
-                        unsigned long long *__restrict__ chunk_off, uint32_t *__restrict__ head,
-                        uint32_t *__restrict__ tail, int extract_outliers);
-// single-pass encoder look-back state (per tile).  Self-validating 64-bit
-// words (flag in the top bits, value below) so pollers need no acquire:
-//   stat[t]  = kLbAgg | (tile bits << 14 | tile outliers)   or
-//              kLbInc | inclusive bits (< 2^44)
-//   incnz[t] = kLbInc | inclusive outlier count (written before stat's INC)
-struct EncLB {
-  unsigned long long *stat;
-  unsigned long long *incnz;
-};
-constexpr unsigned long long kLbAgg = 1ull << 62;
-constexpr unsigned long long kLbInc = 2ull << 62;
-constexpr unsigned long long kLbVal = (1ull << 62) - 1;
-template <typename SymT>
-__global__ void k3_encode_lb(const SymT *__restrict__ sym, uint64_t n, const unsigned long long *__restrict__ ctab,
-                             uint32_t win_lo, uint32_t win_n, const float *__restrict__ x,
-                             uint32_t *__restrict__ payload, unsigned long long *__restrict__ out_idx,
-                             float *__restrict__ out_val, unsigned long long *__restrict__ chunk_off, EncLB st,
-                             unsigned *__restrict__ ticket, int extract_outliers);
 // segment encoder (codes <= 26 bits): per-CTA ranges of segments
 struct SegArgs {
   uint64_t n;
@@ -265,9 +230,6 @@ template <typename SymT>
 __global__ void k3_seg_count(const SymT *__restrict__ sym, SegArgs a);
 template <typename SymT>
 __global__ void k3_seg_pack(const SymT *__restrict__ sym, SegArgs a);
-__global__ void k3_fixup(uint32_t *__restrict__ payload, const unsigned long long *__restrict__ cta_bit0,
-                         const unsigned long long *__restrict__ cta_bits, const uint32_t *__restrict__ head,
-                         const uint32_t *__restrict__ tail, uint32_t ncta);
 
 // mode bit0: short-code entries carry the canonical index instead of the
 // symbol; bit1: long prefixes with a single code length get "exact" entries
@@ -303,6 +265,14 @@ struct DecodeArgs {
   unsigned long long *markers;
   unsigned *status;
 };
+// a decode fault: the call's status word and, right after it, the context's
+// sticky word (collected by actc_ctx_take_status at the caller's next sync --
+// decoders launched without a result mailbox are checked that way)
+__device__ __forceinline__ void report_format_error(const DecodeArgs &a) {
+  atomicOr(a.status, (unsigned)ACTC_EFORMAT);
+  atomicOr(a.status + 1, (unsigned)ACTC_EFORMAT);
+}
+
 // MODE: 0 = fp32 recon, 1 = fp64 recon, 2 = raw u32 symbols
 // SW: staging width of decoded symbols in shared memory (16 or 32 bits)
 template <int MODE, int SW>

@@ -156,9 +156,9 @@ def _dtype_code(x):
 
 def count_nonzero(x, stream=None) -> int:
     """Exact nonzero count on the GPU (tensor.py:181)."""
-    ctx = _lib.context()
-    sh, s = _lib.stream_handle(stream)
     x = to_device(x)
+    ctx = _lib.context(x.device.index)
+    sh, s = _lib.stream_handle(stream, x.device)
     _lib.raise_for(_lib.lib().actc_count_nonzero(C.c_void_p(x.data_ptr()), _dtype_code(x), x.numel(),
                                                   C.c_void_p(ctx.u64_buf.data_ptr()), sh))
     s.synchronize()
@@ -167,9 +167,9 @@ def count_nonzero(x, stream=None) -> int:
 
 def mean_abs(x, stream=None) -> float:
     """mean(|x|) with numpy's pairwise summation order, on the GPU."""
-    ctx = _lib.context()
-    sh, s = _lib.stream_handle(stream)
     x = to_device(x)
+    ctx = _lib.context(x.device.index)
+    sh, s = _lib.stream_handle(stream, x.device)
     _lib.raise_for(_lib.lib().actc_mean_abs(ctx.handle, C.c_void_p(x.data_ptr()), _dtype_code(x), x.numel(),
                                              C.c_void_p(ctx.u64_buf.data_ptr()), sh))
     s.synchronize()
@@ -180,9 +180,9 @@ def per_sample_max(x, stream=None):
     """(per-sample max |x| along axis 0 as a host tuple, mean of it the
     numpy way) -- training.py:360 / tensor.py:190-191."""
     torch = _lib.torch_cuda()
-    ctx = _lib.context()
-    sh, s = _lib.stream_handle(stream)
     x = to_device(x)
+    ctx = _lib.context(x.device.index)
+    sh, s = _lib.stream_handle(stream, x.device)
     N = x.shape[0] if x.dim() else 1
     out = torch.empty(N, dtype=x.dtype, device=x.device)
     _lib.raise_for(_lib.lib().actc_lbar(ctx.handle, C.c_void_p(x.data_ptr()), _dtype_code(x), N, x.numel() // N,

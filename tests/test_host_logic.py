@@ -83,14 +83,6 @@ def test_adaptive_controller_W():
     assert p1.W == 8 and p2.W == 4 and c.intervals_planned == 2
 
 
-def test_kv_config():
-    m = ctl.parse_kv_lines("W_default = 200  # comment\n\nW_floor=10\n")
-    cfg = ctl.controller_config_from_mapping(m)
-    assert cfg.W_default == 200 and cfg.W_floor == 10
-    with pytest.raises(ParameterError):
-        ctl.controller_config_from_mapping({"bogus": "1"})
-
-
 def test_activation_store_lifecycle():
     s = ActivationStore()
     s.put("conv1", ActivationStore.COMPRESSED, object(), 100)
