@@ -215,6 +215,12 @@ int actc_build_chunk_index(actc_ctx *ctx, const actc_stream_t *stream,
 /* prequantize (codec.py:238-251); x_dtype ACTC_DTYPE_F32 or _F64 */
 int actc_prequantize(const void *x_dev, int x_dtype, uint64_t n, double eb, int64_t *q_dev,
                      actc_stream s);
+/* exhaustive check of the fp32 fast quantizer used by compress: every
+ * finite fp32 bit pattern u in [lo, lo+count) (count <= 2^32 - lo) that the
+ * fast path claims is compared with the exact restatement of prequantize +
+ * bound check (codec.py:248-251, 311-312).  out_host (pinned, 2 x u64,
+ * written async): {mismatches, elements the fast path took}. */
+int actc_debug_quant_check(double eb, uint64_t lo, uint64_t count, uint64_t *out_host, actc_stream s);
 /* lorenzo_encode (codec.py:254-272); symbols_dev u32, force_dev may be NULL;
  * n_outliers_host pinned, written async */
 int actc_lorenzo_encode(const int64_t *lattice_dev, uint64_t n, uint32_t radius,

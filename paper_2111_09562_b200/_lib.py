@@ -99,6 +99,7 @@ def lib():
             "actc_ctx_destroy": ([P], None),
             "actc_ctx_device_bytes": ([P], U64),
             "actc_ctx_take_status": ([P, P, P], I),
+            "actc_debug_quant_check": ([D, U64, U64, P, P], I),
             "actc_ctx_set_scratch": ([P, P, U64], I),
             "actc_ctx_set_table_out": ([P, P, U64], I),
             "actc_compress_plan": ([P, P, U64, D, U32, U32, P, P, P], I),
@@ -133,7 +134,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "actc_last_error actc_version actc_ctx_create actc_ctx_destroy actc_ctx_device_bytes actc_ctx_take_status actc_ctx_set_scratch actc_ctx_set_table_out actc_compress_plan "
     "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
-    "actc_prequantize actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
+    "actc_prequantize actc_debug_quant_check actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
     "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats actc_crc32 actc_inject_uniform"
 ).split()

@@ -1078,6 +1078,27 @@ int actc_prequantize(const void *x, int dtype, uint64_t n, double eb, int64_t *q
   return ACTC_OK;
 }
 
+int actc_debug_quant_check(double eb, uint64_t lo, uint64_t count, uint64_t *out_host, actc_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
+  QParams P;  // exactly as launch_k1 builds it
+  P.eb = eb;
+  P.two_eb = 2.0 * eb;
+  P.inv = 1.0 / P.two_eb;
+  P.fast = (isfinite(P.inv) && P.inv >= DBL_MIN) ? 1 : 0;
+  unsigned long long *d = nullptr;
+  CK(cudaMallocAsync((void **)&d, 16, s));
+  CK(cudaMemsetAsync(d, 0, 16, s));
+  if (count) {
+    KT(ACTC_KIND_DEBUG);
+    k_quant_check<<<148 * 16, 256, 0, s>>>(lo, count, P, d);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(out_host, d, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d, s));
+  return ACTC_OK;
+}
+
 int actc_lorenzo_encode(const int64_t *lat, uint64_t n, uint32_t radius, const uint8_t *force, uint32_t *sym,
                         uint64_t *n_out_host, actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -237,6 +237,31 @@ __global__ void k_prequantize(const void *__restrict__ x, int dtype, uint64_t n,
   }
 }
 
+// Exhaustive check of K1's fp32 fast quantizer: every finite fp32 bit
+// pattern in [lo, lo + count) through quant_fast32 (when it claims the
+// element) vs the exact restatement quant_exact (q and "no bound
+// violation").  out[0] += mismatches, out[1] += elements the fast path took.
+__global__ void k_quant_check(uint64_t lo, uint64_t count, QParams P, unsigned long long *__restrict__ out) {
+  unsigned long long bad = 0, fast = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float xf = __uint_as_float((uint32_t)(lo + i));
+    if (!isfinite(xf)) continue;
+    int q32;
+    if (!(P.fast && quant_fast32(xf, P.inv, q32))) continue;
+    fast++;
+    bool viol;
+    const long long qe = quant_exact((double)xf, P.two_eb, P.eb, viol);
+    bad += (qe != (long long)q32) || viol;
+  }
+  bad = warp_sum(bad);
+  fast = warp_sum(fast);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(&out[0], bad);
+    if (fast) atomicAdd(&out[1], fast);
+  }
+}
+
 // lorenzo_encode over an int64 lattice (codec.py:254-272).
 __global__ void k_lorenzo_encode(const long long *__restrict__ lat, uint64_t n, uint32_t radius,
                                  const uint8_t *__restrict__ force, uint32_t *__restrict__ sym,

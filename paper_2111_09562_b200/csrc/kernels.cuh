@@ -58,6 +58,7 @@ __global__ void k1_quant_lorenzo_hist(const float *__restrict__ x, uint64_t n, Q
 __global__ void k_hist_u32(const uint32_t *__restrict__ s, uint64_t n, uint64_t alphabet,
                            unsigned long long *__restrict__ ghist, unsigned *__restrict__ bad,
                            uint32_t win_n);
+__global__ void k_quant_check(uint64_t lo, uint64_t count, QParams P, unsigned long long *__restrict__ out);
 __global__ void k_prequantize(const void *__restrict__ x, int dtype, uint64_t n, double eb,
                               long long *__restrict__ q);
 __global__ void k_lorenzo_encode(const long long *__restrict__ lat, uint64_t n, uint32_t radius,

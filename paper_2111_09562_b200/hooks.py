@@ -8,10 +8,27 @@ Mirrors the reference's hook API and storage policy
 * `ActivationCompressor` -- the train() hook sites (training.py:259-299
   compress after forward, :335-353 lazy decompress in backward, :351-361
   statistics, :381-418 interval boundary) re-expressed for autograd:
-  `torch.autograd.graph.saved_tensors_hooks` pack/unpack.  What autograd
-  saves for a conv layer is its (post-ReLU) output, which the next layer's
-  backward consumes; pack hands it to the GPU codec at the layer's current
-  error bound, unpack reconstructs it (fp32, on device).
+  `torch.autograd.graph.saved_tensors_hooks` pack/unpack.
+
+What is stored.  The reference stores every conv layer's output and
+recomputes the cheap layers after it (ReLU, max-pool) from it
+(training.py:264-299, 344-347).  Autograd saves, for a conv followed by
+(BatchNorm ->) (residual add ->) ReLU, the ReLU's output (ReLU backward and
+the next layer's backward both read it), so that is the stored activation
+of the conv: one slot per conv CALL, found by following the conv's output
+through parameter-free / normalisation modules and in-place ops up to the
+first ReLU (dataflow, not module order -- torchvision's Bottleneck calls
+one ReLU module three times, each call belongs to a different conv).
+Pooling outputs computed from a stored activation are MARKER slots:
+recomputed from the decompressed activation in backward.
+
+Consumer.  The reference's consumer of a conv's stored output is the next
+parameterised layer downstream (`_consumer_map`, training.py:154-166); its
+momentum (M_avg) and output gradient (L_bar) set the layer's error bound.
+Here it is the first Conv2d / Linear whose input is the stored activation
+(or a pooling / dropout output derived from it), followed across residual
+adds by dataflow; when the dataflow passes through a functional view
+(torch.flatten), the next Conv2d / Linear in registration order.
 
 Policy, as in the reference:
 * no compression during the first interval (W iterations) -- there is no
@@ -23,13 +40,15 @@ Policy, as in the reference:
 * layers whose eb is None (skip set) stay raw.
 
 Packing is asynchronous: a stored activation's compression is launched on a
-side stream as soon as its producer has run (`compress_begin`, no host
-sync); the oldest in-flight compression is finished (`compress_end`: plan
-read, exact-size container, original released) once more than `batch_flush`
-are in flight, so the raw activations of at most that many layers coexist
-with their compressed copies.
+side stream as soon as it exists (`compress_begin`, no host sync); the
+oldest in-flight compression is finished (`compress_end`: plan read,
+exact-size container, original released) once more than `batch_flush` are
+in flight.  Decode faults of the (unsynchronised) backward decompressions
+are collected at the end of every iteration and raised as FormatError at
+the next iteration's start (one event wait).
 Under data parallelism the statistics are averaged across ranks before
-planning, so every rank compresses with identical error bounds.
+planning and N is the global batch, so every rank compresses with the error
+bound a single-process run at the same global batch would use.
 """
 from __future__ import annotations
 
@@ -40,7 +59,7 @@ from dataclasses import dataclass, field
 from . import _lib
 from .codec import DEFAULT_RADIUS, CodecParams, compress_begin, compress_end, decompress_device
 from .controller import AdaptiveController, ControllerConfig, LayerTrainingStats, choose_batch_size
-from .errors import LifecycleError, ParameterError
+from .errors import FormatError, LifecycleError, ParameterError
 
 
 class ActivationStore:
@@ -76,9 +95,18 @@ class ActivationStore:
     def __contains__(self, layer_id: str) -> bool:
         return layer_id in self._slots
 
+    def __len__(self):
+        return len(self._slots)
+
 
 def _key(t):
+    """identity of one version of a tensor (saved-tensor matching)"""
     return (t.data_ptr(), t._version, tuple(t.shape), tuple(t.stride()))
+
+
+def _tkey(t):
+    """identity of a tensor across in-place updates (dataflow tags)"""
+    return (t.data_ptr(), tuple(t.shape), tuple(t.stride()))
 
 
 class _Marker:
@@ -101,10 +129,9 @@ class _Marker:
 class _Handle:
     """One saved fp32 tensor.  Autograd saves a module's output while the op
     runs, before the module's forward hook names it, so every saved tensor
-    gets a handle; the producer's forward hook then promotes the handle of
-    its output to a stored activation (layer set): raw until the pending
-    queue is flushed, compressed after.  Handles nobody promotes pass the
-    tensor through."""
+    gets a handle; the dataflow hooks then promote the handle of a stored
+    activation to its slot: raw until the pending queue is flushed,
+    compressed after.  Handles nobody promotes pass the tensor through."""
 
     __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref", "job")
 
@@ -127,35 +154,61 @@ class _Handle:
 @dataclass
 class IterationRecord:
     iteration: int
-    compressed: dict = field(default_factory=dict)  # layer -> (ratio, eb)
-    stored_bytes: int = 0
+    compressed: dict = field(default_factory=dict)  # slot -> (ratio, eb)
+    stored_bytes: int = 0   # CMTZ bytes of compressed slots + raw bytes of the others
+    device_bytes: int = 0   # device memory the stored containers really hold (incl. the decode index)
     raw_bytes: int = 0
-    markers: int = 0  # cheap-layer outputs recomputed instead of stored
+    markers: int = 0        # cheap-layer outputs recomputed instead of stored
+    slots: list = field(default_factory=list)  # stored-activation slots in forward order
 
 
 class _LayerMap(dict):
-    """conv_layer_map's result: the layer map plus the model it came from
-    (whose in-place ReLUs run out of place in collection iterations)."""
+    """conv_layer_map's result: {layer_id: (producer module, consumer module
+    or None)} plus the model it came from."""
 
     def __init__(self, d, model):
         super().__init__(d)
         self.model = model
 
 
+def _is_relu(m):
+    import torch.nn as nn
+
+    return isinstance(m, (nn.ReLU, nn.ReLU6, nn.LeakyReLU))
+
+
+def _is_param_layer(m):
+    import torch.nn as nn
+
+    return isinstance(m, (nn.Conv1d, nn.Conv2d, nn.Conv3d, nn.Linear))
+
+
+def _passes_tags(m):
+    """modules a producer tag flows through on its way to the ReLU (and a
+    consumer tag on its way to the next parameterised layer): parameter-free
+    leaves and normalisations"""
+    import torch.nn as nn
+
+    if isinstance(m, nn.modules.batchnorm._NormBase):
+        return True
+    return not any(True for _ in m.parameters(recurse=False))
+
+
 class ActivationCompressor:
     """Adaptive activation compression for a PyTorch model.
 
-    layers: {layer_id: (producer_module, consumer_module)} -- the producer's
-    forward output is the stored activation (e.g. the ReLU after a conv), the
-    consumer is the next parameterised layer whose momentum and output
-    gradient set the error bound.  `conv_layer_map` builds this map
-    for conv nets (conv -> relu -> ... -> next conv/linear).
+    layers: `conv_layer_map(model)` (every Conv2d of the model is a producer;
+    stored activations and consumers are found by dataflow), or an explicit
+    {layer_id: (producer_module, consumer_module or None)} map -- a producer
+    that is itself a ReLU stores its own output.
     """
 
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 1, dist_group=None,
                  sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
                  recompute_cheap: bool = True):
+        import torch.nn as nn
+
         self.layers = dict(layers)
         self._model = getattr(layers, "model", None)
         self.optimizer = optimizer
@@ -167,23 +220,36 @@ class ActivationCompressor:
         self.batch_flush = batch_flush
         self.dist_group = dist_group
         self.sync_stats = sync_stats
+        self.recompute_cheap = recompute_cheap
         self.plan = None
         self.it = 0
         self.next_collection = self.controller.W
         self.store = ActivationStore()
         self.records: list[IterationRecord] = []
-        self._act_layer: dict = {}
-        self._handles: dict = {}
+        # per-iteration dataflow state
+        self._act_layer: dict = {}   # key -> (slot, ref): stored activations by tensor version
+        self._handles: dict = {}     # key -> _Handle
+        self._ptag: dict = {}        # tkey -> (slot, ref): a producer's output on its way to the ReLU
+        self._ctag: dict = {}        # tkey -> (slot, ref): a stored activation on its way to its consumer
+        self._cheap: dict = {}
+        self._markers: dict = {}
+        self._calls: dict = {}       # layer id -> calls this iteration
+        self._await_consumer: list = []  # slots stored this iteration without a consumer yet
         self._pending: list[_Handle] = []  # compressions launched, not yet synchronised (oldest first)
         self._slot = 0
         self._collecting = False
         self._R: dict[str, float] = {}
-        self._bits: dict[str, int] = {}
         self._lbar: dict[str, float] = {}
+        self._bits: dict[str, int] = {}
         self._batch = None
         self._rec = None
+        self._status = None          # decode-fault collection of the previous iteration
+        self._capture = None         # slots whose (input, container) the next iteration keeps
+        self.captured: dict = {}     # slot -> (host fp32 copy of the stored activation, container)
+        # slot -> consumer module; explicit consumers from the map, the rest by dataflow
+        self.consumers: dict = {}
+        self._slot_layer: dict = {}  # slot -> layer id
         self._hooks = []
-        self._bwd_hooks = []
         # memory-budget batch planner (reference training.py:401-426): per-
         # sample bytes of each stored activation, the ratios observed in the
         # current interval, the model's fixed bytes (weights + velocity)
@@ -194,81 +260,60 @@ class ActivationCompressor:
         self.fixed_bytes = float(fixed_bytes)
         self.batch_size = None  # recommended batch (choose_batch_size), once planned
         self._per_sample: dict[str, float] = {}
-        self._interval_ratios: dict[str, list] = {lid: [] for lid in self.layers}
-        for lid, (prod, cons) in self.layers.items():
-            self._hooks.append(prod.register_forward_hook(self._fwd_hook(lid)))
-        # cheap layers (pooling) fed by a stored activation: their saved
-        # outputs become MARKER slots, recomputed in backward
-        self._cheap: dict = {}
-        self._markers: dict = {}
-        if recompute_cheap and self._model is not None:
-            import torch.nn as nn
+        self._interval_ratios: dict[str, list] = {}
 
-            for name, m in self._model.named_modules():
-                if isinstance(m, (nn.MaxPool2d, nn.AvgPool2d)):
-                    self._hooks.append(m.register_forward_hook(self._cheap_hook(name)))
+        self._producer: dict = {}   # id(module) -> layer id
+        self._explicit_consumer: dict = {}
+        for lid, (prod, cons) in self.layers.items():
+            self._producer[id(prod)] = lid
+            if cons is not None:
+                self._explicit_consumer[lid] = cons
+        # registration-order fallback consumer (reference _consumer_map):
+        # the next Conv/Linear after the producer
+        leaves = self._leaf_modules()
+        self._fallback_consumer: dict = {}
+        for i, (_, m) in enumerate(leaves):
+            lid = self._producer.get(id(m))
+            if lid is None:
+                continue
+            for _, m2 in leaves[i + 1:]:
+                if _is_param_layer(m2):
+                    self._fallback_consumer[lid] = m2
+                    break
+        seen = set()
+        for _, m in leaves:
+            if id(m) in seen:
+                continue
+            seen.add(id(m))
+            self._hooks.append(m.register_forward_hook(self._leaf_hook))
+        self._pools = (nn.MaxPool1d, nn.MaxPool2d, nn.MaxPool3d, nn.AvgPool1d, nn.AvgPool2d, nn.AvgPool3d)
 
     # ---- construction helpers -------------------------------------------
     @staticmethod
     def conv_layer_map(model):
-        """{name: (activation module, consumer module)} for every Conv2d: the
-        activation is the first ReLU after it (else the conv itself), the
-        consumer the next Conv2d / Linear in module registration order
-        (reference _consumer_map, training.py:154-166)."""
+        """{name: (conv module, None)} for every Conv2d of the model: the
+        stored activation and the consumer of each call are found by
+        dataflow (training.py:154-166, 264-283)."""
         import torch.nn as nn
 
-        mods = [(n, m) for n, m in model.named_modules() if not list(m.children())]
-        out = {}
-        for i, (name, m) in enumerate(mods):
-            if not isinstance(m, nn.Conv2d):
-                continue
-            act, cons = m, None
-            for n2, m2 in mods[i + 1:]:
-                if isinstance(m2, nn.ReLU) and act is m:
-                    act = m2
-                if isinstance(m2, (nn.Conv2d, nn.Linear)):
-                    cons = m2
-                    break
-            if cons is not None:
-                out[name] = (act, cons)
-        return _LayerMap(out, model)
+        return _LayerMap({n: (m, None) for n, m in model.named_modules() if isinstance(m, nn.Conv2d)}, model)
 
-    def _modules(self):
-        seen = []
-        for prod, cons in self.layers.values():
-            for m in (prod, cons):
-                if all(m is not x for x in seen):
-                    seen.append(m)
-        return seen
+    def _leaf_modules(self):
+        if self._model is not None:
+            return [(n, m) for n, m in self._model.named_modules() if not list(m.children())]
+        out = []
+        for lid, (prod, cons) in self.layers.items():
+            out.append((lid, prod))
+            if cons is not None:
+                out.append((lid + ".consumer", cons))
+        return out
 
     def remove(self):
-        for h in self._hooks + self._bwd_hooks:
+        for h in self._hooks:
             h.remove()
         self._hooks.clear()
-        self._bwd_hooks.clear()
 
-    # ---- hooks ---------------------------------------------------------------
-    def _fwd_hook(self, lid):
-        def hook(mod, inp, out):
-            if self._batch is None and inp and hasattr(inp[0], "shape"):
-                self._batch = int(inp[0].shape[0])
-            if not hasattr(out, "data_ptr"):
-                return
-            k = _key(out)
-            self._act_layer[k] = (lid, weakref.ref(out))
-            h = self._live(self._handles, k)
-            if h is not None and h.layer is None:
-                self._promote(h, lid)  # saved by the op itself, before this hook
-        return hook
-
-    def _cheap_hook(self, name):
-        def hook(mod, inp, out):
-            if inp and hasattr(inp[0], "data_ptr") and hasattr(out, "data_ptr"):
-                src = self._live(self._handles, _key(inp[0]))
-                if src is not None and src.layer is not None:
-                    self._cheap[_key(out)] = (name, mod, src, weakref.ref(out))
-        return hook
-
+    # ---- dataflow --------------------------------------------------------
     @staticmethod
     def _live(table, k):
         """table[k] if the tensor it was registered for is still alive."""
@@ -281,20 +326,105 @@ class ActivationCompressor:
             return None
         return e
 
-    def _bwd_hook(self, lid):
-        def hook(mod, gin, gout):
-            if self._collecting and gout and gout[0] is not None:
-                from .tensor import per_sample_max
+    def _new_slot(self, lid):
+        k = self._calls.get(lid, 0)
+        self._calls[lid] = k + 1
+        slot = lid if k == 0 else f"{lid}#{k}"
+        self._slot_layer[slot] = lid
+        return slot
 
-                scale = self.grad_scale if self.grad_scale is not None else (self._batch or 1)
-                _, lbar = per_sample_max(gout[0].detach().float())
-                self._lbar[lid] = lbar * scale
-        return hook
+    def _leaf_hook(self, mod, inp, out):
+        import torch
 
+        if not torch.is_tensor(out):
+            return
+        x = inp[0] if inp and torch.is_tensor(inp[0]) else None
+        if x is not None and _is_param_layer(mod):
+            self._match_consumer(mod, x, out)
+        lid = self._producer.get(id(mod))
+        if lid is not None:
+            if self._batch is None and x is not None and x.dim() > 0:
+                self._batch = int(x.shape[0])
+            slot = self._new_slot(lid)
+            if _is_relu(mod):
+                self._store(slot, out)
+            else:
+                self._ptag[_tkey(out)] = (slot, weakref.ref(out))
+            return
+        if x is None:
+            return
+        k = _tkey(x)
+        pt = self._live(self._ptag, k)
+        if pt is not None:
+            if _is_relu(mod):
+                del self._ptag[k]
+                self._store(pt[0], out)
+                return
+            if _passes_tags(mod):
+                self._ptag[_tkey(out)] = (pt[0], weakref.ref(out))
+        ct = self._live(self._ctag, k)
+        if ct is not None and not _is_param_layer(mod) and _passes_tags(mod):
+            self._ctag[_tkey(out)] = (ct[0], weakref.ref(out))
+        if self.recompute_cheap and isinstance(mod, self._pools):
+            src = self._live(self._handles, _key(x))
+            if src is not None and src.layer is not None:
+                self._cheap[_key(out)] = (type(mod).__name__.lower(), mod, src, weakref.ref(out))
+
+    def _store(self, slot, out):
+        """`out` is the stored activation of `slot` (saved by its op before
+        this hook ran, or saved later by its consumer)."""
+        k = _key(out)
+        self._act_layer[k] = (slot, weakref.ref(out))
+        self._ctag[_tkey(out)] = (slot, weakref.ref(out))
+        if self._rec is not None:
+            self._rec.slots.append(slot)
+        lid = self._slot_layer[slot]
+        cons = self._explicit_consumer.get(lid)
+        if cons is not None:
+            self.consumers[slot] = cons
+        elif slot not in self.consumers or self._collecting:
+            self._await_consumer.append(slot)
+        h = self._live(self._handles, k)
+        if h is not None and h.layer is None:
+            self._promote(h, slot)
+
+    def _match_consumer(self, mod, x, out):
+        """mod (a Conv/Linear) consumes x: the consumer of every waiting slot
+        whose activation reaches it by dataflow, or whose registration-order
+        fallback it is."""
+        if not self._await_consumer:
+            return
+        ct = self._live(self._ctag, _tkey(x))
+        hit = []
+        for slot in self._await_consumer:
+            if (ct is not None and ct[0] == slot) or self._fallback_consumer.get(self._slot_layer[slot]) is mod:
+                hit.append(slot)
+        for slot in hit:
+            self._await_consumer.remove(slot)
+            self.consumers[slot] = mod
+            if self._collecting:
+                self._watch_grad(slot, out)
+
+    def _watch_grad(self, slot, out):
+        """L_bar of `slot`: per-sample max |g| of the loss gradient at its
+        consumer's output (training.py:358-361), un-averaged."""
+        if not getattr(out, "requires_grad", False):
+            return
+
+        def hook(g):
+            from .tensor import per_sample_max
+
+            scale = self.grad_scale if self.grad_scale is not None else (self._batch or 1)
+            _, lbar = per_sample_max(g.detach().float())
+            self._lbar[slot] = lbar * scale
+
+        out.register_hook(hook)
+
+    # ---- saved-tensor hooks ------------------------------------------------
     def _pack(self, t):
         import torch
 
-        if not (t.is_cuda and t.dtype == torch.float32) or isinstance(t, torch.nn.Parameter):
+        if t.dtype != torch.float32 or isinstance(t, torch.nn.Parameter):
             return ("raw", t)
         k = _key(t)
         h = self._live(self._handles, k)
@@ -322,22 +452,25 @@ class ActivationCompressor:
             self._promote(h, a[0])
         return h
 
-    def _promote(self, h, lid):
-        """Make h the stored activation of layer lid (raw, or queued for the
-        codec at the layer's planned error bound)."""
-        eb = self.plan.eb.get(lid) if self.plan is not None else None
-        h.layer, h.eb = lid, eb
+    def _promote(self, h, slot):
+        """Make h the stored activation of `slot` (raw, or queued for the
+        codec at the slot's planned error bound)."""
+        eb = self.plan.eb.get(slot) if self.plan is not None else None
+        h.layer, h.eb = slot, eb
         t = h.raw
         nbytes = t.numel() * 4
         if self._batch:
-            self._per_sample[lid] = nbytes / self._batch
+            self._per_sample[slot] = nbytes / self._batch
         if self._rec is not None:
             self._rec.raw_bytes += nbytes
         if eb is None:
-            self.store.put(lid, ActivationStore.RAW, None, nbytes)
+            self.store.put(slot, ActivationStore.RAW, None, nbytes)
             if self._rec is not None:
                 self._rec.stored_bytes += nbytes
+                self._rec.device_bytes += nbytes
             return
+        if not t.is_cuda:
+            raise ParameterError(f"activation of {slot!r} is not on a CUDA device: the codec has no CPU path")
         # launch now (side stream, no host sync); the oldest in-flight
         # compressions are finished -- container built, original released --
         # once more than `batch_flush` are in flight, so at most that many
@@ -345,22 +478,33 @@ class ActivationCompressor:
         params = CodecParams(eb=eb, radius=self.radius, preserve_zeros=self.preserve_zeros)
         # slots 1.. (never the thread's main context, which the decoders use
         # in backward while the last compressions may still be in flight)
-        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(lid)],
+        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(slot)],
                                own_scratch=True)
         self._slot = (self._slot + 1) % (self.batch_flush + 1)
         self._pending.append(h)
         while len(self._pending) > self.batch_flush:
             self._finish(self._pending.pop(0))
 
+    def capture_next_iteration(self, slots=None):
+        """Keep, for the next iteration, a host copy of every compressed
+        stored activation (or of `slots`) and its container, in `captured`
+        -- the per-layer spot check of training tensors against the
+        reference codec (per-layer ratio/eb vs oracle)."""
+        self._capture = set(slots) if slots is not None else True
+        self.captured = {}
+
     def _finish(self, h):
         (c, rep), = compress_end(h.job, compact=True)
         h.job = None
+        if self._capture is True or (self._capture and h.layer in self._capture):
+            self.captured[h.layer] = (h.raw.detach().reshape(-1).cpu().numpy(), c, h.eb)
         h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
         self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
         self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
         self._interval_ratios.setdefault(h.layer, []).append(rep.ratio)
         if self._rec is not None:
             self._rec.stored_bytes += rep.compressed_bytes
+            self._rec.device_bytes += c.device_nbytes
             self._rec.compressed[h.layer] = (rep.ratio, h.eb)
 
     def flush(self):
@@ -397,6 +541,8 @@ class ActivationCompressor:
                 self._pending.remove(h)
                 self._finish(h)
             if h.comp is not None:
+                # collection iterations read R back at once; otherwise the
+                # decode status is collected at the end of the iteration
                 out, nz = decompress_device(h.comp, dtype=torch.float32, check=self._collecting)
                 h.out = out.view(h.shape)
                 if self._collecting:
@@ -418,51 +564,41 @@ class ActivationCompressor:
         return out
 
     # ---- iteration protocol --------------------------------------------------
+    def _reset_iteration_state(self):
+        for d in (self._act_layer, self._handles, self._ptag, self._ctag, self._cheap, self._markers, self._calls):
+            d.clear()
+        self._await_consumer = []
+
     @contextlib.contextmanager
     def iteration(self):
         """Wrap forward + backward of one training iteration."""
         import torch
 
+        if self._status is not None:
+            # decode faults of the previous iteration's backward (reference
+            # decompress raises FormatError, codec.py:356-359)
+            tok, self._status = self._status, None
+            if _lib.decode_status_result(tok):
+                raise FormatError("invalid code in a stored activation's bitstream "
+                                  "(or outlier markers disagree with stored indices)")
         self._collecting = (self.it + 1) == self.next_collection
-        self._act_layer.clear()
-        self._handles.clear()
-        self._cheap.clear()
-        self._markers.clear()
+        self._reset_iteration_state()
+        self._batch = None  # taken from this iteration's first producer input
         self._R.clear()
         self._lbar.clear()
         self.store.clear()
         self.store.peak_bytes = 0
         self._rec = IterationRecord(self.it)
-        # the consumers' output-gradient hooks (L_bar) exist only in collection
-        # iterations: full backward hooks wrap every call of their module
-        relus = []
-        if self._collecting:
-            import torch.nn as nn
-
-            # full backward hooks forbid in-place ops on their modules' outputs:
-            # in-place ReLUs run out of place in collection iterations only
-            scope = self._model.modules() if self._model is not None else (
-                m for mod in self._modules() for m in mod.modules())
-            for m in scope:
-                if isinstance(m, nn.ReLU) and m.inplace:
-                    m.inplace = False
-                    relus.append(m)
-            for lid, (prod, cons) in self.layers.items():
-                self._bwd_hooks.append(cons.register_full_backward_hook(self._bwd_hook(lid)))
         try:
             with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack):
                 yield self
                 self.flush()
         finally:
-            for h in self._bwd_hooks:
-                h.remove()
-            self._bwd_hooks.clear()
-            for m in relus:
-                m.inplace = True
-        self._handles.clear()
-        self._act_layer.clear()
-        self._cheap.clear()
-        self._markers.clear()
+            self._reset_iteration_state()
+            if self.captured:
+                self._capture = None
+        if self.plan is not None and _lib.cuda_available():
+            self._status = _lib.take_decode_status()
 
     def after_step(self):
         """Call after optimizer.step(): interval boundary -> new plan."""
@@ -473,7 +609,7 @@ class ActivationCompressor:
             self.next_collection = (self.it + 1) + self.plan.W
             if budget is not None and self.controller.intervals_planned >= 2:
                 self.batch_size = self.plan_batch_size()
-            self._interval_ratios = {lid: [] for lid in self.layers}
+            self._interval_ratios = {}
         if budget is not None and (self.store.peak_bytes + self.fixed_bytes
                                    > budget * (1.0 - self.config.reserve_fraction)):
             self.controller.note_reserve_breach()  # training.py:420-426
@@ -483,19 +619,18 @@ class ActivationCompressor:
 
     def plan_batch_size(self) -> int:
         """Largest power-of-two batch whose projected activation bytes (per-
-        sample cost / observed ratio per layer, plus the input) and the
+        sample cost / observed ratio per slot, plus the input) and the
         model's fixed bytes fit the memory budget minus the reserve
         (controller.choose_batch_size; reference training.py:401-416)."""
         costs = {}
         if self.input_sample_bytes:
             costs["input"] = float(self.input_sample_bytes)
         ratios = {}
-        for lid in self.layers:
-            if lid in self._per_sample:
-                costs[lid] = self._per_sample[lid]
-            r = self._interval_ratios.get(lid)
+        for slot, cost in self._per_sample.items():
+            costs[slot] = cost
+            r = self._interval_ratios.get(slot)
             if r:
-                ratios[lid] = sum(r) / len(r)
+                ratios[slot] = sum(r) / len(r)
         return choose_batch_size(costs, ratios, self.config, fixed_bytes=self.fixed_bytes)
 
     @property
@@ -505,20 +640,35 @@ class ActivationCompressor:
     def _collect_stats(self):
         from .tensor import mean_abs
 
-        ids = list(self.layers)
-        N = self._batch or 1
-        R = [self._R.get(l, 0.0) for l in ids]
-        Lb = [self._lbar.get(l, 0.0) for l in ids]
+        ids = list(self._rec.slots) if self._rec is not None else []
+        world = 1
+        if self.sync_stats:
+            import torch.distributed as dist
+
+            if dist.is_available() and dist.is_initialized():
+                world = dist.get_world_size(self.dist_group)
+        # DDP averages the ranks' gradients: the error model's N is the
+        # global batch (a single-process run at that batch plans the same eb)
+        N = (self._batch or 1) * world
+        R = [self._R.get(s, 0.0) for s in ids]
+        Lb = [self._lbar.get(s, 0.0) for s in ids]
         M = []
-        for l in ids:
-            cons = self.layers[l][1]
-            st = self.optimizer.state.get(cons.weight, {})
-            v = st.get("momentum_buffer")
+        for s in ids:
+            cons = self.consumers.get(s)
+            v = None
+            w = getattr(cons, "weight", None) if cons is not None else None
+            if w is not None:
+                v = self.optimizer.state.get(w, {}).get("momentum_buffer")
             M.append(mean_abs(v) if v is not None else 0.0)
         if self.sync_stats:
             R, Lb, M = sync_layer_stats(R, Lb, M, self.dist_group)
-        return [LayerTrainingStats(layer_id=l, R=min(1.0, max(0.0, r)), L_bar=lb, M_avg=m, N=N)
-                for l, r, lb, m in zip(ids, R, Lb, M)]
+        return [LayerTrainingStats(layer_id=s, R=min(1.0, max(0.0, r)), L_bar=lb, M_avg=m, N=N)
+                for s, r, lb, m in zip(ids, R, Lb, M)]
+
+    def consumer_names(self) -> dict:
+        """slot -> qualified name of its consumer module (after a forward)."""
+        names = {id(m): n for n, m in (self._model.named_modules() if self._model is not None else [])}
+        return {s: names.get(id(m), type(m).__name__) for s, m in self.consumers.items()}
 
 
 def device_memory_budget(device=None, headroom_bytes: int = 0) -> int:

@@ -96,16 +96,105 @@ def test_activation_store_lifecycle():
         s.pop("conv1")
 
 
-def test_conv_layer_map():
+def _trace(model, x, iters=1):
+    """run the hooks in passthrough mode (first interval: slots filled raw,
+    no codec) on the CPU -- exercises the slot / consumer dataflow"""
+    torch = pytest.importorskip("torch")
+
+    opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
+    comp = ActivationCompressor(ActivationCompressor.conv_layer_map(model), opt,
+                                ctl.ControllerConfig(W_default=1000, W_floor=1))
+    y = torch.zeros(x.shape[0], dtype=torch.long)
+    for _ in range(iters):
+        opt.zero_grad()
+        with comp.iteration():
+            out = model(x)
+            torch.nn.functional.cross_entropy(out, y[: out.shape[0]]).backward()
+        opt.step()
+        comp.after_step()
+        assert comp.store.current_bytes == 0 and len(comp.store) == 0  # every slot consumed once
+    return comp
+
+
+def test_conv_layer_map_sequential():
     torch = pytest.importorskip("torch")
     import torch.nn as nn
 
+    torch.manual_seed(0)
     net = nn.Sequential(nn.Conv2d(3, 8, 3), nn.ReLU(inplace=True), nn.MaxPool2d(2), nn.Conv2d(8, 8, 3), nn.ReLU(),
-                        nn.Flatten(), nn.Linear(8, 4))
+                        nn.Flatten(), nn.Linear(8 * 4 * 4, 4))
     m = ActivationCompressor.conv_layer_map(net)
-    assert list(m) == ["0", "3"]
-    assert m["0"] == (net[1], net[3]) and m["3"] == (net[4], net[6])
-    assert m.model is net and net[1].inplace  # in-place ReLUs are switched off only while collecting
+    assert list(m) == ["0", "3"] and m.model is net
+    comp = _trace(net, torch.randn(2, 3, 14, 14), iters=2)
+    r = comp.records[-1]
+    assert r.slots == ["0", "3"] and r.markers == 1  # the max-pool output is recomputed
+    assert comp.consumer_names() == {"0": "3", "3": "6"}  # through a Flatten module
+    assert net[1].inplace
+
+
+def test_dataflow_slots_resnet50():
+    """torchvision Bottleneck calls one ReLU module three times per block:
+    each call is its own slot (the conv it follows); conv3's consumer is the
+    next block's conv1 across the residual add, not downsample.0 (reference
+    _consumer_map semantics, training.py:154-166)."""
+    torch = pytest.importorskip("torch")
+    tv = pytest.importorskip("torchvision")
+
+    torch.manual_seed(0)
+    net = tv.models.resnet50(num_classes=10)
+    comp = _trace(net, torch.randn(2, 3, 64, 64), iters=2)
+    r = comp.records[-1]
+    convs = [n for n, mod in net.named_modules() if isinstance(mod, torch.nn.Conv2d) and "downsample" not in n]
+    assert r.slots == convs and len(r.slots) == 49
+    cn = comp.consumer_names()
+    assert cn["conv1"] == "layer1.0.conv1"  # through the stem max-pool
+    assert cn["layer1.0.conv3"] == "layer1.1.conv1" and cn["layer1.2.conv3"] == "layer2.0.conv1"
+    assert cn["layer2.0.conv1"] == "layer2.0.conv2" and cn["layer4.2.conv3"] == "fc"
+    assert r.markers == 1  # stem max-pool output, read by layer1.0.conv1 and downsample.0
+
+
+def test_dataflow_slots_vgg16_alexnet():
+    torch = pytest.importorskip("torch")
+    tv = pytest.importorskip("torchvision")
+
+    torch.manual_seed(0)
+    vgg = tv.models.vgg16(num_classes=10)
+    comp = _trace(vgg, torch.randn(2, 3, 32, 32))
+    r = comp.records[-1]
+    assert len(r.slots) == 13 and r.markers == 5
+    assert comp.consumer_names()["features.28"] == "classifier.0"
+    alex = tv.models.alexnet(num_classes=10)
+    comp = _trace(alex, torch.randn(2, 3, 96, 96))
+    assert comp.consumer_names() == {"features.0": "features.3", "features.3": "features.6",
+                                     "features.6": "features.8", "features.8": "features.10",
+                                     "features.10": "classifier.1"}
+
+
+def test_shared_modules_get_per_call_slots():
+    """a conv called twice and a ReLU module shared by two convs: one slot
+    per call, no LifecycleError"""
+    torch = pytest.importorskip("torch")
+    import torch.nn as nn
+
+    class Net(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.a = nn.Conv2d(4, 4, 3, padding=1)
+            self.b = nn.Conv2d(4, 4, 3, padding=1)
+            self.relu = nn.ReLU(inplace=True)
+            self.fc = nn.Linear(4 * 8 * 8, 3)
+
+        def forward(self, x):
+            x = self.relu(self.a(x))
+            x = self.relu(self.a(x))
+            x = self.relu(self.b(x))
+            return self.fc(torch.flatten(x, 1))
+
+    torch.manual_seed(0)
+    net = Net()
+    comp = _trace(net, torch.randn(2, 4, 8, 8), iters=2)
+    assert comp.records[-1].slots == ["a", "a#1", "b"]
+    assert comp.consumer_names() == {"a": "a", "a#1": "b", "b": "fc"}
 
 
 def test_compressor_batch_planner_and_reserve_breaches():
@@ -122,7 +211,7 @@ def test_compressor_batch_planner_and_reserve_breaches():
     comp = ActivationCompressor(ActivationCompressor.conv_layer_map(net), opt, cfg, input_sample_bytes=3 * 32 * 32 * 4)
     nparams = sum(p.numel() for p in net.parameters())
     assert comp.fixed_bytes == 2 * 4 * nparams  # weights + velocity, fp32 (training.py:200)
-    comp._per_sample = {"0": 8 * 30 * 30 * 4.0, "2": 8 * 28 * 28 * 4.0}
+    comp._per_sample = {"0": 8 * 30 * 30 * 4.0, "2": 8 * 28 * 28 * 4.0}  # per stored slot
     comp._interval_ratios = {"0": [4.0, 6.0], "2": [8.0]}
     want = ctl.choose_batch_size({"input": 3 * 32 * 32 * 4.0, "0": 8 * 30 * 30 * 4.0, "2": 8 * 28 * 28 * 4.0},
                                  {"0": 5.0, "2": 8.0}, cfg, fixed_bytes=comp.fixed_bytes)

@@ -12,7 +12,7 @@ import bench  # noqa: E402
 import paper_2111_09562_b200 as pb  # noqa: E402
 
 torch.cuda.set_device(0)
-ts, ebs, info, _ = bench.build_workload(sys.argv[1] if len(sys.argv) > 1 else "alexnet256", "cuda")
+ts, ebs, info, _, _ = bench.build_workload(sys.argv[1] if len(sys.argv) > 1 else "alexnet256", "cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 res = []
 for t, eb in zip(ts, ebs):

@@ -19,7 +19,7 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--only", type=int, default=-1, help="only this layer index")
 args = ap.parse_args()
 torch.cuda.set_device(0)
-tensors, ebs, info, _ = bench.build_workload(args.workload, "cuda")
+tensors, ebs, info, _, _ = bench.build_workload(args.workload, "cuda")
 if args.only >= 0:
     tensors, ebs = [tensors[args.only]], [ebs[args.only]]
 outs = [torch.empty_like(t) for t in tensors]
