@@ -310,9 +310,9 @@ def host_threads():
 def cpu_tasks_for(tensors, ebs, max_elems=None):
     tasks = []
     for t, eb in zip(tensors, ebs):
-        a = t.detach().reshape(-1).cpu().numpy()
+        a = t.detach().cpu().numpy()  # shaped: CMTZ records the dims
         if max_elems:
-            a = a[:max_elems]
+            a = a.reshape(-1)[:max_elems]
         tasks.append((np.ascontiguousarray(a), float(eb)))
     return tasks
 

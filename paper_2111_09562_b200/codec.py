@@ -829,9 +829,11 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
         return out, None
     s.synchronize()
     r = _lib.DecodeResult.from_buffer_copy(ctx.dres)
-    if r.status:
-        raise FormatError("invalid code in bitstream or outlier markers disagree with stored indices")
-    if r.markers != c._n_outliers:
+    if r.status or r.markers != c._n_outliers:
+        # reported here: the context's sticky fault word is collected too
+        _lib.decode_status_result(_lib.take_decode_status(dev.index, s))
+        if r.status:
+            raise FormatError("invalid code in bitstream or outlier markers disagree with stored indices")
         raise FormatError("outlier markers disagree with stored indices")
     return out, int(r.nonzero)
 

@@ -497,7 +497,7 @@ class ActivationCompressor:
         (c, rep), = compress_end(h.job, compact=True)
         h.job = None
         if self._capture is True or (self._capture and h.layer in self._capture):
-            self.captured[h.layer] = (h.raw.detach().reshape(-1).cpu().numpy(), c, h.eb)
+            self.captured[h.layer] = (h.raw.detach().cpu().numpy(), c, h.eb)  # shaped: CMTZ records the dims
         h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
         self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
         self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)

@@ -140,7 +140,7 @@ def test_resnet50_trains_with_compressed_activations(oracle):
         ref = oracle.compress(xh, eb, debug=False)
         assert c.to_bytes() == ref.blob, slot
         out, _ = pb.decompress_device(c, dtype=torch.float32)
-        want = oracle.decompress_blob(ref.blob, xh.size).astype(np.float32)
+        want = oracle.decompress_blob(ref.blob, xh.size).astype(np.float32)  # noqa
         assert np.array_equal(out.reshape(-1).cpu().numpy().view(np.uint32), want.view(np.uint32)), slot
 
 
