@@ -219,7 +219,7 @@ CbLayout cb_layout(uint64_t A) {
 }
 
 // misc counters layout (u64 slots)
-enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SEGTICKET = 8, M_PACKTICKET = 9, M_SLOTS = 10 };
+enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SEGTICKET = 8, M_PACKTICKET = 9, M_K4LTICKET = 10, M_K4LMCOUNT = 11, M_SLOTS = 12 };
 
 constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
@@ -481,15 +481,15 @@ int actc_ctx_create(int device, actc_ctx **out) {
     delete c;
     return rc;
   }
+  CK(cudaMemset(c->misc.p, 0, c->misc.cap));  // self-resetting tickets start at 0
   CK(cudaFuncSetAttribute(k2_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2Smem));
   CK(cudaFuncSetAttribute(k2r_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2rSmem));
   int nb = 0;
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  const void *big[] = {(const void *)k4w_decode<0, 16, false>,  (const void *)k4w_decode<1, 16, false>,
-                       (const void *)k4w_decode<0, 32, false>,  (const void *)k4w_decode<1, 32, false>,
-                       (const void *)k4w_decode<2, 32, false>,  (const void *)k4w_decode<0, 16, true>,
-                       (const void *)k4w_decode<1, 16, true>,   (const void *)k3_seg_pack<uint16_t>,
+  const void *big[] = {(const void *)k4l_decode<0, false>,       (const void *)k4l_decode<1, false>,
+                       (const void *)k4l_decode<0, true>,        (const void *)k4l_decode<1, true>,
+                       (const void *)k4l_decode<2, true>,        (const void *)k3_seg_pack<uint16_t>,
                        (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
                        (const void *)k3_seg_count<uint32_t>,    (const void *)k1_quant_lorenzo_hist<uint16_t>,
                        (const void *)k1_quant_lorenzo_hist<uint32_t>, (const void *)k_hist_u32};
@@ -836,38 +836,29 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   st.agg_r = (int *)(b + o); o += ((ntiles * 4 + 255) / 256) * 256;
   st.agg_v = (long long *)(b + o); o += ntiles * 8;
   st.inc_v = (long long *)(b + o);
-  const bool warp_dec = S.chunk_lat_dev || mode == 2;
+  // indexed streams (compress-time chunk lattice, or the raw-symbol debug
+  // mode) decode with K4L; streams from bytes (bit offsets rebuilt, no
+  // lattice) and the absurd-eb case (2*eb = inf: every value is +-inf/NaN)
+  // with the look-back scan decoder K4
+  const bool lane_dec = (S.chunk_lat_dev || mode == 2) && (mode == 2 || isfinite(2.0 * S.eb));
   unsigned *ticket = (unsigned *)((unsigned long long *)c->misc.p + M_TICKET);
-  if (!warp_dec && phase != 1) {  // look-back state of the scan decoder
+  if (!lane_dec && phase != 1) {  // look-back state of the scan decoder
     CK(cudaMemsetAsync(st.flag, 0, ntiles * 4, s));
     CK(cudaMemsetAsync(ticket, 0, 8, s));
   }
   // the result mailbox is only read back when the caller asks for it
-  if ((res_host || !warp_dec) && phase != 1) CK(cudaMemsetAsync(c->dres_dev, 0, offsetof(DecResult, sticky), s));
-  // decoder choice for indexed streams: the warp decoder with symbols
-  // resolved in the decode chain while the canonical table fits its shared
-  // cache; the lane decoder (sequential reconstruction, canonical indices
-  // translated off the chain) for wide alphabets.  ACTC_DEC=k4w|k4wci|k4x
-  // forces one (measurements).
-  static const char *force = getenv("ACTC_DEC");
+  if ((res_host || !lane_dec) && phase != 1) CK(cudaMemsetAsync(c->dres_dev, 0, offsetof(DecResult, sticky), s));
   const bool sw16 = 2ull * S.radius <= 65536 && mode != 2;
-  int kind = (sw16 && S.live_symbols <= K4W_MAX_LIVE) ? 0 : 2;  // 0 k4w, 1 k4w ci rows, 2 k4x
-  if (force) kind = !strcmp(force, "k4w") ? 0 : !strcmp(force, "k4wci") ? 1 : 2;
-  if (kind == 1 && !(sw16 && mode != 2)) kind = 0;
-  const bool lane_dec = warp_dec && kind == 2;
-  // a table built at compress time (k_build_table_plan) follows the same
-  // choice rule; an ACTC_DEC override or the debug mode builds its own
-  const bool prebuilt = S.table_dev && warp_dec && !force && mode != 2 && kind != 1;
+  // a table built at compress time (the pack kernel's first CTAs) is the K4L table
+  const bool prebuilt = S.table_dev && lane_dec && mode != 2;
   if (prebuilt && phase == 1) return ACTC_OK;
-  // batches skip the table-only call for streams that carry a table; if the
-  // table cannot be used here (decoder override), the decoder call builds one
+  // batches skip the table-only call for streams that carry a table
   if (!prebuilt && (phase != 2 || S.table_dev)) {
     KT(ACTC_KIND_LUT);
     if (lane_dec)
-      k_build_lut8<<<16, 256, 0, s>>>(S.len_counts_dev, (uint8_t *)c->lut.p);
+      k4l_build_table<<<kLutSize / 256, 256, 0, s>>>(S.len_counts_dev, (uint32_t *)c->lut.p);
     else
-      k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p,
-                                                 warp_dec ? ((kind == 1 ? 1 : 0) | 2) : 0);
+      k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p, 0);
   }
   CKL();
   if (phase == 1) return ACTC_OK;
@@ -895,34 +886,24 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.status = &c->dres_dev->status;
   a.chunk_lat = (const long long *)S.chunk_lat_dev;
   a.live = S.live_symbols;
+  a.mcount = nullptr;
   KT(ACTC_KIND_DECODE);
   if (lane_dec) {
-    const void *f = mode == 0 ? (const void *)k4x_decode<0> : mode == 1 ? (const void *)k4x_decode<1>
-                                                                        : (const void *)k4x_decode<2>;
-    const int occ = occupancy(f, K4X_THREADS, 0);
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nchunks, K4X_THREADS),
-                                                                      (uint64_t)std::max(1, occ) * c->num_sms));
-    if (mode == 0)
-      k4x_decode<0><<<grid, K4X_THREADS, 0, s>>>(a);
-    else if (mode == 1)
-      k4x_decode<1><<<grid, K4X_THREADS, 0, s>>>(a);
-    else
-      k4x_decode<2><<<grid, K4X_THREADS, 0, s>>>(a);
-  } else if (warp_dec) {
-    // warp decoder: no scan, no look-back
-    const int NW = K4W_THREADS / 32;
-    const size_t smem = (size_t)NW * 32 * (sw16 ? 33 : 65) * 4;  // ROUND = 64 rows (+1 pad word)
-    const bool cir = kind == 1;
-    const void *f = mode == 0 ? (cir ? (const void *)k4w_decode<0, 16, true>
-                                     : sw16 ? (const void *)k4w_decode<0, 16, false> : (const void *)k4w_decode<0, 32, false>)
-                  : mode == 1 ? (cir ? (const void *)k4w_decode<1, 16, true>
-                                     : sw16 ? (const void *)k4w_decode<1, 16, false> : (const void *)k4w_decode<1, 32, false>)
-                              : (const void *)k4w_decode<2, 32, false>;
-    const int occ = occupancy(f, K4W_THREADS, smem);
-    const uint64_t nwt = cdiv(nchunks, 32);
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(nwt, NW), (uint64_t)std::max(1, occ) * c->num_sms));
+    // K4L: one 1024-thread CTA per SM (persistent over 32-chunk warp tiles);
+    // canonical deltas in shared memory for 16-bit symbols
+    const bool gcanon = !sw16 || S.live_symbols > K4L_SMEM_LIVE;
+    if (mode != 2 && S.n_outliers) {
+      a.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_K4LTICKET);
+      a.mcount = (unsigned long long *)c->misc.p + M_K4LMCOUNT;
+    }
+    const void *f = mode == 2 ? (const void *)k4l_decode<2, true>
+                  : mode == 1 ? (gcanon ? (const void *)k4l_decode<1, true> : (const void *)k4l_decode<1, false>)
+                              : (gcanon ? (const void *)k4l_decode<0, true> : (const void *)k4l_decode<0, false>);
+    const size_t smem = k4l_smem_bytes(S.live_symbols, gcanon);
+    const uint64_t ntl = cdiv(nchunks, 32);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, K4L_THREADS / 32), (uint64_t)c->num_sms));
     void *args[] = {&a};
-    CK(cudaLaunchKernel(f, dim3(grid), dim3(K4W_THREADS), args, smem, s));
+    CK(cudaLaunchKernel(f, dim3(grid), dim3(K4L_THREADS), args, smem, s));
   } else {
     const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
     const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)(sw16 ? c->k4_blocks[0] : c->k4_blocks[1]));

@@ -1,0 +1,487 @@
+// K4L: lane-serial canonical-Huffman decode fused with the inverse Lorenzo
+// reconstruction, outlier splice and re-zero filter, for streams that carry
+// the device-side decode index (bit offset + lattice value before every
+// ACTC_CHUNK-th symbol, recorded at compress time).
+//
+// Replaces huffman_decode/_decode_bits (huffman.py:120-142, 210-236), the
+// marker check (codec.py:356-359), lorenzo_decode (codec.py:275-293) and
+// recon / splice / re-zero (codec.py:360-369).
+//
+// Work unit: a warp owns 32 consecutive chunks (4096 symbols); lane l decodes
+// chunk l sequentially.  Per symbol the serial chain is one shared-memory
+// lookup: W (32-bit left-aligned window, one funnel shift) -> T1[W >> 20],
+// whose entry holds the code length and the canonical index of the first
+// code under the 12-bit prefix, exact whenever every code under the prefix
+// has one length (all prefixes except those a length boundary cuts, at most
+// one per length).  The canonical index -> Lorenzo delta lookup, the running
+// lattice sum, the fp64 reconstruction and the nonzero count hang off that
+// chain (independent of the next symbol's window).  Prefixes with mixed
+// lengths, codes longer than 32 bits, outlier markers and invalid codes take
+// a warp-voted slow path (the reference's bit rule on a 64-bit window).
+// Values leave through a per-warp transposition buffer: lanes store four
+// values at a time (16 B, conflict-free row stride), the warp then writes 8
+// chunk rows of 64 B per instruction.  One 1024-thread CTA per SM holds the
+// prefix table (16 KB), the canonical deltas (int16, <= 128 KB) and the
+// transposition rows (80 KB).
+#include <type_traits>
+
+#include "kernels.cuh"
+
+namespace actc {
+
+namespace {
+
+constexpr int kRowBytes = 80;  // 64 B of values + 16 B pad (odd number of 16-B units)
+
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t n) {  // x >> n, 0 for n >= 32
+  uint32_t r;
+  asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+  return r;
+}
+
+__device__ __forceinline__ uint64_t k4l_bits64(const uint32_t *__restrict__ pw, uint64_t pos) {
+  const uint64_t wi = pos >> 5;
+  const unsigned sh = pos & 31;
+  const uint64_t hi = ((uint64_t)bswap32(__ldg(pw + wi)) << 32) | bswap32(__ldg(pw + wi + 1));
+  if (!sh) return hi;
+  const uint32_t lo = bswap32(__ldg(pw + wi + 2));
+  return (hi << sh) | ((uint64_t)lo >> (32 - sh));
+}
+
+template <int MODE>
+struct OutT;
+template <>
+struct OutT<0> {
+  typedef float T;
+};
+template <>
+struct OutT<1> {
+  typedef double T;
+};
+template <>
+struct OutT<2> {
+  typedef uint32_t T;
+};
+
+}  // namespace
+
+__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, uint32_t *__restrict__ table) {
+  k4l_table_rows(len_counts, table, blockIdx.x);
+}
+
+size_t k4l_smem_bytes(uint32_t live, bool gcanon);
+
+// shared-window address kept in a register (otherwise the compiler rebuilds
+// it from SR_CgaCtaId at every access inside the decode loop)
+__device__ __forceinline__ uint32_t k4l_saddr(const void *p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t k4l_lds(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int k4l_lds_s16(uint32_t addr) {
+  short v;
+  asm("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+
+struct K4LShared {
+  unsigned long long first[64];
+  uint32_t count[64], base[64];
+  uint32_t maxlen;
+};
+
+// Payload staging: every lane streams its own chunk, so each lane keeps a
+// ring of kRingGroups 16-byte groups of its bitstream in shared memory
+// (layout [group slot][lane], 16 B per entry), filled by cp.async (LDGSTS,
+// L1 bypassed) once per round for the groups it has moved past.  The decode
+// chain reads the next word from the ring (shared-memory latency) instead of
+// waiting for a global load on every refill.
+constexpr int kRingGroups = 8;
+constexpr int kRingBytesPerWarp = kRingGroups * 32 * 16;
+
+__device__ __forceinline__ void k4l_cp16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void k4l_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void k4l_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// per-lane decode state of one chunk
+template <bool NARROW>
+struct K4LLane {
+  typedef typename std::conditional<NARROW, int, long long>::type Lat;
+  uint32_t a;       // word index (in the payload) of cur
+  uint32_t issued;  // next 16-B group to stage
+  uint32_t cur, nxt, nn, boff;
+  Lat P;
+  uint32_t ordn;
+  bool ord_known;
+};
+
+struct K4LRing {
+  uint32_t base;   // shared address of this lane's slot 0: ring + lane*16
+  uint32_t capg;   // groups of the payload buffer (staging never reads past it)
+  const uint32_t *pw;
+  __device__ __forceinline__ uint32_t addr(uint32_t w) const {  // shared address of payload word w
+    return base + ((w >> 2) & (kRingGroups - 1)) * 512u + (w & 3u) * 4u;
+  }
+  __device__ __forceinline__ uint32_t word(uint32_t w) const {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr(w)));  // ordered after the cp.async waits
+    return bswap32(v);
+  }
+  // stage groups [issued, upto) (bounded by the buffer)
+  __device__ __forceinline__ void stage(uint32_t &issued, uint32_t upto) const {
+    upto = min(upto, capg);
+    for (; issued < upto; issued++) k4l_cp16(base + (issued & (kRingGroups - 1)) * 512u, pw + 4ull * issued);
+    k4l_commit();
+  }
+};
+
+// (re)seed a lane's ring at word a and load its window (waits for the data)
+template <bool NARROW>
+__device__ __forceinline__ void k4l_seed(const K4LRing &rg, K4LLane<NARROW> &L, uint32_t a) {
+  k4l_wait<0>();  // no copy into the ring may still be in flight
+  L.a = a;
+  L.issued = a >> 2;
+  rg.stage(L.issued, (a >> 2) + kRingGroups);
+  k4l_wait<0>();
+  L.cur = rg.word(a);
+  L.nxt = rg.word(a + 1);
+  L.nn = rg.word(a + 2);
+}
+
+// The rare path of one symbol (lane-divergent): the reference's bit rule
+// for a prefix the table does not resolve (scan from the prefix's shortest
+// length l0), and the outlier-marker splice.  Fixes len/delta/P/val/nzi of
+// the common path; the caller advances the window.
+template <int MODE, bool NARROW, typename T>
+__device__ __forceinline__ void k4l_slow(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg,
+                                         K4LLane<NARROW> &L, uint32_t e, uint32_t W, uint32_t &len, int &delta,
+                                         T &val, uint32_t &nzi, uint64_t e_idx, uint64_t e0, bool &bad,
+                                         unsigned long long &markers) {
+  const int radius = (int)a.radius;
+  const long long Pprev = (long long)L.P - delta;
+  if (len == 0u) {
+    // huffman.py:129-141: the first length whose code offset is in range
+    const int maxlen = (int)sh.maxlen;
+    int l = max(1, (int)(e >> 6));
+    uint32_t ci = 0;
+    len = 0;
+    for (; l <= min(maxlen, 32); l++) {
+      const uint32_t of = shr_clamp(W, 32u - (uint32_t)l) - (uint32_t)sh.first[l];
+      if ((unsigned long long)(shr_clamp(W, 32u - (uint32_t)l)) >= sh.first[l] && of < sh.count[l]) {
+        ci = sh.base[l] + of;
+        len = (uint32_t)l;
+        break;
+      }
+    }
+    if (!len && maxlen > 32) {
+      // codes longer than 32 bits: a 64-bit window from the payload
+      const uint64_t win = k4l_bits64(a.payload, ((uint64_t)L.a << 5) + L.boff);
+      for (l = max(l, 33); l <= maxlen; l++) {
+        const unsigned long long cd = win >> (64 - l), of = cd - sh.first[l];
+        if (of < sh.count[l]) {
+          ci = sh.base[l] + (uint32_t)of;
+          len = (uint32_t)l;
+          break;
+        }
+      }
+    }
+    if (!len) {
+      bad = true;  // invalid code (-2), or a stream cut short
+      len = 1;
+    }
+    delta = (int)(__ldg(a.canon + min(ci, a.live - 1)) - (uint32_t)radius);
+    L.boff += len;
+    if (L.boff >= 64u) {
+      // a code of more than 32 bits ran past the window: re-seed the ring
+      const uint64_t np = ((uint64_t)L.a << 5) + L.boff;
+      L.boff = (uint32_t)(np & 31);
+      k4l_seed(rg, L, (uint32_t)(np >> 5));
+    }
+  }
+  if (!NARROW && MODE != 2 && delta == -radius) {
+    // outlier marker: the chain rebases on prequantize(value) and the value
+    // is spliced, then re-zeroed (codec.py:286-292, 361-368)
+    if (!L.ord_known) {
+      uint64_t lo = 0, hi = a.k;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a.out_idx[mid] < e0) lo = mid + 1; else hi = mid;
+      }
+      L.ordn = (uint32_t)lo;
+      L.ord_known = true;
+    }
+    float ov = 0.0f;
+    if (L.ordn >= a.k || a.out_idx[L.ordn] != e_idx) bad = true;
+    else ov = a.out_val[L.ordn];
+    L.ordn++;
+    markers++;
+    bool dummy;
+    L.P = (typename K4LLane<NARROW>::Lat)quant_exact((double)ov, a.two_eb, a.eb, dummy);
+    double rv = (double)ov;
+    if (a.preserve && fabs(rv) <= a.eb) rv = 0.0;
+    val = (T)rv;
+    nzi = rv != 0.0;
+  } else {
+    L.P = (typename K4LLane<NARROW>::Lat)(Pprev + delta);
+    if (MODE == 2) {
+      val = (T)(uint32_t)(delta + radius);
+    } else {
+      val = (T)__dmul_rn((double)L.P, a.two_eb);
+      nzi = L.P != 0;
+    }
+  }
+}
+
+// decode one lane's chunk (ACTC_CHUNK symbols, or cnt when !FULL) of a
+// 32-chunk tile and write the tile's values out through the warp's rows
+template <int MODE, bool GCANON, bool FULL, bool NARROW>
+__device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg, uint32_t t1_s,
+                                         uint32_t cd_s, uint32_t wrows, uint64_t tile, uint64_t nchunks,
+                                         uint32_t cnt, uint64_t e0, K4LLane<NARROW> &L,
+                                         unsigned long long &nonzero, unsigned long long &markers, bool &bad) {
+  typedef typename OutT<MODE>::T T;
+  constexpr int VPU = 16 / (int)sizeof(T);  // values per 16-B unit
+  constexpr int R = 4 * VPU;                // symbols per lane per round (one 64-B row)
+  const int lane = threadIdx.x & 31;
+  const int radius = (int)a.radius;
+  const double two_eb = a.two_eb;
+  const uint32_t myrow = wrows + lane * kRowBytes;
+  uint32_t nzc = 0;
+  uint32_t safe_g = L.issued;  // groups known to have landed
+  for (int r = 0; r < ACTC_CHUNK / R; r++) {
+    // the fast path reads at most R + 2 words ahead this round
+    if (((L.a + R + 2) >> 2) >= safe_g) k4l_wait<0>();
+    else k4l_wait<1>();
+    for (int u = 0; u < 4; u++) {
+      T v[VPU];
+#pragma unroll
+      for (int q = 0; q < VPU; q++) {
+        const uint32_t i = (uint32_t)(r * R + u * VPU + q);
+        const bool act = FULL || i < cnt;
+        const uint32_t W = __funnelshift_l(L.nxt, L.cur, L.boff);
+        const uint32_t e = k4l_lds(t1_s + ((W >> 20) << 2));
+        uint32_t len = e & 63u;
+        const uint32_t ci = (e >> 6) + shr_clamp(W & 0xFFFFFu, 32u - len);
+        int delta = GCANON ? (int)(__ldg(a.canon + min(ci, a.live - 1)) - (uint32_t)radius)
+                           : k4l_lds_s16(cd_s + 2u * ci);
+        if (!FULL && !act) {
+          len = 0;
+          delta = 0;
+        }
+        L.P += delta;
+        T val;
+        uint32_t nzi = 0;
+        if (MODE == 2) {
+          val = (T)(uint32_t)(delta + radius);
+        } else {
+          val = (T)__dmul_rn((double)L.P, two_eb);
+          nzi = L.P != 0;
+        }
+        L.boff += len;
+        // outlier markers exist only in streams with outliers (not NARROW)
+        const bool spec = (FULL || act) && (len == 0u || (!NARROW && MODE != 2 && delta == -radius));
+        if (spec)
+          k4l_slow<MODE, NARROW, T>(a, sh, rg, L, e, W, len, delta, val, nzi, e0 + i, e0, bad, markers);
+        {
+          // branch-free window advance by one word (the ring read is issued
+          // every symbol; the selects keep the warp converged)
+          const bool adv = L.boff >= 32u;
+          const uint32_t w3 = rg.word(L.a + 3);
+          L.a += adv ? 1u : 0u;
+          L.cur = adv ? L.nxt : L.cur;
+          L.nxt = adv ? L.nn : L.nxt;
+          L.nn = adv ? w3 : L.nn;
+          L.boff -= adv ? 32u : 0u;
+        }
+        if (FULL || act) nzc += nzi;
+        v[q] = val;
+      }
+      uint4 pk;
+      memcpy(&pk, v, 16);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(myrow + 16u * u), "r"(pk.x), "r"(pk.y),
+                   "r"(pk.z), "r"(pk.w)
+                   : "memory");
+    }
+    // stage the groups this lane moved past (one commit group per round)
+    safe_g = L.issued;
+    rg.stage(L.issued, (L.a >> 2) + kRingGroups);
+    __syncwarp();
+    // write-out: instruction t stores rows 8t .. 8t+7 (row = chunk of the
+    // tile), each lane one 16-B unit; unit u of row rho sits at 16*(5*rho+u)
+    const int rho_l = lane & 7, uu = lane >> 3;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int rho = 8 * t + rho_l;
+      uint4 val4;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(val4.x), "=r"(val4.y), "=r"(val4.z), "=r"(val4.w)
+                   : "r"(wrows + rho * kRowBytes + 16u * uu)
+                   : "memory");
+      const uint64_t ch = tile * 32 + rho;
+      const uint64_t el = ch * ACTC_CHUNK + (uint64_t)r * R + (uint64_t)uu * VPU;
+      T *dst = reinterpret_cast<T *>(a.out) + el;
+      if (FULL) {
+        __stcs(reinterpret_cast<uint4 *>(dst), val4);
+      } else if (ch < nchunks) {
+        const uint64_t lim = min(a.n, (ch + 1) * ACTC_CHUNK);
+        if (el + VPU <= lim) {
+          __stcs(reinterpret_cast<uint4 *>(dst), val4);
+        } else {
+          T tmp[VPU];
+          memcpy(tmp, &val4, 16);
+          for (int k = 0; k < VPU; k++)
+            if (el + k < lim) dst[k] = tmp[k];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  nonzero += nzc;
+}
+
+template <int MODE, bool GCANON>
+__global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
+  constexpr int NW = K4L_THREADS / 32;
+  extern __shared__ __align__(16) unsigned char k4l_sm[];
+  uint32_t *t1 = reinterpret_cast<uint32_t *>(k4l_sm);
+  unsigned char *rows = k4l_sm + kLutSize * 4;
+  unsigned char *ring = rows + NW * 32 * kRowBytes;
+  int16_t *cdelta = reinterpret_cast<int16_t *>(ring + NW * kRingBytesPerWarp);
+  __shared__ K4LShared sh;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kLutSize / 4; i += K4L_THREADS)
+    reinterpret_cast<uint4 *>(t1)[i] = __ldg(reinterpret_cast<const uint4 *>(a.lut) + i);
+  const int radius = (int)a.radius;
+  if (!GCANON) {
+    // canonical deltas (symbol - radius; the outlier marker is -radius)
+    const uint32_t live = a.live;
+    for (uint32_t i = 4 * tid; i < live; i += 4 * K4L_THREADS) {
+      if (i + 4 <= live) {
+        const uint4 c = __ldg(reinterpret_cast<const uint4 *>(a.canon + i));
+        const uint32_t lo = ((uint32_t)(c.x - radius) & 0xFFFFu) | ((uint32_t)(c.y - radius) << 16);
+        const uint32_t hi = ((uint32_t)(c.z - radius) & 0xFFFFu) | ((uint32_t)(c.w - radius) << 16);
+        *reinterpret_cast<uint2 *>(cdelta + i) = make_uint2(lo, hi);
+      } else {
+        for (uint32_t k = i; k < live; k++) cdelta[k] = (int16_t)((int)a.canon[k] - radius);
+      }
+    }
+  }
+  if (tid == 0) {
+    unsigned long long code = 0;
+    uint32_t idx = 0, mx = 0;
+    for (int l = 0; l < 64; l++) {
+      code <<= 1;
+      const uint32_t c = a.len_counts[l];
+      sh.first[l] = code;
+      sh.count[l] = c;
+      sh.base[l] = idx;
+      code += c;
+      idx += c;
+      if (c && l > 0) mx = l;
+    }
+    sh.maxlen = mx;
+  }
+  __syncthreads();
+
+  const uint64_t n = a.n;
+  const uint64_t nchunks = (n + ACTC_CHUNK - 1) / ACTC_CHUNK;
+  const uint64_t ntiles = (nchunks + 31) / 32;
+  const uint32_t t1_s = k4l_saddr(t1);
+  const uint32_t cd_s = k4l_saddr(cdelta);
+  K4LRing rg;
+  rg.base = k4l_saddr(ring + warp * kRingBytesPerWarp) + lane * 16u;
+  rg.pw = a.payload;
+  // groups of the payload buffer: 4*ceil(bits/32) + 32 bytes (codec.py
+  // buffers carry the decoder's over-read pad)
+  rg.capg = (uint32_t)(((a.payload_bits + 31) / 32 * 4 + 32) / 16);
+  const uint32_t wrows = k4l_saddr(rows) + warp * 32 * kRowBytes;  // this warp's 32 rows
+  unsigned long long nonzero = 0, markers = 0;
+  bool bad = false;
+  // 32-bit lattice arithmetic: no outliers (no rebase) and 16-bit deltas, so
+  // a chunk moves its running value by < 2^22 from a start below 2^30
+  const bool narrow_ok = MODE == 2 || (a.k == 0 && radius <= 32768);
+
+  for (uint64_t tile = (uint64_t)blockIdx.x * NW + warp; tile < ntiles; tile += (uint64_t)gridDim.x * NW) {
+    const uint64_t c = tile * 32 + lane;
+    const bool valid = c < nchunks;
+    const uint64_t e0 = c * ACTC_CHUNK;
+    const uint32_t cnt = valid ? (uint32_t)min((uint64_t)ACTC_CHUNK, n - e0) : 0u;
+    const bool full = (tile + 1) * 32 * ACTC_CHUNK <= n;  // warp-uniform
+    uint64_t pos0 = 0, endp = 0;
+    long long P0 = 0;
+    if (valid) {
+      pos0 = a.chunk_off[c];
+      endp = (c + 1 < nchunks) ? a.chunk_off[c + 1] : a.payload_bits;
+      if (MODE != 2) P0 = a.chunk_lat[c];
+    }
+    const bool narrow = narrow_ok && __all_sync(0xffffffffu, P0 > -(1ll << 30) && P0 < (1ll << 30));
+    uint64_t pos_end;
+#define K4L_RUN(FULLV, NARROWV)                                                                          \
+  {                                                                                                    \
+    K4LLane<NARROWV> L;                                                                                \
+    L.boff = (uint32_t)(pos0 & 31);                                                                    \
+    k4l_seed(rg, L, (uint32_t)(pos0 >> 5));                                                           \
+    L.P = (typename K4LLane<NARROWV>::Lat)P0;                                                          \
+    L.ordn = 0;                                                                                        \
+    L.ord_known = false;                                                                               \
+    k4l_tile<MODE, GCANON, FULLV, NARROWV>(a, sh, rg, t1_s, cd_s, wrows, tile, nchunks, cnt, e0, L, nonzero, \
+                                            markers, bad);                                             \
+    pos_end = ((uint64_t)L.a << 5) + L.boff;                                                           \
+  }
+    if (full && narrow) K4L_RUN(true, true)
+    else if (full) K4L_RUN(true, false)
+    else K4L_RUN(false, false)
+#undef K4L_RUN
+    if (valid && (pos_end != endp || endp > a.payload_bits)) bad = true;
+  }
+  k4l_wait<0>();
+  if (bad) report_format_error(a);
+  const unsigned long long ws = warp_sum(nonzero), wm = warp_sum(markers);
+  if (lane == 0) {
+    if (ws) atomicAdd(a.nonzero, ws);
+    if (wm) atomicAdd(a.markers, wm);
+    if (wm && a.mcount) atomicAdd(a.mcount, wm);
+  }
+  // the last CTA checks that every stored outlier met its marker
+  // (codec.py:356-359: the marker positions must equal the stored indices)
+  if (a.mcount && MODE != 2) {
+    __shared__ unsigned s_last;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && tid == 0) {
+      __threadfence();
+      const unsigned long long tot = atomicAdd(a.mcount, 0ull);
+      if (tot != a.k) report_format_error(a);
+      *a.mcount = 0;  // self-resetting for the next launch on this context
+      *a.ticket = 0;
+    }
+  }
+}
+
+size_t k4l_smem_bytes(uint32_t live, bool gcanon) {
+  return (size_t)kLutSize * 4 + (size_t)K4L_THREADS / 32 * (32 * kRowBytes + kRingBytesPerWarp) +
+         (gcanon ? 0 : (((size_t)live * 2 + 15) & ~(size_t)15));
+}
+
+template __global__ void k4l_decode<0, false>(DecodeArgs);
+template __global__ void k4l_decode<1, false>(DecodeArgs);
+template __global__ void k4l_decode<0, true>(DecodeArgs);
+template __global__ void k4l_decode<1, true>(DecodeArgs);
+template __global__ void k4l_decode<2, true>(DecodeArgs);
+
+}  // namespace actc

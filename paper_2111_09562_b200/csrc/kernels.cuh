@@ -27,12 +27,10 @@ constexpr int K3L_WORDS = (K3L_SEG * K3_SHORT_MAXLEN + 31) / 32 + 2;      // pac
 // K4 (scan variant, streams without a lattice index): one thread per chunk
 constexpr int K4_THREADS = 128;
 // K4 (warp variant, indexed streams): one warp per 32 chunks
-constexpr int K4W_THREADS = 256;
-constexpr int K4W_CANON_CACHE = 8192;
-// decoder choice for indexed streams: k4w up to this many live symbols (its
-// symbol cache holds the 8192 most frequent; beyond ~2x that the lane
-// decoder k4x is faster: 11.9 K live 205 vs 240 us, 20.7 K 123 vs 104 us)
-constexpr uint32_t K4W_MAX_LIVE = 16384;
+// K4L (indexed streams): one 768-thread CTA per SM, lane per chunk; the
+// canonical deltas stay in shared memory up to K4L_SMEM_LIVE live symbols
+constexpr int K4L_THREADS = 768;
+constexpr uint32_t K4L_SMEM_LIVE = 24576;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
 // lookback status for the encoder (per K3 tile)
@@ -202,7 +200,7 @@ struct SegArgs {
   void *table;    // decode table built by the first pack CTAs (null: none)
   actc_plan_t *plan_host;  // mapped pinned plan mailbox the pack's last CTA fills (null: none)
   unsigned *pack_ticket;   // pack CTAs done (zero, reset by the last)
-  int sw16;       // 16-bit symbols (the k4w / k4x choice of the table)
+  int sw16;       // 16-bit symbols
 };
 // resolve a device-planned SegArgs; false = this stream takes the host path
 __device__ __forceinline__ bool seg_resolve(SegArgs &a) {
@@ -234,7 +232,7 @@ __global__ void k3_seg_pack(const SymT *__restrict__ sym, SegArgs a);
 
 // mode bit0: short-code entries carry the canonical index instead of the
 // symbol; bit1: long prefixes with a single code length get "exact" entries
-// (length field 63, length above it) -- k4w only
+// (length field 63, length above it)
 __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *__restrict__ len_counts,
                             uint32_t *__restrict__ lut, int mode);
 
@@ -265,6 +263,7 @@ struct DecodeArgs {
   unsigned long long *nonzero;
   unsigned long long *markers;
   unsigned *status;
+  unsigned long long *mcount;  // K4L: markers of this launch (null: no stored outliers), self-resetting
 };
 // a decode fault: the call's status word and, right after it, the context's
 // sticky word (collected by actc_ctx_take_status at the caller's next sync --
@@ -278,13 +277,20 @@ __device__ __forceinline__ void report_format_error(const DecodeArgs &a) {
 // SW: staging width of decoded symbols in shared memory (16 or 32 bits)
 template <int MODE, int SW>
 __global__ void k4_decode(DecodeArgs a);
-template <int MODE, int SW, bool CIR>
-__global__ void k4w_decode(DecodeArgs a);
-// K4x: lane per chunk, sequential inverse Lorenzo in registers
-constexpr int K4X_THREADS = 256;
-__global__ void k_build_lut8(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8);
-template <int MODE>
-__global__ void k4x_decode(DecodeArgs a);
+// K4L decode table (kLutWords words): T1[p] for every 12-bit prefix p of
+// the left-aligned 32-bit window = (ci_base << 6) | len when every code
+// under p has length len (<= 32), the canonical index of the code under the
+// window W being ci_base + ((W & 0xFFFFF) >> (32 - len)); otherwise
+// (l0 << 6) with length field 0 (the decoder's slow path), l0 the shortest
+// length a code under p can have (0: no code, or an over-subscribed table,
+// whose first-match rule the scan from length 1 reproduces).  Word kLutSize: 1 if the code table is prefix-free
+// (Kraft <= 1), word kLutSize + 1: the longest code length.
+__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, uint32_t *__restrict__ table);
+// MODE: 0 = fp32 recon, 1 = fp64 recon, 2 = raw u32 symbols;
+// GCANON: canonical symbols read from global memory (wide alphabets)
+template <int MODE, bool GCANON>
+__global__ void k4l_decode(DecodeArgs a);
+size_t k4l_smem_bytes(uint32_t live, bool gcanon);
 __global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
                                 unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
 
@@ -410,53 +416,77 @@ __device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, c
   lut[p] = e;
 }
 
-// K4x u8 length table: lut8[p] = l0 when every code whose left-aligned
-// 32-bit value starts with the kXBits-bit prefix p has a length in
-// [l0, l0+3] (max length <= 32); 0 otherwise.  16 x 256 threads.
-constexpr int kXBits = 12;
-__device__ __forceinline__ void lut8_body(const uint32_t *__restrict__ len_counts, uint8_t *__restrict__ lut8,
-                                          uint32_t blk) {
-  __shared__ unsigned long long lim[65];  // (first + count) << (32 - l): exclusive left-aligned limit
-  __shared__ uint32_t s_max;
+// decode table rows [blk*blockDim, (blk+1)*blockDim) (layout in kernels.cuh)
+__device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_counts, uint32_t *__restrict__ table, uint32_t blk) {
+  __shared__ unsigned long long s_first[33], s_lim[33];
+  __shared__ uint32_t s_base[33];
+  __shared__ unsigned s_ok, s_max;
   if (threadIdx.x == 0) {
-    unsigned long long code = 0;
-    uint32_t mx = 0;
+    unsigned long long code = 0, kraft = 0;
+    uint32_t idx = 0, mx = 0;
+    bool over = false;
     for (int l = 0; l < 64; l++) {
       code <<= 1;
       const uint32_t c = len_counts[l];
-      lim[l] = l <= 32 ? (code + c) << (32 - l) : 0ull;
+      if (l <= 32) {
+        s_first[l] = code;
+        s_lim[l] = (code + c) << (32 - l);
+        s_base[l] = idx;
+      }
+      if (l >= 1) {
+        // Kraft sum in units of 2^-63: an over-subscribed table has no
+        // canonical order (the reference's first-match rule decides)
+        const unsigned long long add = (unsigned long long)c << (63 - l);
+        if ((unsigned long long)c >> l) over = true;
+        if (kraft + add < kraft) over = true;
+        kraft += add;
+        if (kraft > (1ull << 63)) over = true;
+      }
       code += c;
+      idx += c;
       if (c && l > 0) mx = l;
     }
+    s_ok = over ? 0u : 1u;
     s_max = mx;
   }
   __syncthreads();
   const uint32_t p = blk * blockDim.x + threadIdx.x;
-  if (p >= (1u << kXBits)) return;
-  uint8_t e = 0;
-  if (s_max >= 1 && s_max <= 32) {
-    const unsigned long long w0 = (unsigned long long)p << (32 - kXBits);
-    const unsigned long long w1 = w0 | ((1ull << (32 - kXBits)) - 1);
-    // shortest length whose codes cover w0, and the one covering w1
+  if (p >= (uint32_t)kLutSize) return;
+  uint32_t e = 0;
+  if (s_ok) {
+    const unsigned long long w0 = (unsigned long long)p << (32 - kLutBits);
+    const unsigned long long w1 = w0 | ((1ull << (32 - kLutBits)) - 1);
+    const int top = s_max < 32u ? (int)s_max : 32;
     int l0 = 0, l1 = 0;
-    for (int l = 1; l <= (int)s_max; l++)
-      if (!l0 && lim[l] > w0) l0 = l;
-    for (int l = 1; l <= (int)s_max; l++)
-      if (!l1 && lim[l] > w1) l1 = l;
-    if (l0 && l1 && l1 - l0 <= 3) e = (uint8_t)l0;
+    for (int l = 1; l <= top; l++) {
+      if (!l0 && s_lim[l] > w0) l0 = l;
+      if (!l1 && s_lim[l] > w1) l1 = l;
+    }
+    if (l0 && l0 == l1) {
+      const unsigned long long code0 = w0 >> (32 - l0);
+      e = ((s_base[l0] + (uint32_t)(code0 - s_first[l0])) << 6) | (uint32_t)l0;
+    } else if (l0) {
+      e = (uint32_t)l0 << 6;  // mixed lengths: the decoder's scan starts at l0
+    } else if (s_max > 32) {
+      e = 33u << 6;  // past every code of <= 32 bits: longer codes only
+    }
   }
-  lut8[p] = e;
+  table[p] = e;
+  if (p == 0) {
+    table[kLutSize] = s_ok;
+    table[kLutSize + 1] = s_max;
+  }
 }
 
 
-// decode table rows [256*b, 256*b + 256) of a stream with plan p (the pack
-// kernel's first CTAs run it; same choice as launch_decode)
+// decode table rows [256*b, 256*b + 256) of a stream compressed by the
+// async chain (the pack kernel's first CTAs run it): the K4L table
 __device__ __forceinline__ void table_rows_plan(const uint32_t *canon, const uint32_t *len_counts,
                                                 const actc_plan_t *p, void *table, int sw16, uint32_t blk) {
-  if (sw16 && p->live_symbols <= K4W_MAX_LIVE)
-    lut32_body(canon, len_counts, (uint32_t *)table, 2, blk);
-  else
-    lut8_body(len_counts, (uint8_t *)table, blk);
+  (void)canon;
+  (void)p;
+  (void)sw16;
+  k4l_table_rows(len_counts, (uint32_t *)table, blk);
 }
 
 // decode table at compress time (k4_decode.cu): the table launch_decode

@@ -1,6 +1,6 @@
 """Decoder alone, one tensor at a time (CUDA events around actc_decompress on
 the current stream, L2 flushed between reps): us per tensor and Gsym/s for
-the bench workload's tensors.  ACTC_LIB_PATH / ACTC_DEC select A/B builds."""
+the bench workload's tensors.  ACTC_LIB_PATH selects an A/B build."""
 import json
 import os
 import sys
@@ -16,7 +16,7 @@ ts, ebs, info, _, _ = bench.build_workload(sys.argv[1] if len(sys.argv) > 1 else
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 res = []
 for t, eb in zip(ts, ebs):
-    c, rep = pb.compress(t, pb.CodecParams(eb=eb))
+    (c, rep), = pb.compress_batch([t], [pb.CodecParams(eb=eb)])
     out = torch.empty_like(t)
     for _ in range(3):
         pb.decompress_batch([c], [out])
@@ -31,7 +31,8 @@ for t, eb in zip(ts, ebs):
         ms.append(e0.elapsed_time(e1))
     ms.sort()
     m = ms[len(ms) // 2]
+    alg = rep.compressed_bytes + 4 * t.numel() + 16 * ((t.numel() + 127) // 128)
     res.append({"n": t.numel(), "live": c._live, "ratio": round(rep.ratio, 3), "us": round(1e3 * m, 1),
-                "gsym_s": round(t.numel() / m / 1e6, 1)})
-print(json.dumps({"lib": os.environ.get("ACTC_LIB_PATH", "default"), "dec": os.environ.get("ACTC_DEC", "auto"),
+                "gsym_s": round(t.numel() / m / 1e6, 1), "alg_gbs": round(alg / m / 1e6, 1)})
+print(json.dumps({"lib": os.environ.get("ACTC_LIB_PATH", "default"), 
                   "tensors": res, "total_us": round(sum(r["us"] for r in res), 1)}))
