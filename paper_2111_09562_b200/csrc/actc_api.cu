@@ -856,7 +856,8 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   if (!prebuilt && (phase != 2 || S.table_dev)) {
     KT(ACTC_KIND_LUT);
     if (lane_dec)
-      k4l_build_table<<<kLutSize / 256, 256, 0, s>>>(S.len_counts_dev, (uint32_t *)c->lut.p);
+      k4l_build_table<<<kLutSize / 256, 256, 0, s>>>(S.len_counts_dev, S.canon_syms_dev, mode == 2 ? 0u : S.radius,
+                                                     (uint32_t *)c->lut.p);
     else
       k_build_lut<<<kLutSize / 256, 256, 0, s>>>(S.canon_syms_dev, S.len_counts_dev, (uint32_t *)c->lut.p, 0);
   }
@@ -866,7 +867,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.n = S.n;
   a.eb = S.eb;
   a.two_eb = 2.0 * S.eb;
-  a.radius = S.radius;
+  a.radius = mode == 2 ? 0u : S.radius;  // raw symbols: delta = symbol
   a.preserve = (S.flags & ACTC_FLAG_PRESERVE_ZEROS) ? 1 : 0;
   a.k = S.n_outliers;
   a.out_idx = (const unsigned long long *)S.outlier_idx_dev;
@@ -899,11 +900,14 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     const void *f = mode == 2 ? (const void *)k4l_decode<2, true>
                   : mode == 1 ? (gcanon ? (const void *)k4l_decode<1, true> : (const void *)k4l_decode<1, false>)
                               : (gcanon ? (const void *)k4l_decode<0, true> : (const void *)k4l_decode<0, false>);
-    const size_t smem = k4l_smem_bytes(S.live_symbols, gcanon);
+    // one CTA per SM; a stream with fewer 32-chunk tiles than SMs x warps
+    // gets narrower CTAs (every SM busy, and room for a second decoder)
     const uint64_t ntl = cdiv(nchunks, 32);
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, K4L_THREADS / 32), (uint64_t)c->num_sms));
+    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>(K4L_THREADS / 32, cdiv(ntl, c->num_sms)));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, warps), (uint64_t)c->num_sms));
+    const size_t smem = k4l_smem_bytes(S.live_symbols, gcanon, warps);
     void *args[] = {&a};
-    CK(cudaLaunchKernel(f, dim3(grid), dim3(K4L_THREADS), args, smem, s));
+    CK(cudaLaunchKernel(f, dim3(grid), dim3(32 * warps), args, smem, s));
   } else {
     const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
     const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)(sw16 ? c->k4_blocks[0] : c->k4_blocks[1]));

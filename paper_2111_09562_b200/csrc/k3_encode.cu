@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
     // the stream's decode table (kLutSize entries, 16 rows of 256), built
     // here by the first CTAs instead of a launch of its own
     for (uint32_t b = blockIdx.x; b < (uint32_t)(kLutSize / K3L_THREADS); b += gridDim.x) {
-      table_rows_plan(a.canon_out, a.lencnt_out, a.dplan, a.table, a.sw16, b);
+      table_rows_plan(a.canon_out, a.lencnt_out, a.radius, a.table, b);
       __syncthreads();
     }
   }

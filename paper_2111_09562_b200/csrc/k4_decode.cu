@@ -61,16 +61,6 @@ __global__ void k_build_lut(const uint32_t *__restrict__ canon, const uint32_t *
   lut32_body(canon, len_counts, lut, mode, blockIdx.x);
 }
 
-// The decode table of a stream compressed by actc_compress_async, built at
-// the end of its chain from the device plan: the k4w prefix LUT (symbols,
-// exact-long entries) when launch_decode will pick k4w for it (16-bit
-// symbols and <= K4W_MAX_LIVE live symbols), else the k4x u8 length table.
-__global__ void k_build_table_plan(const uint32_t *canon, const uint32_t *len_counts, const actc_plan_t *plan,
-                                   void *table, int sw16) {
-  if (plan->status != ACTC_OK || plan->live_symbols == 0) return;
-  table_rows_plan(canon, len_counts, plan, table, sw16, blockIdx.x);
-}
-
 template <int MODE, int SW>
 __global__ void __launch_bounds__(K4_THREADS) k4_decode(DecodeArgs a) {
   constexpr int kWPC = words_per_chunk<SW>();

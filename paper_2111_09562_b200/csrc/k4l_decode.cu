@@ -31,7 +31,8 @@ namespace actc {
 
 namespace {
 
-constexpr int kRowBytes = 80;  // 64 B of values + 16 B pad (odd number of 16-B units)
+constexpr int kUnitsPerRow = 2;  // 16-B units of values per row and round
+constexpr int kRowBytes = 48;    // 32 B of values + 16 B pad (odd number of 16-B units)
 
 __device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t n) {  // x >> n, 0 for n >= 32
   uint32_t r;
@@ -39,8 +40,9 @@ __device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t n) {  // x >>
   return r;
 }
 
-__device__ __forceinline__ uint64_t k4l_bits64(const uint32_t *__restrict__ pw, uint64_t pos) {
+__device__ __forceinline__ uint64_t k4l_bits64(const uint32_t *__restrict__ pw, uint64_t pos, uint64_t nwords) {
   const uint64_t wi = pos >> 5;
+  if (wi + 3 > nwords) return 0;  // past the buffer (a corrupt stream): no code matches
   const unsigned sh = pos & 31;
   const uint64_t hi = ((uint64_t)bswap32(__ldg(pw + wi)) << 32) | bswap32(__ldg(pw + wi + 1));
   if (!sh) return hi;
@@ -65,11 +67,12 @@ struct OutT<2> {
 
 }  // namespace
 
-__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, uint32_t *__restrict__ table) {
-  k4l_table_rows(len_counts, table, blockIdx.x);
+__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon, uint32_t radius,
+                                uint32_t *__restrict__ table) {
+  k4l_table_rows(len_counts, canon, radius, table, blockIdx.x);
 }
 
-size_t k4l_smem_bytes(uint32_t live, bool gcanon);
+size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps);
 
 // shared-window address kept in a register (otherwise the compiler rebuilds
 // it from SR_CgaCtaId at every access inside the decode loop)
@@ -84,8 +87,8 @@ __device__ __forceinline__ uint32_t k4l_lds(uint32_t addr) {
   return v;
 }
 __device__ __forceinline__ int k4l_lds_s16(uint32_t addr) {
-  short v;
-  asm("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+  int v;
+  asm("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 
@@ -101,7 +104,7 @@ struct K4LShared {
 // L1 bypassed) once per round for the groups it has moved past.  The decode
 // chain reads the next word from the ring (shared-memory latency) instead of
 // waiting for a global load on every refill.
-constexpr int kRingGroups = 8;
+constexpr int kRingGroups = 4;
 constexpr int kRingBytesPerWarp = kRingGroups * 32 * 16;
 
 __device__ __forceinline__ void k4l_cp16(uint32_t dst, const void *src) {
@@ -137,6 +140,13 @@ struct K4LRing {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr(w)));  // ordered after the cp.async waits
     return bswap32(v);
   }
+  __device__ __forceinline__ uint32_t word_if(uint32_t w, bool on) const {  // predicated read
+    uint32_t v = 0;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
+                 : "+r"(v)
+                 : "r"(addr(w)), "r"((uint32_t)on));
+    return bswap32(v);
+  }
   // stage groups [issued, upto) (bounded by the buffer)
   __device__ __forceinline__ void stage(uint32_t &issued, uint32_t upto) const {
     upto = min(upto, capg);
@@ -144,6 +154,19 @@ struct K4LRing {
     k4l_commit();
   }
 };
+
+// the window moves by one word once 32 bits are consumed (branch-free: the
+// selects keep the warp converged; the ring read is predicated)
+template <bool NARROW>
+__device__ __forceinline__ void k4l_advance(const K4LRing &rg, K4LLane<NARROW> &L) {
+  const bool adv = L.boff >= 32u;
+  const uint32_t w3 = rg.word_if(L.a + 3, adv);
+  L.a += adv ? 1u : 0u;
+  L.cur = adv ? L.nxt : L.cur;
+  L.nxt = adv ? L.nn : L.nxt;
+  L.nn = adv ? w3 : L.nn;
+  L.boff -= adv ? 32u : 0u;
+}
 
 // (re)seed a lane's ring at word a and load its window (waits for the data)
 template <bool NARROW>
@@ -158,88 +181,76 @@ __device__ __forceinline__ void k4l_seed(const K4LRing &rg, K4LLane<NARROW> &L, 
   L.nn = rg.word(a + 2);
 }
 
-// The rare path of one symbol (lane-divergent): the reference's bit rule
-// for a prefix the table does not resolve (scan from the prefix's shortest
-// length l0), and the outlier-marker splice.  Fixes len/delta/P/val/nzi of
-// the common path; the caller advances the window.
-template <int MODE, bool NARROW, typename T>
-__device__ __forceinline__ void k4l_slow(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg,
-                                         K4LLane<NARROW> &L, uint32_t e, uint32_t W, uint32_t &len, int &delta,
-                                         T &val, uint32_t &nzi, uint64_t e_idx, uint64_t e0, bool &bad,
-                                         unsigned long long &markers) {
-  const int radius = (int)a.radius;
-  const long long Pprev = (long long)L.P - delta;
-  if (len == 0u) {
-    // huffman.py:129-141: the first length whose code offset is in range
-    const int maxlen = (int)sh.maxlen;
-    int l = max(1, (int)(e >> 6));
-    uint32_t ci = 0;
-    len = 0;
-    for (; l <= min(maxlen, 32); l++) {
-      const uint32_t of = shr_clamp(W, 32u - (uint32_t)l) - (uint32_t)sh.first[l];
-      if ((unsigned long long)(shr_clamp(W, 32u - (uint32_t)l)) >= sh.first[l] && of < sh.count[l]) {
-        ci = sh.base[l] + of;
+// Phase A's rare path (lane-divergent): the reference's bit rule for a
+// prefix the table does not resolve (scan from the prefix's shortest length
+// l0; huffman.py:129-141).  Returns the canonical index, sets len (the
+// caller advances the window).
+template <bool NARROW>
+__device__ __forceinline__ uint32_t k4l_resolve(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg,
+                                             K4LLane<NARROW> &L, uint32_t e, uint32_t W, uint32_t &len, bool &bad) {
+  const int maxlen = (int)sh.maxlen;
+  int l = max(1, (int)(e >> 7));
+  uint32_t ci = 0;
+  len = 0;
+  for (; l <= min(maxlen, 32); l++) {
+    const uint32_t code = shr_clamp(W, 32u - (uint32_t)l);
+    if ((unsigned long long)code >= sh.first[l] && code - (uint32_t)sh.first[l] < sh.count[l]) {
+      ci = sh.base[l] + (code - (uint32_t)sh.first[l]);
+      len = (uint32_t)l;
+      break;
+    }
+  }
+  if (!len && maxlen > 32) {
+    // codes longer than 32 bits: a 64-bit window from the payload
+    const uint64_t win = k4l_bits64(a.payload, ((uint64_t)L.a << 5) + L.boff, 4ull * rg.capg);
+    for (l = max(l, 33); l <= maxlen; l++) {
+      const unsigned long long cd = win >> (64 - l), of = cd - sh.first[l];
+      if (of < sh.count[l]) {
+        ci = sh.base[l] + (uint32_t)of;
         len = (uint32_t)l;
         break;
       }
     }
-    if (!len && maxlen > 32) {
-      // codes longer than 32 bits: a 64-bit window from the payload
-      const uint64_t win = k4l_bits64(a.payload, ((uint64_t)L.a << 5) + L.boff);
-      for (l = max(l, 33); l <= maxlen; l++) {
-        const unsigned long long cd = win >> (64 - l), of = cd - sh.first[l];
-        if (of < sh.count[l]) {
-          ci = sh.base[l] + (uint32_t)of;
-          len = (uint32_t)l;
-          break;
-        }
-      }
-    }
-    if (!len) {
-      bad = true;  // invalid code (-2), or a stream cut short
-      len = 1;
-    }
-    delta = (int)(__ldg(a.canon + min(ci, a.live - 1)) - (uint32_t)radius);
-    L.boff += len;
-    if (L.boff >= 64u) {
-      // a code of more than 32 bits ran past the window: re-seed the ring
-      const uint64_t np = ((uint64_t)L.a << 5) + L.boff;
-      L.boff = (uint32_t)(np & 31);
-      k4l_seed(rg, L, (uint32_t)(np >> 5));
-    }
   }
-  if (!NARROW && MODE != 2 && delta == -radius) {
-    // outlier marker: the chain rebases on prequantize(value) and the value
-    // is spliced, then re-zeroed (codec.py:286-292, 361-368)
-    if (!L.ord_known) {
-      uint64_t lo = 0, hi = a.k;
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (a.out_idx[mid] < e0) lo = mid + 1; else hi = mid;
-      }
-      L.ordn = (uint32_t)lo;
-      L.ord_known = true;
-    }
-    float ov = 0.0f;
-    if (L.ordn >= a.k || a.out_idx[L.ordn] != e_idx) bad = true;
-    else ov = a.out_val[L.ordn];
-    L.ordn++;
-    markers++;
-    bool dummy;
-    L.P = (typename K4LLane<NARROW>::Lat)quant_exact((double)ov, a.two_eb, a.eb, dummy);
-    double rv = (double)ov;
-    if (a.preserve && fabs(rv) <= a.eb) rv = 0.0;
-    val = (T)rv;
-    nzi = rv != 0.0;
-  } else {
-    L.P = (typename K4LLane<NARROW>::Lat)(Pprev + delta);
-    if (MODE == 2) {
-      val = (T)(uint32_t)(delta + radius);
-    } else {
-      val = (T)__dmul_rn((double)L.P, a.two_eb);
-      nzi = L.P != 0;
-    }
+  if (!len) {
+    bad = true;  // invalid code (-2), or a stream cut short
+    len = 1;
   }
+  L.boff += len;
+  if (L.boff >= 64u) {
+    // a code of more than 32 bits ran past the window: re-seed the ring
+    const uint64_t np = ((uint64_t)L.a << 5) + L.boff;
+    L.boff = (uint32_t)(np & 31);
+    k4l_seed(rg, L, (uint32_t)(np >> 5));
+  }
+  return min(ci, a.live - 1);
+}
+
+// Phase B's rare path: an outlier marker.  The chain rebases on
+// prequantize(value) and the value is spliced, then re-zeroed
+// (codec.py:286-292, 356-368); the marker must sit at the next stored index.
+template <bool NARROW>
+__device__ __forceinline__ double k4l_marker(const DecodeArgs &a, K4LLane<NARROW> &L, uint64_t e_idx, uint64_t e0,
+                                          bool &bad, unsigned long long &markers) {
+  if (!L.ord_known) {
+    uint64_t lo = 0, hi = a.k;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (a.out_idx[mid] < e0) lo = mid + 1; else hi = mid;
+    }
+    L.ordn = (uint32_t)lo;
+    L.ord_known = true;
+  }
+  float ov = 0.0f;
+  if (L.ordn >= a.k || a.out_idx[L.ordn] != e_idx) bad = true;
+  else ov = a.out_val[L.ordn];
+  L.ordn++;
+  markers++;
+  bool dummy;
+  L.P = (typename K4LLane<NARROW>::Lat)quant_exact((double)ov, a.two_eb, a.eb, dummy);
+  double rv = (double)ov;
+  if (a.preserve && fabs(rv) <= a.eb) rv = 0.0;
+  return rv;
 }
 
 // decode one lane's chunk (ACTC_CHUNK symbols, or cnt when !FULL) of a
@@ -251,7 +262,7 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
                                          unsigned long long &nonzero, unsigned long long &markers, bool &bad) {
   typedef typename OutT<MODE>::T T;
   constexpr int VPU = 16 / (int)sizeof(T);  // values per 16-B unit
-  constexpr int R = 4 * VPU;                // symbols per lane per round (one 64-B row)
+  constexpr int R = kUnitsPerRow * VPU;     // symbols per lane per round (one 32-B row)
   const int lane = threadIdx.x & 31;
   const int radius = (int)a.radius;
   const double two_eb = a.two_eb;
@@ -259,55 +270,91 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
   uint32_t nzc = 0;
   uint32_t safe_g = L.issued;  // groups known to have landed
   for (int r = 0; r < ACTC_CHUNK / R; r++) {
-    // the fast path reads at most R + 2 words ahead this round
-    if (((L.a + R + 2) >> 2) >= safe_g) k4l_wait<0>();
+    // the fast path reads at most R + 3 words ahead this round (a code of at
+    // most 32 bits per symbol; the ring holds 4 groups from the current one)
+    if (((L.a + R + 3) >> 2) >= safe_g) k4l_wait<0>();
     else k4l_wait<1>();
-    for (int u = 0; u < 4; u++) {
-      T v[VPU];
+    // phase A: the window chain -- R codes resolved to x = (delta << 1) | 1
+    // (direct entries) or ci << 1; nothing here waits on a delta lookup.  A
+    // prefix the table does not resolve takes the per-symbol rule (branch).
+    int x[R];
 #pragma unroll
-      for (int q = 0; q < VPU; q++) {
-        const uint32_t i = (uint32_t)(r * R + u * VPU + q);
-        const bool act = FULL || i < cnt;
-        const uint32_t W = __funnelshift_l(L.nxt, L.cur, L.boff);
-        const uint32_t e = k4l_lds(t1_s + ((W >> 20) << 2));
-        uint32_t len = e & 63u;
-        const uint32_t ci = (e >> 6) + shr_clamp(W & 0xFFFFFu, 32u - len);
-        int delta = GCANON ? (int)(__ldg(a.canon + min(ci, a.live - 1)) - (uint32_t)radius)
-                           : k4l_lds_s16(cd_s + 2u * ci);
-        if (!FULL && !act) {
-          len = 0;
-          delta = 0;
-        }
-        L.P += delta;
-        T val;
-        uint32_t nzi = 0;
-        if (MODE == 2) {
-          val = (T)(uint32_t)(delta + radius);
-        } else {
-          val = (T)__dmul_rn((double)L.P, two_eb);
-          nzi = L.P != 0;
-        }
-        L.boff += len;
-        // outlier markers exist only in streams with outliers (not NARROW)
-        const bool spec = (FULL || act) && (len == 0u || (!NARROW && MODE != 2 && delta == -radius));
-        if (spec)
-          k4l_slow<MODE, NARROW, T>(a, sh, rg, L, e, W, len, delta, val, nzi, e0 + i, e0, bad, markers);
-        {
-          // branch-free window advance by one word (the ring read is issued
-          // every symbol; the selects keep the warp converged)
-          const bool adv = L.boff >= 32u;
-          const uint32_t w3 = rg.word(L.a + 3);
-          L.a += adv ? 1u : 0u;
-          L.cur = adv ? L.nxt : L.cur;
-          L.nxt = adv ? L.nn : L.nxt;
-          L.nn = adv ? w3 : L.nn;
-          L.boff -= adv ? 32u : 0u;
-        }
-        if (FULL || act) nzc += nzi;
-        v[q] = val;
+    for (int j = 0; j < R; j++) {
+      const uint32_t i = (uint32_t)(r * R + j);
+      const uint32_t W = __funnelshift_l(L.nxt, L.cur, L.boff);
+      const uint32_t e = k4l_lds(t1_s + ((W >> 20) << 2));
+      uint32_t len = e & 63u;
+      x[j] = (e & 64u) ? ((int)e >> 6) : (int)(((e >> 7) + shr_clamp(W & 0xFFFFFu, 32u - len)) << 1);
+      if (!FULL && i >= cnt) {
+        len = 64u;  // past the chunk: no code, no advance
+        x[j] = 1;   // delta 0 (direct), never a marker
       }
+      L.boff += len & 63u;
+      if (len == 0u) x[j] = (int)(k4l_resolve<NARROW>(a, sh, rg, L, e, W, len, bad) << 1);
+      k4l_advance(rg, L);
+    }
+    // phase B: deltas (independent lookups), the lattice running sum, the
+    // reconstruction.  Outlier markers only occur in streams with outliers
+    // (not NARROW); a round holding one is redone with the splice rule.
+    int gd[GCANON ? R : 1];
+    if (GCANON) {
+#pragma unroll
+      for (int j = 0; j < R; j++)  // the round's canonical lookups in flight together
+        gd[j] = (x[j] & 1) ? 0 : (int)__ldg(a.canon + ((uint32_t)x[j] >> 1));
+    }
+    int dl[R];
+#pragma unroll
+    for (int j = 0; j < R; j++) {
+      const bool dir = (x[j] & 1) != 0;
+      if (GCANON) {
+        dl[j] = dir ? (x[j] >> 1) : gd[j] - radius;
+      } else {
+        const int d = k4l_lds_s16(cd_s + (dir ? 0u : (uint32_t)x[j]));  // 2 * ci
+        dl[j] = dir ? (x[j] >> 1) : d;
+      }
+    }
+    T vals[R];
+    const typename K4LLane<NARROW>::Lat P0 = L.P;
+    const uint32_t nz0 = nzc;
+#pragma unroll
+    for (int j = 0; j < R; j++) {
+      L.P += dl[j];
+      if (MODE == 2) {
+        vals[j] = (T)(uint32_t)(dl[j] + radius);
+      } else {
+        vals[j] = (T)__dmul_rn((double)L.P, two_eb);
+        if (FULL || (uint32_t)(r * R + j) < cnt) nzc += L.P != 0;
+      }
+    }
+    if (!NARROW && MODE != 2) {
+      bool mk = false;
+#pragma unroll
+      for (int j = 0; j < R; j++) mk |= dl[j] == -radius;
+      if (__any_sync(0xffffffffu, mk)) {
+        L.P = P0;
+        nzc = nz0;
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+          const uint32_t i = (uint32_t)(r * R + j);
+          const bool in = FULL || i < cnt;
+          uint32_t nzi;
+          if (in && dl[j] == -radius) {
+            const double rv = k4l_marker<NARROW>(a, L, e0 + i, e0, bad, markers);
+            vals[j] = (T)rv;
+            nzi = rv != 0.0;
+          } else {
+            L.P += dl[j];
+            vals[j] = (T)__dmul_rn((double)L.P, two_eb);
+            nzi = L.P != 0;
+          }
+          if (in) nzc += nzi;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnitsPerRow; u++) {
       uint4 pk;
-      memcpy(&pk, v, 16);
+      memcpy(&pk, vals + u * VPU, 16);
       asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(myrow + 16u * u), "r"(pk.x), "r"(pk.y),
                    "r"(pk.z), "r"(pk.w)
                    : "memory");
@@ -316,12 +363,13 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
     safe_g = L.issued;
     rg.stage(L.issued, (L.a >> 2) + kRingGroups);
     __syncwarp();
-    // write-out: instruction t stores rows 8t .. 8t+7 (row = chunk of the
-    // tile), each lane one 16-B unit; unit u of row rho sits at 16*(5*rho+u)
-    const int rho_l = lane & 7, uu = lane >> 3;
+    // write-out: instruction t stores rows 16t .. 16t+15 (row = chunk of the
+    // tile), each lane one 16-B unit; unit u of row rho sits at 16*(3*rho+u):
+    // the 8 lanes of a quarter-warp hit 8 distinct 16-B bank groups
+    const int rho_l = lane & 15, uu = lane >> 4;
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
-      const int rho = 8 * t + rho_l;
+    for (int t = 0; t < 2; t++) {
+      const int rho = 16 * t + rho_l;
       uint4 val4;
       asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(val4.x), "=r"(val4.y), "=r"(val4.z), "=r"(val4.w)
@@ -351,7 +399,7 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
 
 template <int MODE, bool GCANON>
 __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
-  constexpr int NW = K4L_THREADS / 32;
+  const int NW = blockDim.x >> 5;  // warps per CTA: fewer for small streams (every SM busy)
   extern __shared__ __align__(16) unsigned char k4l_sm[];
   uint32_t *t1 = reinterpret_cast<uint32_t *>(k4l_sm);
   unsigned char *rows = k4l_sm + kLutSize * 4;
@@ -360,13 +408,13 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
   __shared__ K4LShared sh;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kLutSize / 4; i += K4L_THREADS)
+  for (int i = tid; i < kLutSize / 4; i += blockDim.x)
     reinterpret_cast<uint4 *>(t1)[i] = __ldg(reinterpret_cast<const uint4 *>(a.lut) + i);
   const int radius = (int)a.radius;
   if (!GCANON) {
     // canonical deltas (symbol - radius; the outlier marker is -radius)
     const uint32_t live = a.live;
-    for (uint32_t i = 4 * tid; i < live; i += 4 * K4L_THREADS) {
+    for (uint32_t i = 4 * tid; i < live; i += 4 * blockDim.x) {
       if (i + 4 <= live) {
         const uint4 c = __ldg(reinterpret_cast<const uint4 *>(a.canon + i));
         const uint32_t lo = ((uint32_t)(c.x - radius) & 0xFFFFu) | ((uint32_t)(c.y - radius) << 16);
@@ -473,8 +521,8 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
   }
 }
 
-size_t k4l_smem_bytes(uint32_t live, bool gcanon) {
-  return (size_t)kLutSize * 4 + (size_t)K4L_THREADS / 32 * (32 * kRowBytes + kRingBytesPerWarp) +
+size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps) {
+  return (size_t)kLutSize * 4 + (size_t)warps * (32 * kRowBytes + kRingBytesPerWarp) +
          (gcanon ? 0 : (((size_t)live * 2 + 15) & ~(size_t)15));
 }
 

@@ -27,10 +27,10 @@ constexpr int K3L_WORDS = (K3L_SEG * K3_SHORT_MAXLEN + 31) / 32 + 2;      // pac
 // K4 (scan variant, streams without a lattice index): one thread per chunk
 constexpr int K4_THREADS = 128;
 // K4 (warp variant, indexed streams): one warp per 32 chunks
-// K4L (indexed streams): one 768-thread CTA per SM, lane per chunk; the
+// K4L (indexed streams): one CTA of up to 768 threads per SM, lane per chunk; the
 // canonical deltas stay in shared memory up to K4L_SMEM_LIVE live symbols
-constexpr int K4L_THREADS = 768;
-constexpr uint32_t K4L_SMEM_LIVE = 24576;
+constexpr int K4L_THREADS = 768;  // at most; small streams launch fewer warps per CTA
+constexpr uint32_t K4L_SMEM_LIVE = 49152;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
 // lookback status for the encoder (per K3 tile)
@@ -278,19 +278,24 @@ __device__ __forceinline__ void report_format_error(const DecodeArgs &a) {
 template <int MODE, int SW>
 __global__ void k4_decode(DecodeArgs a);
 // K4L decode table (kLutWords words): T1[p] for every 12-bit prefix p of
-// the left-aligned 32-bit window = (ci_base << 6) | len when every code
-// under p has length len (<= 32), the canonical index of the code under the
-// window W being ci_base + ((W & 0xFFFFF) >> (32 - len)); otherwise
-// (l0 << 6) with length field 0 (the decoder's slow path), l0 the shortest
-// length a code under p can have (0: no code, or an over-subscribed table,
-// whose first-match rule the scan from length 1 reproduces).  Word kLutSize: 1 if the code table is prefix-free
+// the left-aligned 32-bit window; bits 0-5 the code length (0: slow path),
+// bit 6 "direct", bits 7-31 the payload:
+//  * one code under p (length <= 12, radius <= 2^24): direct, payload = its
+//    Lorenzo delta (symbol - radius, signed);
+//  * every code under p of one length len <= 32: payload = ci_base, the
+//    canonical index of the code under the window W being
+//    ci_base + ((W & 0xFFFFF) >> (32 - len));
+//  * otherwise length 0 and payload l0, the shortest length a code under p
+//    can have (0: no code, or an over-subscribed table, whose first-match
+//    rule the scan from length 1 reproduces).  Word kLutSize: 1 if the code table is prefix-free
 // (Kraft <= 1), word kLutSize + 1: the longest code length.
-__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, uint32_t *__restrict__ table);
+__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon, uint32_t radius,
+                                uint32_t *__restrict__ table);
 // MODE: 0 = fp32 recon, 1 = fp64 recon, 2 = raw u32 symbols;
 // GCANON: canonical symbols read from global memory (wide alphabets)
 template <int MODE, bool GCANON>
 __global__ void k4l_decode(DecodeArgs a);
-size_t k4l_smem_bytes(uint32_t live, bool gcanon);
+size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps);
 __global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
                                 unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
 
@@ -417,7 +422,8 @@ __device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, c
 }
 
 // decode table rows [blk*blockDim, (blk+1)*blockDim) (layout in kernels.cuh)
-__device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_counts, uint32_t *__restrict__ table, uint32_t blk) {
+__device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon,
+                                               uint32_t radius, uint32_t *__restrict__ table, uint32_t blk) {
   __shared__ unsigned long long s_first[33], s_lim[33];
   __shared__ uint32_t s_base[33];
   __shared__ unsigned s_ok, s_max;
@@ -464,11 +470,17 @@ __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_
     }
     if (l0 && l0 == l1) {
       const unsigned long long code0 = w0 >> (32 - l0);
-      e = ((s_base[l0] + (uint32_t)(code0 - s_first[l0])) << 6) | (uint32_t)l0;
+      const uint32_t ci = s_base[l0] + (uint32_t)(code0 - s_first[l0]);
+      if (l0 <= kLutBits && radius <= (1u << 24)) {
+        // one code under the prefix: its Lorenzo delta (symbol - radius) itself
+        e = ((uint32_t)((int)canon[ci] - (int)radius) << 7) | 64u | (uint32_t)l0;
+      } else {
+        e = (ci << 7) | (uint32_t)l0;
+      }
     } else if (l0) {
-      e = (uint32_t)l0 << 6;  // mixed lengths: the decoder's scan starts at l0
+      e = (uint32_t)l0 << 7;  // mixed lengths: the decoder's scan starts at l0
     } else if (s_max > 32) {
-      e = 33u << 6;  // past every code of <= 32 bits: longer codes only
+      e = 33u << 7;  // past every code of <= 32 bits: longer codes only
     }
   }
   table[p] = e;
@@ -481,18 +493,10 @@ __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_
 
 // decode table rows [256*b, 256*b + 256) of a stream compressed by the
 // async chain (the pack kernel's first CTAs run it): the K4L table
-__device__ __forceinline__ void table_rows_plan(const uint32_t *canon, const uint32_t *len_counts,
-                                                const actc_plan_t *p, void *table, int sw16, uint32_t blk) {
-  (void)canon;
-  (void)p;
-  (void)sw16;
-  k4l_table_rows(len_counts, (uint32_t *)table, blk);
+__device__ __forceinline__ void table_rows_plan(const uint32_t *canon, const uint32_t *len_counts, uint32_t radius,
+                                                void *table, uint32_t blk) {
+  k4l_table_rows(len_counts, canon, radius, (uint32_t *)table, blk);
 }
-
-// decode table at compress time (k4_decode.cu): the table launch_decode
-// would build for this stream, chosen on the device from the plan
-__global__ void k_build_table_plan(const uint32_t *canon, const uint32_t *len_counts, const actc_plan_t *plan,
-                                   void *table, int sw16);
 
 // K7 uniform error injection (k7_inject.cu); state = {st_hi, st_lo, inc_hi, inc_lo}
 int inject_launch(const void *x, int dtype, uint64_t n, double eb, int preserve, const uint64_t state[4],
