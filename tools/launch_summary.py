@@ -24,4 +24,6 @@ for k in order[-last:]:
     d = seq[k]
     t = d.get('gpu__time_duration.sum', 0) / 1e3
     i = d.get('smsp__inst_executed.sum', 0)
-    print(f"{d['name']:28s} {d['grid']:>14s} {t:9.1f} us  inst {i:12.0f}")
+    mb = (d.get('dram__bytes_read.sum', 0) + d.get('dram__bytes_write.sum', 0)) / 1e6
+    gbs = mb / t * 1e-3 * 1e3 if t else 0.0
+    print(f"{d['name']:28s} {d['grid']:>14s} {t:9.1f} us  inst {i:12.0f}  dram {mb:8.1f} MB {gbs:7.0f} GB/s")
