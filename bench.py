@@ -793,6 +793,73 @@ def run_training(model_name, batch, world, iters=6, warm=4, spot_check=False):
     return out
 
 
+def run_planner_leg(world, budget_bytes, batch=256, iters=6):
+    """The memory-budget batch planner applied (reference training.py:401-416,
+    PAPER.md:727): AlexNet with compressed activations under a device memory
+    budget equal to the uncompressed b256 run's peak; after two planned
+    intervals the compressor's recommended batch (choose_batch_size over the
+    observed per-layer ratios) is adopted and trained at -- images/s at that
+    batch vs the uncompressed run at b256 (the largest power-of-two batch the
+    same budget admits uncompressed)."""
+    import torch
+    import torchvision
+
+    import paper_2111_09562_b200 as pb
+    from paper_2111_09562_b200 import _lib
+    from paper_2111_09562_b200.hooks import ActivationCompressor
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rank = torch.distributed.get_rank() if world > 1 else 0
+    _lib.release_contexts()
+    torch.manual_seed(0)
+    m = torchvision.models.alexnet(num_classes=1000).to(dev)
+    opt = torch.optim.SGD(m.parameters(), lr=0.01, momentum=0.9)
+    ddp = torch.nn.parallel.DistributedDataParallel(m, device_ids=[dev.index]) if world > 1 else m
+    comp = ActivationCompressor(ActivationCompressor.conv_layer_map(m), opt,
+                                pb.ControllerConfig(W_default=2, W_floor=1, memory_budget_bytes=int(budget_bytes)),
+                                input_sample_bytes=3 * 224 * 224 * 4)
+    g = torch.Generator(device=dev).manual_seed(rank)
+
+    def batch_of(b):
+        return (torch.randn(b, 3, 224, 224, device=dev, generator=g),
+                torch.randint(0, 1000, (b,), device=dev, generator=g))
+
+    def it(x, y):
+        opt.zero_grad(set_to_none=True)
+        with comp.iteration():
+            torch.nn.functional.cross_entropy(ddp(x), y).backward()
+        opt.step()
+        comp.after_step()
+
+    x, y = batch_of(batch)
+    while comp.batch_size is None and comp.it < 12:
+        it(x, y)
+    b2 = comp.batch_size or batch
+    x, y = batch_of(b2)
+    for _ in range(2):
+        it(x, y)
+    comp.next_collection = comp.it + 1000
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        it(x, y)
+    e1.record()
+    e1.synchronize()
+    ms = _max_over_ranks(e0.elapsed_time(e1), world, dev)
+    out = {"budget_gb": budget_bytes / 1e9, "planned_batch": b2, "start_batch": batch,
+           "images_per_s": world * b2 * iters / (ms * 1e-3), "ms_per_iter": ms / iters,
+           "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+           "reserve_breaches": comp.reserve_breaches,
+           "note": "planner model = stored activations (raw bytes / observed ratio) + input + weights and "
+                   "velocity (training.py:401-416); peak_mem_gb is the allocator's actual peak at that batch"}
+    comp.remove()
+    del m, opt, ddp, comp, x, y
+    torch.cuda.empty_cache()
+    return out
+
+
 def _spot_check(comp, it, max_slots=8):
     """One more iteration capturing stored activations: each sampled slot's
     container (compressed inside the hooks at the controller's eb) vs the
@@ -852,6 +919,11 @@ def main():
                 legs = {}
                 for name in [s for s in args.train.split(",") if s]:
                     legs[name] = run_training(name, TRAIN_LEGS[name], world, spot_check=not args.no_cpu)
+                if "alexnet" in legs:
+                    base = legs["alexnet"]["baseline"]
+                    pl = run_planner_leg(world, base["peak_mem_gb"] * 1e9)
+                    pl["speedup_vs_uncompressed_b256"] = pl["images_per_s"] / base["images_per_s"]
+                    legs["alexnet_planner"] = pl
                 if line is not None:
                     line["training"] = legs
                     if "alexnet" in legs:

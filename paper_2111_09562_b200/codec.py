@@ -708,10 +708,12 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         dev = _DevBufs()
         # fixed-size arrays, and the capped (data-dependent) ones apart so
         # `compact` can replace the latter by exact-size copies
-        fixed = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8), ("canon", lmax, 4),
+        fixed = dev.carve(x.device, [("chunk_lat", nchunks, 8), ("chunk_off", nchunks, 8),
                                      ("len_counts", 64, 4), ("table", _lib.ACTC_TABLE_BYTES, 1)])
         fp, of = fixed.data_ptr(), dev.offsets
-        capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4)])
+        # data-dependent sizes (capped; `compact` copies their live extent)
+        capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4),
+                                      ("canon", lmax, 4)])
         cp, oc = capped.data_ptr(), dev.offsets
         # recorded after this tensor's allocations: its side stream is ordered
         # after all caller-stream work that used the blocks the allocator reused
@@ -728,7 +730,7 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         if (n, int(p.radius)) not in _FALLBACK_SEEN:
             flags |= _lib.ACTC_ASYNC_NO_FALLBACK
         args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
-                cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, fp + of["canon"],
+                cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, cp + oc["canon"],
                 fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
         # every tensor's K1 goes out before any codebook/encoder launch
         _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
@@ -769,7 +771,7 @@ def compress_end(pend: PendingCompress, compact: bool = False):
             dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
             dev.shrink("canon", max(plan.live_symbols, 1))
             if compact:
-                dev.compact(("out_idx", "payload", "out_val"), s)
+                dev.compact(("out_idx", "payload", "out_val", "canon"), s)
             c, rep = _container(n, p, dims, plan, dev)
             c._desc()
         else:

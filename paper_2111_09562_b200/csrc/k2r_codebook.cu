@@ -369,6 +369,9 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
             atomicAdd(&LC[k], (uint32_t)__popc(peers));
           LW[k] = f;
         }
+        // the next iteration's leaders read what this one's wrote (warp-private
+        // counters): order the lanes' shared accesses explicitly
+        __syncwarp();
         if (s < v1) a.cls16[s] = f ? (uint16_t)k : (uint16_t)0xFFFF;
       }
     }

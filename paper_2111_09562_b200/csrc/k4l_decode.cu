@@ -413,26 +413,38 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
   const int radius = (int)a.radius;
   if (!GCANON) {
     // canonical deltas (symbol - radius; the outlier marker is -radius)
+    // (four 16-B loads in flight per thread)
     const uint32_t live = a.live;
-    for (uint32_t i = 4 * tid; i < live; i += 4 * blockDim.x) {
-      if (i + 4 <= live) {
-        const uint4 c = __ldg(reinterpret_cast<const uint4 *>(a.canon + i));
-        const uint32_t lo = ((uint32_t)(c.x - radius) & 0xFFFFu) | ((uint32_t)(c.y - radius) << 16);
-        const uint32_t hi = ((uint32_t)(c.z - radius) & 0xFFFFu) | ((uint32_t)(c.w - radius) << 16);
-        *reinterpret_cast<uint2 *>(cdelta + i) = make_uint2(lo, hi);
-      } else {
-        for (uint32_t k = i; k < live; k++) cdelta[k] = (int16_t)((int)a.canon[k] - radius);
+    const uint32_t step = 4 * blockDim.x;
+    for (uint32_t i0 = 4 * tid; i0 < live; i0 += 4 * step) {
+      uint4 c[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t i = i0 + u * step;
+        c[u] = i + 4 <= live ? __ldg(reinterpret_cast<const uint4 *>(a.canon + i)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t i = i0 + u * step;
+        if (i + 4 <= live) {
+          const uint32_t lo = ((uint32_t)(c[u].x - radius) & 0xFFFFu) | ((uint32_t)(c[u].y - radius) << 16);
+          const uint32_t hi = ((uint32_t)(c[u].z - radius) & 0xFFFFu) | ((uint32_t)(c[u].w - radius) << 16);
+          *reinterpret_cast<uint2 *>(cdelta + i) = make_uint2(lo, hi);
+        } else {
+          for (uint32_t k = i; k < live; k++) cdelta[k] = (int16_t)((int)a.canon[k] - radius);
+        }
       }
     }
   }
+  stage_len_counts(sh.count, a.len_counts);
+  __syncthreads();
   if (tid == 0) {
     unsigned long long code = 0;
     uint32_t idx = 0, mx = 0;
     for (int l = 0; l < 64; l++) {
       code <<= 1;
-      const uint32_t c = a.len_counts[l];
+      const uint32_t c = sh.count[l];
       sh.first[l] = code;
-      sh.count[l] = c;
       sh.base[l] = idx;
       code += c;
       idx += c;

@@ -117,20 +117,26 @@ __device__ __forceinline__ void k2s_emit_warp(const EmitArgs &e, uint32_t wblk, 
                                               unsigned long long *s_first, uint32_t *s_base) {
   const int lane = threadIdx.x & 31;
   const uint32_t t = wblk * 32 + lane;
+  // the per-length counts: two parallel loads per lane (not 64 dependent
+  // loads by one thread), staged through s_base, then the canonical firsts
+  const uint32_t c0 = __ldg(e.len_counts + lane), c1 = __ldg(e.len_counts + 32 + lane);
+  const unsigned b0 = __ballot_sync(0xffffffffu, c0 != 0 && lane > 0), b1 = __ballot_sync(0xffffffffu, c1 != 0);
+  const uint32_t minlen = b0 ? (uint32_t)(__ffs(b0) - 1) : b1 ? (uint32_t)(32 + __ffs(b1) - 1) : 64u;
+  s_base[lane] = c0;
+  s_base[32 + lane] = c1;
+  __syncwarp();
   if (lane == 0) {
     unsigned long long code = 0;
     uint32_t idx = 0;
     for (int l = 0; l < 64; l++) {
+      const uint32_t c = s_base[l];
       code <<= 1;
       s_first[l] = code;
       s_base[l] = idx;
-      code += e.len_counts[l];
-      idx += e.len_counts[l];
+      code += c;
+      idx += c;
     }
   }
-  uint32_t minlen = 64;
-  for (int l = 63; l >= 1; l--)
-    if (e.len_counts[l]) minlen = l;
   {
     const uint32_t *src = reinterpret_cast<const uint32_t *>(e.rank_tab + (size_t)t * K2R_TS);
     uint32_t *dst = reinterpret_cast<uint32_t *>(s_row + lane * K2R_TS);
@@ -344,7 +350,18 @@ struct CodeTables {
   uint32_t maxlen;
 };
 
+// the 64 per-length code counts into shared memory by the first two warps
+// (parallel loads: a serial per-length loop by one thread would wait on 64
+// dependent-latency global loads); callers __syncthreads() before use
+__device__ __forceinline__ void stage_len_counts(uint32_t *dst, const uint32_t *__restrict__ len_counts) {
+  if (threadIdx.x < 64) dst[threadIdx.x] = __ldg(len_counts + threadIdx.x);
+}
+
 __device__ __forceinline__ void build_tables(CodeTables &t, const uint32_t *len_counts) {
+  __shared__ uint32_t s_cnt[64];
+  stage_len_counts(s_cnt, len_counts);
+  __syncthreads();
+  len_counts = s_cnt;
   if (threadIdx.x == 0) {
     unsigned long long code = 0;
     uint32_t idx = 0, mx = 0;
@@ -425,8 +442,11 @@ __device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, c
 __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon,
                                                uint32_t radius, uint32_t *__restrict__ table, uint32_t blk) {
   __shared__ unsigned long long s_first[33], s_lim[33];
-  __shared__ uint32_t s_base[33];
+  __shared__ uint32_t s_base[33], s_cnt[64];
   __shared__ unsigned s_ok, s_max;
+  stage_len_counts(s_cnt, len_counts);
+  __syncthreads();
+  len_counts = s_cnt;
   if (threadIdx.x == 0) {
     unsigned long long code = 0, kraft = 0;
     uint32_t idx = 0, mx = 0;

@@ -9,6 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+# the reference's own tests run against the drop-in through their own runner
+# (tests/conformance/run_reference_tests.sh), not in the default suite
+collect_ignore_glob = ["conformance/*"]
 
 
 def pytest_configure(config):
