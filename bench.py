@@ -41,7 +41,7 @@ METRIC = "activation compress+decompress GB/s/GPU vs HBM peak; compression ratio
 
 KERNEL_NAMES = {"quant": "k1_quant_lorenzo_hist", "codebook": "k2r_codebook (+ k2s_emit)",
                 "count": "k3_seg_count (+ CTA-total scan in its last CTA)", "pack": "k3_seg_pack",
-                "lut": "k_build_lut(8)", "decode": "k4w_decode (<= 16K live symbols) / k4x_decode"}
+                "lut": "k_build_lut(8)", "decode": "k4l_decode (lane per 128-symbol chunk, one-lookup prefix table)"}
 
 
 def _deterministic():
