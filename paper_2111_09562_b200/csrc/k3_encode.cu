@@ -237,9 +237,10 @@ __device__ __forceinline__ uint32_t k3_lds(uint32_t a) {
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+// OR v into the warp buffer when p (a no-op OR of 0 otherwise: an
+// unconditional reduction keeps the packing loop free of divergent branches)
 __device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v, uint32_t p) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
-               ::"r"(addr), "r"(v), "r"(p) : "memory");
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(p ? v : 0u) : "memory");
 }
 
 __device__ __forceinline__ void k3_plan_out(const SegArgs &a) {
