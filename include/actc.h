@@ -185,9 +185,11 @@ int actc_compress_async(actc_ctx *ctx, const float *x_dev, uint64_t n, double eb
  * ACTC_DEC_LUT_ONLY (build only the decode table into ctx) or ACTC_DEC_REST
  * (launch only the decoder, after a LUT_ONLY call with the same ctx, stream
  * and actc_stream_t): a batch puts every table build on the GPU before any
- * decoder fills it. */
+ * decoder fills it.  The nonzero count of the result (R) is only formed when
+ * result_host is given and ACTC_DEC_NO_NONZERO is not set. */
 #define ACTC_DEC_LUT_ONLY 0x100
 #define ACTC_DEC_REST 0x200
+#define ACTC_DEC_NO_NONZERO 0x400
 int actc_decompress(actc_ctx *ctx, const actc_stream_t *stream, void *out_dev,
                     int out_dtype, actc_decode_result_t *result_host, actc_stream s);
 

@@ -24,6 +24,7 @@ ACTC_EAGAIN = 6
 ACTC_TABLE_BYTES = 16400  # include/actc.h
 ACTC_DEC_LUT_ONLY = 0x100
 ACTC_DEC_REST = 0x200
+ACTC_DEC_NO_NONZERO = 0x400
 ACTC_DTYPE_F32, ACTC_DTYPE_F64 = 0, 1
 ACTC_CHUNK = 128
 

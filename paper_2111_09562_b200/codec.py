@@ -803,12 +803,15 @@ def compress(t, params: CodecParams):
     return compress_device(to_device(t), params, dims=t.dims)
 
 
-def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None, check=True):
+def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None, check=True,
+                      count_nonzero=True):
     """Reconstruct on the device.  Returns (tensor, nonzero_count or None).
 
     dtype torch.float64 is bit-identical to the reference's output; float32
     stores fp32 of it.  With check=False no host synchronisation happens
-    (the status and nonzero count are left in the context's mailbox).
+    (the status and nonzero count are left in the context's mailbox).  With
+    count_nonzero=False the decoder skips the nonzero count (R,
+    training.py:351-352) and None is returned in its place.
     """
     torch = _lib.torch_cuda()
     dtype = torch.float32 if dtype is None else dtype
@@ -825,6 +828,8 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
     if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
         raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
     d = c._desc()
+    if not count_nonzero:
+        code |= _lib.ACTC_DEC_NO_NONZERO
     _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
                                                C.c_void_p(ctx.dres_buf.data_ptr()), sh))
     if not check:
@@ -837,7 +842,7 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
         if r.status:
             raise FormatError("invalid code in bitstream or outlier markers disagree with stored indices")
         raise FormatError("outlier markers disagree with stored indices")
-    return out, int(r.nonzero)
+    return out, (int(r.nonzero) if count_nonzero else None)
 
 
 def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=None):

@@ -183,6 +183,7 @@ struct actc_ctx {
   void *sym_cur = nullptr;
   // decode-table output for the next async compression (actc_ctx_set_table_out)
   void *table_out = nullptr;
+  int smem_optin = 0;  // dynamic shared memory a CTA may opt in to
 };
 
 namespace {
@@ -477,7 +478,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
   }
   cudaMemset(c->dres_dev, 0, sizeof(DecResult));
   int rc;
-  if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, 4 * kLutWords))) {
+  if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, std::max<size_t>(4 * kLutWords, kK4lTableBytes)))) {
     delete c;
     return rc;
   }
@@ -487,9 +488,12 @@ int actc_ctx_create(int device, actc_ctx **out) {
   int nb = 0;
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  const void *big[] = {(const void *)k4l_decode<0, false>,       (const void *)k4l_decode<1, false>,
-                       (const void *)k4l_decode<0, true>,        (const void *)k4l_decode<1, true>,
-                       (const void *)k4l_decode<2, true>,        (const void *)k3_seg_pack<uint16_t>,
+  c->smem_optin = optin;
+  const void *big[] = {(const void *)k4l_decode<0, false, false>, (const void *)k4l_decode<0, false, true>,
+                       (const void *)k4l_decode<1, false, false>, (const void *)k4l_decode<1, false, true>,
+                       (const void *)k4l_decode<0, true, false>,  (const void *)k4l_decode<0, true, true>,
+                       (const void *)k4l_decode<1, true, false>,  (const void *)k4l_decode<1, true, true>,
+                       (const void *)k4l_decode<2, true, false>,  (const void *)k3_seg_pack<uint16_t>,
                        (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
                        (const void *)k3_seg_count<uint32_t>,    (const void *)k1_quant_lorenzo_hist<uint16_t>,
                        (const void *)k1_quant_lorenzo_hist<uint32_t>, (const void *)k_hist_u32};
@@ -817,9 +821,48 @@ int actc_compress_async(actc_ctx *c, const float *x, uint64_t n, double eb, uint
   return ACTC_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// the decoder's output as a 2-D tensor of chunk rows (k4l_decode's TMA
+// stores): rows x ACTC_CHUNK values, box 32 rows x 64 B, 64-B swizzle
+static int make_chunk_rows_map(CUtensorMap *tm, void *out, uint64_t rows, int mode) {
+  memset(tm, 0, sizeof(*tm));
+  if (rows == 0) return ACTC_OK;  // no full tile: the map is never used
+  if ((uintptr_t)out & 15u) return set_err(ACTC_EPARAM, "decode output must be 16-byte aligned");
+  const EncodeTiledFn enc = encode_tiled();
+  if (!enc) return set_err(ACTC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint32_t elem = mode == 1 ? 8u : 4u;
+  const CUtensorMapDataType dt = mode == 1   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                 : mode == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                             : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+  const cuuint64_t dims[2] = {(cuuint64_t)ACTC_CHUNK, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ACTC_CHUNK * elem};
+  const cuuint32_t box[2] = {64u / elem, 32u};
+  const cuuint32_t es[2] = {1u, 1u};
+  const CUresult r = enc(tm, dt, 2, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(ACTC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ACTC_OK;
+}
+
 // phase: 0 = table + decoder, 1 = table only, 2 = decoder only (table built by a phase-1 call)
 static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int mode,
-                         actc_decode_result_t *res_host, cudaStream_t s, int phase = 0) {
+                         actc_decode_result_t *res_host, cudaStream_t s, int phase = 0,
+                         bool no_nonzero = false) {
   const actc_stream_t &S = *st_in;
   if (S.n == 0) return set_err(ACTC_EPARAM, "empty stream");
   if (!S.chunk_offsets_dev) return set_err(ACTC_EPARAM, "stream has no chunk index (call actc_build_chunk_index)");
@@ -890,23 +933,37 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.mcount = nullptr;
   KT(ACTC_KIND_DECODE);
   if (lane_dec) {
-    // K4L: one 1024-thread CTA per SM (persistent over 32-chunk warp tiles);
-    // canonical deltas in shared memory for 16-bit symbols
+    // K4L: one CTA per SM (persistent over 32-chunk warp tiles), as many
+    // warps as the shared memory holds; canonical deltas in shared memory
+    // for 16-bit symbols up to K4L_SMEM_LIVE live codes
     const bool gcanon = !sw16 || S.live_symbols > K4L_SMEM_LIVE;
     if (mode != 2 && S.n_outliers) {
       a.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_K4LTICKET);
       a.mcount = (unsigned long long *)c->misc.p + M_K4LMCOUNT;
     }
-    const void *f = mode == 2 ? (const void *)k4l_decode<2, true>
-                  : mode == 1 ? (gcanon ? (const void *)k4l_decode<1, true> : (const void *)k4l_decode<1, false>)
-                              : (gcanon ? (const void *)k4l_decode<0, true> : (const void *)k4l_decode<0, false>);
+    // the nonzero count (R) only when the caller reads the result back
+    const bool nz = res_host && !no_nonzero;
+    const void *f;
+    if (mode == 2) f = (const void *)k4l_decode<2, true, false>;
+    else if (mode == 1)
+      f = gcanon ? (nz ? (const void *)k4l_decode<1, true, true> : (const void *)k4l_decode<1, true, false>)
+                 : (nz ? (const void *)k4l_decode<1, false, true> : (const void *)k4l_decode<1, false, false>);
+    else
+      f = gcanon ? (nz ? (const void *)k4l_decode<0, true, true> : (const void *)k4l_decode<0, true, false>)
+                 : (nz ? (const void *)k4l_decode<0, false, true> : (const void *)k4l_decode<0, false, false>);
     // one CTA per SM; a stream with fewer 32-chunk tiles than SMs x warps
     // gets narrower CTAs (every SM busy, and room for a second decoder)
     const uint64_t ntl = cdiv(nchunks, 32);
-    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>(K4L_THREADS / 32, cdiv(ntl, c->num_sms)));
+    const int wmax = k4l_max_warps(S.live_symbols, gcanon, (size_t)c->smem_optin);
+    if (wmax < 1) return set_err(ACTC_EPARAM, "decode tables exceed shared memory");
+    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wmax, cdiv(ntl, c->num_sms)));
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, warps), (uint64_t)c->num_sms));
     const size_t smem = k4l_smem_bytes(S.live_symbols, gcanon, warps);
-    void *args[] = {&a};
+    // full tiles leave through TMA stores: the output as [n / ACTC_CHUNK][ACTC_CHUNK]
+    CUtensorMap tm;
+    int rc2;
+    if ((rc2 = make_chunk_rows_map(&tm, out, S.n / ACTC_CHUNK, mode))) return rc2;
+    void *args[] = {&a, &tm};
     CK(cudaLaunchKernel(f, dim3(grid), dim3(32 * warps), args, smem, s));
   } else {
     const size_t smem = (size_t)K4_THREADS * (sw16 ? ACTC_CHUNK / 2 + 1 : ACTC_CHUNK + 1) * 4;
@@ -924,12 +981,14 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
 int actc_decompress(actc_ctx *c, const actc_stream_t *stream, void *out, int out_dtype,
                     actc_decode_result_t *result_host, actc_stream s) {
   const int phase = (out_dtype & ACTC_DEC_LUT_ONLY) ? 1 : (out_dtype & ACTC_DEC_REST) ? 2 : 0;
-  out_dtype &= ~(ACTC_DEC_LUT_ONLY | ACTC_DEC_REST);
+  const bool no_nonzero = (out_dtype & ACTC_DEC_NO_NONZERO) != 0;
+  out_dtype &= ~(ACTC_DEC_LUT_ONLY | ACTC_DEC_REST | ACTC_DEC_NO_NONZERO);
   if (out_dtype != ACTC_DTYPE_F32 && out_dtype != ACTC_DTYPE_F64) return set_err(ACTC_EPARAM, "bad out dtype");
   if (!(stream->eb > 0 && isfinite(stream->eb)) || stream->radius < 2)
     return set_err(ACTC_EFORMAT, "invalid codec params in stream");
   if (2ull * stream->radius > kMaxAlphabet) return set_err(ACTC_EPARAM, "radius too large for the device decoder");
-  return launch_decode(c, stream, out, out_dtype == ACTC_DTYPE_F32 ? 0 : 1, result_host, (cudaStream_t)s, phase);
+  return launch_decode(c, stream, out, out_dtype == ACTC_DTYPE_F32 ? 0 : 1, result_host, (cudaStream_t)s, phase,
+                       no_nonzero);
 }
 
 int actc_crc32(actc_ctx *c, const void *data_dev, uint64_t len, uint32_t crc_in, uint32_t *crc_out_host,

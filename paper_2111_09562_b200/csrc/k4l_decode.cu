@@ -8,21 +8,37 @@
 // recon / splice / re-zero (codec.py:360-369).
 //
 // Work unit: a warp owns 32 consecutive chunks (4096 symbols); lane l decodes
-// chunk l sequentially.  Per symbol the serial chain is one shared-memory
-// lookup: W (32-bit left-aligned window, one funnel shift) -> T1[W >> 20],
-// whose entry holds the code length and the canonical index of the first
-// code under the 12-bit prefix, exact whenever every code under the prefix
-// has one length (all prefixes except those a length boundary cuts, at most
-// one per length).  The canonical index -> Lorenzo delta lookup, the running
-// lattice sum, the fp64 reconstruction and the nonzero count hang off that
-// chain (independent of the next symbol's window).  Prefixes with mixed
-// lengths, codes longer than 32 bits, outlier markers and invalid codes take
-// a warp-voted slow path (the reference's bit rule on a 64-bit window).
-// Values leave through a per-warp transposition buffer: lanes store four
-// values at a time (16 B, conflict-free row stride), the warp then writes 8
-// chunk rows of 64 B per instruction.  One 1024-thread CTA per SM holds the
-// prefix table (16 KB), the canonical deltas (int16, <= 128 KB) and the
-// transposition rows (80 KB).
+// chunk l sequentially.  The decode is bound by the L1 data pipe (shared and
+// global wavefronts), then by instruction issue, so both are budgeted per
+// symbol:
+//
+//   window W     two payload words from the lane's ring    2 LDS (conflict-free)
+//   entry e      T1[W >> 20] (4 B)                         1 LDS (random banks)
+//   advance      pos += e                                  IADD (len in e's low bits)
+//   delta        e >> 16 for a prefix holding one code (direct), else the
+//                canonical delta table at ((e >> 16) + (W >> (32 - len))) mod 2^16
+//                                                          predicated LDS.S16
+//   value        P += delta; fp32(fp64(P) * 2eb)           IADD, I2F, DMUL, F2F
+//   store        16 B per 4 values into a swizzled box     STS.128
+//
+// T1 entry (kernels.cuh, k4l_table_rows): bits 0-4 the code length (0: slow
+// path), bit 15 "direct", bits 16-31 the payload.  `pos` holds the chunk's
+// bit position in its low 15 bits (a chunk spans < 2^13 bits), so `pos += e`
+// advances it by len and lets the rest of e spill into bits >= 15.
+//
+// Payload staging: each lane streams its own chunk through a 32-word ring in
+// shared memory, layout [slot][lane] (a warp's ring reads are conflict-free),
+// with a mirror of slot 0 behind slot 31 so the window's second word is always
+// at +128 B.  Words are fetched 32 B per lane per load (LDG.256, one sector),
+// byte-swapped once, issued a round ahead and never past the chunk's end.
+//
+// Output: lanes store their values into a per-warp 32-row x 64-B box
+// (hardware 64-B swizzle, conflict-free STS.128), and one lane hands every
+// box to the tensor memory accelerator (cp.async.bulk.tensor store, double
+// buffered): the transposition to the tensor's layout costs no load
+// wavefronts and no uncoalesced global stores.
+#include <cuda.h>
+
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -31,8 +47,18 @@ namespace actc {
 
 namespace {
 
-constexpr int kUnitsPerRow = 2;  // 16-B units of values per row and round
-constexpr int kRowBytes = 48;    // 32 B of values + 16 B pad (odd number of 16-B units)
+constexpr int kRingSlots = 32;                              // payload words per lane in the ring
+constexpr int kRingBytesPerWarp = (kRingSlots + 1) * 128;   // + the mirror of slot 0
+constexpr int kBoxBytes = 32 * 64;                          // one TMA box: 32 chunk rows x 64 B
+constexpr int kOutBytesPerWarp = 2 * kBoxBytes;             // double buffered
+constexpr uint32_t kSeedGroups = 3;  // 32-B groups staged at a chunk's start
+constexpr uint32_t kNeed = 15;       // words past a round's first word it may touch
+constexpr uint32_t kTopUp = 17;      // ... staged by the rare synchronous top-up
+constexpr uint32_t kAhead = 24;      // refill while staged words <= round word + kAhead
+constexpr uint32_t kPosMask = 0x7FFFu;
+
+static_assert(kSeedGroups == 3 && 8 * kSeedGroups >= 7 + kTopUp, "seed covers the first round");
+static_assert(kAhead + 8 <= kRingSlots, "refill never overwrites a word still needed");
 
 __device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t n) {  // x >> n, 0 for n >= 32
   uint32_t r;
@@ -65,15 +91,6 @@ struct OutT<2> {
   typedef uint32_t T;
 };
 
-}  // namespace
-
-__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon, uint32_t radius,
-                                uint32_t *__restrict__ table) {
-  k4l_table_rows(len_counts, canon, radius, table, blockIdx.x);
-}
-
-size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps);
-
 // shared-window address kept in a register (otherwise the compiler rebuilds
 // it from SR_CgaCtaId at every access inside the decode loop)
 __device__ __forceinline__ uint32_t k4l_saddr(const void *p) {
@@ -81,15 +98,45 @@ __device__ __forceinline__ uint32_t k4l_saddr(const void *p) {
   asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
   return r;
 }
+// ring reads (volatile: ordered after the lane's own ring stores)
 __device__ __forceinline__ uint32_t k4l_lds(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// read-only tables (written before the __syncthreads ahead of the tile loop)
+__device__ __forceinline__ uint32_t k4l_lds_t(uint32_t addr) {
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ int k4l_lds_s16(uint32_t addr) {
-  int v;
-  asm("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(addr));
+__device__ __forceinline__ int k4l_lds_s16_if(uint32_t addr, int v, bool on) {
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.s16 %0, [%1];\n\t}"
+      : "+r"(v)
+      : "r"(addr), "r"((uint32_t)on));
   return v;
+}
+__device__ __forceinline__ void k4l_sts(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+struct U8 {
+  uint32_t w[8];
+};
+// one 32-B sector, predicated (r keeps its value when !on)
+__device__ __forceinline__ void k4l_ldg256_if(U8 &r, const unsigned char *p, bool on) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+      : "+r"(r.w[0]), "+r"(r.w[1]), "+r"(r.w[2]), "+r"(r.w[3]), "+r"(r.w[4]), "+r"(r.w[5]), "+r"(r.w[6]),
+        "+r"(r.w[7])
+      : "l"(p), "r"((uint32_t)on));
+}
+
+}  // namespace
+
+__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon,
+                                uint32_t radius, uint32_t *__restrict__ table) {
+  k4l_table_rows(len_counts, canon, radius, table, blockIdx.x);
 }
 
 struct K4LShared {
@@ -98,100 +145,77 @@ struct K4LShared {
   uint32_t maxlen;
 };
 
-// Payload staging: every lane streams its own chunk, so each lane keeps a
-// ring of kRingGroups 16-byte groups of its bitstream in shared memory
-// (layout [group slot][lane], 16 B per entry), filled by cp.async (LDGSTS,
-// L1 bypassed) once per round for the groups it has moved past.  The decode
-// chain reads the next word from the ring (shared-memory latency) instead of
-// waiting for a global load on every refill.
-constexpr int kRingGroups = 4;
-constexpr int kRingBytesPerWarp = kRingGroups * 32 * 16;
-
-__device__ __forceinline__ void k4l_cp16(uint32_t dst, const void *src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void k4l_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void k4l_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // per-lane decode state of one chunk
 template <bool NARROW>
 struct K4LLane {
   typedef typename std::conditional<NARROW, int, long long>::type Lat;
-  uint32_t a;       // word index (in the payload) of cur
-  uint32_t issued;  // next 16-B group to stage
-  uint32_t cur, nxt, nn, boff;
+  uint32_t pos;   // bit position relative to the ring origin (low 15 bits)
+  uint32_t G;     // 32-B groups staged or in flight
+  uint32_t pend;  // a group was issued at the last round start (landing now)
+  U8 p;
   Lat P;
   uint32_t ordn;
   bool ord_known;
 };
 
+// the lane's payload ring (layout [slot][lane], slot 32 mirrors slot 0)
 struct K4LRing {
-  uint32_t base;   // shared address of this lane's slot 0: ring + lane*16
-  uint32_t capg;   // groups of the payload buffer (staging never reads past it)
-  const uint32_t *pw;
-  __device__ __forceinline__ uint32_t addr(uint32_t w) const {  // shared address of payload word w
-    return base + ((w >> 2) & (kRingGroups - 1)) * 512u + (w & 3u) * 4u;
+  uint32_t base;             // shared address of this lane's slot 0
+  const unsigned char *src;  // the ring origin: the 32-B sector holding the chunk's first bit
+  uint32_t endg;             // groups up to the chunk's end (loads stop there)
+  __device__ __forceinline__ void load_if(U8 &v, uint32_t g, bool on) const { k4l_ldg256_if(v, src + 32ull * g, on); }
+  // group g's words into slots 8g .. 8g+7 (mod 32), big-endian -> value order
+  __device__ __forceinline__ void store(uint32_t g, const U8 &v) const {
+    const uint32_t s0 = (8u * g) & (kRingSlots - 1);
+    const uint32_t ad = base + s0 * 128u;
+    const uint32_t w0 = bswap32(v.w[0]);
+    k4l_sts(ad, w0);
+#pragma unroll
+    for (int k = 1; k < 8; k++) k4l_sts(ad + 128u * k, bswap32(v.w[k]));
+    if (s0 == 0) k4l_sts(base + kRingSlots * 128u, w0);
   }
-  __device__ __forceinline__ uint32_t word(uint32_t w) const {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr(w)));  // ordered after the cp.async waits
-    return bswap32(v);
-  }
-  __device__ __forceinline__ uint32_t word_if(uint32_t w, bool on) const {  // predicated read
-    uint32_t v = 0;
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
-                 : "+r"(v)
-                 : "r"(addr(w)), "r"((uint32_t)on));
-    return bswap32(v);
-  }
-  // stage groups [issued, upto) (bounded by the buffer)
-  __device__ __forceinline__ void stage(uint32_t &issued, uint32_t upto) const {
-    upto = min(upto, capg);
-    for (; issued < upto; issued++) k4l_cp16(base + (issued & (kRingGroups - 1)) * 512u, pw + 4ull * issued);
-    k4l_commit();
+  // the 32-bit window at bit position pos (relative)
+  __device__ __forceinline__ uint32_t window(uint32_t pos) const {
+    const uint32_t ad = base + ((pos & 0x3E0u) << 2);
+    const uint32_t w0 = k4l_lds(ad), w1 = k4l_lds(ad + 128u);
+    return __funnelshift_l(w1, w0, pos);  // shift = pos & 31
   }
 };
 
-// the window moves by one word once 32 bits are consumed (branch-free: the
-// selects keep the warp converged; the ring read is predicated)
+// Refill at a round's start: store the group that landed, top up
+// synchronously if a run of long codes got ahead of the staging (rare), and
+// issue the next load (at most one group; it lands by the next round).
+// Groups past the chunk's end are counted as staged without a load (the
+// window's look-ahead bits past the last code never decide a code).
 template <bool NARROW>
-__device__ __forceinline__ void k4l_advance(const K4LRing &rg, K4LLane<NARROW> &L) {
-  const bool adv = L.boff >= 32u;
-  const uint32_t w3 = rg.word_if(L.a + 3, adv);
-  L.a += adv ? 1u : 0u;
-  L.cur = adv ? L.nxt : L.cur;
-  L.nxt = adv ? L.nn : L.nxt;
-  L.nn = adv ? w3 : L.nn;
-  L.boff -= adv ? 32u : 0u;
-}
-
-// (re)seed a lane's ring at word a and load its window (waits for the data)
-template <bool NARROW>
-__device__ __forceinline__ void k4l_seed(const K4LRing &rg, K4LLane<NARROW> &L, uint32_t a) {
-  k4l_wait<0>();  // no copy into the ring may still be in flight
-  L.a = a;
-  L.issued = a >> 2;
-  rg.stage(L.issued, (a >> 2) + kRingGroups);
-  k4l_wait<0>();
-  L.cur = rg.word(a);
-  L.nxt = rg.word(a + 1);
-  L.nn = rg.word(a + 2);
+__device__ __forceinline__ void k4l_refill(const K4LRing &rg, K4LLane<NARROW> &L) {
+  if (L.pend) rg.store(L.G - 1, L.p);
+  const uint32_t aw = (L.pos & kPosMask) >> 5;
+  if (8u * L.G < aw + kNeed) {
+    while (8u * L.G < aw + kTopUp) {
+      if (L.G < rg.endg) {
+        U8 t = {};
+        rg.load_if(t, L.G, true);
+        rg.store(L.G, t);
+      }
+      L.G++;
+    }
+  }
+  const bool want = 8u * L.G <= aw + kAhead;
+  L.pend = want && L.G < rg.endg;
+  rg.load_if(L.p, L.G, L.pend);
+  L.G += want;
 }
 
 // Phase A's rare path (lane-divergent): the reference's bit rule for a
 // prefix the table does not resolve (scan from the prefix's shortest length
-// l0; huffman.py:129-141).  Returns the canonical index, sets len (the
-// caller advances the window).
-template <bool NARROW>
-__device__ __forceinline__ uint32_t k4l_resolve(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg,
-                                             K4LLane<NARROW> &L, uint32_t e, uint32_t W, uint32_t &len, bool &bad) {
+// l0; huffman.py:129-141).  Returns {canonical index, length | bad << 31};
+// the caller advances the position.
+__device__ __forceinline__ uint2 k4l_resolve(const K4LShared &sh, const uint32_t *__restrict__ payload, uint64_t nwords,
+                                          uint32_t live, uint64_t abs_pos, uint32_t W, uint32_t l0) {
   const int maxlen = (int)sh.maxlen;
-  int l = max(1, (int)(e >> 7));
-  uint32_t ci = 0;
-  len = 0;
+  int l = max(1, (int)l0);
+  uint32_t ci = 0, len = 0, bad = 0;
   for (; l <= min(maxlen, 32); l++) {
     const uint32_t code = shr_clamp(W, 32u - (uint32_t)l);
     if ((unsigned long long)code >= sh.first[l] && code - (uint32_t)sh.first[l] < sh.count[l]) {
@@ -202,7 +226,7 @@ __device__ __forceinline__ uint32_t k4l_resolve(const DecodeArgs &a, const K4LSh
   }
   if (!len && maxlen > 32) {
     // codes longer than 32 bits: a 64-bit window from the payload
-    const uint64_t win = k4l_bits64(a.payload, ((uint64_t)L.a << 5) + L.boff, 4ull * rg.capg);
+    const uint64_t win = k4l_bits64(payload, abs_pos, nwords);
     for (l = max(l, 33); l <= maxlen; l++) {
       const unsigned long long cd = win >> (64 - l), of = cd - sh.first[l];
       if (of < sh.count[l]) {
@@ -213,17 +237,10 @@ __device__ __forceinline__ uint32_t k4l_resolve(const DecodeArgs &a, const K4LSh
     }
   }
   if (!len) {
-    bad = true;  // invalid code (-2), or a stream cut short
+    bad = 1u;  // invalid code (-2), or a stream cut short
     len = 1;
   }
-  L.boff += len;
-  if (L.boff >= 64u) {
-    // a code of more than 32 bits ran past the window: re-seed the ring
-    const uint64_t np = ((uint64_t)L.a << 5) + L.boff;
-    L.boff = (uint32_t)(np & 31);
-    k4l_seed(rg, L, (uint32_t)(np >> 5));
-  }
-  return min(ci, a.live - 1);
+  return make_uint2(min(ci, live - 1), len | (bad << 31));
 }
 
 // Phase B's rare path: an outlier marker.  The chain rebases on
@@ -231,7 +248,7 @@ __device__ __forceinline__ uint32_t k4l_resolve(const DecodeArgs &a, const K4LSh
 // (codec.py:286-292, 356-368); the marker must sit at the next stored index.
 template <bool NARROW>
 __device__ __forceinline__ double k4l_marker(const DecodeArgs &a, K4LLane<NARROW> &L, uint64_t e_idx, uint64_t e0,
-                                          bool &bad, unsigned long long &markers) {
+                                             bool &bad, unsigned long long &markers) {
   if (!L.ord_known) {
     uint64_t lo = 0, hi = a.k;
     while (lo < hi) {
@@ -253,66 +270,67 @@ __device__ __forceinline__ double k4l_marker(const DecodeArgs &a, K4LLane<NARROW
   return rv;
 }
 
+struct K4LCtx {
+  uint32_t t1_s, cd_s;  // shared addresses: prefix table, canonical deltas
+  uint32_t obox;        // this warp's two output boxes
+  uint64_t nwords;      // payload words incl. the buffers' 32-byte pad
+  const CUtensorMap *tm;
+};
+
 // decode one lane's chunk (ACTC_CHUNK symbols, or cnt when !FULL) of a
-// 32-chunk tile and write the tile's values out through the warp's rows
-template <int MODE, bool GCANON, bool FULL, bool NARROW>
-__device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg, uint32_t t1_s,
-                                         uint32_t cd_s, uint32_t wrows, uint64_t tile, uint64_t nchunks,
-                                         uint32_t cnt, uint64_t e0, K4LLane<NARROW> &L,
-                                         unsigned long long &nonzero, unsigned long long &markers, bool &bad) {
+// 32-chunk tile; FULL tiles leave through the TMA boxes, the partial tile
+// through plain stores
+template <int MODE, bool GCANON, bool FULL, bool NARROW, bool NZ>
+__device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &sh, const K4LRing &rg,
+                                         const K4LCtx &cx, uint64_t tile, uint32_t cnt, uint64_t e0, uint64_t abs0,
+                                         K4LLane<NARROW> &L, unsigned long long &nonzero,
+                                         unsigned long long &markers, bool &bad) {
   typedef typename OutT<MODE>::T T;
   constexpr int VPU = 16 / (int)sizeof(T);  // values per 16-B unit
-  constexpr int R = kUnitsPerRow * VPU;     // symbols per lane per round (one 32-B row)
+  constexpr int R = 2 * VPU;                // symbols per lane per round (32 B)
   const int lane = threadIdx.x & 31;
   const int radius = (int)a.radius;
   const double two_eb = a.two_eb;
-  const uint32_t myrow = wrows + lane * kRowBytes;
+  // this lane's row of the boxes, and the 64-B swizzle of its 16-B units
+  const uint32_t myrow = cx.obox + lane * 64u;
+  const uint32_t swz = (uint32_t)((lane >> 1) & 3);
   uint32_t nzc = 0;
-  uint32_t safe_g = L.issued;  // groups known to have landed
   for (int r = 0; r < ACTC_CHUNK / R; r++) {
-    // the fast path reads at most R + 3 words ahead this round (a code of at
-    // most 32 bits per symbol; the ring holds 4 groups from the current one)
-    if (((L.a + R + 3) >> 2) >= safe_g) k4l_wait<0>();
-    else k4l_wait<1>();
-    // phase A: the window chain -- R codes resolved to x = (delta << 1) | 1
-    // (direct entries) or ci << 1; nothing here waits on a delta lookup.  A
-    // prefix the table does not resolve takes the per-symbol rule (branch).
-    int x[R];
-#pragma unroll
-    for (int j = 0; j < R; j++) {
-      const uint32_t i = (uint32_t)(r * R + j);
-      const uint32_t W = __funnelshift_l(L.nxt, L.cur, L.boff);
-      const uint32_t e = k4l_lds(t1_s + ((W >> 20) << 2));
-      uint32_t len = e & 63u;
-      x[j] = (e & 64u) ? ((int)e >> 6) : (int)(((e >> 7) + shr_clamp(W & 0xFFFFFu, 32u - len)) << 1);
-      if (!FULL && i >= cnt) {
-        len = 64u;  // past the chunk: no code, no advance
-        x[j] = 1;   // delta 0 (direct), never a marker
-      }
-      L.boff += len & 63u;
-      if (len == 0u) x[j] = (int)(k4l_resolve<NARROW>(a, sh, rg, L, e, W, len, bad) << 1);
-      k4l_advance(rg, L);
-    }
-    // phase B: deltas (independent lookups), the lattice running sum, the
-    // reconstruction.  Outlier markers only occur in streams with outliers
-    // (not NARROW); a round holding one is redone with the splice rule.
-    int gd[GCANON ? R : 1];
-    if (GCANON) {
-#pragma unroll
-      for (int j = 0; j < R; j++)  // the round's canonical lookups in flight together
-        gd[j] = (x[j] & 1) ? 0 : (int)__ldg(a.canon + ((uint32_t)x[j] >> 1));
-    }
+    k4l_refill<NARROW>(rg, L);
+    // phase A: the window chain -- R codes resolved to their deltas (the
+    // delta lookups hang off the chain: nothing waits on them until phase B)
     int dl[R];
 #pragma unroll
     for (int j = 0; j < R; j++) {
-      const bool dir = (x[j] & 1) != 0;
-      if (GCANON) {
-        dl[j] = dir ? (x[j] >> 1) : gd[j] - radius;
+      const uint32_t W = rg.window(L.pos);
+      uint32_t e = k4l_lds_t(cx.t1_s + ((W >> 20) << 2));
+      const bool in = FULL || (uint32_t)(r * R + j) < cnt;
+      if (!in) e = 0x8000u;  // past the chunk: direct delta 0, no advance
+      uint32_t ci;
+      bool dir;
+      if ((e & 31u) == 0u && in) {
+        const uint2 rs = k4l_resolve(sh, a.payload, cx.nwords, a.live, abs0 + (L.pos & kPosMask), W, e >> 16);
+        bad |= (rs.y >> 31) != 0u;
+        L.pos += rs.y & 0x7FFFFFFFu;
+        ci = rs.x;  // indirect, index known
+        dir = false;
       } else {
-        const int d = k4l_lds_s16(cd_s + (dir ? 0u : (uint32_t)x[j]));  // 2 * ci
-        dl[j] = dir ? (x[j] >> 1) : d;
+        L.pos += e;
+        ci = ((e >> 16) + __funnelshift_l(W, 0u, e)) & 0xFFFFu;  // W >> (32 - len)
+        dir = (e & 0x8000u) != 0u;
+      }
+      const int dd = (int)e >> 16;
+      if (GCANON) {
+        int g = 0;
+        if (!dir) g = (int)__ldg(a.canon + ci) - radius;
+        dl[j] = dir ? dd : g;
+      } else {
+        dl[j] = k4l_lds_s16_if(cx.cd_s + 2u * ci, dd, !dir);
       }
     }
+    // phase B: the lattice running sum and the reconstruction.  Outlier
+    // markers only occur in streams with outliers (not NARROW); a round
+    // holding one is redone with the splice rule.
     T vals[R];
     const typename K4LLane<NARROW>::Lat P0 = L.P;
     const uint32_t nz0 = nzc;
@@ -323,13 +341,13 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
         vals[j] = (T)(uint32_t)(dl[j] + radius);
       } else {
         vals[j] = (T)__dmul_rn((double)L.P, two_eb);
-        if (FULL || (uint32_t)(r * R + j) < cnt) nzc += L.P != 0;
+        if (NZ && (FULL || (uint32_t)(r * R + j) < cnt)) nzc += L.P != 0;
       }
     }
     if (!NARROW && MODE != 2) {
       bool mk = false;
 #pragma unroll
-      for (int j = 0; j < R; j++) mk |= dl[j] == -radius;
+      for (int j = 0; j < R; j++) mk |= dl[j] == -radius && (FULL || (uint32_t)(r * R + j) < cnt);
       if (__any_sync(0xffffffffu, mk)) {
         L.P = P0;
         nzc = nz0;
@@ -347,63 +365,58 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
             vals[j] = (T)__dmul_rn((double)L.P, two_eb);
             nzi = L.P != 0;
           }
-          if (in) nzc += nzi;
+          if (NZ && in) nzc += nzi;
         }
       }
     }
+    if (FULL) {
+      // units 2(r&1), 2(r&1)+1 of this lane's row in box (r >> 1) & 1
+      const uint32_t box = ((uint32_t)(r >> 1) & 1u) * kBoxBytes;
+      if ((r & 1) == 0) {
+        // the TMA store that read this box last (two boxes ago) must be done
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+      }
 #pragma unroll
-    for (int u = 0; u < kUnitsPerRow; u++) {
-      uint4 pk;
-      memcpy(&pk, vals + u * VPU, 16);
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(myrow + 16u * u), "r"(pk.x), "r"(pk.y),
-                   "r"(pk.z), "r"(pk.w)
-                   : "memory");
-    }
-    // stage the groups this lane moved past (one commit group per round)
-    safe_g = L.issued;
-    rg.stage(L.issued, (L.a >> 2) + kRingGroups);
-    __syncwarp();
-    // write-out: instruction t stores rows 16t .. 16t+15 (row = chunk of the
-    // tile), each lane one 16-B unit; unit u of row rho sits at 16*(3*rho+u):
-    // the 8 lanes of a quarter-warp hit 8 distinct 16-B bank groups
-    const int rho_l = lane & 15, uu = lane >> 4;
-#pragma unroll
-    for (int t = 0; t < 2; t++) {
-      const int rho = 16 * t + rho_l;
-      uint4 val4;
-      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(val4.x), "=r"(val4.y), "=r"(val4.z), "=r"(val4.w)
-                   : "r"(wrows + rho * kRowBytes + 16u * uu)
-                   : "memory");
-      const uint64_t ch = tile * 32 + rho;
-      const uint64_t el = ch * ACTC_CHUNK + (uint64_t)r * R + (uint64_t)uu * VPU;
-      T *dst = reinterpret_cast<T *>(a.out) + el;
-      if (FULL) {
-        __stcs(reinterpret_cast<uint4 *>(dst), val4);
-      } else if (ch < nchunks) {
-        const uint64_t lim = min(a.n, (ch + 1) * ACTC_CHUNK);
-        if (el + VPU <= lim) {
-          __stcs(reinterpret_cast<uint4 *>(dst), val4);
-        } else {
-          T tmp[VPU];
-          memcpy(tmp, &val4, 16);
-          for (int k = 0; k < VPU; k++)
-            if (el + k < lim) dst[k] = tmp[k];
+      for (int u = 0; u < 2; u++) {
+        uint4 pk;
+        memcpy(&pk, vals + u * VPU, 16);
+        const uint32_t unit = ((uint32_t)(2 * (r & 1) + u)) ^ swz;
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(myrow + box + 16u * unit), "r"(pk.x),
+                     "r"(pk.y), "r"(pk.z), "r"(pk.w)
+                     : "memory");
+      }
+      if (r & 1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const int x = (r >> 1) * (64 / (int)sizeof(T));
+          const int y = (int)(tile * 32);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"((uint64_t)cx.tm),
+              "r"(x), "r"(y), "r"(cx.obox + box)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
+    } else {
+      T *dst = reinterpret_cast<T *>(a.out) + e0 + (uint64_t)r * R;
+#pragma unroll
+      for (int j = 0; j < R; j++)
+        if ((uint32_t)(r * R + j) < cnt) dst[j] = vals[j];
     }
-    __syncwarp();
   }
-  nonzero += nzc;
+  if (NZ) nonzero += nzc;
 }
 
-template <int MODE, bool GCANON>
-__global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
-  const int NW = blockDim.x >> 5;  // warps per CTA: fewer for small streams (every SM busy)
-  extern __shared__ __align__(16) unsigned char k4l_sm[];
-  uint32_t *t1 = reinterpret_cast<uint32_t *>(k4l_sm);
-  unsigned char *rows = k4l_sm + kLutSize * 4;
-  unsigned char *ring = rows + NW * 32 * kRowBytes;
+template <int MODE, bool GCANON, bool NZ>
+__global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a, const __grid_constant__ CUtensorMap tm) {
+  const int NW = blockDim.x >> 5;  // warps per CTA (fewer for small streams or big delta tables)
+  extern __shared__ __align__(1024) unsigned char k4l_sm[];
+  // boxes first, on a 1024-B boundary (the swizzle atom repeats every 512 B)
+  unsigned char *obox = k4l_sm + ((1024u - (k4l_saddr(k4l_sm) & 1023u)) & 1023u);
+  unsigned char *t1 = obox + NW * kOutBytesPerWarp;
+  unsigned char *ring = t1 + kLutSize * 4;
   int16_t *cdelta = reinterpret_cast<int16_t *>(ring + NW * kRingBytesPerWarp);
   __shared__ K4LShared sh;
 
@@ -457,22 +470,24 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
   const uint64_t n = a.n;
   const uint64_t nchunks = (n + ACTC_CHUNK - 1) / ACTC_CHUNK;
   const uint64_t ntiles = (nchunks + 31) / 32;
-  const uint32_t t1_s = k4l_saddr(t1);
-  const uint32_t cd_s = k4l_saddr(cdelta);
-  K4LRing rg;
-  rg.base = k4l_saddr(ring + warp * kRingBytesPerWarp) + lane * 16u;
-  rg.pw = a.payload;
-  // groups of the payload buffer: 4*ceil(bits/32) + 32 bytes (codec.py
-  // buffers carry the decoder's over-read pad)
-  rg.capg = (uint32_t)(((a.payload_bits + 31) / 32 * 4 + 32) / 16);
-  const uint32_t wrows = k4l_saddr(rows) + warp * 32 * kRowBytes;  // this warp's 32 rows
+  K4LCtx cx;
+  cx.t1_s = k4l_saddr(t1);
+  cx.cd_s = k4l_saddr(cdelta);
+  cx.obox = k4l_saddr(obox + warp * kOutBytesPerWarp);
+  cx.nwords = (a.payload_bits + 31) / 32 + 8;
+  cx.tm = &tm;
+  const uint32_t rbase = k4l_saddr(ring + warp * kRingBytesPerWarp) + lane * 4u;
+  const uint64_t pay = (uint64_t)a.payload;  // byte address of the payload
   unsigned long long nonzero = 0, markers = 0;
   bool bad = false;
   // 32-bit lattice arithmetic: no outliers (no rebase) and 16-bit deltas, so
   // a chunk moves its running value by < 2^22 from a start below 2^30
   const bool narrow_ok = MODE == 2 || (a.k == 0 && radius <= 32768);
 
-  for (uint64_t tile = (uint64_t)blockIdx.x * NW + warp; tile < ntiles; tile += (uint64_t)gridDim.x * NW) {
+  // tile of pass k: k * (grid * NW) + warp * grid + block -- the tiles of a
+  // last, partial pass spread over every SM (one SM holding all of them
+  // would run alone at the end)
+  for (uint64_t tile = (uint64_t)warp * gridDim.x + blockIdx.x; tile < ntiles; tile += (uint64_t)gridDim.x * NW) {
     const uint64_t c = tile * 32 + lane;
     const bool valid = c < nchunks;
     const uint64_t e0 = c * ACTC_CHUNK;
@@ -484,30 +499,53 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
       pos0 = a.chunk_off[c];
       endp = (c + 1 < nchunks) ? a.chunk_off[c + 1] : a.payload_bits;
       if (MODE != 2) P0 = a.chunk_lat[c];
+      if (pos0 > endp || endp > a.payload_bits) {  // a corrupt index: nothing is read past the buffer
+        bad = true;
+        pos0 = endp = 0;
+      }
     }
     const bool narrow = narrow_ok && __all_sync(0xffffffffu, P0 > -(1ll << 30) && P0 < (1ll << 30));
+    // the ring origin: the 32-B sector holding the chunk's first bit
+    const uint64_t byte0 = pay + (pos0 >> 3);
+    const uint64_t org = byte0 & ~31ull;
+    const uint32_t rel0 = (uint32_t)(((byte0 - org) << 3) + (pos0 & 7));  // pos0 relative to the origin
+    K4LRing rg;
+    rg.base = rbase;
+    rg.src = reinterpret_cast<const unsigned char *>(org);
+    rg.endg = (uint32_t)((rel0 + (endp - pos0) + 255) >> 8);
+    const uint64_t abs0 = pos0 - rel0;  // payload bit position of the origin (mod 2^64)
     uint64_t pos_end;
-#define K4L_RUN(FULLV, NARROWV)                                                                          \
-  {                                                                                                    \
-    K4LLane<NARROWV> L;                                                                                \
-    L.boff = (uint32_t)(pos0 & 31);                                                                    \
-    k4l_seed(rg, L, (uint32_t)(pos0 >> 5));                                                           \
-    L.P = (typename K4LLane<NARROWV>::Lat)P0;                                                          \
-    L.ordn = 0;                                                                                        \
-    L.ord_known = false;                                                                               \
-    k4l_tile<MODE, GCANON, FULLV, NARROWV>(a, sh, rg, t1_s, cd_s, wrows, tile, nchunks, cnt, e0, L, nonzero, \
-                                            markers, bad);                                             \
-    pos_end = ((uint64_t)L.a << 5) + L.boff;                                                           \
+#define K4L_RUN(FULLV, NARROWV)                                                                              \
+  {                                                                                                        \
+    K4LLane<NARROWV> L;                                                                                    \
+    L.pos = rel0;                                                                                          \
+    {                                                                                                      \
+      U8 s0 = {}, s1 = {}, s2 = {}; /* groups past the chunk's end are not loaded (don't-care words) */   \
+      rg.load_if(s0, 0, 0 < rg.endg);                                                                      \
+      rg.load_if(s1, 1, 1 < rg.endg);                                                                      \
+      rg.load_if(s2, 2, 2 < rg.endg);                                                                      \
+      rg.store(0, s0);                                                                                     \
+      rg.store(1, s1);                                                                                     \
+      rg.store(2, s2);                                                                                     \
+    }                                                                                                      \
+    L.G = kSeedGroups;                                                                                     \
+    L.pend = 0;                                                                                            \
+    L.p = U8{};                                                                                            \
+    L.P = (typename K4LLane<NARROWV>::Lat)P0;                                                              \
+    L.ordn = 0;                                                                                            \
+    L.ord_known = false;                                                                                   \
+    k4l_tile<MODE, GCANON, FULLV, NARROWV, NZ>(a, sh, rg, cx, tile, cnt, e0, abs0, L, nonzero, markers, bad); \
+    pos_end = abs0 + (L.pos & kPosMask);                                                                   \
   }
     if (full && narrow) K4L_RUN(true, true)
     else if (full) K4L_RUN(true, false)
     else K4L_RUN(false, false)
 #undef K4L_RUN
-    if (valid && (pos_end != endp || endp > a.payload_bits)) bad = true;
+    if (valid && pos_end != endp) bad = true;
   }
-  k4l_wait<0>();
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (bad) report_format_error(a);
-  const unsigned long long ws = warp_sum(nonzero), wm = warp_sum(markers);
+  const unsigned long long ws = NZ ? warp_sum(nonzero) : 0ull, wm = warp_sum(markers);
   if (lane == 0) {
     if (ws) atomicAdd(a.nonzero, ws);
     if (wm) atomicAdd(a.markers, wm);
@@ -534,14 +572,26 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a) {
 }
 
 size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps) {
-  return (size_t)kLutSize * 4 + (size_t)warps * (32 * kRowBytes + kRingBytesPerWarp) +
+  return 1024 + (size_t)warps * (kOutBytesPerWarp + kRingBytesPerWarp) + (size_t)kLutSize * 4 +
          (gcanon ? 0 : (((size_t)live * 2 + 15) & ~(size_t)15));
 }
 
-template __global__ void k4l_decode<0, false>(DecodeArgs);
-template __global__ void k4l_decode<1, false>(DecodeArgs);
-template __global__ void k4l_decode<0, true>(DecodeArgs);
-template __global__ void k4l_decode<1, true>(DecodeArgs);
-template __global__ void k4l_decode<2, true>(DecodeArgs);
+// warps per CTA: as many as the shared memory holds (up to K4L_THREADS / 32)
+int k4l_max_warps(uint32_t live, bool gcanon, size_t smem_optin) {
+  const size_t fixed = k4l_smem_bytes(live, gcanon, 0) + sizeof(K4LShared) + 64;
+  if (smem_optin <= fixed) return 0;
+  const size_t per = kOutBytesPerWarp + kRingBytesPerWarp;
+  return (int)std::min<size_t>((size_t)(K4L_THREADS / 32), (smem_optin - fixed) / per);
+}
+
+template __global__ void k4l_decode<0, false, false>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<0, false, true>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<1, false, false>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<1, false, true>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<0, true, false>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<0, true, true>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<1, true, false>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<1, true, true>(DecodeArgs, const __grid_constant__ CUtensorMap);
+template __global__ void k4l_decode<2, true, false>(DecodeArgs, const __grid_constant__ CUtensorMap);
 
 }  // namespace actc

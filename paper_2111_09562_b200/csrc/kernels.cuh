@@ -1,5 +1,7 @@
 // kernels.cuh -- launch-shape constants and kernel declarations.
 #pragma once
+#include <cuda.h>
+
 #include "actc_internal.cuh"
 
 namespace actc {
@@ -29,7 +31,7 @@ constexpr int K4_THREADS = 128;
 // K4 (warp variant, indexed streams): one warp per 32 chunks
 // K4L (indexed streams): one CTA of up to 768 threads per SM, lane per chunk; the
 // canonical deltas stay in shared memory up to K4L_SMEM_LIVE live symbols
-constexpr int K4L_THREADS = 768;  // at most; small streams launch fewer warps per CTA
+constexpr int K4L_THREADS = 640;  // at most; small streams launch fewer warps per CTA
 constexpr uint32_t K4L_SMEM_LIVE = 49152;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
@@ -283,25 +285,33 @@ __device__ __forceinline__ void report_format_error(const DecodeArgs &a) {
 // SW: staging width of decoded symbols in shared memory (16 or 32 bits)
 template <int MODE, int SW>
 __global__ void k4_decode(DecodeArgs a);
-// K4L decode table (kLutWords words): T1[p] for every 12-bit prefix p of
-// the left-aligned 32-bit window; bits 0-5 the code length (0: slow path),
-// bit 6 "direct", bits 7-31 the payload:
-//  * one code under p (length <= 12, radius <= 2^24): direct, payload = its
-//    Lorenzo delta (symbol - radius, signed);
-//  * every code under p of one length len <= 32: payload = ci_base, the
-//    canonical index of the code under the window W being
-//    ci_base + ((W & 0xFFFFF) >> (32 - len));
-//  * otherwise length 0 and payload l0, the shortest length a code under p
-//    can have (0: no code, or an over-subscribed table, whose first-match
-//    rule the scan from length 1 reproduces).  Word kLutSize: 1 if the code table is prefix-free
-// (Kraft <= 1), word kLutSize + 1: the longest code length.
-__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon, uint32_t radius,
-                                uint32_t *__restrict__ table);
+// K4L decode table (ACTC_TABLE_BYTES): T1[p] (4 bytes) for every 12-bit
+// prefix p of the left-aligned 32-bit window, then two header words.
+// Entry: bits 0-4 the code length len (0: slow path), bit 15 "direct", bits
+// 16-31 the payload:
+//  * one code under p (len <= 12) whose Lorenzo delta (symbol - radius) fits
+//    int16: direct, payload = that delta;
+//  * every code under p of one length len <= 31, canonical indices < 2^16:
+//    payload = (base[len] - first[len]) mod 2^16 -- the canonical index of
+//    the code under W is (payload + (W >> (32 - len))) mod 2^16;
+//  * otherwise len 0 and payload l0, the shortest length a code under p can
+//    have (0: no code, or an over-subscribed table, whose first-match rule
+//    the scan from length 1 reproduces; 33: past every code of <= 32 bits).
+// Header: word kLutSize = 1 if the code table is prefix-free (Kraft <= 1),
+// word kLutSize + 1 = the longest code length.
+constexpr size_t kK4lTableBytes = (size_t)kLutSize * 4 + 16;
+static_assert(kK4lTableBytes == ACTC_TABLE_BYTES, "include/actc.h ACTC_TABLE_BYTES");
+__global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon,
+                                uint32_t radius, uint32_t *__restrict__ table);
 // MODE: 0 = fp32 recon, 1 = fp64 recon, 2 = raw u32 symbols;
-// GCANON: canonical symbols read from global memory (wide alphabets)
-template <int MODE, bool GCANON>
-__global__ void k4l_decode(DecodeArgs a);
+// GCANON: canonical symbols read from global memory (wide alphabets);
+// NZ: count the nonzero reconstructed values (R, training.py:351-352).
+// tm: the output as a 2-D tensor [n / ACTC_CHUNK rows][ACTC_CHUNK values],
+// box 32 rows x 64 B, 64-B swizzle (TMA stores of full tiles).
+template <int MODE, bool GCANON, bool NZ>
+__global__ void k4l_decode(DecodeArgs a, const __grid_constant__ CUtensorMap tm);
 size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps);
+int k4l_max_warps(uint32_t live, bool gcanon, size_t smem_optin);
 __global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
                                 unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
 
@@ -438,7 +448,7 @@ __device__ __forceinline__ void lut32_body(const uint32_t *__restrict__ canon, c
   lut[p] = e;
 }
 
-// decode table rows [blk*blockDim, (blk+1)*blockDim) (layout in kernels.cuh)
+// decode table rows [blk*blockDim, (blk+1)*blockDim) (layout above)
 __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_counts, const uint32_t *__restrict__ canon,
                                                uint32_t radius, uint32_t *__restrict__ table, uint32_t blk) {
   __shared__ unsigned long long s_first[33], s_lim[33];
@@ -488,19 +498,26 @@ __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_
       if (!l0 && s_lim[l] > w0) l0 = l;
       if (!l1 && s_lim[l] > w1) l1 = l;
     }
-    if (l0 && l0 == l1) {
-      const unsigned long long code0 = w0 >> (32 - l0);
-      const uint32_t ci = s_base[l0] + (uint32_t)(code0 - s_first[l0]);
-      if (l0 <= kLutBits && radius <= (1u << 24)) {
-        // one code under the prefix: its Lorenzo delta (symbol - radius) itself
-        e = ((uint32_t)((int)canon[ci] - (int)radius) << 7) | 64u | (uint32_t)l0;
-      } else {
-        e = (ci << 7) | (uint32_t)l0;
+    bool done = false;
+    if (l0 && l0 == l1 && l0 <= 31) {
+      // every code under p has length l0: canonical indices ci0 .. ci1
+      const uint32_t ci0 = s_base[l0] + (uint32_t)((w0 >> (32 - l0)) - s_first[l0]);
+      const uint32_t ci1 = s_base[l0] + (uint32_t)((w1 >> (32 - l0)) - s_first[l0]);
+      if (ci0 == ci1) {
+        const int d = (int)canon[ci0] - (int)radius;
+        if (d >= -32768 && d <= 32767) {
+          e = ((uint32_t)d << 16) | 0x8000u | (uint32_t)l0;
+          done = true;
+        }
       }
-    } else if (l0) {
-      e = (uint32_t)l0 << 7;  // mixed lengths: the decoder's scan starts at l0
-    } else if (s_max > 32) {
-      e = 33u << 7;  // past every code of <= 32 bits: longer codes only
+      if (!done && ci1 < 65536u) {
+        e = ((s_base[l0] - (uint32_t)s_first[l0]) << 16) | (uint32_t)l0;
+        done = true;
+      }
+    }
+    if (!done) {
+      if (l0) e = (uint32_t)l0 << 16;  // mixed lengths, 32-bit codes, wide index: the scan starts at l0
+      else if (s_max > 32) e = 33u << 16;  // past every code of <= 32 bits: longer codes only
     }
   }
   table[p] = e;
@@ -509,7 +526,6 @@ __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_
     table[kLutSize + 1] = s_max;
   }
 }
-
 
 // decode table rows [256*b, 256*b + 256) of a stream compressed by the
 // async chain (the pack kernel's first CTAs run it): the K4L table

@@ -543,7 +543,8 @@ class ActivationCompressor:
             if h.comp is not None:
                 # collection iterations read R back at once; otherwise the
                 # decode status is collected at the end of the iteration
-                out, nz = decompress_device(h.comp, dtype=torch.float32, check=self._collecting)
+                out, nz = decompress_device(h.comp, dtype=torch.float32, check=self._collecting,
+                                            count_nonzero=self._collecting)
                 h.out = out.view(h.shape)
                 if self._collecting:
                     self._R[h.layer] = nz / out.numel()
