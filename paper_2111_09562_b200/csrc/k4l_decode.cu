@@ -34,9 +34,9 @@
 //
 // Output: lanes store their values into a per-warp 32-row x 64-B box
 // (hardware 64-B swizzle, conflict-free STS.128), and one lane hands every
-// box to the tensor memory accelerator (cp.async.bulk.tensor store, double
-// buffered): the transposition to the tensor's layout costs no load
-// wavefronts and no uncoalesced global stores.
+// box (two rounds) to the tensor memory accelerator (cp.async.bulk.tensor
+// store): the transposition to the tensor's layout costs no load wavefronts
+// and no uncoalesced global stores.
 #include <cuda.h>
 
 #include <type_traits>
@@ -50,7 +50,7 @@ namespace {
 constexpr int kRingSlots = 32;                              // payload words per lane in the ring
 constexpr int kRingBytesPerWarp = (kRingSlots + 1) * 128;   // + the mirror of slot 0
 constexpr int kBoxBytes = 32 * 64;                          // one TMA box: 32 chunk rows x 64 B
-constexpr int kOutBytesPerWarp = 2 * kBoxBytes;             // double buffered
+constexpr int kOutBytesPerWarp = kBoxBytes;                 // one box per warp (its store is read out long before the box is refilled)
 constexpr uint32_t kSeedGroups = 3;  // 32-B groups staged at a chunk's start
 constexpr uint32_t kNeed = 15;       // words past a round's first word it may touch
 constexpr uint32_t kTopUp = 17;      // ... staged by the rare synchronous top-up
@@ -272,7 +272,7 @@ __device__ __forceinline__ double k4l_marker(const DecodeArgs &a, K4LLane<NARROW
 
 struct K4LCtx {
   uint32_t t1_s, cd_s;  // shared addresses: prefix table, canonical deltas
-  uint32_t obox;        // this warp's two output boxes
+  uint32_t obox;        // this warp's output box
   uint64_t nwords;      // payload words incl. the buffers' 32-byte pad
   const CUtensorMap *tm;
 };
@@ -370,11 +370,11 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
       }
     }
     if (FULL) {
-      // units 2(r&1), 2(r&1)+1 of this lane's row in box (r >> 1) & 1
-      const uint32_t box = ((uint32_t)(r >> 1) & 1u) * kBoxBytes;
+      // units 2(r&1), 2(r&1)+1 of this lane's row of the box
+      const uint32_t box = 0;
       if ((r & 1) == 0) {
-        // the TMA store that read this box last (two boxes ago) must be done
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        // the TMA store of the previous box (two rounds ago) must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
       }
 #pragma unroll
@@ -413,7 +413,7 @@ template <int MODE, bool GCANON, bool NZ>
 __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a, const __grid_constant__ CUtensorMap tm) {
   const int NW = blockDim.x >> 5;  // warps per CTA (fewer for small streams or big delta tables)
   extern __shared__ __align__(1024) unsigned char k4l_sm[];
-  // boxes first, on a 1024-B boundary (the swizzle atom repeats every 512 B)
+  // boxes first, on a 1024-B boundary (the 64-B swizzle atom spans 512 B)
   unsigned char *obox = k4l_sm + ((1024u - (k4l_saddr(k4l_sm) & 1023u)) & 1023u);
   unsigned char *t1 = obox + NW * kOutBytesPerWarp;
   unsigned char *ring = t1 + kLutSize * 4;
