@@ -41,6 +41,41 @@ __device__ __forceinline__ void lb_load(const SymT *__restrict__ sym, uint64_t b
   }
 }
 
+// a lane's K3L_EPT symbols, 16-bit ones kept two per register; cnt < K3L_EPT
+// only in the stream's last segment (symbols past the end read as 0 and are
+// masked by cnt)
+template <typename SymT>
+struct SymBuf {
+  static constexpr int W = sizeof(SymT) == 2 ? K3L_EPT / 2 : K3L_EPT;
+  uint32_t w[W];
+  uint32_t cnt;
+  __device__ __forceinline__ uint32_t get(int j) const {
+    if (sizeof(SymT) == 2) return (j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xFFFFu);
+    return w[j];
+  }
+  __device__ __forceinline__ void load(const SymT *__restrict__ sym, uint64_t base, uint64_t n) {
+    if (base + K3L_EPT <= n) {
+      cnt = K3L_EPT;
+      const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
+#pragma unroll
+      for (int j = 0; j < W / 4; j++) {
+        const uint4 v = __ldcs(p + j);  // streaming: the symbol buffer is read once more
+        w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+      }
+    } else {
+      cnt = base < n ? (uint32_t)(n - base) : 0u;
+#pragma unroll
+      for (int j = 0; j < W; j++) w[j] = 0;
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const uint32_t v = (uint32_t)j < cnt ? (uint32_t)sym[base + j] : 0u;
+        if (sizeof(SymT) == 2) w[j >> 1] |= v << (16 * (j & 1));
+        else w[j] = v;
+      }
+    }
+  }
+};
+
 }  // namespace
 
 // ===========================================================================
@@ -58,6 +93,14 @@ __device__ __forceinline__ void lb_load(const SymT *__restrict__ sym, uint64_t b
 
 constexpr uint32_t K3S_L8MAX = 65536;  // byte length table in shared memory (u16 symbol range)
 
+// pack-pass table entry of a (code << 8 | len) code-table word of a code of
+// <= 26 bits: the code left-aligned in 32 bits, its length in the low 6 bits
+// (which a left-aligned code of <= 26 bits leaves zero)
+__device__ __forceinline__ uint32_t k3_entry(unsigned long long g) {
+  const uint32_t len = (uint32_t)(g & 63);
+  return len ? ((uint32_t)(g >> 8) << (32 - len)) | len : 0u;
+}
+
 __device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned long long *__restrict__ ctab,
                                                uint32_t win_lo, uint32_t win_n, int nthreads) {
   for (uint32_t i0 = threadIdx.x; i0 < win_n; i0 += 16 * nthreads) {
@@ -70,7 +113,7 @@ __device__ __forceinline__ void k3_load_window(uint32_t *tab, const unsigned lon
 #pragma unroll
     for (int u = 0; u < 16; u++) {
       const uint32_t i = i0 + u * nthreads;
-      if (i < win_n) tab[i] = (uint32_t)(((e[u] >> 8) << 6) | (e[u] & 63));
+      if (i < win_n) tab[i] = k3_entry(e[u]);
     }
   }
 }
@@ -237,10 +280,9 @@ __device__ __forceinline__ uint32_t k3_lds(uint32_t a) {
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
-// OR v into the warp buffer when p (a no-op OR of 0 otherwise: an
-// unconditional reduction keeps the packing loop free of divergent branches)
-__device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v, uint32_t p) {
-  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(p ? v : 0u) : "memory");
+// OR v into the warp buffer
+__device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void k3_plan_out(const SegArgs &a) {
@@ -273,13 +315,23 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
   const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
   const uint64_t nwarps = (uint64_t)gridDim.x * (K3L_THREADS / 32);
   const uint32_t wlast = a.win_n - 1;
-  const bool fast_tab = a.span <= a.win_n;
-  const uint32_t tab_rel = k3_saddr(tab) - 4u * a.win_lo;  // tab[s - win_lo] at tab_rel + 4s (mod 2^32)
+  const uint32_t tab_s = k3_saddr(tab);
   const uint32_t wb_s = k3_saddr(wb);
-  for (uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + warp; seg < nseg; seg += nwarps) {
+  // the next segment's symbols are loaded while this one is encoded (16-bit
+  // symbols: two per register leave room for the second set)
+  constexpr bool kPrefetch = sizeof(SymT) == 2;
+  uint64_t seg = (uint64_t)blockIdx.x * (K3L_THREADS / 32) + warp;
+  SymBuf<SymT> nxt;
+  if (kPrefetch && seg < nseg) nxt.load(sym, seg * K3L_SEG + (uint64_t)lane * K3L_EPT, a.n);
+  for (; seg < nseg; seg += nwarps) {
     const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
-    uint32_t s[K3L_EPT];
-    lb_load(sym, base, a.n, s);
+    SymBuf<SymT> sb;
+    if (kPrefetch) {
+      sb = nxt;
+      if (seg + nwarps < nseg) nxt.load(sym, (seg + nwarps) * K3L_SEG + (uint64_t)lane * K3L_EPT, a.n);
+    } else {
+      sb.load(sym, base, a.n);
+    }
     const uint64_t r = seg / a.spc;
     const unsigned long long pb = a.cta_bits[r] + a.seg_bits[seg], pz = a.cta_nz[r] + a.seg_nz[seg];
     if (a.seg_long[seg]) {
@@ -289,8 +341,10 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
       uint32_t bits = 0, zm = 0;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        if (s[j] != kSent) bits += (uint32_t)(__ldg(&a.ctab[s[j]]) & 0xFF);
-        zm |= (uint32_t)(s[j] == 0) << j;
+        if ((uint32_t)j < sb.cnt) {
+          bits += (uint32_t)(__ldg(&a.ctab[sb.get(j)]) & 0xFF);
+          zm |= (uint32_t)(sb.get(j) == 0) << j;
+        }
       }
       const uint32_t nzl = __popc(zm);
       const uint32_t ib = warp_incl_sum(bits), iz = warp_incl_sum(nzl);
@@ -308,8 +362,8 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
       unsigned long long P = pb + lane_ex;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        if (s[j] == kSent) continue;
-        const unsigned long long g = __ldg(&a.ctab[s[j]]);
+        if ((uint32_t)j >= sb.cnt) continue;
+        const unsigned long long g = __ldg(&a.ctab[sb.get(j)]);
         const unsigned long long code = g >> 8;
         int len = (int)(g & 0xFF);
         while (len > 0) {
@@ -326,37 +380,37 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
       }
       continue;
     }
-    // one (code << 6 | len) lookup per symbol
+    // one (left-aligned code | len) lookup per symbol, clamped into the
+    // shared window; the few symbols outside it (the tails of the
+    // distribution) are fixed up from the global table, sentinels past the
+    // end get length 0
     uint32_t e[K3L_EPT];
-    uint32_t zmask = 0;
-    if (fast_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
-      // every live symbol is inside the window and the segment is full
-#pragma unroll
-      for (int j = 0; j < K3L_EPT; j++) e[j] = k3_lds(tab_rel + 4u * s[j]);
-      if (a.k) {
-#pragma unroll
-        for (int j = 0; j < K3L_EPT; j++) zmask |= (uint32_t)(s[j] == 0) << j;
-      }
-    } else {
-      // clamped into the shared window, symbols outside it (rare, long
-      // codes) fixed up from the global table; sentinels past the end
-      uint32_t oow = 0;
+    uint32_t zmask = 0, oow = 0;
+    if (__all_sync(0xffffffffu, sb.cnt == (uint32_t)K3L_EPT)) {
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        const uint32_t wi = s[j] - a.win_lo;
-        const bool sent = s[j] == kSent;
+        const uint32_t wi = sb.get(j) - a.win_lo;
+        e[j] = k3_lds(tab_s + 4u * min(wi, wlast));
+        oow |= (uint32_t)(wi > wlast) << j;
+      }
+      if (a.k) {
+#pragma unroll
+        for (int j = 0; j < K3L_EPT; j++) zmask |= (uint32_t)(sb.get(j) == 0) << j;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < K3L_EPT; j++) {
+        const uint32_t wi = sb.get(j) - a.win_lo;
+        const bool sent = (uint32_t)j >= sb.cnt;
         e[j] = sent ? 0u : tab[min(wi, wlast)];
         oow |= (uint32_t)(wi > wlast && !sent) << j;
-        zmask |= (uint32_t)(s[j] == 0) << j;
+        zmask |= (uint32_t)(sb.get(j) == 0 && !sent) << j;
       }
-      if (oow) {
+    }
+    if (oow) {
 #pragma unroll
-        for (int j = 0; j < K3L_EPT; j++) {
-          if ((oow >> j) & 1u) {  // re-read the symbol: s[] is dead here (register pressure)
-            const unsigned long long g = __ldg(&a.ctab[(uint32_t)sym[base + j]]);
-            e[j] = (uint32_t)(((g >> 8) << 6) | (g & 63));
-          }
-        }
+      for (int j = 0; j < K3L_EPT; j++) {
+        if ((oow >> j) & 1u) e[j] = k3_entry(__ldg(&a.ctab[sb.get(j)]));
       }
     }
     uint32_t bits = 0;
@@ -381,38 +435,32 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
       }
     }
     {
-      // codes <= 26 bits complete at most one word each.  Every word goes
-      // into the (zeroed) warp buffer by a predicated shared OR, so the
-      // lane's first and last words -- shared with its neighbours -- need
-      // no special case.  A length-0 entry (past the end) has code 0.
-      const uint32_t rel = off0 + lane_ex;
-      uint32_t addr = wb_s + 4u * (rel >> 5);
-      uint32_t nb = rel & 31;
-      unsigned long long acc = 0;
+      // Every code goes straight into the (zeroed) warp buffer at its bit
+      // offset: a left-aligned code of <= 26 bits touches two words at most,
+      // OR-ed by shared reductions (the second one only when the code
+      // crosses the word boundary), so the words lanes share need no special
+      // case.  A length-0 entry (past the end) has code 0.
+      uint32_t rel = off0 + lane_ex;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        const uint32_t lj = e[j] & 63;
-        acc |= (unsigned long long)(e[j] >> 6) << ((64 - nb - lj) & 63);
-        nb += lj;
-        const uint32_t ready = nb >= 32;
-        k3_red_or(addr, (uint32_t)(acc >> 32), ready);
-        acc = ready ? (acc << 32) : acc;
-        nb -= ready << 5;
-        addr += ready << 2;
+        const uint32_t cl = e[j] & ~63u;
+        const uint32_t ad = wb_s + ((rel >> 3) & ~3u);
+        const uint32_t v0 = __funnelshift_r(cl, 0u, rel);  // cl >> (rel & 31)
+        const uint32_t v1 = __funnelshift_r(0u, cl, rel);  // the bits past the word (0 when aligned)
+        k3_red_or(ad, v0);
+        k3_red_or(ad + 4u, v1);  // 0 unless the code crosses the word (unconditional: no branch)
+        rel += e[j] & 63;
       }
-      k3_red_or(addr, (uint32_t)(acc >> 32), nb > 0);
     }
     __syncwarp();
-    const uint64_t gw0 = pb >> 5;
+    // copy-out: interior words by plain stores, the two words the segment
+    // shares with its neighbours by global ORs (the payload was zeroed)
+    uint32_t *dst = a.payload + (pb >> 5);
     const uint32_t end_off = (off0 + seg_bits) & 31;
-    for (uint32_t i = lane; i < nw; i += 32) {
-      const uint32_t v = bswap32(wb[i]);
-      const bool shared_word = (i == 0 && off0 != 0) || (i == nw - 1 && end_off != 0);
-      if (shared_word)
-        atomicOr(&a.payload[gw0 + i], v);
-      else
-        a.payload[gw0 + i] = v;
-    }
+    const uint32_t i_lo = off0 ? 1u : 0u, i_hi = end_off ? nw - 1 : nw;
+    for (uint32_t i = i_lo + lane; i < i_hi; i += 32) dst[i] = bswap32(wb[i]);
+    if (lane == 0 && off0) atomicOr(dst, bswap32(wb[0]));
+    if (lane == 31 && end_off && (nw > 1 || !off0)) atomicOr(dst + nw - 1, bswap32(wb[nw - 1]));
     __syncwarp();
   }
   if (a.plan_host) {
