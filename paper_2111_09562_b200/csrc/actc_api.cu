@@ -956,7 +956,12 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     const uint64_t ntl = cdiv(nchunks, 32);
     const int wmax = k4l_max_warps(S.live_symbols, gcanon, (size_t)c->smem_optin);
     if (wmax < 1) return set_err(ACTC_EPARAM, "decode tables exceed shared memory");
-    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wmax, cdiv(ntl, c->num_sms)));
+    // every warp runs the same number of 32-chunk tiles: the fewest passes
+    // the shared memory allows, then the fewest warps per SM that still
+    // finish in that many passes (a partial last pass on some SMs would leave
+    // the others idle)
+    const uint64_t passes = cdiv(ntl, (uint64_t)c->num_sms * (uint64_t)wmax);
+    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wmax, cdiv(ntl, (uint64_t)c->num_sms * passes)));
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, warps), (uint64_t)c->num_sms));
     const size_t smem = k4l_smem_bytes(S.live_symbols, gcanon, warps);
     // full tiles leave through TMA stores: the output as [n / ACTC_CHUNK][ACTC_CHUNK]

@@ -31,7 +31,7 @@ constexpr int K4_THREADS = 128;
 // K4 (warp variant, indexed streams): one warp per 32 chunks
 // K4L (indexed streams): one CTA of up to 768 threads per SM, lane per chunk; the
 // canonical deltas stay in shared memory up to K4L_SMEM_LIVE live symbols
-constexpr int K4L_THREADS = 640;  // at most; small streams launch fewer warps per CTA
+constexpr int K4L_THREADS = 768;  // at most; small streams launch fewer warps per CTA
 constexpr uint32_t K4L_SMEM_LIVE = 49152;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
