@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KIND = {"k1_quant_lorenzo_hist": "quant", "k2_codebook": "codebook", "k2r_codebook": "codebook", "k2s_emit": "codebook",
         "k3_count": "count", "k3_seg_count": "count", "k_excl_scan_u64": "scan", "k3_cta_scan": "scan",
         "k3_pack": "pack", "k3_seg_pack": "pack", "k3_fixup": "fixup", "k_build_lut": "lut", "k_build_lut8": "lut",
-        "k4w_decode": "decode", "k4x_decode": "decode", "k4_decode": "decode"}
+        "k4w_decode": "decode", "k4x_decode": "decode", "k4_decode": "decode", "k4l_decode": "decode"}
 
 
 def kernel_base(name):
