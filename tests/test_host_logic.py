@@ -260,3 +260,35 @@ def test_stats_sync_two_ranks_gloo():
     assert R0 == R1 == [pytest.approx(0.55), pytest.approx(0.2)]
     assert L0 == L1 == [pytest.approx(1.5), 0.0]
     assert eb0 == eb1 and sk0 == sk1 == ["c1"]
+
+
+def test_marker_recompute_gives_identical_gradients():
+    """MARKER slots (pooling outputs recomputed in backward from the stored
+    activation, training.py:295-296, 344-347) change no value: with the
+    stored activations raw (first interval), every parameter gradient equals
+    that of the same step without the hooks, bit for bit."""
+    torch = pytest.importorskip("torch")
+    import torch.nn as nn
+
+    def net():
+        torch.manual_seed(3)
+        return nn.Sequential(nn.Conv2d(3, 8, 3), nn.ReLU(inplace=True), nn.MaxPool2d(2), nn.Conv2d(8, 8, 3),
+                             nn.ReLU(), nn.AvgPool2d(2), nn.Conv2d(8, 6, 1), nn.ReLU(), nn.Flatten(),
+                             nn.Linear(6 * 2 * 2, 4))
+
+    x = torch.randn(4, 3, 14, 14, generator=torch.Generator().manual_seed(5))
+    y = torch.tensor([0, 1, 2, 3])
+    ref = net()
+    torch.nn.functional.cross_entropy(ref(x), y).backward()
+    hooked = net()
+    opt = torch.optim.SGD(hooked.parameters(), lr=0.01, momentum=0.9)
+    comp = ActivationCompressor(ActivationCompressor.conv_layer_map(hooked), opt,
+                                ctl.ControllerConfig(W_default=1000, W_floor=1))
+    with comp.iteration():
+        torch.nn.functional.cross_entropy(hooked(x), y).backward()
+    grads = [p.grad.clone() for p in hooked.parameters()]
+    opt.step()
+    comp.after_step()
+    assert comp.records[-1].markers == 2  # max-pool and avg-pool outputs recomputed
+    for (n, _), g, q in zip(hooked.named_parameters(), grads, ref.parameters()):
+        assert torch.equal(g, q.grad), n
