@@ -12,15 +12,21 @@ Mirrors the reference's hook API and storage policy
 
 What is stored.  The reference stores every conv layer's output and
 recomputes the cheap layers after it (ReLU, max-pool) from it
-(training.py:264-299, 344-347).  Autograd saves, for a conv followed by
-(BatchNorm ->) (residual add ->) ReLU, the ReLU's output (ReLU backward and
-the next layer's backward both read it), so that is the stored activation
-of the conv: one slot per conv CALL, found by following the conv's output
-through parameter-free / normalisation modules and in-place ops up to the
-first ReLU (dataflow, not module order -- torchvision's Bottleneck calls
-one ReLU module three times, each call belongs to a different conv).
-Pooling outputs computed from a stored activation are MARKER slots:
-recomputed from the decompressed activation in backward.
+(training.py:264-299, 344-347).  One slot per conv CALL, found by following
+the conv's output through parameter-free / normalisation modules and
+in-place ops up to the first ReLU (dataflow, not module order --
+torchvision's Bottleneck calls one ReLU module three times, each call
+belongs to a different conv):
+* conv -> ReLU (or conv -> BN -> residual add -> ReLU): autograd saves the
+  ReLU's output (ReLU backward and the next layer's backward both read it):
+  that is the stored activation;
+* conv -> training-mode BatchNorm -> ReLU with nothing in between: the
+  stored activation is the conv output (BN's saved input, which would
+  otherwise stay raw), and the ReLU output is a cheap layer recomputed in
+  backward from the decompressed conv output with the forward pass's batch
+  statistics -- the reference's policy;
+* pooling outputs computed from a stored (or recomputed) activation are
+  MARKER slots: recomputed in backward.
 
 Consumer.  The reference's consumer of a conv's stored output is the next
 parameterised layer downstream (`_consumer_map`, training.py:154-166); its
@@ -133,7 +139,7 @@ class _Handle:
     activation to its slot: raw until the pending queue is flushed,
     compressed after.  Handles nobody promotes pass the tensor through."""
 
-    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref", "job")
+    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref", "job", "rec")
 
     def __init__(self, t, layer, eb):
         self.layer = layer
@@ -146,9 +152,55 @@ class _Handle:
         self.out = None
         self.shape = tuple(t.shape)
         self.job = None  # compress_begin batch while the compression is in flight
+        self.rec = None  # (recompute fn, source handle, marker slot): a cheap layer's output, recomputed
         # the tensor's identity: a key (pointer, version, shape, stride) is
         # only unique while the tensor lives -- freed memory is reused
         self.ref = weakref.ref(t)
+
+
+class _BnRelu:
+    """relu(batch_norm(x)) with the forward pass's batch statistics: the
+    saved output of the ReLU after a training-mode BatchNorm, recomputed in
+    backward from the decompressed conv output (reference recompute_cheap,
+    training.py:344-347)."""
+
+    __slots__ = ("scale", "shift")
+
+    def __init__(self, bn, mean, invstd):
+        import torch
+
+        with torch.no_grad():
+            scale = invstd.float()
+            if bn.weight is not None:
+                scale = scale * bn.weight.detach().float()
+            shift = -mean.float() * scale
+            if bn.bias is not None:
+                shift = shift + bn.bias.detach().float()
+        self.scale, self.shift = scale, shift
+
+    def __call__(self, x):
+        import torch
+
+        shape = (1, -1) + (1,) * (x.dim() - 2)
+        return torch.relu(torch.addcmul(self.shift.view(shape), x, self.scale.view(shape)))
+
+
+def _bn_batch_stats(bn, x, out):
+    """(mean, invstd) the training-mode BatchNorm `bn` normalised x with: the
+    ones its autograd node saved (cuDNN / native kernels), else recomputed."""
+    import torch
+
+    g = getattr(out, "grad_fn", None)
+    try:
+        mean, invstd = g._saved_result1, g._saved_result2
+        if mean is not None and invstd is not None and mean.numel() == x.shape[1] == invstd.numel():
+            return mean.detach(), invstd.detach()
+    except (AttributeError, RuntimeError):
+        pass
+    with torch.no_grad():
+        dims = [0] + list(range(2, x.dim()))
+        var, mean = torch.var_mean(x.detach().float(), dim=dims, unbiased=False)
+        return mean, torch.rsqrt(var + bn.eps)
 
 
 @dataclass
@@ -233,6 +285,8 @@ class ActivationCompressor:
         self._ctag: dict = {}        # tkey -> (slot, ref): a stored activation on its way to its consumer
         self._cheap: dict = {}
         self._markers: dict = {}
+        self._bnp: dict = {}         # tkey -> (slot, bn, conv-output ref, output version, fn, ref): a BN output on its way to the ReLU
+        self._slot_out: dict = {}    # slot -> weakref of its producer's output
         self._calls: dict = {}       # layer id -> calls this iteration
         self._await_consumer: list = []  # slots stored this iteration without a consumer yet
         self._pending: list[_Handle] = []  # compressions launched, not yet synchronised (oldest first)
@@ -335,6 +389,7 @@ class ActivationCompressor:
 
     def _leaf_hook(self, mod, inp, out):
         import torch
+        import torch.nn as nn
 
         if not torch.is_tensor(out):
             return
@@ -350,6 +405,7 @@ class ActivationCompressor:
                 self._store(slot, out)
             else:
                 self._ptag[_tkey(out)] = (slot, weakref.ref(out))
+                self._slot_out[slot] = weakref.ref(out)
             return
         if x is None:
             return
@@ -358,17 +414,63 @@ class ActivationCompressor:
         if pt is not None:
             if _is_relu(mod):
                 del self._ptag[k]
-                self._store(pt[0], out)
+                if not self._store_bn_relu(pt[0], mod, x, out):
+                    self._store(pt[0], out)
                 return
             if _passes_tags(mod):
                 self._ptag[_tkey(out)] = (pt[0], weakref.ref(out))
+                if (self.recompute_cheap and isinstance(mod, nn.modules.batchnorm._BatchNorm) and mod.training
+                        and self._is_producer_output(pt[0], x)):
+                    self._bnp[_tkey(out)] = (pt[0], mod, weakref.ref(x), out._version,
+                                             _BnRelu(mod, *_bn_batch_stats(mod, x, out)), weakref.ref(out))
         ct = self._live(self._ctag, k)
         if ct is not None and not _is_param_layer(mod) and _passes_tags(mod):
             self._ctag[_tkey(out)] = (ct[0], weakref.ref(out))
         if self.recompute_cheap and isinstance(mod, self._pools):
             src = self._live(self._handles, _key(x))
-            if src is not None and src.layer is not None:
+            if src is not None and (src.layer is not None or src.rec is not None):
                 self._cheap[_key(out)] = (type(mod).__name__.lower(), mod, src, weakref.ref(out))
+
+    def _is_producer_output(self, slot, x):
+        """x is the producer's own output (conv -> BN directly, nothing between)"""
+        return self._slot_out.get(slot) is not None and self._slot_out[slot]() is x
+
+    def _store_bn_relu(self, slot, relu, x, out):
+        """conv -> training-mode BatchNorm -> ReLU, the BN output untouched in
+        between (no residual add): the stored activation is the conv output
+        (BN's saved input -- stored instead of raw) and the ReLU output is a
+        cheap layer, recomputed in backward from the decompressed conv output
+        with the forward pass's batch statistics (reference MARKER slots,
+        training.py:295-296, 344-347).  False: not that pattern."""
+        bnp = self._live(self._bnp, _tkey(x))
+        if bnp is None or bnp[0] != slot:
+            return False
+        inplace = out is x
+        if x._version != bnp[3] + (1 if inplace else 0):
+            return False  # modified between the BN and the ReLU (e.g. a residual add)
+        conv_out = bnp[2]()
+        if conv_out is None:
+            return False
+        self._store(slot, conv_out)
+        src = self._live(self._handles, _key(conv_out))
+        if src is None or src.layer != slot:
+            return True  # not saved by the BN (eval-like use): only the conv output is stored
+        fn = bnp[4]
+        mslot = f"relu@{slot}"
+        self._ctag[_tkey(out)] = (slot, weakref.ref(out))  # the consumer search continues past the ReLU
+        h = self._live(self._handles, _key(out))
+        if h is not None and h.layer is None and h.rec is None:
+            # the ReLU saved its output while it ran: that handle recomputes
+            h.rec = (fn, src, mslot)
+            h.raw = None
+            src.packs += 1
+            self.store.put(mslot, ActivationStore.MARKER, None, 0)
+            if self._rec is not None:
+                self._rec.markers += 1
+        else:
+            # saved later (by the consumer): the pack makes the marker
+            self._cheap[_key(out)] = ("relu", fn, src, weakref.ref(out))
+        return True
 
     def _store(self, slot, out):
         """`out` is the stored activation of `slot` (saved by its op before
@@ -436,7 +538,8 @@ class ActivationCompressor:
             m.packs += 1
             return m
         cheap = self._live(self._cheap, k)
-        if cheap is not None and cheap[2].ref() is not None:
+        if cheap is not None and (cheap[2].ref() is not None or cheap[2].rec is not None):
+            # (a recomputed source holds no tensor of its own: valid while it recomputes)
             src = cheap[2]
             m = _Marker(f"{cheap[0]}@{src.layer}", cheap[1], src, t)
             src.packs += 1  # the recompute reads the predecessor once more
@@ -532,6 +635,22 @@ class ActivationCompressor:
             if h.unpacks >= h.packs:
                 h.out = None
             return out
+        if h.rec is not None:
+            # a cheap layer's output: recomputed once from its stored source
+            if h.out is None:
+                fn, src, mslot = h.rec
+                if src is None:
+                    raise LifecycleError(f"recomputed output {mslot!r} already released")
+                x = self._unpack(src)
+                with torch.no_grad():
+                    h.out = fn(x)
+                self.store.pop(mslot)
+                h.rec = (fn, None, mslot)
+            h.unpacks += 1
+            out = h.out
+            if h.unpacks >= h.packs:
+                h.out = None
+            return out
         if h.layer is None:
             return h.raw  # a saved tensor that is not a stored activation
         if h.out is None:
@@ -566,7 +685,8 @@ class ActivationCompressor:
 
     # ---- iteration protocol --------------------------------------------------
     def _reset_iteration_state(self):
-        for d in (self._act_layer, self._handles, self._ptag, self._ctag, self._cheap, self._markers, self._calls):
+        for d in (self._act_layer, self._handles, self._ptag, self._ctag, self._cheap, self._markers, self._calls,
+                  self._bnp, self._slot_out):
             d.clear()
         self._await_consumer = []
 

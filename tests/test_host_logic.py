@@ -150,7 +150,11 @@ def test_dataflow_slots_resnet50():
     assert cn["conv1"] == "layer1.0.conv1"  # through the stem max-pool
     assert cn["layer1.0.conv3"] == "layer1.1.conv1" and cn["layer1.2.conv3"] == "layer2.0.conv1"
     assert cn["layer2.0.conv1"] == "layer2.0.conv2" and cn["layer4.2.conv3"] == "fc"
-    assert r.markers == 1  # stem max-pool output, read by layer1.0.conv1 and downsample.0
+    # the ReLU after conv -> BN (stem, conv1 and conv2 of every block) is
+    # recomputed from the stored conv output; conv3's ReLU follows a residual
+    # add and stays stored; plus the stem max-pool (read by layer1.0.conv1
+    # and downsample.0)
+    assert r.markers == 1 + 2 * 16 + 1
 
 
 def test_dataflow_slots_vgg16_alexnet():
@@ -292,3 +296,51 @@ def test_marker_recompute_gives_identical_gradients():
     assert comp.records[-1].markers == 2  # max-pool and avg-pool outputs recomputed
     for (n, _), g, q in zip(hooked.named_parameters(), grads, ref.parameters()):
         assert torch.equal(g, q.grad), n
+
+
+def test_bn_relu_recompute_matches_plain_step():
+    """conv -> BatchNorm -> ReLU: the stored activation is the conv output
+    (BN's saved input) and the ReLU output is recomputed in backward with the
+    forward pass's batch statistics (training.py:344-347).
+    With raw storage (first interval) the step's gradients equal those of the
+    plain step up to the recompute's rounding; after a residual add the ReLU
+    output stays stored."""
+    torch = pytest.importorskip("torch")
+    import torch.nn as nn
+
+    class Net(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.c1, self.b1 = nn.Conv2d(3, 8, 3, padding=1), nn.BatchNorm2d(8)
+            self.c2, self.b2 = nn.Conv2d(8, 8, 3, padding=1), nn.BatchNorm2d(8)
+            self.relu = nn.ReLU(inplace=True)
+            self.pool = nn.MaxPool2d(2)
+            self.fc = nn.Linear(8 * 4 * 4, 4)
+
+        def forward(self, x):
+            x = self.pool(self.relu(self.b1(self.c1(x))))
+            y = self.b2(self.c2(x))
+            y += x  # residual: the ReLU after it keeps its stored output
+            return self.fc(torch.flatten(self.relu(y), 1))
+
+    x = torch.randn(4, 3, 8, 8, generator=torch.Generator().manual_seed(7))
+    y = torch.tensor([0, 1, 2, 3])
+    torch.manual_seed(1)
+    ref = Net()
+    torch.nn.functional.cross_entropy(ref(x), y).backward()
+    torch.manual_seed(1)
+    hooked = Net()
+    opt = torch.optim.SGD(hooked.parameters(), lr=0.01, momentum=0.9)
+    comp = ActivationCompressor(ActivationCompressor.conv_layer_map(hooked), opt,
+                                ctl.ControllerConfig(W_default=1000, W_floor=1))
+    with comp.iteration():
+        torch.nn.functional.cross_entropy(hooked(x), y).backward()
+    grads = [p.grad.clone() for p in hooked.parameters()]
+    opt.step()
+    comp.after_step()
+    r = comp.records[-1]
+    assert r.slots == ["c1", "c2"]
+    assert r.markers == 2  # relu@c1 and the max-pool after it
+    assert comp.store.current_bytes == 0
+    for (n, _), g, q in zip(hooked.named_parameters(), grads, ref.parameters()):
+        assert torch.allclose(g, q.grad, rtol=1e-4, atol=1e-6), n
