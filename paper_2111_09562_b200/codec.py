@@ -232,7 +232,7 @@ class CompressedActivation:
     __slots__ = (
         "dims", "precision", "params", "symbol_count", "payload_bits",
         "_h_outlier_indices", "_h_outlier_values", "_h_code_lengths", "_h_payload",
-        "_dev", "_live", "_n_outliers", "_rle_runs", "_desc_cache",
+        "_dev", "_live", "_n_outliers", "_rle_runs", "_desc_cache", "_ready",
     )
 
     def __init__(self, dims, precision, params, outlier_indices, outlier_values, symbol_count,
@@ -251,6 +251,7 @@ class CompressedActivation:
         self._n_outliers = len(self._h_outlier_indices)
         self._rle_runs = None
         self._desc_cache = None
+        self._ready = None
 
     # ---- device-resident construction (compress) ----
     @classmethod
@@ -270,7 +271,18 @@ class CompressedActivation:
         self._n_outliers = int(n_outliers)
         self._rle_runs = int(rle_runs)
         self._desc_cache = None
+        self._ready = None  # CUDA event: the device buffers are complete (compress_end(order=False))
         return self
+
+    def _wait_ready(self, stream):
+        """order `stream` after the work that fills the device buffers"""
+        if self._ready is not None:
+            stream.wait_event(self._ready)
+
+    def _host_ready(self):
+        """the device buffers are complete before a host read"""
+        if self._ready is not None:
+            self._ready.synchronize()
 
     @property
     def element_count(self) -> int:
@@ -299,18 +311,21 @@ class CompressedActivation:
     # ---- reference host fields (materialised lazily) ----
     @property
     def outlier_indices(self) -> np.ndarray:
+        self._host_ready()
         if self._h_outlier_indices is None:
             self._h_outlier_indices = self._dev["out_idx"].cpu().numpy().view(np.uint64).copy()
         return self._h_outlier_indices
 
     @property
     def outlier_values(self) -> np.ndarray:
+        self._host_ready()
         if self._h_outlier_values is None:
             self._h_outlier_values = self._dev["out_val"].cpu().numpy().copy()
         return self._h_outlier_values
 
     @property
     def code_lengths(self) -> np.ndarray:
+        self._host_ready()
         if self._h_code_lengths is None:
             canon = self._dev["canon"].cpu().numpy().astype(np.int64)
             counts = self._dev["len_counts"].cpu().numpy().astype(np.int64)
@@ -321,6 +336,7 @@ class CompressedActivation:
 
     @property
     def payload(self) -> bytes:
+        self._host_ready()
         if self._h_payload is None:
             nbytes = (self.payload_bits + 7) // 8
             self._h_payload = self._dev["payload"][:nbytes].cpu().numpy().tobytes()
@@ -438,6 +454,7 @@ class CompressedActivation:
         # once, straight into the blob
         nbytes = (self.payload_bits + 7) // 8
         pre = len(out)
+        self._host_ready()
         crc = crc32_device(self._dev["payload"], nbytes, zlib.crc32(out))
         blob = bytearray(pre + nbytes + 4)
         blob[:pre] = out
@@ -661,16 +678,21 @@ _FALLBACK_SEEN: set = set()
 class PendingCompress:
     """Launched, not yet synchronised compressions (compress_begin)."""
 
-    __slots__ = ("jobs", "main", "done")
+    __slots__ = ("jobs", "main", "done", "events")
 
     def __init__(self, jobs, main):
         self.jobs = jobs
         self.main = main
         self.done = False
+        self.events = [job[2].record_event() for job in jobs]  # each chain's end
+
+    def ready(self) -> bool:
+        """every compression of the batch has finished on the device (no wait)"""
+        return all(e.query() for e in self.events)
 
 
 def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
-                   own_scratch: bool = False) -> PendingCompress:
+                   own_scratch: bool = False, on_caller_stream: bool = False) -> PendingCompress:
     """Launch the compression of xs (each on its own side stream and context,
     slots slot_base .. slot_base+len-1) and return without synchronising;
     compress_end reads the plans and builds the containers.  The inputs are
@@ -679,7 +701,9 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
     context, used by compress_device / decompress_device) before compress_end.
     `own_scratch`: the symbol scratch (2-4 bytes per element) comes from
     torch's allocator per call and is released at compress_end, instead of
-    the context's persistent buffer (memory-bound callers such as the hooks)."""
+    the context's persistent buffer (memory-bound callers such as the hooks).
+    `on_caller_stream`: the launches go on the caller's current stream (in
+    order with its other work) instead of side streams."""
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
         params = [params] * len(xs)
@@ -690,7 +714,7 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
     dev_index = xs[0].device.index if xs else torch.cuda.current_device()
     main = torch.cuda.current_stream()
     L = _lib.lib()
-    streams = _stream_pool(dev_index, slot_base + len(xs))[slot_base:]
+    streams = [main] * len(xs) if on_caller_stream else _stream_pool(dev_index, slot_base + len(xs))[slot_base:]
     jobs = []
     for j, (x, p) in enumerate(zip(xs, params)):
         s = streams[j]
@@ -717,7 +741,8 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         cp, oc = capped.data_ptr(), dev.offsets
         # recorded after this tensor's allocations: its side stream is ordered
         # after all caller-stream work that used the blocks the allocator reused
-        s.wait_event(main.record_event())
+        if s is not main:
+            s.wait_event(main.record_event())
         if ready is not None:
             s.wait_event(ready[j])
         symbuf = None
@@ -746,10 +771,14 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
     return PendingCompress(jobs, main)
 
 
-def compress_end(pend: PendingCompress, compact: bool = False):
+def compress_end(pend: PendingCompress, compact: bool = False, order: bool = True):
     """Synchronise a compress_begin batch: [(CompressedActivation, report)]
     in input order.  A tensor whose plan overflowed a cap is redone through
-    the two-phase path (its input is still held)."""
+    the two-phase path (its input is still held).  With order=True the
+    caller's stream is ordered after the compressions; with order=False it
+    is not (training keeps computing): each container carries an event its
+    readers wait for instead (decompress_* on the device, host reads on the
+    host)."""
     if pend.done:
         raise ParameterError("compress_end called twice on the same batch")
     pend.done = True
@@ -786,9 +815,12 @@ def compress_end(pend: PendingCompress, compact: bool = False):
             s.wait_stream(pend.main)
             with torch.cuda.stream(s):
                 c, rep = compress_device(x, p)
+        if not order:
+            c._ready = s.record_event()
         out.append((c, rep))
-    for job in pend.jobs:
-        pend.main.wait_stream(job[2])
+    if order:
+        for job in pend.jobs:
+            pend.main.wait_stream(job[2])
     pend.jobs = []
     return out
 
@@ -828,6 +860,7 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
     if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
         raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
     d = c._desc()
+    c._wait_ready(s)
     if not count_nonzero:
         code |= _lib.ACTC_DEC_NO_NONZERO
     _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
@@ -884,6 +917,7 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
                 ready = main.record_event()  # ... which the side stream must follow
             s = streams[slot]
             s.wait_event(ready)
+            c._wait_ready(s)
             ctx = _lib.context_for(dev_index, slot)
             dt = _lib.ACTC_DTYPE_F32 if out.dtype == f32 else _lib.ACTC_DTYPE_F64
             if not d.table_dev:

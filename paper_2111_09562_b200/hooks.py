@@ -46,10 +46,12 @@ Policy, as in the reference:
 * layers whose eb is None (skip set) stay raw.
 
 Packing is asynchronous: a stored activation's compression is launched on a
-side stream as soon as it exists (`compress_begin`, no host sync); the
-oldest in-flight compression is finished (`compress_end`: plan read,
-exact-size container, original released) once more than `batch_flush` are
-in flight.  Decode faults of the (unsynchronised) backward decompressions
+side stream as soon as it exists (`compress_begin`, no host sync); a
+compression is finished (`compress_end`: plan read, exact-size container,
+original released) as soon as its chain is done, or -- waiting -- once more
+than `batch_flush` are in flight.  The training stream is never ordered
+after a compression: the container's decompression in backward waits for
+its completion event instead.  Decode faults of the (unsynchronised) backward decompressions
 are collected at the end of every iteration and raised as FormatError at
 the next iteration's start (one event wait).
 Under data parallelism the statistics are averaged across ranks before
@@ -258,7 +260,7 @@ class ActivationCompressor:
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 1, dist_group=None,
                  sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
-                 recompute_cheap: bool = True):
+                 recompute_cheap: bool = True, codec_on_compute_stream: bool = False):
         import torch.nn as nn
 
         self.layers = dict(layers)
@@ -273,6 +275,9 @@ class ActivationCompressor:
         self.dist_group = dist_group
         self.sync_stats = sync_stats
         self.recompute_cheap = recompute_cheap
+        # compressions in order on the training stream (no SM contention with
+        # the convolutions) instead of side streams
+        self.codec_on_compute_stream = codec_on_compute_stream
         self.plan = None
         self.it = 0
         self.next_collection = self.controller.W
@@ -538,8 +543,10 @@ class ActivationCompressor:
             m.packs += 1
             return m
         cheap = self._live(self._cheap, k)
-        if cheap is not None and (cheap[2].ref() is not None or cheap[2].rec is not None):
-            # (a recomputed source holds no tensor of its own: valid while it recomputes)
+        if cheap is not None and (cheap[2].layer is not None or cheap[2].rec is not None):
+            # (the source handle -- a stored or recomputed activation of this
+            # iteration -- is valid whether or not its tensor object is
+            # still alive: a finished compression has released it)
             src = cheap[2]
             m = _Marker(f"{cheap[0]}@{src.layer}", cheap[1], src, t)
             src.packs += 1  # the recompute reads the predecessor once more
@@ -582,10 +589,12 @@ class ActivationCompressor:
         # slots 1.. (never the thread's main context, which the decoders use
         # in backward while the last compressions may still be in flight)
         h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(slot)],
-                               own_scratch=True)
+                               own_scratch=True, on_caller_stream=self.codec_on_compute_stream)
         self._slot = (self._slot + 1) % (self.batch_flush + 1)
         self._pending.append(h)
-        while len(self._pending) > self.batch_flush:
+        # finish what is already done without waiting; wait only when more
+        # than batch_flush are in flight (their contexts are reused next)
+        while self._pending and (len(self._pending) > self.batch_flush or self._pending[0].job.ready()):
             self._finish(self._pending.pop(0))
 
     def capture_next_iteration(self, slots=None):
@@ -597,7 +606,9 @@ class ActivationCompressor:
         self.captured = {}
 
     def _finish(self, h):
-        (c, rep), = compress_end(h.job, compact=True)
+        # order=False: the training stream never waits for a compression;
+        # the container's readers (the backward decompression) do
+        (c, rep), = compress_end(h.job, compact=True, order=False)
         h.job = None
         if self._capture is True or (self._capture and h.layer in self._capture):
             self.captured[h.layer] = (h.raw.detach().cpu().numpy(), c, h.eb)  # shaped: CMTZ records the dims
