@@ -12,35 +12,6 @@ namespace {
 
 constexpr uint32_t kSent = 0xFFFFFFFFu;  // symbol past the end of the stream
 
-template <typename SymT>
-__device__ __forceinline__ void lb_load(const SymT *__restrict__ sym, uint64_t base, uint64_t n,
-                                        uint32_t (&s)[K3L_EPT]) {
-  if (base + K3L_EPT <= n) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(sym + base);
-    if (sizeof(SymT) == 2) {
-#pragma unroll
-      for (int j = 0; j < K3L_EPT / 8; j++) {
-        const uint4 v = __ldcs(p + j);  // streaming: the symbol buffer is read once
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          s[8 * j + 2 * k] = w4[k] & 0xFFFFu;
-          s[8 * j + 2 * k + 1] = w4[k] >> 16;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < K3L_EPT / 4; j++) {
-        const uint4 v = __ldcs(p + j);
-        s[4 * j] = v.x; s[4 * j + 1] = v.y; s[4 * j + 2] = v.z; s[4 * j + 3] = v.w;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < K3L_EPT; j++) s[j] = (base + j < n) ? (uint32_t)sym[base + j] : kSent;
-  }
-}
-
 // a lane's K3L_EPT symbols, 16-bit ones kept two per register; cnt < K3L_EPT
 // only in the stream's last segment (symbols past the end read as 0 and are
 // masked by cnt)
@@ -185,31 +156,34 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
   const uint64_t nseg = (a.n + K3L_SEG - 1) / K3L_SEG;
   const uint64_t s0 = (uint64_t)blockIdx.x * a.spc, s1 = min(nseg, s0 + a.spc);
   unsigned long long tb = 0, tz = 0;
+  // the next segment's symbols are loaded while this one is counted
+  SymBuf<SymT> nxt;
+  if (s0 + warp < s1) nxt.load(sym, (s0 + warp) * K3L_SEG + (uint64_t)lane * K3L_EPT, a.n);
   for (uint64_t seg = s0 + warp; seg < s1; seg += K3L_THREADS / 32) {
-    const uint64_t base = seg * K3L_SEG + (uint64_t)lane * K3L_EPT;
-    uint32_t s[K3L_EPT];
-    lb_load(sym, base, a.n, s);
+    const SymBuf<SymT> sb = nxt;
+    if (seg + K3L_THREADS / 32 < s1) nxt.load(sym, (seg + K3L_THREADS / 32) * K3L_SEG + (uint64_t)lane * K3L_EPT, a.n);
     uint32_t bits = 0, nz = 0, mx = 0;
-    if (smem_tab && __all_sync(0xffffffffu, base + K3L_EPT <= a.n)) {
+    if (smem_tab && __all_sync(0xffffffffu, sb.cnt == (uint32_t)K3L_EPT)) {
       // full segment, byte table in shared memory: one LDS.U8 per symbol
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        const uint32_t l = k3c_ldsb(l8_rel + s[j]);
+        const uint32_t l = k3c_ldsb(l8_rel + sb.get(j));
         bits += l;
         mx = max(mx, l);
       }
       if (a.k) {
 #pragma unroll
-        for (int j = 0; j < K3L_EPT; j++) nz += s[j] == 0;
+        for (int j = 0; j < K3L_EPT; j++) nz += sb.get(j) == 0;
       }
     } else {
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
-        if (s[j] != kSent) {
-          const uint32_t l = smem_tab ? (uint32_t)l8[s[j] - a.lo] : (uint32_t)(__ldg(&a.ctab[s[j]]) & 63);
+        if ((uint32_t)j < sb.cnt) {
+          const uint32_t sj = sb.get(j);
+          const uint32_t l = smem_tab ? (uint32_t)l8[sj - a.lo] : (uint32_t)(__ldg(&a.ctab[sj]) & 63);
           bits += l;
           mx = max(mx, l);
-          nz += s[j] == 0;
+          nz += sj == 0;
         }
       }
     }
