@@ -184,6 +184,7 @@ struct actc_ctx {
   // decode-table output for the next async compression (actc_ctx_set_table_out)
   void *table_out = nullptr;
   int smem_optin = 0;  // dynamic shared memory a CTA may opt in to
+  int k4l_dyn_max = 0; // ... for the K4L decoders (opt-in limit minus their static shared memory)
 };
 
 namespace {
@@ -497,10 +498,13 @@ int actc_ctx_create(int device, actc_ctx **out) {
                        (const void *)k3_seg_pack<uint32_t>,     (const void *)k3_seg_count<uint16_t>,
                        (const void *)k3_seg_count<uint32_t>,    (const void *)k1_quant_lorenzo_hist<uint16_t>,
                        (const void *)k1_quant_lorenzo_hist<uint32_t>, (const void *)k_hist_u32};
-  for (const void *f : big) {
+  c->k4l_dyn_max = optin;
+  for (int i = 0; i < (int)(sizeof(big) / sizeof(big[0])); i++) {
+    const void *f = big[i];
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, f));
     CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    if (i < 9) c->k4l_dyn_max = std::min(c->k4l_dyn_max, optin - (int)fa.sharedSizeBytes);  // the K4L variants
   }
   // occupancy-derived persistent grid sizes
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, (size_t)K1_WIN * 4);
@@ -931,6 +935,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.chunk_lat = (const long long *)S.chunk_lat_dev;
   a.live = S.live_symbols;
   a.mcount = nullptr;
+  a.cd_lim = 0;
   KT(ACTC_KIND_DECODE);
   if (lane_dec) {
     // K4L: one CTA per SM (persistent over 32-chunk warp tiles), as many
@@ -954,7 +959,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     // one CTA per SM; a stream with fewer 32-chunk tiles than SMs x warps
     // gets narrower CTAs (every SM busy, and room for a second decoder)
     const uint64_t ntl = cdiv(nchunks, 32);
-    const int wmax = k4l_max_warps(S.live_symbols, gcanon, (size_t)c->smem_optin);
+    const int wmax = k4l_max_warps(gcanon ? 0u : S.live_symbols, (size_t)c->k4l_dyn_max);
     if (wmax < 1) return set_err(ACTC_EPARAM, "decode tables exceed shared memory");
     // every warp runs the same number of 32-chunk tiles: the fewest passes
     // the shared memory allows, then the fewest warps per SM that still
@@ -963,7 +968,15 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     const uint64_t passes = cdiv(ntl, (uint64_t)c->num_sms * (uint64_t)wmax);
     const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wmax, cdiv(ntl, (uint64_t)c->num_sms * passes)));
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, warps), (uint64_t)c->num_sms));
-    const size_t smem = k4l_smem_bytes(S.live_symbols, gcanon, warps);
+    // wide alphabets: the deltas of as many leading (most frequent) canonical
+    // indices as the shared memory left over holds, the rest from the global table
+    a.cd_lim = 0;
+    if (gcanon && sw16) {
+      const size_t used = k4l_smem_bytes(0, warps);
+      const size_t room = (size_t)c->k4l_dyn_max > used ? (size_t)c->k4l_dyn_max - used : 0;
+      a.cd_lim = (uint32_t)std::min<size_t>(S.live_symbols, (room / 2) & ~(size_t)7);
+    }
+    const size_t smem = k4l_smem_bytes(gcanon ? a.cd_lim : S.live_symbols, warps);
     // full tiles leave through TMA stores: the output as [n / ACTC_CHUNK][ACTC_CHUNK]
     CUtensorMap tm;
     int rc2;

@@ -321,9 +321,12 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
       }
       const int dd = (int)e >> 16;
       if (GCANON) {
-        int g = 0;
-        if (!dir) g = (int)__ldg(a.canon + ci) - radius;
-        dl[j] = dir ? dd : g;
+        // the leading (most frequent) canonical indices from shared memory,
+        // the tail of a wide alphabet from the global table
+        const bool sm = ci < a.cd_lim;
+        int g = k4l_lds_s16_if(cx.cd_s + 2u * ci, dd, !dir && sm);
+        if (!dir && !sm) g = (int)__ldg(a.canon + ci) - radius;
+        dl[j] = g;
       } else {
         dl[j] = k4l_lds_s16_if(cx.cd_s + 2u * ci, dd, !dir);
       }
@@ -424,10 +427,11 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a, const
   for (int i = tid; i < kLutSize / 4; i += blockDim.x)
     reinterpret_cast<uint4 *>(t1)[i] = __ldg(reinterpret_cast<const uint4 *>(a.lut) + i);
   const int radius = (int)a.radius;
-  if (!GCANON) {
-    // canonical deltas (symbol - radius; the outlier marker is -radius)
+  {
+    // canonical deltas (symbol - radius; the outlier marker is -radius) of
+    // every code, or (wide alphabets) of the leading cd_lim codes
     // (four 16-B loads in flight per thread)
-    const uint32_t live = a.live;
+    const uint32_t live = GCANON ? a.cd_lim : a.live;
     const uint32_t step = 4 * blockDim.x;
     for (uint32_t i0 = 4 * tid; i0 < live; i0 += 4 * step) {
       uint4 c[4];
@@ -571,17 +575,19 @@ __global__ void __launch_bounds__(K4L_THREADS, 1) k4l_decode(DecodeArgs a, const
   }
 }
 
-size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps) {
+// dynamic shared memory of a launch with `warps` warps and the deltas of
+// `cd_entries` canonical indices
+size_t k4l_smem_bytes(uint32_t cd_entries, int warps) {
   return 1024 + (size_t)warps * (kOutBytesPerWarp + kRingBytesPerWarp) + (size_t)kLutSize * 4 +
-         (gcanon ? 0 : (((size_t)live * 2 + 15) & ~(size_t)15));
+         (((size_t)cd_entries * 2 + 15) & ~(size_t)15);
 }
-
-// warps per CTA: as many as the shared memory holds (up to K4L_THREADS / 32)
-int k4l_max_warps(uint32_t live, bool gcanon, size_t smem_optin) {
-  const size_t fixed = k4l_smem_bytes(live, gcanon, 0) + sizeof(K4LShared) + 64;
-  if (smem_optin <= fixed) return 0;
+// warps per CTA: as many as `dyn_max` bytes of dynamic shared memory hold
+// (up to K4L_THREADS / 32)
+int k4l_max_warps(uint32_t cd_entries, size_t dyn_max) {
+  const size_t fixed = k4l_smem_bytes(cd_entries, 0);
+  if (dyn_max <= fixed) return 0;
   const size_t per = kOutBytesPerWarp + kRingBytesPerWarp;
-  return (int)std::min<size_t>((size_t)(K4L_THREADS / 32), (smem_optin - fixed) / per);
+  return (int)std::min<size_t>((size_t)(K4L_THREADS / 32), (dyn_max - fixed) / per);
 }
 
 template __global__ void k4l_decode<0, false, false>(DecodeArgs, const __grid_constant__ CUtensorMap);

@@ -272,6 +272,7 @@ struct DecodeArgs {
   unsigned long long *markers;
   unsigned *status;
   unsigned long long *mcount;  // K4L: markers of this launch (null: no stored outliers), self-resetting
+  uint32_t cd_lim;             // K4L wide alphabets: leading canonical indices whose deltas are in shared memory
 };
 // a decode fault: the call's status word and, right after it, the context's
 // sticky word (collected by actc_ctx_take_status at the caller's next sync --
@@ -310,8 +311,8 @@ __global__ void k4l_build_table(const uint32_t *__restrict__ len_counts, const u
 // box 32 rows x 64 B, 64-B swizzle (TMA stores of full tiles).
 template <int MODE, bool GCANON, bool NZ>
 __global__ void k4l_decode(DecodeArgs a, const __grid_constant__ CUtensorMap tm);
-size_t k4l_smem_bytes(uint32_t live, bool gcanon, int warps);
-int k4l_max_warps(uint32_t live, bool gcanon, size_t smem_optin);
+size_t k4l_smem_bytes(uint32_t cd_entries, int warps);
+int k4l_max_warps(uint32_t cd_entries, size_t dyn_max);
 __global__ void k_excl_scan_u64(const unsigned long long *__restrict__ in, uint64_t m,
                                 unsigned long long *__restrict__ out, unsigned long long *__restrict__ total);
 
