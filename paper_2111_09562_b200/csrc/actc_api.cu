@@ -938,10 +938,23 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
   a.cd_lim = 0;
   KT(ACTC_KIND_DECODE);
   if (lane_dec) {
-    // K4L: one CTA per SM (persistent over 32-chunk warp tiles), as many
-    // warps as the shared memory holds; canonical deltas in shared memory
-    // for 16-bit symbols up to K4L_SMEM_LIVE live codes
-    const bool gcanon = !sw16 || S.live_symbols > K4L_SMEM_LIVE;
+    // K4L: one CTA per SM (persistent over 32-chunk warp tiles).  Warps
+    // first: every warp runs the same number of 32-chunk tiles -- the fewest
+    // passes the shared memory allows without a delta table, then the fewest
+    // warps per SM that still finish in that many passes (a partial last pass
+    // on some SMs would leave the others idle).  The canonical deltas (16-bit
+    // symbols) then take the shared memory left: all of them, or the leading
+    // (most frequent) canonical indices with the tail from the global table.
+    const uint64_t ntl = cdiv(nchunks, 32);
+    const int wmax = k4l_max_warps(0u, (size_t)c->k4l_dyn_max);
+    if (wmax < 1) return set_err(ACTC_EPARAM, "decode tables exceed shared memory");
+    const uint64_t passes = cdiv(ntl, (uint64_t)c->num_sms * (uint64_t)wmax);
+    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wmax, cdiv(ntl, (uint64_t)c->num_sms * passes)));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, warps), (uint64_t)c->num_sms));
+    const size_t used = k4l_smem_bytes(0, warps);
+    const size_t room = (size_t)c->k4l_dyn_max > used ? (size_t)c->k4l_dyn_max - used : 0;
+    a.cd_lim = sw16 ? (uint32_t)std::min<size_t>(S.live_symbols, (room / 2) & ~(size_t)7) : 0u;
+    const bool gcanon = a.cd_lim < S.live_symbols;
     if (mode != 2 && S.n_outliers) {
       a.ticket = (unsigned *)((unsigned long long *)c->misc.p + M_K4LTICKET);
       a.mcount = (unsigned long long *)c->misc.p + M_K4LMCOUNT;
@@ -956,27 +969,7 @@ static int launch_decode(actc_ctx *c, const actc_stream_t *st_in, void *out, int
     else
       f = gcanon ? (nz ? (const void *)k4l_decode<0, true, true> : (const void *)k4l_decode<0, true, false>)
                  : (nz ? (const void *)k4l_decode<0, false, true> : (const void *)k4l_decode<0, false, false>);
-    // one CTA per SM; a stream with fewer 32-chunk tiles than SMs x warps
-    // gets narrower CTAs (every SM busy, and room for a second decoder)
-    const uint64_t ntl = cdiv(nchunks, 32);
-    const int wmax = k4l_max_warps(gcanon ? 0u : S.live_symbols, (size_t)c->k4l_dyn_max);
-    if (wmax < 1) return set_err(ACTC_EPARAM, "decode tables exceed shared memory");
-    // every warp runs the same number of 32-chunk tiles: the fewest passes
-    // the shared memory allows, then the fewest warps per SM that still
-    // finish in that many passes (a partial last pass on some SMs would leave
-    // the others idle)
-    const uint64_t passes = cdiv(ntl, (uint64_t)c->num_sms * (uint64_t)wmax);
-    const int warps = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)wmax, cdiv(ntl, (uint64_t)c->num_sms * passes)));
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ntl, warps), (uint64_t)c->num_sms));
-    // wide alphabets: the deltas of as many leading (most frequent) canonical
-    // indices as the shared memory left over holds, the rest from the global table
-    a.cd_lim = 0;
-    if (gcanon && sw16) {
-      const size_t used = k4l_smem_bytes(0, warps);
-      const size_t room = (size_t)c->k4l_dyn_max > used ? (size_t)c->k4l_dyn_max - used : 0;
-      a.cd_lim = (uint32_t)std::min<size_t>(S.live_symbols, (room / 2) & ~(size_t)7);
-    }
-    const size_t smem = k4l_smem_bytes(gcanon ? a.cd_lim : S.live_symbols, warps);
+    const size_t smem = k4l_smem_bytes(a.cd_lim, warps);
     // full tiles leave through TMA stores: the output as [n / ACTC_CHUNK][ACTC_CHUNK]
     CUtensorMap tm;
     int rc2;

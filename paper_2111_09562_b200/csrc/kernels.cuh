@@ -30,9 +30,9 @@ constexpr int K3L_WORDS = (K3L_SEG * K3_SHORT_MAXLEN + 31) / 32 + 2;      // pac
 constexpr int K4_THREADS = 128;
 // K4 (warp variant, indexed streams): one warp per 32 chunks
 // K4L (indexed streams): one CTA of up to 768 threads per SM, lane per chunk; the
-// canonical deltas stay in shared memory up to K4L_SMEM_LIVE live symbols
+// canonical deltas in the shared memory the warps leave (all of them, or the
+// leading canonical indices of a wide alphabet)
 constexpr int K4L_THREADS = 768;  // at most; small streams launch fewer warps per CTA
-constexpr uint32_t K4L_SMEM_LIVE = 49152;
 constexpr int K4_TILE = K4_THREADS * ACTC_CHUNK;
 
 // lookback status for the encoder (per K3 tile)
