@@ -15,16 +15,19 @@
 //   window W     two payload words from the lane's ring    2 LDS (conflict-free)
 //   entry e      T1[W >> 20] (4 B)                         1 LDS (random banks)
 //   advance      pos += e                                  IADD (len in e's low bits)
-//   delta        e >> 16 for a prefix holding one code (direct), else the
-//                canonical delta table at ((e >> 16) + (W >> (32 - len))) mod 2^16
-//                                                          predicated LDS.S16
+//   delta        the int16 canonical delta at
+//                ((e >> 16) + (W >> (32 - len))) mod 2^16     LDS.S16
 //   value        P += delta; fp32(fp64(P) * 2eb)           IADD, I2F, DMUL, F2F
 //   store        16 B per 4 values into a swizzled box     STS.128
 //
 // T1 entry (kernels.cuh, k4l_table_rows): bits 0-4 the code length (0: slow
-// path), bit 15 "direct", bits 16-31 the payload.  `pos` holds the chunk's
-// bit position in its low 15 bits (a chunk spans < 2^13 bits), so `pos += e`
-// advances it by len and lets the rest of e spill into bits >= 15.
+// path), bits 16-31 (base[len] - first[len]) mod 2^16 (or, slow path, the
+// shortest length a code under the prefix can have).  `pos` holds the
+// chunk's bit position in its low 15 bits (a chunk spans < 2^13 bits), so
+// `pos += e` advances it by len and lets the rest of e spill into bits >= 15.
+// Wide alphabets keep the deltas of their leading canonical indices in
+// shared memory (the shared memory the warps leave) and read the tail from
+// the global canonical table.
 //
 // Payload staging: each lane streams its own chunk through a 32-word ring in
 // shared memory, layout [slot][lane] (a warp's ring reads are conflict-free),
@@ -108,6 +111,11 @@ __device__ __forceinline__ uint32_t k4l_lds(uint32_t addr) {
 __device__ __forceinline__ uint32_t k4l_lds_t(uint32_t addr) {
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int k4l_lds_s16(uint32_t addr) {
+  int v;
+  asm("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ int k4l_lds_s16_if(uint32_t addr, int v, bool on) {
@@ -305,31 +313,28 @@ __device__ __forceinline__ void k4l_tile(const DecodeArgs &a, const K4LShared &s
       const uint32_t W = rg.window(L.pos);
       uint32_t e = k4l_lds_t(cx.t1_s + ((W >> 20) << 2));
       const bool in = FULL || (uint32_t)(r * R + j) < cnt;
-      if (!in) e = 0x8000u;  // past the chunk: direct delta 0, no advance
+      if (!in) e = 0x8000u;  // past the chunk: no advance in the position's low 15 bits, never the slow path
       uint32_t ci;
-      bool dir;
       if ((e & 31u) == 0u && in) {
         const uint2 rs = k4l_resolve(sh, a.payload, cx.nwords, a.live, abs0 + (L.pos & kPosMask), W, e >> 16);
         bad |= (rs.y >> 31) != 0u;
         L.pos += rs.y & 0x7FFFFFFFu;
-        ci = rs.x;  // indirect, index known
-        dir = false;
+        ci = rs.x;
       } else {
         L.pos += e;
         ci = ((e >> 16) + __funnelshift_l(W, 0u, e)) & 0xFFFFu;  // W >> (32 - len)
-        dir = (e & 0x8000u) != 0u;
       }
-      const int dd = (int)e >> 16;
       if (GCANON) {
         // the leading (most frequent) canonical indices from shared memory,
         // the tail of a wide alphabet from the global table
         const bool sm = ci < a.cd_lim;
-        int g = k4l_lds_s16_if(cx.cd_s + 2u * ci, dd, !dir && sm);
-        if (!dir && !sm) g = (int)__ldg(a.canon + ci) - radius;
+        int g = k4l_lds_s16_if(cx.cd_s + 2u * ci, 0, sm);
+        if (!sm) g = (int)__ldg(a.canon + ci) - radius;
         dl[j] = g;
       } else {
-        dl[j] = k4l_lds_s16_if(cx.cd_s + 2u * ci, dd, !dir);
+        dl[j] = k4l_lds_s16(cx.cd_s + 2u * ci);
       }
+      if (!in) dl[j] = 0;
     }
     // phase B: the lattice running sum and the reconstruction.  Outlier
     // markers only occur in streams with outliers (not NARROW); a round

@@ -288,10 +288,7 @@ template <int MODE, int SW>
 __global__ void k4_decode(DecodeArgs a);
 // K4L decode table (ACTC_TABLE_BYTES): T1[p] (4 bytes) for every 12-bit
 // prefix p of the left-aligned 32-bit window, then two header words.
-// Entry: bits 0-4 the code length len (0: slow path), bit 15 "direct", bits
-// 16-31 the payload:
-//  * one code under p (len <= 12) whose Lorenzo delta (symbol - radius) fits
-//    int16: direct, payload = that delta;
+// Entry: bits 0-4 the code length len (0: slow path), bits 16-31 the payload:
 //  * every code under p of one length len <= 31, canonical indices < 2^16:
 //    payload = (base[len] - first[len]) mod 2^16 -- the canonical index of
 //    the code under W is (payload + (W >> (32 - len))) mod 2^16;
@@ -501,17 +498,9 @@ __device__ __forceinline__ void k4l_table_rows(const uint32_t *__restrict__ len_
     }
     bool done = false;
     if (l0 && l0 == l1 && l0 <= 31) {
-      // every code under p has length l0: canonical indices ci0 .. ci1
-      const uint32_t ci0 = s_base[l0] + (uint32_t)((w0 >> (32 - l0)) - s_first[l0]);
+      // every code under p has length l0: canonical indices up to ci1
       const uint32_t ci1 = s_base[l0] + (uint32_t)((w1 >> (32 - l0)) - s_first[l0]);
-      if (ci0 == ci1) {
-        const int d = (int)canon[ci0] - (int)radius;
-        if (d >= -32768 && d <= 32767) {
-          e = ((uint32_t)d << 16) | 0x8000u | (uint32_t)l0;
-          done = true;
-        }
-      }
-      if (!done && ci1 < 65536u) {
+      if (ci1 < 65536u) {
         e = ((s_base[l0] - (uint32_t)s_first[l0]) << 16) | (uint32_t)l0;
         done = true;
       }
