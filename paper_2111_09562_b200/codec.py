@@ -16,6 +16,7 @@ hooks (fp32 output, no host round trip).
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import math
 import struct
@@ -673,6 +674,9 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
 # symbol-level fallback in an earlier async compression: they queue the
 # fallback behind it; all others skip that launch (ACTC_ASYNC_NO_FALLBACK)
 _FALLBACK_SEEN: set = set()
+# the last redos of compress_end (n, status, max_len, n_outliers, k_cap,
+# payload_bits, cap_bits): why a launch overflowed a cap
+REDOS: collections.deque = collections.deque(maxlen=64)
 
 
 class PendingCompress:
@@ -692,7 +696,8 @@ class PendingCompress:
 
 
 def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
-                   own_scratch: bool = False, on_caller_stream: bool = False) -> PendingCompress:
+                   own_scratch: bool = False, on_caller_stream: bool = False,
+                   outlier_hints=None) -> PendingCompress:
     """Launch the compression of xs (each on its own side stream and context,
     slots slot_base .. slot_base+len-1) and return without synchronising;
     compress_end reads the plans and builds the containers.  The inputs are
@@ -703,7 +708,12 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
     torch's allocator per call and is released at compress_end, instead of
     the context's persistent buffer (memory-bound callers such as the hooks).
     `on_caller_stream`: the launches go on the caller's current stream (in
-    order with its other work) instead of side streams."""
+    order with its other work) instead of side streams.
+    `outlier_hints` (optional, per tensor: expected outlier count or None)
+    raises the outlier cap (default max(4096, n/64)) to 4x the hint + n/64
+    -- small error bounds can put several percent of the elements outside
+    the quantization radius, and a training activation's tail can grow
+    several-fold in one step; an overflow is redone exactly."""
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
         params = [params] * len(xs)
@@ -729,6 +739,8 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
             cap_bits = min(cap_bits, int(bit_hints[j] * 1.25) + 4096)
         cap = _payload_buffer_bytes(cap_bits)
         k_cap = max(4096, n // 64)
+        if outlier_hints is not None and outlier_hints[j]:
+            k_cap = min(n, max(k_cap, 4 * int(outlier_hints[j]) + n // 64))
         dev = _DevBufs()
         # fixed-size arrays, and the capped (data-dependent) ones apart so
         # `compact` can replace the latter by exact-size copies
@@ -804,6 +816,8 @@ def compress_end(pend: PendingCompress, compact: bool = False, order: bool = Tru
             c, rep = _container(n, p, dims, plan, dev)
             c._desc()
         else:
+            REDOS.append((n, int(plan.status), int(plan.max_len), int(plan.n_outliers), k_cap,
+                          int(plan.payload_bits), 8 * (cap - 32)))
             if plan.status == _lib.ACTC_EAGAIN:
                 _FALLBACK_SEEN.add((n, int(p.radius)))  # next time: queue the fallback codebook
             else:

@@ -299,7 +299,7 @@ class ActivationCompressor:
         self._collecting = False
         self._R: dict[str, float] = {}
         self._lbar: dict[str, float] = {}
-        self._bits: dict[str, int] = {}
+        self._bits: dict[str, tuple] = {}
         self._batch = None
         self._rec = None
         self._status = None          # decode-fault collection of the previous iteration
@@ -586,9 +586,10 @@ class ActivationCompressor:
         # once more than `batch_flush` are in flight, so at most that many
         # raw activations outlive their compression
         params = CodecParams(eb=eb, radius=self.radius, preserve_zeros=self.preserve_zeros)
+        hb, ho = self._hint(slot, eb)
         # slots 1.. (never the thread's main context, which the decoders use
         # in backward while the last compressions may still be in flight)
-        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[self._bits.get(slot)],
+        h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[hb], outlier_hints=[ho],
                                own_scratch=True, on_caller_stream=self.codec_on_compute_stream)
         self._slot = (self._slot + 1) % (self.batch_flush + 1)
         self._pending.append(h)
@@ -596,6 +597,22 @@ class ActivationCompressor:
         # than batch_flush are in flight (their contexts are reused next)
         while self._pending and (len(self._pending) > self.batch_flush or self._pending[0].job.ready()):
             self._finish(self._pending.pop(0))
+
+    def _hint(self, slot, eb):
+        """Cap hints (payload bits, outlier count) for `slot` from its last
+        compression.  The payload hint only holds at the same error bound: a
+        new plan changes the eb and with it the payload size (a smaller eb
+        can need far more than 1.25x the old bits), and an overflowing cap
+        means a synchronous re-compression, so a new eb starts from the safe
+        n*ceil(log2 L) cap.  The outlier count is scaled by the eb ratio
+        when the eb shrank (the tail beyond the radius grows)."""
+        prev = self._bits.get(slot)
+        if prev is None:
+            return None, None
+        peb, bits, nout = prev
+        if peb == eb:
+            return bits, nout
+        return None, int(nout * max(1.0, peb / eb)) if nout else None
 
     def capture_next_iteration(self, slots=None):
         """Keep, for the next iteration, a host copy of every compressed
@@ -613,7 +630,7 @@ class ActivationCompressor:
         if self._capture is True or (self._capture and h.layer in self._capture):
             self.captured[h.layer] = (h.raw.detach().cpu().numpy(), c, h.eb)  # shaped: CMTZ records the dims
         h.comp, h.report, h.raw = c, rep, None  # the original activation is released here
-        self._bits[h.layer] = c.payload_bits  # next iteration's payload cap hint
+        self._bits[h.layer] = (h.eb, c.payload_bits, c._n_outliers)  # next iteration's cap hints
         self.store.put(h.layer, ActivationStore.COMPRESSED, c, rep.compressed_bytes)
         self._interval_ratios.setdefault(h.layer, []).append(rep.ratio)
         if self._rec is not None:
