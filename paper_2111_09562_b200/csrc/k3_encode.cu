@@ -254,6 +254,9 @@ __device__ __forceinline__ uint32_t k3_lds(uint32_t a) {
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void k3_sts(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 // OR v into the warp buffer
 __device__ __forceinline__ void k3_red_or(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -396,7 +399,9 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
     const uint32_t lane_ex = ib - bits;
     const uint32_t off0 = (uint32_t)(pb & 31);
     const uint32_t nw = (off0 + seg_bits + 31) >> 5;
-    for (uint32_t i = lane; i < nw; i += 32) wb[i] = 0;
+    // only the segment's last word can be left without a plain store (no
+    // code completes it): it alone is zeroed for the shared ORs
+    if (lane == 0) wb[nw - 1] = 0;
     __syncwarp();
     if (((lane * K3L_EPT) % ACTC_CHUNK) == 0 && base < a.n) a.chunk_off[base / ACTC_CHUNK] = pb + lane_ex;  // every ACTC_CHUNK-th symbol
     if (a.extract && nz) {
@@ -409,22 +414,31 @@ __global__ void __launch_bounds__(K3L_THREADS, 2) k3_seg_pack(const SymT *__rest
       }
     }
     {
-      // Every code goes straight into the (zeroed) warp buffer at its bit
-      // offset: a left-aligned code of <= 26 bits touches two words at most,
-      // OR-ed by shared reductions (the second one only when the code
-      // crosses the word boundary), so the words lanes share need no special
-      // case.  A length-0 entry (past the end) has code 0.
-      uint32_t rel = off0 + lane_ex;
+      // Codes accumulate in a register word at the lane's bit position; a
+      // word the lane completes is written by a plain shared store (exactly
+      // one lane completes each word), and after a warp barrier the lane's
+      // last, partial word is OR-ed in (it may share the word with the next
+      // lanes, or be the segment's zeroed last word).  A left-aligned code of
+      // <= 26 bits completes at most one word.  A length-0 entry (past the
+      // end) has code 0.
+      uint32_t pos = off0 + lane_ex;
+      uint32_t wad = wb_s + ((pos >> 3) & ~3u);
+      uint32_t fill = pos & 31u, hi = 0u;
 #pragma unroll
       for (int j = 0; j < K3L_EPT; j++) {
         const uint32_t cl = e[j] & ~63u;
-        const uint32_t ad = wb_s + ((rel >> 3) & ~3u);
-        const uint32_t v0 = __funnelshift_r(cl, 0u, rel);  // cl >> (rel & 31)
-        const uint32_t v1 = __funnelshift_r(0u, cl, rel);  // the bits past the word (0 when aligned)
-        k3_red_or(ad, v0);
-        k3_red_or(ad + 4u, v1);  // 0 unless the code crosses the word (unconditional: no branch)
-        rel += e[j] & 63;
+        hi |= __funnelshift_r(cl, 0u, fill);          // cl >> fill
+        const uint32_t ov = __funnelshift_r(0u, cl, fill);  // the bits past the word (0 unless it completes)
+        const uint32_t t = fill + (e[j] & 63u);
+        if (t >= 32u) {
+          k3_sts(wad, hi);
+          wad += 4u;
+          hi = ov;
+        }
+        fill = t & 31u;
       }
+      __syncwarp();
+      if (fill) k3_red_or(wad, hi);
     }
     __syncwarp();
     // copy-out: interior words by plain stores, the two words the segment
