@@ -564,6 +564,20 @@ void actc_ctx_destroy(actc_ctx *c) {
   delete c;
 }
 
+// K1's quantizer parameters for error bound eb (actc_internal.cuh QParams)
+static QParams make_qparams(double eb) {
+  QParams P;
+  P.eb = eb;
+  P.two_eb = 2.0 * eb;
+  const double inv = 1.0 / P.two_eb;
+  P.inv = inv;
+  P.fast = (isfinite(inv) && inv >= DBL_MIN) ? 1 : 0;
+  P.ih = (float)inv;
+  P.il = (float)(inv - (double)P.ih);
+  P.dfast = (P.fast && isfinite(P.ih) && P.ih >= FLT_MIN) ? 1 : 0;
+  return P;
+}
+
 static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_t radius, int64_t *chunk_lat,
                      cudaStream_t s) {
   if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
@@ -588,12 +602,7 @@ static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_
   CK(cudaMemsetAsync(c->misc.p, 0, 8 * M_SLOTS, s));
   unsigned long long *misc = (unsigned long long *)c->misc.p;
 
-  QParams P;
-  P.eb = eb;
-  P.two_eb = 2.0 * eb;
-  const double inv = 1.0 / P.two_eb;
-  P.inv = inv;
-  P.fast = (isfinite(inv) && inv >= DBL_MIN) ? 1 : 0;
+  const QParams P = make_qparams(eb);
   uint32_t win_n = (uint32_t)std::min<uint64_t>(A, K1_WIN);
   uint32_t win_lo = A <= K1_WIN ? 0 : radius - K1_WIN / 2;
   uint64_t ntiles = cdiv(n, K1_TILE);
@@ -1136,11 +1145,7 @@ int actc_prequantize(const void *x, int dtype, uint64_t n, double eb, int64_t *q
 int actc_debug_quant_check(double eb, uint64_t lo, uint64_t count, uint64_t *out_host, actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (!(eb > 0 && isfinite(eb))) return set_err(ACTC_EPARAM, "eb must be a positive finite real, got %g", eb);
-  QParams P;  // exactly as launch_k1 builds it
-  P.eb = eb;
-  P.two_eb = 2.0 * eb;
-  P.inv = 1.0 / P.two_eb;
-  P.fast = (isfinite(P.inv) && P.inv >= DBL_MIN) ? 1 : 0;
+  const QParams P = make_qparams(eb);  // exactly as launch_k1 builds it
   unsigned long long *d = nullptr;
   CK(cudaMallocAsync((void **)&d, 16, s));
   CK(cudaMemsetAsync(d, 0, 16, s));

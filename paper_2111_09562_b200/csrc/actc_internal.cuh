@@ -26,6 +26,8 @@ struct QParams {
   double two_eb;   // 2.0 * eb (exact scaling; may be +inf like numpy)
   double inv;      // fl64(1 / two_eb) -- fast-path multiplier
   int fast;        // inv is finite and normal
+  float ih, il;    // inv as an unevaluated fp32 pair: ih = fl32(inv), il = fl32(inv - ih)
+  int dfast;       // the fp32-pair tier applies (ih finite and normal)
 };
 
 // Exact restatement: v = x / (2eb); q = sign(v)*floor(fl(|v| + 0.5));
@@ -58,6 +60,27 @@ __device__ __forceinline__ bool quant_fast32(float xf, double inv, int &q) {
   q = xf > 0.0f ? qi : -qi;
   return safe;
 }
+// First tier, all fp32 at full rate (no fp64, no conversion-pipe op):
+// v ~ x*(ih + il) as p + e (p = fl32(x*ih), e = the product's exact error by
+// FMA plus x*il), rounded to the nearest integer r by the 1.5*2^23 magic
+// add (|p| < 2^22), d = (p - r) + e.  |(ih + il) - 1/two_eb| <= inv*2^-47.9,
+// and with |p| < 2^22 the rounding errors of e and d stay below 2^-23, so
+// |v - r| < 0.5 - 2^-21 whenever |d| < 0.5 - 2^-20: then q = r is numpy's
+// sign(v)*floor(|v| + 0.5) (fl64(|v| + 0.5) cannot reach the next integer)
+// and |x - q*2eb| <= eb*(1 - 2^-20) rules out a bound violation.  Returns
+// false (caller takes quant_fast32 / quant_exact) otherwise, and for
+// non-finite x.  Verified for every fp32 pattern by k_quant_check.
+__device__ __forceinline__ bool quant_df(float xf, float ih, float il, int &q) {
+  const float p = __fmul_rn(xf, ih);
+  float e = __fmaf_rn(xf, ih, -p);
+  e = __fmaf_rn(xf, il, e);
+  const float m = __fadd_rn(p, 12582912.0f);  // 1.5 * 2^23: rounds p to an integer
+  const float r = __fsub_rn(m, 12582912.0f);
+  const float d = __fadd_rn(__fsub_rn(p, r), e);
+  q = __float_as_int(m) - 0x4B400000;
+  return fabsf(p) < 0x1p22f && fabsf(d) < 0.49999904632568359375f;  // 0.5 - 2^-20
+}
+
 __device__ __forceinline__ bool quant_fast(float xf, double inv, long long &q) {
   int q32;
   const bool safe = quant_fast32(xf, inv, q32);
@@ -68,6 +91,8 @@ __device__ __forceinline__ bool quant_fast(float xf, double inv, long long &q) {
 __device__ __forceinline__ long long quant_elem(float xf, const QParams &P, bool &viol) {
   long long q;
   viol = false;
+  int qd;
+  if (P.dfast && quant_df(xf, P.ih, P.il, qd)) return qd;
   if (P.fast && quant_fast(xf, P.inv, q)) return q;
   return quant_exact((double)xf, P.two_eb, P.eb, viol);
 }

@@ -77,10 +77,19 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) xv[j] = (base + j < n) ? x[base + j] : 0.0f;
     }
-    // fp32 fast quantizer for all 16 elements; exact fp64 only where needed
+    // fp32-pair quantizer for all 16 elements, the fp64 multiply tier for
+    // the few it declines, exact fp64 only where both decline
     int q32[K1_EPT];
     unsigned slow = 0;
-    if (P.fast) {
+    if (P.dfast) {
+#pragma unroll
+      for (int j = 0; j < K1_EPT; j++) slow |= (unsigned)!quant_df(xv[j], P.ih, P.il, q32[j]) << j;
+      if (slow) {
+#pragma unroll
+        for (int j = 0; j < K1_EPT; j++)
+          if ((slow >> j) & 1u) slow &= ~((unsigned)quant_fast32(xv[j], P.inv, q32[j]) << j);
+      }
+    } else if (P.fast) {
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) slow |= (unsigned)!quant_fast32(xv[j], P.inv, q32[j]) << j;
     } else {
@@ -237,10 +246,11 @@ __global__ void k_prequantize(const void *__restrict__ x, int dtype, uint64_t n,
   }
 }
 
-// Exhaustive check of K1's fp32 fast quantizer: every finite fp32 bit
-// pattern in [lo, lo + count) through quant_fast32 (when it claims the
-// element) vs the exact restatement quant_exact (q and "no bound
-// violation").  out[0] += mismatches, out[1] += elements the fast path took.
+// Exhaustive check of K1's fast quantizer tiers: every finite fp32 bit
+// pattern in [lo, lo + count) through quant_df, else quant_fast32 (when one
+// claims the element; the order K1 uses) vs the exact restatement
+// quant_exact (q and "no bound violation").  out[0] += mismatches, out[1]
+// += elements a fast tier took.
 __global__ void k_quant_check(uint64_t lo, uint64_t count, QParams P, unsigned long long *__restrict__ out) {
   unsigned long long bad = 0, fast = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
@@ -248,7 +258,7 @@ __global__ void k_quant_check(uint64_t lo, uint64_t count, QParams P, unsigned l
     const float xf = __uint_as_float((uint32_t)(lo + i));
     if (!isfinite(xf)) continue;
     int q32;
-    if (!(P.fast && quant_fast32(xf, P.inv, q32))) continue;
+    if (!((P.dfast && quant_df(xf, P.ih, P.il, q32)) || (P.fast && quant_fast32(xf, P.inv, q32)))) continue;
     fast++;
     bool viol;
     const long long qe = quant_exact((double)xf, P.two_eb, P.eb, viol);
