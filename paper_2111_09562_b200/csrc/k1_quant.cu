@@ -21,13 +21,17 @@ __device__ __forceinline__ uint32_t k1_saddr(const void *p) {
   asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
   return r;
 }
-__device__ __forceinline__ void k1_hist_add(uint32_t hbase, uint32_t win_lo, uint32_t win_n,
-                                            unsigned long long *__restrict__ ghist, uint32_t sj) {
+// one histogram count for symbol sj unless it is a zero delta or an outlier
+// (both counted in registers): a predicated shared add inside the window
+// (no branch), the window's misses flagged in *oow for the caller's
+// (rare) global adds
+__device__ __forceinline__ void k1_hist_add(uint32_t hbase, uint32_t win_lo, uint32_t win_n, uint32_t sj,
+                                            bool skip, unsigned &oow, int j) {
   const uint32_t w = sj - win_lo;
-  if (w < win_n)
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * w) : "memory");
-  else
-    atomicAdd(&ghist[sj], 1ull);
+  const bool in = w < win_n;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+               ::"r"(hbase + 4u * w), "r"((uint32_t)(in && !skip)) : "memory");
+  oow |= (unsigned)(!in && !skip) << j;
 }
 
 template <typename SymT>
@@ -125,6 +129,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q32[K1_EPT - 1];
       }
       int prev = (int)prev64;
+      unsigned oow = 0;
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) {
         const int d = q32[j] - prev;
@@ -133,12 +138,15 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         const uint32_t sj = o ? 0u : (uint32_t)(d + R);
         s[j] = sj;
         outl += o;
-        if (d == 0)
-          zc++;
-        else
-          k1_hist_add(hbase, win_lo, win_n, ghist, sj);
+        zc += d == 0;
+        k1_hist_add(hbase, win_lo, win_n, sj, d == 0 || o, oow, j);
       }
       k1_store<SymT>(sym, base, s);
+      if (oow) {
+#pragma unroll
+        for (int j = 0; j < K1_EPT; j++)
+          if ((oow >> j) & 1u) atomicAdd(&ghist[s[j]], 1ull);
+      }
     } else {
       // general path: exact fp64 where the fast path declined, int64 deltas
       long long q[K1_EPT];
@@ -157,6 +165,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q[K1_EPT - 1];
       }
       long long prev = prev64;
+      unsigned oow = 0;
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) {
         long long d = q[j] - prev;
@@ -165,13 +174,15 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         bool o = ad >= radius || ((viol >> j) & 1u);
         uint32_t sj = o ? 0u : (uint32_t)(d + (long long)radius);
         s[j] = sj;
-        if (base + j < n) {
-          outl += o;
-          if (sj == radius)
-            zc++;
-          else
-            k1_hist_add(hbase, win_lo, win_n, ghist, sj);
-        }
+        const bool valid = base + j < n;
+        outl += valid && o;
+        zc += valid && sj == radius;
+        k1_hist_add(hbase, win_lo, win_n, sj, !valid || o || sj == radius, oow, j);
+      }
+      if (oow) {
+#pragma unroll
+        for (int j = 0; j < K1_EPT; j++)
+          if ((oow >> j) & 1u) atomicAdd(&ghist[s[j]], 1ull);
       }
       if (full_tile) {
         k1_store<SymT>(sym, base, s);
@@ -192,6 +203,13 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
       atomicAdd(&sh_hist[w], zsum);
     else
       atomicAdd(&ghist[radius], (unsigned long long)zsum);
+  }
+  // outliers are symbol 0 (bincount counts them too)
+  if (lane == 0 && wsum) {
+    if (win_lo == 0)
+      atomicAdd(&sh_hist[0], wsum);
+    else
+      atomicAdd(&ghist[0], (unsigned long long)wsum);
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) {
