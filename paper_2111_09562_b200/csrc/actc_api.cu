@@ -507,7 +507,7 @@ int actc_ctx_create(int device, actc_ctx **out) {
     if (i < 9) c->k4l_dyn_max = std::min(c->k4l_dyn_max, optin - (int)fa.sharedSizeBytes);  // the K4L variants
   }
   // occupancy-derived persistent grid sizes
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, (size_t)K1_WIN * 4);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1_quant_lorenzo_hist<uint16_t>, K1_THREADS, (size_t)(K1_WIN + 32) * 4);
   c->k1_blocks = std::max(1, nb) * c->num_sms;
   size_t s16 = (size_t)K4_THREADS * (ACTC_CHUNK / 2 + 1) * 4, s32 = (size_t)K4_THREADS * (ACTC_CHUNK + 1) * 4;
   CK(cudaFuncSetAttribute(k4_decode<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s16));
@@ -610,11 +610,11 @@ static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_
   {
     KT(ACTC_KIND_QUANT);
     if (sb == 2)
-      k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, win_n * 4, s>>>(
+      k1_quant_lorenzo_hist<uint16_t><<<grid, K1_THREADS, (win_n + 32) * 4, s>>>(
           x, n, P, radius, (uint16_t *)c->sym_cur, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
           (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
     else
-      k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, win_n * 4, s>>>(
+      k1_quant_lorenzo_hist<uint32_t><<<grid, K1_THREADS, (win_n + 32) * 4, s>>>(
           x, n, P, radius, (uint32_t *)c->sym_cur, (unsigned long long *)c->hist.p, misc + M_NOUT, win_lo, win_n,
           (unsigned *)(misc + M_BAD), (long long *)chunk_lat);
   }

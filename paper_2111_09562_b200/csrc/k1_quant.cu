@@ -22,15 +22,15 @@ __device__ __forceinline__ uint32_t k1_saddr(const void *p) {
   return r;
 }
 // one histogram count for symbol sj unless it is a zero delta or an outlier
-// (both counted in registers): a predicated shared add inside the window
-// (no branch), the window's misses flagged in *oow for the caller's
-// (rare) global adds
+// (both counted in registers): an unconditional shared add (no branch: the
+// skipped elements add into a per-lane scratch bin past the window), the
+// window's misses flagged in oow for the caller's (rare) global adds
 __device__ __forceinline__ void k1_hist_add(uint32_t hbase, uint32_t win_lo, uint32_t win_n, uint32_t sj,
                                             bool skip, unsigned &oow, int j) {
   const uint32_t w = sj - win_lo;
   const bool in = w < win_n;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
-               ::"r"(hbase + 4u * w), "r"((uint32_t)(in && !skip)) : "memory");
+  const uint32_t bin = (in && !skip) ? w : win_n + (threadIdx.x & 31);
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * bin) : "memory");
   oow |= (unsigned)(!in && !skip) << j;
 }
 
