@@ -21,17 +21,31 @@ __device__ __forceinline__ uint32_t k1_saddr(const void *p) {
   asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a));
   return r;
 }
-// one histogram count for symbol sj unless it is a zero delta or an outlier
-// (both counted in registers): an unconditional shared add (no branch: the
-// skipped elements add into a per-lane scratch bin past the window), the
-// window's misses flagged in oow for the caller's (rare) global adds
-__device__ __forceinline__ void k1_hist_add(uint32_t hbase, uint32_t win_lo, uint32_t win_n, uint32_t sj,
-                                            bool skip, unsigned &oow, int j) {
+// one histogram count for symbol sj: an unconditional shared add (ptxas
+// emits ATOMS.POPC.INC, which counts the lanes of a warp that hit one bin in
+// one operation -- the dominant zero-delta bin costs no serialisation).
+// Elements that must not count here (outside the window, or not valid) add
+// into a per-lane scratch bin past the window; returns "outside the window"
+__device__ __forceinline__ bool k1_hist_add(uint32_t hbase, uint32_t win_lo, uint32_t win_n, uint32_t sj,
+                                            bool valid) {
   const uint32_t w = sj - win_lo;
   const bool in = w < win_n;
-  const uint32_t bin = (in && !skip) ? w : win_n + (threadIdx.x & 31);
+  const uint32_t bin = (in && valid) ? w : win_n + (threadIdx.x & 31);
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * bin) : "memory");
-  oow |= (unsigned)(!in && !skip) << j;
+  return !in;
+}
+
+// the tile's elements outside the histogram window (rare): global adds.
+// Outliers (symbol 0) are excluded when bin 0 is outside the window: the
+// kernel adds their count once at the end
+__device__ __forceinline__ void k1_hist_misses(unsigned long long *__restrict__ ghist, uint32_t win_lo,
+                                               uint32_t win_n, const uint32_t (&s)[K1_EPT], uint64_t base,
+                                               uint64_t n) {
+#pragma unroll
+  for (int j = 0; j < K1_EPT; j++) {
+    const uint32_t sj = s[j];
+    if (sj - win_lo >= win_n && sj != 0 && base + j < n) atomicAdd(&ghist[sj], 1ull);
+  }
 }
 
 template <typename SymT>
@@ -64,7 +78,6 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
   const uint64_t nfull = n / K1_TILE;  // tiles with no element past n
   const int R = (int)min(radius, 0x40000000u);
   unsigned outl = 0;
-  unsigned zc = 0;  // zero deltas (symbol `radius`, the dominant one): counted in a register
   bool fin_all = true;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t base = tile * K1_TILE + (uint64_t)threadIdx.x * K1_EPT;
@@ -129,7 +142,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q32[K1_EPT - 1];
       }
       int prev = (int)prev64;
-      unsigned oow = 0;
+      bool miss = false;
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) {
         const int d = q32[j] - prev;
@@ -138,15 +151,10 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         const uint32_t sj = o ? 0u : (uint32_t)(d + R);
         s[j] = sj;
         outl += o;
-        zc += d == 0;
-        k1_hist_add(hbase, win_lo, win_n, sj, d == 0 || o, oow, j);
+        miss |= k1_hist_add(hbase, win_lo, win_n, sj, true) && !o;
       }
       k1_store<SymT>(sym, base, s);
-      if (oow) {
-#pragma unroll
-        for (int j = 0; j < K1_EPT; j++)
-          if ((oow >> j) & 1u) atomicAdd(&ghist[s[j]], 1ull);
-      }
+      if (miss) k1_hist_misses(ghist, win_lo, win_n, s, base, n);
     } else {
       // general path: exact fp64 where the fast path declined, int64 deltas
       long long q[K1_EPT];
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         if (((base + K1_EPT) % ACTC_CHUNK) == 0 && base + K1_EPT < n) chunk_lat[(base + K1_EPT) / ACTC_CHUNK] = q[K1_EPT - 1];
       }
       long long prev = prev64;
-      unsigned oow = 0;
+      bool miss = false;
 #pragma unroll
       for (int j = 0; j < K1_EPT; j++) {
         long long d = q[j] - prev;
@@ -176,14 +184,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
         s[j] = sj;
         const bool valid = base + j < n;
         outl += valid && o;
-        zc += valid && sj == radius;
-        k1_hist_add(hbase, win_lo, win_n, sj, !valid || o || sj == radius, oow, j);
+        miss |= k1_hist_add(hbase, win_lo, win_n, sj, valid) && valid && !o;
       }
-      if (oow) {
-#pragma unroll
-        for (int j = 0; j < K1_EPT; j++)
-          if ((oow >> j) & 1u) atomicAdd(&ghist[s[j]], 1ull);
-      }
+      if (miss) k1_hist_misses(ghist, win_lo, win_n, s, base, n);
       if (full_tile) {
         k1_store<SymT>(sym, base, s);
       } else {
@@ -196,21 +199,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) k1_quant_lorenzo_hist(
   if (!__all_sync(0xffffffffu, fin_all) && !fin_all) atomicOr(nonfinite, 1u);  // tensor.py:56-57
   unsigned wsum = warp_sum(outl);
   if (lane == 0 && wsum) atomicAdd(n_outliers, (unsigned long long)wsum);
-  const unsigned zsum = warp_sum(zc);
-  if (lane == 0 && zsum) {
-    const uint32_t w = radius - win_lo;
-    if (w < win_n)
-      atomicAdd(&sh_hist[w], zsum);
-    else
-      atomicAdd(&ghist[radius], (unsigned long long)zsum);
-  }
-  // outliers are symbol 0 (bincount counts them too)
-  if (lane == 0 && wsum) {
-    if (win_lo == 0)
-      atomicAdd(&sh_hist[0], wsum);
-    else
-      atomicAdd(&ghist[0], (unsigned long long)wsum);
-  }
+  // outliers are symbol 0 (bincount counts them too): counted in the window
+  // when bin 0 is in it, else added here
+  if (lane == 0 && wsum && win_lo != 0) atomicAdd(&ghist[0], (unsigned long long)wsum);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) {
     unsigned c = sh_hist[i];
