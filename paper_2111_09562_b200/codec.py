@@ -850,14 +850,16 @@ def compress(t, params: CodecParams):
 
 
 def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None, check=True,
-                      count_nonzero=True):
+                      count_nonzero=True, slot: int = 0):
     """Reconstruct on the device.  Returns (tensor, nonzero_count or None).
 
     dtype torch.float64 is bit-identical to the reference's output; float32
     stores fp32 of it.  With check=False no host synchronisation happens
     (the status and nonzero count are left in the context's mailbox).  With
     count_nonzero=False the decoder skips the nonzero count (R,
-    training.py:351-352) and None is returned in its place.
+    training.py:351-352) and None is returned in its place.  `slot` picks
+    the library context (0: the thread's main one; another slot for a
+    decode running concurrently on another stream).
     """
     torch = _lib.torch_cuda()
     dtype = torch.float32 if dtype is None else dtype
@@ -866,10 +868,11 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
         raise FormatError(f"symbol count {c.symbol_count} != element count {n}")
     c._ensure_index()
     dev = c.device
-    ctx = _lib.context(dev.index)
+    ctx = _lib.context_for(dev.index, slot)
     sh, s = _lib.stream_handle(stream, dev)
     if out is None:
-        out = torch.empty(c.dims, dtype=dtype, device=dev)
+        with torch.cuda.stream(s):  # stream-ordered for the decoding stream
+            out = torch.empty(c.dims, dtype=dtype, device=dev)
     code = _lib.ACTC_DTYPE_F32 if out.dtype == torch.float32 else _lib.ACTC_DTYPE_F64
     if out.dtype not in (torch.float32, torch.float64) or out.numel() != n or not out.is_contiguous():
         raise ParameterError("output must be a contiguous fp32/fp64 tensor with the stream's element count")
@@ -879,6 +882,8 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
         code |= _lib.ACTC_DEC_NO_NONZERO
     _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
                                                C.c_void_p(ctx.dres_buf.data_ptr()), sh))
+    if s != torch.cuda.current_stream(dev):
+        c._record_stream(s)  # the container is read on `s` (caching allocator)
     if not check:
         return out, None
     s.synchronize()

@@ -49,7 +49,8 @@ Packing is asynchronous: a stored activation's compression is launched on a
 side stream as soon as it exists (`compress_begin`, no host sync); a
 compression is finished (`compress_end`: plan read, exact-size container,
 original released) as soon as its chain is done, or -- waiting -- once more
-than `batch_flush` are in flight.  The training stream is never ordered
+than `batch_flush` are in flight or the raw activations waiting behind the
+newest one exceed `inflight_bytes`.  The training stream is never ordered
 after a compression: the container's decompression in backward waits for
 its completion event instead.  Decode faults of the (unsynchronised) backward decompressions
 are collected at the end of every iteration and raised as FormatError at
@@ -134,6 +135,13 @@ class _Marker:
         self.ref = weakref.ref(t)
 
 
+def _numel(shape) -> int:
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
 class _Handle:
     """One saved fp32 tensor.  Autograd saves a module's output while the op
     runs, before the module's forward hook names it, so every saved tensor
@@ -141,7 +149,8 @@ class _Handle:
     activation to its slot: raw until the pending queue is flushed,
     compressed after.  Handles nobody promotes pass the tensor through."""
 
-    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref", "job", "rec")
+    __slots__ = ("layer", "eb", "raw", "comp", "report", "packs", "unpacks", "out", "shape", "ref", "job", "rec",
+                 "pos", "pf")
 
     def __init__(self, t, layer, eb):
         self.layer = layer
@@ -155,6 +164,8 @@ class _Handle:
         self.shape = tuple(t.shape)
         self.job = None  # compress_begin batch while the compression is in flight
         self.rec = None  # (recompute fn, source handle, marker slot): a cheap layer's output, recomputed
+        self.pos = -1  # index among this iteration's compressed stored activations (promotion order)
+        self.pf = None  # (tensor, event): reconstruction prefetched on the decode stream
         # the tensor's identity: a key (pointer, version, shape, stride) is
         # only unique while the tensor lives -- freed memory is reused
         self.ref = weakref.ref(t)
@@ -260,7 +271,8 @@ class ActivationCompressor:
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 1, dist_group=None,
                  sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
-                 recompute_cheap: bool = True, codec_on_compute_stream: bool = False):
+                 recompute_cheap: bool = True, codec_on_compute_stream: bool = False,
+                 prefetch_decode: bool = True, inflight_bytes: int = 1 << 29):
         import torch.nn as nn
 
         self.layers = dict(layers)
@@ -271,13 +283,25 @@ class ActivationCompressor:
         self.radius = radius
         self.preserve_zeros = preserve_zeros
         self.grad_scale = grad_scale  # None: use the batch size (mean-reduced loss)
+        # at most `batch_flush` compressions in flight (each holds a side
+        # stream + library context), and the raw activations of all but the
+        # newest below `inflight_bytes`: the host runs ahead of the GPU by
+        # that much instead of waiting for each compression
         self.batch_flush = batch_flush
+        self.inflight_bytes = inflight_bytes
+        self._pending_bytes = 0
         self.dist_group = dist_group
         self.sync_stats = sync_stats
         self.recompute_cheap = recompute_cheap
         # compressions in order on the training stream (no SM contention with
         # the convolutions) instead of side streams
         self.codec_on_compute_stream = codec_on_compute_stream
+        # backward: while one stored activation is reconstructed for autograd,
+        # the one stored before it (the next one backward needs) is decoded
+        # on a side stream, overlapping the decoder with backward's kernels
+        self.prefetch_decode = prefetch_decode
+        self._pf_stream = None
+        self._order: list = []  # this iteration's compressed stored activations, promotion order
         self.plan = None
         self.it = 0
         self.next_collection = self.controller.W
@@ -591,11 +615,16 @@ class ActivationCompressor:
         # in backward while the last compressions may still be in flight)
         h.job = compress_begin([t], [params], slot_base=1 + self._slot, bit_hints=[hb], outlier_hints=[ho],
                                own_scratch=True, on_caller_stream=self.codec_on_compute_stream)
+        h.pos = len(self._order)
+        self._order.append(h)
         self._slot = (self._slot + 1) % (self.batch_flush + 1)
         self._pending.append(h)
+        self._pending_bytes += nbytes
         # finish what is already done without waiting; wait only when more
-        # than batch_flush are in flight (their contexts are reused next)
-        while self._pending and (len(self._pending) > self.batch_flush or self._pending[0].job.ready()):
+        # than batch_flush are in flight (their contexts are reused next) or
+        # the older raw activations exceed inflight_bytes
+        while self._pending and (len(self._pending) > self.batch_flush or self._pending[0].job.ready()
+                                 or (len(self._pending) > 1 and self._pending_bytes > self.inflight_bytes)):
             self._finish(self._pending.pop(0))
 
     def _hint(self, slot, eb):
@@ -623,6 +652,7 @@ class ActivationCompressor:
         self.captured = {}
 
     def _finish(self, h):
+        self._pending_bytes -= 4 * _numel(h.shape)
         # order=False: the training stream never waits for a compression;
         # the container's readers (the backward decompression) do
         (c, rep), = compress_end(h.job, compact=True, order=False)
@@ -681,6 +711,17 @@ class ActivationCompressor:
             return out
         if h.layer is None:
             return h.raw  # a saved tensor that is not a stored activation
+        if h.out is None and h.pf is not None:
+            # decoded ahead on the prefetch stream
+            out, ev = h.pf
+            h.pf = None
+            cur = torch.cuda.current_stream()
+            cur.wait_event(ev)
+            out.record_stream(cur)
+            h.out = out.view(h.shape)
+            self.store.pop(h.layer)
+            h.comp = None
+            self._prefetch_before(h)
         if h.out is None:
             if h.comp is None and h.raw is None:
                 raise LifecycleError(f"activation of {h.layer!r} already released")
@@ -697,6 +738,7 @@ class ActivationCompressor:
                     self._R[h.layer] = nz / out.numel()
                 self.store.pop(h.layer)
                 h.comp = None
+                self._prefetch_before(h)
             else:
                 h.out = h.raw
                 if self._collecting:
@@ -711,11 +753,39 @@ class ActivationCompressor:
             h.out = None
         return out
 
+    def _prefetch_before(self, h):
+        """Launch the decode of the compressed activation stored just before
+        h (backward's next one) on the prefetch stream, its own library
+        context; not in collection iterations (they read R back at once)."""
+        import torch
+
+        if not self.prefetch_decode or self._collecting or h.pos <= 0:
+            return
+        g = self._order[h.pos - 1]
+        if g.comp is None or g.out is not None or g.pf is not None or g.unpacks or g.job is not None:
+            return
+        cur = torch.cuda.current_stream()
+        if self._pf_stream is None:
+            self._pf_stream = torch.cuda.Stream(device=cur.device)
+        ps = self._pf_stream
+        ps.wait_stream(cur)  # after the caller's queued work (memory the allocator handed back)
+        out, _ = decompress_device(g.comp, dtype=torch.float32, stream=ps, check=False, count_nonzero=False,
+                                   slot=self.batch_flush + 2)
+        g.pf = (out, ps.record_event())
+
     # ---- iteration protocol --------------------------------------------------
     def _reset_iteration_state(self):
         for d in (self._act_layer, self._handles, self._ptag, self._ctag, self._cheap, self._markers, self._calls,
                   self._bnp, self._slot_out):
             d.clear()
+        for h in self._order:
+            if h.pf is not None:  # decoded ahead but never read back: join its stream
+                import torch
+
+                torch.cuda.current_stream().wait_event(h.pf[1])
+                h.pf[0].record_stream(torch.cuda.current_stream())
+                h.pf = None
+        self._order = []
         self._await_consumer = []
 
     @contextlib.contextmanager
@@ -732,6 +802,10 @@ class ActivationCompressor:
                                   "(or outlier markers disagree with stored indices)")
         self._collecting = (self.it + 1) == self.next_collection
         self._reset_iteration_state()
+        # the same slot (side stream + library context) for the same stored
+        # activation every iteration: each context's scratch reaches its
+        # size once, no allocation (device-wide synchronisation) later
+        self._slot = 0
         self._batch = None  # taken from this iteration's first producer input
         self._R.clear()
         self._lbar.clear()

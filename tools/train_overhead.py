@@ -17,12 +17,18 @@ for mode in sys.argv[3].split(",") if len(sys.argv) > 3 else ("plain", "hooks_ra
     torch.manual_seed(0)
     m = getattr(torchvision.models, name)(num_classes=1000).to(dev)
     opt = torch.optim.SGD(m.parameters(), lr=0.01, momentum=0.9)
+    from paper_2111_09562_b200 import codec as _codec
+    _codec._side_streams.clear()
+    if "_pri0" in mode:  # side streams at the training stream's priority
+        _codec._side_streams[0] = [torch.cuda.Stream(device=dev, priority=0) for _ in range(16)]
     comp = None
     if mode != "plain":
         w = 1000 if mode == "hooks_raw" else 2
         comp = ActivationCompressor(ActivationCompressor.conv_layer_map(m), opt,
                                     pb.ControllerConfig(W_default=w, W_floor=1),
-                                    codec_on_compute_stream=mode.endswith("inorder"))
+                                    codec_on_compute_stream=mode.endswith("inorder"),
+                                    prefetch_decode=not mode.endswith("nopf"),
+                                    **({"batch_flush": int(mode.split("_bf")[1].split("_")[0])} if "_bf" in mode else {}))
     x = torch.randn(batch, 3, 224, 224, device=dev)
     y = torch.randint(0, 1000, (batch,), device=dev)
 
@@ -43,13 +49,19 @@ for mode in sys.argv[3].split(",") if len(sys.argv) > 3 else ("plain", "hooks_ra
         comp.next_collection = comp.it + 1000
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(6):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    st0 = torch.cuda.memory_stats(dev)
+    r0 = len(_codec.REDOS)
+    evs[0].record()
+    for i in range(6):
         it()
-    e1.record()
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / 6
+        evs[i + 1].record()
+    evs[-1].synchronize()
+    ms = evs[0].elapsed_time(evs[-1]) / 6
+    st1 = torch.cuda.memory_stats(dev)
+    per = [round(evs[i].elapsed_time(evs[i + 1]), 1) for i in range(6)]
+    print(f"   per-iteration ms {per}; cudaMalloc calls {st1.get('num_device_alloc', 0) - st0.get('num_device_alloc', 0)}, "
+          f"redos {len(_codec.REDOS) - r0}", flush=True)
     print(f"{name} b{batch} {mode}: {batch / ms * 1e3:.0f} img/s, {ms:.1f} ms/iter, "
           f"peak {torch.cuda.max_memory_allocated(dev) / 1e9:.2f} GB", flush=True)
     if comp:

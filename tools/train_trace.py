@@ -72,3 +72,20 @@ for sid, es in sorted(streams.items(), key=lambda kv: -sum(e.time_range.elapsed_
             end = f
     print(f"stream {sid}: {len(es)} kernels, busy {busy / 1e3:.1f} ms of {(t1 - t0) / 1e3:.1f}; "
           + ", ".join(f"{k} {v / 1e3:.1f}" for k, v in tot.most_common()))
+
+# the training stream's largest idle gaps: the kernels around them and what
+# the other streams ran meanwhile
+main_sid = max(streams, key=lambda k: sum(e.time_range.elapsed_us() for e in streams[k]))
+es = sorted(streams[main_sid], key=lambda e: e.time_range.start)
+gaps = []
+for a, b in zip(es, es[1:]):
+    g = b.time_range.start - a.time_range.end
+    if g > 50:
+        gaps.append((g, a, b))
+gaps.sort(key=lambda t: -t[0])
+print(f"main stream gaps > 50 us: {len(gaps)}, total {sum(g for g, _, _ in gaps) / 1e3:.1f} ms")
+for g, a, b in gaps[:12]:
+    other = [e for sid, l in streams.items() if sid != main_sid for e in l
+             if e.time_range.start < b.time_range.start and e.time_range.end > a.time_range.end]
+    print(f"  {g / 1e3:.2f} ms at {(a.time_range.end - t0) / 1e3:.1f}: after {a.name[:40]!r} before {b.name[:40]!r}; "
+          f"others: {collections.Counter(cat(e.name) for e in other).most_common(4)}")
