@@ -269,6 +269,11 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   const uint32_t L = s_L;
   const uint32_t nbig = s_nbig;
   if (L == 0 || nbig > kBigCap || s_sum >= (1ull << 32)) {
+    if (tid == 0 && a.dbg) {
+      a.dbg[20] = 1;
+      a.dbg[21] = nbig;
+      a.dbg[22] = L;
+    }
     if (tid == 0) {
       *a.fallback = 1u;
       a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
@@ -317,6 +322,11 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   }
   const uint32_t R = Rs + nu;
   if (R > kRCap) {
+    if (tid == 0 && a.dbg) {
+      a.dbg[20] = 2;
+      a.dbg[21] = R;
+      a.dbg[22] = L;
+    }
     if (tid == 0) {
       *a.fallback = 1u;
       a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
@@ -622,6 +632,13 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
     __syncthreads();
   }
   if (s_fail) {
+    if (tid == 0 && a.dbg) {
+      a.dbg[20] = 3;
+      a.dbg[21] = ((unsigned long long)s_ni << 32) | s_nside;
+      a.dbg[22] = L;
+      a.dbg[23] = s_nph;
+      a.dbg[24] = R;
+    }
     if (tid == 0) {
       *a.fallback = 1u;
       a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
@@ -764,6 +781,12 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   }
   __syncthreads();
   if (s_fail) {
+    if (tid == 0 && a.dbg) {
+      a.dbg[20] = 4;
+      a.dbg[21] = ((unsigned long long)s_minlen << 32) | s_maxlen;
+      a.dbg[22] = L;
+      a.dbg[23] = s_nsc;
+    }
     if (tid == 0) {
       *a.fallback = 1u;
       a.plan->status = ACTC_EAGAIN;  // k2_codebook (if queued) rewrites the plan
