@@ -272,7 +272,7 @@ class ActivationCompressor:
                  preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 1, dist_group=None,
                  sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
                  recompute_cheap: bool = True, codec_on_compute_stream: bool = False,
-                 prefetch_decode: bool = True, inflight_bytes: int = 1 << 29):
+                 prefetch_decode: bool = False, inflight_bytes: int = 1 << 29):
         import torch.nn as nn
 
         self.layers = dict(layers)
