@@ -200,6 +200,13 @@ int actc_decompress(actc_ctx *ctx, const actc_stream_t *stream, void *out_dev,
 int actc_crc32(actc_ctx *ctx, const void *data_dev, uint64_t len, uint32_t crc_in,
                uint32_t *crc_out_host, actc_stream s);
 
+/* Utility (no reference counterpart): count <= 16 device-to-device copies
+ * queued on one stream in one call -- the exact-size container compaction
+ * after an asynchronous compression (codec.py compress_end, compact=True).
+ * Asynchronous. */
+int actc_memcpy_batch(void *const *dst_dev, const void *const *src_dev, const uint64_t *bytes, int count,
+                      actc_stream s);
+
 /* Build the canonical code table from a per-symbol length table (the
  * form CMTZ stores, codec.py:164) -- used after from_bytes
  * (codec.py:121-179).  canon_syms_dev needs [count of nonzero lengths]. */

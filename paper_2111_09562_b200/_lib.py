@@ -110,6 +110,7 @@ def lib():
             "actc_codebook_from_lengths": ([P, P, U64, P, P, P, P], I),
             "actc_build_chunk_index": ([P, P, P, P, P], I),
             "actc_crc32": ([P, P, U64, U32, P, P], I),
+            "actc_memcpy_batch": ([P, P, P, I, P], I),
             "actc_inject_uniform": ([P, P, I, U64, D, I, P, P, P], I),
             "actc_prequantize": ([P, I, U64, D, P, P], I),
             "actc_lorenzo_encode": ([P, U64, U32, P, P, P, P], I),
@@ -137,7 +138,7 @@ EXPORTED_SYMBOLS = (
     "actc_compress_encode actc_compress_async actc_decompress actc_codebook_from_lengths actc_build_chunk_index "
     "actc_prequantize actc_debug_quant_check actc_lorenzo_encode actc_lorenzo_decode actc_huffman_plan "
     "actc_huffman_encode actc_huffman_decode actc_code_lengths actc_count_nonzero "
-    "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats actc_crc32 actc_inject_uniform"
+    "actc_mean_abs actc_lbar actc_timing_enable actc_kernel_stats actc_crc32 actc_inject_uniform actc_memcpy_batch"
 ).split()
 
 # instrumentation kinds (include/actc.h ACTC_KIND_*)

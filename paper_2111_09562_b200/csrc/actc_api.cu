@@ -1011,6 +1011,14 @@ int actc_decompress(actc_ctx *c, const actc_stream_t *stream, void *out, int out
                        no_nonzero);
 }
 
+int actc_memcpy_batch(void *const *dst, const void *const *src, const uint64_t *bytes, int count, actc_stream stream) {
+  if (count < 0 || count > 16) return set_err(ACTC_EPARAM, "memcpy_batch: count %d not in [0, 16]", count);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int i = 0; i < count; i++)
+    if (bytes[i]) CK(cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyDeviceToDevice, s));
+  return ACTC_OK;
+}
+
 int actc_crc32(actc_ctx *c, const void *data_dev, uint64_t len, uint32_t crc_in, uint32_t *crc_out_host,
                actc_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
