@@ -181,9 +181,10 @@ class _DevBufs:
     def __contains__(self, name):
         return name in self._slots
 
-    def compact(self, names, stream):
+    def compact(self, names, stream, cur=None):
         """Move the named slots into one exact-size allocation (copies on
-        `stream`); their old backing allocation is released once unused."""
+        `stream`); their old backing allocation is released once unused.
+        `cur`: the caller's current stream (else looked up)."""
         torch = _lib.torch_cuda()
         olds = {self._slots[nm][0] for nm in names}
         layout = [(nm, self._slots[nm][2], self._slots[nm][3]) for nm in names]
@@ -191,12 +192,15 @@ class _DevBufs:
         for nm, numel, isz in layout:
             offs[nm] = o
             o += (numel * isz + 15) & ~15
-        cur = torch.cuda.current_stream()
-        # allocated on the copying stream: a block handed out for the caller's
-        # stream could still be in use by that stream's queued work, which
-        # `stream` is not ordered after
-        with torch.cuda.stream(stream):
-            base = torch.empty(max(o, 16), dtype=torch.uint8, device=next(iter(olds)).device)
+        if cur is None:
+            cur = _lib.current_stream()
+        # allocated on the caller's stream, read later there (the decoders);
+        # a block the allocator hands out could still be in use by that
+        # stream's queued work, so the copying stream waits for it first
+        base = torch.empty(max(o, 16), dtype=torch.uint8, device=next(iter(olds)).device)
+        if cur != stream:
+            stream.wait_event(cur.record_event())
+            base.record_stream(stream)
         # one library call queues every copy (torch slicing + copy_ per slot
         # costs ~10x the host time)
         k = len(layout)
@@ -208,8 +212,6 @@ class _DevBufs:
             self._slots[nm] = (base, offs[nm], numel, isz)
             self._views.pop(nm, None)
         _lib.raise_for(_lib.lib().actc_memcpy_batch(dst, src, nbs, k, C.c_void_p(stream.cuda_stream)))
-        if cur != stream:
-            base.record_stream(cur)  # read later on the caller's stream (decoders)
         still = {self._slots[nm][0] for nm in self._slots}
         self._bufs = [b for b in self._bufs if b not in olds or b in still] + [base]
 
@@ -726,7 +728,7 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         if x.dtype != torch.float32:
             raise ParameterError("compress expects a 32-bit tensor; convert explicitly with astype(4)")
     dev_index = xs[0].device.index if xs else torch.cuda.current_device()
-    main = torch.cuda.current_stream()
+    main = _lib.current_stream()
     L = _lib.lib()
     streams = [main] * len(xs) if on_caller_stream else _stream_pool(dev_index, slot_base + len(xs))[slot_base:]
     jobs = []
@@ -755,18 +757,17 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         capped = dev.carve(x.device, [("out_idx", k_cap, 8), ("payload", cap, 1), ("out_val", k_cap, 4),
                                       ("canon", lmax, 4)])
         cp, oc = capped.data_ptr(), dev.offsets
+        symbuf = None
+        if own_scratch:
+            sb = 2 if 2 * int(p.radius) <= 65536 else 4
+            symbuf = torch.empty(sb * n + 64, dtype=torch.uint8, device=x.device)
+            _lib.raise_for(L.actc_ctx_set_scratch(ctx.handle, symbuf.data_ptr(), symbuf.numel()))
         # recorded after this tensor's allocations: its side stream is ordered
         # after all caller-stream work that used the blocks the allocator reused
         if s is not main:
             s.wait_event(main.record_event())
         if ready is not None:
             s.wait_event(ready[j])
-        symbuf = None
-        if own_scratch:
-            sb = 2 if 2 * int(p.radius) <= 65536 else 4
-            with torch.cuda.stream(s):  # stream-ordered for the side stream
-                symbuf = torch.empty(sb * n + 64, dtype=torch.uint8, device=x.device)
-            _lib.raise_for(L.actc_ctx_set_scratch(ctx.handle, symbuf.data_ptr(), symbuf.numel()))
         flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
         if (n, int(p.radius)) not in _FALLBACK_SEEN:
             flags |= _lib.ACTC_ASYNC_NO_FALLBACK
@@ -775,9 +776,12 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
                 fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
         # every tensor's K1 goes out before any codebook/encoder launch
         _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
-        fixed.record_stream(s)
-        capped.record_stream(s)
-        x.record_stream(s)
+        if s is not main:
+            fixed.record_stream(s)
+            capped.record_stream(s)
+            x.record_stream(s)
+            if symbuf is not None:
+                symbuf.record_stream(s)
         jobs.append((x, p, s, ctx, dev, cap, k_cap, args, symbuf))
     for job in jobs:
         args, dev = job[7], job[4]
@@ -816,7 +820,7 @@ def compress_end(pend: PendingCompress, compact: bool = False, order: bool = Tru
             dev.shrink("payload", _payload_buffer_bytes(plan.payload_bits))
             dev.shrink("canon", max(plan.live_symbols, 1))
             if compact:
-                dev.compact(("out_idx", "payload", "out_val", "canon"), s)
+                dev.compact(("out_idx", "payload", "out_val", "canon"), s, pend.main)
             c, rep = _container(n, p, dims, plan, dev)
             c._desc()
         else:
@@ -886,7 +890,7 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
         code |= _lib.ACTC_DEC_NO_NONZERO
     _lib.raise_for(_lib.lib().actc_decompress(ctx.handle, C.byref(d), C.c_void_p(out.data_ptr()), code,
                                                C.c_void_p(ctx.dres_buf.data_ptr()), sh))
-    if s != torch.cuda.current_stream(dev):
+    if stream is not None:
         c._record_stream(s)  # the container is read on `s` (caching allocator)
     if not check:
         return out, None
