@@ -50,7 +50,8 @@ side stream as soon as it exists (`compress_begin`, no host sync); a
 compression is finished (`compress_end`: plan read, exact-size container,
 original released) as soon as its chain is done, or -- waiting -- once more
 than `batch_flush` are in flight or the raw activations waiting behind the
-newest one exceed `inflight_bytes`.  The training stream is never ordered
+newest one exceed `inflight_bytes` (default: a quarter of the previous
+iteration's raw stored bytes).  The training stream is never ordered
 after a compression: the container's decompression in backward waits for
 its completion event instead.  Decode faults of the (unsynchronised) backward decompressions
 are collected at the end of every iteration and raised as FormatError at
@@ -269,10 +270,10 @@ class ActivationCompressor:
     """
 
     def __init__(self, layers, optimizer, config: ControllerConfig | None = None, radius: int = DEFAULT_RADIUS,
-                 preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 1, dist_group=None,
+                 preserve_zeros: bool = True, grad_scale=None, batch_flush: int = 8, dist_group=None,
                  sync_stats: bool = True, input_sample_bytes: float | None = None, fixed_bytes: float | None = None,
                  recompute_cheap: bool = True, codec_on_compute_stream: bool = False,
-                 prefetch_decode: bool = False, inflight_bytes: int = 1 << 29):
+                 prefetch_decode: bool = False, inflight_bytes: int | None = None):
         import torch.nn as nn
 
         self.layers = dict(layers)
@@ -287,6 +288,10 @@ class ActivationCompressor:
         # stream + library context), and the raw activations of all but the
         # newest below `inflight_bytes`: the host runs ahead of the GPU by
         # that much instead of waiting for each compression
+        # inflight_bytes None: a quarter of the previous iteration's raw stored
+        # bytes (0 -- one compression at a time -- until an iteration is seen),
+        # so a model with few large activations keeps its forward peak while
+        # one with many (ResNet-50: 49 per iteration) overlaps compressions
         self.batch_flush = batch_flush
         self.inflight_bytes = inflight_bytes
         self._pending_bytes = 0
@@ -623,8 +628,11 @@ class ActivationCompressor:
         # finish what is already done without waiting; wait only when more
         # than batch_flush are in flight (their contexts are reused next) or
         # the older raw activations exceed inflight_bytes
+        limit = self.inflight_bytes
+        if limit is None:
+            limit = self.records[-1].raw_bytes // 4 if self.records else 0
         while self._pending and (len(self._pending) > self.batch_flush or self._pending[0].job.ready()
-                                 or (len(self._pending) > 1 and self._pending_bytes > self.inflight_bytes)):
+                                 or (len(self._pending) > 1 and self._pending_bytes > limit)):
             self._finish(self._pending.pop(0))
 
     def _hint(self, slot, eb):
