@@ -758,15 +758,27 @@ def run_training(model_name, batch, world, iters=6, warm=4, spot_check=False):
         torch.cuda.reset_peak_memory_stats(dev)
         if world > 1:
             torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(iters):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+        from paper_2111_09562_b200 import codec as _codec
+        redos0 = len(_codec.REDOS)
+        st0 = torch.cuda.memory_stats(dev)
+        evs[0].record()
+        for i in range(iters):
             it()
-        e1.record()
-        e1.synchronize()
-        ms = _max_over_ranks(e0.elapsed_time(e1), world, dev)
+            evs[i + 1].record()
+        evs[-1].synchronize()
+        ms = _max_over_ranks(evs[0].elapsed_time(evs[-1]), world, dev)
         rec = {"images_per_s": world * batch * iters / (ms * 1e-3), "ms_per_iter": ms / iters,
+               "ms_each_iter": [round(evs[i].elapsed_time(evs[i + 1]), 2) for i in range(iters)],
                "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9}
+        st1 = torch.cuda.memory_stats(dev)
+        # allocator events inside the timed window (each cudaMalloc / retry
+        # synchronises the device): evidence for an outlier iteration
+        rec["allocator_in_timed_window"] = {
+            "cuda_mallocs": st1.get("num_device_alloc", 0) - st0.get("num_device_alloc", 0),
+            "alloc_retries": st1.get("num_alloc_retries", 0) - st0.get("num_alloc_retries", 0)}
+        if comp:
+            rec["recompressions_in_timed_window"] = len(_codec.REDOS) - redos0
         if comp:
             # the codec contexts' scratch is cudaMalloc'ed by the library,
             # outside torch's allocator: reported beside the allocator peak
