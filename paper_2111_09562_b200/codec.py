@@ -677,8 +677,11 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
 
 
 # tensors (element count, radius) whose frequency-class codebook needed the
-# symbol-level fallback in an earlier async compression: they queue the
-# fallback behind it; all others skip that launch (ACTC_ASYNC_NO_FALLBACK)
+# symbol-level fallback in an earlier async compression (diagnostics: every
+# compression queues the fallback behind the frequency-class codebook -- a
+# launch that exits at once unless it is needed -- because a tensor whose
+# class count crosses the capacity mid-training would otherwise be redone
+# synchronously, a multi-millisecond stall on the training stream)
 _FALLBACK_SEEN: set = set()
 # the last redos of compress_end (n, status, max_len, n_outliers, k_cap,
 # payload_bits, cap_bits): why a launch overflowed a cap
@@ -703,7 +706,7 @@ class PendingCompress:
 
 def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
                    own_scratch: bool = False, on_caller_stream: bool = False,
-                   outlier_hints=None) -> PendingCompress:
+                   outlier_hints=None, queue_fallback: bool = True) -> PendingCompress:
     """Launch the compression of xs (each on its own side stream and context,
     slots slot_base .. slot_base+len-1) and return without synchronising;
     compress_end reads the plans and builds the containers.  The inputs are
@@ -719,7 +722,9 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
     raises the outlier cap (default max(4096, n/64)) to 4x the hint + n/64
     -- small error bounds can put several percent of the elements outside
     the quantization radius, and a training activation's tail can grow
-    several-fold in one step; an overflow is redone exactly."""
+    several-fold in one step; an overflow is redone exactly.
+    `queue_fallback=False` skips the (gated) symbol-level codebook launch
+    (ACTC_ASYNC_NO_FALLBACK): a tensor that needs it is then redone."""
     torch = _lib.torch_cuda()
     if isinstance(params, CodecParams):
         params = [params] * len(xs)
@@ -769,7 +774,7 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         if ready is not None:
             s.wait_event(ready[j])
         flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0
-        if (n, int(p.radius)) not in _FALLBACK_SEEN:
+        if not queue_fallback:
             flags |= _lib.ACTC_ASYNC_NO_FALLBACK
         args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
                 cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, cp + oc["canon"],

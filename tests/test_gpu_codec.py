@@ -291,9 +291,10 @@ def test_long_codes_bit_exact(oracle, depth):
 
 def test_async_codebook_fallback_redo_and_memory(oracle):
     """> 6144 distinct symbol frequencies exceed the frequency-class codebook:
-    the first batched compression runs without the fallback launch, sees
-    ACTC_EAGAIN and redoes the tensor; the next one queues the fallback
-    codebook on the device.  Both bit-exact."""
+    without the fallback launch (queue_fallback=False) the compression sees
+    ACTC_EAGAIN and is redone through the two-phase path; by default the
+    gated symbol-level codebook runs on the device right behind it, no redo.
+    Both bit-exact."""
     K = 6500
     rng = np.random.default_rng(1)
     vals = np.array([((i + 1) // 2) * (1 if i % 2 else -1) for i in range(K)], dtype=np.int64)
@@ -305,9 +306,11 @@ def test_async_codebook_fallback_redo_and_memory(oracle):
     xt = torch.from_numpy(x).cuda()
     key = (x.size, p.radius)
     pc._FALLBACK_SEEN.discard(key)
-    (c1, r1), = pb.compress_batch([xt], [p])
-    assert key in pc._FALLBACK_SEEN
+    (c1, r1), = pc.compress_end(pc.compress_begin([xt], [p], queue_fallback=False))
+    assert key in pc._FALLBACK_SEEN  # redone
+    n0 = len(pc.REDOS)
     (c2, r2), = pb.compress_batch([xt], [p])
+    assert len(pc.REDOS) == n0  # the device ran the fallback codebook
     for c, r in ((c1, r1), (c2, r2)):
         assert c.to_bytes() == ref.blob
         assert r.ratio == ref.ratio
