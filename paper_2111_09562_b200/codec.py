@@ -267,7 +267,10 @@ class CompressedActivation:
         self.dims = tuple(int(d) for d in dims)
         self.precision = 4
         self.params = params
-        self.symbol_count = int(np.prod(self.dims)) if self.dims else 0
+        n = 1
+        for d in self.dims:
+            n *= d
+        self.symbol_count = n if self.dims else 0
         self.payload_bits = int(payload_bits)
         self._h_outlier_indices = None
         self._h_outlier_values = None
@@ -808,6 +811,7 @@ def compress_end(pend: PendingCompress, compact: bool = False, order: bool = Tru
         raise ParameterError("compress_end called twice on the same batch")
     pend.done = True
     out = []
+    redone = set()
     # containers are built as each stream finishes (the host work of the
     # early tensors overlaps the GPU tail of the late ones), and each
     # container's stream descriptor is built once here
@@ -840,14 +844,20 @@ def compress_end(pend: PendingCompress, compact: bool = False, order: bool = Tru
             # allocate on the stream it runs on
             torch = _lib.torch_cuda()
             s.wait_stream(pend.main)
+            redone.add(s)
             with torch.cuda.stream(s):
                 c, rep = compress_device(x, p)
         if not order:
             c._ready = s.record_event()
         out.append((c, rep))
     if order:
-        for job in pend.jobs:
-            pend.main.wait_stream(job[2])
+        # each chain's end event was recorded at launch (PendingCompress);
+        # compaction copies and redos put more work on the stream after it
+        for job, ev in zip(pend.jobs, pend.events):
+            if compact or job[2] in redone:
+                pend.main.wait_stream(job[2])
+            else:
+                pend.main.wait_event(ev)
     pend.jobs = []
     return out
 
@@ -910,6 +920,17 @@ def decompress_device(c: CompressedActivation, dtype=None, out=None, stream=None
     return out, (int(r.nonzero) if count_nonzero else None)
 
 
+def _decode_rest(L, i, c, out, d, s, ctx, dt, evs):
+    """queue stream i's decoder on side stream s (no result mailbox: nothing is read back)"""
+    rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(), dt | _lib.ACTC_DEC_REST, None, s.cuda_stream)
+    if rc:
+        _lib.raise_for(rc)
+    out.record_stream(s)
+    c._record_stream(s)
+    if evs is not None:
+        evs[i] = s.record_event()
+
+
 def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=None):
     """Reconstruct several streams concurrently, each on its own stream and
     context (a small tensor's decode alone does not fill the GPU).  Results
@@ -953,22 +974,20 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
             ctx = _lib.context_for(dev_index, slot)
             dt = _lib.ACTC_DTYPE_F32 if out.dtype == f32 else _lib.ACTC_DTYPE_F64
             if not d.table_dev:
-                # every decode table goes out before any decoder fills the GPU
-                # (streams from compress_batch carry theirs already)
+                # every decode table goes out before any table-less stream's
+                # decoder fills the GPU
                 rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(), dt | _lib.ACTC_DEC_LUT_ONLY,
                                        None, s.cuda_stream)
                 if rc:
                     _lib.raise_for(rc)
-            jobs.append((i, c, out, d, s, ctx, dt))
+                jobs.append((i, c, out, d, s, ctx, dt))
+            else:
+                # streams from compress_batch carry their decode table: the
+                # decoder goes out at once (the GPU would idle until the first
+                # one is queued; the host prepares the next while it runs)
+                _decode_rest(L, i, c, out, d, s, ctx, dt, evs if done is not None else None)
         for i, c, out, d, s, ctx, dt in jobs:
-            rc = L.actc_decompress(ctx.handle, C.byref(d), out.data_ptr(), dt | _lib.ACTC_DEC_REST,
-                                   None, s.cuda_stream)  # no result mailbox: nothing is read back
-            if rc:
-                _lib.raise_for(rc)
-            out.record_stream(s)
-            c._record_stream(s)
-            if done is not None:
-                evs[i] = s.record_event()
+            _decode_rest(L, i, c, out, d, s, ctx, dt, evs if done is not None else None)
         for slot in range(len(group)):
             main.wait_stream(streams[slot])
     if done is not None:
