@@ -183,11 +183,21 @@ def cuda_available() -> bool:
     return torch.cuda.is_available()
 
 
+_TORCH_CUDA = None
+
+
 def torch_cuda():
+    """torch, once a CUDA device is known to be present (checked once per
+    process: torch.cuda.is_available() re-reads the environment per call,
+    and the codec's host path asks several times per compression)"""
+    global _TORCH_CUDA
+    if _TORCH_CUDA is not None:
+        return _TORCH_CUDA
     import torch
 
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2111_09562_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    _TORCH_CUDA = torch
     return torch
 
 

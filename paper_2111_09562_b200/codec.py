@@ -946,7 +946,7 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
     if not cs:
         return outs
     dev_index = outs[0].device.index
-    main = torch.cuda.current_stream()
+    main = _lib.current_stream()
     order = sorted(range(len(cs)), key=lambda i: -cs[i].element_count)  # largest first
     evs = [None] * len(cs)
     for g0 in range(0, len(cs), max_concurrency):

@@ -723,7 +723,7 @@ class ActivationCompressor:
             # decoded ahead on the prefetch stream
             out, ev = h.pf
             h.pf = None
-            cur = torch.cuda.current_stream()
+            cur = _lib.current_stream()
             cur.wait_event(ev)
             out.record_stream(cur)
             h.out = out.view(h.shape)
@@ -772,7 +772,7 @@ class ActivationCompressor:
         g = self._order[h.pos - 1]
         if g.comp is None or g.out is not None or g.pf is not None or g.unpacks or g.job is not None:
             return
-        cur = torch.cuda.current_stream()
+        cur = _lib.current_stream()
         if self._pf_stream is None:
             self._pf_stream = torch.cuda.Stream(device=cur.device)
         ps = self._pf_stream
@@ -788,10 +788,9 @@ class ActivationCompressor:
             d.clear()
         for h in self._order:
             if h.pf is not None:  # decoded ahead but never read back: join its stream
-                import torch
-
-                torch.cuda.current_stream().wait_event(h.pf[1])
-                h.pf[0].record_stream(torch.cuda.current_stream())
+                cur = _lib.current_stream()
+                cur.wait_event(h.pf[1])
+                h.pf[0].record_stream(cur)
                 h.pf = None
         self._order = []
         self._await_consumer = []
