@@ -782,8 +782,13 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
         args = (ctx.handle, x.data_ptr(), n, float(p.eb), int(p.radius), flags, fp + of["chunk_lat"],
                 cp + oc["payload"], cap, cp + oc["out_idx"], cp + oc["out_val"], k_cap, cp + oc["canon"],
                 fp + of["len_counts"], fp + of["chunk_off"], ctx.plan_buf.data_ptr(), s.cuda_stream)
-        # every tensor's K1 goes out before any codebook/encoder launch
-        _lib.raise_for(L.actc_compress_async(*args[:5], flags | _lib.ACTC_ASYNC_K1_ONLY, *args[6:]))
+        # the whole chain (K1 -> codebook -> count -> pack) goes out in one
+        # call: launching every tensor's K1 first held the first tensor's
+        # codebook -- the batch's critical path -- back by the other tensors'
+        # host preparation (~55 us each)
+        # the chain's tail builds the stream's decode table into the container
+        _lib.raise_for(L.actc_ctx_set_table_out(ctx.handle, dev.ptr("table"), _lib.ACTC_TABLE_BYTES))
+        _lib.raise_for(L.actc_compress_async(*args))
         if s is not main:
             fixed.record_stream(s)
             capped.record_stream(s)
@@ -791,11 +796,6 @@ def compress_begin(xs, params, slot_base: int = 0, ready=None, bit_hints=None,
             if symbuf is not None:
                 symbuf.record_stream(s)
         jobs.append((x, p, s, ctx, dev, cap, k_cap, args, symbuf))
-    for job in jobs:
-        args, dev = job[7], job[4]
-        # the chain's tail builds the stream's decode table into the container
-        _lib.raise_for(L.actc_ctx_set_table_out(args[0], dev.ptr("table"), _lib.ACTC_TABLE_BYTES))
-        _lib.raise_for(L.actc_compress_async(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:]))
     return PendingCompress(jobs, main)
 
 

@@ -239,18 +239,23 @@ __global__ void k_plan_out(const actc_plan_t *__restrict__ src, actc_plan_t *dst
 
 // device alias of a pinned host buffer (UVA-mapped), or null
 void *mapped_alias(const void *host) {
-  static thread_local const void *last_host = nullptr;
-  static thread_local void *last_dev = nullptr;
-  if (host != last_host) {
-    cudaPointerAttributes at{};
-    void *dev = nullptr;
-    if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost)
-      dev = at.devicePointer;
-    cudaGetLastError();
-    last_host = host;
-    last_dev = dev;
-  }
-  return last_dev;
+  // a few recent answers per thread: a batch cycles through one plan
+  // mailbox per context (cudaPointerGetAttributes costs a few us a call)
+  constexpr int kN = 16;
+  static thread_local const void *hosts[kN] = {};
+  static thread_local void *devs[kN] = {};
+  static thread_local int next = 0;
+  for (int i = 0; i < kN; i++)
+    if (hosts[i] == host && host) return devs[i];
+  cudaPointerAttributes at{};
+  void *dev = nullptr;
+  if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost)
+    dev = at.devicePointer;
+  cudaGetLastError();
+  hosts[next] = host;
+  devs[next] = dev;
+  next = (next + 1) % kN;
+  return dev;
 }
 
 int plan_to_host(actc_ctx *c, actc_plan_t *plan_host, cudaStream_t s) {
