@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
   __shared__ double s_wbd[NW + 1];
   __shared__ PhS s_wbp[NW + 1];
   __shared__ uint32_t s_lastw_t[NT];
+  __shared__ uint32_t s_dummy[NW];
   __shared__ unsigned s_fail, s_err;
   __shared__ uint32_t s_L, s_lo, s_hi, s_nbig, s_lastw;
   __shared__ unsigned long long s_sum;
@@ -371,17 +372,15 @@ __global__ void __launch_bounds__(NT, 1) k2r_codebook(CodebookArgs a) {
             k = Rs + l2;
           }
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, k);
-        if (f && lane == __ffs(peers) - 1) {
-          if (k < kHot)
-            wcnt[warp * kHot + k] += __popc(peers);  // warp-private: the lightest classes are the hot ones
-          else
-            atomicAdd(&LC[k], (uint32_t)__popc(peers));
-          LW[k] = f;
-        }
-        // the next iteration's leaders read what this one's wrote (warp-private
-        // counters): order the lanes' shared accesses explicitly
-        __syncwarp();
+        // one unconditional constant add per lane: ptxas turns it into
+        // ATOMS.POPC.INC, which aggregates a warp's equal addresses in the
+        // atomic unit (a __match_any_sync + leader update cost ~1.4 K cycles
+        // per symbol and thread on wide alphabets); dead lanes count into a
+        // per-warp dummy.  Warp-private counters for the lightest (hottest)
+        // classes keep the warps off each other's addresses.
+        uint32_t *ctr = !f ? &s_dummy[warp] : (k < kHot ? &wcnt[warp * kHot + k] : &LC[k]);
+        atomicAdd(ctr, 1u);
+        if (f) LW[k] = f;
         if (s < v1) a.cls16[s] = f ? (uint16_t)k : (uint16_t)0xFFFF;
       }
     }
