@@ -108,8 +108,15 @@ __global__ void __launch_bounds__(K3L_THREADS) k3_seg_count(const SymT *__restri
   if (a.dplan) {
     // device-planned: zero the payload (the pack ORs boundary words)
     const uint64_t nw = (a.dplan->payload_bits + 31) / 32 + 2;
-    for (uint64_t i = (uint64_t)blockIdx.x * K3L_THREADS + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * K3L_THREADS)
-      a.payload[i] = 0u;
+    const uint64_t stride = (uint64_t)gridDim.x * K3L_THREADS;
+    if (!(reinterpret_cast<uintptr_t>(a.payload) & 15)) {
+      // 16-byte stores (the buffer carries a 32-byte pad past its last word)
+      uint4 *p4 = reinterpret_cast<uint4 *>(a.payload);
+      for (uint64_t i = (uint64_t)blockIdx.x * K3L_THREADS + threadIdx.x; i < (nw + 3) / 4; i += stride)
+        p4[i] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      for (uint64_t i = (uint64_t)blockIdx.x * K3L_THREADS + threadIdx.x; i < nw; i += stride) a.payload[i] = 0u;
+    }
     if (a.canon_src) {
       // the table is in ctx scratch: copy it to the caller's buffers
       const uint32_t live = a.dplan->live_symbols;
