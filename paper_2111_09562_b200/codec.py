@@ -851,13 +851,12 @@ def compress_end(pend: PendingCompress, compact: bool = False, order: bool = Tru
             c._ready = s.record_event()
         out.append((c, rep))
     if order:
-        # each chain's end event was recorded at launch (PendingCompress);
-        # compaction copies and redos put more work on the stream after it
-        for job, ev in zip(pend.jobs, pend.events):
+        # every chain has completed (its stream was synchronised above), so
+        # only work queued after that -- compaction copies, redos -- needs
+        # the caller's stream to wait
+        for job in pend.jobs:
             if compact or job[2] in redone:
                 pend.main.wait_stream(job[2])
-            else:
-                pend.main.wait_event(ev)
     pend.jobs = []
     return out
 
