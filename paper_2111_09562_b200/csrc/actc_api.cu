@@ -161,7 +161,8 @@ struct actc_ctx {
   int device = 0;
   int num_sms = 148;
   Buf sym, hist, cb, ctab, len8, canon, lencnt, status, misc, lut, idx, part, crc, crc_copy;
-  actc_plan_t *plan_dev = nullptr;
+  actc_plan_t *plan_dev = nullptr;  // inside misc (kMiscPlanOff)
+  bool plan_zeroed = false;          // launch_k1 zeroed it: the next codebook launch skips its memset
   DecResult *dres_dev = nullptr;
   // state carried from plan to encode
   uint64_t n = 0, A = 0;
@@ -222,6 +223,7 @@ CbLayout cb_layout(uint64_t A) {
 
 // misc counters layout (u64 slots)
 enum { M_NOUT = 0, M_TICKET = 1, M_BAD = 2, M_SCAN_TOT = 3, M_CHANGED = 4, M_STATUS = 5, M_SCAN_TOT2 = 6, M_K2GATE = 7, M_SEGTICKET = 8, M_PACKTICKET = 9, M_K4LTICKET = 10, M_K4LMCOUNT = 11, M_SLOTS = 12 };
+constexpr size_t kMiscPlanOff = (8 * M_SLOTS + 63) & ~(size_t)63;  // device plan inside the misc buffer
 
 constexpr size_t kK2Smem = 4096 * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 64;
 
@@ -316,20 +318,23 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
     if (rc2) return rc2;
     a.dbg = (unsigned long long *)c->idx.p;
   }
-  CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
+  if (!c->plan_zeroed) CK(cudaMemsetAsync(c->plan_dev, 0, sizeof(actc_plan_t), s));
+  c->plan_zeroed = false;
   // frequency-class codebook first; it hands over to k2_codebook (gated)
   // when its capacities are exceeded
+  // the single-CTA codebooks sit on the critical path of their tensor's
+  // chain: highest execution priority, so a freed SM goes to them before the
+  // pending CTAs of other tensors' bandwidth kernels (the gated fallback
+  // too: it needs a whole SM's shared memory, and at default priority it
+  // waited ~5 us per chain for one to drain)
+  static int hi = [] {
+    int lo = 0, h = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &h);
+    return h;
+  }();
   if (!in_lengths && A <= 65536 && n_symbols < (1ull << 32)) {
     KT(ACTC_KIND_CODEBOOK);
-    // the single-CTA codebook sits on the critical path of its tensor's
-    // chain: highest execution priority, so a freed SM goes to it before the
-    // pending CTAs of other tensors' bandwidth kernels
     {
-      static int hi = [] {
-        int lo = 0, h = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &h);
-        return h;
-      }();
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(1);
       cfg.blockDim = dim3(K2_THREADS);
@@ -346,7 +351,17 @@ int run_codebook(actc_ctx *c, const unsigned long long *hist, uint64_t A, const 
   }
   if (!(a.gate && c->no_fallback)) {
     KT(ACTC_KIND_CODEBOOK);
-    k2_codebook<<<1, K2_THREADS, kK2Smem, s>>>(a);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(K2_THREADS);
+    cfg.dynamicSmemBytes = kK2Smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = hi;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k2_codebook, a));
   }
   c->emit = EmitArgs{};
   if (a.gate && c->defer_emit) {
@@ -477,18 +492,21 @@ int actc_ctx_create(int device, actc_ctx **out) {
   actc_ctx *c = new actc_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->plan_dev, sizeof(actc_plan_t)) != cudaSuccess ||
-      cudaMalloc(&c->dres_dev, sizeof(DecResult)) != cudaSuccess) {
+  if (cudaMalloc(&c->dres_dev, sizeof(DecResult)) != cudaSuccess) {
     delete c;
     return set_err(ACTC_ENOMEM, "ctx alloc failed");
   }
   cudaMemset(c->dres_dev, 0, sizeof(DecResult));
   int rc;
-  if ((rc = grow(c->misc, 8 * M_SLOTS)) || (rc = grow(c->lut, std::max<size_t>(4 * kLutWords, kK4lTableBytes)))) {
+  // the device plan lives right after the misc words: launch_k1 zeroes both
+  // with one memset (no separate zeroing step between K1 and the codebook)
+  if ((rc = grow(c->misc, kMiscPlanOff + sizeof(actc_plan_t))) ||
+      (rc = grow(c->lut, std::max<size_t>(4 * kLutWords, kK4lTableBytes)))) {
     delete c;
     return rc;
   }
   CK(cudaMemset(c->misc.p, 0, c->misc.cap));  // self-resetting tickets start at 0
+  c->plan_dev = (actc_plan_t *)((char *)c->misc.p + kMiscPlanOff);
   CK(cudaFuncSetAttribute(k2_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2Smem));
   CK(cudaFuncSetAttribute(k2r_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2rSmem));
   int nb = 0;
@@ -564,7 +582,6 @@ void actc_ctx_destroy(actc_ctx *c) {
                  &c->status, &c->misc, &c->lut, &c->idx, &c->part, &c->crc, &c->crc_copy};
   for (Buf *b : bufs)
     if (b->p) cudaFree(b->p);
-  cudaFree(c->plan_dev);
   cudaFree(c->dres_dev);
   delete c;
 }
@@ -604,7 +621,8 @@ static int launch_k1(actc_ctx *c, const float *x, uint64_t n, double eb, uint32_
   c->sym_ext_bytes = 0;
   if ((rc = grow(c->hist, 8 * A))) return rc;
   CK(cudaMemsetAsync(c->hist.p, 0, 8 * A, s));
-  CK(cudaMemsetAsync(c->misc.p, 0, 8 * M_SLOTS, s));
+  CK(cudaMemsetAsync(c->misc.p, 0, kMiscPlanOff + sizeof(actc_plan_t), s));  // counters + device plan
+  c->plan_zeroed = true;
   unsigned long long *misc = (unsigned long long *)c->misc.p;
 
   const QParams P = make_qparams(eb);
