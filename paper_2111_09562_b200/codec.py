@@ -395,22 +395,19 @@ class CompressedActivation:
         if with_index and self._desc_cache is not None:
             return self._desc_cache
         dev = self._dev
-        d = _lib.StreamDesc()
-        d.n = self.symbol_count
-        d.eb = float(self.params.eb)
-        d.radius = int(self.params.radius)
-        d.flags = _lib.ACTC_FLAG_PRESERVE_ZEROS if self.params.preserve_zeros else 0
-        d.n_outliers = self._n_outliers
-        d.outlier_idx_dev = dev.ptr("out_idx")
-        d.outlier_val_dev = dev.ptr("out_val")
-        d.live_symbols = self._live
-        d.canon_syms_dev = dev.ptr("canon")
-        d.len_counts_dev = dev.ptr("len_counts")
-        d.payload_dev = dev.ptr("payload")
-        d.payload_bits = self.payload_bits
-        d.chunk_offsets_dev = dev.ptr("chunk_off") if (with_index and "chunk_off" in dev) else None
-        d.chunk_lat_dev = dev.ptr("chunk_lat") if (with_index and "chunk_lat" in dev) else None
-        d.table_dev = dev.ptr("table") if (with_index and "table" in dev) else None
+        ptr = dev.ptr
+        p = self.params
+        # positional construction: one ctypes call instead of 15 attribute sets
+        # (this runs per container between a batch's last compression and its
+        # first decoder launch)
+        d = _lib.StreamDesc(
+            self.symbol_count, float(p.eb), int(p.radius),
+            _lib.ACTC_FLAG_PRESERVE_ZEROS if p.preserve_zeros else 0, self._n_outliers,
+            ptr("out_idx"), ptr("out_val"), self._live, ptr("canon"), ptr("len_counts"), ptr("payload"),
+            self.payload_bits,
+            ptr("chunk_off") if (with_index and "chunk_off" in dev) else None,
+            ptr("chunk_lat") if (with_index and "chunk_lat" in dev) else None,
+            ptr("table") if (with_index and "table" in dev) else None)
         if with_index and d.chunk_offsets_dev:
             self._desc_cache = d  # device buffers are fixed for the container's lifetime
         return d
