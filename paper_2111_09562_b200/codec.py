@@ -948,11 +948,14 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
     for g0 in range(0, len(cs), max_concurrency):
         group = order[g0:g0 + max_concurrency]
         streams = _stream_pool(dev_index, len(group))
-        ready = main.record_event()
         L = _lib.lib()
         f32 = torch.float32
-        jobs = []
-        for slot, i in enumerate(group):
+        # uploads / index rebuilds of containers parsed from bytes run first,
+        # on the caller's stream and the thread's main context -- which slot
+        # 0's decoder uses too, so none may run while a decoder of the group
+        # is already queued
+        descs = {}
+        for i in group:
             c, out = cs[i], outs[i]
             n = c.symbol_count
             if out.numel() != n or out.dtype not in (f32, torch.float64) or not out.is_contiguous():
@@ -961,9 +964,13 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
             if d is None:
                 if n != c.element_count:
                     raise FormatError(f"symbol count {n} != element count {c.element_count}")
-                c._ensure_index()  # uploads / index rebuild on the caller's stream
+                c._ensure_index()
                 d = c._desc()
-                ready = main.record_event()  # ... which the side stream must follow
+            descs[i] = d
+        ready = main.record_event()  # the side streams follow the caller's queued work
+        jobs = []
+        for slot, i in enumerate(group):
+            c, out, d = cs[i], outs[i], descs[i]
             s = streams[slot]
             s.wait_event(ready)
             c._wait_ready(s)

@@ -214,6 +214,30 @@ def test_decompress_batch_matches_single(oracle):
         assert np.array_equal(o.cpu().numpy().reshape(-1), want.astype(np.float32))
 
 
+def test_decompress_batch_mixed_table_and_blob_streams(oracle):
+    """a batch mixing containers that carry the pack kernel's decode table
+    (decoded as soon as prepared) with containers parsed from bytes (table
+    first, decoder after every table): every reconstruction bit-exact, and
+    one completion event per stream in input order"""
+    rng = np.random.default_rng(31)
+    xs, ps = [], []
+    for k in range(7):
+        n = int(rng.integers(1000, 300000))
+        xs.append(torch.from_numpy(np.maximum(rng.normal(0, 1, n), 0).astype(np.float32)).cuda())
+        ps.append(pb.CodecParams(eb=float(10 ** rng.uniform(-5, -2))))
+    comp = [c for c, _ in pb.compress_batch(xs, ps)]
+    mixed = [c if k % 2 == 0 else pc.CompressedActivation.from_bytes(c.to_bytes()) for k, c in enumerate(comp)]
+    done = []
+    outs = pb.decompress_batch(mixed, max_concurrency=4, done=done)
+    assert len(done) == len(mixed) and all(e is not None for e in done)
+    for e in done:
+        e.synchronize()
+    pb.check_decode_status()
+    for x, p, o in zip(xs, ps, outs):
+        want = oracle.decompress_blob(oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob, x.numel())
+        assert np.array_equal(o.cpu().numpy().reshape(-1), want.astype(np.float32))
+
+
 def test_compress_batch_cap_overflow_takes_two_phase_path(oracle):
     """actc_compress_async sizes outlier buffers by a cap (max(4096, n/64));
     a tensor with more outliers must come back through the two-phase path,
