@@ -668,9 +668,12 @@ def compress_batch(xs, params, max_concurrency: int = 8, ready=None, compact: bo
     del torch
     for g0 in range(0, len(xs), max_concurrency):
         group = order[g0:g0 + max_concurrency]
+        # a lone tensor runs on the caller's stream: no side-stream event
+        # hand-offs on the host path (the call synchronises on it anyway)
         pend = compress_begin([xs[i] for i in group], [params[i] for i in group],
                               ready=None if ready is None else [ready[i] for i in group],
-                              bit_hints=None if bit_hints is None else [bit_hints[i] for i in group])
+                              bit_hints=None if bit_hints is None else [bit_hints[i] for i in group],
+                              on_caller_stream=len(xs) == 1 and ready is None)
         for i, r in zip(group, compress_end(pend, compact=compact)):
             results[i] = r
     return results
@@ -947,7 +950,8 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
     evs = [None] * len(cs)
     for g0 in range(0, len(cs), max_concurrency):
         group = order[g0:g0 + max_concurrency]
-        streams = _stream_pool(dev_index, len(group))
+        # a lone stream decodes on the caller's stream (no event hand-offs)
+        streams = [main] if len(cs) == 1 else _stream_pool(dev_index, len(group))
         L = _lib.lib()
         f32 = torch.float32
         # uploads / index rebuilds of containers parsed from bytes run first,
@@ -967,12 +971,13 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
                 c._ensure_index()
                 d = c._desc()
             descs[i] = d
-        ready = main.record_event()  # the side streams follow the caller's queued work
+        ready = main.record_event() if streams[0] is not main else None  # side streams follow the caller
         jobs = []
         for slot, i in enumerate(group):
             c, out, d = cs[i], outs[i], descs[i]
             s = streams[slot]
-            s.wait_event(ready)
+            if ready is not None:
+                s.wait_event(ready)
             c._wait_ready(s)
             ctx = _lib.context_for(dev_index, slot)
             dt = _lib.ACTC_DTYPE_F32 if out.dtype == f32 else _lib.ACTC_DTYPE_F64
@@ -992,7 +997,8 @@ def decompress_batch(cs, outs=None, dtype=None, max_concurrency: int = 8, done=N
         for i, c, out, d, s, ctx, dt in jobs:
             _decode_rest(L, i, c, out, d, s, ctx, dt, evs if done is not None else None)
         for slot in range(len(group)):
-            main.wait_stream(streams[slot])
+            if streams[slot] is not main:
+                main.wait_stream(streams[slot])
     if done is not None:
         done.extend(evs)
     return outs
