@@ -81,6 +81,31 @@ def _union_ms(iv):
     return tot
 
 
+def _shares_ms(timeline, kinds):
+    """Step time attributed to each kind: every instant is split evenly among
+    the kinds (of `kinds`) with a launch running then.  A kind whose
+    launches overlap other kinds' (pack beside count and K1) gets less than
+    its busy time; one that runs alone (the decoders) keeps all of it."""
+    ev = []
+    for k, a, b in timeline:
+        if k in kinds and b > a:
+            ev.append((a, 1, k))
+            ev.append((b, -1, k))
+    ev.sort(key=lambda e: (e[0], e[1]))
+    share = {k: 0.0 for k in kinds}
+    live = {}
+    prev = None
+    for t, d, k in ev:
+        if prev is not None and live and t > prev:
+            for kk in live:
+                share[kk] += (t - prev) / len(live)
+        live[k] = live.get(k, 0) + d
+        if live[k] == 0:
+            del live[k]
+        prev = t
+    return share
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -570,7 +595,14 @@ def run_gpu(args, rank, world):
             ent["achieved_gbs_per_launch_avg"] = alg_step[kind] * args.steps / (ms * 1e-3) / 1e9
         kernels[kind] = ent
     hbm_kinds = [k for k in ("quant", "count", "pack", "decode") if k in kernels]
-    dom = max(hbm_kinds or list(kernels), key=lambda k: kernels[k]["busy_ms_per_step"])
+    # dominant = the largest share of the step (each instant split among the
+    # bandwidth kernels running then); busy time alone flips between pack and
+    # the decoders from run to run (pack's launches overlap count's and K1's)
+    shares = _shares_ms(timeline, set(hbm_kinds))
+    for k in hbm_kinds:
+        kernels[k]["step_share_ms_per_step"] = shares[k] / args.steps
+    dom = max(hbm_kinds or list(kernels), key=lambda k: kernels[k].get("step_share_ms_per_step",
+                                                                       kernels[k]["busy_ms_per_step"]))
     peak, peak_kind = _peaks()
     achieved = kernels[dom].get("achieved_gbs", 0.0)
     traffic = None
@@ -604,11 +636,14 @@ def run_gpu(args, rank, world):
                          "busy_ms_per_step": kernels[dom]["busy_ms_per_step"],
                          "achieved_per_launch_avg": kernels[dom].get("achieved_gbs_per_launch_avg"),
                          "frac_per_launch_avg": (kernels[dom].get("achieved_gbs_per_launch_avg") or 0.0) / peak,
+                         "step_share_ms_per_step": kernels[dom].get("step_share_ms_per_step"),
                          "timing": "CUDA events around every launch on its own stream, a second pass of the "
                                    "same K steps; achieved = the kernel's algorithmic bytes per step / the time "
                                    "per step during which at least one of its launches runs (the tensors' "
                                    "launches overlap on their streams); the per-launch-average figure "
-                                   "(bytes per launch / mean launch duration) is beside it"},
+                                   "(bytes per launch / mean launch duration) is beside it; dominant = the "
+                                   "bandwidth kernel with the largest share of the step (each instant split "
+                                   "evenly among the bandwidth kernels running then)"},
             "kernels": kernels,
             "e2e": {"value": e2e_gbs, "unit": "GB/s", "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": in_bytes},
             "gpu_launches": gpu_launches,  # counted by libactc (actc_kernel_stats) over the timed region
