@@ -238,6 +238,34 @@ def test_decompress_batch_mixed_table_and_blob_streams(oracle):
         assert np.array_equal(o.cpu().numpy().reshape(-1), want.astype(np.float32))
 
 
+def test_compress_async_split_launch_matches_oracle(oracle):
+    """the C ABI's split form of actc_compress_async (ACTC_ASYNC_K1_ONLY, then
+    ACTC_ASYNC_REST on the same context and stream) gives the one-call
+    result: every blob equal to the oracle's"""
+    from paper_2111_09562_b200 import _lib
+
+    L = _lib.lib()
+    one_call = L.actc_compress_async
+
+    def split(*args):
+        rc = one_call(*args[:5], args[5] | _lib.ACTC_ASYNC_K1_ONLY, *args[6:])
+        if rc:
+            return rc
+        return one_call(*args[:5], args[5] | _lib.ACTC_ASYNC_REST, *args[6:])
+
+    rng = np.random.default_rng(37)
+    xs = [torch.from_numpy(np.maximum(rng.normal(0, 1, int(n)), 0).astype(np.float32)).cuda()
+          for n in rng.integers(1000, 200000, 4)]
+    ps = [pb.CodecParams(eb=float(10 ** rng.uniform(-5, -2))) for _ in xs]
+    L.actc_compress_async = split
+    try:
+        out = pb.compress_batch(xs, ps)
+    finally:
+        L.actc_compress_async = one_call
+    for (c, rep), x, p in zip(out, xs, ps):
+        assert c.to_bytes() == oracle.compress(x.cpu().numpy(), p.eb, debug=False).blob
+
+
 def test_compress_batch_cap_overflow_takes_two_phase_path(oracle):
     """actc_compress_async sizes outlier buffers by a cap (max(4096, n/64));
     a tensor with more outliers must come back through the two-phase path,
